@@ -1,0 +1,236 @@
+/*
+ * opscale_b200.h -- C ABI of the B200-native candidate-evaluation path.
+ *
+ * This library replaces the search core of the opscaler planners
+ * (arXiv 2511.02248 reference, pkg/src/opscaler/autoscaler.py):
+ *
+ *   opsc_menu_build        <- _Evaluator.predict_op menu loops
+ *                             (autoscaler.py:743-757; perfmodel.py:62-64,133-171;
+ *                              queueing.py:54-87)
+ *   opsc_stability_check   <- init_configs NoStableConfig pre-check that the
+ *                             brute-force oracle inherits from its greedy warm
+ *                             start (autoscaler.py:254-294, 771)
+ *   opsc_compose_argmin    <- brute_force_autoscale descend + leaf mask +
+ *                             lexicographic argmin (autoscaler.py:786-826)
+ *   opsc_menu_fallback     <- infeasible-SLO per-op fallback (autoscaler.py:828-841)
+ *   opsc_decode_decisions  <- best_assign -> OperatorConfig (autoscaler.py:843-845)
+ *   opsc_model_grid        <- model_level_autoscale (autoscaler.py:596-681)
+ *   opsc_materialize       <- _Evaluator.evaluate + _make_plan
+ *                             (autoscaler.py:196-247; opgraph.py:199-244),
+ *                             metrics.request_energy (metrics.py:84-102),
+ *                             provisioned_memory (metrics.py:130-132) and
+ *                             default_stream_place.devices_used
+ *                             (placement.py:358-385, 465-491)
+ *   opsc_plan_windows_host <- runner.plan_for_mode looped over windows
+ *                             (runner.py:38-52, cli.py:135-150), host buffers in
+ *                             and out, one call per batch of windows.
+ *
+ * Conventions
+ *   - Operators are indexed by their rank in sorted(node_ids) ("lex rank").
+ *     That is the brute-force menu order (autoscaler.py:725).
+ *   - All floating point is IEEE binary64, evaluated in exactly the
+ *     reference's association order with no FMA contraction.
+ *   - Device-pointer entry points take a cudaStream_t (passed as void*) and
+ *     never allocate or synchronise. Host-buffer entry points go through an
+ *     opaque context that owns its device workspace.
+ *   - Every entry point returns an int status (OPSC_OK = 0); no exception
+ *     crosses the ABI. Per-window semantic outcomes (NoStableConfig, ...) are
+ *     reported in per-window status words (OPSC_W_* bits).
+ */
+#ifndef OPSCALE_B200_H
+#define OPSCALE_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OPSC_ABI_VERSION 1
+
+#define OPSC_MAX_OPS 32
+#define OPSC_MAX_EDGES 256
+#define OPSC_MAX_P 8
+#define OPSC_MAX_DEVICES 1024
+#define OPSC_PRED_FIELDS 7 /* op_latency, lam, mu, utilization, wait, service, comm */
+
+/* call status codes */
+#define OPSC_OK 0
+#define OPSC_ERR_ARG 1      /* bad argument / size limit exceeded        */
+#define OPSC_ERR_CUDA 2     /* CUDA runtime error                          */
+#define OPSC_ERR_SPACE 3    /* candidate space exceeds the 2^40 key field  */
+#define OPSC_ERR_NODEVICE 4 /* no CUDA device / extension unusable         */
+
+/* per-window status bits */
+#define OPSC_W_NO_STABLE_BOUNDS 0x1u   /* NoStableConfig: op has no stable entry in bounds (autoscaler.py:835) */
+#define OPSC_W_NO_STABLE_PARAMS 0x2u   /* NoStableConfig: init_configs pre-check failed (autoscaler.py:289) */
+#define OPSC_W_NO_STABLE_MODEL 0x4u    /* NoStableConfig: model-level found no stable batch (autoscaler.py:678) */
+#define OPSC_W_ZERO_DIVISION 0x8u      /* reference would raise ZeroDivisionError (T*layers == 0) */
+#define OPSC_W_UNSTABLE_ROUNDING 0x10u /* lam < R*mu but lam/(R*mu) rounds to 1.0: reference raises Unstable */
+#define OPSC_W_FLEET_EXHAUSTED 0x20u   /* default-stream placement ran out of devices (placement.py:183-187) */
+#define OPSC_W_INFEASIBLE_PLACEMENT 0x40u /* a replica exceeds device memory (placement.py:379-383, 485-489) */
+#define OPSC_W_IDLE 0x80u              /* qps <= 0: no plan (cli.py:138-144) */
+
+/* planning modes (runner.py:38-52) */
+#define OPSC_MODE_ORACLE 0 /* brute_force_autoscale, exhaustive */
+#define OPSC_MODE_MODEL 1  /* model_level_autoscale */
+
+#define OPSC_KEY_INFEASIBLE 0x7fffffffffffffffLL
+#define OPSC_KEY_LEX_BITS 40
+
+/* Static DAG + profile tables, indexed by lex rank.
+ * Built once per planning instance by the host (opgraph.py:71-148,
+ * perfmodel.py:79-130). Passed by value to every kernel. */
+typedef struct OpscDag {
+  int32_t n_ops;
+  int32_t n_edges;
+  int32_t topo[OPSC_MAX_OPS];        /* lex ranks in OperatorDag.topo_order   */
+  int32_t node_order[OPSC_MAX_OPS];  /* lex ranks in OperatorDag.node_ids order */
+  int32_t layer_count[OPSC_MAX_OPS];
+  uint32_t pred_mask[OPSC_MAX_OPS];  /* bit p set iff edge p -> v              */
+  uint32_t sink_mask;                /* bit v set iff v has no successor       */
+  uint32_t has_phase[2];             /* bit v set iff profile of v models phase (0 prefill, 1 decode) */
+  double c0[2][OPSC_MAX_OPS];        /* LatencyModel per phase (perfmodel.py:50-64) */
+  double c1[2][OPSC_MAX_OPS];
+  double c2[2][OPSC_MAX_OPS];
+  double eta[OPSC_MAX_OPS];
+  double weight_mem[OPSC_MAX_OPS];
+  double m0[OPSC_MAX_OPS];
+  double m1[OPSC_MAX_OPS];
+  double s0[OPSC_MAX_OPS];
+  double s1[OPSC_MAX_OPS];
+  int32_t out_ptr[OPSC_MAX_OPS + 1]; /* out edges of v: [out_ptr[v], out_ptr[v+1]) in dag.out_edges order */
+  double out_v0[OPSC_MAX_EDGES];     /* volume_ref profile v0 / v1 of each out edge */
+  double out_v1[OPSC_MAX_EDGES];
+  double link_bw;
+} OpscDag;
+
+/* Brute-force candidate grid (BruteForceBounds, autoscaler.py:688-700).
+ * Menu of op v: entries e in lexicographic (P, R, B) order,
+ * e = (pi * r_max + (r - 1)) * b_max[v] + (b - 1). */
+typedef struct OpscGrid {
+  int32_t r_max;
+  int32_t n_p[OPSC_MAX_OPS];
+  int32_t p_vals[OPSC_MAX_OPS][OPSC_MAX_P]; /* ascending, duplicates kept */
+  int32_t b_max[OPSC_MAX_OPS];
+  int32_t menu_off[OPSC_MAX_OPS + 1];       /* prefix sum of menu sizes      */
+  /* AutoscaleParams view used by the init_configs pre-check */
+  int32_t r_cap;
+  int32_t params_n_p[OPSC_MAX_OPS];
+  int32_t params_p_vals[OPSC_MAX_OPS][OPSC_MAX_P];
+  int32_t params_b_max[OPSC_MAX_OPS];
+} OpscGrid;
+
+/* Model-level grid (autoscaler.py:612-615). */
+typedef struct OpscModelSpec {
+  int32_t p_base[OPSC_MAX_OPS]; /* smallest allowed P per op */
+  int32_t b_cap;                /* min over ops of b_max     */
+  int32_t r_cap;
+} OpscModelSpec;
+
+/* Default-stream placement + energy inputs (placement.py:465-491, metrics.py:34-47). */
+typedef struct OpscPlaceSpec {
+  int32_t n_devices;     /* fleet size; devices in sorted-id order */
+  int32_t uniform_cap;   /* 1: every device has mem_cap[0] */
+  double alpha;
+  double beta;
+  const double* mem_cap; /* [n_devices] host or device pointer (see entry point) */
+} OpscPlaceSpec;
+
+/* Per-window planning inputs, structure of arrays (workload.py:38-54). */
+typedef struct OpscWindows {
+  int32_t n;
+  const double* qps;
+  const int32_t* seq_len;
+  const uint8_t* phase; /* 0 prefill, 1 decode */
+  const double* slo;
+  const double* eps;
+} OpscWindows;
+
+/* Per-window decided plan, structure of arrays (autoscaler.py:76-99). */
+typedef struct OpscDecisions {
+  int64_t* key;       /* [W] best packed key (cost << 40 | lex index) or OPSC_KEY_INFEASIBLE */
+  int16_t* cfg;       /* [W][n_ops][3] P, R, B (lex-rank order)              */
+  uint8_t* feasible;  /* [W]                                                 */
+  uint32_t* status;   /* [W] OPSC_W_* bits                                   */
+  double* latency;    /* [W] iteration_latency (critical path)               */
+  int32_t* objective; /* [W] sum P*R                                         */
+  int8_t* path;       /* [W][n_ops] critical path, lex ranks, -1 padded      */
+  double* pred;       /* [W][n_ops][7] PredictedSojourn fields               */
+  uint8_t* stable;    /* [W][n_ops]                                          */
+  double* energy;     /* [W] request_energy under default-stream placement   */
+  double* memory;     /* [W] provisioned_memory under default-stream placement */
+  int32_t* devices;   /* [W] devices_used under default-stream placement     */
+} OpscDecisions;
+
+/* ---- library info ---- */
+int opsc_abi_version(void);
+const char* opsc_status_string(int status);
+int opsc_device_count(int* count);
+
+/* ---- device-pointer entry points (stream passed as cudaStream_t cast to void*) ---- */
+
+/* menu_w: [W][grid.menu_off[n_ops]] critical-path weight of every menu entry
+ * ((W+T/B)+C)*layers, +inf when unstable. status |= ZERO_DIVISION / UNSTABLE_ROUNDING. */
+int opsc_menu_build(const OpscDag* dag, const OpscGrid* grid, OpscWindows win,
+                    double* menu_w, uint32_t* status, void* stream);
+
+/* status |= OPSC_W_NO_STABLE_PARAMS when some op has no (P, B) in AutoscaleParams
+ * whose strict-stability replica floor is <= r_cap. */
+int opsc_stability_check(const OpscDag* dag, const OpscGrid* grid, OpscWindows win,
+                         uint32_t* status, void* stream);
+
+/* Exhaustive compose + SLO mask + lexicographic argmin over the shard
+ * [shard/n_shards] of every window's candidate space. key_out must be
+ * initialised to OPSC_KEY_INFEASIBLE (opsc_fill_keys); results are min-merged. */
+int opsc_compose_argmin(const OpscDag* dag, const OpscGrid* grid, OpscWindows win,
+                        const double* menu_w, int32_t shard, int32_t n_shards,
+                        int64_t* key_out, void* stream);
+
+int opsc_fill_keys(int64_t* key, int32_t n, void* stream);
+
+/* fb_entry: [W][n_ops] argmin over finite menu weights of (weight, entry), -1 if none. */
+int opsc_menu_fallback(const OpscDag* dag, const OpscGrid* grid, int32_t n_windows,
+                       const double* menu_w, int32_t* fb_entry, void* stream);
+
+/* key (+ fallback) -> cfg[W][n_ops][3], feasible, status |= NO_STABLE_BOUNDS. */
+int opsc_decode_decisions(const OpscDag* dag, const OpscGrid* grid, int32_t n_windows,
+                          const int64_t* key, const int32_t* fb_entry,
+                          int16_t* cfg, uint8_t* feasible, uint32_t* status, void* stream);
+
+/* model_level_autoscale per window -> cfg, feasible, status |= NO_STABLE_MODEL. */
+int opsc_model_grid(const OpscDag* dag, const OpscModelSpec* spec, OpscWindows win,
+                    int16_t* cfg, uint8_t* feasible, uint32_t* status, void* stream);
+
+/* cfg -> predicted, latency, path, objective, energy, memory, devices.
+ * config_order: 0 = lex-rank order (brute force), 1 = node order (model level).
+ * place.mem_cap must be a device pointer here. */
+int opsc_materialize(const OpscDag* dag, OpscWindows win, int32_t config_order,
+                     const OpscPlaceSpec* place, OpscDecisions out, void* stream);
+
+/* ---- host-buffer path: one call plans a batch of windows end to end ---- */
+typedef struct OpscContext OpscContext;
+
+int opsc_ctx_create(int32_t device, int32_t max_windows, OpscContext** out);
+int opsc_ctx_destroy(OpscContext* ctx);
+
+/* win / out / place.mem_cap are HOST pointers. Copies in, runs the mode's
+ * kernels on the context stream, copies out, synchronises. */
+int opsc_plan_windows_host(OpscContext* ctx, int32_t mode, const OpscDag* dag,
+                           const OpscGrid* grid, const OpscModelSpec* model,
+                           const OpscPlaceSpec* place, OpscWindows win,
+                           OpscDecisions out);
+
+/* Number of kernels the last opsc_plan_windows_host call launched. */
+int opsc_ctx_last_launches(const OpscContext* ctx, int32_t* launches);
+
+/* ---- measurement helper: FP64 add throughput microbenchmark ----
+ * Runs `iters` dependent-chain DADD/DSETP pairs per thread on a full grid;
+ * writes elapsed milliseconds and the executed FP64 op count. */
+int opsc_fp64_peak(int32_t iters, float* ms, double* fp64_ops, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OPSCALE_B200_H */

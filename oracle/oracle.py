@@ -1,0 +1,107 @@
+"""ctypes front-end of the CPU restatement (oracle/opsc_oracle.c).
+
+TEST INFRASTRUCTURE: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this module. The product
+package never does.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+from paper_2511_02248_b200 import abi, tables
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_build", "libopsc_oracle.so")
+
+_lib = None
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        D, I, U = C.c_double, C.c_int32, C.c_uint32
+        L.orc_op_latency.restype = D
+        L.orc_op_latency.argtypes = [D, D, D, D, C.c_int64, C.c_int64, C.c_int64]
+        L.orc_comm_time.restype = D
+        L.orc_comm_time.argtypes = [D, D, C.c_int64, C.c_int64, D]
+        L.orc_op_memory.restype = D
+        L.orc_op_memory.argtypes = [D, D, D, C.c_int64, C.c_int64, C.c_int64]
+        L.orc_erlang_c.restype = D
+        L.orc_erlang_c.argtypes = [I, D]
+        L.orc_expected_wait.restype = D
+        L.orc_expected_wait.argtypes = [D, D, I]
+        L.orc_strict_min_replicas.restype = I
+        L.orc_strict_min_replicas.argtypes = [D, D, I]
+        L.orc_py_sum.restype = D
+        L.orc_py_sum.argtypes = [P, I]
+        L.orc_critical_path.restype = D
+        L.orc_critical_path.argtypes = [P, P, P]
+        L.orc_predict.restype = I
+        L.orc_predict.argtypes = [P, D, I, I, I, I, I, I, P, P]
+        L.orc_menu_build.argtypes = [P, P, abi.OpscWindows, P, P, I]
+        L.orc_stability_check.argtypes = [P, P, abi.OpscWindows, P, I]
+        L.orc_compose_argmin.argtypes = [P, P, abi.OpscWindows, P, I, I, P, I]
+        L.orc_menu_fallback.argtypes = [P, P, I, P, P]
+        L.orc_decode_decisions.argtypes = [P, P, I, P, P, P, P, P]
+        L.orc_model_grid.argtypes = [P, P, abi.OpscWindows, P, P, P, I]
+        L.orc_materialize.argtypes = [P, abi.OpscWindows, I, P, abi.OpscDecisions, I]
+        L.orc_plan_windows.argtypes = [I, P, P, P, P, abi.OpscWindows, abi.OpscDecisions, I]
+        for f in ("orc_menu_build", "orc_stability_check", "orc_compose_argmin",
+                  "orc_menu_fallback", "orc_decode_decisions", "orc_model_grid",
+                  "orc_materialize", "orc_plan_windows"):
+            getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def threads():
+    return int(os.environ.get("OPSC_ORACLE_THREADS", os.cpu_count() or 1))
+
+
+def ref(x):
+    return C.cast(C.byref(x), C.c_void_p)
+
+
+def plan_windows(mode, problem, windows, grid=None, model=None, place=None, n_threads=None):
+    """Whole pipeline (menus -> argmin -> decode -> materialise) on the CPU."""
+    place = place or tables.pack_place()
+    out = tables.DecisionArrays(windows.n, problem.n_ops)
+    g = grid if grid is not None else abi.OpscGrid()
+    m = model if model is not None else abi.OpscModelSpec()
+    rc = lib().orc_plan_windows(mode, ref(problem.table), ref(g), ref(m), ref(place.spec),
+                                windows.struct(), out.struct(), n_threads or threads())
+    if rc != abi.OK:
+        raise RuntimeError(f"oracle status {rc}")
+    return out
+
+
+def menus(problem, grid, windows, n_threads=None):
+    E = grid.menu_off[problem.n_ops]
+    mw = np.zeros((windows.n, E), dtype=np.float64)
+    st = np.zeros(windows.n, dtype=np.uint32)
+    lib().orc_menu_build(ref(problem.table), ref(grid), windows.struct(), mw.ctypes.data,
+                         st.ctypes.data, n_threads or threads())
+    return mw, st
+
+
+def compose(problem, grid, windows, menu_w, shard=0, n_shards=1, n_threads=None, key=None):
+    key = np.full(windows.n, abi.KEY_INFEASIBLE, dtype=np.int64) if key is None else key
+    rc = lib().orc_compose_argmin(ref(problem.table), ref(grid), windows.struct(),
+                                  np.ascontiguousarray(menu_w).ctypes.data, shard, n_shards,
+                                  key.ctypes.data, n_threads or threads())
+    if rc != abi.OK:
+        raise RuntimeError(f"oracle status {rc}")
+    return key

@@ -1,0 +1,79 @@
+"""ctypes mirror of include/opscale_b200.h (structs and constants).
+
+Kept byte-for-byte in step with the header; tests/test_abi.py checks the
+struct sizes against the ones the compiled library reports.
+"""
+
+import ctypes as C
+
+ABI_VERSION = 1
+MAX_OPS = 32
+MAX_EDGES = 256
+MAX_P = 8
+MAX_DEVICES = 1024
+PRED_FIELDS = 7
+
+OK, ERR_ARG, ERR_CUDA, ERR_SPACE, ERR_NODEVICE = 0, 1, 2, 3, 4
+
+W_NO_STABLE_BOUNDS = 0x1
+W_NO_STABLE_PARAMS = 0x2
+W_NO_STABLE_MODEL = 0x4
+W_ZERO_DIVISION = 0x8
+W_UNSTABLE_ROUNDING = 0x10
+W_FLEET_EXHAUSTED = 0x20
+W_INFEASIBLE_PLACEMENT = 0x40
+W_IDLE = 0x80
+
+MODE_ORACLE = 0
+MODE_MODEL = 1
+
+KEY_INFEASIBLE = 0x7FFFFFFFFFFFFFFF
+KEY_LEX_BITS = 40
+
+_D = C.c_double
+_I = C.c_int32
+_U = C.c_uint32
+
+
+class OpscDag(C.Structure):
+    _fields_ = [
+        ("n_ops", _I), ("n_edges", _I),
+        ("topo", _I * MAX_OPS), ("node_order", _I * MAX_OPS),
+        ("layer_count", _I * MAX_OPS), ("pred_mask", _U * MAX_OPS),
+        ("sink_mask", _U), ("has_phase", _U * 2),
+        ("c0", (_D * MAX_OPS) * 2), ("c1", (_D * MAX_OPS) * 2), ("c2", (_D * MAX_OPS) * 2),
+        ("eta", _D * MAX_OPS), ("weight_mem", _D * MAX_OPS), ("m0", _D * MAX_OPS),
+        ("m1", _D * MAX_OPS), ("s0", _D * MAX_OPS), ("s1", _D * MAX_OPS),
+        ("out_ptr", _I * (MAX_OPS + 1)),
+        ("out_v0", _D * MAX_EDGES), ("out_v1", _D * MAX_EDGES),
+        ("link_bw", _D),
+    ]
+
+
+class OpscGrid(C.Structure):
+    _fields_ = [
+        ("r_max", _I), ("n_p", _I * MAX_OPS), ("p_vals", (_I * MAX_P) * MAX_OPS),
+        ("b_max", _I * MAX_OPS), ("menu_off", _I * (MAX_OPS + 1)),
+        ("r_cap", _I), ("params_n_p", _I * MAX_OPS),
+        ("params_p_vals", (_I * MAX_P) * MAX_OPS), ("params_b_max", _I * MAX_OPS),
+    ]
+
+
+class OpscModelSpec(C.Structure):
+    _fields_ = [("p_base", _I * MAX_OPS), ("b_cap", _I), ("r_cap", _I)]
+
+
+class OpscPlaceSpec(C.Structure):
+    _fields_ = [("n_devices", _I), ("uniform_cap", _I), ("alpha", _D), ("beta", _D),
+                ("mem_cap", C.c_void_p)]
+
+
+class OpscWindows(C.Structure):
+    _fields_ = [("n", _I), ("qps", C.c_void_p), ("seq_len", C.c_void_p),
+                ("phase", C.c_void_p), ("slo", C.c_void_p), ("eps", C.c_void_p)]
+
+
+class OpscDecisions(C.Structure):
+    _fields_ = [(name, C.c_void_p) for name in (
+        "key", "cfg", "feasible", "status", "latency", "objective", "path",
+        "pred", "stable", "energy", "memory", "devices")]

@@ -1,0 +1,99 @@
+"""Turn per-window decision arrays into reference-shaped ScalingPlans.
+
+The device path returns structure-of-arrays decisions (OpscDecisions); this
+module maps them back onto the planner API: OperatorConfig / PredictedSojourn
+/ ScalingPlan objects (autoscaler.py:44-99, _make_plan :231-247) and the
+reference's exceptions, raised in the order the reference would hit them
+(autoscaler.py:706-847 for the oracle, :596-681 for the model level).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+from . import abi, errors, model
+
+# config dict order per mode: brute force builds configs in sorted-id order
+# (autoscaler.py:825, 843-845); the model level in dag.node_ids order (:617-618)
+ORDER_LEX, ORDER_NODE = 0, 1
+
+
+def raise_for_status(status: int, mode: int, err=errors):
+    if status & abi.W_ZERO_DIVISION:
+        raise ZeroDivisionError("float division by zero")
+    if status & abi.W_UNSTABLE_ROUNDING:
+        raise err.Unstable("utilization rounds to 1: queue has no steady state")
+    if mode == abi.MODE_ORACLE:
+        if status & abi.W_NO_STABLE_PARAMS:
+            raise err.NoStableConfig(
+                "arrival rate exceeds capacity at every (B, P) within r_cap")
+        if status & abi.W_NO_STABLE_BOUNDS:
+            raise err.NoStableConfig("operator has no stable configuration within bounds")
+    elif status & abi.W_NO_STABLE_MODEL:
+        raise err.NoStableConfig(
+            "model-level: arrival rate exceeds capacity at every batch size within r_cap")
+
+
+@dataclass
+class PlanMetrics:
+    """Default-stream placement figures of a feasible plan (runner.py:94-96)."""
+
+    devices_used: int
+    energy_joules: float
+    memory_bytes: float
+    error: str | None = None
+
+
+class WindowDecisions:
+    """Decisions for a batch of windows, with lazy plan materialisation."""
+
+    def __init__(self, problem, points, arrays, mode, types=model, err=errors):
+        self.problem, self.points, self.arrays, self.mode = problem, points, arrays, mode
+        self.types, self.err = types, err
+
+    def __len__(self):
+        return self.arrays.n_windows
+
+    def status(self, i):
+        return int(self.arrays.status[i])
+
+    def plan(self, i):
+        a, n, ids, T = self.arrays, self.problem.n_ops, self.problem.ids, self.types
+        st = int(a.status[i])
+        if st & abi.W_IDLE:
+            return None
+        raise_for_status(st, self.mode, self.err)
+        if self.mode == abi.MODE_ORACLE:
+            order = range(n)
+        else:
+            order = [self.problem.table.node_order[k] for k in range(n)]
+        configs, predicted = {}, {}
+        for v in order:
+            p, r, b = (int(x) for x in a.cfg[i, v])
+            configs[ids[v]] = T.OperatorConfig(p=p, r=r, b=b)
+            f = [float(x) for x in a.pred[i, v]]
+            predicted[ids[v]] = T.PredictedSojourn(
+                op_latency=f[0], lam=f[1], mu=f[2], utilization=f[3], wait=f[4],
+                service=f[5], comm=f[6], stable=bool(a.stable[i, v]))
+        lat = float(a.latency[i])
+        path = [ids[x] for x in a.path[i] if x >= 0] if math.isfinite(lat) else []
+        return T.ScalingPlan(
+            configs=configs, predicted=predicted, iteration_latency=lat,
+            critical_path=path, objective=int(a.objective[i]),
+            feasible=bool(a.feasible[i]), phase=self.points[i].phase, trace=[])
+
+    def plans(self):
+        return [self.plan(i) for i in range(len(self))]
+
+    def metrics(self, i):
+        a = self.arrays
+        st = int(a.status[i])
+        if not a.feasible[i] or st & abi.W_IDLE:
+            return None
+        error = None
+        if st & abi.W_FLEET_EXHAUSTED:
+            error = "FleetExhausted"
+        elif st & abi.W_INFEASIBLE_PLACEMENT:
+            error = "InfeasiblePlacement"
+        return PlanMetrics(int(a.devices[i]), float(a.energy[i]), float(a.memory[i]), error)

@@ -1,0 +1,499 @@
+"""Freeze golden vectors from the REFERENCE planner (build container only).
+
+Imports the read-only reference from /root/reference/pkg/src and runs its
+own public functions on seeded synthetic instances; every float is stored as
+float.hex() so parity checks are bit-exact. Output: tests/golden/*.json.
+
+    PYTHONHASHSEED=0 PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+What is frozen (reference call sites in brackets):
+  kats.json      erlang_c / expected_wait / min_replicas_stable / op_latency /
+                 comm_time / op_memory / critical_path_latency on grids and the
+                 SPEC.md examples  [queueing.py:54-97, perfmodel.py:133-171,
+                 opgraph.py:199-244]
+  menus.json     predict_op for every brute-force menu entry of sampled windows
+                 [autoscaler.py:174-194, 743-757]
+  oracle.json    brute_force_autoscale plans (or the error raised) on scenario
+                 windows and random DAGs, plus default-stream placement metrics
+                 [autoscaler.py:706-847, placement.py:465-491, metrics.py:84-132]
+  model.json     model_level_autoscale plans (+ metrics) [autoscaler.py:596-681]
+
+Brute-force leaves sum path weights in frozenset order, which depends on
+PYTHONHASHSEED (autoscaler.py:765, 792-794). Every oracle case is re-run
+under hash seeds 1..3 in subprocesses; cases whose decision changes are
+flagged "hash_sensitive" (the canonical critical-path order decides them).
+"""
+
+import json
+import math
+import os
+import subprocess
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import opscaler as ref  # noqa: E402
+from opscaler import autoscaler as A  # noqa: E402
+from opscaler import metrics as M  # noqa: E402
+from opscaler import placement as PL  # noqa: E402
+from opscaler import perfmodel as PM  # noqa: E402
+from opscaler import queueing as Q  # noqa: E402
+from opscaler import opgraph as G  # noqa: E402
+
+from paper_2511_02248_b200 import scenarios as S  # noqa: E402
+
+A.MAX_ENUMERATION = 10**12  # sampled windows exceed the 1e7 guard on purpose
+
+
+def H(x):
+    return float(x).hex()
+
+
+# ----------------------------------------------------------------- instances
+
+KINDS = ["attention", "linear", "norm", "activation", "embedding", "other"]
+
+
+def random_instance(rng, idx):
+    """Random DAG (chain / diamond / merge / fork / random) with random profiles."""
+    shape = ["chain", "diamond", "merge", "fork", "random"][idx % 5]
+    if shape == "chain":
+        n = int(rng.integers(1, 7))
+        ids = [f"op{i}" for i in range(n)]
+        rng.shuffle(ids)  # ids not in path order, so lex order != topo order
+        edges = list(zip(ids, ids[1:]))
+    elif shape == "diamond":
+        ids = ["s", "a", "b", "t"]
+        edges = [("s", "a"), ("s", "b"), ("a", "t"), ("b", "t")]
+    elif shape == "merge":
+        ids = ["v1", "v2", "t1", "m", "z"]
+        edges = [("v1", "v2"), ("v2", "m"), ("t1", "m"), ("m", "z")]
+    elif shape == "fork":
+        ids = ["root", "x", "y", "yy", "w"]
+        edges = [("root", "x"), ("root", "y"), ("y", "yy"), ("x", "w")]
+    else:
+        n = int(rng.integers(3, 7))
+        ids = [f"n{c}" for c in "fbdaec"[:n]]
+        edges = []
+        for j in range(1, n):
+            for i in range(j):
+                if rng.uniform() < 0.4:
+                    edges.append((ids[i], ids[j]))
+        if not edges:
+            edges = [(ids[0], ids[1])]
+    nodes = []
+    prof = {"_link_bandwidth": float(rng.choice([600e9, 900e9])),
+            "_interference": {"theta": 0.5, "exponent": 1.0}}
+    for i in ids:
+        kind = KINDS[int(rng.integers(0, len(KINDS)))]
+        layers = int(rng.choice([1, 2, 8, 32, 80]))
+        nodes.append({"id": i, "kind": kind, "layer_count": layers, "profile_ref": "p_" + i})
+        c0 = float(rng.uniform(2e-6, 4e-5))
+        c1 = float(10 ** rng.uniform(-9.5, -6.3))
+        c2 = float(10 ** rng.uniform(-11, -9.6)) if kind == "attention" else 0.0
+        prof["p_" + i] = {
+            "prefill": {"c0": c0, "c1": c1, "c2": c2},
+            "decode": {"c0": c0 * 1.5, "c1": c1 * 1.2, "c2": 0.0},
+            "weight_mem": float(rng.choice([0.0, 1e7, 2e8, 3e9])),
+            "m0": float(rng.choice([0.0, 1e6])), "m1": float(rng.uniform(1e3, 7e4)),
+            "v0": float(rng.choice([0.0, 4096.0])), "v1": float(rng.uniform(4e3, 5e4)),
+            "s0": float(rng.uniform(0.02, 0.4)), "s1": float(rng.uniform(1e-6, 7e-4)),
+            "eta": float(rng.choice([0.9, 0.8, 1.0])), "kind": kind,
+        }
+    dag = {"nodes": nodes,
+           "edges": [{"src": a, "dst": b, "volume_ref": "p_" + a} for a, b in edges]}
+    phase = "prefill" if rng.uniform() < 0.6 else "decode"
+    seq_len = int(rng.choice([1, 128, 1024, 4096])) if phase == "prefill" else 1
+    qps = float(10 ** rng.uniform(0.0, 2.3)) if phase == "prefill" else float(10 ** rng.uniform(1.5, 3.6))
+    return shape, dag, prof, phase, seq_len, qps
+
+
+def build(dag_spec, prof):
+    return ref.build_dag(dag_spec), PM.profiles_from_dict(prof)
+
+
+def plan_json(plan):
+    return {
+        "configs": [[op, c.p, c.r, c.b] for op, c in plan.configs.items()],
+        "predicted": {op: [H(p.op_latency), H(p.lam), H(p.mu), H(p.utilization),
+                           H(p.wait), H(p.service), H(p.comm), bool(p.stable)]
+                      for op, p in plan.predicted.items()},
+        "iteration_latency": H(plan.iteration_latency),
+        "critical_path": list(plan.critical_path),
+        "objective": int(plan.objective),
+        "feasible": bool(plan.feasible),
+        "phase": plan.phase,
+    }
+
+
+def metrics_json(plan, dag, profiles, point, n_devices, mem_cap):
+    """Default-stream placement + Eq. 9 energy + provisioned memory."""
+    if not plan.feasible:
+        return None
+    fleet = PL.make_fleet(n_devices, mem_cap=mem_cap)
+    try:
+        placed = PL.default_stream_place(plan, dag, profiles, fleet,
+                                         PL.PlacementParams(slo=1.0), point)
+    except ref.OpscalerError as exc:
+        return {"error": type(exc).__name__}
+    energy = M.request_energy(plan, placed, dag, profiles, point, M.EnergyParams())
+    return {"devices": placed.devices_used, "energy": H(energy),
+            "memory": H(M.provisioned_memory(plan, placed))}
+
+
+def run_oracle(dag_spec, prof, point, params, bounds):
+    dag, profiles = build(dag_spec, prof)
+    try:
+        plan = A.brute_force_autoscale(dag, profiles, point, params, bounds)
+    except ref.OpscalerError as exc:
+        return {"error": type(exc).__name__}, None, dag, profiles
+    return plan_json(plan), plan, dag, profiles
+
+
+def run_model(dag_spec, prof, point, params):
+    dag, profiles = build(dag_spec, prof)
+    try:
+        plan = A.model_level_autoscale(dag, profiles, point, params)
+    except ref.OpscalerError as exc:
+        return {"error": type(exc).__name__}, None, dag, profiles
+    return plan_json(plan), plan, dag, profiles
+
+
+def params_json(p):
+    return {"slo": H(p.slo), "epsilon": H(p.epsilon), "b_max": p.b_max,
+            "parallelism": list(p.parallelism), "r_cap": p.r_cap}
+
+
+def point_json(pt):
+    return {"qps": H(pt.qps), "seq_len": pt.seq_len, "phase": pt.phase}
+
+
+# ----------------------------------------------------------------- case lists
+
+
+def oracle_cases():
+    cases = []
+    rng = np.random.default_rng(2511)
+    # scenario windows
+    for cfg, windows in (("cfg1", [0]), ("cfg3s", [0, 2, 5, 17, 33, 41]),
+                         ("cfg5", [0, 90, 200, 333, 480, 611, 700, 777, 860, 905,
+                                   1000, 1100, 1203, 1300, 1377, 1439])):
+        dag_spec, prof = S.SCENARIOS[cfg]
+        tw = S.trace_windows(cfg)
+        g = S.GRIDS[cfg]
+        for w in windows:
+            for ph in ("prefill", "decode"):
+                if cfg == "cfg5" and ph == "decode" and w % 3:
+                    continue
+                qps = float(tw[ph + "_qps"][w])
+                if qps <= 0:
+                    continue
+                cases.append(dict(name=f"{cfg}/w{w}/{ph}", scenario=cfg,
+                                  point=dict(qps=qps, seq_len=int(tw[ph + "_len"][w]), phase=ph),
+                                  params=dict(slo=S.SLO[cfg][ph]),
+                                  bounds=dict(r_max=g["r_max"], b_max=g["b_max"],
+                                              parallelism=list(g["parallelism"]))))
+    # targeted edge cases: NoStableConfig from the greedy pre-check (params)
+    # and from the bounds fallback, infeasible SLO, single op, SLO == latency
+    c7, p7 = S.SCENARIOS["cfg1"]
+    cases.append(dict(name="edge/nostable_params", scenario="cfg1",
+                      point=dict(qps=1e9, seq_len=2048, phase="prefill"), params=dict(slo=0.5),
+                      bounds=dict(r_max=3, b_max=2, parallelism=[1, 2])))
+    cases.append(dict(name="edge/nostable_bounds", scenario="cfg1",
+                      point=dict(qps=40.0, seq_len=4096, phase="prefill"), params=dict(slo=0.5),
+                      bounds=dict(r_max=1, b_max=1, parallelism=[1])))
+    cases.append(dict(name="edge/infeasible_slo", scenario="cfg1",
+                      point=dict(qps=10.0, seq_len=1024, phase="prefill"), params=dict(slo=1e-4),
+                      bounds=dict(r_max=2, b_max=2, parallelism=[1, 2])))
+    one = {"nodes": [{"id": "solo", "kind": "linear", "layer_count": 32, "profile_ref": "mlp"}],
+           "edges": []}
+    cases.append(dict(name="edge/single_op", dag=one, profiles=p7,
+                      point=dict(qps=50.0, seq_len=2048, phase="prefill"), params=dict(slo=0.2),
+                      bounds=dict(r_max=8, b_max=4, parallelism=[1, 2, 4, 8])))
+    two = {"nodes": [{"id": "b2", "kind": "linear", "layer_count": 32, "profile_ref": "mlp"},
+                     {"id": "a1", "kind": "attention", "layer_count": 32, "profile_ref": "attn"}],
+           "edges": [{"src": "b2", "dst": "a1", "volume_ref": "mlp"}]}
+    d2, pr2 = build(two, p7)
+    pt2 = ref.WorkloadPoint(30.0, 2048, "prefill")
+    ev = A._Evaluator(d2, pr2, pt2, ref.AutoscaleParams(slo=1.0))
+    for cfgs in ({"b2": (1, 2, 1), "a1": (2, 2, 1)}, {"b2": (2, 3, 2), "a1": (1, 3, 2)}):
+        lat = ev.evaluate({k: A.OperatorConfig(*v) for k, v in cfgs.items()}).latency
+        for slo in (lat, float(np.nextafter(lat, 0.0))):
+            cases.append(dict(name=f"edge/slo_eq_latency/{slo.hex()}", dag=two, profiles=p7,
+                              point=dict(qps=30.0, seq_len=2048, phase="prefill"),
+                              params=dict(slo=slo), bounds=dict(r_max=3, b_max=2, parallelism=[1, 2])))
+    # random small DAGs
+    for i in range(90):
+        shape, dag_spec, prof, phase, L, qps = random_instance(rng, i)
+        n = len(dag_spec["nodes"])
+        r_max = int(rng.integers(1, 5))
+        b_max = int(rng.integers(1, 4))
+        par = [1, 2] if rng.uniform() < 0.7 else [1, 2, 4]
+        while (len(par) * r_max * b_max) ** n > 3_000_000:
+            r_max = max(1, r_max - 1)
+            if (len(par) * r_max * b_max) ** n > 3_000_000:
+                b_max = max(1, b_max - 1)
+            if r_max == 1 and b_max == 1:
+                break
+        # SLO drawn around the uniform lower bound so feasible/infeasible mix
+        slo = float(10 ** rng.uniform(-3.0, 0.5))
+        eps = 0.0 if rng.uniform() < 0.7 else slo * 0.1
+        cases.append(dict(name=f"rand{i}/{shape}", dag=dag_spec, profiles=prof,
+                          point=dict(qps=qps, seq_len=L, phase=phase),
+                          params=dict(slo=slo, epsilon=eps),
+                          bounds=dict(r_max=r_max, b_max=b_max, parallelism=par)))
+    return cases
+
+
+def model_cases():
+    cases = []
+    rng = np.random.default_rng(4242)
+    for cfg, windows in (("cfg1", [0]), ("cfg2", list(range(60))),
+                         ("cfg3", list(range(0, 60, 3))), ("cfg5", list(range(0, 1440, 97)))):
+        dag_spec, prof = S.SCENARIOS[cfg]
+        tw = S.trace_windows(cfg)
+        for w in windows:
+            for ph in ("prefill", "decode"):
+                qps = float(tw[ph + "_qps"][w])
+                if qps <= 0:
+                    continue
+                cases.append(dict(name=f"{cfg}/w{w}/{ph}", scenario=cfg,
+                                  point=dict(qps=qps, seq_len=int(tw[ph + "_len"][w]), phase=ph),
+                                  params=dict(slo=S.SLO[cfg][ph],
+                                              epsilon=0.0 if w % 2 else S.SLO[cfg][ph] * 0.05)))
+    c7, p7 = S.SCENARIOS["cfg1"]
+    cases.append(dict(name="edge/model_nostable", scenario="cfg1",
+                      point=dict(qps=5e4, seq_len=2048, phase="prefill"),
+                      params=dict(slo=0.5, r_cap=4)))
+    cases.append(dict(name="edge/model_fallback", scenario="cfg1",
+                      point=dict(qps=30.0, seq_len=2048, phase="prefill"),
+                      params=dict(slo=0.01, r_cap=16)))
+    for i in range(60):
+        shape, dag_spec, prof, phase, L, qps = random_instance(rng, i)
+        slo = float(10 ** rng.uniform(-3.0, 0.5))
+        eps = 0.0 if rng.uniform() < 0.6 else slo * float(rng.uniform(0.01, 0.3))
+        b_max = int(rng.choice([1, 4, 8, 32]))
+        par = [1, 2, 4, 8] if rng.uniform() < 0.5 else [2, 4]
+        r_cap = int(rng.choice([8, 64, 512]))
+        cases.append(dict(name=f"rand{i}/{shape}", dag=dag_spec, profiles=prof,
+                          point=dict(qps=qps, seq_len=L, phase=phase),
+                          params=dict(slo=slo, epsilon=eps, b_max=b_max, parallelism=par,
+                                      r_cap=r_cap)))
+    return cases
+
+
+def case_inputs(c):
+    if "scenario" in c:
+        dag_spec, prof = S.SCENARIOS[c["scenario"]]
+    else:
+        dag_spec, prof = c["dag"], c["profiles"]
+    pt = ref.WorkloadPoint(c["point"]["qps"], c["point"]["seq_len"], c["point"]["phase"])
+    kw = dict(c["params"])
+    if "parallelism" in kw:
+        kw["parallelism"] = tuple(kw["parallelism"])
+    params = ref.AutoscaleParams(**kw)
+    bounds = None
+    if "bounds" in c:
+        b = dict(c["bounds"])
+        b["parallelism"] = tuple(b["parallelism"])
+        bounds = ref.BruteForceBounds(**b)
+    return dag_spec, prof, pt, params, bounds
+
+
+def serialise_case(c, pt, params, bounds):
+    out = {"name": c["name"]}
+    if "scenario" in c:
+        out["scenario"] = c["scenario"]
+    else:
+        out["dag"], out["profiles"] = c["dag"], c["profiles"]
+    out["point"] = point_json(pt)
+    out["params"] = params_json(params)
+    if bounds is not None:
+        out["bounds"] = {"r_max": bounds.r_max, "b_max": bounds.b_max,
+                         "parallelism": list(bounds.parallelism)}
+    return out
+
+
+def decisions_only():
+    """Child mode: print brute-force decisions (configs/objective/feasible)."""
+    res = []
+    for c in oracle_cases():
+        dag_spec, prof, pt, params, bounds = case_inputs(c)
+        j, _, _, _ = run_oracle(dag_spec, prof, pt, params, bounds)
+        res.append(j.get("error") or [j["configs"], j["objective"], j["feasible"]])
+    print(json.dumps(res))
+
+
+# ----------------------------------------------------------------- KATs
+
+
+def kats():
+    out = {"erlang_c": [], "expected_wait": [], "min_replicas_stable": [],
+           "op_latency": [], "comm_time": [], "op_memory": [], "critical_path": []}
+    rng = np.random.default_rng(7)
+    for R in (1, 2, 3, 4, 7, 8, 16, 64, 100, 511, 512):
+        for rho in (1e-6, 0.01, 0.3, 0.5, 0.7, 0.9, 0.99, 0.999999, float(rng.uniform(0, 1))):
+            out["erlang_c"].append([R, H(rho), H(Q.erlang_c(R, rho))])
+    for _ in range(200):
+        R = int(rng.integers(1, 40))
+        mu = float(10 ** rng.uniform(-2, 3))
+        lam = float(R * mu * rng.uniform(0.01, 0.999))
+        out["expected_wait"].append([H(lam), H(mu), R, H(Q.expected_wait(Q.QueueOperatingPoint(lam, mu, R)))])
+    out["expected_wait"] += [[H(1.0), H(2.0), 1, H(0.5)], [H(1.0), H(1.0), 2, H(Q.expected_wait(Q.QueueOperatingPoint(1.0, 1.0, 2)))]]
+    for lam, mu in ((10.0, 3.0), (6.0, 3.0), (0.1, 100.0)) + tuple(
+            (float(10 ** rng.uniform(-1, 3)), float(10 ** rng.uniform(-1, 2))) for _ in range(100)):
+        out["min_replicas_stable"].append([H(lam), H(mu), Q.min_replicas_stable(lam, mu),
+                                           A._strict_min_replicas(lam, mu, 512)])
+    for _ in range(300):
+        c = [float(10 ** rng.uniform(-7, -4)), float(10 ** rng.uniform(-10, -6)),
+             float(10 ** rng.uniform(-12, -9)) if rng.uniform() < 0.4 else 0.0]
+        eta = float(rng.choice([0.9, 0.8, 1.0, 0.75]))
+        prof = PM.OperatorProfile("x", {"prefill": PM.LatencyModel(*c)}, eta=eta,
+                                  s0=float(rng.uniform(0, 0.5)), s1=float(rng.uniform(0, 1e-3)),
+                                  weight_mem=float(rng.uniform(0, 1e10)), m0=float(rng.uniform(0, 1e7)),
+                                  m1=float(rng.uniform(0, 1e5)), v0=float(rng.uniform(0, 1e4)),
+                                  v1=float(rng.uniform(0, 1e5)))
+        B, L, P = int(rng.integers(1, 65)), int(rng.integers(1, 32769)), int(rng.choice([1, 2, 4, 8]))
+        bw = float(rng.choice([600e9, 900e9, 1.8e12]))
+        out["op_latency"].append([[H(x) for x in c], H(eta), B, L, P,
+                                  H(PM.op_latency(prof, "prefill", B, L, P))])
+        out["comm_time"].append([H(prof.v0), H(prof.v1), B, L, H(bw), H(PM.comm_time(prof, B, L, bw))])
+        out["op_memory"].append([H(prof.weight_mem), H(prof.m0), H(prof.m1), B, L, P,
+                                 H(PM.op_memory(prof, B, L, P))])
+    # SPEC.md:132 example (eta=1) and the default-eta variant
+    prof = PM.OperatorProfile("a", {"prefill": PM.LatencyModel(0.0, 0.0, 1e-9)}, eta=1.0)
+    out["op_latency"].append([[H(0.0), H(0.0), H(1e-9)], H(1.0), 1, 2048, 1,
+                              H(PM.op_latency(prof, "prefill", 1, 2048, 1))])
+    # critical path: SPEC examples + random DAGs with ties
+    specs = [
+        ({"nodes": [{"id": "a"}, {"id": "b"}, {"id": "c"}],
+          "edges": [{"src": "a", "dst": "b"}, {"src": "b", "dst": "c"}]},
+         {"a": (1.0, 0.0), "b": (2.0, 0.0), "c": (3.0, 0.0)}),
+        ({"nodes": [{"id": "s"}, {"id": "a"}, {"id": "b"}, {"id": "t"}],
+          "edges": [{"src": "s", "dst": "a"}, {"src": "s", "dst": "b"},
+                    {"src": "a", "dst": "t"}, {"src": "b", "dst": "t"}]},
+         {"s": (1.0, 0.0), "a": (2.0, 0.0), "b": (5.0, 0.0), "t": (1.0, 0.0)}),
+        ({"nodes": [{"id": "a"}, {"id": "b", "layer_count": 32}],
+          "edges": [{"src": "a", "dst": "b"}]},
+         {"a": (1.0, 0.0), "b": (2.0, 0.0)}),
+        # equal-weight branches: path tie-break by lexicographic id tuple
+        ({"nodes": [{"id": "s"}, {"id": "y"}, {"id": "x"}, {"id": "t"}, {"id": "u"}],
+          "edges": [{"src": "s", "dst": "y"}, {"src": "s", "dst": "x"},
+                    {"src": "y", "dst": "t"}, {"src": "x", "dst": "t"}, {"src": "u", "dst": "t"}]},
+         {"s": (1.0, 0.0), "y": (2.0, 0.0), "x": (2.0, 0.0), "t": (1.0, 0.0), "u": (3.0, 0.0)}),
+    ]
+    for _ in range(60):
+        n = int(rng.integers(2, 9))
+        ids = [f"k{i}" for i in rng.permutation(n)]
+        edges = [{"src": ids[i], "dst": ids[j]} for j in range(1, n) for i in range(j)
+                 if rng.uniform() < 0.35]
+        nodes = [{"id": i, "layer_count": int(rng.choice([1, 2, 32]))} for i in ids]
+        # small integer weights create many exact ties
+        soj = {i: (float(rng.integers(0, 4)), float(rng.integers(0, 2)) * 0.5) for i in ids}
+        specs.append(({"nodes": nodes, "edges": edges}, soj))
+    for spec, soj in specs:
+        dag = G.build_dag(spec)
+        lat, path = G.critical_path_latency(dag, {k: G.NodeSojourn(*v) for k, v in soj.items()})
+        out["critical_path"].append({"dag": spec, "sojourn": {k: [H(a), H(b)] for k, (a, b) in soj.items()},
+                                     "latency": H(lat), "path": path})
+    return out
+
+
+# ----------------------------------------------------------------- menus
+
+
+def menus():
+    out = []
+    for cfg, windows in (("cfg1", [0]), ("cfg3s", [0, 2]), ("cfg5", [0, 700, 1439]), ("cfg2", [0, 31])):
+        dag_spec, prof = S.SCENARIOS[cfg]
+        dag, profiles = build(dag_spec, prof)
+        tw = S.trace_windows(cfg)
+        g = S.GRIDS[cfg]
+        for w in windows:
+            for ph in ("prefill", "decode"):
+                pt = ref.WorkloadPoint(float(tw[ph + "_qps"][w]), int(tw[ph + "_len"][w]), ph)
+                params = ref.AutoscaleParams(slo=S.SLO[cfg][ph])
+                ev = A._Evaluator(dag, profiles, pt, params)
+                ent = {}
+                for op in sorted(dag.node_ids):
+                    rows = []
+                    for p in g["parallelism"]:
+                        for r in range(1, g["r_max"] + 1):
+                            for b in range(1, g["b_max"] + 1):
+                                pr = ev.predict_op(op, A.OperatorConfig(p=p, r=r, b=b))
+                                wgt = ((pr.sojourn + pr.comm) * dag.node(op).layer_count
+                                       if pr.stable else math.inf)
+                                rows.append([p, r, b, H(pr.op_latency), H(pr.wait), H(pr.comm), H(wgt)])
+                    ent[op] = rows
+                out.append({"scenario": cfg, "window": w, "point": point_json(pt), "grid": g,
+                            "entries": ent})
+    return out
+
+
+# ----------------------------------------------------------------- main
+
+
+def main():
+    if "--decisions-only" in sys.argv:
+        decisions_only()
+        return
+    os.makedirs(HERE, exist_ok=True)
+    json.dump(kats(), open(os.path.join(HERE, "kats.json"), "w"), separators=(",", ":"))
+    print("kats done")
+    json.dump(menus(), open(os.path.join(HERE, "menus.json"), "w"), separators=(",", ":"))
+    print("menus done")
+
+    oracle = []
+    for c in oracle_cases():
+        dag_spec, prof, pt, params, bounds = case_inputs(c)
+        j, plan, dag, profiles = run_oracle(dag_spec, prof, pt, params, bounds)
+        rec = serialise_case(c, pt, params, bounds)
+        rec["expected"] = j
+        if plan is not None:
+            rec["metrics"] = metrics_json(plan, dag, profiles, pt, 256, 180e9)
+            rec["metrics_small_fleet"] = metrics_json(plan, dag, profiles, pt, 4, 40e9)
+            rec["metrics_tiny_cap"] = metrics_json(plan, dag, profiles, pt, 64, 2.0e8)
+        oracle.append(rec)
+    # hash-seed sensitivity of the frozenset leaf order
+    base = [r["expected"].get("error") or [r["expected"]["configs"], r["expected"]["objective"],
+                                           r["expected"]["feasible"]] for r in oracle]
+    base = json.loads(json.dumps(base))
+    sensitive = set()
+    for seed in ("1", "2", "3"):
+        env = dict(os.environ, PYTHONHASHSEED=seed, PYTHONDONTWRITEBYTECODE="1")
+        res = subprocess.run([sys.executable, __file__, "--decisions-only"], env=env,
+                             capture_output=True, text=True, check=True)
+        other = json.loads(res.stdout.strip().splitlines()[-1])
+        for i, (a, b) in enumerate(zip(base, other)):
+            if a != b:
+                sensitive.add(i)
+    for i, r in enumerate(oracle):
+        r["hash_sensitive"] = i in sensitive
+    json.dump(oracle, open(os.path.join(HERE, "oracle.json"), "w"), separators=(",", ":"))
+    n_err = sum("error" in r["expected"] for r in oracle)
+    n_feas = sum(r["expected"].get("feasible", False) for r in oracle)
+    print(f"oracle: {len(oracle)} cases, {n_feas} feasible, {n_err} errors, "
+          f"{len(sensitive)} hash-sensitive")
+
+    model = []
+    for c in model_cases():
+        dag_spec, prof, pt, params, _ = case_inputs(c)
+        j, plan, dag, profiles = run_model(dag_spec, prof, pt, params)
+        rec = serialise_case(c, pt, params, None)
+        rec["expected"] = j
+        if plan is not None:
+            rec["metrics"] = metrics_json(plan, dag, profiles, pt, 4096, 180e9)
+        model.append(rec)
+    json.dump(model, open(os.path.join(HERE, "model.json"), "w"), separators=(",", ":"))
+    n_err = sum("error" in r["expected"] for r in model)
+    n_feas = sum(r["expected"].get("feasible", False) for r in model)
+    print(f"model: {len(model)} cases, {n_feas} feasible, {n_err} errors")
+
+
+if __name__ == "__main__":
+    main()
