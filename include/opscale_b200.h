@@ -43,6 +43,12 @@
 #include <stdint.h>
 #include <stddef.h>
 
+#if defined(__GNUC__)
+#define OPSC_API __attribute__((visibility("default")))
+#else
+#define OPSC_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -165,70 +171,70 @@ typedef struct OpscDecisions {
 } OpscDecisions;
 
 /* ---- library info ---- */
-int opsc_abi_version(void);
-const char* opsc_status_string(int status);
-int opsc_device_count(int* count);
+OPSC_API int opsc_abi_version(void);
+OPSC_API const char* opsc_status_string(int status);
+OPSC_API int opsc_device_count(int* count);
 
 /* ---- device-pointer entry points (stream passed as cudaStream_t cast to void*) ---- */
 
 /* menu_w: [W][grid.menu_off[n_ops]] critical-path weight of every menu entry
  * ((W+T/B)+C)*layers, +inf when unstable. status |= ZERO_DIVISION / UNSTABLE_ROUNDING. */
-int opsc_menu_build(const OpscDag* dag, const OpscGrid* grid, OpscWindows win,
+OPSC_API int opsc_menu_build(const OpscDag* dag, const OpscGrid* grid, OpscWindows win,
                     double* menu_w, uint32_t* status, void* stream);
 
 /* status |= OPSC_W_NO_STABLE_PARAMS when some op has no (P, B) in AutoscaleParams
  * whose strict-stability replica floor is <= r_cap. */
-int opsc_stability_check(const OpscDag* dag, const OpscGrid* grid, OpscWindows win,
+OPSC_API int opsc_stability_check(const OpscDag* dag, const OpscGrid* grid, OpscWindows win,
                          uint32_t* status, void* stream);
 
 /* Exhaustive compose + SLO mask + lexicographic argmin over the shard
  * [shard/n_shards] of every window's candidate space. key_out must be
  * initialised to OPSC_KEY_INFEASIBLE (opsc_fill_keys); results are min-merged. */
-int opsc_compose_argmin(const OpscDag* dag, const OpscGrid* grid, OpscWindows win,
+OPSC_API int opsc_compose_argmin(const OpscDag* dag, const OpscGrid* grid, OpscWindows win,
                         const double* menu_w, int32_t shard, int32_t n_shards,
                         int64_t* key_out, void* stream);
 
-int opsc_fill_keys(int64_t* key, int32_t n, void* stream);
+OPSC_API int opsc_fill_keys(int64_t* key, int32_t n, void* stream);
 
 /* fb_entry: [W][n_ops] argmin over finite menu weights of (weight, entry), -1 if none. */
-int opsc_menu_fallback(const OpscDag* dag, const OpscGrid* grid, int32_t n_windows,
+OPSC_API int opsc_menu_fallback(const OpscDag* dag, const OpscGrid* grid, int32_t n_windows,
                        const double* menu_w, int32_t* fb_entry, void* stream);
 
 /* key (+ fallback) -> cfg[W][n_ops][3], feasible, status |= NO_STABLE_BOUNDS. */
-int opsc_decode_decisions(const OpscDag* dag, const OpscGrid* grid, int32_t n_windows,
+OPSC_API int opsc_decode_decisions(const OpscDag* dag, const OpscGrid* grid, int32_t n_windows,
                           const int64_t* key, const int32_t* fb_entry,
                           int16_t* cfg, uint8_t* feasible, uint32_t* status, void* stream);
 
 /* model_level_autoscale per window -> cfg, feasible, status |= NO_STABLE_MODEL. */
-int opsc_model_grid(const OpscDag* dag, const OpscModelSpec* spec, OpscWindows win,
+OPSC_API int opsc_model_grid(const OpscDag* dag, const OpscModelSpec* spec, OpscWindows win,
                     int16_t* cfg, uint8_t* feasible, uint32_t* status, void* stream);
 
 /* cfg -> predicted, latency, path, objective, energy, memory, devices.
  * config_order: 0 = lex-rank order (brute force), 1 = node order (model level).
  * place.mem_cap must be a device pointer here. */
-int opsc_materialize(const OpscDag* dag, OpscWindows win, int32_t config_order,
+OPSC_API int opsc_materialize(const OpscDag* dag, OpscWindows win, int32_t config_order,
                      const OpscPlaceSpec* place, OpscDecisions out, void* stream);
 
 /* ---- host-buffer path: one call plans a batch of windows end to end ---- */
 typedef struct OpscContext OpscContext;
 
-int opsc_ctx_create(int32_t device, int32_t max_windows, OpscContext** out);
-int opsc_ctx_destroy(OpscContext* ctx);
+OPSC_API int opsc_ctx_create(int32_t device, int32_t max_windows, OpscContext** out);
+OPSC_API int opsc_ctx_destroy(OpscContext* ctx);
 
 /* win / out / place.mem_cap are HOST pointers. Copies in, runs the mode's
  * kernels on the context stream, copies out, synchronises. */
-int opsc_plan_windows_host(OpscContext* ctx, int32_t mode, const OpscDag* dag,
+OPSC_API int opsc_plan_windows_host(OpscContext* ctx, int32_t mode, const OpscDag* dag,
                            const OpscGrid* grid, const OpscModelSpec* model,
                            const OpscPlaceSpec* place, OpscWindows win,
                            OpscDecisions out);
 
 /* Number of kernels the last opsc_plan_windows_host call launched. */
-int opsc_ctx_last_launches(const OpscContext* ctx, int32_t* launches);
+OPSC_API int opsc_ctx_last_launches(const OpscContext* ctx, int32_t* launches);
 
 /* ---- measurement helper: FP64 add throughput microbenchmark ----
  * Runs `iters` dependent-chain DADD/DSETP pairs per thread on a full grid;
  * writes elapsed milliseconds and the executed FP64 op count. */
-int opsc_fp64_peak(int32_t iters, float* ms, double* fp64_ops, void* stream);
+OPSC_API int opsc_fp64_peak(int32_t iters, float* ms, double* fp64_ops, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,145 @@
+"""ctypes binding of libopscale_b200.so (the C ABI in include/opscale_b200.h).
+
+The planner search has no CPU implementation in this package: if the
+library is missing or no CUDA device is visible, every entry point raises
+DeviceUnavailable.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from . import abi, tables
+from .errors import DeviceUnavailable, SearchSpaceTooLarge
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libopscale_b200.so")
+
+# every symbol include/opscale_b200.h declares
+EXPORTS = (
+    "opsc_abi_version", "opsc_status_string", "opsc_device_count", "opsc_menu_build",
+    "opsc_stability_check", "opsc_compose_argmin", "opsc_fill_keys", "opsc_menu_fallback",
+    "opsc_decode_decisions", "opsc_model_grid", "opsc_materialize", "opsc_ctx_create",
+    "opsc_ctx_destroy", "opsc_plan_windows_host", "opsc_ctx_last_launches", "opsc_fp64_peak",
+)
+
+_lib = None
+_lock = threading.Lock()
+_tls = threading.local()
+
+
+def load():
+    """Load the library and declare signatures (no CUDA call is made)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise DeviceUnavailable(
+                f"{LIB_PATH} is not built; run `python -m paper_2511_02248_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        P, I = C.c_void_p, C.c_int32
+        W, D = abi.OpscWindows, abi.OpscDecisions
+        sig = {
+            "opsc_abi_version": ([], C.c_int),
+            "opsc_status_string": ([C.c_int], C.c_char_p),
+            "opsc_device_count": ([P], C.c_int),
+            "opsc_menu_build": ([P, P, W, P, P, P], C.c_int),
+            "opsc_stability_check": ([P, P, W, P, P], C.c_int),
+            "opsc_compose_argmin": ([P, P, W, P, I, I, P, P], C.c_int),
+            "opsc_fill_keys": ([P, I, P], C.c_int),
+            "opsc_menu_fallback": ([P, P, I, P, P, P], C.c_int),
+            "opsc_decode_decisions": ([P, P, I, P, P, P, P, P, P], C.c_int),
+            "opsc_model_grid": ([P, P, W, P, P, P, P], C.c_int),
+            "opsc_materialize": ([P, W, I, P, D, P], C.c_int),
+            "opsc_ctx_create": ([I, I, P], C.c_int),
+            "opsc_ctx_destroy": ([P], C.c_int),
+            "opsc_plan_windows_host": ([P, I, P, P, P, P, W, D], C.c_int),
+            "opsc_ctx_last_launches": ([P, P], C.c_int),
+            "opsc_fp64_peak": ([I, P, P, P], C.c_int),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes, f.restype = args, res
+        if L.opsc_abi_version() != abi.ABI_VERSION:
+            raise DeviceUnavailable("libopscale_b200.so ABI version mismatch; rebuild it")
+        _lib = L
+        return L
+
+
+def ref(x):
+    return C.cast(C.byref(x), C.c_void_p)
+
+
+def check(rc, what):
+    if rc == abi.OK:
+        return
+    msg = load().opsc_status_string(rc).decode()
+    if rc == abi.ERR_SPACE:
+        raise SearchSpaceTooLarge(f"{what}: {msg}")
+    if rc == abi.ERR_NODEVICE:
+        raise DeviceUnavailable(f"{what}: {msg}")
+    raise RuntimeError(f"{what}: {msg} (status {rc})")
+
+
+def device_count():
+    n = C.c_int(0)
+    load().opsc_device_count(C.cast(C.byref(n), C.c_void_p))
+    return n.value
+
+
+class Context:
+    """Owns an OpscContext (stream + device workspace) for host-buffer calls."""
+
+    def __init__(self, device=0, max_windows=0):
+        L = load()
+        if device_count() <= device:
+            raise DeviceUnavailable("no CUDA device visible: the planner search runs only on the GPU")
+        self._p = C.c_void_p()
+        check(L.opsc_ctx_create(device, max_windows, C.cast(C.byref(self._p), C.c_void_p)),
+              "opsc_ctx_create")
+
+    def close(self):
+        if self._p:
+            load().opsc_ctx_destroy(self._p)
+            self._p = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._p
+
+    def last_launches(self):
+        n = C.c_int32(0)
+        check(load().opsc_ctx_last_launches(self._p, C.cast(C.byref(n), C.c_void_p)), "launches")
+        return n.value
+
+    def plan_windows(self, mode, problem, windows, grid=None, model=None, place=None, out=None):
+        place = place or tables.pack_place()
+        out = out if out is not None else tables.DecisionArrays(windows.n, problem.n_ops)
+        g = grid if grid is not None else abi.OpscGrid()
+        m = model if model is not None else abi.OpscModelSpec()
+        rc = load().opsc_plan_windows_host(self._p, mode, ref(problem.table), ref(g), ref(m),
+                                           ref(place.spec), windows.struct(), out.struct())
+        check(rc, "opsc_plan_windows_host")
+        return out
+
+
+def context():
+    """Per-thread context: concurrent planner calls never share a stream."""
+    ctx = getattr(_tls, "ctx", None)
+    if ctx is None:
+        ctx = Context()
+        _tls.ctx = ctx
+    return ctx
+
+
+def plan_windows_host(mode, problem, windows, grid=None, model=None, place=None):
+    return context().plan_windows(mode, problem, windows, grid=grid, model=model, place=place)

@@ -1,0 +1,363 @@
+// capi.cu -- extern "C" entry points of libopscale_b200.so (include/opscale_b200.h).
+//
+// Device-pointer entry points only enqueue kernels on the caller's stream.
+// The host-buffer path owns a per-context stream and device workspace, so
+// concurrent callers (runner.sweep's threads, runner.py:237-240) each use
+// their own context and never share mutable state.
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "opsc_common.cuh"
+
+using namespace opsc;
+
+namespace {
+
+int from_cuda(cudaError_t e) { return e == cudaSuccess ? OPSC_OK : OPSC_ERR_CUDA; }
+
+__global__ void fp64_peak_kernel(int iters, double seed, double* sink) {
+  // 8 independent DADD chains per thread; DADD throughput bound
+  double a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3;
+  double a4 = a0 + 4, a5 = a0 + 5, a6 = a0 + 6, a7 = a0 + 7;
+  const double x = seed * 1e-300;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a0 = a0 + x; a1 = a1 + x; a2 = a2 + x; a3 = a3 + x;
+      a4 = a4 + x; a5 = a5 + x; a6 = a6 + x; a7 = a7 + x;
+    }
+  }
+  const double s = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+  if (s == 12345.678) sink[blockIdx.x] = s;
+}
+
+}  // namespace
+
+namespace opsc {
+cudaError_t launch_fp64_peak(int iters, double* sink, int* blocks, int* threads, cudaStream_t s) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  *blocks = sms * 8;
+  *threads = 256;
+  fp64_peak_kernel<<<*blocks, *threads, 0, s>>>(iters, 1.0, sink);
+  return cudaGetLastError();
+}
+}  // namespace opsc
+
+struct OpscContext {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int launches = 0;
+  size_t cap_w = 0, cap_e = 0, cap_n = 0, cap_dev = 0;
+  // windows
+  double *qps = nullptr, *slo = nullptr, *eps = nullptr;
+  int32_t* seq_len = nullptr;
+  uint8_t* phase = nullptr;
+  // workspace
+  double* menu = nullptr;
+  int32_t* fb = nullptr;
+  double* mem_cap = nullptr;
+  // decisions
+  unsigned long long* key = nullptr;
+  int16_t* cfg = nullptr;
+  uint8_t *feasible = nullptr, *stable = nullptr;
+  uint32_t* status = nullptr;
+  double *latency = nullptr, *pred = nullptr, *energy = nullptr, *memory = nullptr;
+  int32_t *objective = nullptr, *devices = nullptr;
+  int8_t* path = nullptr;
+};
+
+namespace {
+
+template <class T>
+cudaError_t regrow(T*& p, size_t n) {
+  if (p) cudaFree(p);
+  p = nullptr;
+  return cudaMalloc((void**)&p, n * sizeof(T) > 0 ? n * sizeof(T) : sizeof(T));
+}
+
+int ensure(OpscContext* c, size_t W, size_t E, size_t n, size_t ndev) {
+  cudaError_t e = cudaSuccess;
+  if (W > c->cap_w || n > c->cap_n) {
+    const size_t w2 = W > c->cap_w ? W : c->cap_w, n2 = n > c->cap_n ? n : c->cap_n;
+    if ((e = regrow(c->qps, w2)) || (e = regrow(c->slo, w2)) || (e = regrow(c->eps, w2)) ||
+        (e = regrow(c->seq_len, w2)) || (e = regrow(c->phase, w2)) || (e = regrow(c->key, w2)) ||
+        (e = regrow(c->feasible, w2)) || (e = regrow(c->status, w2)) || (e = regrow(c->latency, w2)) ||
+        (e = regrow(c->objective, w2)) || (e = regrow(c->energy, w2)) || (e = regrow(c->memory, w2)) ||
+        (e = regrow(c->devices, w2)) || (e = regrow(c->cfg, w2 * n2 * 3)) ||
+        (e = regrow(c->stable, w2 * n2)) || (e = regrow(c->path, w2 * n2)) ||
+        (e = regrow(c->pred, w2 * n2 * OPSC_PRED_FIELDS)) || (e = regrow(c->fb, w2 * n2)))
+      return from_cuda(e);
+    c->cap_w = w2;
+    c->cap_n = n2;
+    c->cap_e = 0;  // menu depends on W too
+  }
+  if (W * E > c->cap_e) {
+    if ((e = regrow(c->menu, W * E))) return from_cuda(e);
+    c->cap_e = W * E;
+  }
+  if (ndev > c->cap_dev) {
+    if ((e = regrow(c->mem_cap, ndev))) return from_cuda(e);
+    c->cap_dev = ndev;
+  }
+  return OPSC_OK;
+}
+
+OpscWindows dev_windows(const OpscContext* c, int n) {
+  OpscWindows w;
+  w.n = n;
+  w.qps = c->qps;
+  w.seq_len = c->seq_len;
+  w.phase = c->phase;
+  w.slo = c->slo;
+  w.eps = c->eps;
+  return w;
+}
+
+OpscDecisions dev_decisions(const OpscContext* c) {
+  OpscDecisions d;
+  d.key = (int64_t*)c->key;
+  d.cfg = c->cfg;
+  d.feasible = c->feasible;
+  d.status = c->status;
+  d.latency = c->latency;
+  d.objective = c->objective;
+  d.path = c->path;
+  d.pred = c->pred;
+  d.stable = c->stable;
+  d.energy = c->energy;
+  d.memory = c->memory;
+  d.devices = c->devices;
+  return d;
+}
+
+bool valid_dag(const OpscDag* d) { return d && d->n_ops >= 1 && d->n_ops <= OPSC_MAX_OPS; }
+
+}  // namespace
+
+extern "C" {
+
+int opsc_abi_version(void) { return OPSC_ABI_VERSION; }
+
+const char* opsc_status_string(int status) {
+  switch (status) {
+    case OPSC_OK: return "ok";
+    case OPSC_ERR_ARG: return "invalid argument or table limit exceeded";
+    case OPSC_ERR_CUDA: return "CUDA runtime error";
+    case OPSC_ERR_SPACE: return "candidate space exceeds the 2^40 lexicographic key field";
+    case OPSC_ERR_NODEVICE: return "no CUDA device";
+    default: return "unknown status";
+  }
+}
+
+int opsc_device_count(int* count) {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *count = 0;
+    return OPSC_ERR_NODEVICE;
+  }
+  *count = n;
+  return OPSC_OK;
+}
+
+int opsc_menu_build(const OpscDag* dag, const OpscGrid* grid, OpscWindows win, double* menu_w,
+                    uint32_t* status, void* stream) {
+  if (!valid_dag(dag) || !grid) return OPSC_ERR_ARG;
+  return from_cuda(launch_menu_build(*dag, *grid, win, menu_w, status, (cudaStream_t)stream));
+}
+
+int opsc_stability_check(const OpscDag* dag, const OpscGrid* grid, OpscWindows win, uint32_t* status,
+                         void* stream) {
+  if (!valid_dag(dag) || !grid) return OPSC_ERR_ARG;
+  return from_cuda(launch_stability(*dag, *grid, win, status, (cudaStream_t)stream));
+}
+
+int opsc_compose_argmin(const OpscDag* dag, const OpscGrid* grid, OpscWindows win, const double* menu_w,
+                        int32_t shard, int32_t n_shards, int64_t* key_out, void* stream) {
+  if (!valid_dag(dag) || !grid) return OPSC_ERR_ARG;
+  ComposeCfg c;
+  const int rc = compose_setup(*dag, *grid, win.n, shard, n_shards, &c);
+  if (rc != OPSC_OK) return rc;
+  return from_cuda(launch_compose(c, *grid, win.n, menu_w, win.slo, win.qps,
+                                  (unsigned long long*)key_out, (cudaStream_t)stream));
+}
+
+int opsc_fill_keys(int64_t* key, int32_t n, void* stream) {
+  return from_cuda(launch_fill_keys((unsigned long long*)key, n, (cudaStream_t)stream));
+}
+
+int opsc_menu_fallback(const OpscDag* dag, const OpscGrid* grid, int32_t n_windows, const double* menu_w,
+                       int32_t* fb_entry, void* stream) {
+  if (!valid_dag(dag) || !grid) return OPSC_ERR_ARG;
+  return from_cuda(launch_fallback(*dag, *grid, n_windows, menu_w, fb_entry, (cudaStream_t)stream));
+}
+
+int opsc_decode_decisions(const OpscDag* dag, const OpscGrid* grid, int32_t n_windows, const int64_t* key,
+                          const int32_t* fb_entry, int16_t* cfg, uint8_t* feasible, uint32_t* status,
+                          void* stream) {
+  if (!valid_dag(dag) || !grid) return OPSC_ERR_ARG;
+  return from_cuda(launch_decode(*dag, *grid, n_windows, (const unsigned long long*)key, fb_entry, cfg,
+                                 feasible, status, (cudaStream_t)stream));
+}
+
+int opsc_model_grid(const OpscDag* dag, const OpscModelSpec* spec, OpscWindows win, int16_t* cfg,
+                    uint8_t* feasible, uint32_t* status, void* stream) {
+  if (!valid_dag(dag) || !spec) return OPSC_ERR_ARG;
+  return from_cuda(launch_model_grid(*dag, *spec, win, cfg, feasible, status, (cudaStream_t)stream));
+}
+
+int opsc_materialize(const OpscDag* dag, OpscWindows win, int32_t config_order, const OpscPlaceSpec* place,
+                     OpscDecisions out, void* stream) {
+  if (!valid_dag(dag) || !place) return OPSC_ERR_ARG;
+  return from_cuda(launch_materialize(*dag, win, config_order, *place, out, (cudaStream_t)stream));
+}
+
+int opsc_ctx_create(int32_t device, int32_t max_windows, OpscContext** out) {
+  if (!out) return OPSC_ERR_ARG;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= device) {
+    cudaGetLastError();
+    return OPSC_ERR_NODEVICE;
+  }
+  OpscContext* c = new (std::nothrow) OpscContext();
+  if (!c) return OPSC_ERR_ARG;
+  c->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return OPSC_ERR_CUDA;
+  }
+  if (max_windows > 0) {
+    const int rc = ensure(c, (size_t)max_windows, 64, 8, 1);
+    if (rc) {
+      opsc_ctx_destroy(c);
+      return rc;
+    }
+  }
+  *out = c;
+  return OPSC_OK;
+}
+
+int opsc_ctx_destroy(OpscContext* c) {
+  if (!c) return OPSC_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  void* ptrs[] = {c->qps, c->slo, c->eps, c->seq_len, c->phase, c->menu, c->fb, c->mem_cap, c->key,
+                  c->cfg, c->feasible, c->stable, c->status, c->latency, c->pred, c->energy,
+                  c->memory, c->objective, c->devices, c->path};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return OPSC_OK;
+}
+
+int opsc_ctx_last_launches(const OpscContext* c, int32_t* launches) {
+  if (!c || !launches) return OPSC_ERR_ARG;
+  *launches = c->launches;
+  return OPSC_OK;
+}
+
+int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, const OpscGrid* grid,
+                           const OpscModelSpec* model, const OpscPlaceSpec* place, OpscWindows win,
+                           OpscDecisions out) {
+  if (!c || !valid_dag(dag) || !place || win.n < 0) return OPSC_ERR_ARG;
+  if (mode == OPSC_MODE_ORACLE && !grid) return OPSC_ERR_ARG;
+  if (mode == OPSC_MODE_MODEL && !model) return OPSC_ERR_ARG;
+  if (mode != OPSC_MODE_ORACLE && mode != OPSC_MODE_MODEL) return OPSC_ERR_ARG;
+  cudaSetDevice(c->device);
+  const int W = win.n, n = dag->n_ops;
+  if (W == 0) return OPSC_OK;
+  const size_t E = mode == OPSC_MODE_ORACLE ? (size_t)grid->menu_off[n] : 0;
+  const size_t ndev = place->uniform_cap ? 1 : (size_t)place->n_devices;
+  int rc = ensure(c, W, E, n, ndev);
+  if (rc) return rc;
+  cudaStream_t s = c->stream;
+  c->launches = 0;
+  cudaError_t e;
+#define CK(x)                   \
+  do {                          \
+    e = (x);                    \
+    if (e != cudaSuccess) {     \
+      cudaGetLastError();       \
+      return OPSC_ERR_CUDA;     \
+    }                           \
+  } while (0)
+  CK(cudaMemcpyAsync(c->qps, win.qps, W * sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->seq_len, win.seq_len, W * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->phase, win.phase, W * sizeof(uint8_t), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->slo, win.slo, W * sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->eps, win.eps, W * sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(c->mem_cap, place->mem_cap, ndev * sizeof(double), cudaMemcpyHostToDevice, s));
+  OpscPlaceSpec dplace = *place;
+  dplace.mem_cap = c->mem_cap;
+  const OpscWindows dw = dev_windows(c, W);
+  CK(launch_init(W, c->qps, c->status, c->key, c->feasible, s));
+  c->launches++;
+  if (mode == OPSC_MODE_ORACLE) {
+    ComposeCfg cc;
+    rc = compose_setup(*dag, *grid, W, 0, 1, &cc);
+    if (rc) return rc;
+    CK(launch_menu_build(*dag, *grid, dw, c->menu, c->status, s));
+    CK(launch_stability(*dag, *grid, dw, c->status, s));
+    CK(launch_compose(cc, *grid, W, c->menu, c->slo, c->qps, c->key, s));
+    CK(launch_fallback(*dag, *grid, W, c->menu, c->fb, s));
+    CK(launch_decode(*dag, *grid, W, c->key, c->fb, c->cfg, c->feasible, c->status, s));
+    c->launches += 5;
+    CK(launch_materialize(*dag, dw, 0, dplace, dev_decisions(c), s));
+  } else {
+    CK(launch_model_grid(*dag, *model, dw, c->cfg, c->feasible, c->status, s));
+    c->launches += 1;
+    CK(launch_materialize(*dag, dw, 1, dplace, dev_decisions(c), s));
+  }
+  c->launches++;
+  const size_t wn = (size_t)W * n;
+  if (out.key) CK(cudaMemcpyAsync(out.key, c->key, W * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  if (out.cfg) CK(cudaMemcpyAsync(out.cfg, c->cfg, wn * 3 * sizeof(int16_t), cudaMemcpyDeviceToHost, s));
+  if (out.feasible) CK(cudaMemcpyAsync(out.feasible, c->feasible, W, cudaMemcpyDeviceToHost, s));
+  if (out.status) CK(cudaMemcpyAsync(out.status, c->status, W * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  if (out.latency) CK(cudaMemcpyAsync(out.latency, c->latency, W * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (out.objective) CK(cudaMemcpyAsync(out.objective, c->objective, W * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  if (out.path) CK(cudaMemcpyAsync(out.path, c->path, wn, cudaMemcpyDeviceToHost, s));
+  if (out.pred) CK(cudaMemcpyAsync(out.pred, c->pred, wn * OPSC_PRED_FIELDS * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (out.stable) CK(cudaMemcpyAsync(out.stable, c->stable, wn, cudaMemcpyDeviceToHost, s));
+  if (out.energy) CK(cudaMemcpyAsync(out.energy, c->energy, W * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (out.memory) CK(cudaMemcpyAsync(out.memory, c->memory, W * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (out.devices) CK(cudaMemcpyAsync(out.devices, c->devices, W * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+#undef CK
+  return OPSC_OK;
+}
+
+int opsc_fp64_peak(int32_t iters, float* ms, double* fp64_ops, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  double* sink = nullptr;
+  if (cudaMalloc(&sink, 4096 * sizeof(double)) != cudaSuccess) return OPSC_ERR_CUDA;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  int blocks = 0, threads = 0;
+  launch_fp64_peak(iters / 10 + 1, sink, &blocks, &threads, s);  // warm-up
+  cudaEventRecord(a, s);
+  cudaError_t e = launch_fp64_peak(iters, sink, &blocks, &threads, s);
+  cudaEventRecord(b, s);
+  cudaEventSynchronize(b);
+  float t = 0.0f;
+  cudaEventElapsedTime(&t, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  if (e != cudaSuccess) return OPSC_ERR_CUDA;
+  *ms = t;
+  *fp64_ops = (double)blocks * threads * (double)iters * 32.0;
+  return OPSC_OK;
+}
+
+}  // extern "C"

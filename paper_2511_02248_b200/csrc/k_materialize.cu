@@ -1,0 +1,226 @@
+// k_materialize.cu -- K4: decided configs -> ScalingPlan fields + metrics.
+//
+// Per window (one thread each; this is per-decision work, not per-candidate):
+//   * _Evaluator.evaluate of the decided configs (autoscaler.py:196-206):
+//     PredictedSojourn per op and the critical path with the reference's
+//     lexicographic path tie-break (opgraph.py:199-244); objective = sum P*R;
+//   * default_stream_place (placement.py:358-396, 465-491): devices_used and
+//     provisioned memory (metrics.py:130-132, CPython-3.12 float sum order);
+//   * request_energy (metrics.py:84-102) with every interference factor equal
+//     to 1 (single-group devices under default-stream placement), i.e.
+//     t_eff = (T * R) / R as _adjusted_ops computes it (placement.py:257).
+#include "opsc_common.cuh"
+
+namespace opsc {
+
+__device__ __forceinline__ bool path_less(const int8_t* a, int la, const int8_t* b, int lb) {
+  const int n = la < lb ? la : lb;
+  for (int i = 0; i < n; ++i)
+    if (a[i] != b[i]) return a[i] < b[i];
+  return la < lb;
+}
+
+__device__ double critical_path(const OpscDag& d, const double* wt, int8_t* path_out) {
+  const int n = d.n_ops;
+  double val[OPSC_MAX_OPS];
+  int8_t pth[OPSC_MAX_OPS][OPSC_MAX_OPS];
+  int plen[OPSC_MAX_OPS];
+  for (int i = 0; i < n; ++i) {
+    const int v = d.topo[i];
+    const uint32_t pm = d.pred_mask[v];
+    if (!pm) {
+      val[v] = wt[v];
+      pth[v][0] = (int8_t)v;
+      plen[v] = 1;
+      continue;
+    }
+    int cand = -1;
+    double cv = 0.0;
+    for (int p = 0; p < n; ++p) {
+      if (!(pm >> p & 1u)) continue;
+      const double ev = val[p] + wt[v];
+      // candidate path = pth[p] + (v,); compare against pth[cand] + (v,)
+      bool take = cand < 0 || ev > cv;
+      if (!take && ev == cv) {
+        // (pp + (v,)) < (cp + (v,)) lexicographically
+        const int la = plen[p], lb = plen[cand];
+        const int mn = la < lb ? la : lb;
+        int i2 = 0;
+        while (i2 < mn && pth[p][i2] == pth[cand][i2]) ++i2;
+        if (i2 < mn) take = pth[p][i2] < pth[cand][i2];
+        else if (la < lb) take = (int8_t)v < pth[cand][la];
+        else if (lb < la) take = pth[p][lb] < (int8_t)v;
+      }
+      if (take) {
+        cand = p;
+        cv = ev;
+      }
+    }
+    val[v] = cv;
+    for (int k = 0; k < plen[cand]; ++k) pth[v][k] = pth[cand][k];
+    pth[v][plen[cand]] = (int8_t)v;
+    plen[v] = plen[cand] + 1;
+  }
+  int tv = -1;
+  double top = 0.0;
+  for (int s = 0; s < n; ++s) {
+    if (!(d.sink_mask >> s & 1u)) continue;
+    if (tv < 0 || val[s] > top || (val[s] == top && path_less(pth[s], plen[s], pth[tv], plen[tv]))) {
+      tv = s;
+      top = val[s];
+    }
+  }
+  for (int i = 0; i < n; ++i) path_out[i] = i < plen[tv] ? pth[tv][i] : (int8_t)-1;
+  return top;
+}
+
+__device__ __forceinline__ double op_memory(const OpscDag& d, int v, int p, int b, int L) {
+  return (d.weight_mem[v] / (double)p + d.m0[v]) + (d.m1[v] * (double)b) * (double)L;
+}
+
+// default_stream_place; returns 0 or an error bit
+__device__ uint32_t place_default_stream(const OpscDag& d, const OpscPlaceSpec& pl, const int16_t* c,
+                                         const double* T, int L, int* devices, double* memory) {
+  const int n = d.n_ops;
+  int k_base = 1 << 30;
+  double mem[OPSC_MAX_OPS], ratio[OPSC_MAX_OPS];
+  int order[OPSC_MAX_OPS], xord[OPSC_MAX_OPS];
+  for (int v = 0; v < n; ++v) {
+    k_base = min(k_base, (int)c[v * 3 + 1]);
+    mem[v] = op_memory(d, v, c[v * 3], c[v * 3 + 2], L);
+    ratio[v] = -(d.weight_mem[v] / (double)c[v * 3]);
+    order[v] = v;
+    xord[v] = v;
+  }
+  // sort keys (-(weight_mem/P), id) and (-op_latency, id); insertion sort is stable
+  for (int i = 1; i < n; ++i) {
+    const int x = order[i];
+    int j = i - 1;
+    while (j >= 0 && ratio[order[j]] > ratio[x]) { order[j + 1] = order[j]; --j; }
+    order[j + 1] = x;
+    const int y = xord[i];
+    j = i - 1;
+    while (j >= 0 && -T[xord[j]] > -T[y]) { xord[j + 1] = xord[j]; --j; }
+    xord[j + 1] = y;
+  }
+  PySum total;
+  total.reset();
+  int used = 0;
+  auto cap_of = [&](int dev) { return pl.uniform_cap ? pl.mem_cap[0] : pl.mem_cap[dev]; };
+  // base instances (placement.py:358-385)
+  int inst_dev[OPSC_MAX_OPS];
+  PySum dev_sum[OPSC_MAX_OPS];
+  const int full_sim = pl.uniform_cap ? 1 : k_base;  // uniform caps: every instance packs alike
+  int per_inst = 0;
+  for (int inst = 1; inst <= full_sim; ++inst) {
+    int nd = 0;
+    for (int i = 0; i < n; ++i) {
+      const int v = order[i];
+      int t = -1;
+      for (int j = 0; j < nd; ++j)
+        if (dev_sum[j].value() + mem[v] <= cap_of(inst_dev[j])) { t = j; break; }
+      if (t < 0) {
+        if (used >= pl.n_devices) return OPSC_W_FLEET_EXHAUSTED;
+        const int dev = used++;
+        if (mem[v] > cap_of(dev)) return OPSC_W_INFEASIBLE_PLACEMENT;
+        inst_dev[nd] = dev;
+        dev_sum[nd].reset();
+        t = nd++;
+      }
+      dev_sum[t].add(mem[v]);
+      total.add(mem[v]);
+    }
+    per_inst = nd;
+  }
+  if (pl.uniform_cap && k_base > 1) {
+    if ((long long)used + (long long)(k_base - 1) * per_inst > (long long)pl.n_devices)
+      return OPSC_W_FLEET_EXHAUSTED;
+    used += (k_base - 1) * per_inst;
+    for (int inst = 2; inst <= k_base; ++inst)
+      for (int i = 0; i < n; ++i) total.add(mem[order[i]]);
+  }
+  // extra replicas on dedicated devices, heaviest op_latency first (placement.py:388-396, 482-490)
+  for (int i = 0; i < n; ++i) {
+    const int v = xord[i];
+    for (int k = k_base + 1; k <= c[v * 3 + 1]; ++k) {
+      if (used >= pl.n_devices) return OPSC_W_FLEET_EXHAUSTED;
+      const int dev = used++;
+      if (mem[v] > cap_of(dev)) return OPSC_W_INFEASIBLE_PLACEMENT;
+      total.add(mem[v]);
+    }
+  }
+  *devices = used;
+  *memory = total.value();
+  return 0;
+}
+
+__global__ void __launch_bounds__(64) materialize_kernel(const __grid_constant__ OpscDag d,
+                                                         const __grid_constant__ OpscWindows win,
+                                                         int config_order,
+                                                         const __grid_constant__ OpscPlaceSpec pl,
+                                                         const __grid_constant__ OpscDecisions out) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= win.n) return;
+  const int n = d.n_ops;
+  uint32_t st = out.status[w];
+  out.latency[w] = OPSC_INF;
+  out.objective[w] = 0;
+  out.energy[w] = 0.0;
+  out.memory[w] = 0.0;
+  out.devices[w] = 0;
+  for (int v = 0; v < n; ++v) out.path[(size_t)w * n + v] = -1;
+  if (st & (OPSC_W_IDLE | OPSC_W_NO_STABLE_BOUNDS | OPSC_W_NO_STABLE_PARAMS | OPSC_W_NO_STABLE_MODEL))
+    return;
+  const int16_t* c = out.cfg + (size_t)w * n * 3;
+  const double qps = win.qps[w];
+  const int L = win.seq_len[w], ph = win.phase[w];
+  double wt[OPSC_MAX_OPS], T[OPSC_MAX_OPS];
+  bool all = true;
+  int obj = 0;
+  for (int v = 0; v < n; ++v) {
+    const Pred o = predict(d, qps, L, ph, v, c[v * 3], c[v * 3 + 1], c[v * 3 + 2], &st);
+    double* pf = out.pred + ((size_t)w * n + v) * OPSC_PRED_FIELDS;
+    pf[0] = o.t; pf[1] = o.lam; pf[2] = o.mu; pf[3] = o.util;
+    pf[4] = o.wait; pf[5] = o.service; pf[6] = o.comm;
+    out.stable[(size_t)w * n + v] = o.stable;
+    all &= o.stable;
+    wt[v] = weight(o, d.layer_count[v]);
+    T[v] = o.t;
+    obj += (int)c[v * 3] * (int)c[v * 3 + 1];
+  }
+  out.objective[w] = obj;
+  if (all) out.latency[w] = critical_path(d, wt, out.path + (size_t)w * n);
+  if (out.feasible[w]) {
+    int dev = 0;
+    double mem = 0.0;
+    const uint32_t e = place_default_stream(d, pl, c, T, L, &dev, &mem);
+    st |= e;
+    if (!e) {
+      out.devices[w] = dev;
+      out.memory[w] = mem;
+      double total = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const int v = config_order == 0 ? i : d.node_order[i];
+        const int p = c[v * 3], r = c[v * 3 + 1], b = c[v * 3 + 2];
+        const double layers = (double)d.layer_count[v];
+        const double t_eff = (T[v] * (double)r) / (double)r;
+        const double mu = 1.0 / (t_eff * layers), lam = qps / (double)b;
+        const double wait = lam < (double)r * mu ? expected_wait(lam, mu, r) : OPSC_INF;
+        const double wl = wait * layers, sl = t_eff * layers;
+        total = total + ((pl.alpha * (double)p) * (double)r) * (wl + sl);
+        total = total + pl.beta * sl;
+      }
+      out.energy[w] = total;
+    }
+  }
+  out.status[w] = st;
+}
+
+cudaError_t launch_materialize(const OpscDag& d, OpscWindows w, int config_order, const OpscPlaceSpec& p,
+                               OpscDecisions out, cudaStream_t s) {
+  if (w.n <= 0) return cudaSuccess;
+  materialize_kernel<<<(w.n + 63) / 64, 64, 0, s>>>(d, w, config_order, p, out);
+  return cudaGetLastError();
+}
+
+}  // namespace opsc

@@ -1,0 +1,206 @@
+// k_model.cu -- K3 model_grid: model_level_autoscale on the device.
+//
+// Mirrors autoscaler.py:596-681 exactly, including its search sequence:
+// for every batch size B the replica floor is the max strict-stability floor
+// over operators (:643-656), then the smallest R meeting slo - eps (else slo)
+// is found with the reference's exponential probe + bisection (:620-639), so
+// the evaluated (B, R) points -- and hence the bits of every latency -- are
+// the reference's. Argmin of R * sum(P_base) with strict `<` (smallest B
+// wins), fallback = min latency at r_cap (first B wins).
+//
+// One CTA per window, one warp per batch size, one lane per operator: a
+// candidate evaluation runs all operators' Erlang-B recurrences in parallel
+// lanes and the critical-path DP on lane 0.
+#include "opsc_common.cuh"
+
+namespace opsc {
+
+struct ModelArgs {
+  OpscDag d;
+  OpscModelSpec m;
+};
+
+// evaluate(uniform(b, r)) latency (autoscaler.py:196-206, opgraph.py:199-244)
+__device__ double eval_uniform(const OpscDag& d, const OpscModelSpec& m, double qps, int L, int ph,
+                               int b, int r, double* wsh, uint32_t* st) {
+  const int lane = threadIdx.x & 31;
+  const int n = d.n_ops;
+  bool stable = true;
+  if (lane < n) {
+    const Pred o = predict(d, qps, L, ph, lane, m.p_base[lane], r, b, st);
+    stable = o.stable;
+    wsh[lane] = weight(o, d.layer_count[lane]);
+  }
+  const bool all = __all_sync(0xffffffffu, stable);
+  __syncwarp();
+  double lat = OPSC_INF;
+  if (lane == 0 && all) {
+    double val[OPSC_MAX_OPS];
+    for (int i = 0; i < n; ++i) {
+      const int v = d.topo[i];
+      double in = 0.0;
+      uint32_t pm = d.pred_mask[v];
+      while (pm) {
+        const int p = __ffs(pm) - 1;
+        pm &= pm - 1;
+        in = fmax(in, val[p]);
+      }
+      val[v] = in + wsh[v];
+    }
+    lat = 0.0;
+    for (int v = 0; v < n; ++v)
+      if (d.sink_mask >> v & 1u) lat = fmax(lat, val[v]);
+  }
+  __syncwarp();
+  return __shfl_sync(0xffffffffu, lat, 0);
+}
+
+// autoscaler.py:620-639
+__device__ int smallest_r(const OpscDag& d, const OpscModelSpec& m, double qps, int L, int ph, int b,
+                          int r_floor, double bound, double* wsh, uint32_t* st, double* lat_out) {
+  const double lo_lat = eval_uniform(d, m, qps, L, ph, b, r_floor, wsh, st);
+  if (lo_lat <= bound) {
+    *lat_out = lo_lat;
+    return r_floor;
+  }
+  int hi = r_floor;
+  double hi_lat = lo_lat;
+  while (hi_lat > bound && hi < m.r_cap) {
+    hi = min(hi * 2, m.r_cap);
+    hi_lat = eval_uniform(d, m, qps, L, ph, b, hi, wsh, st);
+  }
+  if (hi_lat > bound) {
+    *lat_out = hi_lat;
+    return -1;
+  }
+  int lo = r_floor;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) / 2;
+    const double ml = eval_uniform(d, m, qps, L, ph, b, mid, wsh, st);
+    if (ml <= bound) {
+      hi = mid;
+      hi_lat = ml;
+    } else {
+      lo = mid;
+    }
+  }
+  *lat_out = hi_lat;
+  return hi;
+}
+
+__global__ void __launch_bounds__(1024) model_grid_kernel(const __grid_constant__ ModelArgs a,
+                                                          const __grid_constant__ OpscWindows win,
+                                                          int16_t* __restrict__ cfg,
+                                                          uint8_t* __restrict__ feasible,
+                                                          uint32_t* __restrict__ status) {
+  const OpscDag& d = a.d;
+  const OpscModelSpec& m = a.m;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nwarps = blockDim.x >> 5;
+  double* wsh_all = reinterpret_cast<double*>(smem_raw);       // [nwarps][32]
+  double* res_lat = wsh_all + nwarps * 32;                      // [b_cap]
+  int32_t* res_r = reinterpret_cast<int32_t*>(res_lat + m.b_cap);  // [b_cap]; -2 skip, -1 fallback
+  __shared__ uint32_t st_sh;
+
+  const int w = blockIdx.x;
+  const double qps = win.qps[w];
+  if (!(qps > 0.0)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) st_sh = 0;
+  __syncthreads();
+  const int L = win.seq_len[w], ph = win.phase[w];
+  const double slo = win.slo[w], target = win.slo[w] - win.eps[w];
+  double* wsh = wsh_all + warp * 32;
+  uint32_t st = 0;
+
+  for (int b = warp + 1; b <= m.b_cap; b += nwarps) {
+    int rm = 1;
+    bool bad = false;
+    if (lane < d.n_ops) {
+      const double tl = op_latency(d, ph, lane, b, L, m.p_base[lane]) * (double)d.layer_count[lane];
+      if (tl == 0.0) st |= OPSC_W_ZERO_DIVISION;
+      rm = strict_min_replicas(qps / (double)b, 1.0 / tl, m.r_cap);
+      bad = rm < 0;
+    }
+    const bool unstable = __any_sync(0xffffffffu, bad);
+    const int r_floor = max(1, __reduce_max_sync(0xffffffffu, bad ? 1 : rm));
+    if (unstable) {
+      if (lane == 0) res_r[b - 1] = -2;
+      continue;
+    }
+    double lat;
+    int r = smallest_r(d, m, qps, L, ph, b, r_floor, target, wsh, &st, &lat);
+    if (r < 0) r = smallest_r(d, m, qps, L, ph, b, r_floor, slo, wsh, &st, &lat);
+    if (lane == 0) {
+      res_r[b - 1] = r;
+      res_lat[b - 1] = lat;
+    }
+  }
+  if (st) atomicOr(&st_sh, st);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int p_sum = 0;
+    for (int v = 0; v < d.n_ops; ++v) p_sum += m.p_base[v];
+    int best_b = -1, best_r = 0, best_obj = 0, fb_b = -1;
+    double fb_lat = 0.0;
+    for (int b = 1; b <= m.b_cap; ++b) {
+      const int r = res_r[b - 1];
+      if (r == -2) continue;
+      if (r == -1) {
+        if (fb_b < 0 || res_lat[b - 1] < fb_lat) {
+          fb_b = b;
+          fb_lat = res_lat[b - 1];
+        }
+        continue;
+      }
+      const int obj = r * p_sum;
+      if (best_b < 0 || obj < best_obj) {
+        best_b = b;
+        best_r = r;
+        best_obj = obj;
+      }
+    }
+    uint32_t s = st_sh;
+    int bb = -1, rr = 0;
+    feasible[w] = 0;
+    if (best_b >= 0) {
+      bb = best_b;
+      rr = best_r;
+      feasible[w] = 1;
+    } else if (fb_b >= 0) {
+      bb = fb_b;
+      rr = m.r_cap;
+    } else {
+      s |= OPSC_W_NO_STABLE_MODEL;
+    }
+    if (bb > 0) {
+      for (int v = 0; v < d.n_ops; ++v) {
+        int16_t* c = cfg + ((size_t)w * d.n_ops + v) * 3;
+        c[0] = (int16_t)m.p_base[v];
+        c[1] = (int16_t)rr;
+        c[2] = (int16_t)bb;
+      }
+    }
+    status[w] |= s;
+  }
+}
+
+cudaError_t launch_model_grid(const OpscDag& d, const OpscModelSpec& m, OpscWindows w, int16_t* cfg,
+                              uint8_t* feasible, uint32_t* status, cudaStream_t s) {
+  if (w.n <= 0) return cudaSuccess;
+  if (m.b_cap < 1 || m.r_cap < 1) return cudaErrorInvalidValue;
+  ModelArgs a;
+  a.d = d;
+  a.m = m;
+  const int nwarps = m.b_cap < 32 ? m.b_cap : 32;
+  const size_t smem = (size_t)nwarps * 32 * sizeof(double) + (size_t)m.b_cap * (sizeof(double) + sizeof(int32_t));
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(model_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  model_grid_kernel<<<w.n, nwarps * 32, smem, s>>>(a, w, cfg, feasible, status);
+  return cudaGetLastError();
+}
+
+}  // namespace opsc

@@ -1,0 +1,185 @@
+// opsc_common.cuh -- shared device arithmetic for the sm_100a planner kernels.
+//
+// Bit-exactness contract: every expression below keeps
+// the reference's Python association order, the whole library is compiled
+// with --fmad=false (no DFMA contraction), and double division is CUDA's
+// IEEE round-to-nearest `/`. Integers convert to double exactly.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "../../include/opscale_b200.h"
+
+#define OPSC_INF CUDART_INF
+#define OPSC_LEXMASK ((1ull << OPSC_KEY_LEX_BITS) - 1ull)
+
+namespace opsc {
+
+// perfmodel.py:62-64 and :133-157. At the planners' sm_share = 1.0 the
+// SM-share factor is exactly 1: demand = min(1, s0+s1*B*L) <= 1 gives
+// 1/demand >= 1, so effective = min(1, 1/demand) = 1.0 and base/1.0 = base.
+// (The CPU oracle evaluates the factor literally; the golden tests pin both.)
+__device__ __forceinline__ double op_latency(const OpscDag& d, int ph, int v, long long b,
+                                             long long l, long long p) {
+  const long long bl = b * l;
+  const double base = (d.c0[ph][v] + d.c1[ph][v] * (double)bl) + (d.c2[ph][v] * (double)bl) * (double)l;
+  return base / (d.eta[v] * (double)p);
+}
+
+// queueing.py:54-75: Erlang-B recurrence recomputed with a = R*rho.
+__device__ __forceinline__ double erlang_c(int r, double rho) {
+  const double a = (double)r * rho;
+  double b = 1.0;
+  for (int k = 1; k <= r; ++k) {
+    const double ab = a * b;
+    b = ab / ((double)k + ab);
+  }
+  return ((double)r * b) / ((double)r - a * (1.0 - b));
+}
+
+// queueing.py:78-87
+__device__ __forceinline__ double expected_wait(double lam, double mu, int r) {
+  const double rho = lam / ((double)r * mu);
+  return erlang_c(r, rho) / ((double)r * mu - lam);
+}
+
+// autoscaler.py:224-228; -1 == None
+__device__ __forceinline__ int strict_min_replicas(double lam, double mu, int r_cap) {
+  const double q = ceil(lam / mu);
+  if (!(q <= (double)r_cap)) return -1;
+  int r = q < 1.0 ? 1 : (int)q;
+  while (lam >= (double)r * mu) {
+    if (++r > r_cap) return -1;
+  }
+  return r;
+}
+
+// perfmodel.py:167-171 via autoscaler.py:163-172 (max over out edges, strict >)
+__device__ __forceinline__ double comm_time(const OpscDag& d, int v, long long b, long long l) {
+  double best = 0.0;
+  for (int e = d.out_ptr[v]; e < d.out_ptr[v + 1]; ++e) {
+    const double t = (d.out_v0[e] + (d.out_v1[e] * (double)b) * (double)l) / d.link_bw;
+    if (t > best) best = t;
+  }
+  return best;
+}
+
+struct Pred {
+  double t, lam, mu, util, wait, service, comm;
+  bool stable;
+};
+
+// autoscaler.py:174-194 predict_op; status bits flag the reference's
+// ZeroDivisionError / Unstable raises.
+__device__ __forceinline__ Pred predict(const OpscDag& d, double qps, int L, int ph, int v, int p,
+                                        int r, int b, uint32_t* st) {
+  Pred o;
+  o.t = op_latency(d, ph, v, b, L, p);
+  const double tl = o.t * (double)d.layer_count[v];
+  if (tl == 0.0) *st |= OPSC_W_ZERO_DIVISION;
+  o.mu = 1.0 / tl;
+  o.lam = qps / (double)b;
+  o.stable = o.lam < (double)r * o.mu;
+  o.util = o.lam / ((double)r * o.mu);
+  o.wait = OPSC_INF;
+  if (o.stable) {
+    if (o.util >= 1.0 || o.util <= 0.0) *st |= OPSC_W_UNSTABLE_ROUNDING;
+    o.wait = erlang_c(r, o.util) / ((double)r * o.mu - o.lam);
+  }
+  o.service = o.t / (double)b;
+  o.comm = comm_time(d, v, b, L);
+  return o;
+}
+
+// ((W + T/B) + C) * layers (autoscaler.py:751-755, opgraph.py:218)
+__device__ __forceinline__ double weight(const Pred& o, int layers) {
+  return ((o.wait + o.service) + o.comm) * (double)layers;
+}
+
+// menu entry -> (P, R, B), lexicographic (P, R, B) order (autoscaler.py:747-749)
+__device__ __forceinline__ void entry_prb(const OpscGrid& g, int v, int e, int& p, int& r, int& b) {
+  const int bm = g.b_max[v];
+  b = e % bm + 1;
+  r = (e / bm) % g.r_max + 1;
+  p = g.p_vals[v][e / (bm * g.r_max)];
+}
+
+// CPython 3.12 builtin sum() over floats (Neumaier), used by placement memory
+// bookkeeping and provisioned_memory (placement.py:171-172, metrics.py:130-132).
+struct PySum {
+  double f, c;
+  bool started;
+  __device__ void reset() { f = 0.0; c = 0.0; started = false; }
+  __device__ void add(double x) {
+    if (!started) { f = 0.0 + x; c = 0.0; started = true; return; }
+    const double t = f + x;
+    if (fabs(f) >= fabs(x)) c += (f - t) + x;
+    else c += (x - t) + f;
+    f = t;
+  }
+  __device__ double value() const {
+    if (!started) return 0.0;
+    return (c != 0.0 && isfinite(c)) ? f + c : f;
+  }
+};
+
+// warp / block minimum of a u64 key
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, v, o);
+    v = x < v ? x : v;
+  }
+  return v;
+}
+
+}  // namespace opsc
+
+// ---------------------------------------------------------------- compose cfg
+#define OPSC_CMAX (OPSC_MAX_OPS + 2)
+
+// Host-computed view of one compose launch (topological positions).
+struct ComposeCfg {
+  int32_t n;            // positions (>= 2, virtual positions prepended when needed)
+  int32_t il;           // inner levels held by one thread (>= 2)
+  int32_t E;            // menu entries per window (window stride of menu_w)
+  int32_t n_real_ops;
+  int32_t m[OPSC_CMAX];        // menu size per position
+  int32_t off[OPSC_CMAX];      // menu offset per position (virtual -> E)
+  unsigned long long stride[OPSC_CMAX];  // lexicographic stride per position (0 virtual)
+  uint32_t pmask[OPSC_CMAX];   // predecessor positions
+  uint32_t sinkmask;           // sink positions
+  uint32_t m_out;              // outer index space per window
+  uint32_t lo, hi;             // this shard's outer index range
+  uint32_t mid_count;          // product of middle-level menu sizes
+  int32_t blocks_per_window;
+  int32_t nj;                  // register tile of the innermost menu
+};
+
+namespace opsc {
+// launchers (defined in the k_*.cu files), all asynchronous on `s`
+cudaError_t launch_init(int n_windows, const double* qps, uint32_t* status, unsigned long long* key,
+                        uint8_t* feasible, cudaStream_t s);
+cudaError_t launch_menu_build(const OpscDag& d, const OpscGrid& g, OpscWindows w, double* menu_w,
+                              uint32_t* status, cudaStream_t s);
+cudaError_t launch_stability(const OpscDag& d, const OpscGrid& g, OpscWindows w, uint32_t* status,
+                             cudaStream_t s);
+cudaError_t launch_fallback(const OpscDag& d, const OpscGrid& g, int n_windows, const double* menu_w,
+                            int32_t* fb, cudaStream_t s);
+cudaError_t launch_decode(const OpscDag& d, const OpscGrid& g, int n_windows,
+                          const unsigned long long* key, const int32_t* fb, int16_t* cfg,
+                          uint8_t* feasible, uint32_t* status, cudaStream_t s);
+cudaError_t launch_fill_keys(unsigned long long* key, int n, cudaStream_t s);
+int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard, int n_shards,
+                  ComposeCfg* cfg);
+cudaError_t launch_compose(const ComposeCfg& c, const OpscGrid& g, int n_windows,
+                           const double* menu_w, const double* slo, const double* qps,
+                           unsigned long long* key, cudaStream_t s);
+cudaError_t launch_model_grid(const OpscDag& d, const OpscModelSpec& m, OpscWindows w, int16_t* cfg,
+                              uint8_t* feasible, uint32_t* status, cudaStream_t s);
+cudaError_t launch_materialize(const OpscDag& d, OpscWindows w, int config_order,
+                               const OpscPlaceSpec& p, OpscDecisions out, cudaStream_t s);
+cudaError_t launch_fp64_peak(int iters, double* sink, int* blocks, int* threads, cudaStream_t s);
+}  // namespace opsc

@@ -1,0 +1,132 @@
+"""Drop-in planners: the reference's planner signatures, searched on the GPU.
+
+  brute_force_autoscale(dag, profiles, point, params, bounds=None)
+      autoscaler.py:706-847 -- exhaustive (P,R,B)^n argmin, on device
+  model_level_autoscale(dag, profiles, point, params)
+      autoscaler.py:596-681 -- uniform (B,R) probe/bisect, on device
+  plan_windows(dag, profiles, points, params, mode, bounds=None)
+      batched form of the above over many WorkloadPoints (new; equals mapping
+      the per-point call over `points`, minus the per-point launch cost)
+
+Argument checks and exceptions follow the reference in its order:
+ValueError for qps <= 0 and UnknownProfile (_Evaluator, :148-150), the >6-op
+and MAX_ENUMERATION guards (:725-738; MAX_ENUMERATION is read at call time,
+so patching it works as in the reference), UnknownPhase (first predict_op),
+then the device-reported NoStableConfig cases (:289, :835, :678).
+
+The batched entry lifts the 6-op / MAX_ENUMERATION guards by default (it is
+the path for the 10-op 70B DAG and ~1e8-candidate windows); the per-point
+planners keep them unless called with guards=False.
+"""
+
+from __future__ import annotations
+
+import math
+
+from . import _native, abi, errors, model, tables
+from .plans import WindowDecisions
+
+MAX_ENUMERATION = 10_000_000
+MAX_BRUTE_FORCE_OPS = 6
+
+
+def _guard(problem, params, bounds, max_enumeration, err):
+    ops = problem.ids
+    if len(ops) > MAX_BRUTE_FORCE_OPS:
+        raise err.SearchSpaceTooLarge(f"{len(ops)} operators > {MAX_BRUTE_FORCE_OPS}")
+    projected = 1
+    for op in ops:
+        projected *= (len(bounds.parallelism_for(params, op)) * bounds.b_max_for(params, op)
+                      * bounds.r_max)
+    if projected > max_enumeration:
+        raise err.SearchSpaceTooLarge(
+            f"projected enumeration {projected} exceeds {max_enumeration}")
+
+
+def _points_ok(points):
+    for p in points:
+        if not p.qps > 0:
+            raise ValueError("workload point must have qps > 0")
+
+
+def brute_force_autoscale(dag, profiles, point, params, bounds=None, *, guards=True,
+                          fleet=None, energy=None, types=model, err=errors,
+                          max_enumeration=None):
+    """Exact minimum-objective plan over the bounded configuration space
+    (ties: lexicographically smallest config vector in node-id order)."""
+    bounds = bounds if bounds is not None else types.BruteForceBounds()
+    _points_ok([point])
+    problem = tables.pack_problem(dag, profiles)
+    if guards:
+        _guard(problem, params, bounds,
+               MAX_ENUMERATION if max_enumeration is None else max_enumeration, err)
+    return _run(abi.MODE_ORACLE, problem, [point], params, bounds, fleet, energy, types, err).plan(0)
+
+
+def model_level_autoscale(dag, profiles, point, params, *, fleet=None, energy=None,
+                          types=model, err=errors):
+    """Monolithic baseline: one (B, R) shared by every operator."""
+    _points_ok([point])
+    problem = tables.pack_problem(dag, profiles)
+    return _run(abi.MODE_MODEL, problem, [point], params, None, fleet, energy, types, err).plan(0)
+
+
+def _run(mode, problem, points, params, bounds, fleet, energy, types, err):
+    phases = {p.phase for p in points}
+    for ph in sorted(phases):
+        problem.require_phase(ph)
+    win = tables.pack_windows(points, params.slo, params.epsilon)
+    grid = tables.pack_grid(problem, params, bounds) if mode == abi.MODE_ORACLE else None
+    spec = tables.pack_model(problem, params) if mode == abi.MODE_MODEL else None
+    place = tables.pack_place(fleet, energy)
+    arrays = _native.plan_windows_host(mode, problem, win, grid=grid, model=spec, place=place)
+    return WindowDecisions(problem, points, arrays, mode, types, err)
+
+
+_MODES = {"oracle": abi.MODE_ORACLE, "model": abi.MODE_MODEL}
+
+
+def decide_windows(dag, profiles, points, params, mode="oracle", bounds=None, *,
+                   fleet=None, energy=None, guards=False, types=model, err=errors):
+    """Batched planning over many WorkloadPoints.
+
+    `params` is an AutoscaleParams or a {phase: AutoscaleParams} map (prefill
+    SLO = TTFT, decode SLO = TBT; cli.py:114-120). Points with qps <= 0 are
+    idle windows: they get no plan (cli.py:138-144). Returns a list of
+    WindowDecisions groups aligned with `points` via .index.
+    """
+    m = _MODES[mode] if isinstance(mode, str) else mode
+    bounds = bounds if (bounds is not None or m != abi.MODE_ORACLE) else types.BruteForceBounds()
+    problem = tables.pack_problem(dag, profiles)
+    by_phase = params if isinstance(params, dict) else None
+    groups = {}
+    for i, p in enumerate(points):
+        if not p.qps > 0:
+            continue
+        groups.setdefault(p.phase, []).append(i)
+    out = []
+    for ph, idx in sorted(groups.items()):
+        prm = by_phase[ph] if by_phase is not None else params
+        if guards and m == abi.MODE_ORACLE:
+            _guard(problem, prm, bounds, MAX_ENUMERATION, err)
+        dec = _run(m, problem, [points[i] for i in idx], prm, bounds, fleet, energy, types, err)
+        dec.index = idx
+        out.append(dec)
+    return out
+
+
+def plan_windows(dag, profiles, points, params, mode="oracle", bounds=None, *, fleet=None,
+                 energy=None, guards=False, types=model, err=errors):
+    """list[ScalingPlan | None] aligned with `points` (None for idle windows).
+    Errors of individual windows raise, as the per-point call would."""
+    plans = [None] * len(points)
+    for dec in decide_windows(dag, profiles, points, params, mode, bounds, fleet=fleet,
+                              energy=energy, guards=guards, types=types, err=err):
+        for k, i in enumerate(dec.index):
+            plans[i] = dec.plan(k)
+    return plans
+
+
+def candidate_space(problem, grid):
+    """Semantic candidate count (|P|*R*B)^n of one window."""
+    return math.prod(tables.menu_sizes(problem, grid))

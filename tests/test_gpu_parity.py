@@ -1,0 +1,180 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden vectors (bit-exact) and against the CPU oracle at full config sizes."""
+
+import numpy as np
+import pytest
+
+import golden_cases as G
+from paper_2511_02248_b200 import abi, model, plans, scenarios, tables
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nat():
+    from paper_2511_02248_b200 import _native
+    _native.load()
+    assert _native.device_count() >= 1, "no CUDA device"
+    return _native
+
+
+def _golden(nat, c, mode):
+    prob = G.case_problem(c)
+    params = G.case_params(c)
+    win = G.case_windows(c)
+    grid = tables.pack_grid(prob, params, G.case_bounds(c)) if mode == abi.MODE_ORACLE else None
+    spec = tables.pack_model(prob, params) if mode == abi.MODE_MODEL else None
+    kinds = (["metrics", "metrics_small_fleet", "metrics_tiny_cap"] if mode == abi.MODE_ORACLE
+             else ["model_metrics"])
+    errs = []
+    for kind in kinds:
+        place = tables.pack_place(G.fleet_for(kind), model.EnergyParams())
+        out = nat.plan_windows_host(mode, prob, win, grid=grid, model=spec, place=place)
+        dec = plans.WindowDecisions(prob, [G.case_point(c)], out, mode)
+        exp = c["expected"]
+        if "error" in exp:
+            with pytest.raises(Exception) as ei:
+                dec.plan(0)
+            assert type(ei.value).__name__ == exp["error"], c["name"]
+            return
+        if kind == kinds[0]:
+            errs += G.compare_plan(dec.plan(0), exp, prob)
+        key = "metrics" if kind == "model_metrics" else kind
+        errs += [f"{kind}: {e}" for e in G.compare_metrics(dec.metrics(0), c.get(key))]
+    assert not errs, (c["name"], errs)
+
+
+def test_golden_oracle_cases(nat):
+    for c in G.load("oracle.json"):
+        _golden(nat, c, abi.MODE_ORACLE)
+
+
+def test_golden_model_cases(nat):
+    for c in G.load("model.json"):
+        _golden(nat, c, abi.MODE_MODEL)
+
+
+def _device_menus(nat, prob, grid, win):
+    import torch
+    dev = torch.device("cuda:0")
+    E = grid.menu_off[prob.n_ops]
+    t = {k: torch.from_numpy(np.ascontiguousarray(getattr(win, k))).to(dev)
+         for k in ("qps", "seq_len", "phase", "slo", "eps")}
+    dw = abi.OpscWindows()
+    dw.n = win.n
+    for k in t:
+        setattr(dw, k, t[k].data_ptr())
+    mw = torch.empty((win.n, E), dtype=torch.float64, device=dev)
+    st = torch.zeros(win.n, dtype=torch.int32, device=dev)
+    s = torch.cuda.current_stream().cuda_stream
+    nat.check(nat.load().opsc_menu_build(nat.ref(prob.table), nat.ref(grid), dw, mw.data_ptr(),
+                                         st.data_ptr(), s), "menu_build")
+    torch.cuda.synchronize()
+    return mw.cpu().numpy(), st.cpu().numpy(), dw, t, mw
+
+
+def test_menus_bit_exact(nat):
+    for m in G.load("menus.json"):
+        prob = G.case_problem(m)
+        g = m["grid"]
+        grid = tables.pack_grid(prob, model.AutoscaleParams(slo=1.0),
+                                model.BruteForceBounds(r_max=g["r_max"], b_max=g["b_max"],
+                                                       parallelism=tuple(g["parallelism"])))
+        win = tables.pack_windows([G.case_point(m)], 1.0, 0.0)
+        mw, st, *_ = _device_menus(nat, prob, grid, win)
+        assert st[0] == 0
+        for op, rows in m["entries"].items():
+            v = prob.rank[op]
+            got = [mw[0, grid.menu_off[v] + e].hex() for e in range(len(rows))]
+            assert got == [r[6] for r in rows], (m["scenario"], op)
+
+
+def _scenario_windows(cfg, phase, idx):
+    tw = scenarios.trace_windows(cfg)
+    q = tw[phase + "_qps"][idx]
+    L = tw[phase + "_len"][idx]
+    return tables.window_arrays(q, L, tables.PHASE_INDEX[phase], scenarios.SLO[cfg][phase])
+
+
+def _grid(cfg, prob):
+    g = scenarios.GRIDS[cfg]
+    return tables.pack_grid(prob, model.AutoscaleParams(slo=1.0),
+                            model.BruteForceBounds(r_max=g["r_max"], b_max=g["b_max"],
+                                                   parallelism=g["parallelism"]))
+
+
+@pytest.mark.parametrize("cfg,phase,idx", [
+    ("cfg1", "prefill", [0]), ("cfg1", "decode", [0]),
+    ("cfg5", "prefill", list(range(0, 1440, 180))),
+    ("cfg2", "prefill", [0, 7, 13]), ("cfg2", "decode", [3, 40]),
+    ("cfg3s", "prefill", list(range(0, 60, 9))),
+])
+def test_full_size_vs_oracle(nat, orc, cfg, phase, idx):
+    """Full BASELINE grids (cfg5: 24^6 = 1.9e8 candidates per window; cfg2:
+    6^10 = 6e7 on the 10-op 70B DAG) -- GPU decisions == CPU oracle, bitwise."""
+    prob = tables.pack_problem(*scenarios.scenario(cfg))
+    grid = _grid(cfg, prob)
+    win = _scenario_windows(cfg, phase, np.array(idx))
+    gpu = nat.plan_windows_host(abi.MODE_ORACLE, prob, win, grid=grid)
+    cpu = orc.plan_windows(abi.MODE_ORACLE, prob, win, grid=grid)
+    for f in tables.DecisionArrays.FIELDS:
+        a, b = getattr(gpu, f), getattr(cpu, f)
+        assert a.tobytes() == b.tobytes(), (cfg, phase, f, a, b)
+
+
+def test_full_size_model_grid_vs_oracle(nat, orc):
+    for cfg in ("cfg2", "cfg3"):
+        prob = tables.pack_problem(*scenarios.scenario(cfg))
+        tw = scenarios.trace_windows(cfg)
+        for phase in ("prefill", "decode"):
+            win = tables.window_arrays(tw[phase + "_qps"], tw[phase + "_len"],
+                                       tables.PHASE_INDEX[phase], scenarios.SLO[cfg][phase])
+            spec = tables.pack_model(prob, model.AutoscaleParams(slo=1.0))
+            gpu = nat.plan_windows_host(abi.MODE_MODEL, prob, win, model=spec)
+            cpu = orc.plan_windows(abi.MODE_MODEL, prob, win, model=spec)
+            for f in tables.DecisionArrays.FIELDS:
+                assert getattr(gpu, f).tobytes() == getattr(cpu, f).tobytes(), (cfg, phase, f)
+
+
+def test_sharded_compose_equals_unsharded(nat):
+    """Candidate-range shards min-merge to the single-GPU decision (the
+    multi-GPU path's all-reduce is exactly this merge)."""
+    import torch
+    prob = tables.pack_problem(*scenarios.scenario("cfg5"))
+    grid = _grid("cfg5", prob)
+    win = _scenario_windows("cfg5", "prefill", np.arange(0, 1440, 90))
+    _, _, dw, _t, mw = _device_menus(nat, prob, grid, win)
+    s = torch.cuda.current_stream().cuda_stream
+    L = nat.load()
+
+    def run(n_shards):
+        key = torch.full((win.n,), abi.KEY_INFEASIBLE, dtype=torch.int64, device="cuda")
+        for sh in range(n_shards):
+            part = torch.full_like(key, abi.KEY_INFEASIBLE)
+            nat.check(L.opsc_compose_argmin(nat.ref(prob.table), nat.ref(grid), dw, mw.data_ptr(),
+                                            sh, n_shards, part.data_ptr(), s), "compose")
+            key = torch.minimum(key, part)
+        return key.cpu().numpy()
+
+    base = run(1)
+    assert (base != abi.KEY_INFEASIBLE).any()
+    for n in (2, 3, 8):
+        assert (run(n) == base).all()
+
+
+def test_public_api_matches_per_point(nat):
+    """plan_windows over a batch == mapping the per-point planners."""
+    from paper_2511_02248_b200 import planners
+    dag, prof = scenarios.scenario("cfg3s")
+    tw = scenarios.trace_windows("cfg3s")
+    pts = [model.WorkloadPoint(float(tw["prefill_qps"][i]), int(tw["prefill_len"][i]), "prefill")
+           for i in range(0, 60, 7)]
+    params = model.AutoscaleParams(slo=scenarios.SLO["cfg3s"]["prefill"])
+    b = model.BruteForceBounds(r_max=3, b_max=2, parallelism=(1, 2))
+    batch = planners.plan_windows(dag, prof, pts, params, "oracle", b)
+    for p, plan in zip(pts, batch):
+        one = planners.brute_force_autoscale(dag, prof, p, params, b)
+        assert one.to_dict() == plan.to_dict()
+    ml = planners.plan_windows(dag, prof, pts, params, "model")
+    for p, plan in zip(pts, ml):
+        assert planners.model_level_autoscale(dag, prof, p, params).to_dict() == plan.to_dict()

@@ -1,0 +1,42 @@
+"""Quick device timing of the cfg5 pipeline (dev tool)."""
+import time
+import numpy as np
+import torch
+from paper_2511_02248_b200 import _native, abi, model, scenarios, tables
+
+nat = _native
+L = nat.load()
+prob = tables.pack_problem(*scenarios.scenario("cfg5"))
+g = scenarios.GRIDS["cfg5"]
+grid = tables.pack_grid(prob, model.AutoscaleParams(slo=1.0), model.BruteForceBounds(**g))
+tw = scenarios.trace_windows("cfg5")
+win = tables.window_arrays(tw["prefill_qps"], tw["prefill_len"], 0, 0.5)
+dev = torch.device("cuda:0")
+t = {k: torch.from_numpy(np.ascontiguousarray(getattr(win, k))).to(dev) for k in ("qps", "seq_len", "phase", "slo", "eps")}
+dw = abi.OpscWindows(); dw.n = win.n
+for k in t: setattr(dw, k, t[k].data_ptr())
+E = grid.menu_off[prob.n_ops]
+mw = torch.empty((win.n, E), dtype=torch.float64, device=dev)
+st = torch.zeros(win.n, dtype=torch.int32, device=dev)
+key = torch.empty(win.n, dtype=torch.int64, device=dev)
+s = torch.cuda.current_stream().cuda_stream
+def step():
+    nat.check(L.opsc_menu_build(nat.ref(prob.table), nat.ref(grid), dw, mw.data_ptr(), st.data_ptr(), s), "m")
+    nat.check(L.opsc_fill_keys(key.data_ptr(), win.n, s), "f")
+    nat.check(L.opsc_compose_argmin(nat.ref(prob.table), nat.ref(grid), dw, mw.data_ptr(), 0, 1, key.data_ptr(), s), "c")
+for _ in range(3): step()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(); 
+for _ in range(5): step()
+e1.record(); torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 5
+cands = win.n * 24**6
+print(f"cfg5 step {ms:.3f} ms  candidates {cands:.3e}  rate {cands/ms*1e3:.3e}/s")
+ms2 = ctypes_ms = None
+import ctypes as C
+f = C.c_float(); ops = C.c_double()
+nat.check(L.opsc_fp64_peak(20000, C.cast(C.byref(f), C.c_void_p), C.cast(C.byref(ops), C.c_void_p), s), "peak")
+print(f"fp64 DADD peak: {ops.value/f.value*1e3:.3e} op/s ({f.value:.2f} ms)")
+k = key.cpu().numpy()
+print("feasible windows", (k != abi.KEY_INFEASIBLE).sum())
