@@ -168,7 +168,11 @@ __global__ void __launch_bounds__(64) materialize_kernel(const __grid_constant__
   out.energy[w] = 0.0;
   out.memory[w] = 0.0;
   out.devices[w] = 0;
-  for (int v = 0; v < n; ++v) out.path[(size_t)w * n + v] = -1;
+  for (int v = 0; v < n; ++v) {
+    out.path[(size_t)w * n + v] = -1;
+    out.stable[(size_t)w * n + v] = 0;
+    for (int f = 0; f < OPSC_PRED_FIELDS; ++f) out.pred[((size_t)w * n + v) * OPSC_PRED_FIELDS + f] = 0.0;
+  }
   if (st & (OPSC_W_IDLE | OPSC_W_NO_STABLE_BOUNDS | OPSC_W_NO_STABLE_PARAMS | OPSC_W_NO_STABLE_MODEL))
     return;
   const int16_t* c = out.cfg + (size_t)w * n * 3;

@@ -149,6 +149,8 @@ __global__ void decode_kernel(int n_ops, int n_windows, const __grid_constant__ 
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= n_windows) return;
   feasible[w] = 0;
+  int16_t* cw = cfg + (size_t)w * n_ops * 3;
+  for (int i = 0; i < n_ops * 3; ++i) cw[i] = 0;  // defined output for idle / error windows
   if (status[w] & OPSC_W_IDLE) return;
   int ent[OPSC_MAX_OPS];
   if (key[w] != (unsigned long long)OPSC_KEY_INFEASIBLE) {

@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(1024) model_grid_kernel(const __grid_constant_
 
   const int w = blockIdx.x;
   const double qps = win.qps[w];
+  for (int i = threadIdx.x; i < d.n_ops * 3; i += blockDim.x) cfg[(size_t)w * d.n_ops * 3 + i] = 0;
   if (!(qps > 0.0)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) st_sh = 0;
