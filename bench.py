@@ -1,0 +1,390 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 candidate-evaluation path (BASELINE.json metric:
+candidate configs evaluated/s; per-window decision latency in ms).
+
+Workload (N = 1 and per GPU count): BASELINE config 5 -- the 6-operator
+Llama-2-7B DAG over a synthetic 24 h trace cut into 1440 x 60 s prefill
+windows, exhaustive brute-force grid P in {1,2}, R <= 4, B <= 3, i.e.
+24^6 = 1.91e8 candidates per window (2.75e11 per step). One step = one pass
+of the hot path over the whole batch: per-window prologue, menu build
+(predict_op for every (op, P, R, B)), init_configs stability pre-check,
+exhaustive compose + SLO mask + lexicographic argmin, per-op fallback,
+decode, and plan materialisation (critical path, energy, memory, devices).
+At N > 1 every rank enumerates a contiguous slice of every window's
+candidate space and one NCCL MIN all-reduce of the packed keys gives the
+decision (strong scaling: the job is fixed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+WORKLOAD = ("cfg5: 6-op Llama-2-7B operator DAG, 1440 x 60 s prefill windows of a synthetic "
+            "24 h diurnal trace, exhaustive (P in {1,2}, R<=4, B<=3)^6 = 1.91e8 candidates/window")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-latency", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def workload():
+    from paper_2511_02248_b200 import model, scenarios, tables
+    problem = tables.pack_problem(*scenarios.scenario("cfg5"))
+    g = scenarios.GRIDS["cfg5"]
+    grid = tables.pack_grid(problem, model.AutoscaleParams(slo=scenarios.SLO["cfg5"]["prefill"]),
+                            model.BruteForceBounds(**g))
+    tw = scenarios.trace_windows("cfg5")
+    win = tables.window_arrays(tw["prefill_qps"], tw["prefill_len"], 0,
+                               scenarios.SLO["cfg5"]["prefill"])
+    space = 1
+    for m in tables.menu_sizes(problem, grid):
+        space *= m
+    active = int((win.qps > 0).sum())
+    return problem, grid, win, space, active
+
+
+# ---------------------------------------------------------------- CPU arm
+
+
+def cpu_run(problem, grid, win, target_s=12.0, threads=None):
+    """The CPU port (oracle/, literal enumeration, OpenMP over all host
+    threads) on an evenly spaced bounded sample of the workload windows."""
+    from oracle import oracle as orc
+    from paper_2511_02248_b200 import abi
+    threads = threads or os.cpu_count() or 1
+    t = time.perf_counter()
+    orc.plan_windows(abi.MODE_ORACLE, problem, win.take(np.array([0])), grid=grid, n_threads=threads)
+    t1 = time.perf_counter() - t
+    k = int(max(1, min(win.n, round(target_s / max(t1, 1e-6)))))
+    idx = np.linspace(0, win.n - 1, k).round().astype(np.int64)
+    sub = win.take(idx)
+    t = time.perf_counter()
+    orc.plan_windows(abi.MODE_ORACLE, problem, sub, grid=grid, n_threads=threads)
+    dt = time.perf_counter() - t
+    return k, dt, threads
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    problem, grid, win, space, active = workload()
+    times = []
+    sample = None
+    for i in range(args.warmup + args.steps):
+        k, dt, threads = cpu_run(problem, grid, win, target_s=8.0)
+        if i >= args.warmup:
+            times.append((k, dt))
+        sample = k
+    cands = sum(k * space for k, _ in times)
+    secs = sum(dt for _, dt in times)
+    value = cands / secs
+    line = {
+        "impl": "reference", "metric": "candidate configs evaluated/sec", "value": value,
+        "unit": "candidates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": secs / len(times) * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "windows": win.n, "candidates_per_window": space},
+        "cpu_baseline": {"value": value, "unit": "candidates/s", "cores": threads, "kind": "port",
+                         "sample": f"{sample} of {win.n} cfg5 prefill windows per step "
+                                   f"(evenly spaced), full pipeline, {cpu_model()}"},
+        "e2e": {"value": value, "unit": "candidates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc, self.out = index, None, ""
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.out = self.proc.communicate(timeout=5)[0]
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        loaded = [x for x in sm if x > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": mx or None, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- GPU arm
+
+
+def ours(args):
+    import torch
+
+    from paper_2511_02248_b200 import _native, abi, device, tables
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    problem, grid, win, space, active = workload()
+    planner = device.DevicePlanner(problem, win, abi.MODE_ORACLE, grid=grid, device=dev)
+
+    def allreduce(key):
+        if world > 1:
+            torch.distributed.all_reduce(key, op=torch.distributed.ReduceOp.MIN)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        planner.step(rank, world, allreduce)
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    launches0 = planner.launches
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # L2 (126 MB) flushed between timed steps, outside the events
+            ev[i][0].record()
+            planner.step(rank, world, allreduce, compose_events=cev[i])
+            ev[i][1].record()
+        barrier()
+    launches = planner.launches - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    comp_ms = [a.elapsed_time(b) for a, b in cev]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.MAX)
+    total_ms = float(tot.item())
+    cands_step = active * space
+    value = cands_step * args.steps / (total_ms * 1e-3)
+
+    # parity of this very run against the CPU oracle on a few windows
+    dec = planner.decisions()
+    parity = None
+    if rank == 0:
+        from oracle import oracle as orc
+        idx = np.array([0, 719, 1439])
+        ref = orc.plan_windows(abi.MODE_ORACLE, problem, win.take(idx), grid=grid)
+        parity = all(getattr(dec, f)[idx].tobytes() == getattr(ref, f).tobytes()
+                     for f in ("key", "cfg", "latency", "energy", "memory", "devices"))
+
+    # roofline of the dominant kernel (compose_argmin)
+    peak = device.fp64_peak()
+    comp_avg = sum(comp_ms) / len(comp_ms) * 1e-3
+    my_cands = cands_step / world
+    achieved = 2.0 * my_cands / comp_avg  # DADD + DSETP per composed candidate
+    n_ops = problem.n_ops
+    traffic = None
+    tp = os.path.join(REPO, "profiles", "compose_ncu_summary.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    # e2e through the C-ABI host-buffer call (pinned host windows in, decisions out)
+    e2e = None
+    if world == 1:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        hwin = tables.WindowArrays(*(pin(getattr(win, k)) for k in
+                                     ("qps", "seq_len", "phase", "slo", "eps")))
+        hout = tables.DecisionArrays(win.n, n_ops)
+        for f in tables.DecisionArrays.FIELDS:
+            setattr(hout, f, pin(getattr(hout, f)))
+        ctx = _native.Context(device=local, max_windows=win.n)
+        for _ in range(args.warmup):
+            ctx.plan_windows(abi.MODE_ORACLE, problem, hwin, grid=grid, out=hout)
+        t = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            ctx.plan_windows(abi.MODE_ORACLE, problem, hwin, grid=grid, out=hout)
+            t.append(time.perf_counter() - t0)
+        e2e_launches = ctx.last_launches()
+        ctx.close()
+        bi = sum(getattr(hwin, k).nbytes for k in ("qps", "seq_len", "phase", "slo", "eps"))
+        e2e = {"value": cands_step * len(t) / sum(t), "unit": "candidates/s",
+               "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(hout.nbytes()),
+               "api": "opsc_plan_windows_host (C ABI, host buffers)",
+               "launches_per_step": e2e_launches,
+               "parity_vs_device_path": bool(all(
+                   getattr(hout, f).tobytes() == getattr(dec, f).tobytes()
+                   for f in ("key", "cfg", "latency", "energy")))}
+
+    # per-window decision latency on the 70B DAG (cfg2), W = 1
+    latency = None
+    if rank == 0 and not args.no_latency:
+        latency = decision_latency(dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        k, dt, threads = cpu_run(problem, grid, win, target_s=12.0)
+        cpu = {"value": k * space / dt, "unit": "candidates/s", "cores": threads, "kind": "port",
+               "sample": f"{k} of {win.n} cfg5 prefill windows (evenly spaced), full pipeline "
+                         f"(menus, literal enumeration, decode, materialise), OpenMP, {cpu_model()}"}
+
+    if rank == 0:
+        line = {
+            "metric": "candidate configs evaluated/sec", "value": value, "unit": "candidates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "windows": win.n, "active_windows": active,
+                       "candidates_per_window": space, "candidates_per_step": cands_step,
+                       "mode": "oracle (exhaustive brute force, every candidate composed)",
+                       "parallelism": f"candidate-range shards x{world} + NCCL MIN all-reduce"
+                                      if world > 1 else "single GPU",
+                       "l2": "flushed between timed steps (256 MiB write outside the events)"},
+            "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "compose_kernel (opsc_compose_argmin)",
+                         "algorithmic_ops_per_candidate": 2,
+                         "peak_source": "live DADD microbenchmark (opsc_fp64_peak); "
+                                        "MEASURED_PEAKS.json has no FP64 figure",
+                         "survey_n_ops_per_candidate": n_ops,
+                         "survey_frac": n_ops * my_cands / comp_avg / peak,
+                         "kernel_ms": comp_avg * 1e3,
+                         "kernel_share_of_step": comp_avg * 1e3 / (sum(step_ms) / len(step_ms))},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "decision_latency_ms": latency,
+            "parity_vs_oracle": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+def decision_latency(dev):
+    """Window stats resident on device -> decoded decision, one window at a
+    time, for the 10-op Llama-2-70B DAG (cfg2): exhaustive oracle over
+    (P in {1,2}, R<=3, B=1)^10 = 6.0e7 candidates, and the model-level grid."""
+    import torch
+
+    from paper_2511_02248_b200 import abi, device, model, scenarios, tables
+    problem = tables.pack_problem(*scenarios.scenario("cfg2"))
+    g = scenarios.GRIDS["cfg2"]
+    tw = scenarios.trace_windows("cfg2")
+    out = {}
+    for mode, name in ((abi.MODE_ORACLE, "oracle_6e7_candidates"), (abi.MODE_MODEL, "model_level")):
+        samples = []
+        for phase in ("prefill", "decode"):
+            slo = scenarios.SLO["cfg2"][phase]
+            params = model.AutoscaleParams(slo=slo)
+            grid = tables.pack_grid(problem, params, model.BruteForceBounds(**g))
+            spec = tables.pack_model(problem, params)
+            qs, ls = tw[phase + "_qps"], tw[phase + "_len"]
+            one = tables.window_arrays(qs[:1], ls[:1], tables.PHASE_INDEX[phase], slo)
+            p = device.DevicePlanner(problem, one, mode, grid=grid, model=spec, device=dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            for i in range(len(qs)):
+                if not qs[i] > 0:
+                    continue
+                p.win_t["qps"].fill_(float(qs[i]))
+                p.win_t["seq_len"].fill_(int(ls[i]))
+                if i == 0:
+                    p.step()
+                torch.cuda.synchronize(dev)
+                e0.record()
+                p.step()
+                e1.record()
+                e1.synchronize()
+                samples.append(e0.elapsed_time(e1))
+        samples.sort()
+        out[name] = {"median": statistics.median(samples),
+                     "p99": samples[min(len(samples) - 1, int(0.99 * len(samples)))],
+                     "windows": len(samples)}
+    out["dag"] = "cfg2 Llama-2-70B 10-op chain, 60 x 60 s windows x {prefill, decode}, W = 1"
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        ours(args)
+
+
+if __name__ == "__main__":
+    main()

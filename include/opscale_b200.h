@@ -196,6 +196,11 @@ OPSC_API int opsc_compose_argmin(const OpscDag* dag, const OpscGrid* grid, OpscW
 
 OPSC_API int opsc_fill_keys(int64_t* key, int32_t n, void* stream);
 
+/* Per-window prologue: status = OPSC_W_IDLE for qps <= 0 (cli.py:138-144)
+ * else 0; key = OPSC_KEY_INFEASIBLE; feasible = 0. key/feasible may be NULL. */
+OPSC_API int opsc_init_windows(OpscWindows win, uint32_t* status, int64_t* key, uint8_t* feasible,
+                               void* stream);
+
 /* fb_entry: [W][n_ops] argmin over finite menu weights of (weight, entry), -1 if none. */
 OPSC_API int opsc_menu_fallback(const OpscDag* dag, const OpscGrid* grid, int32_t n_windows,
                        const double* menu_w, int32_t* fb_entry, void* stream);

@@ -20,7 +20,8 @@ LIB_PATH = os.path.join(HERE, "_lib", "libopscale_b200.so")
 # every symbol include/opscale_b200.h declares
 EXPORTS = (
     "opsc_abi_version", "opsc_status_string", "opsc_device_count", "opsc_menu_build",
-    "opsc_stability_check", "opsc_compose_argmin", "opsc_fill_keys", "opsc_menu_fallback",
+    "opsc_stability_check", "opsc_compose_argmin", "opsc_fill_keys", "opsc_init_windows",
+    "opsc_menu_fallback",
     "opsc_decode_decisions", "opsc_model_grid", "opsc_materialize", "opsc_ctx_create",
     "opsc_ctx_destroy", "opsc_plan_windows_host", "opsc_ctx_last_launches", "opsc_fp64_peak",
 )
@@ -50,6 +51,7 @@ def load():
             "opsc_stability_check": ([P, P, W, P, P], C.c_int),
             "opsc_compose_argmin": ([P, P, W, P, I, I, P, P], C.c_int),
             "opsc_fill_keys": ([P, I, P], C.c_int),
+            "opsc_init_windows": ([W, P, P, P, P], C.c_int),
             "opsc_menu_fallback": ([P, P, I, P, P, P], C.c_int),
             "opsc_decode_decisions": ([P, P, I, P, P, P, P, P, P], C.c_int),
             "opsc_model_grid": ([P, P, W, P, P, P, P], C.c_int),

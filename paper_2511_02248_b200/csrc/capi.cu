@@ -191,6 +191,12 @@ int opsc_fill_keys(int64_t* key, int32_t n, void* stream) {
   return from_cuda(launch_fill_keys((unsigned long long*)key, n, (cudaStream_t)stream));
 }
 
+int opsc_init_windows(OpscWindows win, uint32_t* status, int64_t* key, uint8_t* feasible, void* stream) {
+  if (!status || win.n < 0) return OPSC_ERR_ARG;
+  return from_cuda(launch_init(win.n, win.qps, status, (unsigned long long*)key, feasible,
+                               (cudaStream_t)stream));
+}
+
 int opsc_menu_fallback(const OpscDag* dag, const OpscGrid* grid, int32_t n_windows, const double* menu_w,
                        int32_t* fb_entry, void* stream) {
   if (!valid_dag(dag) || !grid) return OPSC_ERR_ARG;

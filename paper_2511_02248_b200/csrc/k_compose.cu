@@ -6,21 +6,24 @@
 // as the critical-path DP of opgraph.py:223-244 (max over predecessors, then
 // + own weight, in topological order), masked with `<= slo`, and reduced with
 // key = (objective << 40) | lexicographic index (ops sorted by id, per op
-// (P,R,B) ascending; autoscaler.py:725, 747-749, 795). Because the key carries
-// the global lexicographic index, traversal order, sharding and reduction
+// (P,R,B) ascending; autoscaler.py:725, 747-749, 795). The key carries the
+// global lexicographic index, so traversal order, sharding and reduction
 // order cannot change the winner.
 //
-// Work split (one CTA = 256 threads of one window):
-//   * positions = topological order of the ops; the last two positions are the
-//     k and j levels, `il-2` middle levels sit above them, the rest are
-//     "outer" and fixed per thread (decoded from the thread's outer index);
-//   * the j menu (innermost) lives in registers: per candidate the thread does
-//     one DADD (path extension), one DSETP (SLO mask) and one predicated
-//     32-bit min of (P*R << 16 | j) -- prefix hoisting keeps the rest of the
-//     DP out of the inner loop;
-//   * menus + per-entry costs are staged once per CTA in shared memory; the
-//     k level reads them as warp-broadcast LDS;
-//   * CTA result = warp-shuffle u64 min -> smem -> one atomicMin per CTA.
+// Work split (one CTA = 256 threads, one window):
+//   * positions = topological order; the last two are the k and j levels,
+//     `il-2` middle levels sit above them, the rest are "outer" and fixed per
+//     thread (decoded from the thread's outer index);
+//   * the j menu (innermost op) is staged SORTED by its key (P*R, entry) and
+//     held in registers; per candidate the thread issues exactly
+//         DADD  lat = B_j + w_j          (path extension, the DP's last add)
+//         DSETP lat <= slo               (SLO mask)
+//         @P MOV inner = rank            (descending scan: the last hit is the
+//                                         cheapest feasible j of this prefix)
+//     with no loop-carried dependency, so warps issue back to back;
+//   * per k entry the cheapest feasible (k, j) pair is folded into a u64 key
+//     from shared-memory key tables; CTA result = warp-shuffle u64 min ->
+//     smem -> one atomicMin per CTA.
 #include <algorithm>
 #include <cstring>
 
@@ -29,6 +32,7 @@
 namespace opsc {
 
 constexpr int kComposeThreads = 256;
+constexpr unsigned long long kSentinel = 1ull << 62;  // > any real key (objective < 2^17)
 
 __device__ __forceinline__ double dp_in(uint32_t pm, const double* val) {
   double in = 0.0;
@@ -40,47 +44,71 @@ __device__ __forceinline__ double dp_in(uint32_t pm, const double* val) {
   return in;
 }
 
-template <int NJ>
-__global__ void __launch_bounds__(kComposeThreads, 2)
+struct ComposeSmem {
+  double* w;                 // [E+1] weights (entry E = virtual, 0.0)
+  int32_t* cost;             // [E+1] P*R per entry
+  unsigned long long* kk;    // [m_k] (cost_k << 40) + a * kstride
+  double* jw;                // [m_j] j weights sorted by key
+  unsigned long long* jk;    // [m_j + 1] sorted j keys, jk[m_j] = sentinel
+};
+
+template <int NJ, bool CHAIN>
+__global__ void __launch_bounds__(kComposeThreads, 3)
 compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ OpscGrid g,
                const double* __restrict__ menu_w, const double* __restrict__ slo_w,
                const double* __restrict__ qps_w, unsigned long long* __restrict__ key_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* sw = reinterpret_cast<double*>(smem_raw);
-  int32_t* sc = reinterpret_cast<int32_t*>(sw + c.E + 1);
   __shared__ unsigned long long warp_best[kComposeThreads / 32];
+  const int jp = c.n - 1, kp = c.n - 2;
+  const int mj = c.m[jp], mk = c.m[kp];
+  ComposeSmem s;
+  s.kk = reinterpret_cast<unsigned long long*>(smem_raw);
+  s.jk = s.kk + mk;
+  s.w = reinterpret_cast<double*>(s.jk + mj + 1);
+  s.jw = s.w + c.E + 1;
+  s.cost = reinterpret_cast<int32_t*>(s.jw + mj);
 
   const int w = blockIdx.x / c.blocks_per_window;
   const int bw = blockIdx.x - w * c.blocks_per_window;
   const double* src = menu_w + (size_t)w * c.E;
   for (int i = threadIdx.x; i < c.E; i += kComposeThreads) {
-    sw[i] = src[i];
+    s.w[i] = src[i];
     int v = 0;
     while (i >= g.menu_off[v + 1]) ++v;
     int p, r, b;
     entry_prb(g, v, i - g.menu_off[v], p, r, b);
-    sc[i] = p * r;  // objective contribution (autoscaler.py:220-221, 756)
+    s.cost[i] = p * r;  // objective contribution (autoscaler.py:220-221, 756)
   }
-  if (threadIdx.x == 0) {  // the virtual entry (weight 0, cost 0)
-    sw[c.E] = 0.0;
-    sc[c.E] = 0;
+  if (threadIdx.x == 0) {
+    s.w[c.E] = 0.0;
+    s.cost[c.E] = 0;
   }
+  __syncthreads();
+  const int koff = c.off[kp], joff = c.off[jp];
+  for (int a = threadIdx.x; a < mk; a += kComposeThreads)
+    s.kk[a] = ((unsigned long long)s.cost[koff + a] << OPSC_KEY_LEX_BITS) + (unsigned long long)a * c.stride[kp];
+  for (int i = threadIdx.x; i < mj; i += kComposeThreads) {
+    // rank of entry i in (cost, entry) order == order of its key
+    const int ci = s.cost[joff + i];
+    int rank = 0;
+    for (int q = 0; q < mj; ++q) {
+      const int cq = s.cost[joff + q];
+      rank += (cq < ci) || (cq == ci && q < i);
+    }
+    s.jw[rank] = s.w[joff + i];
+    s.jk[rank] = ((unsigned long long)ci << OPSC_KEY_LEX_BITS) + (unsigned long long)i * c.stride[jp];
+  }
+  if (threadIdx.x == 0) s.jk[mj] = kSentinel;
   __syncthreads();
 
   const double slo = slo_w[w];
-  unsigned long long best = (unsigned long long)OPSC_KEY_INFEASIBLE;
+  unsigned long long best = kSentinel;
   const uint32_t o = c.lo + (uint32_t)bw * kComposeThreads + threadIdx.x;
   if (qps_w[w] > 0.0 && o < c.hi) {
-    const int jp = c.n - 1, kp = c.n - 2, nout = c.n - c.il;
-    const int joff = c.off[jp], mj = c.m[jp];
+    const int nout = c.n - c.il;
     double wj[NJ > 0 ? NJ : 1];
-    uint32_t kj[NJ > 0 ? NJ : 1];
 #pragma unroll
-    for (int i = 0; i < NJ; ++i) {
-      const bool ok = i < mj;
-      wj[i] = ok ? sw[joff + i] : OPSC_INF;
-      kj[i] = ok ? ((uint32_t)sc[joff + i] << 16 | (uint32_t)i) : 0xffffffffu;
-    }
+    for (int i = 0; i < NJ; ++i) wj[i] = i < mj ? s.jw[i] : OPSC_INF;
     double val[OPSC_CMAX];
     int dig[OPSC_CMAX];
     uint32_t rem = o;
@@ -94,15 +122,13 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
     unsigned long long lex0 = 0;
     for (int pos = 0; pos < nout; ++pos) {
       const int e = c.off[pos] + dig[pos];
-      val[pos] = dp_in(c.pmask[pos], val) + sw[e];
-      cost0 += sc[e];
+      val[pos] = dp_in(c.pmask[pos], val) + s.w[e];
+      cost0 += s.cost[e];
       lex0 += (unsigned long long)dig[pos] * c.stride[pos];
     }
     const uint32_t kmask = 1u << kp, jmask = 1u << jp;
     const bool k_to_j = (c.pmask[jp] & kmask) != 0;
     const bool k_sink = (c.sinkmask & kmask) != 0;
-    const int koff = c.off[kp], mk = c.m[kp];
-    const unsigned long long kstride = c.stride[kp], jstride = c.stride[jp];
 
     for (uint32_t mid = 0; mid < c.mid_count; ++mid) {
       uint32_t r2 = mid;
@@ -116,45 +142,45 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
       unsigned long long lex1 = lex0;
       for (int pos = nout; pos < kp; ++pos) {
         const int e = c.off[pos] + dig[pos];
-        val[pos] = dp_in(c.pmask[pos], val) + sw[e];
-        cost1 += sc[e];
+        val[pos] = dp_in(c.pmask[pos], val) + s.w[e];
+        cost1 += s.cost[e];
         lex1 += (unsigned long long)dig[pos] * c.stride[pos];
       }
-      const double in_k = dp_in(c.pmask[kp], val);
+      double in_k = dp_in(c.pmask[kp], val);
       const double bj0 = dp_in(c.pmask[jp] & ~kmask, val);
       const double lo0 = dp_in(c.sinkmask & ~(kmask | jmask), val);
+      if (CHAIN && !(lo0 <= slo)) in_k = OPSC_INF;  // another sink already misses the SLO
 
+      unsigned long long mbest = kSentinel;
       for (int a = 0; a < mk; ++a) {
-        const double bk = in_k + sw[koff + a];
-        double bj = k_to_j ? fmax(bj0, bk) : bj0;
-        const double lo = k_sink ? fmax(lo0, bk) : lo0;
-        if (!(lo <= slo)) bj = OPSC_INF;
-        uint32_t in0 = 0xffffffffu, in1 = 0xffffffffu;
+        const double bk = in_k + s.w[koff + a];
+        double bj;
+        if (CHAIN) {
+          bj = bk;  // j's only predecessor is k, k is not a sink
+        } else {
+          bj = k_to_j ? fmax(bj0, bk) : bj0;
+          const double lo = k_sink ? fmax(lo0, bk) : lo0;
+          if (!(lo <= slo)) bj = OPSC_INF;
+        }
+        int inner = mj;
         if (NJ > 0) {
 #pragma unroll
-          for (int i = 0; i < NJ; i += 2) {
-            const double l0 = bj + wj[i];
-            if (l0 <= slo) in0 = min(in0, kj[i]);
-            if (i + 1 < NJ) {
-              const double l1 = bj + wj[i + 1];
-              if (l1 <= slo) in1 = min(in1, kj[i + 1]);
-            }
+          for (int i = NJ - 1; i >= 0; --i) {
+            const double lat = bj + wj[i];
+            if (lat <= slo) inner = i;
           }
         } else {
-          for (int i = 0; i < mj; ++i) {
-            const double l0 = bj + sw[joff + i];
-            if (l0 <= slo) in0 = min(in0, (uint32_t)sc[joff + i] << 16 | (uint32_t)i);
+          for (int i = mj - 1; i >= 0; --i) {
+            const double lat = bj + s.jw[i];
+            if (lat <= slo) inner = i;
           }
         }
-        const uint32_t inner = min(in0, in1);
-        if (inner != 0xffffffffu) {
-          const unsigned long long cst =
-              (unsigned long long)(cost1 + sc[koff + a] + (long long)(inner >> 16));
-          const unsigned long long lx = lex1 + (unsigned long long)a * kstride +
-                                        (unsigned long long)(inner & 0xffffu) * jstride;
-          const unsigned long long key = cst << OPSC_KEY_LEX_BITS | lx;
-          best = key < best ? key : best;
-        }
+        const unsigned long long kl = s.kk[a] + s.jk[inner];
+        mbest = kl < mbest ? kl : mbest;
+      }
+      if (mbest < kSentinel) {
+        const unsigned long long key = ((unsigned long long)cost1 << OPSC_KEY_LEX_BITS) + lex1 + mbest;
+        best = key < best ? key : best;
       }
     }
   }
@@ -162,10 +188,9 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
   if ((threadIdx.x & 31) == 0) warp_best[threadIdx.x >> 5] = best;
   __syncthreads();
   if (threadIdx.x < 32) {
-    unsigned long long b = threadIdx.x < kComposeThreads / 32 ? warp_best[threadIdx.x]
-                                                               : (unsigned long long)OPSC_KEY_INFEASIBLE;
+    unsigned long long b = threadIdx.x < kComposeThreads / 32 ? warp_best[threadIdx.x] : kSentinel;
     b = warp_min_u64(b);
-    if (threadIdx.x == 0 && b != (unsigned long long)OPSC_KEY_INFEASIBLE) atomicMin(&key_out[w], b);
+    if (threadIdx.x == 0 && b < kSentinel) atomicMin(&key_out[w], b);
   }
 }
 
@@ -197,8 +222,6 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
     if (pos < nvirt) {
       c.m[pos] = 1;
       c.off[pos] = c.E;
-      c.stride[pos] = 0;
-      c.pmask[pos] = 0;
       continue;
     }
     const int v = d.topo[pos - nvirt];
@@ -211,26 +234,33 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
     c.pmask[pos] = pm;
     if (d.sink_mask >> v & 1u) c.sinkmask |= 1u << pos;
   }
-  // entry costs: P*R of each entry (multiplies of <= 8 x r_max) must fit 15 bits
-  for (int v = 0; v < nr; ++v)
-    for (int i = 0; i < g.n_p[v]; ++i)
-      if ((long long)g.p_vals[v][i] * g.r_max > 32767) return OPSC_ERR_ARG;
-  // level split: as many in-thread levels as keep >= ~1 wave of threads
-  auto m_out = [&](int il) {
+  // the objective of any candidate must stay below 2^17 (key headroom under the sentinel)
+  long long max_obj = 0;
+  for (int v = 0; v < nr; ++v) {
+    int pmax = 0;
+    for (int i = 0; i < g.n_p[v]; ++i) pmax = std::max(pmax, g.p_vals[v][i]);
+    max_obj += (long long)pmax * g.r_max;
+  }
+  if (max_obj >= (1 << 17)) return OPSC_ERR_ARG;
+  // level split: enough in-thread candidates to amortise the outer decode,
+  // while keeping at least half a wave of threads
+  auto prod = [&](int lo, int hi) {
     double x = 1.0;
-    for (int pos = 0; pos < c.n - il; ++pos) x *= c.m[pos];
+    for (int pos = lo; pos < hi; ++pos) x *= c.m[pos];
     return x;
   };
-  const double target = 148.0 * 1024.0;
+  const double min_threads = 148.0 * 512.0;
   int il = 2;
-  while (il < c.n && il < 6 &&
-         (m_out(il) >= 4294967295.0 || (double)n_windows * m_out(il + 1) >= target))
+  while (il < c.n && il < 6) {
+    const bool too_many = prod(0, c.n - il) >= 4294967295.0;
+    if (!too_many && prod(c.n - il, c.n) >= 2048.0) break;
+    if (!too_many && (double)n_windows * prod(0, c.n - il - 1) < min_threads) break;
     ++il;
-  if (m_out(il) >= 4294967295.0) return OPSC_ERR_SPACE;
+  }
+  if (prod(0, c.n - il) >= 4294967295.0) return OPSC_ERR_SPACE;
   c.il = il;
-  c.m_out = (uint32_t)m_out(il);
-  double mid = 1.0;
-  for (int pos = c.n - il; pos < c.n - 2; ++pos) mid *= c.m[pos];
+  c.m_out = (uint32_t)prod(0, c.n - il);
+  const double mid = prod(c.n - il, c.n - 2);
   if (mid >= 4294967295.0) return OPSC_ERR_SPACE;
   c.mid_count = (uint32_t)mid;
   c.lo = (uint32_t)((unsigned long long)c.m_out * shard / n_shards);
@@ -239,29 +269,39 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
   if (c.blocks_per_window < 1) c.blocks_per_window = 1;
   const int mj = c.m[c.n - 1];
   c.nj = mj <= 4 ? 4 : mj <= 8 ? 8 : mj <= 12 ? 12 : mj <= 16 ? 16 : mj <= 24 ? 24 : mj <= 32 ? 32 : 0;
+  // chain fast path: j's only predecessor is k and k is not a sink
+  const int jp = c.n - 1, kp = c.n - 2;
+  c.chain = (c.pmask[jp] == (1u << kp)) && !(c.sinkmask >> kp & 1u);
   *cfg = c;
   return OPSC_OK;
 }
 
-template <int NJ>
-static cudaError_t launch_nj(const ComposeCfg& c, const OpscGrid& g, int n_windows,
-                             const double* menu_w, const double* slo, const double* qps,
-                             unsigned long long* key, cudaStream_t s) {
-  const size_t smem = (size_t)(c.E + 1) * (sizeof(double) + sizeof(int32_t));
+template <int NJ, bool CHAIN>
+static cudaError_t launch_t(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,
+                            const double* slo, const double* qps, unsigned long long* key, cudaStream_t s) {
+  const int mj = c.m[c.n - 1], mk = c.m[c.n - 2];
+  const size_t smem = (size_t)mk * 8 + (size_t)(mj + 1) * 8 + (size_t)(c.E + 1) * 8 + (size_t)mj * 8 +
+                      (size_t)(c.E + 1) * 4;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(compose_kernel<NJ>,
+    cudaError_t e = cudaFuncSetAttribute(compose_kernel<NJ, CHAIN>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   const long long blocks = (long long)n_windows * c.blocks_per_window;
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  compose_kernel<NJ><<<(unsigned)blocks, kComposeThreads, smem, s>>>(c, g, menu_w, slo, qps, key);
+  compose_kernel<NJ, CHAIN><<<(unsigned)blocks, kComposeThreads, smem, s>>>(c, g, menu_w, slo, qps, key);
   return cudaGetLastError();
 }
 
-cudaError_t launch_compose(const ComposeCfg& c, const OpscGrid& g, int n_windows,
-                           const double* menu_w, const double* slo, const double* qps,
-                           unsigned long long* key, cudaStream_t s) {
+template <int NJ>
+static cudaError_t launch_nj(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,
+                             const double* slo, const double* qps, unsigned long long* key, cudaStream_t s) {
+  return c.chain ? launch_t<NJ, true>(c, g, n_windows, menu_w, slo, qps, key, s)
+                 : launch_t<NJ, false>(c, g, n_windows, menu_w, slo, qps, key, s);
+}
+
+cudaError_t launch_compose(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,
+                           const double* slo, const double* qps, unsigned long long* key, cudaStream_t s) {
   if (n_windows <= 0 || c.hi <= c.lo) return cudaSuccess;
   switch (c.nj) {
     case 4: return launch_nj<4>(c, g, n_windows, menu_w, slo, qps, key, s);

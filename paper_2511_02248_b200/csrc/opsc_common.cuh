@@ -156,6 +156,7 @@ struct ComposeCfg {
   uint32_t mid_count;          // product of middle-level menu sizes
   int32_t blocks_per_window;
   int32_t nj;                  // register tile of the innermost menu
+  int32_t chain;               // j's only predecessor is k and k is not a sink
 };
 
 namespace opsc {

@@ -1,0 +1,147 @@
+"""Device-resident planning pipeline (torch owns the HBM buffers).
+
+`DevicePlanner` keeps a batch of windows resident in HBM and runs the search
+kernels through the device-pointer C-ABI entry points on torch's current
+stream. It is what bench.py times (`value`) and what the multi-GPU path
+shards: every rank enumerates its slice of each window's candidate space and
+one MIN all-reduce of the packed (objective << 40 | lexicographic index) keys
+yields the global decision -- the same merge the single-GPU kernel does with
+atomicMin, so the decision is identical for any number of ranks.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _native, abi, tables
+
+
+class DevicePlanner:
+    def __init__(self, problem, windows: tables.WindowArrays, mode=abi.MODE_ORACLE, grid=None,
+                 model=None, place=None, device="cuda"):
+        self.problem, self.mode = problem, mode
+        self.grid = grid if grid is not None else abi.OpscGrid()
+        self.model = model if model is not None else abi.OpscModelSpec()
+        self.place = place or tables.pack_place()
+        self.dev = torch.device(device)
+        self.L = _native.load()
+        n, W = problem.n_ops, windows.n
+        self.W, self.n = W, n
+        to = lambda a: torch.from_numpy(np.array(a, copy=True)).to(self.dev)
+        self.win_t = {k: to(getattr(windows, k)) for k in ("qps", "seq_len", "phase", "slo", "eps")}
+        self.win = abi.OpscWindows()
+        self.win.n = W
+        for k, t in self.win_t.items():
+            setattr(self.win, k, t.data_ptr())
+        E = self.grid.menu_off[n] if mode == abi.MODE_ORACLE else 0
+        self.E = E
+        z = lambda *shape, dt: torch.zeros(shape, dtype=dt, device=self.dev)
+        self.menu = z(max(W * E, 1), dt=torch.float64)
+        self.fb = z(max(W * n, 1), dt=torch.int32)
+        self.key = z(W, dt=torch.int64)
+        self.out_t = {
+            "key": self.key, "cfg": z(W, n, 3, dt=torch.int16), "feasible": z(W, dt=torch.uint8),
+            "status": z(W, dt=torch.int32), "latency": z(W, dt=torch.float64),
+            "objective": z(W, dt=torch.int32), "path": z(W, n, dt=torch.int8),
+            "pred": z(W, n, abi.PRED_FIELDS, dt=torch.float64), "stable": z(W, n, dt=torch.uint8),
+            "energy": z(W, dt=torch.float64), "memory": z(W, dt=torch.float64),
+            "devices": z(W, dt=torch.int32),
+        }
+        self.out = abi.OpscDecisions()
+        for k, t in self.out_t.items():
+            setattr(self.out, k, t.data_ptr())
+        caps = torch.from_numpy(self.place.mem_cap).to(self.dev)
+        self._caps = caps
+        self.dplace = abi.OpscPlaceSpec()
+        for f, _ in abi.OpscPlaceSpec._fields_:
+            setattr(self.dplace, f, getattr(self.place.spec, f))
+        self.dplace.mem_cap = caps.data_ptr()
+        self.launches = 0
+
+    def _s(self):
+        return torch.cuda.current_stream(self.dev).cuda_stream
+
+    def _ck(self, rc, what):
+        _native.check(rc, what)
+        self.launches += 1
+
+    def _init(self):
+        # status = idle bit for qps <= 0, keys = +inf, feasible = 0
+        self._ck(self.L.opsc_init_windows(self.win, self.out_t["status"].data_ptr(),
+                                          self.key.data_ptr(), self.out_t["feasible"].data_ptr(),
+                                          self._s()), "init_windows")
+
+    def menus(self):
+        r = _native.ref
+        self._ck(self.L.opsc_menu_build(r(self.problem.table), r(self.grid), self.win,
+                                        self.menu.data_ptr(), self.out_t["status"].data_ptr(),
+                                        self._s()), "menu_build")
+        self._ck(self.L.opsc_stability_check(r(self.problem.table), r(self.grid), self.win,
+                                             self.out_t["status"].data_ptr(), self._s()),
+                 "stability_check")
+
+    def compose(self, shard=0, n_shards=1):
+        r = _native.ref
+        self._ck(self.L.opsc_compose_argmin(r(self.problem.table), r(self.grid), self.win,
+                                            self.menu.data_ptr(), shard, n_shards,
+                                            self.key.data_ptr(), self._s()), "compose_argmin")
+
+    def finish(self):
+        r, s = _native.ref, self._s()
+        if self.mode == abi.MODE_ORACLE:
+            self._ck(self.L.opsc_menu_fallback(r(self.problem.table), r(self.grid), self.W,
+                                               self.menu.data_ptr(), self.fb.data_ptr(), s),
+                     "menu_fallback")
+            self._ck(self.L.opsc_decode_decisions(
+                r(self.problem.table), r(self.grid), self.W, self.key.data_ptr(),
+                self.fb.data_ptr(), self.out_t["cfg"].data_ptr(), self.out_t["feasible"].data_ptr(),
+                self.out_t["status"].data_ptr(), s), "decode")
+            order = 0
+        else:
+            order = 1
+        self._ck(self.L.opsc_materialize(r(self.problem.table), self.win, order, r(self.dplace),
+                                         self.out, s), "materialize")
+
+    def model_grid(self):
+        r = _native.ref
+        self._ck(self.L.opsc_model_grid(r(self.problem.table), r(self.model), self.win,
+                                        self.out_t["cfg"].data_ptr(),
+                                        self.out_t["feasible"].data_ptr(),
+                                        self.out_t["status"].data_ptr(), self._s()), "model_grid")
+
+    def step(self, shard=0, n_shards=1, allreduce=None, compose_events=None):
+        """One pass of the hot path over the resident batch of windows."""
+        self._init()
+        if self.mode == abi.MODE_ORACLE:
+            self.menus()
+            if compose_events:
+                compose_events[0].record()
+            self.compose(shard, n_shards)
+            if compose_events:
+                compose_events[1].record()
+            if allreduce is not None:
+                allreduce(self.key)
+        else:
+            self.model_grid()
+        self.finish()
+
+    def decisions(self) -> tables.DecisionArrays:
+        torch.cuda.synchronize(self.dev)
+        out = tables.DecisionArrays(self.W, self.n)
+        for k, t in self.out_t.items():
+            getattr(out, k)[...] = t.cpu().numpy().astype(getattr(out, k).dtype).reshape(
+                getattr(out, k).shape)
+        return out
+
+
+def fp64_peak(iters=20000):
+    """Measured FP64 (DADD) issue peak of this GPU, op/s (live microbenchmark)."""
+    L = _native.load()
+    ms, ops = C.c_float(), C.c_double()
+    _native.check(L.opsc_fp64_peak(iters, C.cast(C.byref(ms), C.c_void_p),
+                                   C.cast(C.byref(ops), C.c_void_p),
+                                   torch.cuda.current_stream().cuda_stream), "fp64_peak")
+    return ops.value / (ms.value * 1e-3)
