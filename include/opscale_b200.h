@@ -241,6 +241,12 @@ OPSC_API int opsc_ctx_last_launches(const OpscContext* ctx, int32_t* launches);
  * writes elapsed milliseconds and the executed FP64 op count. */
 OPSC_API int opsc_fp64_peak(int32_t iters, float* ms, double* fp64_ops, void* stream);
 
+/* Candidate-loop probe: the compose inner loop on synthetic register menus
+ * (kind 1: DADD + DSETP + select per candidate, kind 2: DSETP + select).
+ * Gives the instruction-mix ceiling of the compose kernel on this GPU. */
+OPSC_API int opsc_candidate_probe(int32_t kind, int32_t iters, float* ms, double* candidates,
+                                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,6 +36,6 @@ def __getattr__(name):
         from . import planners
         return getattr(planners, name)
     if name == "install":
-        from .install import install
+        from .installer import install
         return install
     raise AttributeError(name)

@@ -24,6 +24,7 @@ EXPORTS = (
     "opsc_menu_fallback",
     "opsc_decode_decisions", "opsc_model_grid", "opsc_materialize", "opsc_ctx_create",
     "opsc_ctx_destroy", "opsc_plan_windows_host", "opsc_ctx_last_launches", "opsc_fp64_peak",
+    "opsc_candidate_probe",
 )
 
 _lib = None
@@ -61,6 +62,7 @@ def load():
             "opsc_plan_windows_host": ([P, I, P, P, P, P, W, D], C.c_int),
             "opsc_ctx_last_launches": ([P, P], C.c_int),
             "opsc_fp64_peak": ([I, P, P, P], C.c_int),
+            "opsc_candidate_probe": ([I, I, P, P, P], C.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

@@ -32,6 +32,34 @@ __global__ void fp64_peak_kernel(int iters, double seed, double* sink) {
   if (s == 12345.678) sink[blockIdx.x] = s;
 }
 
+// Candidate-loop probes: kind 1 = literal (DADD + DSETP + select) per
+// candidate, kind 2 = threshold form (DSETP + select) per candidate. Each
+// iteration evaluates 24 candidates against a register-resident menu.
+template <int KIND>
+__global__ void __launch_bounds__(256, 3) cand_probe_kernel(int iters, double seed, double* sink) {
+  double wj[24];
+#pragma unroll
+  for (int i = 0; i < 24; ++i) wj[i] = seed * (1.0 + 0.01 * i) + 1e-3 * threadIdx.x;
+  const double slo = seed * 1.2;
+  double bj = 1e-4 * (threadIdx.x & 7);
+  int acc = 0;
+  for (int it = 0; it < iters; ++it) {
+    int inner = 24;
+#pragma unroll
+    for (int i = 23; i >= 0; --i) {
+      if (KIND == 1) {
+        const double lat = bj + wj[i];
+        if (lat <= slo) inner = i;
+      } else {
+        if (wj[i] <= bj) inner = i;
+      }
+    }
+    acc += inner;
+    bj = bj + 1e-7;
+  }
+  if (acc == 12345) sink[blockIdx.x] = bj;
+}
+
 }  // namespace
 
 namespace opsc {
@@ -339,6 +367,38 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
   if (out.devices) CK(cudaMemcpyAsync(out.devices, c->devices, W * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
 #undef CK
+  return OPSC_OK;
+}
+
+int opsc_candidate_probe(int32_t kind, int32_t iters, float* ms, double* candidates, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  double* sink = nullptr;
+  if (cudaMalloc(&sink, 8192 * sizeof(double)) != cudaSuccess) return OPSC_ERR_CUDA;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int blocks = sms * 3 * 8;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  auto go = [&](int it) {
+    if (kind == 1) cand_probe_kernel<1><<<blocks, 256, 0, s>>>(it, 1.0, sink);
+    else cand_probe_kernel<2><<<blocks, 256, 0, s>>>(it, 1.0, sink);
+  };
+  go(iters / 10 + 1);
+  cudaEventRecord(a, s);
+  go(iters);
+  cudaEventRecord(b, s);
+  cudaEventSynchronize(b);
+  const cudaError_t e = cudaGetLastError();
+  float t = 0.0f;
+  cudaEventElapsedTime(&t, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  if (e != cudaSuccess) return OPSC_ERR_CUDA;
+  *ms = t;
+  *candidates = (double)blocks * 256.0 * (double)iters * 24.0;
   return OPSC_OK;
 }
 

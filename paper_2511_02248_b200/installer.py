@@ -1,0 +1,72 @@
+"""Reroute an installed reference planner (`opscaler`) onto the GPU search.
+
+The reference has no plugin registry: runner.plan_for_mode resolves
+`autoscaler.greedy_autoscale / model_level_autoscale / brute_force_autoscale`
+by module attribute at call time (runner.py:38-52), and the planners call
+each other by global name inside autoscaler.py (:352, :497, :771). Rebinding
+those module attributes therefore reroutes the CLI, runner.sweep and the
+greedy planner's uniform reseed without editing the reference.
+
+    import opscaler
+    from paper_2511_02248_b200 import install
+    install(opscaler)              # brute_force / model_level now run on the B200
+
+The wrappers accept the reference's own objects, return the reference's own
+ScalingPlan / OperatorConfig / PredictedSojourn instances and raise its own
+exception classes. `MAX_ENUMERATION` is read from opscaler.autoscaler at call
+time, as the reference does (autoscaler.py:735).
+"""
+
+from __future__ import annotations
+
+import functools
+import types
+
+from . import planners
+
+
+def _namespaces(pkg):
+    A = pkg.autoscaler
+    types_ns = types.SimpleNamespace(
+        OperatorConfig=A.OperatorConfig, PredictedSojourn=A.PredictedSojourn,
+        ScalingPlan=A.ScalingPlan, BruteForceBounds=A.BruteForceBounds)
+    err_ns = types.SimpleNamespace(
+        NoStableConfig=A.NoStableConfig, SearchSpaceTooLarge=A.SearchSpaceTooLarge,
+        Unstable=pkg.queueing.Unstable)
+    return types_ns, err_ns
+
+
+def install(pkg=None):
+    """Rebind the reference's planners to the GPU drop-ins; returns an
+    `uninstall` callable restoring the originals."""
+    if pkg is None:
+        import opscaler as pkg  # noqa: F811
+    A = pkg.autoscaler
+    T, E = _namespaces(pkg)
+    saved = {
+        (A, "brute_force_autoscale"): A.brute_force_autoscale,
+        (A, "model_level_autoscale"): A.model_level_autoscale,
+        (pkg, "brute_force_autoscale"): getattr(pkg, "brute_force_autoscale", None),
+        (pkg, "model_level_autoscale"): getattr(pkg, "model_level_autoscale", None),
+    }
+
+    @functools.wraps(saved[(A, "brute_force_autoscale")])
+    def brute_force_autoscale(dag, profiles, point, params, bounds=None):
+        return planners.brute_force_autoscale(
+            dag, profiles, point, params, bounds, types=T, err=E,
+            max_enumeration=A.MAX_ENUMERATION)
+
+    @functools.wraps(saved[(A, "model_level_autoscale")])
+    def model_level_autoscale(dag, profiles, point, params):
+        return planners.model_level_autoscale(dag, profiles, point, params, types=T, err=E)
+
+    for mod in (A, pkg):
+        mod.brute_force_autoscale = brute_force_autoscale
+        mod.model_level_autoscale = model_level_autoscale
+
+    def uninstall():
+        for (mod, name), fn in saved.items():
+            if fn is not None:
+                setattr(mod, name, fn)
+
+    return uninstall

@@ -178,3 +178,37 @@ def test_public_api_matches_per_point(nat):
     ml = planners.plan_windows(dag, prof, pts, params, "model")
     for p, plan in zip(pts, ml):
         assert planners.model_level_autoscale(dag, prof, p, params).to_dict() == plan.to_dict()
+
+
+def test_device_planner_matches_host_path(nat):
+    """The device-resident pipeline (bench `value`, multi-GPU path) and the
+    host-buffer C-ABI path produce identical decisions; 4 shards merged with
+    a MIN reduction equal 1 shard."""
+    import torch
+    from paper_2511_02248_b200 import device
+    for cfg, mode in (("cfg5", abi.MODE_ORACLE), ("cfg2", abi.MODE_ORACLE), ("cfg2", abi.MODE_MODEL)):
+        prob = tables.pack_problem(*scenarios.scenario(cfg))
+        grid = _grid(cfg, prob)
+        spec = tables.pack_model(prob, model.AutoscaleParams(slo=1.0))
+        win = _scenario_windows(cfg, "prefill", np.arange(0, 60, 7))
+        host = nat.plan_windows_host(mode, prob, win, grid=grid, model=spec)
+        p = device.DevicePlanner(prob, win, mode, grid=grid, model=spec)
+        p.step()
+        d1 = p.decisions()
+        for f in tables.DecisionArrays.FIELDS:
+            assert getattr(d1, f).tobytes() == getattr(host, f).tobytes(), (cfg, mode, f)
+        if mode == abi.MODE_ORACLE:
+            acc = {}
+
+            def merge(key):
+                acc.setdefault("k", torch.full_like(key, abi.KEY_INFEASIBLE))
+                acc["k"] = torch.minimum(acc["k"], key)
+
+            for sh in range(4):
+                p.step(sh, 4, allreduce=merge)
+            assert (acc["k"].cpu().numpy() == host.key).all()
+
+
+def test_smoke_entry():
+    import __graft_entry__
+    __graft_entry__.smoke()

@@ -40,3 +40,6 @@ nat.check(L.opsc_fp64_peak(20000, C.cast(C.byref(f), C.c_void_p), C.cast(C.byref
 print(f"fp64 DADD peak: {ops.value/f.value*1e3:.3e} op/s ({f.value:.2f} ms)")
 k = key.cpu().numpy()
 print("feasible windows", (k != abi.KEY_INFEASIBLE).sum())
+for kind, name in ((1, "literal DADD+DSETP+SEL"), (2, "threshold DSETP+SEL")):
+    nat.check(L.opsc_candidate_probe(kind, 20000, C.cast(C.byref(f), C.c_void_p), C.cast(C.byref(ops), C.c_void_p), s), "probe")
+    print(f"probe {name}: {ops.value/f.value*1e3:.3e} candidates/s ({f.value:.2f} ms)")
