@@ -45,10 +45,13 @@ class Problem:
         """UnknownPhase exactly when some operator's profile lacks `phase`
         (perfmodel.py:100-105), which the reference hits on the first
         predict_op of that operator."""
+        if phase not in PHASE_INDEX:
+            raise UnknownPhase(f"unknown phase {phase!r}")
         bit = self.table.has_phase[PHASE_INDEX[phase]]
         for v, op in enumerate(self.ids):
             if not (bit >> v) & 1:
                 prof = self.profiles.get(self.dag.node(op).profile_ref)
+                prof.latency_model(phase)  # raises the profile's own UnknownPhase
                 raise UnknownPhase(f"profile {prof.name} has no {phase} model")
 
 
