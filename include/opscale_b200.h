@@ -21,6 +21,7 @@
  *                             provisioned_memory (metrics.py:130-132) and
  *                             default_stream_place.devices_used
  *                             (placement.py:358-385, 465-491)
+ *   opsc_greedy            <- greedy_autoscale (autoscaler.py:334-589)
  *   opsc_plan_windows_host <- runner.plan_for_mode looped over windows
  *                             (runner.py:38-52, cli.py:135-150), host buffers in
  *                             and out, one call per batch of windows.
@@ -79,8 +80,19 @@ extern "C" {
 #define OPSC_W_IDLE 0x80u              /* qps <= 0: no plan (cli.py:138-144) */
 
 /* planning modes (runner.py:38-52) */
-#define OPSC_MODE_ORACLE 0 /* brute_force_autoscale, exhaustive */
-#define OPSC_MODE_MODEL 1  /* model_level_autoscale */
+#define OPSC_MODE_ORACLE 0   /* brute_force_autoscale, exhaustive */
+#define OPSC_MODE_MODEL 1    /* model_level_autoscale */
+#define OPSC_MODE_OPERATOR 2 /* greedy_autoscale (operator level, Alg. 1 as coded) */
+
+#define OPSC_W_NO_STABLE_INIT 0x100u    /* NoStableConfig from init_configs (autoscaler.py:289) in greedy mode */
+#define OPSC_W_TRACE_TRUNCATED 0x200u   /* more trace entries than trace_cap */
+
+/* greedy trace actions (autoscaler.py:363, 446-454, 478-486, 549-557, 579-587) */
+#define OPSC_ACT_UPSCALE 1
+#define OPSC_ACT_DOWNSCALE 2
+#define OPSC_ACT_HEADROOM 3
+#define OPSC_ACT_PRUNE 4
+#define OPSC_ACT_RESEED 5
 
 #define OPSC_KEY_INFEASIBLE 0x7fffffffffffffffLL
 #define OPSC_KEY_LEX_BITS 40
@@ -135,6 +147,27 @@ typedef struct OpscModelSpec {
   int32_t r_cap;
 } OpscModelSpec;
 
+/* Greedy operator-level planner knobs (AutoscaleParams, autoscaler.py:102-131).
+ * The uniform reseed (autoscaler.py:357-367, 492-500) uses `model`. */
+typedef struct OpscGreedySpec {
+  int32_t n_p[OPSC_MAX_OPS];
+  int32_t p_vals[OPSC_MAX_OPS][OPSC_MAX_P]; /* params.parallelism_for(op): sorted, duplicates kept */
+  int32_t b_max[OPSC_MAX_OPS];
+  int32_t r_cap;
+  int32_t max_iterations;
+  int32_t prune_excess_replicas;
+  OpscModelSpec model;
+} OpscGreedySpec;
+
+/* One accepted greedy move (ScalingPlan.trace entry). */
+typedef struct OpscTraceEntry {
+  double latency;     /* trial latency (reseed: unused)        */
+  int32_t objective;  /* objective after the move               */
+  int16_t to_r, to_b, to_p;
+  int8_t op;          /* lex rank; -1 for reseed_uniform        */
+  uint8_t action;     /* OPSC_ACT_*                              */
+} OpscTraceEntry;
+
 /* Default-stream placement + energy inputs (placement.py:465-491, metrics.py:34-47). */
 typedef struct OpscPlaceSpec {
   int32_t n_devices;     /* fleet size; devices in sorted-id order */
@@ -168,6 +201,9 @@ typedef struct OpscDecisions {
   double* energy;     /* [W] request_energy under default-stream placement   */
   double* memory;     /* [W] provisioned_memory under default-stream placement */
   int32_t* devices;   /* [W] devices_used under default-stream placement     */
+  int32_t trace_cap;  /* entries per window in `trace` (operator mode)       */
+  int32_t* trace_len; /* [W] number of moves (may exceed trace_cap)          */
+  OpscTraceEntry* trace; /* [W][trace_cap]                                   */
 } OpscDecisions;
 
 /* ---- library info ---- */
@@ -220,6 +256,16 @@ OPSC_API int opsc_model_grid(const OpscDag* dag, const OpscModelSpec* spec, Opsc
 OPSC_API int opsc_materialize(const OpscDag* dag, OpscWindows win, int32_t config_order,
                      const OpscPlaceSpec* place, OpscDecisions out, void* stream);
 
+/* greedy_autoscale per window (autoscaler.py:334-589): init_configs, the
+ * bottleneck up/downscale loop, uniform reseed + prune, headroom restore and
+ * the optional prune pass. uniform_cfg / uniform_feasible / uniform_status are
+ * opsc_model_grid's outputs for the same windows (_uniform_optimum, :492-500).
+ * Writes out.cfg (lex-rank order), out.feasible, out.status
+ * (OPSC_W_NO_STABLE_INIT), out.trace_len and out.trace. */
+OPSC_API int opsc_greedy(const OpscDag* dag, const OpscGreedySpec* spec, OpscWindows win,
+                         const int16_t* uniform_cfg, const uint8_t* uniform_feasible,
+                         const uint32_t* uniform_status, OpscDecisions out, void* stream);
+
 /* ---- host-buffer path: one call plans a batch of windows end to end ---- */
 typedef struct OpscContext OpscContext;
 
@@ -230,8 +276,8 @@ OPSC_API int opsc_ctx_destroy(OpscContext* ctx);
  * kernels on the context stream, copies out, synchronises. */
 OPSC_API int opsc_plan_windows_host(OpscContext* ctx, int32_t mode, const OpscDag* dag,
                            const OpscGrid* grid, const OpscModelSpec* model,
-                           const OpscPlaceSpec* place, OpscWindows win,
-                           OpscDecisions out);
+                           const OpscGreedySpec* greedy, const OpscPlaceSpec* place,
+                           OpscWindows win, OpscDecisions out);
 
 /* Number of kernels the last opsc_plan_windows_host call launched. */
 OPSC_API int opsc_ctx_last_launches(const OpscContext* ctx, int32_t* launches);

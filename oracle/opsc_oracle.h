@@ -56,10 +56,16 @@ int orc_model_grid(const OpscDag* dag, const OpscModelSpec* spec, OpscWindows wi
 int orc_materialize(const OpscDag* dag, OpscWindows win, int32_t config_order,
                     const OpscPlaceSpec* place, OpscDecisions out, int32_t n_threads);
 
+/* greedy_autoscale (opsc_oracle_greedy.c); uniform_* = orc_model_grid outputs. */
+int orc_greedy(const OpscDag* dag, const OpscGreedySpec* spec, OpscWindows win,
+               const int16_t* uniform_cfg, const uint8_t* uniform_feasible,
+               const uint32_t* uniform_status, OpscDecisions out, int32_t n_threads);
+
 /* Whole pipeline of one planning mode over a batch of windows. */
 int orc_plan_windows(int32_t mode, const OpscDag* dag, const OpscGrid* grid,
-                     const OpscModelSpec* model, const OpscPlaceSpec* place,
-                     OpscWindows win, OpscDecisions out, int32_t n_threads);
+                     const OpscModelSpec* model, const OpscGreedySpec* greedy,
+                     const OpscPlaceSpec* place, OpscWindows win, OpscDecisions out,
+                     int32_t n_threads);
 
 #ifdef __cplusplus
 }

@@ -58,10 +58,11 @@ def lib():
         L.orc_decode_decisions.argtypes = [P, P, I, P, P, P, P, P]
         L.orc_model_grid.argtypes = [P, P, abi.OpscWindows, P, P, P, I]
         L.orc_materialize.argtypes = [P, abi.OpscWindows, I, P, abi.OpscDecisions, I]
-        L.orc_plan_windows.argtypes = [I, P, P, P, P, abi.OpscWindows, abi.OpscDecisions, I]
+        L.orc_plan_windows.argtypes = [I, P, P, P, P, P, abi.OpscWindows, abi.OpscDecisions, I]
+        L.orc_greedy.argtypes = [P, P, abi.OpscWindows, P, P, P, abi.OpscDecisions, I]
         for f in ("orc_menu_build", "orc_stability_check", "orc_compose_argmin",
                   "orc_menu_fallback", "orc_decode_decisions", "orc_model_grid",
-                  "orc_materialize", "orc_plan_windows"):
+                  "orc_materialize", "orc_plan_windows", "orc_greedy"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -75,13 +76,16 @@ def ref(x):
     return C.cast(C.byref(x), C.c_void_p)
 
 
-def plan_windows(mode, problem, windows, grid=None, model=None, place=None, n_threads=None):
+def plan_windows(mode, problem, windows, grid=None, model=None, place=None, n_threads=None,
+                 greedy=None, trace_cap=4096):
     """Whole pipeline (menus -> argmin -> decode -> materialise) on the CPU."""
     place = place or tables.pack_place()
-    out = tables.DecisionArrays(windows.n, problem.n_ops)
+    out = tables.DecisionArrays(windows.n, problem.n_ops,
+                                trace_cap if mode == abi.MODE_OPERATOR else 0)
     g = grid if grid is not None else abi.OpscGrid()
     m = model if model is not None else abi.OpscModelSpec()
-    rc = lib().orc_plan_windows(mode, ref(problem.table), ref(g), ref(m), ref(place.spec),
+    gs = greedy if greedy is not None else abi.OpscGreedySpec()
+    rc = lib().orc_plan_windows(mode, ref(problem.table), ref(g), ref(m), ref(gs), ref(place.spec),
                                 windows.struct(), out.struct(), n_threads or threads())
     if rc != abi.OK:
         raise RuntimeError(f"oracle status {rc}")

@@ -31,7 +31,7 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # planners pull in the native loader; keep package import CPU-safe
-    if name in ("brute_force_autoscale", "model_level_autoscale", "plan_windows",
+    if name in ("brute_force_autoscale", "model_level_autoscale", "greedy_autoscale", "plan_windows",
                 "decide_windows", "MAX_ENUMERATION"):
         from . import planners
         return getattr(planners, name)

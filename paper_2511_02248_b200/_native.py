@@ -24,7 +24,7 @@ EXPORTS = (
     "opsc_menu_fallback",
     "opsc_decode_decisions", "opsc_model_grid", "opsc_materialize", "opsc_ctx_create",
     "opsc_ctx_destroy", "opsc_plan_windows_host", "opsc_ctx_last_launches", "opsc_fp64_peak",
-    "opsc_candidate_probe",
+    "opsc_candidate_probe", "opsc_greedy",
 )
 
 _lib = None
@@ -59,7 +59,8 @@ def load():
             "opsc_materialize": ([P, W, I, P, D, P], C.c_int),
             "opsc_ctx_create": ([I, I, P], C.c_int),
             "opsc_ctx_destroy": ([P], C.c_int),
-            "opsc_plan_windows_host": ([P, I, P, P, P, P, W, D], C.c_int),
+            "opsc_plan_windows_host": ([P, I, P, P, P, P, P, W, D], C.c_int),
+            "opsc_greedy": ([P, P, W, P, P, P, D, P], C.c_int),
             "opsc_ctx_last_launches": ([P, P], C.c_int),
             "opsc_fp64_peak": ([I, P, P, P], C.c_int),
             "opsc_candidate_probe": ([I, I, P, P, P], C.c_int),
@@ -125,13 +126,18 @@ class Context:
         check(load().opsc_ctx_last_launches(self._p, C.cast(C.byref(n), C.c_void_p)), "launches")
         return n.value
 
-    def plan_windows(self, mode, problem, windows, grid=None, model=None, place=None, out=None):
+    def plan_windows(self, mode, problem, windows, grid=None, model=None, place=None, out=None,
+                     greedy=None, trace_cap=4096):
         place = place or tables.pack_place()
-        out = out if out is not None else tables.DecisionArrays(windows.n, problem.n_ops)
+        if out is None:
+            out = tables.DecisionArrays(windows.n, problem.n_ops,
+                                        trace_cap if mode == abi.MODE_OPERATOR else 0)
         g = grid if grid is not None else abi.OpscGrid()
         m = model if model is not None else abi.OpscModelSpec()
+        gs = greedy if greedy is not None else abi.OpscGreedySpec()
         rc = load().opsc_plan_windows_host(self._p, mode, ref(problem.table), ref(g), ref(m),
-                                           ref(place.spec), windows.struct(), out.struct())
+                                           ref(gs), ref(place.spec), windows.struct(),
+                                           out.struct())
         check(rc, "opsc_plan_windows_host")
         return out
 
@@ -145,5 +151,7 @@ def context():
     return ctx
 
 
-def plan_windows_host(mode, problem, windows, grid=None, model=None, place=None):
-    return context().plan_windows(mode, problem, windows, grid=grid, model=model, place=place)
+def plan_windows_host(mode, problem, windows, grid=None, model=None, place=None, greedy=None,
+                      trace_cap=4096):
+    return context().plan_windows(mode, problem, windows, grid=grid, model=model, place=place,
+                                  greedy=greedy, trace_cap=trace_cap)

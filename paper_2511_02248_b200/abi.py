@@ -23,9 +23,15 @@ W_UNSTABLE_ROUNDING = 0x10
 W_FLEET_EXHAUSTED = 0x20
 W_INFEASIBLE_PLACEMENT = 0x40
 W_IDLE = 0x80
+W_NO_STABLE_INIT = 0x100
+W_TRACE_TRUNCATED = 0x200
+
+ACT_UPSCALE, ACT_DOWNSCALE, ACT_HEADROOM, ACT_PRUNE, ACT_RESEED = 1, 2, 3, 4, 5
+ACTION_NAMES = {1: "upscale", 2: "downscale", 3: "headroom", 4: "prune", 5: "reseed_uniform"}
 
 MODE_ORACLE = 0
 MODE_MODEL = 1
+MODE_OPERATOR = 2
 
 KEY_INFEASIBLE = 0x7FFFFFFFFFFFFFFF
 KEY_LEX_BITS = 40
@@ -63,6 +69,17 @@ class OpscModelSpec(C.Structure):
     _fields_ = [("p_base", _I * MAX_OPS), ("b_cap", _I), ("r_cap", _I)]
 
 
+class OpscGreedySpec(C.Structure):
+    _fields_ = [("n_p", _I * MAX_OPS), ("p_vals", (_I * MAX_P) * MAX_OPS),
+                ("b_max", _I * MAX_OPS), ("r_cap", _I), ("max_iterations", _I),
+                ("prune_excess_replicas", _I), ("model", OpscModelSpec)]
+
+
+class OpscTraceEntry(C.Structure):
+    _fields_ = [("latency", _D), ("objective", _I), ("to_r", C.c_int16), ("to_b", C.c_int16),
+                ("to_p", C.c_int16), ("op", C.c_int8), ("action", C.c_uint8)]
+
+
 class OpscPlaceSpec(C.Structure):
     _fields_ = [("n_devices", _I), ("uniform_cap", _I), ("alpha", _D), ("beta", _D),
                 ("mem_cap", C.c_void_p)]
@@ -76,4 +93,5 @@ class OpscWindows(C.Structure):
 class OpscDecisions(C.Structure):
     _fields_ = [(name, C.c_void_p) for name in (
         "key", "cfg", "feasible", "status", "latency", "objective", "path",
-        "pred", "stable", "energy", "memory", "devices")]
+        "pred", "stable", "energy", "memory", "devices")] + [
+        ("trace_cap", _I), ("trace_len", C.c_void_p), ("trace", C.c_void_p)]

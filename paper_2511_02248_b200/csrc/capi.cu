@@ -96,6 +96,13 @@ struct OpscContext {
   double *latency = nullptr, *pred = nullptr, *energy = nullptr, *memory = nullptr;
   int32_t *objective = nullptr, *devices = nullptr;
   int8_t* path = nullptr;
+  // operator mode: uniform reseed inputs and the move trace
+  int16_t* u_cfg = nullptr;
+  uint8_t* u_feas = nullptr;
+  uint32_t* u_status = nullptr;
+  int32_t* trace_len = nullptr;
+  OpscTraceEntry* trace = nullptr;
+  size_t cap_trace = 0;
 };
 
 namespace {
@@ -107,7 +114,7 @@ cudaError_t regrow(T*& p, size_t n) {
   return cudaMalloc((void**)&p, n * sizeof(T) > 0 ? n * sizeof(T) : sizeof(T));
 }
 
-int ensure(OpscContext* c, size_t W, size_t E, size_t n, size_t ndev) {
+int ensure(OpscContext* c, size_t W, size_t E, size_t n, size_t ndev, size_t trace_cap = 0) {
   cudaError_t e = cudaSuccess;
   if (W > c->cap_w || n > c->cap_n) {
     const size_t w2 = W > c->cap_w ? W : c->cap_w, n2 = n > c->cap_n ? n : c->cap_n;
@@ -117,8 +124,11 @@ int ensure(OpscContext* c, size_t W, size_t E, size_t n, size_t ndev) {
         (e = regrow(c->objective, w2)) || (e = regrow(c->energy, w2)) || (e = regrow(c->memory, w2)) ||
         (e = regrow(c->devices, w2)) || (e = regrow(c->cfg, w2 * n2 * 3)) ||
         (e = regrow(c->stable, w2 * n2)) || (e = regrow(c->path, w2 * n2)) ||
-        (e = regrow(c->pred, w2 * n2 * OPSC_PRED_FIELDS)) || (e = regrow(c->fb, w2 * n2)))
+        (e = regrow(c->pred, w2 * n2 * OPSC_PRED_FIELDS)) || (e = regrow(c->fb, w2 * n2)) ||
+        (e = regrow(c->u_cfg, w2 * n2 * 3)) || (e = regrow(c->u_feas, w2)) ||
+        (e = regrow(c->u_status, w2)) || (e = regrow(c->trace_len, w2)))
       return from_cuda(e);
+    c->cap_trace = 0;
     c->cap_w = w2;
     c->cap_n = n2;
     c->cap_e = 0;  // menu depends on W too
@@ -130,6 +140,10 @@ int ensure(OpscContext* c, size_t W, size_t E, size_t n, size_t ndev) {
   if (ndev > c->cap_dev) {
     if ((e = regrow(c->mem_cap, ndev))) return from_cuda(e);
     c->cap_dev = ndev;
+  }
+  if (W * trace_cap > c->cap_trace) {
+    if ((e = regrow(c->trace, W * trace_cap))) return from_cuda(e);
+    c->cap_trace = W * trace_cap;
   }
   return OPSC_OK;
 }
@@ -159,6 +173,9 @@ OpscDecisions dev_decisions(const OpscContext* c) {
   d.energy = c->energy;
   d.memory = c->memory;
   d.devices = c->devices;
+  d.trace_cap = 0;
+  d.trace_len = c->trace_len;
+  d.trace = c->trace;
   return d;
 }
 
@@ -285,7 +302,8 @@ int opsc_ctx_destroy(OpscContext* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   void* ptrs[] = {c->qps, c->slo, c->eps, c->seq_len, c->phase, c->menu, c->fb, c->mem_cap, c->key,
                   c->cfg, c->feasible, c->stable, c->status, c->latency, c->pred, c->energy,
-                  c->memory, c->objective, c->devices, c->path};
+                  c->memory, c->objective, c->devices, c->path, c->u_cfg, c->u_feas,
+                  c->u_status, c->trace_len, c->trace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -299,19 +317,29 @@ int opsc_ctx_last_launches(const OpscContext* c, int32_t* launches) {
   return OPSC_OK;
 }
 
+int opsc_greedy(const OpscDag* dag, const OpscGreedySpec* spec, OpscWindows win, const int16_t* uniform_cfg,
+                const uint8_t* uniform_feasible, const uint32_t* uniform_status, OpscDecisions out,
+                void* stream) {
+  if (!valid_dag(dag) || !spec || !out.trace_len || (out.trace_cap > 0 && !out.trace)) return OPSC_ERR_ARG;
+  return from_cuda(launch_greedy(*dag, *spec, win, uniform_cfg, uniform_feasible, uniform_status, out,
+                                 (cudaStream_t)stream));
+}
+
 int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, const OpscGrid* grid,
-                           const OpscModelSpec* model, const OpscPlaceSpec* place, OpscWindows win,
-                           OpscDecisions out) {
+                           const OpscModelSpec* model, const OpscGreedySpec* greedy,
+                           const OpscPlaceSpec* place, OpscWindows win, OpscDecisions out) {
   if (!c || !valid_dag(dag) || !place || win.n < 0) return OPSC_ERR_ARG;
   if (mode == OPSC_MODE_ORACLE && !grid) return OPSC_ERR_ARG;
   if (mode == OPSC_MODE_MODEL && !model) return OPSC_ERR_ARG;
-  if (mode != OPSC_MODE_ORACLE && mode != OPSC_MODE_MODEL) return OPSC_ERR_ARG;
+  if (mode == OPSC_MODE_OPERATOR && !greedy) return OPSC_ERR_ARG;
+  if (mode != OPSC_MODE_ORACLE && mode != OPSC_MODE_MODEL && mode != OPSC_MODE_OPERATOR) return OPSC_ERR_ARG;
+  const size_t tcap = mode == OPSC_MODE_OPERATOR && out.trace_cap > 0 ? (size_t)out.trace_cap : 0;
   cudaSetDevice(c->device);
   const int W = win.n, n = dag->n_ops;
   if (W == 0) return OPSC_OK;
   const size_t E = mode == OPSC_MODE_ORACLE ? (size_t)grid->menu_off[n] : 0;
   const size_t ndev = place->uniform_cap ? 1 : (size_t)place->n_devices;
-  int rc = ensure(c, W, E, n, ndev);
+  int rc = ensure(c, W, E, n, ndev, tcap);
   if (rc) return rc;
   cudaStream_t s = c->stream;
   c->launches = 0;
@@ -346,10 +374,19 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
     CK(launch_decode(*dag, *grid, W, c->key, c->fb, c->cfg, c->feasible, c->status, s));
     c->launches += 5;
     CK(launch_materialize(*dag, dw, 0, dplace, dev_decisions(c), s));
-  } else {
+  } else if (mode == OPSC_MODE_MODEL) {
     CK(launch_model_grid(*dag, *model, dw, c->cfg, c->feasible, c->status, s));
     c->launches += 1;
     CK(launch_materialize(*dag, dw, 1, dplace, dev_decisions(c), s));
+  } else {
+    // _uniform_optimum = model_level_autoscale on the same windows (autoscaler.py:492-500)
+    CK(launch_init(W, c->qps, c->u_status, nullptr, c->u_feas, s));
+    CK(launch_model_grid(*dag, greedy->model, dw, c->u_cfg, c->u_feas, c->u_status, s));
+    OpscDecisions dd = dev_decisions(c);
+    dd.trace_cap = (int32_t)tcap;
+    CK(launch_greedy(*dag, *greedy, dw, c->u_cfg, c->u_feas, c->u_status, dd, s));
+    c->launches += 3;
+    CK(launch_materialize(*dag, dw, 1, dplace, dd, s));
   }
   c->launches++;
   const size_t wn = (size_t)W * n;
@@ -365,6 +402,10 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
   if (out.energy) CK(cudaMemcpyAsync(out.energy, c->energy, W * sizeof(double), cudaMemcpyDeviceToHost, s));
   if (out.memory) CK(cudaMemcpyAsync(out.memory, c->memory, W * sizeof(double), cudaMemcpyDeviceToHost, s));
   if (out.devices) CK(cudaMemcpyAsync(out.devices, c->devices, W * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  if (tcap && out.trace_len)
+    CK(cudaMemcpyAsync(out.trace_len, c->trace_len, W * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  if (tcap && out.trace)
+    CK(cudaMemcpyAsync(out.trace, c->trace, W * tcap * sizeof(OpscTraceEntry), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
 #undef CK
   return OPSC_OK;

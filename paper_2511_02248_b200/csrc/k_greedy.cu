@@ -1,0 +1,533 @@
+// k_greedy.cu -- K5: greedy_autoscale (operator-level planner) on the device.
+//
+// One CTA per window runs the reference's sequential algorithm
+// (autoscaler.py:334-589) with the data-parallel parts spread over threads:
+//   * init_configs (:254-294): (op, B) pairs in parallel per parallelism rank;
+//   * every upscale / downscale / headroom step evaluates its whole move set
+//     (all distinct (B, P) at R +- 1 for the bottleneck operator, :306-331) in
+//     parallel -- one thread per move: predict_op for the moved operator and
+//     the critical-path DP with that operator's weight replaced;
+//   * thread 0 applies the reference's selection keys in move order and
+//     recomputes the critical path (with its lexicographic tie-break) for the
+//     bottleneck of the next step; the prune pass is sequential as in :562-589.
+// The uniform reseed uses K3's model-level result for the same window.
+#include "opsc_common.cuh"
+
+namespace opsc {
+
+constexpr int kGreedyThreads = 128;
+constexpr int kMaxMoves = 32 * OPSC_MAX_P * 2;  // b_max <= 64 per op in this kernel
+
+struct GreedyArgs {
+  OpscDag d;
+  OpscGreedySpec s;
+};
+
+struct GShared {
+  int p[OPSC_MAX_OPS], r[OPSC_MAX_OPS], b[OPSC_MAX_OPS];
+  double soj[OPSC_MAX_OPS], wt[OPSC_MAX_OPS];
+  int8_t path[OPSC_MAX_OPS];
+  double lat;
+  int stable;
+  // move results
+  double m_lat[kMaxMoves], m_soj[kMaxMoves], m_wt[kMaxMoves];
+  uint8_t m_ok[kMaxMoves];
+  // init scratch
+  double i_soj[OPSC_MAX_OPS][64];
+  int i_r[OPSC_MAX_OPS][64];
+  int chosen[OPSC_MAX_OPS];
+  // control
+  int op, applied, flag;
+  int np_d[OPSC_MAX_OPS];
+  int pd[OPSC_MAX_OPS][OPSC_MAX_P];
+  uint32_t st;
+  int trace_len;
+};
+
+__device__ double crit_path(const OpscDag& d, const double* wt, int8_t* path_out);
+
+// critical path with the reference's lexicographic path tie-break (opgraph.py:223-244)
+__device__ double crit_path(const OpscDag& d, const double* wt, int8_t* path_out) {
+  const int n = d.n_ops;
+  double val[OPSC_MAX_OPS];
+  int8_t pth[OPSC_MAX_OPS][OPSC_MAX_OPS];
+  int plen[OPSC_MAX_OPS];
+  for (int i = 0; i < n; ++i) {
+    const int v = d.topo[i];
+    const uint32_t pm = d.pred_mask[v];
+    if (!pm) {
+      val[v] = wt[v];
+      pth[v][0] = (int8_t)v;
+      plen[v] = 1;
+      continue;
+    }
+    int cand = -1;
+    double cv = 0.0;
+    for (int p = 0; p < n; ++p) {
+      if (!(pm >> p & 1u)) continue;
+      const double ev = val[p] + wt[v];
+      bool take = cand < 0 || ev > cv;
+      if (!take && ev == cv) {
+        const int la = plen[p], lb = plen[cand], mn = la < lb ? la : lb;
+        int k = 0;
+        while (k < mn && pth[p][k] == pth[cand][k]) ++k;
+        if (k < mn) take = pth[p][k] < pth[cand][k];
+        else if (la < lb) take = (int8_t)v < pth[cand][la];
+        else if (lb < la) take = pth[p][lb] < (int8_t)v;
+      }
+      if (take) {
+        cand = p;
+        cv = ev;
+      }
+    }
+    val[v] = cv;
+    for (int k = 0; k < plen[cand]; ++k) pth[v][k] = pth[cand][k];
+    pth[v][plen[cand]] = (int8_t)v;
+    plen[v] = plen[cand] + 1;
+  }
+  int tv = -1;
+  double top = 0.0;
+  for (int s = 0; s < n; ++s) {
+    if (!(d.sink_mask >> s & 1u)) continue;
+    bool take = tv < 0 || val[s] > top;
+    if (!take && val[s] == top) {
+      const int la = plen[s], lb = plen[tv], mn = la < lb ? la : lb;
+      int k = 0;
+      while (k < mn && pth[s][k] == pth[tv][k]) ++k;
+      take = k < mn ? pth[s][k] < pth[tv][k] : la < lb;
+    }
+    if (take) {
+      tv = s;
+      top = val[s];
+    }
+  }
+  for (int i = 0; i < n; ++i) path_out[i] = i < plen[tv] ? pth[tv][i] : (int8_t)-1;
+  return top;
+}
+
+// latency of the current plan with op `v`'s weight replaced (value only)
+__device__ double trial_latency(const OpscDag& d, const double* wt, int v, double wv) {
+  double val[OPSC_MAX_OPS];
+  double top = 0.0;
+  for (int i = 0; i < d.n_ops; ++i) {
+    const int u = d.topo[i];
+    double in = 0.0;
+    uint32_t pm = d.pred_mask[u];
+    while (pm) {
+      const int p = __ffs(pm) - 1;
+      pm &= pm - 1;
+      in = fmax(in, val[p]);
+    }
+    val[u] = in + (u == v ? wv : wt[u]);
+    if (d.sink_mask >> u & 1u) top = fmax(top, val[u]);
+  }
+  return top;
+}
+
+__device__ int objective(const GShared& S, int n) {
+  int o = 0;
+  for (int v = 0; v < n; ++v) o += S.p[v] * S.r[v];
+  return o;
+}
+
+__device__ int bottleneck(const GShared& S, int n) {
+  int best = -1;
+  for (int i = 0; i < n && S.path[i] >= 0; ++i) {
+    const int v = S.path[i];
+    if (best < 0 || S.soj[v] > S.soj[best] || (S.soj[v] == S.soj[best] && v < best)) best = v;
+  }
+  return best;
+}
+
+__device__ void push_trace(GShared& S, const OpscDecisions& out, int w, int action, int op, int r,
+                           int b, int p, double lat, int obj) {
+  if (S.trace_len < out.trace_cap) {
+    OpscTraceEntry* t = out.trace + (size_t)w * out.trace_cap + S.trace_len;
+    t->latency = lat;
+    t->objective = obj;
+    t->to_r = (int16_t)r;
+    t->to_b = (int16_t)b;
+    t->to_p = (int16_t)p;
+    t->op = (int8_t)op;
+    t->action = (uint8_t)action;
+  }
+  S.trace_len++;
+}
+
+// full evaluation of the current configs (all threads; ends synchronised)
+__device__ void eval_full(GShared& S, const OpscDag& d, double qps, int L, int ph) {
+  __shared__ int s_unstable;
+  if (threadIdx.x == 0) s_unstable = 0;
+  __syncthreads();
+  for (int v = threadIdx.x; v < d.n_ops; v += blockDim.x) {
+    uint32_t st = 0;
+    const Pred o = predict(d, qps, L, ph, v, S.p[v], S.r[v], S.b[v], &st);
+    S.soj[v] = o.wait + o.service;
+    S.wt[v] = weight(o, d.layer_count[v]);
+    if (!o.stable) atomicOr(&s_unstable, 1);
+    if (st) atomicOr(&S.st, st);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    S.stable = !s_unstable;
+    if (S.stable) {
+      S.lat = crit_path(d, S.wt, S.path);
+    } else {
+      S.lat = OPSC_INF;
+      for (int i = 0; i < d.n_ops; ++i) S.path[i] = -1;
+    }
+  }
+  __syncthreads();
+}
+
+// Evaluate the move set of `op` at replica count r_new over B in [b_lo, b_max]
+// and all distinct P (all threads; ends synchronised).
+__device__ int eval_moves(GShared& S, const GreedyArgs& a, int op, int r_new, int b_lo, double qps, int L,
+                          int ph) {
+  const int np = S.np_d[op];
+  const int nb = a.s.b_max[op] - b_lo + 1;
+  const int M = nb * np;
+  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+    const int b = b_lo + m / np, p = S.pd[op][m % np];
+    uint32_t st = 0;
+    const Pred o = predict(a.d, qps, L, ph, op, p, r_new, b, &st);
+    S.m_ok[m] = o.stable;
+    if (o.stable) {
+      S.m_wt[m] = weight(o, a.d.layer_count[op]);
+      S.m_soj[m] = o.wait + o.service;
+      S.m_lat[m] = trial_latency(a.d, S.wt, op, S.m_wt[m]);
+    }
+    if (st) atomicOr(&S.st, st);
+  }
+  __syncthreads();
+  return M;
+}
+
+struct Pick {
+  int m;
+  double k0, k1;
+  int k2;
+};
+
+__device__ __forceinline__ bool pick_less(double k0, double k1, int k2, int b, int p, const Pick& y, int yb,
+                                          int yp) {
+  if (k0 != y.k0) return k0 < y.k0;
+  if (k1 != y.k1) return k1 < y.k1;
+  if (k2 != y.k2) return k2 < y.k2;
+  if (b != yb) return b < yb;
+  return p < yp;
+}
+
+// thread 0: apply move m of `op` (new r), recompute the critical path
+__device__ void apply_move(GShared& S, const OpscDag& d, int op, int m, int r_new, int b_lo) {
+  const int np = S.np_d[op];
+  S.p[op] = S.pd[op][m % np];
+  S.b[op] = b_lo + m / np;
+  S.r[op] = r_new;
+  S.wt[op] = S.m_wt[m];
+  S.soj[op] = S.m_soj[m];
+  S.lat = crit_path(d, S.wt, S.path);
+  S.stable = 1;
+}
+
+// One upscale step (greedy loop when headroom == false, _restore_headroom
+// otherwise). All threads; returns (via S.applied) whether a move was made.
+__device__ void upscale_step(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps,
+                             int L, int ph, double slo, double eps, bool headroom) {
+  if (threadIdx.x == 0) S.op = bottleneck(S, a.d.n_ops);
+  __syncthreads();
+  const int op = S.op;
+  const int cur_p = S.p[op], cur_r = S.r[op];
+  if (cur_r + 1 > a.s.r_cap) {
+    __syncthreads();
+    if (threadIdx.x == 0) S.applied = 0;
+    __syncthreads();
+    return;
+  }
+  const int M = eval_moves(S, a, op, cur_r + 1, 1, qps, L, ph);
+  if (threadIdx.x == 0) {
+    const int np = S.np_d[op];
+    const int base = objective(S, a.d.n_ops);
+    const double target = slo - eps;
+    Pick ach = {-1, 0, 0, 0}, ach2 = {-1, 0, 0, 0}, imp = {-1, 0, 0, 0};
+    int ab = 0, ap = 0, a2b = 0, a2p = 0, ib = 0, ip = 0;
+    for (int m = 0; m < M; ++m) {
+      if (!S.m_ok[m]) continue;
+      const int b = 1 + m / np, p = S.pd[op][m % np];
+      const double lat = S.m_lat[m];
+      const int obj = base - cur_p * cur_r + p * (cur_r + 1);
+      if (lat <= target && (ach.m < 0 || pick_less((double)obj, lat, 0, b, p, ach, ab, ap))) {
+        ach = {m, (double)obj, lat, 0}; ab = b; ap = p;
+      }
+      if (!headroom && lat <= slo && (ach2.m < 0 || pick_less((double)obj, lat, 0, b, p, ach2, a2b, a2p))) {
+        ach2 = {m, (double)obj, lat, 0}; a2b = b; a2p = p;
+      }
+      const bool improving = headroom ? lat < S.lat - 1e-9 * slo : lat < S.lat;
+      if (improving) {
+        const int dobj = obj - base;
+        const double cost = dobj >= 1 ? (double)dobj : 1e-9;
+        const double neg_eff = -((S.lat - lat) / cost);
+        const int k2 = headroom ? 0 : obj;
+        if (imp.m < 0 || pick_less(neg_eff, lat, k2, b, p, imp, ib, ip)) {
+          imp = {m, neg_eff, lat, k2}; ib = b; ip = p;
+        }
+      }
+    }
+    const int m = ach.m >= 0 ? ach.m : (!headroom && ach2.m >= 0) ? ach2.m : imp.m;
+    S.applied = m >= 0;
+    if (m >= 0) {
+      apply_move(S, a.d, op, m, cur_r + 1, 1);
+      push_trace(S, out, w, headroom ? OPSC_ACT_HEADROOM : OPSC_ACT_UPSCALE, op, S.r[op], S.b[op], S.p[op],
+                 S.lat, objective(S, a.d.n_ops));
+    }
+  }
+  __syncthreads();
+}
+
+__device__ void downscale_step(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps,
+                               int L, int ph, double slo, double eps) {
+  if (threadIdx.x == 0) S.op = bottleneck(S, a.d.n_ops);
+  __syncthreads();
+  const int op = S.op;
+  const int cur_p = S.p[op], cur_r = S.r[op], cur_b = S.b[op];
+  if (cur_r - 1 < 1) {
+    __syncthreads();
+    if (threadIdx.x == 0) S.applied = 0;
+    __syncthreads();
+    return;
+  }
+  const int M = eval_moves(S, a, op, cur_r - 1, cur_b, qps, L, ph);
+  if (threadIdx.x == 0) {
+    const int np = S.np_d[op];
+    const int base = objective(S, a.d.n_ops);
+    const double bound = slo - eps;
+    int best = -1, bo = 0, bb = 0, bp = 0;
+    for (int m = 0; m < M; ++m) {
+      if (!S.m_ok[m] || S.m_lat[m] > bound) continue;
+      const int b = cur_b + m / np, p = S.pd[op][m % np];
+      const int obj = base - cur_p * cur_r + p * (cur_r - 1);
+      if (obj >= base) continue;
+      if (best < 0 || obj < bo || (obj == bo && (b < bb || (b == bb && p < bp)))) {
+        best = m; bo = obj; bb = b; bp = p;
+      }
+    }
+    S.applied = best >= 0;
+    if (best >= 0) {
+      apply_move(S, a.d, op, best, cur_r - 1, cur_b);
+      push_trace(S, out, w, OPSC_ACT_DOWNSCALE, op, S.r[op], S.b[op], S.p[op], S.lat,
+                 objective(S, a.d.n_ops));
+    }
+  }
+  __syncthreads();
+}
+
+__device__ void greedy_loop(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps,
+                            int L, int ph, double slo, double eps) {
+  for (int it = 0; it < a.s.max_iterations; ++it) {
+    const double lat = S.lat;
+    if (lat > slo) {
+      upscale_step(S, a, out, w, qps, L, ph, slo, eps, false);
+    } else if (lat <= slo - eps) {
+      downscale_step(S, a, out, w, qps, L, ph, slo, eps);
+    } else {
+      break;
+    }
+    if (!S.applied) break;
+  }
+}
+
+// _prune_pass (thread 0; sequential by construction)
+__device__ void prune_pass(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps, int L,
+                           int ph, double target) {
+  if (threadIdx.x == 0) {
+    const OpscDag& d = a.d;
+    bool changed = true;
+    while (changed) {
+      changed = false;
+      for (int v = 0; v < d.n_ops; ++v) {
+        if (S.r[v] <= 1) continue;
+        uint32_t st = 0;
+        const Pred o = predict(d, qps, L, ph, v, S.p[v], S.r[v] - 1, S.b[v], &st);
+        S.st |= st;
+        if (!o.stable) continue;
+        const double wv = weight(o, d.layer_count[v]);
+        if (!(trial_latency(d, S.wt, v, wv) <= target)) continue;
+        S.r[v] -= 1;
+        S.wt[v] = wv;
+        S.soj[v] = o.wait + o.service;
+        S.lat = crit_path(d, S.wt, S.path);
+        push_trace(S, out, w, OPSC_ACT_PRUNE, v, S.r[v], S.b[v], S.p[v], S.lat, objective(S, d.n_ops));
+        changed = true;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
+    const __grid_constant__ GreedyArgs a, const __grid_constant__ OpscWindows win,
+    const int16_t* __restrict__ ucfg, const uint8_t* __restrict__ ufeas, const uint32_t* __restrict__ ustatus,
+    const __grid_constant__ OpscDecisions out) {
+  __shared__ GShared S;
+  const OpscDag& d = a.d;
+  const int n = d.n_ops;
+  const int w = blockIdx.x;
+  const double qps = win.qps[w];
+  if (threadIdx.x == 0) {
+    out.feasible[w] = 0;
+    out.trace_len[w] = 0;
+  }
+  for (int i = threadIdx.x; i < n * 3; i += blockDim.x) out.cfg[(size_t)w * n * 3 + i] = 0;
+  if (!(qps > 0.0)) return;
+  const int L = win.seq_len[w], ph = win.phase[w];
+  const double slo = win.slo[w], eps = win.eps[w];
+  if (threadIdx.x == 0) {
+    S.st = 0;
+    S.trace_len = 0;
+    for (int v = 0; v < n; ++v) {
+      int k = 0;
+      for (int i = 0; i < a.s.n_p[v]; ++i) {
+        bool dup = false;
+        for (int j = 0; j < k; ++j) dup |= S.pd[v][j] == a.s.p_vals[v][i];
+        if (!dup) S.pd[v][k++] = a.s.p_vals[v][i];
+      }
+      S.np_d[v] = k;
+      S.chosen[v] = 0;
+    }
+  }
+  __syncthreads();
+
+  // ---- init_configs (:254-294): per parallelism rank, (op, B) pairs in parallel
+  int max_np = 0;
+  for (int v = 0; v < n; ++v) max_np = max(max_np, a.s.n_p[v]);
+  for (int pi = 0; pi < max_np; ++pi) {
+    for (int k = threadIdx.x; k < n * 64; k += blockDim.x) {
+      const int v = k / 64, b = k % 64 + 1;
+      if (S.chosen[v] || pi >= a.s.n_p[v] || b > a.s.b_max[v]) continue;
+      const int p = a.s.p_vals[v][pi];
+      const double t = op_latency(d, ph, v, b, L, p);
+      const double tl = t * (double)d.layer_count[v];
+      uint32_t st = 0;
+      if (tl == 0.0) st |= OPSC_W_ZERO_DIVISION;
+      const double mu = 1.0 / tl, lam = qps / (double)b;
+      const int r = strict_min_replicas(lam, mu, a.s.r_cap);
+      S.i_r[v][b - 1] = r;
+      if (r >= 0) {
+        const double util = lam / ((double)r * mu);
+        if (util >= 1.0 || util <= 0.0) st |= OPSC_W_UNSTABLE_ROUNDING;
+        S.i_soj[v][b - 1] = expected_wait(lam, mu, r) + t / (double)b;
+      }
+      if (st) atomicOr(&S.st, st);
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < n; v += blockDim.x) {
+      if (S.chosen[v] || pi >= a.s.n_p[v]) continue;
+      int bb = -1;
+      double bs = 0.0;
+      for (int b = 1; b <= a.s.b_max[v]; ++b) {
+        if (S.i_r[v][b - 1] < 0) continue;
+        if (bb < 0 || S.i_soj[v][b - 1] < bs) {
+          bb = b;
+          bs = S.i_soj[v][b - 1];
+        }
+      }
+      if (bb > 0) {
+        S.p[v] = a.s.p_vals[v][pi];
+        S.b[v] = bb;
+        S.r[v] = S.i_r[v][bb - 1];
+        S.chosen[v] = 1;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    S.flag = 1;
+    for (int v = 0; v < n; ++v) S.flag &= S.chosen[v];
+  }
+  __syncthreads();
+  if (!S.flag) {
+    if (threadIdx.x == 0) out.status[w] |= S.st | OPSC_W_NO_STABLE_INIT;
+    return;
+  }
+  eval_full(S, d, qps, L, ph);
+  greedy_loop(S, a, out, w, qps, L, ph, slo, eps);
+
+  // ---- uniform reseed (:357-367)
+  const uint32_t us = ustatus[w];
+  if (threadIdx.x == 0) S.st |= us & (OPSC_W_ZERO_DIVISION | OPSC_W_UNSTABLE_ROUNDING);
+  if (!(us & OPSC_W_NO_STABLE_MODEL) && ufeas[w]) {
+    __shared__ int keep_p[OPSC_MAX_OPS], keep_r[OPSC_MAX_OPS], keep_b[OPSC_MAX_OPS];
+    __shared__ double keep_soj[OPSC_MAX_OPS], keep_wt[OPSC_MAX_OPS], keep_lat;
+    __shared__ int8_t keep_path[OPSC_MAX_OPS];
+    __shared__ int reseed, base_obj;
+    if (threadIdx.x == 0) {
+      base_obj = objective(S, n);
+      int uobj = 0;
+      for (int v = 0; v < n; ++v) uobj += ucfg[((size_t)w * n + v) * 3] * ucfg[((size_t)w * n + v) * 3 + 1];
+      reseed = uobj < base_obj;
+      if (reseed) {
+        push_trace(S, out, w, OPSC_ACT_RESEED, -1, 0, 0, 0, 0.0, uobj);
+        for (int v = 0; v < n; ++v) {
+          keep_p[v] = S.p[v]; keep_r[v] = S.r[v]; keep_b[v] = S.b[v];
+          keep_soj[v] = S.soj[v]; keep_wt[v] = S.wt[v]; keep_path[v] = S.path[v];
+          S.p[v] = ucfg[((size_t)w * n + v) * 3];
+          S.r[v] = ucfg[((size_t)w * n + v) * 3 + 1];
+          S.b[v] = ucfg[((size_t)w * n + v) * 3 + 2];
+        }
+        keep_lat = S.lat;
+      }
+    }
+    __syncthreads();
+    if (reseed) {
+      eval_full(S, d, qps, L, ph);
+      prune_pass(S, a, out, w, qps, L, ph, slo - eps);
+      greedy_loop(S, a, out, w, qps, L, ph, slo, eps);
+      if (threadIdx.x == 0 && !(objective(S, n) < base_obj)) {
+        for (int v = 0; v < n; ++v) {
+          S.p[v] = keep_p[v]; S.r[v] = keep_r[v]; S.b[v] = keep_b[v];
+          S.soj[v] = keep_soj[v]; S.wt[v] = keep_wt[v]; S.path[v] = keep_path[v];
+        }
+        S.lat = keep_lat;
+        S.stable = 1;
+      }
+      __syncthreads();
+    }
+  }
+  // ---- headroom restore (:369-374, 503-559)
+  if (eps > 0 && S.lat <= slo) {
+    while (S.lat > slo - eps) {
+      upscale_step(S, a, out, w, qps, L, ph, slo, eps, true);
+      if (!S.applied) break;
+    }
+  }
+  // ---- optional prune (:376-377)
+  if (a.s.prune_excess_replicas && S.lat <= slo) prune_pass(S, a, out, w, qps, L, ph, slo - eps);
+
+  if (threadIdx.x == 0) {
+    out.feasible[w] = (uint8_t)(S.stable && S.lat <= slo);
+    for (int v = 0; v < n; ++v) {
+      int16_t* c = out.cfg + ((size_t)w * n + v) * 3;
+      c[0] = (int16_t)S.p[v];
+      c[1] = (int16_t)S.r[v];
+      c[2] = (int16_t)S.b[v];
+    }
+    out.trace_len[w] = S.trace_len;
+    uint32_t st = S.st;
+    if (S.trace_len > out.trace_cap) st |= OPSC_W_TRACE_TRUNCATED;
+    out.status[w] |= st;
+  }
+}
+
+cudaError_t launch_greedy(const OpscDag& d, const OpscGreedySpec& s, OpscWindows w, const int16_t* ucfg,
+                          const uint8_t* ufeas, const uint32_t* ustatus, OpscDecisions out, cudaStream_t st) {
+  if (w.n <= 0) return cudaSuccess;
+  for (int v = 0; v < d.n_ops; ++v)
+    if (s.b_max[v] < 1 || s.b_max[v] > 64 || s.n_p[v] < 1) return cudaErrorInvalidValue;
+  GreedyArgs a;
+  a.d = d;
+  a.s = s;
+  greedy_kernel<<<w.n, kGreedyThreads, 0, st>>>(a, w, ucfg, ufeas, ustatus, out);
+  return cudaGetLastError();
+}
+
+}  // namespace opsc

@@ -173,7 +173,8 @@ __global__ void __launch_bounds__(64) materialize_kernel(const __grid_constant__
     out.stable[(size_t)w * n + v] = 0;
     for (int f = 0; f < OPSC_PRED_FIELDS; ++f) out.pred[((size_t)w * n + v) * OPSC_PRED_FIELDS + f] = 0.0;
   }
-  if (st & (OPSC_W_IDLE | OPSC_W_NO_STABLE_BOUNDS | OPSC_W_NO_STABLE_PARAMS | OPSC_W_NO_STABLE_MODEL))
+  if (st & (OPSC_W_IDLE | OPSC_W_NO_STABLE_BOUNDS | OPSC_W_NO_STABLE_PARAMS | OPSC_W_NO_STABLE_MODEL |
+            OPSC_W_NO_STABLE_INIT))
     return;
   const int16_t* c = out.cfg + (size_t)w * n * 3;
   const double qps = win.qps[w];

@@ -183,4 +183,6 @@ cudaError_t launch_model_grid(const OpscDag& d, const OpscModelSpec& m, OpscWind
 cudaError_t launch_materialize(const OpscDag& d, OpscWindows w, int config_order,
                                const OpscPlaceSpec& p, OpscDecisions out, cudaStream_t s);
 cudaError_t launch_fp64_peak(int iters, double* sink, int* blocks, int* threads, cudaStream_t s);
+cudaError_t launch_greedy(const OpscDag& d, const OpscGreedySpec& s, OpscWindows w, const int16_t* ucfg,
+                          const uint8_t* ufeas, const uint32_t* ustatus, OpscDecisions out, cudaStream_t st);
 }  // namespace opsc

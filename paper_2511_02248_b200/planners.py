@@ -71,19 +71,32 @@ def model_level_autoscale(dag, profiles, point, params, *, fleet=None, energy=No
     return _run(abi.MODE_MODEL, problem, [point], params, None, fleet, energy, types, err).plan(0)
 
 
-def _run(mode, problem, points, params, bounds, fleet, energy, types, err):
+def greedy_autoscale(dag, profiles, point, params, *, fleet=None, energy=None, types=model,
+                     err=errors, trace_cap=4096):
+    """Greedy bottleneck-driven operator-level planner (Alg. 1 as the reference
+    codes it, autoscaler.py:334-589), one CTA per window on the device; the
+    returned plan carries the reference's move trace."""
+    _points_ok([point])
+    problem = tables.pack_problem(dag, profiles)
+    return _run(abi.MODE_OPERATOR, problem, [point], params, None, fleet, energy, types, err,
+                trace_cap).plan(0)
+
+
+def _run(mode, problem, points, params, bounds, fleet, energy, types, err, trace_cap=4096):
     phases = {p.phase for p in points}
     for ph in sorted(phases):
         problem.require_phase(ph)
     win = tables.pack_windows(points, params.slo, params.epsilon)
     grid = tables.pack_grid(problem, params, bounds) if mode == abi.MODE_ORACLE else None
     spec = tables.pack_model(problem, params) if mode == abi.MODE_MODEL else None
+    greedy = tables.pack_greedy(problem, params) if mode == abi.MODE_OPERATOR else None
     place = tables.pack_place(fleet, energy)
-    arrays = _native.plan_windows_host(mode, problem, win, grid=grid, model=spec, place=place)
+    arrays = _native.plan_windows_host(mode, problem, win, grid=grid, model=spec, place=place,
+                                       greedy=greedy, trace_cap=trace_cap)
     return WindowDecisions(problem, points, arrays, mode, types, err)
 
 
-_MODES = {"oracle": abi.MODE_ORACLE, "model": abi.MODE_MODEL}
+_MODES = {"oracle": abi.MODE_ORACLE, "model": abi.MODE_MODEL, "operator": abi.MODE_OPERATOR}
 
 
 def decide_windows(dag, profiles, points, params, mode="oracle", bounds=None, *,

@@ -30,6 +30,12 @@ def raise_for_status(status: int, mode: int, err=errors):
                 "arrival rate exceeds capacity at every (B, P) within r_cap")
         if status & abi.W_NO_STABLE_BOUNDS:
             raise err.NoStableConfig("operator has no stable configuration within bounds")
+    elif mode == abi.MODE_OPERATOR:
+        if status & abi.W_NO_STABLE_INIT:
+            raise err.NoStableConfig(
+                "arrival rate exceeds capacity at every (B, P) within r_cap")
+        if status & abi.W_TRACE_TRUNCATED:
+            raise RuntimeError("greedy move trace exceeded trace_cap; raise trace_cap")
     elif status & abi.W_NO_STABLE_MODEL:
         raise err.NoStableConfig(
             "model-level: arrival rate exceeds capacity at every batch size within r_cap")
@@ -81,7 +87,24 @@ class WindowDecisions:
         return T.ScalingPlan(
             configs=configs, predicted=predicted, iteration_latency=lat,
             critical_path=path, objective=int(a.objective[i]),
-            feasible=bool(a.feasible[i]), phase=self.points[i].phase, trace=[])
+            feasible=bool(a.feasible[i]), phase=self.points[i].phase, trace=self.trace(i))
+
+    def trace(self, i):
+        """ScalingPlan.trace of the greedy planner (autoscaler.py:363, 446-454,
+        478-486, 549-557, 579-587); empty for the other planners."""
+        a = self.arrays
+        if self.mode != abi.MODE_OPERATOR or not a.trace_cap:
+            return []
+        out = []
+        for t in a.trace[i, :min(int(a.trace_len[i]), a.trace_cap)]:
+            name = abi.ACTION_NAMES[int(t["action"])]
+            if name == "reseed_uniform":
+                out.append({"action": name, "objective": int(t["objective"])})
+            else:
+                out.append({"action": name, "op": self.problem.ids[int(t["op"])],
+                            "to": {"R": int(t["to_r"]), "B": int(t["to_b"]), "P": int(t["to_p"])},
+                            "latency": float(t["latency"]), "objective": int(t["objective"])})
+        return out
 
     def plans(self):
         return [self.plan(i) for i in range(len(self))]

@@ -161,6 +161,23 @@ def pack_model(problem: Problem, params) -> abi.OpscModelSpec:
     return s
 
 
+def pack_greedy(problem: Problem, params) -> abi.OpscGreedySpec:
+    """greedy_autoscale knobs (AutoscaleParams) + the model-level grid of its
+    uniform reseed (autoscaler.py:357-367)."""
+    s = abi.OpscGreedySpec()
+    for v, op in enumerate(problem.ids):
+        pv = _pset(params.parallelism_for(op))
+        s.n_p[v] = len(pv)
+        for i, p in enumerate(pv):
+            s.p_vals[v][i] = p
+        s.b_max[v] = int(params.b_max_for(op))
+    s.r_cap = int(params.r_cap)
+    s.max_iterations = int(getattr(params, "max_iterations", 10_000))
+    s.prune_excess_replicas = int(bool(getattr(params, "prune_excess_replicas", False)))
+    s.model = pack_model(problem, params)
+    return s
+
+
 @dataclass
 class PlaceInputs:
     spec: abi.OpscPlaceSpec
@@ -238,10 +255,16 @@ def window_arrays(qps, seq_len, phase, slo, eps=0.0) -> WindowArrays:
     )
 
 
+TRACE_DTYPE = np.dtype([("latency", "<f8"), ("objective", "<i4"), ("to_r", "<i2"),
+                        ("to_b", "<i2"), ("to_p", "<i2"), ("op", "i1"), ("action", "u1")],
+                       align=True)
+assert TRACE_DTYPE.itemsize == C.sizeof(abi.OpscTraceEntry)
+
+
 class DecisionArrays:
     """Host SoA of OpscDecisions for W windows x n ops."""
 
-    def __init__(self, n_windows, n_ops):
+    def __init__(self, n_windows, n_ops, trace_cap=0):
         W, n = n_windows, n_ops
         self.n_windows, self.n_ops = W, n
         self.key = np.full(W, abi.KEY_INFEASIBLE, dtype=np.int64)
@@ -256,6 +279,9 @@ class DecisionArrays:
         self.energy = np.zeros(W, dtype=np.float64)
         self.memory = np.zeros(W, dtype=np.float64)
         self.devices = np.zeros(W, dtype=np.int32)
+        self.trace_cap = int(trace_cap)
+        self.trace_len = np.zeros(W, dtype=np.int32)
+        self.trace = np.zeros((W, max(self.trace_cap, 1)), dtype=TRACE_DTYPE)
 
     FIELDS = ("key", "cfg", "feasible", "status", "latency", "objective", "path",
               "pred", "stable", "energy", "memory", "devices")
@@ -264,10 +290,14 @@ class DecisionArrays:
         d = abi.OpscDecisions()
         for f in self.FIELDS:
             setattr(d, f, getattr(self, f).ctypes.data)
+        d.trace_cap = self.trace_cap
+        d.trace_len = self.trace_len.ctypes.data
+        d.trace = self.trace.ctypes.data
         return d
 
     def nbytes(self):
-        return sum(getattr(self, f).nbytes for f in self.FIELDS)
+        n = sum(getattr(self, f).nbytes for f in self.FIELDS)
+        return n + (self.trace_len.nbytes + self.trace.nbytes if self.trace_cap else 0)
 
 
 def c_ptr(x):

@@ -155,6 +155,74 @@ def run_oracle(dag_spec, prof, point, params, bounds):
     return plan_json(plan), plan, dag, profiles
 
 
+def trace_json(trace):
+    out = []
+    for t in trace:
+        e = {"action": t["action"], "objective": int(t["objective"])}
+        if "op" in t:
+            e["op"] = t["op"]
+            e["to"] = [t["to"]["R"], t["to"]["B"], t["to"]["P"]]
+            e["latency"] = H(t["latency"])
+        out.append(e)
+    return out
+
+
+def run_greedy(dag_spec, prof, point, params):
+    dag, profiles = build(dag_spec, prof)
+    try:
+        plan = A.greedy_autoscale(dag, profiles, point, params)
+    except ref.OpscalerError as exc:
+        return {"error": type(exc).__name__}, None, dag, profiles
+    j = plan_json(plan)
+    j["trace"] = trace_json(plan.trace)
+    return j, plan, dag, profiles
+
+
+def greedy_cases():
+    cases = []
+    rng = np.random.default_rng(777)
+    for cfg, windows in (("cfg1", [0]), ("cfg2", list(range(0, 60, 2))),
+                         ("cfg3", list(range(0, 60, 6))), ("cfg5", list(range(0, 1440, 160)))):
+        dag_spec, prof = S.SCENARIOS[cfg]
+        tw = S.trace_windows(cfg)
+        for w in windows:
+            for ph in ("prefill", "decode"):
+                qps = float(tw[ph + "_qps"][w])
+                if qps <= 0:
+                    continue
+                kw = dict(slo=S.SLO[cfg][ph])
+                if w % 3 == 1:
+                    kw["epsilon"] = S.SLO[cfg][ph] * 0.1
+                if w % 4 == 2:
+                    kw["prune_excess_replicas"] = True
+                cases.append(dict(name=f"{cfg}/w{w}/{ph}", scenario=cfg,
+                                  point=dict(qps=qps, seq_len=int(tw[ph + "_len"][w]), phase=ph),
+                                  params=kw))
+    c7, p7 = S.SCENARIOS["cfg1"]
+    cases.append(dict(name="edge/greedy_nostable", scenario="cfg1",
+                      point=dict(qps=1e9, seq_len=2048, phase="prefill"), params=dict(slo=0.5)))
+    cases.append(dict(name="edge/greedy_infeasible", scenario="cfg1",
+                      point=dict(qps=20.0, seq_len=2048, phase="prefill"),
+                      params=dict(slo=1e-3, r_cap=16)))
+    cases.append(dict(name="edge/greedy_maxiter", scenario="cfg1",
+                      point=dict(qps=200.0, seq_len=2048, phase="prefill"),
+                      params=dict(slo=0.3, max_iterations=3)))
+    cases.append(dict(name="edge/greedy_dup_p", scenario="cfg1",
+                      point=dict(qps=60.0, seq_len=1024, phase="prefill"),
+                      params=dict(slo=0.4, parallelism=[1, 1, 2, 4], b_max=6, epsilon=0.04)))
+    for i in range(70):
+        shape, dag_spec, prof, phase, L, qps = random_instance(rng, i)
+        slo = float(10 ** rng.uniform(-2.5, 0.5))
+        kw = dict(slo=slo, epsilon=0.0 if rng.uniform() < 0.5 else slo * float(rng.uniform(0.01, 0.3)),
+                  b_max=int(rng.choice([1, 4, 8, 32])),
+                  parallelism=[1, 2, 4, 8] if rng.uniform() < 0.5 else [1, 2],
+                  r_cap=int(rng.choice([16, 64, 512])),
+                  prune_excess_replicas=bool(rng.uniform() < 0.3))
+        cases.append(dict(name=f"rand{i}/{shape}", dag=dag_spec, profiles=prof,
+                          point=dict(qps=qps, seq_len=L, phase=phase), params=kw))
+    return cases
+
+
 def run_model(dag_spec, prof, point, params):
     dag, profiles = build(dag_spec, prof)
     try:
@@ -166,7 +234,8 @@ def run_model(dag_spec, prof, point, params):
 
 def params_json(p):
     return {"slo": H(p.slo), "epsilon": H(p.epsilon), "b_max": p.b_max,
-            "parallelism": list(p.parallelism), "r_cap": p.r_cap}
+            "parallelism": list(p.parallelism), "r_cap": p.r_cap,
+            "max_iterations": p.max_iterations, "prune_excess_replicas": p.prune_excess_replicas}
 
 
 def point_json(pt):
@@ -442,6 +511,9 @@ def main():
     if "--decisions-only" in sys.argv:
         decisions_only()
         return
+    if "--greedy-only" in sys.argv:
+        write_greedy()
+        return
     os.makedirs(HERE, exist_ok=True)
     json.dump(kats(), open(os.path.join(HERE, "kats.json"), "w"), separators=(",", ":"))
     print("kats done")
@@ -493,6 +565,24 @@ def main():
     n_err = sum("error" in r["expected"] for r in model)
     n_feas = sum(r["expected"].get("feasible", False) for r in model)
     print(f"model: {len(model)} cases, {n_feas} feasible, {n_err} errors")
+    write_greedy()
+
+
+def write_greedy():
+    greedy = []
+    for c in greedy_cases():
+        dag_spec, prof, pt, params, _ = case_inputs(c)
+        j, plan, dag, profiles = run_greedy(dag_spec, prof, pt, params)
+        rec = serialise_case(c, pt, params, None)
+        rec["expected"] = j
+        if plan is not None:
+            rec["metrics"] = metrics_json(plan, dag, profiles, pt, 4096, 180e9)
+        greedy.append(rec)
+    json.dump(greedy, open(os.path.join(HERE, "greedy.json"), "w"), separators=(",", ":"))
+    n_err = sum("error" in r["expected"] for r in greedy)
+    n_feas = sum(r["expected"].get("feasible", False) for r in greedy)
+    n_tr = sum(len(r["expected"].get("trace", [])) for r in greedy)
+    print(f"greedy: {len(greedy)} cases, {n_feas} feasible, {n_err} errors, {n_tr} trace entries")
 
 
 if __name__ == "__main__":

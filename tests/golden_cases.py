@@ -33,7 +33,9 @@ def case_problem(c):
 def case_params(c):
     p = c["params"]
     return model.AutoscaleParams(slo=F(p["slo"]), epsilon=F(p["epsilon"]), b_max=p["b_max"],
-                                 parallelism=tuple(p["parallelism"]), r_cap=p["r_cap"])
+                                 parallelism=tuple(p["parallelism"]), r_cap=p["r_cap"],
+                                 max_iterations=p.get("max_iterations", 10_000),
+                                 prune_excess_replicas=p.get("prune_excess_replicas", False))
 
 
 def case_bounds(c):
@@ -78,6 +80,17 @@ def compare_plan(plan, exp, problem):
         errs.append(f"latency {plan.iteration_latency.hex()} != {exp['iteration_latency']}")
     if plan.critical_path != exp["critical_path"]:
         errs.append(f"path {plan.critical_path} != {exp['critical_path']}")
+    if "trace" in exp:
+        got_tr = []
+        for t in plan.trace:
+            e = {"action": t["action"], "objective": t["objective"]}
+            if "op" in t:
+                e["op"] = t["op"]
+                e["to"] = [t["to"]["R"], t["to"]["B"], t["to"]["P"]]
+                e["latency"] = t["latency"].hex()
+            got_tr.append(e)
+        if got_tr != exp["trace"]:
+            errs.append(f"trace {got_tr} != {exp['trace']}")
     for op, fields in exp["predicted"].items():
         p = plan.predicted[op]
         got = [p.op_latency.hex(), p.lam.hex(), p.mu.hex(), p.utilization.hex(),

@@ -212,3 +212,60 @@ def test_device_planner_matches_host_path(nat):
 def test_smoke_entry():
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+def test_golden_greedy_cases(nat):
+    """greedy_autoscale (operator mode) on the device == the reference's plans,
+    move traces and metrics, bit for bit."""
+    errs = []
+    for c in G.load("greedy.json"):
+        prob = G.case_problem(c)
+        params = G.case_params(c)
+        place = tables.pack_place(G.fleet_for("model_metrics"), model.EnergyParams())
+        out = nat.plan_windows_host(abi.MODE_OPERATOR, prob, G.case_windows(c),
+                                    greedy=tables.pack_greedy(prob, params), place=place)
+        dec = plans.WindowDecisions(prob, [G.case_point(c)], out, abi.MODE_OPERATOR)
+        exp = c["expected"]
+        if "error" in exp:
+            with pytest.raises(Exception) as ei:
+                dec.plan(0)
+            assert type(ei.value).__name__ == exp["error"], c["name"]
+            continue
+        e = G.compare_plan(dec.plan(0), exp, prob) + G.compare_metrics(dec.metrics(0), c.get("metrics"))
+        if e:
+            errs.append((c["name"], e))
+    assert not errs, errs[:3]
+
+
+def test_full_trace_greedy_vs_oracle(nat, orc):
+    """Every window of the cfg2 (70B) and cfg3 (multimodal) traces, both
+    phases, operator mode: device == CPU oracle on every field + trace."""
+    for cfg in ("cfg2", "cfg3"):
+        prob = tables.pack_problem(*scenarios.scenario(cfg))
+        tw = scenarios.trace_windows(cfg)
+        for phase in ("prefill", "decode"):
+            slo = scenarios.SLO[cfg][phase]
+            params = model.AutoscaleParams(slo=slo, epsilon=slo * 0.05)
+            win = tables.window_arrays(tw[phase + "_qps"], tw[phase + "_len"],
+                                       tables.PHASE_INDEX[phase], slo, slo * 0.05)
+            gs = tables.pack_greedy(prob, params)
+            gpu = nat.plan_windows_host(abi.MODE_OPERATOR, prob, win, greedy=gs)
+            cpu = orc.plan_windows(abi.MODE_OPERATOR, prob, win, greedy=gs)
+            for f in tables.DecisionArrays.FIELDS + ("trace_len",):
+                assert getattr(gpu, f).tobytes() == getattr(cpu, f).tobytes(), (cfg, phase, f)
+            for i in range(win.n):
+                k = min(int(cpu.trace_len[i]), cpu.trace_cap)
+                assert gpu.trace[i, :k].tobytes() == cpu.trace[i, :k].tobytes(), (cfg, phase, i)
+
+
+def test_public_greedy_api(nat):
+    from paper_2511_02248_b200 import planners
+    dag, prof = scenarios.scenario("cfg2")
+    tw = scenarios.trace_windows("cfg2")
+    pts = [model.WorkloadPoint(float(tw["prefill_qps"][i]), int(tw["prefill_len"][i]), "prefill")
+           for i in range(0, 60, 11)]
+    params = model.AutoscaleParams(slo=2.0)
+    batch = planners.plan_windows(dag, prof, pts, params, "operator")
+    for p, plan in zip(pts, batch):
+        assert planners.greedy_autoscale(dag, prof, p, params).to_dict() == plan.to_dict()
+        assert plan.trace  # the move trace travels with the plan

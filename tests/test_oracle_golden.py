@@ -145,3 +145,27 @@ def test_oracle_decisions(orc, idx):
 def test_model_decisions(orc, idx):
     c = G.load("model.json")[idx]
     _check_case(orc, c, abi.MODE_MODEL)
+
+
+def _check_greedy(orc, c):
+    prob = G.case_problem(c)
+    params = G.case_params(c)
+    win = G.case_windows(c)
+    place = tables.pack_place(G.fleet_for("model_metrics"), model.EnergyParams())
+    out = orc.plan_windows(abi.MODE_OPERATOR, prob, win, greedy=tables.pack_greedy(prob, params),
+                           place=place)
+    dec = plans.WindowDecisions(prob, [G.case_point(c)], out, abi.MODE_OPERATOR)
+    exp = c["expected"]
+    if "error" in exp:
+        with pytest.raises(Exception) as ei:
+            dec.plan(0)
+        assert type(ei.value).__name__ == exp["error"]
+        return
+    errs = G.compare_plan(dec.plan(0), exp, prob)
+    errs += G.compare_metrics(dec.metrics(0), c.get("metrics"))
+    assert not errs, (c["name"], errs)
+
+
+@pytest.mark.parametrize("idx", range(len(G.load("greedy.json"))))
+def test_greedy_decisions(orc, idx):
+    _check_greedy(orc, G.load("greedy.json")[idx])
