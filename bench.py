@@ -346,16 +346,31 @@ def decision_latency(dev):
     g = scenarios.GRIDS["cfg2"]
     tw = scenarios.trace_windows("cfg2")
     out = {}
-    for mode, name in ((abi.MODE_ORACLE, "oracle_6e7_candidates"), (abi.MODE_MODEL, "model_level")):
+    for mode, name in ((abi.MODE_ORACLE, "oracle_6e7_candidates"), (abi.MODE_MODEL, "model_level"),
+                       (abi.MODE_OPERATOR, "operator_greedy")):
         samples = []
+        batch_ms = 0.0
         for phase in ("prefill", "decode"):
             slo = scenarios.SLO["cfg2"][phase]
             params = model.AutoscaleParams(slo=slo)
             grid = tables.pack_grid(problem, params, model.BruteForceBounds(**g))
             spec = tables.pack_model(problem, params)
+            gspec = tables.pack_greedy(problem, params)
             qs, ls = tw[phase + "_qps"], tw[phase + "_len"]
+            # whole trace in one batch
+            allw = tables.window_arrays(qs, ls, tables.PHASE_INDEX[phase], slo)
+            pb = device.DevicePlanner(problem, allw, mode, grid=grid, model=spec, greedy=gspec,
+                                      device=dev)
+            pb.step()
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record()
+            pb.step()
+            b1.record()
+            b1.synchronize()
+            batch_ms += b0.elapsed_time(b1)
             one = tables.window_arrays(qs[:1], ls[:1], tables.PHASE_INDEX[phase], slo)
-            p = device.DevicePlanner(problem, one, mode, grid=grid, model=spec, device=dev)
+            p = device.DevicePlanner(problem, one, mode, grid=grid, model=spec, greedy=gspec,
+                                     device=dev)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             for i in range(len(qs)):
                 if not qs[i] > 0:
@@ -373,7 +388,8 @@ def decision_latency(dev):
         samples.sort()
         out[name] = {"median": statistics.median(samples),
                      "p99": samples[min(len(samples) - 1, int(0.99 * len(samples)))],
-                     "windows": len(samples)}
+                     "windows": len(samples),
+                     "batched_ms_per_window": batch_ms / max(1, len(samples))}
     out["dag"] = "cfg2 Llama-2-70B 10-op chain, 60 x 60 s windows x {prefill, decode}, W = 1"
     return out
 

@@ -21,10 +21,11 @@ from . import _native, abi, tables
 
 class DevicePlanner:
     def __init__(self, problem, windows: tables.WindowArrays, mode=abi.MODE_ORACLE, grid=None,
-                 model=None, place=None, device="cuda"):
+                 model=None, place=None, device="cuda", greedy=None, trace_cap=1024):
         self.problem, self.mode = problem, mode
         self.grid = grid if grid is not None else abi.OpscGrid()
         self.model = model if model is not None else abi.OpscModelSpec()
+        self.greedy = greedy if greedy is not None else abi.OpscGreedySpec()
         self.place = place or tables.pack_place()
         self.dev = torch.device(device)
         self.L = _native.load()
@@ -53,6 +54,16 @@ class DevicePlanner:
         self.out = abi.OpscDecisions()
         for k, t in self.out_t.items():
             setattr(self.out, k, t.data_ptr())
+        # operator mode: uniform reseed inputs + move trace
+        self.trace_cap = trace_cap if mode == abi.MODE_OPERATOR else 0
+        self.u_cfg = z(W, n, 3, dt=torch.int16)
+        self.u_feas = z(W, dt=torch.uint8)
+        self.u_status = z(W, dt=torch.int32)
+        self.trace_len = z(W, dt=torch.int32)
+        self.trace = z(max(W * self.trace_cap * tables.TRACE_DTYPE.itemsize, 1), dt=torch.uint8)
+        self.out.trace_cap = self.trace_cap
+        self.out.trace_len = self.trace_len.data_ptr()
+        self.out.trace = self.trace.data_ptr()
         caps = torch.from_numpy(self.place.mem_cap).to(self.dev)
         self._caps = caps
         self.dplace = abi.OpscPlaceSpec()
@@ -105,6 +116,18 @@ class DevicePlanner:
         self._ck(self.L.opsc_materialize(r(self.problem.table), self.win, order, r(self.dplace),
                                          self.out, s), "materialize")
 
+    def operator(self):
+        """greedy_autoscale: model-level reseed candidates, then the greedy kernel."""
+        r, s = _native.ref, self._s()
+        self._ck(self.L.opsc_init_windows(self.win, self.u_status.data_ptr(), None,
+                                          self.u_feas.data_ptr(), s), "init_windows")
+        self._ck(self.L.opsc_model_grid(r(self.problem.table), r(self.greedy.model), self.win,
+                                        self.u_cfg.data_ptr(), self.u_feas.data_ptr(),
+                                        self.u_status.data_ptr(), s), "model_grid")
+        self._ck(self.L.opsc_greedy(r(self.problem.table), r(self.greedy), self.win,
+                                    self.u_cfg.data_ptr(), self.u_feas.data_ptr(),
+                                    self.u_status.data_ptr(), self.out, s), "greedy")
+
     def model_grid(self):
         r = _native.ref
         self._ck(self.L.opsc_model_grid(r(self.problem.table), r(self.model), self.win,
@@ -124,16 +147,22 @@ class DevicePlanner:
                 compose_events[1].record()
             if allreduce is not None:
                 allreduce(self.key)
+        elif self.mode == abi.MODE_OPERATOR:
+            self.operator()
         else:
             self.model_grid()
         self.finish()
 
     def decisions(self) -> tables.DecisionArrays:
         torch.cuda.synchronize(self.dev)
-        out = tables.DecisionArrays(self.W, self.n)
+        out = tables.DecisionArrays(self.W, self.n, self.trace_cap)
         for k, t in self.out_t.items():
             getattr(out, k)[...] = t.cpu().numpy().astype(getattr(out, k).dtype).reshape(
                 getattr(out, k).shape)
+        if self.trace_cap:
+            out.trace_len[...] = self.trace_len.cpu().numpy()
+            out.trace[...] = self.trace.cpu().numpy().view(tables.TRACE_DTYPE).reshape(
+                self.W, self.trace_cap)
         return out
 
 

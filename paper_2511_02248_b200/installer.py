@@ -4,12 +4,13 @@ The reference has no plugin registry: runner.plan_for_mode resolves
 `autoscaler.greedy_autoscale / model_level_autoscale / brute_force_autoscale`
 by module attribute at call time (runner.py:38-52), and the planners call
 each other by global name inside autoscaler.py (:352, :497, :771). Rebinding
-those module attributes therefore reroutes the CLI, runner.sweep and the
-greedy planner's uniform reseed without editing the reference.
+those module attributes therefore reroutes the CLI (all three --mode values),
+runner.sweep / compare_point and the planners' internal calls without editing
+the reference.
 
     import opscaler
     from paper_2511_02248_b200 import install
-    install(opscaler)              # brute_force / model_level now run on the B200
+    install(opscaler)   # brute_force / model_level / greedy now run on the B200
 
 The wrappers accept the reference's own objects, return the reference's own
 ScalingPlan / OperatorConfig / PredictedSojourn instances and raise its own
@@ -43,12 +44,8 @@ def install(pkg=None):
         import opscaler as pkg  # noqa: F811
     A = pkg.autoscaler
     T, E = _namespaces(pkg)
-    saved = {
-        (A, "brute_force_autoscale"): A.brute_force_autoscale,
-        (A, "model_level_autoscale"): A.model_level_autoscale,
-        (pkg, "brute_force_autoscale"): getattr(pkg, "brute_force_autoscale", None),
-        (pkg, "model_level_autoscale"): getattr(pkg, "model_level_autoscale", None),
-    }
+    names = ("brute_force_autoscale", "model_level_autoscale", "greedy_autoscale")
+    saved = {(mod, name): getattr(mod, name, None) for mod in (A, pkg) for name in names}
 
     @functools.wraps(saved[(A, "brute_force_autoscale")])
     def brute_force_autoscale(dag, profiles, point, params, bounds=None):
@@ -60,9 +57,14 @@ def install(pkg=None):
     def model_level_autoscale(dag, profiles, point, params):
         return planners.model_level_autoscale(dag, profiles, point, params, types=T, err=E)
 
+    @functools.wraps(saved[(A, "greedy_autoscale")])
+    def greedy_autoscale(dag, profiles, point, params):
+        return planners.greedy_autoscale(dag, profiles, point, params, types=T, err=E)
+
     for mod in (A, pkg):
         mod.brute_force_autoscale = brute_force_autoscale
         mod.model_level_autoscale = model_level_autoscale
+        mod.greedy_autoscale = greedy_autoscale
 
     def uninstall():
         for (mod, name), fn in saved.items():

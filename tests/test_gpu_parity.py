@@ -186,17 +186,24 @@ def test_device_planner_matches_host_path(nat):
     a MIN reduction equal 1 shard."""
     import torch
     from paper_2511_02248_b200 import device
-    for cfg, mode in (("cfg5", abi.MODE_ORACLE), ("cfg2", abi.MODE_ORACLE), ("cfg2", abi.MODE_MODEL)):
+    for cfg, mode in (("cfg5", abi.MODE_ORACLE), ("cfg2", abi.MODE_ORACLE), ("cfg2", abi.MODE_MODEL),
+                      ("cfg2", abi.MODE_OPERATOR), ("cfg3", abi.MODE_OPERATOR)):
         prob = tables.pack_problem(*scenarios.scenario(cfg))
         grid = _grid(cfg, prob)
-        spec = tables.pack_model(prob, model.AutoscaleParams(slo=1.0))
+        prm = model.AutoscaleParams(slo=1.0)
+        spec = tables.pack_model(prob, prm)
+        gs = tables.pack_greedy(prob, prm)
         win = _scenario_windows(cfg, "prefill", np.arange(0, 60, 7))
-        host = nat.plan_windows_host(mode, prob, win, grid=grid, model=spec)
-        p = device.DevicePlanner(prob, win, mode, grid=grid, model=spec)
+        host = nat.plan_windows_host(mode, prob, win, grid=grid, model=spec, greedy=gs, trace_cap=1024)
+        p = device.DevicePlanner(prob, win, mode, grid=grid, model=spec, greedy=gs, trace_cap=1024)
         p.step()
         d1 = p.decisions()
-        for f in tables.DecisionArrays.FIELDS:
+        for f in tables.DecisionArrays.FIELDS + ("trace_len",):
             assert getattr(d1, f).tobytes() == getattr(host, f).tobytes(), (cfg, mode, f)
+        if mode == abi.MODE_OPERATOR:
+            for i in range(win.n):
+                k = int(host.trace_len[i])
+                assert d1.trace[i, :k].tobytes() == host.trace[i, :k].tobytes()
         if mode == abi.MODE_ORACLE:
             acc = {}
 
