@@ -266,6 +266,31 @@ OPSC_API int opsc_greedy(const OpscDag* dag, const OpscGreedySpec* spec, OpscWin
                          const int16_t* uniform_cfg, const uint8_t* uniform_feasible,
                          const uint32_t* uniform_status, OpscDecisions out, void* stream);
 
+/* ---- trace windowing (workload.py:107-158) ---- */
+
+/* A request trace as structure of arrays (RequestRecord, workload.py:31-35). */
+typedef struct OpscTraceRecords {
+  int64_t n;
+  const double* arrival;     /* seconds, >= 0, any order */
+  const int32_t* input_len;  /* >= 1 */
+  const int32_t* output_len; /* >= 0 */
+} OpscTraceRecords;
+
+/* Bytes of device workspace opsc_windowize needs. */
+OPSC_API size_t opsc_windowize_workspace(int64_t n_records, int32_t max_windows);
+
+/* windowize(records, window_len, quantile) on the device: n_windows =
+ * max(1, ceil(horizon/len + 1e-12)), record -> min(int(t/len), n-1); per
+ * window prefill qps = count/len, prefill seq_len = max(1, q-"higher"
+ * quantile of input lengths), decode qps = sum(output)/len (decode seq_len is
+ * 1). Empty windows give qps 0 and seq_len 1. `n_windows` is a device int32;
+ * if it exceeds max_windows it is written but no window is produced and the
+ * call returns OPSC_ERR_ARG at the next synchronisation of the host path. */
+OPSC_API int opsc_windowize(OpscTraceRecords rec, double window_len, double quantile,
+                            int32_t max_windows, int32_t* n_windows, double* prefill_qps,
+                            int32_t* prefill_len, double* decode_qps, void* workspace,
+                            size_t workspace_bytes, void* stream);
+
 /* ---- host-buffer path: one call plans a batch of windows end to end ---- */
 typedef struct OpscContext OpscContext;
 

@@ -61,6 +61,11 @@ int orc_greedy(const OpscDag* dag, const OpscGreedySpec* spec, OpscWindows win,
                const int16_t* uniform_cfg, const uint8_t* uniform_feasible,
                const uint32_t* uniform_status, OpscDecisions out, int32_t n_threads);
 
+/* windowize (workload.py:107-158); returns n_windows or -1 if > max_windows. */
+int32_t orc_windowize(OpscTraceRecords rec, double window_len, double quantile,
+                      int32_t max_windows, double* prefill_qps, int32_t* prefill_len,
+                      double* decode_qps);
+
 /* Whole pipeline of one planning mode over a batch of windows. */
 int orc_plan_windows(int32_t mode, const OpscDag* dag, const OpscGrid* grid,
                      const OpscModelSpec* model, const OpscGreedySpec* greedy,

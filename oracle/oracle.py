@@ -60,6 +60,8 @@ def lib():
         L.orc_materialize.argtypes = [P, abi.OpscWindows, I, P, abi.OpscDecisions, I]
         L.orc_plan_windows.argtypes = [I, P, P, P, P, P, abi.OpscWindows, abi.OpscDecisions, I]
         L.orc_greedy.argtypes = [P, P, abi.OpscWindows, P, P, P, abi.OpscDecisions, I]
+        L.orc_windowize.argtypes = [abi.OpscTraceRecords, D, D, I, P, P, P]
+        L.orc_windowize.restype = I
         for f in ("orc_menu_build", "orc_stability_check", "orc_compose_argmin",
                   "orc_menu_fallback", "orc_decode_decisions", "orc_model_grid",
                   "orc_materialize", "orc_plan_windows", "orc_greedy"):
@@ -109,3 +111,17 @@ def compose(problem, grid, windows, menu_w, shard=0, n_shards=1, n_threads=None,
     if rc != abi.OK:
         raise RuntimeError(f"oracle status {rc}")
     return key
+
+
+def windowize(arrival, input_len, output_len, window_len=60.0, quantile=0.95, max_windows=1 << 20):
+    """(prefill_qps, prefill_len, decode_qps) per window, CPU restatement."""
+    a = np.ascontiguousarray(arrival, dtype=np.float64)
+    i = np.ascontiguousarray(input_len, dtype=np.int32)
+    o = np.ascontiguousarray(output_len, dtype=np.int32)
+    rec = abi.OpscTraceRecords(len(a), a.ctypes.data, i.ctypes.data, o.ctypes.data)
+    pq = np.zeros(max_windows); pl = np.zeros(max_windows, dtype=np.int32); dq = np.zeros(max_windows)
+    n = lib().orc_windowize(rec, window_len, quantile, max_windows, pq.ctypes.data, pl.ctypes.data,
+                            dq.ctypes.data)
+    if n < 0:
+        raise ValueError("more windows than max_windows")
+    return pq[:n].copy(), pl[:n].copy(), dq[:n].copy()

@@ -95,3 +95,8 @@ class OpscDecisions(C.Structure):
         "key", "cfg", "feasible", "status", "latency", "objective", "path",
         "pred", "stable", "energy", "memory", "devices")] + [
         ("trace_cap", _I), ("trace_len", C.c_void_p), ("trace", C.c_void_p)]
+
+
+class OpscTraceRecords(C.Structure):
+    _fields_ = [("n", C.c_int64), ("arrival", C.c_void_p), ("input_len", C.c_void_p),
+                ("output_len", C.c_void_p)]

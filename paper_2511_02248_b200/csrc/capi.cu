@@ -317,6 +317,20 @@ int opsc_ctx_last_launches(const OpscContext* c, int32_t* launches) {
   return OPSC_OK;
 }
 
+size_t opsc_windowize_workspace(int64_t n_records, int32_t max_windows) {
+  return windowize_workspace(n_records, max_windows);
+}
+
+int opsc_windowize(OpscTraceRecords rec, double window_len, double quantile, int32_t max_windows,
+                   int32_t* n_windows, double* prefill_qps, int32_t* prefill_len, double* decode_qps,
+                   void* workspace, size_t workspace_bytes, void* stream) {
+  if (!(window_len > 0.0) || !(quantile > 0.0 && quantile <= 1.0) || rec.n <= 0 || max_windows < 1 ||
+      !n_windows || !workspace)
+    return OPSC_ERR_ARG;
+  return from_cuda(launch_windowize(rec, window_len, quantile, max_windows, n_windows, prefill_qps,
+                                    prefill_len, decode_qps, workspace, workspace_bytes, (cudaStream_t)stream));
+}
+
 int opsc_greedy(const OpscDag* dag, const OpscGreedySpec* spec, OpscWindows win, const int16_t* uniform_cfg,
                 const uint8_t* uniform_feasible, const uint32_t* uniform_status, OpscDecisions out,
                 void* stream) {

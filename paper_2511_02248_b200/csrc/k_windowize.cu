@@ -1,0 +1,222 @@
+// k_windowize.cu -- trace -> per-window demand points on the device
+// (reference workload.py:107-158).
+//
+//   horizon      = max arrival            (block max -> atomicMax on the IEEE bits)
+//   n_windows    = max(1, ceil(horizon / len + 1e-12))
+//   window(r)    = min(int(t / len), n - 1)   (count + output-token sum atomics)
+//   grouping     = exclusive scan of counts + scatter of input lengths
+//   q-quantile   = k-th smallest input length, k = max(0, ceil(q*count) - 1)
+//                  ("higher" empirical quantile), by a per-window CTA radix
+//                  select (3 passes of 11/11/10 bits over the uint32 values)
+// Integer counts / sums are exact, so qps = count/len and sum/len are the
+// reference's bits.
+#include "opsc_common.cuh"
+
+namespace opsc {
+
+struct WzWork {
+  unsigned long long* horizon_bits;
+  uint32_t* err;
+  uint32_t* counts;
+  unsigned long long* sums;
+  unsigned long long* offsets;
+  uint32_t* cursors;
+  uint32_t* widx;
+  uint32_t* grouped;
+};
+
+static size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+size_t windowize_workspace(long long n, int max_w) {
+  size_t s = 0;
+  s += align16(8) + align16(4);
+  s += align16(4ull * max_w) + align16(8ull * max_w) + align16(8ull * (max_w + 1)) + align16(4ull * max_w);
+  s += align16(4ull * (size_t)n) * 2;
+  return s;
+}
+
+static WzWork carve(void* ws, long long n, int max_w) {
+  char* p = (char*)ws;
+  WzWork w;
+  w.horizon_bits = (unsigned long long*)p; p += align16(8);
+  w.err = (uint32_t*)p; p += align16(4);
+  w.counts = (uint32_t*)p; p += align16(4ull * max_w);
+  w.sums = (unsigned long long*)p; p += align16(8ull * max_w);
+  w.offsets = (unsigned long long*)p; p += align16(8ull * (max_w + 1));
+  w.cursors = (uint32_t*)p; p += align16(4ull * max_w);
+  w.widx = (uint32_t*)p; p += align16(4ull * (size_t)n);
+  w.grouped = (uint32_t*)p;
+  return w;
+}
+
+__global__ void wz_zero(WzWork w, int max_w) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) {
+    *w.horizon_bits = 0ull;
+    *w.err = 0u;
+  }
+  if (i < max_w) {
+    w.counts[i] = 0;
+    w.sums[i] = 0;
+    w.cursors[i] = 0;
+  }
+}
+
+// non-negative doubles order like their unsigned bit patterns
+__global__ void wz_horizon(const double* __restrict__ t, long long n, WzWork w) {
+  unsigned long long m = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(t[i]);
+    m = b > m ? b : m;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, m, o);
+    m = x > m ? x : m;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(w.horizon_bits, m);
+}
+
+__global__ void wz_nwin(WzWork w, double len, int max_w, int32_t* n_windows) {
+  const double horizon = __longlong_as_double((long long)*w.horizon_bits);
+  const double nw = ceil(horizon / len + 1e-12);
+  long long n = nw < 1.0 ? 1 : (long long)nw;
+  if (n > max_w) {
+    *w.err = 1u;
+    n = n > 0x7fffffffLL ? 0x7fffffffLL : n;
+  }
+  *n_windows = (int32_t)n;
+}
+
+__global__ void wz_count(OpscTraceRecords rec, double len, WzWork w, const int32_t* __restrict__ n_windows) {
+  if (*w.err) return;
+  const long long n = *n_windows;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < rec.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long k = (long long)(rec.arrival[i] / len);  // int() truncates (t >= 0)
+    if (k > n - 1) k = n - 1;
+    w.widx[i] = (uint32_t)k;
+    atomicAdd(&w.counts[k], 1u);
+    atomicAdd(&w.sums[k], (unsigned long long)rec.output_len[i]);
+  }
+}
+
+// single-CTA exclusive scan of counts (chunks of 1024)
+__global__ void __launch_bounds__(1024) wz_scan(WzWork w, const int32_t* __restrict__ n_windows) {
+  __shared__ unsigned long long part[1024];
+  __shared__ unsigned long long carry;
+  if (*w.err) return;
+  const int n = *n_windows;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += 1024) {
+    const int i = base + threadIdx.x;
+    const unsigned long long v = i < n ? w.counts[i] : 0;
+    part[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+      const unsigned long long add = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+      __syncthreads();
+      part[threadIdx.x] += add;
+      __syncthreads();
+    }
+    if (i < n) w.offsets[i] = carry + part[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += part[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) w.offsets[n] = carry;
+}
+
+__global__ void wz_scatter(OpscTraceRecords rec, WzWork w) {
+  if (*w.err) return;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < rec.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint32_t k = w.widx[i];
+    const unsigned long long pos = w.offsets[k] + atomicAdd(&w.cursors[k], 1u);
+    w.grouped[pos] = (uint32_t)rec.input_len[i];
+  }
+}
+
+__global__ void __launch_bounds__(256) wz_select(WzWork w, double len, double q, const int32_t* __restrict__ n_windows,
+                                                 double* __restrict__ pq, int32_t* __restrict__ pl,
+                                                 double* __restrict__ dq) {
+  __shared__ uint32_t hist[2048];
+  __shared__ uint32_t s_prefix, s_mask;
+  __shared__ long long s_k;
+  if (*w.err) return;
+  const int win = blockIdx.x;
+  if (win >= *n_windows) return;
+  const unsigned long long c = w.counts[win];
+  if (c == 0) {
+    if (threadIdx.x == 0) {
+      pq[win] = 0.0;
+      pl[win] = 1;
+      dq[win] = 0.0;
+    }
+    return;
+  }
+  const unsigned long long off = w.offsets[win];
+  if (threadIdx.x == 0) {
+    long long k = (long long)ceil(q * (double)c) - 1;
+    s_k = k < 0 ? 0 : k;
+    s_prefix = 0;
+    s_mask = 0;
+  }
+  const int shifts[3] = {21, 10, 0};
+  const int bits[3] = {11, 11, 10};
+  for (int pass = 0; pass < 3; ++pass) {
+    const int nb = 1 << bits[pass];
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    const uint32_t prefix = s_prefix, mask = s_mask;
+    for (unsigned long long i = threadIdx.x; i < c; i += blockDim.x) {
+      const uint32_t v = w.grouped[off + i];
+      if ((v & mask) == prefix) atomicAdd(&hist[(v >> shifts[pass]) & (uint32_t)(nb - 1)], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long k = s_k, cum = 0;
+      int sel = nb - 1;
+      for (int b = 0; b < nb; ++b) {
+        if (cum + hist[b] > k) {
+          sel = b;
+          break;
+        }
+        cum += hist[b];
+      }
+      s_k = k - cum;
+      s_prefix = prefix | ((uint32_t)sel << shifts[pass]);
+      s_mask = mask | ((uint32_t)(nb - 1) << shifts[pass]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const int v = (int)s_prefix;
+    pq[win] = (double)c / len;
+    pl[win] = v < 1 ? 1 : v;
+    dq[win] = (double)w.sums[win] / len;
+  }
+}
+
+cudaError_t launch_windowize(OpscTraceRecords rec, double len, double q, int max_w, int32_t* n_windows,
+                             double* pq, int32_t* pl, double* dq, void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (rec.n <= 0 || max_w < 1) return cudaErrorInvalidValue;
+  if (ws_bytes < windowize_workspace(rec.n, max_w)) return cudaErrorInvalidValue;
+  WzWork w = carve(ws, rec.n, max_w);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long rb = (rec.n + 255) / 256;
+  const int grid = (int)(rb < (long long)sms * 8 ? rb : (long long)sms * 8);
+  wz_zero<<<(max_w + 255) / 256, 256, 0, s>>>(w, max_w);
+  wz_horizon<<<grid, 256, 0, s>>>(rec.arrival, rec.n, w);
+  wz_nwin<<<1, 1, 0, s>>>(w, len, max_w, n_windows);
+  wz_count<<<grid, 256, 0, s>>>(rec, len, w, n_windows);
+  wz_scan<<<1, 1024, 0, s>>>(w, n_windows);
+  wz_scatter<<<grid, 256, 0, s>>>(rec, w);
+  wz_select<<<max_w, 256, 0, s>>>(w, len, q, n_windows, pq, pl, dq);
+  return cudaGetLastError();
+}
+
+}  // namespace opsc

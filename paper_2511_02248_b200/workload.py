@@ -119,3 +119,67 @@ def windowize(records, window_len: float = 60.0, quantile: float = 0.95):
             dec = WorkloadPoint(0.0, 1, "decode", win)
         result.append((pre, dec))
     return result
+
+
+def windowize_device(arrival, input_len, output_len, window_len: float = 60.0,
+                     quantile: float = 0.95, device="cuda", max_windows=None):
+    """windowize on the GPU (opsc_windowize, csrc/k_windowize.cu). Inputs are
+    record arrays (host or device); returns device tensors (prefill_qps,
+    prefill_len, decode_qps) of length n_windows, already resident in HBM for
+    the planners."""
+    import ctypes as C
+
+    import torch
+
+    from . import _native, abi
+    if window_len <= 0:
+        raise ValueError("window_len must be positive")
+    if not (0.0 < quantile <= 1.0):
+        raise ValueError("quantile must be in (0, 1]")
+    dev = torch.device(device)
+    t = torch.as_tensor(arrival, dtype=torch.float64, device=dev).contiguous()
+    li = torch.as_tensor(input_len, dtype=torch.int32, device=dev).contiguous()
+    lo = torch.as_tensor(output_len, dtype=torch.int32, device=dev).contiguous()
+    n = int(t.numel())
+    if n == 0:
+        z = torch.zeros(0, dtype=torch.float64, device=dev)
+        return z, torch.zeros(0, dtype=torch.int32, device=dev), z
+    if max_windows is None:
+        horizon = float(t.max().item())
+        max_windows = max(1, math.ceil(horizon / window_len + 1e-12))
+    L = _native.load()
+    ws_bytes = L.opsc_windowize_workspace(n, max_windows)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    nw = torch.zeros(1, dtype=torch.int32, device=dev)
+    pq = torch.empty(max_windows, dtype=torch.float64, device=dev)
+    pl = torch.empty(max_windows, dtype=torch.int32, device=dev)
+    dq = torch.empty(max_windows, dtype=torch.float64, device=dev)
+    rec = abi.OpscTraceRecords(n, t.data_ptr(), li.data_ptr(), lo.data_ptr())
+    _native.check(L.opsc_windowize(rec, float(window_len), float(quantile), max_windows,
+                                   nw.data_ptr(), pq.data_ptr(), pl.data_ptr(), dq.data_ptr(),
+                                   ws.data_ptr(), C.c_size_t(ws_bytes),
+                                   torch.cuda.current_stream(dev).cuda_stream), "opsc_windowize")
+    k = int(nw.item())
+    if k > max_windows:
+        raise ValueError(f"trace spans {k} windows > max_windows={max_windows}")
+    return pq[:k], pl[:k], dq[:k]
+
+
+def windowize_points(records, window_len: float = 60.0, quantile: float = 0.95, device="cuda"):
+    """Drop-in for windowize() computed on the GPU: [(prefill, decode)] points."""
+    if window_len <= 0:
+        raise ValueError("window_len must be positive")
+    if not (0.0 < quantile <= 1.0):
+        raise ValueError("quantile must be in (0, 1]")
+    if not records:
+        return []
+    arr = np.array([r.arrival_time for r in records], dtype=np.float64)
+    li = np.array([r.input_len for r in records], dtype=np.int32)
+    lo = np.array([r.output_len for r in records], dtype=np.int32)
+    pq, pl, dq = (x.cpu().numpy() for x in windowize_device(arr, li, lo, window_len, quantile, device))
+    out = []
+    for i in range(len(pq)):
+        win = (i * window_len, (i + 1) * window_len)
+        out.append((WorkloadPoint(float(pq[i]), int(pl[i]), "prefill", win),
+                    WorkloadPoint(float(dq[i]), 1, "decode", win)))
+    return out

@@ -174,3 +174,21 @@ def test_workload_mirror_matches_reference_fixture(cfg):
     assert np.array_equal(np.array([p.qps for p, _ in wins]), tw["prefill_qps"])
     assert np.array_equal(np.array([p.seq_len for p, _ in wins]), tw["prefill_len"])
     assert np.array_equal(np.array([d.qps for _, d in wins]), tw["decode_qps"])
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2", "cfg3", "cfg5"])
+def test_oracle_windowize_matches_reference_fixture(orc, cfg):
+    spec = scenarios.TRACES[cfg]
+    recs = workload.synth_workload(workload.SynthSpec(**spec["spec"]), spec["seed"])
+    arr = np.array([r.arrival_time for r in recs])
+    li = np.array([r.input_len for r in recs])
+    lo = np.array([r.output_len for r in recs])
+    pq, pl, dq = orc.windowize(arr, li, lo, spec["window_len"], spec["quantile"])
+    tw = scenarios.trace_windows(cfg)
+    assert np.array_equal(pq, tw["prefill_qps"])
+    assert np.array_equal(pl, tw["prefill_len"])
+    assert np.array_equal(dq, tw["decode_qps"])
+    # order independence (windowize buckets; the quantile sorts)
+    perm = np.random.default_rng(0).permutation(len(arr))
+    pq2, pl2, dq2 = orc.windowize(arr[perm], li[perm], lo[perm], spec["window_len"], spec["quantile"])
+    assert np.array_equal(pq, pq2) and np.array_equal(pl, pl2) and np.array_equal(dq, dq2)
