@@ -266,6 +266,16 @@ OPSC_API int opsc_greedy(const OpscDag* dag, const OpscGreedySpec* spec, OpscWin
                          const int16_t* uniform_cfg, const uint8_t* uniform_feasible,
                          const uint32_t* uniform_status, OpscDecisions out, void* stream);
 
+/* The same planner split in two launches: phase 1 = init_configs + first
+ * greedy loop (needs no model-level input), phase 2 = uniform reseed,
+ * headroom restore, prune, outputs. Lets the caller run opsc_model_grid
+ * concurrently with phase 1. `state` holds opsc_greedy_state_bytes(W) bytes. */
+OPSC_API size_t opsc_greedy_state_bytes(int32_t n_windows);
+OPSC_API int opsc_greedy_phase(const OpscDag* dag, const OpscGreedySpec* spec, OpscWindows win,
+                               int32_t phase, void* state, const int16_t* uniform_cfg,
+                               const uint8_t* uniform_feasible, const uint32_t* uniform_status,
+                               OpscDecisions out, void* stream);
+
 /* ---- trace windowing (workload.py:107-158) ---- */
 
 /* A request trace as structure of arrays (RequestRecord, workload.py:31-35). */

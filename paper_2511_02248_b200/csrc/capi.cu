@@ -103,6 +103,9 @@ struct OpscContext {
   int32_t* trace_len = nullptr;
   OpscTraceEntry* trace = nullptr;
   size_t cap_trace = 0;
+  unsigned char* gstate = nullptr;  // greedy phase-1 state
+  cudaStream_t side = nullptr;      // K3 runs here concurrently with greedy phase 1
+  cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 namespace {
@@ -126,7 +129,8 @@ int ensure(OpscContext* c, size_t W, size_t E, size_t n, size_t ndev, size_t tra
         (e = regrow(c->stable, w2 * n2)) || (e = regrow(c->path, w2 * n2)) ||
         (e = regrow(c->pred, w2 * n2 * OPSC_PRED_FIELDS)) || (e = regrow(c->fb, w2 * n2)) ||
         (e = regrow(c->u_cfg, w2 * n2 * 3)) || (e = regrow(c->u_feas, w2)) ||
-        (e = regrow(c->u_status, w2)) || (e = regrow(c->trace_len, w2)))
+        (e = regrow(c->u_status, w2)) || (e = regrow(c->trace_len, w2)) ||
+        (e = regrow(c->gstate, greedy_state_bytes((int)w2))))
       return from_cuda(e);
     c->cap_trace = 0;
     c->cap_w = w2;
@@ -281,6 +285,9 @@ int opsc_ctx_create(int32_t device, int32_t max_windows, OpscContext** out) {
   c->device = device;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     delete c;
     return OPSC_ERR_CUDA;
@@ -303,10 +310,13 @@ int opsc_ctx_destroy(OpscContext* c) {
   void* ptrs[] = {c->qps, c->slo, c->eps, c->seq_len, c->phase, c->menu, c->fb, c->mem_cap, c->key,
                   c->cfg, c->feasible, c->stable, c->status, c->latency, c->pred, c->energy,
                   c->memory, c->objective, c->devices, c->path, c->u_cfg, c->u_feas,
-                  c->u_status, c->trace_len, c->trace};
+                  c->u_status, c->trace_len, c->trace, c->gstate};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->fork) cudaEventDestroy(c->fork);
+  if (c->join) cudaEventDestroy(c->join);
   delete c;
   return OPSC_OK;
 }
@@ -337,6 +347,18 @@ int opsc_greedy(const OpscDag* dag, const OpscGreedySpec* spec, OpscWindows win,
   if (!valid_dag(dag) || !spec || !out.trace_len || (out.trace_cap > 0 && !out.trace)) return OPSC_ERR_ARG;
   return from_cuda(launch_greedy(*dag, *spec, win, uniform_cfg, uniform_feasible, uniform_status, out,
                                  (cudaStream_t)stream));
+}
+
+size_t opsc_greedy_state_bytes(int32_t n_windows) { return greedy_state_bytes(n_windows); }
+
+int opsc_greedy_phase(const OpscDag* dag, const OpscGreedySpec* spec, OpscWindows win, int32_t phase,
+                      void* state, const int16_t* uniform_cfg, const uint8_t* uniform_feasible,
+                      const uint32_t* uniform_status, OpscDecisions out, void* stream) {
+  if (!valid_dag(dag) || !spec || !out.trace_len || (out.trace_cap > 0 && !out.trace) || !state ||
+      (phase != 1 && phase != 2))
+    return OPSC_ERR_ARG;
+  return from_cuda(launch_greedy(*dag, *spec, win, uniform_cfg, uniform_feasible, uniform_status, out,
+                                 (cudaStream_t)stream, phase, state));
 }
 
 int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, const OpscGrid* grid,
@@ -393,13 +415,20 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
     c->launches += 1;
     CK(launch_materialize(*dag, dw, 1, dplace, dev_decisions(c), s));
   } else {
-    // _uniform_optimum = model_level_autoscale on the same windows (autoscaler.py:492-500)
-    CK(launch_init(W, c->qps, c->u_status, nullptr, c->u_feas, s));
-    CK(launch_model_grid(*dag, greedy->model, dw, c->u_cfg, c->u_feas, c->u_status, s));
+    // _uniform_optimum = model_level_autoscale on the same windows
+    // (autoscaler.py:492-500); it does not depend on the first greedy loop, so
+    // it runs on the side stream while phase 1 runs on the main stream.
+    CK(cudaEventRecord(c->fork, s));
+    CK(cudaStreamWaitEvent(c->side, c->fork, 0));
+    CK(launch_init(W, c->qps, c->u_status, nullptr, c->u_feas, c->side));
+    CK(launch_model_grid(*dag, greedy->model, dw, c->u_cfg, c->u_feas, c->u_status, c->side));
+    CK(cudaEventRecord(c->join, c->side));
     OpscDecisions dd = dev_decisions(c);
     dd.trace_cap = (int32_t)tcap;
-    CK(launch_greedy(*dag, *greedy, dw, c->u_cfg, c->u_feas, c->u_status, dd, s));
-    c->launches += 3;
+    CK(launch_greedy(*dag, *greedy, dw, c->u_cfg, c->u_feas, c->u_status, dd, s, 1, c->gstate));
+    CK(cudaStreamWaitEvent(s, c->join, 0));
+    CK(launch_greedy(*dag, *greedy, dw, c->u_cfg, c->u_feas, c->u_status, dd, s, 2, c->gstate));
+    c->launches += 4;
     CK(launch_materialize(*dag, dw, 1, dplace, dd, s));
   }
   c->launches++;

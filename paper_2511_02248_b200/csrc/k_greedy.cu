@@ -364,23 +364,70 @@ __device__ void prune_pass(GShared& S, const GreedyArgs& a, const OpscDecisions&
   __syncthreads();
 }
 
+// Greedy state carried from phase 1 (init + first loop) to phase 2 (reseed,
+// headroom, prune), so K3 -- needed only by phase 2 -- can run concurrently
+// with phase 1 on another stream.
+struct GSave {
+  int p[OPSC_MAX_OPS], r[OPSC_MAX_OPS], b[OPSC_MAX_OPS];
+  double soj[OPSC_MAX_OPS], wt[OPSC_MAX_OPS];
+  double lat;
+  int8_t path[OPSC_MAX_OPS];
+  int stable, trace_len, ok;
+  uint32_t st;
+};
+
+size_t greedy_state_bytes(int n_windows) { return sizeof(GSave) * (size_t)(n_windows > 0 ? n_windows : 1); }
+
+__device__ void distinct_p(GShared& S, const GreedyArgs& a, int n) {
+  for (int v = 0; v < n; ++v) {
+    int k = 0;
+    for (int i = 0; i < a.s.n_p[v]; ++i) {
+      bool dup = false;
+      for (int j = 0; j < k; ++j) dup |= S.pd[v][j] == a.s.p_vals[v][i];
+      if (!dup) S.pd[v][k++] = a.s.p_vals[v][i];
+    }
+    S.np_d[v] = k;
+  }
+}
+
+// phase 0: whole planner; phase 1: init_configs + first greedy loop, state
+// saved; phase 2: state loaded, uniform reseed, headroom, prune, outputs.
 __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
     const __grid_constant__ GreedyArgs a, const __grid_constant__ OpscWindows win,
     const int16_t* __restrict__ ucfg, const uint8_t* __restrict__ ufeas, const uint32_t* __restrict__ ustatus,
-    const __grid_constant__ OpscDecisions out) {
+    const __grid_constant__ OpscDecisions out, int phase, GSave* __restrict__ save) {
   __shared__ GShared S;
   const OpscDag& d = a.d;
   const int n = d.n_ops;
   const int w = blockIdx.x;
   const double qps = win.qps[w];
+  const int L = win.seq_len[w], ph = win.phase[w];
+  const double slo = win.slo[w], eps = win.eps[w];
+  if (phase == 2) {
+    if (!(qps > 0.0)) return;
+    if (threadIdx.x == 0) {
+      const GSave& g = save[w];
+      distinct_p(S, a, n);
+      for (int v = 0; v < n; ++v) {
+        S.p[v] = g.p[v]; S.r[v] = g.r[v]; S.b[v] = g.b[v];
+        S.soj[v] = g.soj[v]; S.wt[v] = g.wt[v]; S.path[v] = g.path[v];
+      }
+      S.lat = g.lat;
+      S.stable = g.stable;
+      S.trace_len = g.trace_len;
+      S.st = g.st;
+      S.flag = g.ok;
+    }
+    __syncthreads();
+    if (!S.flag) return;
+  } else {
   if (threadIdx.x == 0) {
     out.feasible[w] = 0;
     out.trace_len[w] = 0;
+    if (phase == 1) save[w].ok = 0;
   }
   for (int i = threadIdx.x; i < n * 3; i += blockDim.x) out.cfg[(size_t)w * n * 3 + i] = 0;
   if (!(qps > 0.0)) return;
-  const int L = win.seq_len[w], ph = win.phase[w];
-  const double slo = win.slo[w], eps = win.eps[w];
   if (threadIdx.x == 0) {
     S.st = 0;
     S.trace_len = 0;
@@ -451,6 +498,22 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
   }
   eval_full(S, d, qps, L, ph);
   greedy_loop(S, a, out, w, qps, L, ph, slo, eps);
+  if (phase == 1) {
+    if (threadIdx.x == 0) {
+      GSave& g = save[w];
+      for (int v = 0; v < n; ++v) {
+        g.p[v] = S.p[v]; g.r[v] = S.r[v]; g.b[v] = S.b[v];
+        g.soj[v] = S.soj[v]; g.wt[v] = S.wt[v]; g.path[v] = S.path[v];
+      }
+      g.lat = S.lat;
+      g.stable = S.stable;
+      g.trace_len = S.trace_len;
+      g.st = S.st;
+      g.ok = 1;
+    }
+    return;
+  }
+  }  // phase != 2
 
   // ---- uniform reseed (:357-367)
   const uint32_t us = ustatus[w];
@@ -519,14 +582,16 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
 }
 
 cudaError_t launch_greedy(const OpscDag& d, const OpscGreedySpec& s, OpscWindows w, const int16_t* ucfg,
-                          const uint8_t* ufeas, const uint32_t* ustatus, OpscDecisions out, cudaStream_t st) {
+                          const uint8_t* ufeas, const uint32_t* ustatus, OpscDecisions out, cudaStream_t st,
+                          int phase, void* save) {
   if (w.n <= 0) return cudaSuccess;
+  if (phase < 0 || phase > 2 || (phase != 0 && !save)) return cudaErrorInvalidValue;
   for (int v = 0; v < d.n_ops; ++v)
     if (s.b_max[v] < 1 || s.b_max[v] > 64 || s.n_p[v] < 1) return cudaErrorInvalidValue;
   GreedyArgs a;
   a.d = d;
   a.s = s;
-  greedy_kernel<<<w.n, kGreedyThreads, 0, st>>>(a, w, ucfg, ufeas, ustatus, out);
+  greedy_kernel<<<w.n, kGreedyThreads, 0, st>>>(a, w, ucfg, ufeas, ustatus, out, phase, (GSave*)save);
   return cudaGetLastError();
 }
 

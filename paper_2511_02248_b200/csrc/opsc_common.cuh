@@ -184,7 +184,9 @@ cudaError_t launch_materialize(const OpscDag& d, OpscWindows w, int config_order
                                const OpscPlaceSpec& p, OpscDecisions out, cudaStream_t s);
 cudaError_t launch_fp64_peak(int iters, double* sink, int* blocks, int* threads, cudaStream_t s);
 cudaError_t launch_greedy(const OpscDag& d, const OpscGreedySpec& s, OpscWindows w, const int16_t* ucfg,
-                          const uint8_t* ufeas, const uint32_t* ustatus, OpscDecisions out, cudaStream_t st);
+                          const uint8_t* ufeas, const uint32_t* ustatus, OpscDecisions out, cudaStream_t st,
+                          int phase = 0, void* save = nullptr);
+size_t greedy_state_bytes(int n_windows);
 size_t windowize_workspace(long long n, int max_w);
 cudaError_t launch_windowize(OpscTraceRecords rec, double len, double q, int max_w, int32_t* n_windows,
                              double* pq, int32_t* pl, double* dq, void* ws, size_t ws_bytes, cudaStream_t s);

@@ -117,16 +117,29 @@ class DevicePlanner:
                                          self.out, s), "materialize")
 
     def operator(self):
-        """greedy_autoscale: model-level reseed candidates, then the greedy kernel."""
-        r, s = _native.ref, self._s()
+        """greedy_autoscale. The model-level reseed candidates (K3) are
+        computed on a side stream concurrently with greedy phase 1 (init +
+        first loop); phase 2 (reseed, headroom, prune) joins both."""
+        r = _native.ref
+        if not hasattr(self, "_side"):
+            self._side = torch.cuda.Stream(self.dev)
+            nb = self.L.opsc_greedy_state_bytes(self.W)
+            self._gstate = torch.empty(max(nb, 1), dtype=torch.uint8, device=self.dev)
+        main = torch.cuda.current_stream(self.dev)
+        self._side.wait_stream(main)
+        side = self._side.cuda_stream
         self._ck(self.L.opsc_init_windows(self.win, self.u_status.data_ptr(), None,
-                                          self.u_feas.data_ptr(), s), "init_windows")
+                                          self.u_feas.data_ptr(), side), "init_windows")
         self._ck(self.L.opsc_model_grid(r(self.problem.table), r(self.greedy.model), self.win,
                                         self.u_cfg.data_ptr(), self.u_feas.data_ptr(),
-                                        self.u_status.data_ptr(), s), "model_grid")
-        self._ck(self.L.opsc_greedy(r(self.problem.table), r(self.greedy), self.win,
-                                    self.u_cfg.data_ptr(), self.u_feas.data_ptr(),
-                                    self.u_status.data_ptr(), self.out, s), "greedy")
+                                        self.u_status.data_ptr(), side), "model_grid")
+        args = (r(self.problem.table), r(self.greedy), self.win)
+        uni = (self.u_cfg.data_ptr(), self.u_feas.data_ptr(), self.u_status.data_ptr())
+        self._ck(self.L.opsc_greedy_phase(*args, 1, self._gstate.data_ptr(), *uni, self.out,
+                                          main.cuda_stream), "greedy_phase1")
+        main.wait_stream(self._side)
+        self._ck(self.L.opsc_greedy_phase(*args, 2, self._gstate.data_ptr(), *uni, self.out,
+                                          main.cuda_stream), "greedy_phase2")
 
     def model_grid(self):
         r = _native.ref
