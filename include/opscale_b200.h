@@ -276,6 +276,15 @@ OPSC_API int opsc_greedy_phase(const OpscDag* dag, const OpscGreedySpec* spec, O
                                const uint8_t* uniform_feasible, const uint32_t* uniform_status,
                                OpscDecisions out, void* stream);
 
+/* Small-batch model level: every (B, R) point of every window is tabulated in
+ * parallel (same arithmetic as the in-warp probes, so the same bits) and the
+ * reference's probe/bisect then walks the table. Needs
+ * opsc_model_table_bytes(spec, W, n_ops) bytes of device workspace. */
+OPSC_API size_t opsc_model_table_bytes(const OpscModelSpec* spec, int32_t n_windows, int32_t n_ops);
+OPSC_API int opsc_model_grid_table(const OpscDag* dag, const OpscModelSpec* spec, OpscWindows win,
+                                   int16_t* cfg, uint8_t* feasible, uint32_t* status,
+                                   void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- trace windowing (workload.py:107-158) ---- */
 
 /* A request trace as structure of arrays (RequestRecord, workload.py:31-35). */

@@ -25,7 +25,8 @@ EXPORTS = (
     "opsc_decode_decisions", "opsc_model_grid", "opsc_materialize", "opsc_ctx_create",
     "opsc_ctx_destroy", "opsc_plan_windows_host", "opsc_ctx_last_launches", "opsc_fp64_peak",
     "opsc_candidate_probe", "opsc_greedy", "opsc_windowize", "opsc_windowize_workspace",
-    "opsc_greedy_state_bytes", "opsc_greedy_phase",
+    "opsc_greedy_state_bytes", "opsc_greedy_phase", "opsc_model_table_bytes",
+    "opsc_model_grid_table",
 )
 
 _lib = None
@@ -64,6 +65,8 @@ def load():
             "opsc_greedy": ([P, P, W, P, P, P, D, P], C.c_int),
             "opsc_windowize_workspace": ([C.c_int64, I], C.c_size_t),
             "opsc_greedy_state_bytes": ([I], C.c_size_t),
+            "opsc_model_table_bytes": ([P, I, I], C.c_size_t),
+            "opsc_model_grid_table": ([P, P, W, P, P, P, P, C.c_size_t, P], C.c_int),
             "opsc_greedy_phase": ([P, P, W, I, P, P, P, P, D, P], C.c_int),
             "opsc_windowize": ([abi.OpscTraceRecords, C.c_double, C.c_double, I, P, P, P, P, P,
                                 C.c_size_t, P], C.c_int),

@@ -104,6 +104,8 @@ struct OpscContext {
   OpscTraceEntry* trace = nullptr;
   size_t cap_trace = 0;
   unsigned char* gstate = nullptr;  // greedy phase-1 state
+  unsigned char* mtab = nullptr;    // model-level (B, R) table (small batches)
+  size_t cap_mtab = 0;
   cudaStream_t side = nullptr;      // K3 runs here concurrently with greedy phase 1
   cudaEvent_t fork = nullptr, join = nullptr;
 };
@@ -184,6 +186,30 @@ OpscDecisions dev_decisions(const OpscContext* c) {
 }
 
 bool valid_dag(const OpscDag* d) { return d && d->n_ops >= 1 && d->n_ops <= OPSC_MAX_OPS; }
+
+// small batches tabulate every (B, R) point (4M weights max, ~40 MB)
+constexpr long long kModelTablePoints = 1ll << 22;
+
+bool want_model_table(int W, const OpscModelSpec& m, int n) {
+  return (long long)W * m.b_cap * m.r_cap * n <= kModelTablePoints;
+}
+
+// returns workspace pointer (or null -> per-window probe path)
+void* model_table_ws(OpscContext* c, int W, const OpscModelSpec& m, int n, size_t* bytes) {
+  *bytes = 0;
+  if (!want_model_table(W, m, n)) return nullptr;
+  const size_t need = model_table_bytes(W, m, n);
+  if (need > c->cap_mtab) {
+    if (regrow(c->mtab, need) != cudaSuccess) {
+      cudaGetLastError();
+      c->cap_mtab = 0;
+      return nullptr;
+    }
+    c->cap_mtab = need;
+  }
+  *bytes = c->cap_mtab;
+  return c->mtab;
+}
 
 }  // namespace
 
@@ -310,7 +336,7 @@ int opsc_ctx_destroy(OpscContext* c) {
   void* ptrs[] = {c->qps, c->slo, c->eps, c->seq_len, c->phase, c->menu, c->fb, c->mem_cap, c->key,
                   c->cfg, c->feasible, c->stable, c->status, c->latency, c->pred, c->energy,
                   c->memory, c->objective, c->devices, c->path, c->u_cfg, c->u_feas,
-                  c->u_status, c->trace_len, c->trace, c->gstate};
+                  c->u_status, c->trace_len, c->trace, c->gstate, c->mtab};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -350,6 +376,21 @@ int opsc_greedy(const OpscDag* dag, const OpscGreedySpec* spec, OpscWindows win,
 }
 
 size_t opsc_greedy_state_bytes(int32_t n_windows) { return greedy_state_bytes(n_windows); }
+
+size_t opsc_model_table_bytes(const OpscModelSpec* spec, int32_t n_windows, int32_t n_ops) {
+  if (!spec) return 0;
+  return model_table_bytes(n_windows, *spec, n_ops);
+}
+
+int opsc_model_grid_table(const OpscDag* dag, const OpscModelSpec* spec, OpscWindows win, int16_t* cfg,
+                          uint8_t* feasible, uint32_t* status, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  if (!valid_dag(dag) || !spec || !workspace ||
+      workspace_bytes < model_table_bytes(win.n, *spec, dag->n_ops))
+    return OPSC_ERR_ARG;
+  return from_cuda(launch_model_grid(*dag, *spec, win, cfg, feasible, status, (cudaStream_t)stream,
+                                     workspace, workspace_bytes));
+}
 
 int opsc_greedy_phase(const OpscDag* dag, const OpscGreedySpec* spec, OpscWindows win, int32_t phase,
                       void* state, const int16_t* uniform_cfg, const uint8_t* uniform_feasible,
@@ -411,7 +452,9 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
     c->launches += 5;
     CK(launch_materialize(*dag, dw, 0, dplace, dev_decisions(c), s));
   } else if (mode == OPSC_MODE_MODEL) {
-    CK(launch_model_grid(*dag, *model, dw, c->cfg, c->feasible, c->status, s));
+    size_t tb = 0;
+    void* tw = model_table_ws(c, W, *model, n, &tb);
+    CK(launch_model_grid(*dag, *model, dw, c->cfg, c->feasible, c->status, s, tw, tb));
     c->launches += 1;
     CK(launch_materialize(*dag, dw, 1, dplace, dev_decisions(c), s));
   } else {
@@ -421,7 +464,9 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
     CK(cudaEventRecord(c->fork, s));
     CK(cudaStreamWaitEvent(c->side, c->fork, 0));
     CK(launch_init(W, c->qps, c->u_status, nullptr, c->u_feas, c->side));
-    CK(launch_model_grid(*dag, greedy->model, dw, c->u_cfg, c->u_feas, c->u_status, c->side));
+    size_t tb = 0;
+    void* tw = model_table_ws(c, W, greedy->model, n, &tb);
+    CK(launch_model_grid(*dag, greedy->model, dw, c->u_cfg, c->u_feas, c->u_status, c->side, tw, tb));
     CK(cudaEventRecord(c->join, c->side));
     OpscDecisions dd = dev_decisions(c);
     dd.trace_cap = (int32_t)tcap;

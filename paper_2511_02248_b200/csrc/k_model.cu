@@ -55,10 +55,27 @@ __device__ double eval_uniform(const OpscDag& d, const OpscModelSpec& m, double 
   return __shfl_sync(0xffffffffu, lat, 0);
 }
 
+// One (B, R) probe: evaluated in-warp, or looked up in the precomputed
+// table of the small-batch path (same arithmetic, so the same bits; the
+// table's per-point status bits are ORed only for points the reference visits).
+template <bool TABLE>
+__device__ __forceinline__ double probe(const OpscDag& d, const OpscModelSpec& m, double qps, int L, int ph,
+                                        int b, int r, double* wsh, uint32_t* st, const double* lt,
+                                        const uint8_t* ls) {
+  if (TABLE) {
+    const size_t i = (size_t)(b - 1) * m.r_cap + (r - 1);
+    *st |= ls[i];
+    return lt[i];
+  }
+  return eval_uniform(d, m, qps, L, ph, b, r, wsh, st);
+}
+
 // autoscaler.py:620-639
+template <bool TABLE>
 __device__ int smallest_r(const OpscDag& d, const OpscModelSpec& m, double qps, int L, int ph, int b,
-                          int r_floor, double bound, double* wsh, uint32_t* st, double* lat_out) {
-  const double lo_lat = eval_uniform(d, m, qps, L, ph, b, r_floor, wsh, st);
+                          int r_floor, double bound, double* wsh, uint32_t* st, double* lat_out,
+                          const double* lt, const uint8_t* ls) {
+  const double lo_lat = probe<TABLE>(d, m, qps, L, ph, b, r_floor, wsh, st, lt, ls);
   if (lo_lat <= bound) {
     *lat_out = lo_lat;
     return r_floor;
@@ -67,7 +84,7 @@ __device__ int smallest_r(const OpscDag& d, const OpscModelSpec& m, double qps, 
   double hi_lat = lo_lat;
   while (hi_lat > bound && hi < m.r_cap) {
     hi = min(hi * 2, m.r_cap);
-    hi_lat = eval_uniform(d, m, qps, L, ph, b, hi, wsh, st);
+    hi_lat = probe<TABLE>(d, m, qps, L, ph, b, hi, wsh, st, lt, ls);
   }
   if (hi_lat > bound) {
     *lat_out = hi_lat;
@@ -76,7 +93,7 @@ __device__ int smallest_r(const OpscDag& d, const OpscModelSpec& m, double qps, 
   int lo = r_floor;
   while (hi - lo > 1) {
     const int mid = (lo + hi) / 2;
-    const double ml = eval_uniform(d, m, qps, L, ph, b, mid, wsh, st);
+    const double ml = probe<TABLE>(d, m, qps, L, ph, b, mid, wsh, st, lt, ls);
     if (ml <= bound) {
       hi = mid;
       hi_lat = ml;
@@ -88,11 +105,14 @@ __device__ int smallest_r(const OpscDag& d, const OpscModelSpec& m, double qps, 
   return hi;
 }
 
+template <bool TABLE>
 __global__ void __launch_bounds__(1024) model_grid_kernel(const __grid_constant__ ModelArgs a,
                                                           const __grid_constant__ OpscWindows win,
                                                           int16_t* __restrict__ cfg,
                                                           uint8_t* __restrict__ feasible,
-                                                          uint32_t* __restrict__ status) {
+                                                          uint32_t* __restrict__ status,
+                                                          const double* __restrict__ lt_all,
+                                                          const uint8_t* __restrict__ ls_all) {
   const OpscDag& d = a.d;
   const OpscModelSpec& m = a.m;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -113,6 +133,9 @@ __global__ void __launch_bounds__(1024) model_grid_kernel(const __grid_constant_
   const double slo = win.slo[w], target = win.slo[w] - win.eps[w];
   double* wsh = wsh_all + warp * 32;
   uint32_t st = 0;
+  const size_t tab = (size_t)m.b_cap * m.r_cap;
+  const double* lt = TABLE ? lt_all + (size_t)w * tab : nullptr;
+  const uint8_t* ls = TABLE ? ls_all + (size_t)w * tab : nullptr;
 
   for (int b = warp + 1; b <= m.b_cap; b += nwarps) {
     int rm = 1;
@@ -130,8 +153,8 @@ __global__ void __launch_bounds__(1024) model_grid_kernel(const __grid_constant_
       continue;
     }
     double lat;
-    int r = smallest_r(d, m, qps, L, ph, b, r_floor, target, wsh, &st, &lat);
-    if (r < 0) r = smallest_r(d, m, qps, L, ph, b, r_floor, slo, wsh, &st, &lat);
+    int r = smallest_r<TABLE>(d, m, qps, L, ph, b, r_floor, target, wsh, &st, &lat, lt, ls);
+    if (r < 0) r = smallest_r<TABLE>(d, m, qps, L, ph, b, r_floor, slo, wsh, &st, &lat, lt, ls);
     if (lane == 0) {
       res_r[b - 1] = r;
       res_lat[b - 1] = lat;
@@ -186,8 +209,77 @@ __global__ void __launch_bounds__(1024) model_grid_kernel(const __grid_constant_
   }
 }
 
+// ---- small-batch path: every (B, R) point tabulated in parallel ----------
+// thread per (window, B, R, op): weight of op under uniform (B, R) at P_base
+__global__ void model_tab_weights(const __grid_constant__ ModelArgs a, const __grid_constant__ OpscWindows win,
+                                  double* __restrict__ wt, uint8_t* __restrict__ wst) {
+  const OpscDag& d = a.d;
+  const OpscModelSpec& m = a.m;
+  const int n = d.n_ops;
+  const long long total = (long long)win.n * m.b_cap * m.r_cap * n;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int v = (int)(i % n);
+    long long t = i / n;
+    const int r = (int)(t % m.r_cap) + 1;
+    t /= m.r_cap;
+    const int b = (int)(t % m.b_cap) + 1;
+    const int w = (int)(t / m.b_cap);
+    const double qps = win.qps[w];
+    if (!(qps > 0.0)) continue;
+    uint32_t st = 0;
+    const Pred o = predict(d, qps, win.seq_len[w], win.phase[w], v, m.p_base[v], r, b, &st);
+    wt[i] = o.stable ? weight(o, d.layer_count[v]) : OPSC_INF;
+    wst[i] = (uint8_t)st;
+  }
+}
+
+// thread per (window, B, R): evaluate(uniform(B, R)).latency (inf if unstable)
+__global__ void model_tab_latency(const __grid_constant__ ModelArgs a, int n_windows,
+                                  const double* __restrict__ wt, const uint8_t* __restrict__ wst,
+                                  double* __restrict__ lt, uint8_t* __restrict__ ls) {
+  const OpscDag& d = a.d;
+  const int n = d.n_ops;
+  const long long total = (long long)n_windows * a.m.b_cap * a.m.r_cap;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double* x = wt + i * n;
+    uint8_t st = 0;
+    bool all = true;
+    for (int v = 0; v < n; ++v) {
+      st |= wst[i * n + v];
+      all &= x[v] != OPSC_INF;
+    }
+    double lat = OPSC_INF;
+    if (all) {
+      double val[OPSC_MAX_OPS];
+      lat = 0.0;
+      for (int k = 0; k < n; ++k) {
+        const int v = d.topo[k];
+        double in = 0.0;
+        uint32_t pm = d.pred_mask[v];
+        while (pm) {
+          const int p = __ffs(pm) - 1;
+          pm &= pm - 1;
+          in = fmax(in, val[p]);
+        }
+        val[v] = in + x[v];
+        if (d.sink_mask >> v & 1u) lat = fmax(lat, val[v]);
+      }
+    }
+    lt[i] = lat;
+    ls[i] = st;
+  }
+}
+
+size_t model_table_bytes(int n_windows, const OpscModelSpec& m, int n_ops) {
+  const size_t pts = (size_t)n_windows * m.b_cap * m.r_cap;
+  return pts * (size_t)n_ops * 9 + pts * 9 + 64;
+}
+
 cudaError_t launch_model_grid(const OpscDag& d, const OpscModelSpec& m, OpscWindows w, int16_t* cfg,
-                              uint8_t* feasible, uint32_t* status, cudaStream_t s) {
+                              uint8_t* feasible, uint32_t* status, cudaStream_t s, void* table_ws,
+                              size_t table_bytes) {
   if (w.n <= 0) return cudaSuccess;
   if (m.b_cap < 1 || m.r_cap < 1) return cudaErrorInvalidValue;
   ModelArgs a;
@@ -195,12 +287,31 @@ cudaError_t launch_model_grid(const OpscDag& d, const OpscModelSpec& m, OpscWind
   a.m = m;
   const int nwarps = m.b_cap < 32 ? m.b_cap : 32;
   const size_t smem = (size_t)nwarps * 32 * sizeof(double) + (size_t)m.b_cap * (sizeof(double) + sizeof(int32_t));
+  const bool table = table_ws && table_bytes >= model_table_bytes(w.n, m, d.n_ops);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(model_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(table ? model_grid_kernel<true> : model_grid_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  model_grid_kernel<<<w.n, nwarps * 32, smem, s>>>(a, w, cfg, feasible, status);
+  if (!table) {
+    model_grid_kernel<false><<<w.n, nwarps * 32, smem, s>>>(a, w, cfg, feasible, status, nullptr, nullptr);
+    return cudaGetLastError();
+  }
+  const size_t pts = (size_t)w.n * m.b_cap * m.r_cap;
+  double* wt = (double*)table_ws;
+  double* lt = wt + pts * d.n_ops;
+  uint8_t* wst = (uint8_t*)(lt + pts);
+  uint8_t* ls = wst + pts * d.n_ops;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long t1 = (long long)pts * d.n_ops;
+  const int g1 = (int)((t1 + 127) / 128 < (long long)sms * 32 ? (t1 + 127) / 128 : (long long)sms * 32);
+  model_tab_weights<<<g1, 128, 0, s>>>(a, w, wt, wst);
+  const int g2 = (int)(((long long)pts + 127) / 128 < (long long)sms * 32 ? ((long long)pts + 127) / 128
+                                                                          : (long long)sms * 32);
+  model_tab_latency<<<g2, 128, 0, s>>>(a, w.n, wt, wst, lt, ls);
+  model_grid_kernel<true><<<w.n, nwarps * 32, smem, s>>>(a, w, cfg, feasible, status, lt, ls);
   return cudaGetLastError();
 }
 

@@ -179,7 +179,9 @@ cudaError_t launch_compose(const ComposeCfg& c, const OpscGrid& g, int n_windows
                            const double* menu_w, const double* slo, const double* qps,
                            unsigned long long* key, cudaStream_t s);
 cudaError_t launch_model_grid(const OpscDag& d, const OpscModelSpec& m, OpscWindows w, int16_t* cfg,
-                              uint8_t* feasible, uint32_t* status, cudaStream_t s);
+                              uint8_t* feasible, uint32_t* status, cudaStream_t s,
+                              void* table_ws = nullptr, size_t table_bytes = 0);
+size_t model_table_bytes(int n_windows, const OpscModelSpec& m, int n_ops);
 cudaError_t launch_materialize(const OpscDag& d, OpscWindows w, int config_order,
                                const OpscPlaceSpec& p, OpscDecisions out, cudaStream_t s);
 cudaError_t launch_fp64_peak(int iters, double* sink, int* blocks, int* threads, cudaStream_t s);

@@ -130,9 +130,7 @@ class DevicePlanner:
         side = self._side.cuda_stream
         self._ck(self.L.opsc_init_windows(self.win, self.u_status.data_ptr(), None,
                                           self.u_feas.data_ptr(), side), "init_windows")
-        self._ck(self.L.opsc_model_grid(r(self.problem.table), r(self.greedy.model), self.win,
-                                        self.u_cfg.data_ptr(), self.u_feas.data_ptr(),
-                                        self.u_status.data_ptr(), side), "model_grid")
+        self._model_grid_into(self.greedy.model, self.u_cfg, self.u_feas, self.u_status, side)
         args = (r(self.problem.table), r(self.greedy), self.win)
         uni = (self.u_cfg.data_ptr(), self.u_feas.data_ptr(), self.u_status.data_ptr())
         self._ck(self.L.opsc_greedy_phase(*args, 1, self._gstate.data_ptr(), *uni, self.out,
@@ -141,12 +139,27 @@ class DevicePlanner:
         self._ck(self.L.opsc_greedy_phase(*args, 2, self._gstate.data_ptr(), *uni, self.out,
                                           main.cuda_stream), "greedy_phase2")
 
-    def model_grid(self):
+    # small batches tabulate every (B, R) point in parallel (csrc/k_model.cu)
+    MODEL_TABLE_POINTS = 1 << 22
+
+    def _model_grid_into(self, spec, cfg, feas, status, stream):
         r = _native.ref
-        self._ck(self.L.opsc_model_grid(r(self.problem.table), r(self.model), self.win,
-                                        self.out_t["cfg"].data_ptr(),
-                                        self.out_t["feasible"].data_ptr(),
-                                        self.out_t["status"].data_ptr(), self._s()), "model_grid")
+        pts = self.W * spec.b_cap * spec.r_cap * self.n
+        if pts <= self.MODEL_TABLE_POINTS:
+            nb = self.L.opsc_model_table_bytes(r(spec), self.W, self.n)
+            if getattr(self, "_mtab", None) is None or self._mtab.numel() < nb:
+                self._mtab = torch.empty(nb, dtype=torch.uint8, device=self.dev)
+            self._ck(self.L.opsc_model_grid_table(r(self.problem.table), r(spec), self.win,
+                                                  cfg.data_ptr(), feas.data_ptr(), status.data_ptr(),
+                                                  self._mtab.data_ptr(), self._mtab.numel(), stream),
+                     "model_grid_table")
+        else:
+            self._ck(self.L.opsc_model_grid(r(self.problem.table), r(spec), self.win, cfg.data_ptr(),
+                                            feas.data_ptr(), status.data_ptr(), stream), "model_grid")
+
+    def model_grid(self):
+        self._model_grid_into(self.model, self.out_t["cfg"], self.out_t["feasible"],
+                              self.out_t["status"], self._s())
 
     def step(self, shard=0, n_shards=1, allreduce=None, compose_events=None):
         """One pass of the hot path over the resident batch of windows."""
