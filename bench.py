@@ -348,7 +348,7 @@ def decision_latency(dev):
     out = {}
     for mode, name in ((abi.MODE_ORACLE, "oracle_6e7_candidates"), (abi.MODE_MODEL, "model_level"),
                        (abi.MODE_OPERATOR, "operator_greedy")):
-        samples = []
+        samples, eager = [], []
         batch_ms = 0.0
         for phase in ("prefill", "decode"):
             slo = scenarios.SLO["cfg2"][phase]
@@ -372,23 +372,32 @@ def decision_latency(dev):
             p = device.DevicePlanner(problem, one, mode, grid=grid, model=spec, greedy=gspec,
                                      device=dev)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            graph = p.capture()  # the per-window pipeline as one CUDA graph launch
             for i in range(len(qs)):
                 if not qs[i] > 0:
                     continue
                 p.win_t["qps"].fill_(float(qs[i]))
                 p.win_t["seq_len"].fill_(int(ls[i]))
-                if i == 0:
-                    p.step()
                 torch.cuda.synchronize(dev)
                 e0.record()
                 p.step()
                 e1.record()
                 e1.synchronize()
+                eager.append(e0.elapsed_time(e1))
+                torch.cuda.synchronize(dev)
+                e0.record()
+                graph.replay()
+                e1.record()
+                e1.synchronize()
                 samples.append(e0.elapsed_time(e1))
         samples.sort()
+        eager.sort()
         out[name] = {"median": statistics.median(samples),
                      "p99": samples[min(len(samples) - 1, int(0.99 * len(samples)))],
                      "windows": len(samples),
+                     "launch": "CUDA graph replay of the whole per-window pipeline",
+                     "eager_median": statistics.median(eager),
+                     "eager_p99": eager[min(len(eager) - 1, int(0.99 * len(eager)))],
                      "batched_ms_per_window": batch_ms / max(1, len(samples))}
     out["dag"] = "cfg2 Llama-2-70B 10-op chain, 60 x 60 s windows x {prefill, decode}, W = 1"
     return out

@@ -166,6 +166,7 @@ typedef struct OpscTraceEntry {
   int16_t to_r, to_b, to_p;
   int8_t op;          /* lex rank; -1 for reseed_uniform        */
   uint8_t action;     /* OPSC_ACT_*                              */
+  int32_t reserved;   /* zero (explicit padding to 24 bytes)     */
 } OpscTraceEntry;
 
 /* Default-stream placement + energy inputs (placement.py:465-491, metrics.py:34-47). */

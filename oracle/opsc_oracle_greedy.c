@@ -87,6 +87,7 @@ static void push_trace(G* g, int action, int op, const GCfg* to, double lat, int
     t->to_p = (int16_t)(to ? to->p : 0);
     t->op = (int8_t)op;
     t->action = (uint8_t)action;
+    t->reserved = 0;
   }
   g->len++;
 }

@@ -77,7 +77,8 @@ class OpscGreedySpec(C.Structure):
 
 class OpscTraceEntry(C.Structure):
     _fields_ = [("latency", _D), ("objective", _I), ("to_r", C.c_int16), ("to_b", C.c_int16),
-                ("to_p", C.c_int16), ("op", C.c_int8), ("action", C.c_uint8)]
+                ("to_p", C.c_int16), ("op", C.c_int8), ("action", C.c_uint8),
+                ("reserved", C.c_int32)]
 
 
 class OpscPlaceSpec(C.Structure):

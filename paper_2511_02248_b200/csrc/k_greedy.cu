@@ -150,6 +150,7 @@ __device__ void push_trace(GShared& S, const OpscDecisions& out, int w, int acti
     t->to_p = (int16_t)p;
     t->op = (int8_t)op;
     t->action = (uint8_t)action;
+    t->reserved = 0;
   }
   S.trace_len++;
 }

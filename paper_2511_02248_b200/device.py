@@ -179,6 +179,17 @@ class DevicePlanner:
             self.model_grid()
         self.finish()
 
+    def capture(self, shard=0, n_shards=1, allreduce=None):
+        """Record one step into a CUDA graph (after a warm-up step that creates
+        the lazily allocated workspaces). Update `win_t` in place, then
+        `graph.replay()` re-plans the resident windows with one launch."""
+        self.step(shard, n_shards, allreduce)
+        torch.cuda.synchronize(self.dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step(shard, n_shards, allreduce)
+        return g
+
     def decisions(self) -> tables.DecisionArrays:
         torch.cuda.synchronize(self.dev)
         out = tables.DecisionArrays(self.W, self.n, self.trace_cap)

@@ -256,8 +256,8 @@ def window_arrays(qps, seq_len, phase, slo, eps=0.0) -> WindowArrays:
 
 
 TRACE_DTYPE = np.dtype([("latency", "<f8"), ("objective", "<i4"), ("to_r", "<i2"),
-                        ("to_b", "<i2"), ("to_p", "<i2"), ("op", "i1"), ("action", "u1")],
-                       align=True)
+                        ("to_b", "<i2"), ("to_p", "<i2"), ("op", "i1"), ("action", "u1"),
+                        ("reserved", "<i4")], align=True)
 assert TRACE_DTYPE.itemsize == C.sizeof(abi.OpscTraceEntry)
 
 
