@@ -337,32 +337,49 @@ __device__ void greedy_loop(GShared& S, const GreedyArgs& a, const OpscDecisions
   }
 }
 
-// _prune_pass (thread 0; sequential by construction)
+// _prune_pass (:562-589). The sweep itself is sequential (each accepted
+// prune changes the state the next trial sees), but a trial's predict_op
+// depends only on its own operator's config, so the Erlang-B recurrences of
+// all pending trials run in parallel threads; thread 0 then sweeps in id
+// order with the cheap DP, and only accepted operators are re-predicted
+// before the next pass (the same set of evaluations the reference makes).
 __device__ void prune_pass(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps, int L,
                            int ph, double target) {
-  if (threadIdx.x == 0) {
-    const OpscDag& d = a.d;
-    bool changed = true;
-    while (changed) {
-      changed = false;
+  __shared__ double t_wt[OPSC_MAX_OPS], t_soj[OPSC_MAX_OPS];
+  __shared__ uint8_t t_ok[OPSC_MAX_OPS], t_need[OPSC_MAX_OPS];
+  __shared__ int changed;
+  const OpscDag& d = a.d;
+  for (int v = threadIdx.x; v < d.n_ops; v += blockDim.x) t_need[v] = 1;
+  __syncthreads();
+  while (true) {
+    for (int v = threadIdx.x; v < d.n_ops; v += blockDim.x) {
+      if (!t_need[v] || S.r[v] <= 1) continue;
+      uint32_t st = 0;
+      const Pred o = predict(d, qps, L, ph, v, S.p[v], S.r[v] - 1, S.b[v], &st);
+      if (st) atomicOr(&S.st, st);
+      t_ok[v] = o.stable;
+      t_wt[v] = weight(o, d.layer_count[v]);
+      t_soj[v] = o.wait + o.service;
+      t_need[v] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      changed = 0;
       for (int v = 0; v < d.n_ops; ++v) {
-        if (S.r[v] <= 1) continue;
-        uint32_t st = 0;
-        const Pred o = predict(d, qps, L, ph, v, S.p[v], S.r[v] - 1, S.b[v], &st);
-        S.st |= st;
-        if (!o.stable) continue;
-        const double wv = weight(o, d.layer_count[v]);
-        if (!(trial_latency(d, S.wt, v, wv) <= target)) continue;
+        if (S.r[v] <= 1 || !t_ok[v]) continue;
+        if (!(trial_latency(d, S.wt, v, t_wt[v]) <= target)) continue;
         S.r[v] -= 1;
-        S.wt[v] = wv;
-        S.soj[v] = o.wait + o.service;
+        S.wt[v] = t_wt[v];
+        S.soj[v] = t_soj[v];
         S.lat = crit_path(d, S.wt, S.path);
         push_trace(S, out, w, OPSC_ACT_PRUNE, v, S.r[v], S.b[v], S.p[v], S.lat, objective(S, d.n_ops));
-        changed = true;
+        t_need[v] = 1;
+        changed = 1;
       }
     }
+    __syncthreads();
+    if (!changed) break;
   }
-  __syncthreads();
 }
 
 // Greedy state carried from phase 1 (init + first loop) to phase 2 (reseed,

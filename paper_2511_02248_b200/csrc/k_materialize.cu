@@ -154,51 +154,81 @@ __device__ uint32_t place_default_stream(const OpscDag& d, const OpscPlaceSpec& 
   return 0;
 }
 
-__global__ void __launch_bounds__(64) materialize_kernel(const __grid_constant__ OpscDag d,
-                                                         const __grid_constant__ OpscWindows win,
-                                                         int config_order,
-                                                         const __grid_constant__ OpscPlaceSpec pl,
-                                                         const __grid_constant__ OpscDecisions out) {
-  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+// One warp per window: lane v predicts operator v (its Erlang-B recurrences
+// run in parallel lanes) and its Eq. 9 energy terms; lane 0 then runs the
+// order-dependent parts (critical path, placement, the energy sum in the
+// plan's config order), exactly as the sequential reference.
+constexpr int kMatWarps = 4;
+
+__global__ void __launch_bounds__(32 * kMatWarps) materialize_kernel(const __grid_constant__ OpscDag d,
+                                                                     const __grid_constant__ OpscWindows win,
+                                                                     int config_order,
+                                                                     const __grid_constant__ OpscPlaceSpec pl,
+                                                                     const __grid_constant__ OpscDecisions out) {
+  __shared__ double s_wt[kMatWarps][OPSC_MAX_OPS], s_T[kMatWarps][OPSC_MAX_OPS];
+  __shared__ double s_e1[kMatWarps][OPSC_MAX_OPS], s_e2[kMatWarps][OPSC_MAX_OPS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = blockIdx.x * kMatWarps + warp;
   if (w >= win.n) return;
   const int n = d.n_ops;
-  uint32_t st = out.status[w];
-  out.latency[w] = OPSC_INF;
-  out.objective[w] = 0;
-  out.energy[w] = 0.0;
-  out.memory[w] = 0.0;
-  out.devices[w] = 0;
-  for (int v = 0; v < n; ++v) {
-    out.path[(size_t)w * n + v] = -1;
-    out.stable[(size_t)w * n + v] = 0;
-    for (int f = 0; f < OPSC_PRED_FIELDS; ++f) out.pred[((size_t)w * n + v) * OPSC_PRED_FIELDS + f] = 0.0;
+  const uint32_t st0 = out.status[w];
+  if (lane < n) {
+    out.path[(size_t)w * n + lane] = -1;
+    out.stable[(size_t)w * n + lane] = 0;
+    for (int f = 0; f < OPSC_PRED_FIELDS; ++f) out.pred[((size_t)w * n + lane) * OPSC_PRED_FIELDS + f] = 0.0;
   }
-  if (st & (OPSC_W_IDLE | OPSC_W_NO_STABLE_BOUNDS | OPSC_W_NO_STABLE_PARAMS | OPSC_W_NO_STABLE_MODEL |
-            OPSC_W_NO_STABLE_INIT))
+  if (lane == 0) {
+    out.latency[w] = OPSC_INF;
+    out.objective[w] = 0;
+    out.energy[w] = 0.0;
+    out.memory[w] = 0.0;
+    out.devices[w] = 0;
+  }
+  if (st0 & (OPSC_W_IDLE | OPSC_W_NO_STABLE_BOUNDS | OPSC_W_NO_STABLE_PARAMS | OPSC_W_NO_STABLE_MODEL |
+             OPSC_W_NO_STABLE_INIT))
     return;
   const int16_t* c = out.cfg + (size_t)w * n * 3;
   const double qps = win.qps[w];
   const int L = win.seq_len[w], ph = win.phase[w];
-  double wt[OPSC_MAX_OPS], T[OPSC_MAX_OPS];
-  bool all = true;
-  int obj = 0;
-  for (int v = 0; v < n; ++v) {
-    const Pred o = predict(d, qps, L, ph, v, c[v * 3], c[v * 3 + 1], c[v * 3 + 2], &st);
+  const bool feas = out.feasible[w] != 0;
+  uint32_t st = 0;
+  bool stable = true;
+  if (lane < n) {
+    const int v = lane;
+    const int p = c[v * 3], r = c[v * 3 + 1], b = c[v * 3 + 2];
+    const Pred o = predict(d, qps, L, ph, v, p, r, b, &st);
     double* pf = out.pred + ((size_t)w * n + v) * OPSC_PRED_FIELDS;
     pf[0] = o.t; pf[1] = o.lam; pf[2] = o.mu; pf[3] = o.util;
     pf[4] = o.wait; pf[5] = o.service; pf[6] = o.comm;
     out.stable[(size_t)w * n + v] = o.stable;
-    all &= o.stable;
-    wt[v] = weight(o, d.layer_count[v]);
-    T[v] = o.t;
-    obj += (int)c[v * 3] * (int)c[v * 3 + 1];
+    stable = o.stable;
+    s_wt[warp][v] = weight(o, d.layer_count[v]);
+    s_T[warp][v] = o.t;
+    if (feas) {
+      // request_energy terms under default-stream placement: factors 1,
+      // t_eff = (T * R) / R (placement.py:257), wait re-derived from t_eff
+      const double layers = (double)d.layer_count[v];
+      const double t_eff = (o.t * (double)r) / (double)r;
+      const double mu = 1.0 / (t_eff * layers), lam = qps / (double)b;
+      const double wait = lam < (double)r * mu ? expected_wait(lam, mu, r) : OPSC_INF;
+      const double wl = wait * layers, sl = t_eff * layers;
+      s_e1[warp][v] = ((pl.alpha * (double)p) * (double)r) * (wl + sl);
+      s_e2[warp][v] = pl.beta * sl;
+    }
   }
+  const bool all = __all_sync(0xffffffffu, stable);
+  st = __reduce_or_sync(0xffffffffu, st);
+  __syncwarp();
+  if (lane != 0) return;
+  int obj = 0;
+  for (int v = 0; v < n; ++v) obj += (int)c[v * 3] * (int)c[v * 3 + 1];
   out.objective[w] = obj;
-  if (all) out.latency[w] = critical_path(d, wt, out.path + (size_t)w * n);
-  if (out.feasible[w]) {
+  if (all) out.latency[w] = critical_path(d, s_wt[warp], out.path + (size_t)w * n);
+  st |= st0;
+  if (feas) {
     int dev = 0;
     double mem = 0.0;
-    const uint32_t e = place_default_stream(d, pl, c, T, L, &dev, &mem);
+    const uint32_t e = place_default_stream(d, pl, c, s_T[warp], L, &dev, &mem);
     st |= e;
     if (!e) {
       out.devices[w] = dev;
@@ -206,14 +236,8 @@ __global__ void __launch_bounds__(64) materialize_kernel(const __grid_constant__
       double total = 0.0;
       for (int i = 0; i < n; ++i) {
         const int v = config_order == 0 ? i : d.node_order[i];
-        const int p = c[v * 3], r = c[v * 3 + 1], b = c[v * 3 + 2];
-        const double layers = (double)d.layer_count[v];
-        const double t_eff = (T[v] * (double)r) / (double)r;
-        const double mu = 1.0 / (t_eff * layers), lam = qps / (double)b;
-        const double wait = lam < (double)r * mu ? expected_wait(lam, mu, r) : OPSC_INF;
-        const double wl = wait * layers, sl = t_eff * layers;
-        total = total + ((pl.alpha * (double)p) * (double)r) * (wl + sl);
-        total = total + pl.beta * sl;
+        total = total + s_e1[warp][v];
+        total = total + s_e2[warp][v];
       }
       out.energy[w] = total;
     }
@@ -224,7 +248,7 @@ __global__ void __launch_bounds__(64) materialize_kernel(const __grid_constant__
 cudaError_t launch_materialize(const OpscDag& d, OpscWindows w, int config_order, const OpscPlaceSpec& p,
                                OpscDecisions out, cudaStream_t s) {
   if (w.n <= 0) return cudaSuccess;
-  materialize_kernel<<<(w.n + 63) / 64, 64, 0, s>>>(d, w, config_order, p, out);
+  materialize_kernel<<<(w.n + kMatWarps - 1) / kMatWarps, 32 * kMatWarps, 0, s>>>(d, w, config_order, p, out);
   return cudaGetLastError();
 }
 
