@@ -286,6 +286,54 @@ OPSC_API int opsc_model_grid_table(const OpscDag* dag, const OpscModelSpec* spec
                                    int16_t* cfg, uint8_t* feasible, uint32_t* status,
                                    void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- shared (interference-aware) placement, Alg. 2 (placement.py:399-462) ---- */
+
+/* Fleet (DeviceSpec, devices in sorted-id order), PlacementParams,
+ * InterferenceParams and EnergyParams (placement.py:46-55, 112-117;
+ * perfmodel.py:67-76; metrics.py:34-47). */
+typedef struct OpscPlaceShared {
+  int32_t n_devices;
+  const double* mem_cap;     /* [n_devices] */
+  const double* compute_cap; /* [n_devices] */
+  double slo;                /* PlacementParams.slo */
+  double slack_weight_mem;
+  double slack_weight_compute;
+  double max_sm_load;
+  double theta;              /* InterferenceParams */
+  double exponent;           /* 1.0 / 2.0 / 0.5 bit-exact; other values use pow() */
+  double alpha;              /* EnergyParams */
+  double beta;
+} OpscPlaceShared;
+
+/* Placement of each window's plan; per-window capacities. */
+typedef struct OpscPlacement {
+  int32_t cap_assign;    /* assignment slots per window (>= sum of R)        */
+  int32_t cap_dev;       /* device-load slots per window                     */
+  int32_t* n_assign;     /* [W]                                              */
+  int32_t* devices_used; /* [W]                                              */
+  uint8_t* feasible;     /* [W] recomputed latency <= slo                    */
+  uint32_t* status;      /* [W] OPSC_W_FLEET_EXHAUSTED / INFEASIBLE_PLACEMENT */
+  double* latency;       /* [W] recomputed_latency                           */
+  double* energy;        /* [W] request_energy under this placement          */
+  double* memory;        /* [W] provisioned_memory                           */
+  int8_t* a_op;          /* [W][cap_assign] lex rank                         */
+  int16_t* a_replica;
+  int32_t* a_device;     /* sorted-id device index                          */
+  int16_t* a_share;      /* sm_share percent                                 */
+  double* a_latency;     /* interference_adjusted_latency                    */
+  double* d_mem;         /* [W][cap_dev] DeviceLoad.mem_used                 */
+  double* d_sm;          /* DeviceLoad.sm_demand (standing load)             */
+  double* d_energy;      /* fill_device_energy                              */
+} OpscPlacement;
+
+/* place() + request_energy + fill_device_energy + provisioned_memory for the
+ * decided plan of every window (cfg [W][n][3] lex-rank order, plan feasible
+ * flags; config_order as in opsc_materialize). Windows whose plan is not
+ * feasible or idle are skipped (n_assign = 0). */
+OPSC_API int opsc_place_shared(const OpscDag* dag, const OpscPlaceShared* fleet, OpscWindows win,
+                               const int16_t* cfg, const uint8_t* plan_feasible,
+                               int32_t config_order, OpscPlacement out, void* stream);
+
 /* ---- trace windowing (workload.py:107-158) ---- */
 
 /* A request trace as structure of arrays (RequestRecord, workload.py:31-35). */

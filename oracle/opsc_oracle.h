@@ -61,6 +61,11 @@ int orc_greedy(const OpscDag* dag, const OpscGreedySpec* spec, OpscWindows win,
                const int16_t* uniform_cfg, const uint8_t* uniform_feasible,
                const uint32_t* uniform_status, OpscDecisions out, int32_t n_threads);
 
+/* shared placement + placement metrics (opsc_oracle_place.c) */
+int orc_place_shared(const OpscDag* dag, const OpscPlaceShared* fleet, OpscWindows win,
+                     const int16_t* cfg, const uint8_t* plan_feasible, int32_t config_order,
+                     OpscPlacement out, int32_t n_threads);
+
 /* windowize (workload.py:107-158); returns n_windows or -1 if > max_windows. */
 int32_t orc_windowize(OpscTraceRecords rec, double window_len, double quantile,
                       int32_t max_windows, double* prefill_qps, int32_t* prefill_len,

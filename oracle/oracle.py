@@ -60,11 +60,12 @@ def lib():
         L.orc_materialize.argtypes = [P, abi.OpscWindows, I, P, abi.OpscDecisions, I]
         L.orc_plan_windows.argtypes = [I, P, P, P, P, P, abi.OpscWindows, abi.OpscDecisions, I]
         L.orc_greedy.argtypes = [P, P, abi.OpscWindows, P, P, P, abi.OpscDecisions, I]
+        L.orc_place_shared.argtypes = [P, P, abi.OpscWindows, P, P, I, abi.OpscPlacement, I]
         L.orc_windowize.argtypes = [abi.OpscTraceRecords, D, D, I, P, P, P]
         L.orc_windowize.restype = I
         for f in ("orc_menu_build", "orc_stability_check", "orc_compose_argmin",
                   "orc_menu_fallback", "orc_decode_decisions", "orc_model_grid",
-                  "orc_materialize", "orc_plan_windows", "orc_greedy"):
+                  "orc_materialize", "orc_plan_windows", "orc_greedy", "orc_place_shared"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -125,3 +126,17 @@ def windowize(arrival, input_len, output_len, window_len=60.0, quantile=0.95, ma
     if n < 0:
         raise ValueError("more windows than max_windows")
     return pq[:n].copy(), pl[:n].copy(), dq[:n].copy()
+
+
+def place_shared(problem, windows, cfg, plan_feasible, fleet, config_order, n_threads=None):
+    """Shared placement + metrics of decided plans on the CPU (PlacementArrays)."""
+    from paper_2511_02248_b200 import placement
+    cfg = np.ascontiguousarray(cfg, dtype=np.int16)
+    feas = np.ascontiguousarray(plan_feasible, dtype=np.uint8)
+    ca, cd = placement.capacities(cfg, fleet.spec.n_devices)
+    out = placement.PlacementArrays(windows.n, ca, cd)
+    rc = lib().orc_place_shared(ref(problem.table), ref(fleet.spec), windows.struct(), cfg.ctypes.data,
+                                feas.ctypes.data, config_order, out.struct(), n_threads or threads())
+    if rc != abi.OK:
+        raise RuntimeError(f"oracle status {rc}")
+    return out

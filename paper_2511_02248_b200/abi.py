@@ -101,3 +101,15 @@ class OpscDecisions(C.Structure):
 class OpscTraceRecords(C.Structure):
     _fields_ = [("n", C.c_int64), ("arrival", C.c_void_p), ("input_len", C.c_void_p),
                 ("output_len", C.c_void_p)]
+
+
+class OpscPlaceShared(C.Structure):
+    _fields_ = [("n_devices", _I), ("mem_cap", C.c_void_p), ("compute_cap", C.c_void_p),
+                ("slo", _D), ("slack_weight_mem", _D), ("slack_weight_compute", _D),
+                ("max_sm_load", _D), ("theta", _D), ("exponent", _D), ("alpha", _D), ("beta", _D)]
+
+
+class OpscPlacement(C.Structure):
+    _fields_ = [("cap_assign", _I), ("cap_dev", _I)] + [(name, C.c_void_p) for name in (
+        "n_assign", "devices_used", "feasible", "status", "latency", "energy", "memory",
+        "a_op", "a_replica", "a_device", "a_share", "a_latency", "d_mem", "d_sm", "d_energy")]

@@ -1,0 +1,83 @@
+"""Shared (interference-aware) placement of decided plans -- Alg. 2 of the
+reference (placement.py:399-462) -- and its Eq. 9 energy / memory metrics
+(metrics.py:84-132), as packed C-ABI inputs and SoA outputs.
+
+`place_windows` runs opsc_place_shared on the GPU (one CTA per window);
+`placement_objects` turns the arrays into reference-shaped Placement objects.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import abi
+
+
+class SharedFleet:
+    """Fleet (devices sorted by id, placement.py:155-156) + PlacementParams +
+    InterferenceParams + EnergyParams packed as an OpscPlaceShared."""
+
+    def __init__(self, fleet, slo, interference=None, energy=None, slack_weight_mem=0.5,
+                 slack_weight_compute=0.5, max_sm_load=1.5):
+        if not fleet:
+            raise ValueError("fleet must not be empty")
+        self.devices = sorted(fleet, key=lambda d: d.id)
+        self.mem_cap = np.array([float(d.mem_cap) for d in self.devices])
+        self.compute_cap = np.array([float(getattr(d, "compute_cap", 1.0)) for d in self.devices])
+        s = abi.OpscPlaceShared()
+        s.n_devices = len(self.devices)
+        s.mem_cap, s.compute_cap = self.mem_cap.ctypes.data, self.compute_cap.ctypes.data
+        s.slo = float(slo)
+        s.slack_weight_mem, s.slack_weight_compute = float(slack_weight_mem), float(slack_weight_compute)
+        s.max_sm_load = float(max_sm_load)
+        s.theta = float(interference.theta) if interference is not None else 0.5
+        s.exponent = float(interference.exponent) if interference is not None else 1.0
+        s.alpha = float(energy.alpha) if energy is not None else 0.3 * 400.0
+        s.beta = float(energy.beta) if energy is not None else 0.7 * 400.0
+        self.spec = s
+
+    @classmethod
+    def from_params(cls, fleet, placement_params, profiles, energy=None):
+        p = placement_params
+        return cls(fleet, p.slo, getattr(profiles, "interference", None), energy,
+                   p.slack_weight_mem, p.slack_weight_compute, p.max_sm_load)
+
+
+class PlacementArrays:
+    """Host SoA of OpscPlacement for W windows."""
+
+    FIELDS = ("n_assign", "devices_used", "feasible", "status", "latency", "energy", "memory",
+              "a_op", "a_replica", "a_device", "a_share", "a_latency", "d_mem", "d_sm", "d_energy")
+
+    def __init__(self, n_windows, cap_assign, cap_dev):
+        W, A, D = n_windows, max(1, cap_assign), max(1, cap_dev)
+        self.cap_assign, self.cap_dev = A, D
+        self.n_assign = np.zeros(W, np.int32)
+        self.devices_used = np.zeros(W, np.int32)
+        self.feasible = np.zeros(W, np.uint8)
+        self.status = np.zeros(W, np.uint32)
+        self.latency = np.zeros(W)
+        self.energy = np.zeros(W)
+        self.memory = np.zeros(W)
+        self.a_op = np.zeros((W, A), np.int8)
+        self.a_replica = np.zeros((W, A), np.int16)
+        self.a_device = np.zeros((W, A), np.int32)
+        self.a_share = np.zeros((W, A), np.int16)
+        self.a_latency = np.zeros((W, A))
+        self.d_mem = np.zeros((W, D))
+        self.d_sm = np.zeros((W, D))
+        self.d_energy = np.zeros((W, D))
+
+    def struct(self):
+        s = abi.OpscPlacement()
+        s.cap_assign, s.cap_dev = self.cap_assign, self.cap_dev
+        for f in self.FIELDS:
+            setattr(s, f, getattr(self, f).ctypes.data)
+        return s
+
+
+def capacities(cfg, n_devices):
+    """Assignment / device slots needed by the plans in cfg [W][n][3]:
+    every replica is one assignment and needs at most one device."""
+    total_r = int(cfg[:, :, 1].sum(axis=1).max()) if cfg.size else 1
+    return max(1, total_r), max(1, min(int(n_devices), total_r))
