@@ -330,9 +330,12 @@ typedef struct OpscPlacement {
  * decided plan of every window (cfg [W][n][3] lex-rank order, plan feasible
  * flags; config_order as in opsc_materialize). Windows whose plan is not
  * feasible or idle are skipped (n_assign = 0). */
+OPSC_API size_t opsc_place_shared_workspace(int32_t n_windows, int32_t cap_assign, int32_t cap_dev,
+                                            int32_t n_ops);
 OPSC_API int opsc_place_shared(const OpscDag* dag, const OpscPlaceShared* fleet, OpscWindows win,
                                const int16_t* cfg, const uint8_t* plan_feasible,
-                               int32_t config_order, OpscPlacement out, void* stream);
+                               int32_t config_order, OpscPlacement out, void* workspace,
+                               size_t workspace_bytes, void* stream);
 
 /* ---- trace windowing (workload.py:107-158) ---- */
 

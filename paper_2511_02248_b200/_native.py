@@ -26,7 +26,7 @@ EXPORTS = (
     "opsc_ctx_destroy", "opsc_plan_windows_host", "opsc_ctx_last_launches", "opsc_fp64_peak",
     "opsc_candidate_probe", "opsc_greedy", "opsc_windowize", "opsc_windowize_workspace",
     "opsc_greedy_state_bytes", "opsc_greedy_phase", "opsc_model_table_bytes",
-    "opsc_model_grid_table",
+    "opsc_model_grid_table", "opsc_place_shared_workspace", "opsc_place_shared",
 )
 
 _lib = None
@@ -66,6 +66,8 @@ def load():
             "opsc_windowize_workspace": ([C.c_int64, I], C.c_size_t),
             "opsc_greedy_state_bytes": ([I], C.c_size_t),
             "opsc_model_table_bytes": ([P, I, I], C.c_size_t),
+            "opsc_place_shared_workspace": ([I, I, I, I], C.c_size_t),
+            "opsc_place_shared": ([P, P, W, P, P, I, abi.OpscPlacement, P, C.c_size_t, P], C.c_int),
             "opsc_model_grid_table": ([P, P, W, P, P, P, P, C.c_size_t, P], C.c_int),
             "opsc_greedy_phase": ([P, P, W, I, P, P, P, P, D, P], C.c_int),
             "opsc_windowize": ([abi.OpscTraceRecords, C.c_double, C.c_double, I, P, P, P, P, P,

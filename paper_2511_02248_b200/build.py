@@ -19,6 +19,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT, "libopscale_b200.so")
 SOURCES = ["k_menu.cu", "k_compose.cu", "k_model.cu", "k_materialize.cu", "k_greedy.cu", "k_windowize.cu",
+           "k_place.cu",
            "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -353,6 +353,19 @@ int opsc_ctx_last_launches(const OpscContext* c, int32_t* launches) {
   return OPSC_OK;
 }
 
+size_t opsc_place_shared_workspace(int32_t n_windows, int32_t cap_assign, int32_t cap_dev, int32_t n_ops) {
+  return place_shared_workspace(n_windows, cap_assign, cap_dev, n_ops);
+}
+
+int opsc_place_shared(const OpscDag* dag, const OpscPlaceShared* fleet, OpscWindows win, const int16_t* cfg,
+                      const uint8_t* plan_feasible, int32_t config_order, OpscPlacement out, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  if (!valid_dag(dag) || !fleet || fleet->n_devices < 1 || out.cap_assign < 1 || out.cap_dev < 1)
+    return OPSC_ERR_ARG;
+  return from_cuda(launch_place_shared(*dag, *fleet, win, cfg, plan_feasible, config_order, out, workspace,
+                                       workspace_bytes, (cudaStream_t)stream));
+}
+
 size_t opsc_windowize_workspace(int64_t n_records, int32_t max_windows) {
   return windowize_workspace(n_records, max_windows);
 }

@@ -1,0 +1,495 @@
+// k_place.cu -- K6: shared (interference-aware) placement, Alg. 2 of the
+// reference (placement.py:399-462), with its placement-dependent metrics
+// (request_energy, fill_device_energy, provisioned_memory; metrics.py:84-132).
+//
+// One CTA per window. Base instances are packed first-fit-decreasing
+// (placement.py:358-385, sequential, thread 0). Each extra replica, heaviest
+// op_latency first (:388-396), probes every used device; a probe needs the
+// interference factors of the device's members with the tentative replica
+// added (:209-231), the adjusted service time and Erlang-C wait of every
+// operator with a replica there (:245-273) and the critical path. Those
+// (device, operator) re-evaluations -- the Erlang-B recurrences -- run in
+// parallel threads; thread 0 scores the feasible devices by weighted slack
+// (:338-351, best score, ties to the lowest device id) and commits.
+// Sums the reference takes with Python's sum() use CPython 3.12's Neumaier
+// summation (PySum), in the reference's iteration order.
+#include "opsc_common.cuh"
+
+namespace opsc {
+
+constexpr int kPlaceThreads = 128;
+constexpr int kMaxDevProbe = 128;  // device probes per chunk held in smem
+
+struct PlaceArgs {
+  OpscDag d;
+  OpscPlaceShared f;
+};
+
+struct PWork {  // per-window global workspace
+  int32_t* a_group;
+  int32_t* a_next;
+  double* a_dem;
+  double* a_mem;
+  double* a_fac;
+  int32_t* dev_head;
+  int32_t* dev_tail;
+  int32_t* dev_cnt;
+  double* dev_mem_f;
+  double* dev_mem_c;
+  int32_t* rep;  // [sum R] assignment index per (op, replica), -1 unplaced
+};
+
+__host__ __device__ inline size_t pw_bytes(int A, int D, int n) {
+  (void)n;
+  return (size_t)A * (4 + 4 + 8 + 8 + 8) + (size_t)D * (4 + 4 + 4 + 8 + 8) + (size_t)A * 4 + 64;
+}
+
+__device__ PWork carve(unsigned char* base, int A, int D) {
+  PWork p;
+  double* dp = (double*)base;
+  p.a_dem = dp; dp += A;
+  p.a_mem = dp; dp += A;
+  p.a_fac = dp; dp += A;
+  p.dev_mem_f = dp; dp += D;
+  p.dev_mem_c = dp; dp += D;
+  int32_t* ip = (int32_t*)dp;
+  p.a_group = ip; ip += A;
+  p.a_next = ip; ip += A;
+  p.dev_head = ip; ip += D;
+  p.dev_tail = ip; ip += D;
+  p.dev_cnt = ip; ip += D;
+  p.rep = ip;
+  return p;
+}
+
+__device__ __forceinline__ double pow_expo(double x, double e) {
+  if (e == 1.0) return x;
+  if (e == 2.0) return x * x;
+  if (e == 0.5) return sqrt(x);
+  return pow(x, e);
+}
+
+__device__ __forceinline__ double interference(const OpscPlaceShared& f, double load, double adding) {
+  const double excess = load + adding - 1.0;
+  if (excess <= 0.0) return 1.0;
+  return 1.0 + f.theta * pow_expo(excess, f.exponent);
+}
+
+__device__ __forceinline__ double psum_value(double f, double c, bool started) {
+  if (!started) return 0.0;
+  return (c != 0.0 && isfinite(c)) ? f + c : f;
+}
+
+// standing load of device `dev` (+ optional extra member of group xg, demand xd):
+// Neumaier sum of group maxima in insertion order; returns total, and the
+// group max of `query_group` in *qmax
+__device__ double dev_load(const PWork& P, int dev, int xg, double xd, int query_group, double* qmax) {
+  // groups of one device are few; scan members for first occurrences
+  PySum t;
+  t.reset();
+  double qm = 0.0;
+  for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) {
+    const int g = P.a_group[i];
+    bool first = true;
+    for (int j = P.dev_head[dev]; j != i; j = P.a_next[j]) first &= P.a_group[j] != g;
+    if (!first) continue;
+    double m = 0.0;
+    for (int j = i; j >= 0; j = P.a_next[j])
+      if (P.a_group[j] == g) m = m >= P.a_dem[j] ? m : P.a_dem[j];
+    if (g == xg) m = m >= xd ? m : xd;
+    t.add(m);
+    if (g == query_group) qm = m;
+  }
+  if (xg >= 0) {  // the extra's group is new (extras own their group)
+    bool seen = false;
+    for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) seen |= P.a_group[i] == xg;
+    if (!seen) {
+      const double m = 0.0 >= xd ? 0.0 : xd;
+      t.add(m);
+      if (xg == query_group) qm = m;
+    }
+  }
+  if (qmax) *qmax = qm;
+  return t.value();
+}
+
+// interference factor of member i of `dev` with an optional extra (group xg, demand xd)
+__device__ double member_factor(const PWork& P, const OpscPlaceShared& f, int dev, int i, int xg, double xd,
+                                double total) {
+  double gm = 0.0;
+  for (int j = P.dev_head[dev]; j >= 0; j = P.a_next[j])
+    if (P.a_group[j] == P.a_group[i]) gm = gm >= P.a_dem[j] ? gm : P.a_dem[j];
+  if (xg == P.a_group[i]) gm = gm >= xd ? gm : xd;
+  return interference(f, total - gm, P.a_dem[i]);
+}
+
+struct OpAdj {
+  double t_eff, wait, wt;
+  bool stable;
+};
+
+// adjusted figures of op u: factors of its replicas (k = 1..R) with the
+// members of `dev` re-evaluated under the extra (xg, xd, xop, xk, xf)
+__device__ OpAdj adjust_op(const OpscDag& d, const OpscPlaceShared& f, const PWork& P, const int* rep_off,
+                           const int32_t* adev, int u, int p, int r, int b, double T, double comm, double qps,
+                           int dev, int xg, double xd, int xop, int xk, double xf, double total) {
+  PySum s;
+  s.reset();
+  for (int k = 1; k <= r; ++k) {
+    const int idx = P.rep[rep_off[u] + k - 1];
+    double fk = 1.0;
+    if (idx >= 0) {
+      const bool on_dev = dev >= 0 && adev[idx] == dev;
+      fk = on_dev ? member_factor(P, f, dev, idx, xg, xd, total) : P.a_fac[idx];
+    } else if (u == xop && k == xk) {
+      fk = xf;
+    }
+    s.add(fk);
+  }
+  OpAdj o;
+  o.t_eff = (T * s.value()) / (double)r;
+  const double layers = (double)d.layer_count[u];
+  const double mu = 1.0 / (o.t_eff * layers), lam = qps / (double)b;
+  o.stable = lam < (double)r * mu;
+  o.wait = o.stable ? expected_wait(lam, mu, r) : OPSC_INF;
+  o.wt = ((o.wait + o.t_eff / (double)b) + comm) * layers;
+  return o;
+}
+
+__device__ double dp_latency(const OpscDag& d, const double* wt) {
+  double val[OPSC_MAX_OPS];
+  double top = 0.0;
+  for (int i = 0; i < d.n_ops; ++i) {
+    const int v = d.topo[i];
+    double in = 0.0;
+    uint32_t pm = d.pred_mask[v];
+    while (pm) {
+      const int q = __ffs(pm) - 1;
+      pm &= pm - 1;
+      in = fmax(in, val[q]);
+    }
+    val[v] = in + wt[v];
+    if (d.sink_mask >> v & 1u) top = fmax(top, val[v]);
+  }
+  return top;
+}
+
+struct PShared {
+  int p[OPSC_MAX_OPS], r[OPSC_MAX_OPS], b[OPSC_MAX_OPS];
+  double T[OPSC_MAX_OPS], comm[OPSC_MAX_OPS], dem[OPSC_MAX_OPS], mem[OPSC_MAX_OPS];
+  int rep_off[OPSC_MAX_OPS + 1];
+  double cur_wt[OPSC_MAX_OPS], cur_teff[OPSC_MAX_OPS], cur_wait[OPSC_MAX_OPS];
+  bool cur_stable[OPSC_MAX_OPS];
+  uint32_t on_dev[kMaxDevProbe];    // ops with a replica on device d (bitmask)
+  double dev_total[kMaxDevProbe];   // standing load with the tentative replica
+  double dev_load0[kMaxDevProbe];   // standing load without it
+  double dev_xf[kMaxDevProbe];      // tentative replica's factor on d
+  uint8_t dev_ok[kMaxDevProbe];
+  double probe_wt[kMaxDevProbe][OPSC_MAX_OPS];
+  int used, na, err, best;
+};
+
+__global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_constant__ PlaceArgs a,
+                                                              const __grid_constant__ OpscWindows win,
+                                                              const int16_t* __restrict__ cfg,
+                                                              const uint8_t* __restrict__ plan_feasible,
+                                                              int config_order,
+                                                              const __grid_constant__ OpscPlacement out,
+                                                              unsigned char* __restrict__ ws) {
+  __shared__ PShared S;
+  const OpscDag& d = a.d;
+  const OpscPlaceShared& f = a.f;
+  const int n = d.n_ops;
+  const int w = blockIdx.x;
+  const int A = out.cap_assign, D = out.cap_dev;
+  if (threadIdx.x == 0) {
+    out.n_assign[w] = 0; out.devices_used[w] = 0; out.feasible[w] = 0; out.status[w] = 0;
+    out.latency[w] = 0.0; out.energy[w] = 0.0; out.memory[w] = 0.0;
+  }
+  const double qps = win.qps[w];
+  if (!(qps > 0.0) || !plan_feasible[w]) return;
+  const int L = win.seq_len[w], ph = win.phase[w];
+  PWork P = carve(ws + (size_t)w * pw_bytes(A, D, n), A, D);
+  const int32_t* adev = out.a_device + (size_t)w * A;
+  if (threadIdx.x == 0) {
+    S.rep_off[0] = 0;
+    for (int v = 0; v < n; ++v) {
+      S.p[v] = cfg[((size_t)w * n + v) * 3];
+      S.r[v] = cfg[((size_t)w * n + v) * 3 + 1];
+      S.b[v] = cfg[((size_t)w * n + v) * 3 + 2];
+      S.rep_off[v + 1] = S.rep_off[v] + S.r[v];
+    }
+    S.err = S.rep_off[n] > A ? OPSC_W_TRACE_TRUNCATED : 0;
+    S.used = 0;
+    S.na = 0;
+  }
+  __syncthreads();
+  if (S.err) {
+    if (threadIdx.x == 0) out.status[w] = S.err;
+    return;
+  }
+  for (int v = threadIdx.x; v < n; v += blockDim.x) {
+    uint32_t st = 0;
+    const Pred o = predict(d, qps, L, ph, v, S.p[v], S.r[v], S.b[v], &st);
+    S.T[v] = o.t;
+    S.comm[v] = o.comm;
+    const double dm = d.s0[v] + (d.s1[v] * (double)S.b[v]) * (double)L;
+    S.dem[v] = 1.0 <= dm ? 1.0 : dm;
+    S.mem[v] = (d.weight_mem[v] / (double)S.p[v] + d.m0[v]) + (d.m1[v] * (double)S.b[v]) * (double)L;
+  }
+  for (int i = threadIdx.x; i < S.rep_off[n]; i += blockDim.x) P.rep[i] = -1;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) {
+    P.dev_head[i] = -1; P.dev_tail[i] = -1; P.dev_cnt[i] = 0;
+    P.dev_mem_f[i] = 0.0; P.dev_mem_c[i] = 0.0;
+  }
+  __syncthreads();
+
+  // thread 0 helpers -------------------------------------------------------
+  auto push = [&](int v, int k, int dev, int group, int share) {
+    const int i = S.na++;
+    P.a_group[i] = group;
+    P.a_next[i] = -1;
+    P.a_dem[i] = S.dem[v];
+    P.a_mem[i] = S.mem[v];
+    P.a_fac[i] = 1.0;
+    if (P.dev_tail[dev] >= 0) P.a_next[P.dev_tail[dev]] = i;
+    else P.dev_head[dev] = i;
+    P.dev_tail[dev] = i;
+    // device memory: Python sum over members in order
+    const double x = S.mem[v];
+    if (P.dev_cnt[dev] == 0) {
+      P.dev_mem_f[dev] = 0.0 + x;
+      P.dev_mem_c[dev] = 0.0;
+    } else {
+      const double fs = P.dev_mem_f[dev], t = fs + x;
+      if (fabs(fs) >= fabs(x)) P.dev_mem_c[dev] += (fs - t) + x;
+      else P.dev_mem_c[dev] += (x - t) + fs;
+      P.dev_mem_f[dev] = t;
+    }
+    P.dev_cnt[dev]++;
+    P.rep[S.rep_off[v] + k - 1] = i;
+    const size_t o = (size_t)w * A + i;
+    out.a_op[o] = (int8_t)v;
+    out.a_replica[o] = (int16_t)k;
+    out.a_device[o] = dev;
+    out.a_share[o] = (int16_t)share;
+  };
+  auto dev_mem = [&](int dev) { return psum_value(P.dev_mem_f[dev], P.dev_mem_c[dev], P.dev_cnt[dev] > 0); };
+  auto refresh_factors = [&](int dev) {
+    const double total = dev_load(P, dev, -1, 0.0, -1, nullptr);
+    for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) P.a_fac[i] = member_factor(P, f, dev, i, -1, 0.0, total);
+  };
+
+  // ---- base instances (placement.py:358-385), thread 0
+  int k_base = 1 << 30;
+  for (int v = 0; v < n; ++v) k_base = min(k_base, S.r[v]);
+  if (threadIdx.x == 0) {
+    int order[OPSC_MAX_OPS];
+    double key[OPSC_MAX_OPS];
+    for (int v = 0; v < n; ++v) { order[v] = v; key[v] = -(d.weight_mem[v] / (double)S.p[v]); }
+    for (int i = 1; i < n; ++i) {
+      const int x = order[i];
+      int j = i - 1;
+      while (j >= 0 && key[order[j]] > key[x]) { order[j + 1] = order[j]; --j; }
+      order[j + 1] = x;
+    }
+    for (int inst = 1; inst <= k_base && !S.err; ++inst) {
+      int idev[OPSC_MAX_OPS], nd = 0;
+      for (int i = 0; i < n && !S.err; ++i) {
+        const int v = order[i];
+        int target = -1;
+        for (int j = 0; j < nd; ++j)
+          if (dev_mem(idev[j]) + S.mem[v] <= f.mem_cap[idev[j]]) { target = idev[j]; break; }
+        if (target < 0) {
+          if (S.used >= f.n_devices || S.used >= D) { S.err = OPSC_W_FLEET_EXHAUSTED; break; }
+          target = S.used++;
+          if (S.mem[v] > f.mem_cap[target]) { S.err = OPSC_W_INFEASIBLE_PLACEMENT; break; }
+          idev[nd++] = target;
+        }
+        push(v, inst, target, inst - 1, 100);
+      }
+    }
+    for (int dev = 0; dev < S.used; ++dev) refresh_factors(dev);
+  }
+  __syncthreads();
+  if (S.err) {
+    if (threadIdx.x == 0) out.status[w] = S.err;
+    return;
+  }
+  // current adjusted figures of every op (parallel over ops)
+  for (int v = threadIdx.x; v < n; v += blockDim.x) {
+    const OpAdj o = adjust_op(d, f, P, S.rep_off, adev, v, S.p[v], S.r[v], S.b[v], S.T[v], S.comm[v], qps, -1, -1,
+                              0.0, -1, 0, 1.0, 0.0);
+    S.cur_wt[v] = o.wt; S.cur_teff[v] = o.t_eff; S.cur_wait[v] = o.wait; S.cur_stable[v] = o.stable;
+  }
+  __syncthreads();
+
+  // ---- extra replicas, heaviest op_latency first (-T, id, k)
+  int xord[OPSC_MAX_OPS];
+  for (int v = 0; v < n; ++v) xord[v] = v;
+  for (int i = 1; i < n; ++i) {
+    const int x = xord[i];
+    int j = i - 1;
+    while (j >= 0 && -S.T[xord[j]] > -S.T[x]) { xord[j + 1] = xord[j]; --j; }
+    xord[j + 1] = x;
+  }
+  int group = k_base;
+  for (int xi = 0; xi < n; ++xi) {
+    const int v = xord[xi];
+    for (int k = k_base + 1; k <= S.r[v]; ++k, ++group) {
+      const double mem = S.mem[v], demand = S.dem[v];
+      const double shf = nearbyint(demand * 100.0);
+      const int share = shf < 1.0 ? 1 : (shf > 100.0 ? 100 : (int)shf);
+      __shared__ int s_best;
+      __shared__ double s_best_score;
+      if (threadIdx.x == 0) s_best = -1;
+      for (int c0 = 0; c0 < S.used; c0 += kMaxDevProbe) {
+      const int U = min(S.used - c0, kMaxDevProbe);
+      // stage 1: per-device admission + tentative group totals
+      for (int dj = threadIdx.x; dj < U; dj += blockDim.x) {
+        const int dev = c0 + dj;
+        const double mu = dev_mem(dev);
+        bool ok = !(mu + mem > f.mem_cap[dev]);
+        const double load = dev_load(P, dev, -1, 0.0, -1, nullptr);
+        ok = ok && !(load + demand > f.max_sm_load);
+        double xg_max = 0.0;
+        const double total = dev_load(P, dev, group, demand, group, &xg_max);
+        uint32_t mask = 0;
+        for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) mask |= 1u << out.a_op[(size_t)w * A + i];
+        S.on_dev[dj] = mask | (1u << v);
+        S.dev_total[dj] = total;
+        S.dev_load0[dj] = load;
+        S.dev_xf[dj] = interference(f, total - xg_max, demand);
+        S.dev_ok[dj] = ok;
+      }
+      __syncthreads();
+      // stage 2: (device, affected op) re-evaluations in parallel
+      for (int t = threadIdx.x; t < U * n; t += blockDim.x) {
+        const int dj = t / n, u = t - dj * n;
+        if (!S.dev_ok[dj]) continue;
+        if (!(S.on_dev[dj] >> u & 1u)) {
+          S.probe_wt[dj][u] = S.cur_stable[u] ? S.cur_wt[u] : OPSC_INF;
+          continue;
+        }
+        const OpAdj o = adjust_op(d, f, P, S.rep_off, adev, u, S.p[u], S.r[u], S.b[u], S.T[u], S.comm[u], qps,
+                                  c0 + dj, group, demand, v, k, S.dev_xf[dj], S.dev_total[dj]);
+        S.probe_wt[dj][u] = o.stable ? o.wt : OPSC_INF;
+      }
+      __syncthreads();
+      // stage 3: recomputed latency must meet the SLO (placement.py:434-438)
+      for (int dj = threadIdx.x; dj < U; dj += blockDim.x) {
+        if (!S.dev_ok[dj]) continue;
+        bool fin = true;
+        for (int u = 0; u < n; ++u) fin &= S.probe_wt[dj][u] != OPSC_INF;
+        const double lat = fin ? dp_latency(d, S.probe_wt[dj]) : OPSC_INF;
+        if (lat > f.slo) S.dev_ok[dj] = 0;
+      }
+      __syncthreads();
+      // weighted slack (placement.py:338-351); best score, ties to the lowest id
+      if (threadIdx.x == 0) {
+        for (int dj = 0; dj < U; ++dj) {
+          if (!S.dev_ok[dj]) continue;
+          const int dev = c0 + dj;
+          const double mu = dev_mem(dev), load = S.dev_load0[dj];
+          const double ms = f.mem_cap[dev] - (mu + mem), cs = f.compute_cap[dev] - (load + demand);
+          const double mf = (0.0 >= ms ? 0.0 : ms) / f.mem_cap[dev];
+          const double cf = (0.0 >= cs ? 0.0 : cs) / f.compute_cap[dev];
+          const double score = f.slack_weight_mem * mf + f.slack_weight_compute * cf;
+          if (s_best < 0 || score > s_best_score) { s_best = dev; s_best_score = score; }
+        }
+      }
+      __syncthreads();
+      }
+      if (threadIdx.x == 0) {
+        int best = s_best;
+        if (best >= 0) {
+          push(v, k, best, group, share);
+        } else if (S.used >= f.n_devices || S.used >= D) {
+          S.err = OPSC_W_FLEET_EXHAUSTED;
+        } else {
+          best = S.used++;
+          if (mem > f.mem_cap[best]) S.err = OPSC_W_INFEASIBLE_PLACEMENT;
+          else push(v, k, best, group, 100);
+        }
+        if (!S.err) refresh_factors(best);
+        S.best = best;
+      }
+      __syncthreads();
+      if (S.err) {
+        if (threadIdx.x == 0) out.status[w] = S.err;
+        return;
+      }
+      // refresh the cached figures of ops with a replica on the chosen device
+      {
+        const int dev = S.best;
+        uint32_t mask = 0;
+        for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) mask |= 1u << out.a_op[(size_t)w * A + i];
+        for (int u = threadIdx.x; u < n; u += blockDim.x) {
+          if (!(mask >> u & 1u)) continue;
+          const OpAdj o = adjust_op(d, f, P, S.rep_off, adev, u, S.p[u], S.r[u], S.b[u], S.T[u], S.comm[u], qps, -1,
+                                    -1, 0.0, -1, 0, 1.0, 0.0);
+          S.cur_wt[u] = o.wt; S.cur_teff[u] = o.t_eff; S.cur_wait[u] = o.wait; S.cur_stable[u] = o.stable;
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- _finalize + metrics (thread 0)
+  if (threadIdx.x == 0) {
+    bool all = true;
+    for (int u = 0; u < n; ++u) all &= S.cur_stable[u];
+    const double lat = all ? dp_latency(d, S.cur_wt) : OPSC_INF;
+    out.latency[w] = lat;
+    out.feasible[w] = lat <= f.slo;
+    out.devices_used[w] = S.used;
+    out.n_assign[w] = S.na;
+    PySum memsum;
+    memsum.reset();
+    double* de = out.d_energy + (size_t)w * D;
+    for (int dev = 0; dev < S.used; ++dev) {
+      out.d_mem[(size_t)w * D + dev] = dev_mem(dev);
+      out.d_sm[(size_t)w * D + dev] = dev_load(P, dev, -1, 0.0, -1, nullptr);
+      de[dev] = 0.0;
+    }
+    for (int i = 0; i < S.na; ++i) {
+      const size_t o = (size_t)w * A + i;
+      const int u = out.a_op[o];
+      out.a_latency[o] = S.T[u] * P.a_fac[i];
+      memsum.add(P.a_mem[i]);
+      const double layers = (double)d.layer_count[u];
+      double sh = ((f.alpha * (double)S.p[u]) * (S.cur_wait[u] + S.cur_teff[u])) * layers;
+      sh += ((f.beta * S.cur_teff[u]) * layers) / (double)S.r[u];
+      de[out.a_device[o]] += sh;
+    }
+    out.memory[w] = memsum.value();
+    double total = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const int u = config_order == 0 ? i : d.node_order[i];
+      const double layers = (double)d.layer_count[u];
+      const double wl = S.cur_wait[u] * layers, sl = S.cur_teff[u] * layers;
+      total += ((f.alpha * (double)S.p[u]) * (double)S.r[u]) * (wl + sl);
+      total += f.beta * sl;
+    }
+    out.energy[w] = total;
+  }
+}
+
+size_t place_shared_workspace(int n_windows, int A, int D, int n) {
+  return (size_t)(n_windows > 0 ? n_windows : 1) * pw_bytes(A, D, n);
+}
+
+cudaError_t launch_place_shared(const OpscDag& d, const OpscPlaceShared& f, OpscWindows w, const int16_t* cfg,
+                                const uint8_t* feas, int config_order, OpscPlacement out, void* ws,
+                                size_t ws_bytes, cudaStream_t s) {
+  if (w.n <= 0) return cudaSuccess;
+  if (!ws || ws_bytes < place_shared_workspace(w.n, out.cap_assign, out.cap_dev, d.n_ops))
+    return cudaErrorInvalidValue;
+  PlaceArgs a;
+  a.d = d;
+  a.f = f;
+  place_kernel<<<w.n, kPlaceThreads, 0, s>>>(a, w, cfg, feas, config_order, out, (unsigned char*)ws);
+  return cudaGetLastError();
+}
+
+}  // namespace opsc

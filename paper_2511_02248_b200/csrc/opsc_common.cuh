@@ -190,6 +190,10 @@ cudaError_t launch_greedy(const OpscDag& d, const OpscGreedySpec& s, OpscWindows
                           int phase = 0, void* save = nullptr);
 size_t greedy_state_bytes(int n_windows);
 size_t windowize_workspace(long long n, int max_w);
+size_t place_shared_workspace(int n_windows, int A, int D, int n);
+cudaError_t launch_place_shared(const OpscDag& d, const OpscPlaceShared& f, OpscWindows w, const int16_t* cfg,
+                                const uint8_t* feas, int config_order, OpscPlacement out, void* ws,
+                                size_t ws_bytes, cudaStream_t s);
 cudaError_t launch_windowize(OpscTraceRecords rec, double len, double q, int max_w, int32_t* n_windows,
                              double* pq, int32_t* pl, double* dq, void* ws, size_t ws_bytes, cudaStream_t s);
 }  // namespace opsc

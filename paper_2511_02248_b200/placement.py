@@ -81,3 +81,43 @@ def capacities(cfg, n_devices):
     every replica is one assignment and needs at most one device."""
     total_r = int(cfg[:, :, 1].sum(axis=1).max()) if cfg.size else 1
     return max(1, total_r), max(1, min(int(n_devices), total_r))
+
+
+def place_windows(problem, windows, cfg, plan_feasible, fleet: SharedFleet, config_order,
+                  device="cuda"):
+    """opsc_place_shared on the GPU for every window's decided plan; host
+    arrays in, PlacementArrays out."""
+    import torch
+
+    from . import _native, tables
+    dev = torch.device(device)
+    L = _native.load()
+    cfg = np.ascontiguousarray(cfg, dtype=np.int16)
+    ca, cd = capacities(cfg, fleet.spec.n_devices)
+    host = PlacementArrays(windows.n, ca, cd)
+    to = lambda a: torch.from_numpy(np.array(a, copy=True)).to(dev)
+    wt = {k: to(getattr(windows, k)) for k in ("qps", "seq_len", "phase", "slo", "eps")}
+    w = abi.OpscWindows()
+    w.n = windows.n
+    for k, t in wt.items():
+        setattr(w, k, t.data_ptr())
+    cfg_t, feas_t = to(cfg), to(np.ascontiguousarray(plan_feasible, dtype=np.uint8))
+    caps_t, ccap_t = to(fleet.mem_cap), to(fleet.compute_cap)
+    spec = abi.OpscPlaceShared()
+    for f, _ in abi.OpscPlaceShared._fields_:
+        setattr(spec, f, getattr(fleet.spec, f))
+    spec.mem_cap, spec.compute_cap = caps_t.data_ptr(), ccap_t.data_ptr()
+    dt = {f: to(getattr(host, f)) for f in PlacementArrays.FIELDS}
+    out = abi.OpscPlacement()
+    out.cap_assign, out.cap_dev = host.cap_assign, host.cap_dev
+    for f, t in dt.items():
+        setattr(out, f, t.data_ptr())
+    nb = L.opsc_place_shared_workspace(windows.n, host.cap_assign, host.cap_dev, problem.n_ops)
+    ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+    _native.check(L.opsc_place_shared(_native.ref(problem.table), _native.ref(spec), w, cfg_t.data_ptr(),
+                                      feas_t.data_ptr(), config_order, out, ws.data_ptr(), nb,
+                                      torch.cuda.current_stream(dev).cuda_stream), "opsc_place_shared")
+    torch.cuda.synchronize(dev)
+    for f, t in dt.items():
+        getattr(host, f)[...] = t.cpu().numpy()
+    return host
