@@ -31,9 +31,14 @@ def _namespaces(pkg):
     types_ns = types.SimpleNamespace(
         OperatorConfig=A.OperatorConfig, PredictedSojourn=A.PredictedSojourn,
         ScalingPlan=A.ScalingPlan, BruteForceBounds=A.BruteForceBounds)
+    PL = pkg.placement
+    types_ns.ReplicaAssignment = PL.ReplicaAssignment
+    types_ns.DeviceLoad = PL.DeviceLoad
+    types_ns.Placement = PL.Placement
     err_ns = types.SimpleNamespace(
         NoStableConfig=A.NoStableConfig, SearchSpaceTooLarge=A.SearchSpaceTooLarge,
-        Unstable=pkg.queueing.Unstable)
+        Unstable=pkg.queueing.Unstable, FleetExhausted=PL.FleetExhausted,
+        InfeasiblePlacement=PL.InfeasiblePlacement)
     return types_ns, err_ns
 
 
@@ -46,6 +51,8 @@ def install(pkg=None):
     T, E = _namespaces(pkg)
     names = ("brute_force_autoscale", "model_level_autoscale", "greedy_autoscale")
     saved = {(mod, name): getattr(mod, name, None) for mod in (A, pkg) for name in names}
+    saved[(pkg.placement, "place")] = pkg.placement.place
+    saved[(pkg, "place")] = getattr(pkg, "place", None)
 
     @functools.wraps(saved[(A, "brute_force_autoscale")])
     def brute_force_autoscale(dag, profiles, point, params, bounds=None):
@@ -61,10 +68,18 @@ def install(pkg=None):
     def greedy_autoscale(dag, profiles, point, params):
         return planners.greedy_autoscale(dag, profiles, point, params, types=T, err=E)
 
+    from . import placement as gpu_placement
+
+    @functools.wraps(saved[(pkg.placement, "place")])
+    def place(plan, dag, profiles, fleet, params, point):
+        return gpu_placement.place(plan, dag, profiles, fleet, params, point, types=T, err=E)
+
     for mod in (A, pkg):
         mod.brute_force_autoscale = brute_force_autoscale
         mod.model_level_autoscale = model_level_autoscale
         mod.greedy_autoscale = greedy_autoscale
+    pkg.placement.place = place
+    pkg.place = place
 
     def uninstall():
         for (mod, name), fn in saved.items():

@@ -389,3 +389,43 @@ def make_fleet(n: int, mem_cap: float = 80e9, link_bw: float = 600e9):
     width = len(str(max(0, n - 1)))
     return [DeviceSpec(id=f"gpu{i:0{width}d}", mem_cap=mem_cap, link_bw=link_bw)
             for i in range(n)]
+
+
+# --------------------------------------------------------------------------
+# placement value types (placement.py:58-117)
+
+
+@dataclass
+class ReplicaAssignment:
+    op_id: str
+    replica_index: int
+    device_id: str
+    sm_share: int
+    sm_demand: float
+    mem_bytes: float
+    group: str
+    interference_adjusted_latency: float = 0.0
+
+
+@dataclass
+class DeviceLoad:
+    mem_used: float = 0.0
+    sm_demand: float = 0.0
+    energy: float = 0.0
+
+
+@dataclass
+class Placement:
+    assignments: list
+    device_loads: dict
+    devices_used: int
+    feasible: bool
+    recomputed_latency: float
+
+
+@dataclass(frozen=True)
+class PlacementParams:
+    slo: float
+    slack_weight_mem: float = 0.5
+    slack_weight_compute: float = 0.5
+    max_sm_load: float = 1.5

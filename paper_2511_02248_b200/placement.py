@@ -121,3 +121,61 @@ def place_windows(problem, windows, cfg, plan_feasible, fleet: SharedFleet, conf
     for f, t in dt.items():
         getattr(host, f)[...] = t.cpu().numpy()
     return host
+
+
+def place(plan, dag, profiles, fleet, params, point, *, types=None, err=None, energy=None,
+          return_metrics=False):
+    """Drop-in for the reference's placement.place() (placement.py:399-462):
+    Alg. 2 on the GPU for one decided plan. Returns a Placement whose
+    device_loads already carry fill_device_energy's per-device energy; with
+    return_metrics=True also (request_energy, provisioned_memory)."""
+    import ctypes as C
+
+    from . import errors, model, tables
+    from .tables import PHASE_INDEX
+    T = types or model
+    E = err or errors
+    if not plan.feasible:
+        raise ValueError("placement requires an SLO-feasible plan")
+    if not fleet:
+        raise ValueError("fleet must not be empty")
+    problem = tables.pack_problem(dag, profiles)
+    # the plan's config order drives the energy sum (metrics.py:95-101)
+    order = [problem.rank[op] for op in plan.configs]
+    C.memmove(C.addressof(problem.table) + abi.OpscDag.node_order.offset,
+              (C.c_int32 * len(order))(*order), 4 * len(order))
+    cfg = np.zeros((1, problem.n_ops, 3), np.int16)
+    for op, c in plan.configs.items():
+        cfg[0, problem.rank[op]] = (c.p, c.r, c.b)
+    win = tables.pack_windows([point], params.slo, 0.0)
+    sf = SharedFleet.from_params(fleet, params, profiles, energy)
+    arr = place_windows(problem, win, cfg, np.ones(1, np.uint8), sf, 1)
+    st = int(arr.status[0])
+    if st & abi.W_FLEET_EXHAUSTED:
+        raise E.FleetExhausted(f"all {len(fleet)} devices in use, none left to provision")
+    if st & abi.W_INFEASIBLE_PLACEMENT:
+        raise E.InfeasiblePlacement("a replica needs more memory than its device holds")
+    L = int(point.seq_len)
+    k_base = min(c.r for c in plan.configs.values())
+    assignments = []
+    for i in range(int(arr.n_assign[0])):
+        op = problem.ids[int(arr.a_op[0, i])]
+        c = plan.configs[op]
+        prof = profiles.get(dag.node(op).profile_ref)
+        k = int(arr.a_replica[0, i])
+        assignments.append(T.ReplicaAssignment(
+            op_id=op, replica_index=k, device_id=sf.devices[int(arr.a_device[0, i])].id,
+            sm_share=int(arr.a_share[0, i]), sm_demand=min(1.0, prof.s0 + prof.s1 * c.b * L),
+            mem_bytes=prof.weight_mem / c.p + prof.m0 + prof.m1 * c.b * L,
+            group=f"base{k}" if k <= k_base else f"extra:{op}:{k}",
+            interference_adjusted_latency=float(arr.a_latency[0, i])))
+    loads = {sf.devices[d].id: T.DeviceLoad(mem_used=float(arr.d_mem[0, d]),
+                                            sm_demand=float(arr.d_sm[0, d]),
+                                            energy=float(arr.d_energy[0, d]))
+             for d in range(int(arr.devices_used[0]))}
+    placed = T.Placement(assignments=assignments, device_loads=loads,
+                         devices_used=int(arr.devices_used[0]), feasible=bool(arr.feasible[0]),
+                         recomputed_latency=float(arr.latency[0]))
+    if return_metrics:
+        return placed, float(arr.energy[0]), float(arr.memory[0])
+    return placed

@@ -37,3 +37,48 @@ def test_gpu_place_vs_oracle_large_plans(orc):
             cpu = orc.place_shared(prob, win, dec.cfg, dec.feasible, fleet, 1)
             for f in placement.PlacementArrays.FIELDS:
                 assert getattr(gpu, f).tobytes() == getattr(cpu, f).tobytes(), (mode, theta, f)
+
+
+def test_place_dropin_matches_reference_objects():
+    """placement.place() (reference signature) on GPU-decided plans returns
+    the reference's Placement field for field (golden 'a100' setting)."""
+    from paper_2511_02248_b200 import planners
+    setting = next(s for s in TP.SETTINGS if s[0] == "a100")
+    checked = 0
+    for rec in TP.CASES[::5]:
+        exp = rec["settings"]["a100"]
+        src = G.load(rec["source"])
+        c = next(c for c in src if c["name"] == rec["name"])
+        dag_spec, prof = (scenarios.SCENARIOS[c["scenario"]] if "scenario" in c
+                          else (c["dag"], c["profiles"]))
+        dag, profiles = model.build_dag(dag_spec), model.profiles_from_dict(prof)
+        params, pt = G.case_params(c), G.case_point(c)
+        if rec["source"] == "oracle.json":
+            plan = planners.brute_force_autoscale(dag, profiles, pt, params, G.case_bounds(c), guards=False)
+        elif rec["source"] == "model.json":
+            plan = planners.model_level_autoscale(dag, profiles, pt, params)
+        else:
+            plan = planners.greedy_autoscale(dag, profiles, pt, params)
+        assert [[op, cf.p, cf.r, cf.b] for op, cf in plan.configs.items()] == rec["plan"]
+        name, n, caps, ccap, theta, expo, over = setting
+        width = len(str(max(0, n - 1)))
+        fleet = [model.DeviceSpec(id=f"dev{i:0{width}d}", mem_cap=caps[i % len(caps)], compute_cap=ccap)
+                 for i in range(n)]
+        profiles.interference = model.InterferenceParams(theta, expo)
+        pp = model.PlacementParams(slo=params.slo, **over)
+        if "error" in exp:
+            with pytest.raises(Exception) as ei:
+                placement.place(plan, dag, profiles, fleet, pp, pt)
+            assert type(ei.value).__name__ == exp["error"]
+            continue
+        placed, energy, memory = placement.place(plan, dag, profiles, fleet, pp, pt, return_metrics=True)
+        got = [[a.op_id, a.replica_index, a.device_id, a.sm_share, a.interference_adjusted_latency.hex()]
+               for a in placed.assignments]
+        assert got == exp["assignments"], rec["name"]
+        assert [[d, l.mem_used.hex(), l.sm_demand.hex(), l.energy.hex()]
+                for d, l in placed.device_loads.items()] == exp["devices"]
+        assert (placed.devices_used, placed.feasible, placed.recomputed_latency.hex()) == \
+            (exp["devices_used"], exp["feasible"], exp["recomputed_latency"])
+        assert (energy.hex(), memory.hex()) == (exp["energy"], exp["memory"])
+        checked += 1
+    assert checked > 10
