@@ -27,7 +27,7 @@ FLAGS = [
     "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
     "-Xptxas", "-v",
-]
+] + os.environ.get("OPSC_NVCC_EXTRA", "").split()
 
 
 def _stale(target, deps):

@@ -31,7 +31,13 @@
 
 namespace opsc {
 
-constexpr int kComposeThreads = 256;
+#ifndef OPSC_COMPOSE_THREADS
+#define OPSC_COMPOSE_THREADS 256
+#endif
+#ifndef OPSC_COMPOSE_MINB
+#define OPSC_COMPOSE_MINB 3
+#endif
+constexpr int kComposeThreads = OPSC_COMPOSE_THREADS;
 constexpr unsigned long long kSentinel = 1ull << 62;  // > any real key (objective < 2^17)
 
 __device__ __forceinline__ double dp_in(uint32_t pm, const double* val) {
@@ -53,7 +59,7 @@ struct ComposeSmem {
 };
 
 template <int NJ, bool CHAIN>
-__global__ void __launch_bounds__(kComposeThreads, 3)
+__global__ void __launch_bounds__(kComposeThreads, OPSC_COMPOSE_MINB)
 compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ OpscGrid g,
                const double* __restrict__ menu_w, const double* __restrict__ slo_w,
                const double* __restrict__ qps_w, unsigned long long* __restrict__ key_out) {
