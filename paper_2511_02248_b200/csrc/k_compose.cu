@@ -65,20 +65,37 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
                const double* __restrict__ qps_w, unsigned long long* __restrict__ key_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ unsigned long long warp_best[kComposeThreads / 32];
+  __shared__ __align__(8) unsigned long long tma_bar;
   const int jp = c.n - 1, kp = c.n - 2;
   const int mj = c.m[jp], mk = c.m[kp];
   ComposeSmem s;
-  s.kk = reinterpret_cast<unsigned long long*>(smem_raw);
+  s.w = reinterpret_cast<double*>(smem_raw);  // offset 0: 16-byte aligned TMA target
+  s.kk = reinterpret_cast<unsigned long long*>(s.w + c.E + 1);
   s.jk = s.kk + mk;
-  s.w = reinterpret_cast<double*>(s.jk + mj + 1);
-  s.jw = s.w + c.E + 1;
+  s.jw = reinterpret_cast<double*>(s.jk + mj + 1);
   s.cost = reinterpret_cast<int32_t*>(s.jw + mj);
 
   const int w = blockIdx.x / c.blocks_per_window;
   const int bw = blockIdx.x - w * c.blocks_per_window;
   const double* src = menu_w + (size_t)w * c.E;
+  // The window's menu slab is one contiguous tile: when it is 16-byte sized
+  // and aligned, one thread moves it with a TMA bulk copy (cp.async.bulk,
+  // completion on an mbarrier) while the CTA builds the cost table.
+  const uint32_t slab = (uint32_t)c.E * 8u;
+  const bool use_tma = (slab % 16u) == 0u && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0u) && slab > 0u;
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&tma_bar);
+  if (use_tma && threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(slab) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(s.w)),
+        "l"(src), "r"(slab), "r"(bar)
+        : "memory");
+  }
   for (int i = threadIdx.x; i < c.E; i += kComposeThreads) {
-    s.w[i] = src[i];
+    if (!use_tma) s.w[i] = src[i];
     int v = 0;
     while (i >= g.menu_off[v + 1]) ++v;
     int p, r, b;
@@ -88,6 +105,16 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
   if (threadIdx.x == 0) {
     s.w[c.E] = 0.0;
     s.cost[c.E] = 0;
+  }
+  if (use_tma) {
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(bar)
+          : "memory");
+    }
   }
   __syncthreads();
   const int koff = c.off[kp], joff = c.off[jp];

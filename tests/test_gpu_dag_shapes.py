@@ -1,0 +1,72 @@
+"""Exhaustive compose on non-chain DAGs at scale (the generic, non-CHAIN
+kernel path: merges, forks, multi-sink) and on the 12-op multimodal DAG --
+GPU decisions and every plan field against the CPU oracle."""
+
+import numpy as np
+import pytest
+
+from paper_2511_02248_b200 import abi, model, scenarios, tables
+
+pytestmark = pytest.mark.gpu
+
+
+def _random_dag(rng, n, shape):
+    ids = [f"op{chr(97 + i)}" for i in range(n)]
+    if shape == "merge":      # last node merges two branches
+        edges = [(ids[i], ids[i + 1]) for i in range(n - 3)] + [(ids[n - 3], ids[n - 1]), (ids[n - 2], ids[n - 1])]
+    elif shape == "fork":     # two sinks
+        edges = [(ids[i], ids[i + 1]) for i in range(n - 2)] + [(ids[n - 3], ids[n - 1])]
+    else:                     # random DAG
+        edges = [(ids[i], ids[j]) for j in range(1, n) for i in range(j) if rng.uniform() < 0.35]
+    nodes = [{"id": i, "kind": "linear", "layer_count": int(rng.choice([1, 8, 32])), "profile_ref": "p" + i}
+             for i in ids]
+    prof = {"_link_bandwidth": 900e9}
+    for i in ids:
+        c0, c1 = float(rng.uniform(2e-6, 3e-5)), float(10 ** rng.uniform(-9, -6.8))
+        prof["p" + i] = {"prefill": {"c0": c0, "c1": c1}, "decode": {"c0": c0, "c1": c1},
+                         "weight_mem": 1e8, "m1": 1e4, "v1": float(rng.uniform(4e3, 4e4)),
+                         "s0": 0.1, "s1": 1e-4}
+    dag = {"nodes": nodes, "edges": [{"src": a, "dst": b, "volume_ref": "p" + a} for a, b in edges]}
+    return model.build_dag(dag), model.profiles_from_dict(prof)
+
+
+@pytest.mark.parametrize("shape,n", [("merge", 7), ("fork", 7), ("random", 7), ("random", 8)])
+def test_generic_dag_exhaustive_vs_oracle(nat_loaded, orc, shape, n):
+    from paper_2511_02248_b200 import _native
+    rng = np.random.default_rng(n * 7 + len(shape))
+    dag, prof = _random_dag(rng, n, shape)
+    prob = tables.pack_problem(dag, prof)
+    grid = tables.pack_grid(prob, model.AutoscaleParams(slo=1.0),
+                            model.BruteForceBounds(r_max=3, b_max=2, parallelism=(1, 2)))  # 12^n
+    qps = rng.uniform(5, 60, 6)
+    win = tables.window_arrays(qps, rng.integers(256, 4096, 6), 0, rng.uniform(0.02, 0.6, 6))
+    gpu = _native.plan_windows_host(abi.MODE_ORACLE, prob, win, grid=grid)
+    cpu = orc.plan_windows(abi.MODE_ORACLE, prob, win, grid=grid)
+    for f in tables.DecisionArrays.FIELDS:
+        assert getattr(gpu, f).tobytes() == getattr(cpu, f).tobytes(), (shape, n, f)
+    assert gpu.feasible.any()
+
+
+def test_multimodal_12op_exhaustive_vs_oracle(nat_loaded, orc):
+    """cfg3: 12 operators, (P in {1,2}, R<=3, B=1)^12 = 2.2e9 candidates per window."""
+    from paper_2511_02248_b200 import _native
+    prob = tables.pack_problem(*scenarios.scenario("cfg3"))
+    g = scenarios.GRIDS["cfg3"]
+    grid = tables.pack_grid(prob, model.AutoscaleParams(slo=1.0), model.BruteForceBounds(**g))
+    tw = scenarios.trace_windows("cfg3")
+    idx = np.array([3, 30])
+    for phase in ("prefill", "decode"):
+        win = tables.window_arrays(tw[phase + "_qps"][idx], tw[phase + "_len"][idx],
+                                   tables.PHASE_INDEX[phase], scenarios.SLO["cfg3"][phase])
+        gpu = _native.plan_windows_host(abi.MODE_ORACLE, prob, win, grid=grid)
+        cpu = orc.plan_windows(abi.MODE_ORACLE, prob, win, grid=grid)
+        for f in tables.DecisionArrays.FIELDS:
+            assert getattr(gpu, f).tobytes() == getattr(cpu, f).tobytes(), (phase, f)
+
+
+@pytest.fixture(scope="module")
+def nat_loaded():
+    from paper_2511_02248_b200 import _native
+    _native.load()
+    assert _native.device_count() >= 1
+    return _native
