@@ -84,9 +84,15 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
   const uint32_t slab = (uint32_t)c.E * 8u;
   const bool use_tma = (slab % 16u) == 0u && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0u) && slab > 0u;
   const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&tma_bar);
+  if (use_tma) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();  // the barrier is initialised before anyone polls it
+  }
   if (use_tma && threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(slab) : "memory");
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
