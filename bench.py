@@ -292,6 +292,7 @@ def ours(args):
     latency = None
     if rank == 0 and not args.no_latency:
         latency = decision_latency(dev)
+        latency["trace_pipeline"] = trace_pipeline(dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -400,6 +401,39 @@ def decision_latency(dev):
                      "eager_p99": eager[min(len(eager) - 1, int(0.99 * len(eager)))],
                      "batched_ms_per_window": batch_ms / max(1, len(samples))}
     out["dag"] = "cfg2 Llama-2-70B 10-op chain, 60 x 60 s windows x {prefill, decode}, W = 1"
+    return out
+
+
+def trace_pipeline(dev):
+    """Whole 1 h cfg2 trace (records resident in HBM) -> per-window decisions
+    for both phases: GPU windowize + planner + materialise, CUDA events
+    around the call (includes the host's launch gaps)."""
+    import torch
+
+    from paper_2511_02248_b200 import model, pipeline, scenarios, workload
+    spec = scenarios.TRACES["cfg2"]
+    recs = workload.synth_workload(workload.SynthSpec(**spec["spec"]), spec["seed"])
+    arr = torch.tensor([r.arrival_time for r in recs], dtype=torch.float64, device=dev)
+    li = torch.tensor([r.input_len for r in recs], dtype=torch.int32, device=dev)
+    lo = torch.tensor([r.output_len for r in recs], dtype=torch.int32, device=dev)
+    dag, prof = scenarios.scenario("cfg2")
+    params = {ph: model.AutoscaleParams(slo=scenarios.SLO["cfg2"][ph]) for ph in ("prefill", "decode")}
+    out = {"trace": "cfg2 1 h burst trace", "records": len(recs)}
+    for mode in ("operator", "model", "oracle"):
+        bounds = model.BruteForceBounds(**scenarios.GRIDS["cfg2"]) if mode == "oracle" else None
+        tp = pipeline.TracePlanner(dag, prof, params, mode, bounds, device_=dev)
+        tp.run(arr, li, lo)
+        ts = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize(dev)
+            e0.record()
+            res = tp.run(arr, li, lo)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        out[mode + "_ms"] = statistics.median(ts)
+        out["windows"] = res["prefill"].W
     return out
 
 

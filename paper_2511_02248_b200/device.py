@@ -29,10 +29,17 @@ class DevicePlanner:
         self.place = place or tables.pack_place()
         self.dev = torch.device(device)
         self.L = _native.load()
-        n, W = problem.n_ops, windows.n
+        n = problem.n_ops
+        if isinstance(windows, dict):
+            # window SoA already resident in HBM (e.g. straight from windowize_device)
+            self.win_t = {k: windows[k].to(self.dev).contiguous()
+                          for k in ("qps", "seq_len", "phase", "slo", "eps")}
+            W = int(self.win_t["qps"].numel())
+        else:
+            W = windows.n
+            to = lambda a: torch.from_numpy(np.array(a, copy=True)).to(self.dev)
+            self.win_t = {k: to(getattr(windows, k)) for k in ("qps", "seq_len", "phase", "slo", "eps")}
         self.W, self.n = W, n
-        to = lambda a: torch.from_numpy(np.array(a, copy=True)).to(self.dev)
-        self.win_t = {k: to(getattr(windows, k)) for k in ("qps", "seq_len", "phase", "slo", "eps")}
         self.win = abi.OpscWindows()
         self.win.n = W
         for k, t in self.win_t.items():
