@@ -303,7 +303,14 @@ typedef struct OpscPlaceShared {
   double exponent;           /* 1.0 / 2.0 / 0.5 bit-exact; other values use pow() */
   double alpha;              /* EnergyParams */
   double beta;
+  int32_t flags;             /* OPSC_PLACE_* */
 } OpscPlaceShared;
+
+/* OpscPlaceShared.flags */
+#define OPSC_PLACE_DEFAULT_STREAM 0x1 /* default_stream_place (placement.py:465-491): every extra
+                                         replica on a dedicated device, no probing */
+#define OPSC_PLACE_WINDOW_SLO 0x2     /* PlacementParams.slo per window = OpscWindows.slo[w]
+                                         (runner.run_point, runner.py:70), else .slo */
 
 /* Placement of each window's plan; per-window capacities. */
 typedef struct OpscPlacement {
@@ -312,7 +319,8 @@ typedef struct OpscPlacement {
   int32_t* n_assign;     /* [W]                                              */
   int32_t* devices_used; /* [W]                                              */
   uint8_t* feasible;     /* [W] recomputed latency <= slo                    */
-  uint32_t* status;      /* [W] OPSC_W_FLEET_EXHAUSTED / INFEASIBLE_PLACEMENT */
+  uint32_t* status;      /* [W] OPSC_W_FLEET_EXHAUSTED / INFEASIBLE_PLACEMENT; when set, the
+                            window's other outputs are unspecified */
   double* latency;       /* [W] recomputed_latency                           */
   double* energy;        /* [W] request_energy under this placement          */
   double* memory;        /* [W] provisioned_memory                           */

@@ -44,7 +44,7 @@ typedef struct {
   const OpscDag* d;
   const OpscPlaceShared* f;
   int n, L, ph;
-  double qps;
+  double qps, slo; /* PlacementParams.slo of this window */
   int p[OPSC_MAX_OPS], r[OPSC_MAX_OPS], b[OPSC_MAX_OPS];
   double T[OPSC_MAX_OPS], comm[OPSC_MAX_OPS], dem[OPSC_MAX_OPS], mem[OPSC_MAX_OPS];
   int order[OPSC_MAX_OPS]; /* plan.configs order */
@@ -216,7 +216,9 @@ static uint32_t place_one(PL* s) {
       double* fac = current_factors(s);
       int best = -1;
       double best_score = 0.0;
-      for (int dev = 0; dev < s->used; ++dev) {
+      /* default_stream_place (placement.py:465-491): no probing */
+      const int n_probe = (f->flags & OPSC_PLACE_DEFAULT_STREAM) ? 0 : s->used;
+      for (int dev = 0; dev < n_probe; ++dev) {
         double mu = dev_mem(s, dev);
         if (mu + mem > f->mem_cap[dev]) continue;
         double load = dev_load(s, dev, NULL);
@@ -229,7 +231,7 @@ static uint32_t place_one(PL* s) {
         adjusted(s, tf, &t, ef, adj);
         double lat = latency_of(s, adj);
         free(tf);
-        if (lat > f->slo) continue;
+        if (lat > s->slo) continue;
         double ms = f->mem_cap[dev] - (mu + mem), cs = f->compute_cap[dev] - (load + demand);
         double mf = (0.0 >= ms ? 0.0 : ms) / f->mem_cap[dev];
         double cf = (0.0 >= cs ? 0.0 : cs) / f->compute_cap[dev];
@@ -261,7 +263,8 @@ int orc_place_shared(const OpscDag* d, const OpscPlaceShared* f, OpscWindows win
     if (!(win.qps[w] > 0.0) || !plan_feasible[w]) continue;
     PL s;
     memset(&s, 0, sizeof(s));
-    s.d = d; s.f = f; s.n = n; s.qps = win.qps[w]; s.L = win.seq_len[w]; s.ph = win.phase[w];
+    s.d = d; s.f = f; s.n = n;
+    s.slo = (f->flags & OPSC_PLACE_WINDOW_SLO) ? win.slo[w] : f->slo; s.qps = win.qps[w]; s.L = win.seq_len[w]; s.ph = win.phase[w];
     int total_r = 0;
     for (int v = 0; v < n; ++v) {
       s.p[v] = cfg[(w * n + v) * 3]; s.r[v] = cfg[(w * n + v) * 3 + 1]; s.b[v] = cfg[(w * n + v) * 3 + 2];
@@ -288,7 +291,7 @@ int orc_place_shared(const OpscDag* d, const OpscPlaceShared* f, OpscWindows win
     adjusted(&s, fac, NULL, 1.0, adj);
     double lat = latency_of(&s, adj);
     out.latency[w] = lat;
-    out.feasible[w] = lat <= f->slo;
+    out.feasible[w] = lat <= s.slo;
     out.devices_used[w] = s.used;
     out.n_assign[w] = s.na;
     PS memsum = {0, 0, 0};

@@ -106,7 +106,12 @@ class OpscTraceRecords(C.Structure):
 class OpscPlaceShared(C.Structure):
     _fields_ = [("n_devices", _I), ("mem_cap", C.c_void_p), ("compute_cap", C.c_void_p),
                 ("slo", _D), ("slack_weight_mem", _D), ("slack_weight_compute", _D),
-                ("max_sm_load", _D), ("theta", _D), ("exponent", _D), ("alpha", _D), ("beta", _D)]
+                ("max_sm_load", _D), ("theta", _D), ("exponent", _D), ("alpha", _D), ("beta", _D),
+                ("flags", _I)]
+
+
+PLACE_DEFAULT_STREAM = 0x1
+PLACE_WINDOW_SLO = 0x2
 
 
 class OpscPlacement(C.Structure):

@@ -1,5 +1,8 @@
 // k_place.cu -- K6: shared (interference-aware) placement, Alg. 2 of the
-// reference (placement.py:399-462), with its placement-dependent metrics
+// reference (placement.py:399-462), or with OPSC_PLACE_DEFAULT_STREAM its
+// no-sharing variant (default_stream_place, :465-491: same base instances
+// and _finalize, every extra replica on an unused device), with the
+// placement-dependent metrics
 // (request_energy, fill_device_energy, provisioned_memory; metrics.py:84-132).
 //
 // One CTA per window. Base instances are packed first-fit-decreasing
@@ -41,7 +44,9 @@ struct PWork {  // per-window global workspace
 
 __host__ __device__ inline size_t pw_bytes(int A, int D, int n) {
   (void)n;
-  return (size_t)A * (4 + 4 + 8 + 8 + 8) + (size_t)D * (4 + 4 + 4 + 8 + 8) + (size_t)A * 4 + 64;
+  // rounded to 16 B so every window's double arrays stay 8-byte aligned
+  const size_t b = (size_t)A * (4 + 4 + 8 + 8 + 8) + (size_t)D * (4 + 4 + 4 + 8 + 8) + (size_t)A * 4 + 64;
+  return (b + 15) & ~(size_t)15;
 }
 
 __device__ PWork carve(unsigned char* base, int A, int D) {
@@ -209,6 +214,8 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
   const double qps = win.qps[w];
   if (!(qps > 0.0) || !plan_feasible[w]) return;
   const int L = win.seq_len[w], ph = win.phase[w];
+  const double slo = (f.flags & OPSC_PLACE_WINDOW_SLO) ? win.slo[w] : f.slo;
+  const bool probe = !(f.flags & OPSC_PLACE_DEFAULT_STREAM);
   PWork P = carve(ws + (size_t)w * pw_bytes(A, D, n), A, D);
   const int32_t* adev = out.a_device + (size_t)w * A;
   if (threadIdx.x == 0) {
@@ -343,7 +350,8 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
       __shared__ int s_best;
       __shared__ double s_best_score;
       if (threadIdx.x == 0) s_best = -1;
-      for (int c0 = 0; c0 < S.used; c0 += kMaxDevProbe) {
+      // default-stream placement never shares: straight to take_unused
+      for (int c0 = 0; probe && c0 < S.used; c0 += kMaxDevProbe) {
       const int U = min(S.used - c0, kMaxDevProbe);
       // stage 1: per-device admission + tentative group totals
       for (int dj = threadIdx.x; dj < U; dj += blockDim.x) {
@@ -382,7 +390,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
         bool fin = true;
         for (int u = 0; u < n; ++u) fin &= S.probe_wt[dj][u] != OPSC_INF;
         const double lat = fin ? dp_latency(d, S.probe_wt[dj]) : OPSC_INF;
-        if (lat > f.slo) S.dev_ok[dj] = 0;
+        if (lat > slo) S.dev_ok[dj] = 0;
       }
       __syncthreads();
       // weighted slack (placement.py:338-351); best score, ties to the lowest id
@@ -441,7 +449,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
     for (int u = 0; u < n; ++u) all &= S.cur_stable[u];
     const double lat = all ? dp_latency(d, S.cur_wt) : OPSC_INF;
     out.latency[w] = lat;
-    out.feasible[w] = lat <= f.slo;
+    out.feasible[w] = lat <= slo;
     out.devices_used[w] = S.used;
     out.n_assign[w] = S.na;
     PySum memsum;

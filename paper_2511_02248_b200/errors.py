@@ -51,3 +51,16 @@ class InfeasiblePlacement(OpscalerError):
 class DeviceUnavailable(OpscalerError):
     """The CUDA extension is missing or no B200 is visible: there is no
     CPU fallback for the planner search."""
+
+
+class MismatchedScenario(OpscalerError):
+    """Savings comparison across different workload/SLO fingerprints
+    (metrics.py:30-31)."""
+
+
+class ParseError(OpscalerError):
+    """Malformed trace file (workload.py:23-24)."""
+
+
+class EmptyTrace(OpscalerError):
+    """Trace file without data rows (workload.py:27-28)."""

@@ -10,7 +10,8 @@ the reference.
 
     import opscaler
     from paper_2511_02248_b200 import install
-    install(opscaler)   # brute_force / model_level / greedy now run on the B200
+    install(opscaler)   # planners, placement, runner.sweep and cli.cmd_autoscale
+                        # now run on the B200
 
 The wrappers accept the reference's own objects, return the reference's own
 ScalingPlan / OperatorConfig / PredictedSojourn instances and raise its own
@@ -40,6 +41,20 @@ def _namespaces(pkg):
         Unstable=pkg.queueing.Unstable, FleetExhausted=PL.FleetExhausted,
         InfeasiblePlacement=PL.InfeasiblePlacement)
     return types_ns, err_ns
+
+
+def _runner_types(pkg, T, E):
+    from . import runner as gpu_runner
+    E.MismatchedScenario = pkg.metrics.MismatchedScenario
+
+    class RT(gpu_runner.Types):
+        PointResult = pkg.runner.PointResult
+        ScenarioEval = pkg.metrics.ScenarioEval
+        SavingsReport = pkg.metrics.SavingsReport
+        ComparisonRow = pkg.runner.ComparisonRow
+        plan_types = T
+        err = E
+    return RT
 
 
 def install(pkg=None):
@@ -80,6 +95,39 @@ def install(pkg=None):
         mod.greedy_autoscale = greedy_autoscale
     pkg.placement.place = place
     pkg.place = place
+
+    @functools.wraps(pkg.placement.default_stream_place)
+    def default_stream_place(plan, dag, profiles, fleet, params, point):
+        return gpu_placement.default_stream_place(plan, dag, profiles, fleet, params, point,
+                                                  types=T, err=E)
+
+    saved[(pkg.placement, "default_stream_place")] = pkg.placement.default_stream_place
+    pkg.placement.default_stream_place = default_stream_place
+
+    # batched runner: sweep (runner.py:190-240) and cli.cmd_autoscale
+    # (cli.py:123-186) plan and place all points of a DAG per launch
+    from . import runner as gpu_runner
+    RT = _runner_types(pkg, T, E)
+
+    @functools.wraps(pkg.runner.sweep)
+    def sweep(axis, values, dag, profiles, fleet, base_point, params, placement_mode="shared",
+              energy_params=None, max_workers=4):
+        return gpu_runner.sweep(axis, values, dag, profiles, fleet, base_point, params,
+                                placement_mode, energy_params, max_workers, types=RT)
+
+    cli = pkg.cli
+
+    @functools.wraps(cli.cmd_autoscale)
+    def cmd_autoscale(args):
+        dag, profiles, fleet = cli._load_scenario(args)
+        windows = cli._workload_points(args)
+        return gpu_runner.autoscale_windows(dag, profiles, fleet, windows, args.mode, args.placement,
+                                            lambda ph: cli._params(args, ph), args.out, types=RT,
+                                            max_enumeration=A.MAX_ENUMERATION)
+
+    for mod, name, fn in ((pkg.runner, "sweep", sweep), (cli, "cmd_autoscale", cmd_autoscale)):
+        saved[(mod, name)] = getattr(mod, name)
+        setattr(mod, name, fn)
 
     def uninstall():
         for (mod, name), fn in saved.items():

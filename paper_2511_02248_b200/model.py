@@ -422,6 +422,22 @@ class Placement:
     feasible: bool
     recomputed_latency: float
 
+    def to_dict(self) -> dict:
+        """Same keys and order as the reference's Placement.to_dict
+        (placement.py:85-110); devices sorted by id."""
+        return {
+            "assignments": [{"op": a.op_id, "replica": a.replica_index, "device": a.device_id,
+                             "sm_share": a.sm_share,
+                             "interference_adjusted_latency": a.interference_adjusted_latency}
+                            for a in self.assignments],
+            "devices": [{"id": dev, "mem_used": ld.mem_used, "sm_demand": ld.sm_demand,
+                         "energy": ld.energy}
+                        for dev, ld in sorted(self.device_loads.items())],
+            "devices_used": self.devices_used,
+            "feasible": self.feasible,
+            "recomputed_latency": self.recomputed_latency,
+        }
+
 
 @dataclass(frozen=True)
 class PlacementParams:

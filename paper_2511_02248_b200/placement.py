@@ -8,6 +8,8 @@ reference (placement.py:399-462) -- and its Eq. 9 energy / memory metrics
 
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 
 from . import abi
@@ -18,7 +20,7 @@ class SharedFleet:
     InterferenceParams + EnergyParams packed as an OpscPlaceShared."""
 
     def __init__(self, fleet, slo, interference=None, energy=None, slack_weight_mem=0.5,
-                 slack_weight_compute=0.5, max_sm_load=1.5):
+                 slack_weight_compute=0.5, max_sm_load=1.5, default_stream=False, window_slo=False):
         if not fleet:
             raise ValueError("fleet must not be empty")
         self.devices = sorted(fleet, key=lambda d: d.id)
@@ -34,13 +36,14 @@ class SharedFleet:
         s.exponent = float(interference.exponent) if interference is not None else 1.0
         s.alpha = float(energy.alpha) if energy is not None else 0.3 * 400.0
         s.beta = float(energy.beta) if energy is not None else 0.7 * 400.0
+        s.flags = (abi.PLACE_DEFAULT_STREAM if default_stream else 0) | (abi.PLACE_WINDOW_SLO if window_slo else 0)
         self.spec = s
 
     @classmethod
-    def from_params(cls, fleet, placement_params, profiles, energy=None):
+    def from_params(cls, fleet, placement_params, profiles, energy=None, **flags):
         p = placement_params
         return cls(fleet, p.slo, getattr(profiles, "interference", None), energy,
-                   p.slack_weight_mem, p.slack_weight_compute, p.max_sm_load)
+                   p.slack_weight_mem, p.slack_weight_compute, p.max_sm_load, **flags)
 
 
 class PlacementArrays:
@@ -123,16 +126,45 @@ def place_windows(problem, windows, cfg, plan_feasible, fleet: SharedFleet, conf
     return host
 
 
-def place(plan, dag, profiles, fleet, params, point, *, types=None, err=None, energy=None,
-          return_metrics=False):
-    """Drop-in for the reference's placement.place() (placement.py:399-462):
-    Alg. 2 on the GPU for one decided plan. Returns a Placement whose
-    device_loads already carry fill_device_energy's per-device energy; with
-    return_metrics=True also (request_energy, provisioned_memory)."""
-    import ctypes as C
+def placement_object(arr, i, plan, dag, profiles, problem, fleet: SharedFleet, seq_len, types):
+    """Window i of PlacementArrays as the reference's Placement
+    (placement.py:59-110): assignments in placement order with
+    interference-adjusted latency, device loads (sorted-id order) carrying
+    fill_device_energy's per-device energy."""
+    T = types
+    L = int(seq_len)
+    k_base = min(c.r for c in plan.configs.values())
+    assignments = []
+    for a in range(int(arr.n_assign[i])):
+        op = problem.ids[int(arr.a_op[i, a])]
+        c = plan.configs[op]
+        prof = profiles.get(dag.node(op).profile_ref)
+        k = int(arr.a_replica[i, a])
+        assignments.append(T.ReplicaAssignment(
+            op_id=op, replica_index=k, device_id=fleet.devices[int(arr.a_device[i, a])].id,
+            sm_share=int(arr.a_share[i, a]), sm_demand=min(1.0, prof.s0 + prof.s1 * c.b * L),
+            mem_bytes=prof.weight_mem / c.p + prof.m0 + prof.m1 * c.b * L,
+            group=f"base{k}" if k <= k_base else f"extra:{op}:{k}",
+            interference_adjusted_latency=float(arr.a_latency[i, a])))
+    loads = {fleet.devices[d].id: T.DeviceLoad(mem_used=float(arr.d_mem[i, d]),
+                                               sm_demand=float(arr.d_sm[i, d]),
+                                               energy=float(arr.d_energy[i, d]))
+             for d in range(int(arr.devices_used[i]))}
+    return T.Placement(assignments=assignments, device_loads=loads,
+                       devices_used=int(arr.devices_used[i]), feasible=bool(arr.feasible[i]),
+                       recomputed_latency=float(arr.latency[i]))
 
+
+def raise_placement_status(status, n_devices, err):
+    if status & abi.W_FLEET_EXHAUSTED:
+        raise err.FleetExhausted(f"all {n_devices} devices in use, none left to provision")
+    if status & abi.W_INFEASIBLE_PLACEMENT:
+        raise err.InfeasiblePlacement("a replica needs more memory than its device holds")
+
+
+def _place_one(plan, dag, profiles, fleet, params, point, types, err, energy, return_metrics,
+               default_stream):
     from . import errors, model, tables
-    from .tables import PHASE_INDEX
     T = types or model
     E = err or errors
     if not plan.feasible:
@@ -148,34 +180,26 @@ def place(plan, dag, profiles, fleet, params, point, *, types=None, err=None, en
     for op, c in plan.configs.items():
         cfg[0, problem.rank[op]] = (c.p, c.r, c.b)
     win = tables.pack_windows([point], params.slo, 0.0)
-    sf = SharedFleet.from_params(fleet, params, profiles, energy)
+    sf = SharedFleet.from_params(fleet, params, profiles, energy, default_stream=default_stream)
     arr = place_windows(problem, win, cfg, np.ones(1, np.uint8), sf, 1)
-    st = int(arr.status[0])
-    if st & abi.W_FLEET_EXHAUSTED:
-        raise E.FleetExhausted(f"all {len(fleet)} devices in use, none left to provision")
-    if st & abi.W_INFEASIBLE_PLACEMENT:
-        raise E.InfeasiblePlacement("a replica needs more memory than its device holds")
-    L = int(point.seq_len)
-    k_base = min(c.r for c in plan.configs.values())
-    assignments = []
-    for i in range(int(arr.n_assign[0])):
-        op = problem.ids[int(arr.a_op[0, i])]
-        c = plan.configs[op]
-        prof = profiles.get(dag.node(op).profile_ref)
-        k = int(arr.a_replica[0, i])
-        assignments.append(T.ReplicaAssignment(
-            op_id=op, replica_index=k, device_id=sf.devices[int(arr.a_device[0, i])].id,
-            sm_share=int(arr.a_share[0, i]), sm_demand=min(1.0, prof.s0 + prof.s1 * c.b * L),
-            mem_bytes=prof.weight_mem / c.p + prof.m0 + prof.m1 * c.b * L,
-            group=f"base{k}" if k <= k_base else f"extra:{op}:{k}",
-            interference_adjusted_latency=float(arr.a_latency[0, i])))
-    loads = {sf.devices[d].id: T.DeviceLoad(mem_used=float(arr.d_mem[0, d]),
-                                            sm_demand=float(arr.d_sm[0, d]),
-                                            energy=float(arr.d_energy[0, d]))
-             for d in range(int(arr.devices_used[0]))}
-    placed = T.Placement(assignments=assignments, device_loads=loads,
-                         devices_used=int(arr.devices_used[0]), feasible=bool(arr.feasible[0]),
-                         recomputed_latency=float(arr.latency[0]))
+    raise_placement_status(int(arr.status[0]), len(fleet), E)
+    placed = placement_object(arr, 0, plan, dag, profiles, problem, sf, point.seq_len, T)
     if return_metrics:
         return placed, float(arr.energy[0]), float(arr.memory[0])
     return placed
+
+
+def place(plan, dag, profiles, fleet, params, point, *, types=None, err=None, energy=None,
+          return_metrics=False):
+    """Drop-in for the reference's placement.place() (placement.py:399-462):
+    Alg. 2 on the GPU for one decided plan. Returns a Placement whose
+    device_loads already carry fill_device_energy's per-device energy; with
+    return_metrics=True also (request_energy, provisioned_memory)."""
+    return _place_one(plan, dag, profiles, fleet, params, point, types, err, energy, return_metrics, False)
+
+
+def default_stream_place(plan, dag, profiles, fleet, params, point, *, types=None, err=None,
+                         energy=None, return_metrics=False):
+    """Drop-in for default_stream_place() (placement.py:465-491): the same
+    base instances, every extra replica on a dedicated device."""
+    return _place_one(plan, dag, profiles, fleet, params, point, types, err, energy, return_metrics, True)

@@ -2,7 +2,8 @@
 
 Build container only (imports /root/reference). For decided plans of the
 golden planner cases (tests/golden/{oracle,model,greedy}.json inputs) the
-reference's own placement.place() (placement.py:399-462) and metrics
+reference's own placement.place() (placement.py:399-462) and
+default_stream_place() (:465-491) with their metrics
 (request_energy, fill_device_energy, provisioned_memory; metrics.py:84-132)
 are run on several fleets / interference settings; every float is stored as
 float.hex().
@@ -55,14 +56,14 @@ def fleet(n, caps, ccap):
     return [PL.DeviceSpec(id=ids[i], mem_cap=caps[i % len(caps)], compute_cap=ccap) for i in order]
 
 
-def place_json(plan, dag, profiles, point, setting):
+def place_json(plan, dag, profiles, point, setting, place_fn=PL.place):
     name, n, caps, ccap, theta, expo, over = setting
     prof = PM.ProfileSet(profiles.profiles, profiles.link_bandwidth,
                          PM.InterferenceParams(theta=theta, exponent=expo))
     fl = fleet(n, caps, ccap)
     pp = PL.PlacementParams(slo=plan_slo[0], **over)
     try:
-        placed = PL.place(plan, dag, prof, fl, pp, point)
+        placed = place_fn(plan, dag, prof, fl, pp, point)
     except ref.OpscalerError as exc:
         return {"error": type(exc).__name__}
     ep = M.EnergyParams()
@@ -118,6 +119,9 @@ def main():
                    "settings": {}}
             for s in SETTINGS:
                 rec["settings"][s[0]] = place_json(plan, dag, profiles, pt, s)
+            # the no-sharing variant (placement.py:465-491) on the same fleets
+            rec["default_stream"] = {s[0]: place_json(plan, dag, profiles, pt, s, PL.default_stream_place)
+                                     for s in SETTINGS}
             out.append(rec)
     json.dump({"settings": [[s[0], s[1], s[2], s[3], s[4], s[5], s[6]] for s in SETTINGS],
                "cases": out}, open(os.path.join(HERE, "place.json"), "w"), separators=(",", ":"))

@@ -11,10 +11,11 @@ from paper_2511_02248_b200 import abi, model, placement, scenarios, tables
 pytestmark = pytest.mark.gpu
 
 
-def test_gpu_place_golden():
+@pytest.mark.parametrize("variant", ["settings", "default_stream"])
+def test_gpu_place_golden(variant):
     errs = []
     for rec in TP.CASES:
-        e = TP.check_place(placement.place_windows, rec, TP.SETTINGS)
+        e = TP.check_place(placement.place_windows, rec, TP.SETTINGS, variant)
         if e:
             errs.append((rec["name"], e[:2]))
     assert not errs, errs[:3]
@@ -30,13 +31,20 @@ def test_gpu_place_vs_oracle_large_plans(orc):
         prm = model.AutoscaleParams(slo=2.0)
         dec = _native.plan_windows_host(mode, prob, win, model=tables.pack_model(prob, prm),
                                         greedy=tables.pack_greedy(prob, prm))
+        # per-window placement SLOs straddling the planning SLO (OPSC_PLACE_WINDOW_SLO)
+        pwin = tables.window_arrays(tw["prefill_qps"][:24], tw["prefill_len"][:24], 0,
+                                    np.linspace(1.2, 2.4, 24))
         for theta, caps in ((0.5, [80e9]), (1.5, [180e9, 40e9])):
             devs = [model.DeviceSpec(id=f"g{i:04d}", mem_cap=caps[i % len(caps)]) for i in range(2048)]
-            fleet = placement.SharedFleet(devs, 2.0, model.InterferenceParams(theta, 1.0), model.EnergyParams())
-            gpu = placement.place_windows(prob, win, dec.cfg, dec.feasible, fleet, 1)
-            cpu = orc.place_shared(prob, win, dec.cfg, dec.feasible, fleet, 1)
-            for f in placement.PlacementArrays.FIELDS:
-                assert getattr(gpu, f).tobytes() == getattr(cpu, f).tobytes(), (mode, theta, f)
+            for ds in (False, True):
+                for wslo in (False, True):
+                    fleet = placement.SharedFleet(devs, 2.0, model.InterferenceParams(theta, 1.0),
+                                                  model.EnergyParams(), default_stream=ds, window_slo=wslo)
+                    w = pwin if wslo else win
+                    gpu = placement.place_windows(prob, w, dec.cfg, dec.feasible, fleet, 1)
+                    cpu = orc.place_shared(prob, w, dec.cfg, dec.feasible, fleet, 1)
+                    for f in placement.PlacementArrays.FIELDS:
+                        assert getattr(gpu, f).tobytes() == getattr(cpu, f).tobytes(), (mode, theta, ds, wslo, f)
 
 
 def test_place_dropin_matches_reference_objects():
@@ -82,3 +90,30 @@ def test_place_dropin_matches_reference_objects():
         assert (energy.hex(), memory.hex()) == (exp["energy"], exp["memory"])
         checked += 1
     assert checked > 10
+
+
+def test_gpu_place_odd_workspace_strides(orc):
+    """Odd assignment / device capacities (per-window workspace strides that
+    are not multiples of 8 B before rounding) on many windows, incl.
+    FleetExhausted mid-batch."""
+    from paper_2511_02248_b200 import _native
+    prob = tables.pack_problem(*scenarios.scenario("cfg1"))
+    tw = scenarios.trace_windows("cfg2")
+    win = tables.window_arrays(tw["prefill_qps"][:33] * 3.0, tw["prefill_len"][:33], 0, 0.5)
+    prm = model.AutoscaleParams(slo=0.5)
+    dec = _native.plan_windows_host(abi.MODE_OPERATOR, prob, win, model=tables.pack_model(prob, prm),
+                                    greedy=tables.pack_greedy(prob, prm))
+    for n_dev in (1, 3, 5, 7, 9, 31):
+        devs = [model.DeviceSpec(id=f"d{i:02d}", mem_cap=80e9) for i in range(n_dev)]
+        for ds in (False, True):
+            fleet = placement.SharedFleet(devs, 0.5, model.InterferenceParams(0.5, 1.0), model.EnergyParams(),
+                                          default_stream=ds)
+            gpu = placement.place_windows(prob, win, dec.cfg, dec.feasible, fleet, 1)
+            cpu = orc.place_shared(prob, win, dec.cfg, dec.feasible, fleet, 1)
+            assert np.array_equal(gpu.status, cpu.status), n_dev
+            bad = gpu.status != 0
+            for f in placement.PlacementArrays.FIELDS:
+                g, c = getattr(gpu, f).copy(), getattr(cpu, f).copy()
+                g[bad] = 0  # a failed window's slots are unspecified (only status counts)
+                c[bad] = 0
+                assert g.tobytes() == c.tobytes(), (n_dev, ds, f)

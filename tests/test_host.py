@@ -2,8 +2,11 @@
 drop-in planners (all raised before any device work), the installer, and the
 workload mirror against the reference-generated trace fixture."""
 
+import contextlib
+import io
 import os
 import sys
+import tempfile
 
 import numpy as np
 import pytest
@@ -142,6 +145,8 @@ def test_installer_reroutes_reference():
         from opscaler import runner
         from paper_2511_02248_b200 import DeviceUnavailable, install, _native
         orig = opscaler.autoscaler.brute_force_autoscale
+        from opscaler import cli
+        orig_cli = (cli.cmd_autoscale, runner.sweep, opscaler.placement.default_stream_place)
         undo = install(opscaler)
         try:
             assert opscaler.autoscaler.brute_force_autoscale is not orig
@@ -156,9 +161,29 @@ def test_installer_reroutes_reference():
             if _native.device_count() == 0:
                 with pytest.raises(DeviceUnavailable):
                     runner.plan_for_mode("model", dag, prof, pt, params)
+            # the CLI: cmd_autoscale and runner.sweep are the batched drop-ins
+            now = (cli.cmd_autoscale, runner.sweep, opscaler.placement.default_stream_place)
+            assert all(a is not b for a, b in zip(now, orig_cli))
+            import golden_cases as G
+            gdir = os.path.join(os.path.dirname(__file__), "golden", "cli")
+            cwd = os.getcwd()
+            os.chdir(gdir)
+            try:
+                for c in G.load("cli.json"):
+                    if c["name"] == "auto_7b_oracle_guard":
+                        err = io.StringIO()
+                        with contextlib.redirect_stderr(err):
+                            assert cli.main(c["argv"] + ["--out", tempfile.mkdtemp()]) == c["exit"]
+                        assert err.getvalue() == c["stderr"]
+                    elif c["name"] == "sweep_qps" and _native.device_count() == 0:
+                        with pytest.raises(DeviceUnavailable):
+                            cli.main(c["argv"] + ["--out", tempfile.mkdtemp()])
+            finally:
+                os.chdir(cwd)
         finally:
             undo()
         assert opscaler.autoscaler.brute_force_autoscale is orig
+        assert (cli.cmd_autoscale, runner.sweep, opscaler.placement.default_stream_place) == orig_cli
     finally:
         sys.path.remove(REF)
 

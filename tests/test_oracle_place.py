@@ -9,13 +9,13 @@ import golden_cases as G
 from paper_2511_02248_b200 import abi, model, placement, scenarios, tables
 
 
-def _setting_fleet(setting, slo):
+def _setting_fleet(setting, slo, default_stream=False):
     name, n, caps, ccap, theta, expo, over = setting
     width = len(str(max(0, n - 1)))
     devs = [model.DeviceSpec(id=f"dev{i:0{width}d}", mem_cap=caps[i % len(caps)], compute_cap=ccap)
             for i in range(n)]
     return placement.SharedFleet(devs, slo, model.InterferenceParams(theta, expo), model.EnergyParams(),
-                                 **over)
+                                 default_stream=default_stream, **over)
 
 
 def _inputs(rec):
@@ -31,12 +31,13 @@ def _inputs(rec):
     return prob, params, win, cfg, order
 
 
-def check_place(place_fn, rec, settings):
+def check_place(place_fn, rec, settings, variant="settings"):
+    """variant: "settings" = shared placement, "default_stream" = no sharing."""
     prob, params, win, cfg, order = _inputs(rec)
     errs = []
     for s in settings:
-        exp = rec["settings"][s[0]]
-        fleet = _setting_fleet(s, params.slo)
+        exp = rec[variant][s[0]]
+        fleet = _setting_fleet(s, params.slo, default_stream=variant == "default_stream")
         out = place_fn(prob, win, cfg, np.ones(1, np.uint8), fleet, order)
         if "error" in exp:
             want = {"FleetExhausted": abi.W_FLEET_EXHAUSTED,
@@ -70,4 +71,10 @@ SETTINGS = G.load("place.json")["settings"]
 @pytest.mark.parametrize("idx", range(len(CASES)))
 def test_oracle_place_shared(orc, idx):
     errs = check_place(orc.place_shared, CASES[idx], SETTINGS)
+    assert not errs, (CASES[idx]["name"], errs[:3])
+
+
+@pytest.mark.parametrize("idx", range(0, len(CASES)))
+def test_oracle_default_stream(orc, idx):
+    errs = check_place(orc.place_shared, CASES[idx], SETTINGS, "default_stream")
     assert not errs, (CASES[idx]["name"], errs[:3])
