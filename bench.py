@@ -189,10 +189,13 @@ def ours(args):
 
     from paper_2511_02248_b200 import _native, abi, device, tables
     rank, world, local = dist_env()
+    # one rank per GPU; OPSC_DIST_BACKEND=gloo (test only) lets several ranks
+    # share a GPU to exercise the N>1 path on a 1-GPU box
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("OPSC_DIST_BACKEND", "nccl"))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     problem, grid, win, space, active = workload()
@@ -260,13 +263,35 @@ def ours(args):
 
     # e2e through the C-ABI host-buffer call (pinned host windows in, decisions out)
     e2e = None
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    hwin = tables.WindowArrays(*(pin(getattr(win, k)) for k in ("qps", "seq_len", "phase", "slo", "eps")))
+    hout = tables.DecisionArrays(win.n, n_ops)
+    for f in tables.DecisionArrays.FIELDS:
+        setattr(hout, f, pin(getattr(hout, f)))
+    bi = sum(getattr(hwin, k).nbytes for k in ("qps", "seq_len", "phase", "slo", "eps"))
+    if world > 1:
+        # N ranks: host windows in, this rank's candidate shard, NCCL MIN merge,
+        # decode + materialise, decisions back to host on every rank
+        from paper_2511_02248_b200 import dist as pdist
+        for _ in range(args.warmup):
+            pdist.plan_windows_host_sharded(planner, hwin, hout)
+        t = []
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            t0 = time.perf_counter()
+            pdist.plan_windows_host_sharded(planner, hwin, hout)
+            t.append(time.perf_counter() - t0)
+        tt = torch.tensor([sum(t)], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": cands_step * len(t) / float(tt.item()), "unit": "candidates/s",
+               "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(hout.nbytes()),
+               "api": "dist.plan_windows_host_sharded (host buffers, shard per rank, NCCL MIN merge)",
+               "timing": "wall clock per rank, max over ranks",
+               "parity_vs_device_path": bool(all(
+                   getattr(hout, f).tobytes() == getattr(dec, f).tobytes()
+                   for f in ("key", "cfg", "latency", "energy")))}
     if world == 1:
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
-        hwin = tables.WindowArrays(*(pin(getattr(win, k)) for k in
-                                     ("qps", "seq_len", "phase", "slo", "eps")))
-        hout = tables.DecisionArrays(win.n, n_ops)
-        for f in tables.DecisionArrays.FIELDS:
-            setattr(hout, f, pin(getattr(hout, f)))
         ctx = _native.Context(device=local, max_windows=win.n)
         for _ in range(args.warmup):
             ctx.plan_windows(abi.MODE_ORACLE, problem, hwin, grid=grid, out=hout)

@@ -197,6 +197,23 @@ class DevicePlanner:
             self.step(shard, n_shards, allreduce)
         return g
 
+    def load_windows(self, host: tables.WindowArrays):
+        """Async H2D of a host window SoA (pinned for overlap) into the
+        resident buffers, on the current stream."""
+        for k, t in self.win_t.items():
+            a = getattr(host, k)
+            t.copy_(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a), non_blocking=True)
+
+    def fetch(self, host: tables.DecisionArrays):
+        """D2H of the decisions into a (pinned) host DecisionArrays; waits
+        for the current stream."""
+        for k, t in self.out_t.items():
+            a = getattr(host, k)
+            dst = torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a)
+            dst.copy_(t.view(dst.shape), non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        return host
+
     def decisions(self) -> tables.DecisionArrays:
         torch.cuda.synchronize(self.dev)
         out = tables.DecisionArrays(self.W, self.n, self.trace_cap)

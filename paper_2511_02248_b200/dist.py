@@ -39,5 +39,15 @@ def plan_windows_sharded(planner, group=None):
     return planner
 
 
+def plan_windows_host_sharded(planner, host_windows, host_out, group=None):
+    """Host buffers in, decisions out, on N ranks: H2D of the window SoA,
+    this rank's candidate shard, the MIN merge, decode + materialise, D2H.
+    `host_out` (tables.DecisionArrays) ends with the full decisions on every
+    rank."""
+    planner.load_windows(host_windows)
+    plan_windows_sharded(planner, group)
+    return planner.fetch(host_out)
+
+
 def infeasible_keys(n, device="cpu"):
     return torch.full((n,), abi.KEY_INFEASIBLE, dtype=torch.int64, device=device)
