@@ -11,8 +11,9 @@ of the hot path over the whole batch: per-window prologue, menu build
 exhaustive compose + SLO mask + lexicographic argmin, per-op fallback,
 decode, and plan materialisation (critical path, energy, memory, devices).
 At N > 1 every rank enumerates a contiguous slice of every window's
-candidate space and one NCCL MIN all-reduce of the packed keys gives the
-decision (strong scaling: the job is fixed).
+candidate space; the packed keys are min-merged inside the compose kernel
+over NVLink peer memory (dist.PeerMerge; --merge nccl: an NCCL MIN
+all-reduce after it). Strong scaling: the job is fixed.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -45,6 +46,9 @@ def parse():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--merge", choices=("peer", "nccl"), default="peer",
+                    help="N>1 key merge: fused into the compose kernel over NVLink peer memory "
+                         "(falls back to nccl if peer mapping fails) or an NCCL all-reduce")
     return ap.parse_args()
 
 
@@ -212,8 +216,28 @@ def ours(args):
         torch.cuda.synchronize(dev)
 
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    merge, merge_kind = None, "none" if world == 1 else "nccl all-reduce MIN"
+    if world > 1 and args.merge == "peer":
+        from paper_2511_02248_b200 import dist as pdist
+        try:
+            merge = pdist.PeerMerge(win.n, dev)
+            # verified once against the NCCL merge before it is used
+            planner.step(rank, world, allreduce)
+            want = planner.key.clone()
+            planner.step(merge=merge)
+            merge.check()
+            bad = torch.tensor([0 if torch.equal(planner.key, want) else 1], device=dev)
+        except Exception as exc:  # noqa: BLE001 -- fall back, consistently on all ranks
+            print(f"rank {rank}: peer merge unavailable: {exc}", file=sys.stderr, flush=True)
+            bad = torch.tensor([1], device=dev)
+        torch.distributed.all_reduce(bad, op=torch.distributed.ReduceOp.MAX)
+        if int(bad.item()):
+            merge = None
+            merge_kind = "nccl all-reduce MIN (peer merge unavailable or mismatched)"
+        else:
+            merge_kind = "fused: compose CTAs atomicMin into every rank's keys over NVLink peer memory + device barrier"
     for _ in range(args.warmup):
-        planner.step(rank, world, allreduce)
+        planner.step(rank, world, allreduce, merge=merge)
     barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
@@ -224,7 +248,7 @@ def ours(args):
         for i in range(args.steps):
             flush.zero_()  # L2 (126 MB) flushed between timed steps, outside the events
             ev[i][0].record()
-            planner.step(rank, world, allreduce, compose_events=cev[i])
+            planner.step(rank, world, allreduce, compose_events=cev[i], merge=merge)
             ev[i][1].record()
         barrier()
     launches = planner.launches - launches0
@@ -274,19 +298,19 @@ def ours(args):
         # decode + materialise, decisions back to host on every rank
         from paper_2511_02248_b200 import dist as pdist
         for _ in range(args.warmup):
-            pdist.plan_windows_host_sharded(planner, hwin, hout)
+            pdist.plan_windows_host_sharded(planner, hwin, hout, merge=merge)
         t = []
         for _ in range(args.steps):
             flush.zero_()
             barrier()
             t0 = time.perf_counter()
-            pdist.plan_windows_host_sharded(planner, hwin, hout)
+            pdist.plan_windows_host_sharded(planner, hwin, hout, merge=merge)
             t.append(time.perf_counter() - t0)
         tt = torch.tensor([sum(t)], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e = {"value": cands_step * len(t) / float(tt.item()), "unit": "candidates/s",
                "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(hout.nbytes()),
-               "api": "dist.plan_windows_host_sharded (host buffers, shard per rank, NCCL MIN merge)",
+               "api": "dist.plan_windows_host_sharded (host buffers, shard per rank, key merge)",
                "timing": "wall clock per rank, max over ranks",
                "parity_vs_device_path": bool(all(
                    getattr(hout, f).tobytes() == getattr(dec, f).tobytes()
@@ -335,8 +359,8 @@ def ours(args):
             "config": {"workload": WORKLOAD, "windows": win.n, "active_windows": active,
                        "candidates_per_window": space, "candidates_per_step": cands_step,
                        "mode": "oracle (exhaustive brute force, every candidate composed)",
-                       "parallelism": f"candidate-range shards x{world} + NCCL MIN all-reduce"
-                                      if world > 1 else "single GPU",
+                       "parallelism": f"candidate-range shards x{world}" if world > 1 else "single GPU",
+                       "merge": merge_kind,
                        "l2": "flushed between timed steps (256 MiB write outside the events)"},
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
@@ -356,6 +380,9 @@ def ours(args):
             "parity_vs_oracle": parity,
         }
         print(json.dumps(line), flush=True)
+    if merge is not None:
+        merge.check()
+        merge.close()
     if world > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()

@@ -391,6 +391,38 @@ OPSC_API int opsc_ctx_last_launches(const OpscContext* ctx, int32_t* launches);
  * writes elapsed milliseconds and the executed FP64 op count. */
 OPSC_API int opsc_fp64_peak(int32_t iters, float* ms, double* fp64_ops, void* stream);
 
+/* ---- multi-GPU key merge over NVLink peer memory ----
+ * The MIN merge of per-window keys (dist.merge_keys' NCCL all-reduce,
+ * SURVEY §8(e)) fused into the compose kernel: every CTA's atomicMin goes
+ * straight to the key buffer of every rank (peer pointers mapped with CUDA
+ * IPC), then one device-side flag barrier orders the merge before decode.
+ * Buffers are double-buffered by the caller (paper_2511_02248_b200/dist.py
+ * PeerMerge): the buffer for step s+1 is reset before the barrier of step s. */
+#define OPSC_MAX_PEERS 8
+
+/* cudaMalloc + zero + cudaIpcGetMemHandle; handle = 64 bytes */
+OPSC_API int opsc_ipc_alloc(size_t bytes, void** dptr, void* handle);
+/* cudaIpcOpenMemHandle (lazy peer access) of a handle from another process */
+OPSC_API int opsc_ipc_open(const void* handle, void** dptr);
+OPSC_API int opsc_ipc_close(void* dptr);
+OPSC_API int opsc_ipc_free(void* dptr);
+
+/* opsc_compose_argmin with the merge fused: peer_keys[0..n_peers) are the
+ * [W] int64 key buffers of every rank (this rank's included). */
+OPSC_API int opsc_compose_argmin_peers(const OpscDag* dag, const OpscGrid* grid, OpscWindows win,
+                                       const double* menu_w, int32_t shard, int32_t n_shards,
+                                       int64_t* const* peer_keys, int32_t n_peers, void* stream);
+
+/* Stream-ordered device copy of n int64 keys (merged keys -> decisions). */
+OPSC_API int opsc_copy_keys(int64_t* dst, const int64_t* src, int32_t n, void* stream);
+
+/* Device flag barrier over n ranks: flags[p] is rank p's [n] uint32 arrival
+ * array (this rank's own pointer at index `rank`); `epoch` increases by one
+ * per barrier. Release/acquire at system scope; a wait longer than
+ * timeout_ms sets *err = 1 instead of hanging. */
+OPSC_API int opsc_peer_barrier(uint32_t* const* flags, int32_t rank, int32_t n, uint32_t epoch,
+                               int32_t timeout_ms, int32_t* err, void* stream);
+
 /* Candidate-loop probe: the compose inner loop on synthetic register menus
  * (kind 1: DADD + DSETP + select per candidate, kind 2: DSETP + select).
  * Gives the instruction-mix ceiling of the compose kernel on this GPU. */

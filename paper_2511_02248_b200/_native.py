@@ -27,6 +27,8 @@ EXPORTS = (
     "opsc_candidate_probe", "opsc_greedy", "opsc_windowize", "opsc_windowize_workspace",
     "opsc_greedy_state_bytes", "opsc_greedy_phase", "opsc_model_table_bytes",
     "opsc_model_grid_table", "opsc_place_shared_workspace", "opsc_place_shared",
+    "opsc_ipc_alloc", "opsc_ipc_open", "opsc_ipc_close", "opsc_ipc_free",
+    "opsc_compose_argmin_peers", "opsc_peer_barrier", "opsc_copy_keys",
 )
 
 _lib = None
@@ -75,6 +77,13 @@ def load():
             "opsc_ctx_last_launches": ([P, P], C.c_int),
             "opsc_fp64_peak": ([I, P, P, P], C.c_int),
             "opsc_candidate_probe": ([I, I, P, P, P], C.c_int),
+            "opsc_ipc_alloc": ([C.c_size_t, P, P], C.c_int),
+            "opsc_ipc_open": ([P, P], C.c_int),
+            "opsc_ipc_close": ([P], C.c_int),
+            "opsc_ipc_free": ([P], C.c_int),
+            "opsc_compose_argmin_peers": ([P, P, W, P, I, I, P, I, P], C.c_int),
+            "opsc_peer_barrier": ([P, I, I, C.c_uint32, I, P, P], C.c_int),
+            "opsc_copy_keys": ([P, P, I, P], C.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

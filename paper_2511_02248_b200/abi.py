@@ -110,6 +110,9 @@ class OpscPlaceShared(C.Structure):
                 ("flags", _I)]
 
 
+MAX_PEERS = 8
+IPC_HANDLE_BYTES = 64
+
 PLACE_DEFAULT_STREAM = 0x1
 PLACE_WINDOW_SLO = 0x2
 

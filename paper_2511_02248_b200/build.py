@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT, "libopscale_b200.so")
-SOURCES = ["k_menu.cu", "k_compose.cu", "k_model.cu", "k_materialize.cu", "k_greedy.cu", "k_windowize.cu",
+SOURCES = ["k_menu.cu", "k_compose.cu", "k_model.cu", "k_materialize.cu", "k_greedy.cu", "k_windowize.cu", "k_peer.cu",
            "k_place.cu",
            "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -262,6 +262,67 @@ int opsc_compose_argmin(const OpscDag* dag, const OpscGrid* grid, OpscWindows wi
                                   (unsigned long long*)key_out, (cudaStream_t)stream));
 }
 
+int opsc_compose_argmin_peers(const OpscDag* dag, const OpscGrid* grid, OpscWindows win, const double* menu_w,
+                              int32_t shard, int32_t n_shards, int64_t* const* peer_keys, int32_t n_peers,
+                              void* stream) {
+  if (!valid_dag(dag) || !grid || !peer_keys || n_peers < 1 || n_peers > OPSC_MAX_PEERS) return OPSC_ERR_ARG;
+  ComposeCfg c;
+  const int rc = compose_setup(*dag, *grid, win.n, shard, n_shards, &c);
+  if (rc != OPSC_OK) return rc;
+  PeerKeys pk;
+  memset(&pk, 0, sizeof(pk));
+  pk.n = n_peers;
+  for (int p = 0; p < n_peers; ++p) {
+    if (!peer_keys[p]) return OPSC_ERR_ARG;
+    pk.p[p] = (unsigned long long*)peer_keys[p];
+  }
+  return from_cuda(launch_compose(c, *grid, win.n, menu_w, win.slo, win.qps, nullptr, (cudaStream_t)stream, &pk));
+}
+
+int opsc_peer_barrier(uint32_t* const* flags, int32_t rank, int32_t n, uint32_t epoch, int32_t timeout_ms,
+                      int32_t* err, void* stream) {
+  if (!flags || !err || n < 1 || n > OPSC_MAX_PEERS || rank < 0 || rank >= n || timeout_ms < 1) return OPSC_ERR_ARG;
+  PeerFlags f;
+  memset(&f, 0, sizeof(f));
+  for (int p = 0; p < n; ++p) {
+    if (!flags[p]) return OPSC_ERR_ARG;
+    f.p[p] = flags[p];
+  }
+  return from_cuda(launch_peer_barrier(f, rank, n, epoch, timeout_ms, err, (cudaStream_t)stream));
+}
+
+int opsc_copy_keys(int64_t* dst, const int64_t* src, int32_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!dst || !src))) return OPSC_ERR_ARG;
+  if (n == 0) return OPSC_OK;
+  return from_cuda(cudaMemcpyAsync(dst, src, (size_t)n * 8, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+}
+
+int opsc_ipc_alloc(size_t bytes, void** dptr, void* handle) {
+  if (!dptr || !handle || bytes == 0) return OPSC_ERR_ARG;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) return from_cuda(e);
+  e = cudaMemset(p, 0, bytes);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle((cudaIpcMemHandle_t*)handle, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return from_cuda(e);
+  }
+  *dptr = p;
+  return OPSC_OK;
+}
+
+int opsc_ipc_open(const void* handle, void** dptr) {
+  if (!dptr || !handle) return OPSC_ERR_ARG;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return from_cuda(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+}
+
+int opsc_ipc_close(void* dptr) { return from_cuda(cudaIpcCloseMemHandle(dptr)); }
+
+int opsc_ipc_free(void* dptr) { return from_cuda(cudaFree(dptr)); }
+
 int opsc_fill_keys(int64_t* key, int32_t n, void* stream) {
   return from_cuda(launch_fill_keys((unsigned long long*)key, n, (cudaStream_t)stream));
 }

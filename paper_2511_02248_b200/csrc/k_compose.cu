@@ -62,7 +62,8 @@ template <int NJ, bool CHAIN>
 __global__ void __launch_bounds__(kComposeThreads, OPSC_COMPOSE_MINB)
 compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ OpscGrid g,
                const double* __restrict__ menu_w, const double* __restrict__ slo_w,
-               const double* __restrict__ qps_w, unsigned long long* __restrict__ key_out) {
+               const double* __restrict__ qps_w, unsigned long long* __restrict__ key_out,
+               const __grid_constant__ PeerKeys peers) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ unsigned long long warp_best[kComposeThreads / 32];
   __shared__ __align__(8) unsigned long long tma_bar;
@@ -229,7 +230,16 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
   if (threadIdx.x < 32) {
     unsigned long long b = threadIdx.x < kComposeThreads / 32 ? warp_best[threadIdx.x] : kSentinel;
     b = warp_min_u64(b);
-    if (threadIdx.x == 0 && b < kSentinel) atomicMin(&key_out[w], b);
+    if (threadIdx.x == 0 && b < kSentinel) {
+      if (peers.n == 0) {
+        atomicMin(&key_out[w], b);
+      } else {
+        // fused multi-GPU merge: the CTA's minimum straight into every
+        // rank's key buffer over NVLink (IPC-mapped peer memory)
+        for (int p = 0; p < peers.n; ++p) atomicMin(peers.p[p] + w, b);
+        __threadfence_system();
+      }
+    }
   }
 }
 
@@ -317,7 +327,8 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
 
 template <int NJ, bool CHAIN>
 static cudaError_t launch_t(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,
-                            const double* slo, const double* qps, unsigned long long* key, cudaStream_t s) {
+                            const double* slo, const double* qps, unsigned long long* key, cudaStream_t s,
+                            const PeerKeys& pk) {
   const int mj = c.m[c.n - 1], mk = c.m[c.n - 2];
   const size_t smem = (size_t)mk * 8 + (size_t)(mj + 1) * 8 + (size_t)(c.E + 1) * 8 + (size_t)mj * 8 +
                       (size_t)(c.E + 1) * 4;
@@ -328,28 +339,33 @@ static cudaError_t launch_t(const ComposeCfg& c, const OpscGrid& g, int n_window
   }
   const long long blocks = (long long)n_windows * c.blocks_per_window;
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  compose_kernel<NJ, CHAIN><<<(unsigned)blocks, kComposeThreads, smem, s>>>(c, g, menu_w, slo, qps, key);
+  compose_kernel<NJ, CHAIN><<<(unsigned)blocks, kComposeThreads, smem, s>>>(c, g, menu_w, slo, qps, key, pk);
   return cudaGetLastError();
 }
 
 template <int NJ>
 static cudaError_t launch_nj(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,
-                             const double* slo, const double* qps, unsigned long long* key, cudaStream_t s) {
-  return c.chain ? launch_t<NJ, true>(c, g, n_windows, menu_w, slo, qps, key, s)
-                 : launch_t<NJ, false>(c, g, n_windows, menu_w, slo, qps, key, s);
+                             const double* slo, const double* qps, unsigned long long* key, cudaStream_t s,
+                             const PeerKeys& pk) {
+  return c.chain ? launch_t<NJ, true>(c, g, n_windows, menu_w, slo, qps, key, s, pk)
+                 : launch_t<NJ, false>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
 }
 
 cudaError_t launch_compose(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,
-                           const double* slo, const double* qps, unsigned long long* key, cudaStream_t s) {
+                           const double* slo, const double* qps, unsigned long long* key, cudaStream_t s,
+                           const PeerKeys* peers) {
   if (n_windows <= 0 || c.hi <= c.lo) return cudaSuccess;
+  PeerKeys pk;
+  memset(&pk, 0, sizeof(pk));
+  if (peers) pk = *peers;
   switch (c.nj) {
-    case 4: return launch_nj<4>(c, g, n_windows, menu_w, slo, qps, key, s);
-    case 8: return launch_nj<8>(c, g, n_windows, menu_w, slo, qps, key, s);
-    case 12: return launch_nj<12>(c, g, n_windows, menu_w, slo, qps, key, s);
-    case 16: return launch_nj<16>(c, g, n_windows, menu_w, slo, qps, key, s);
-    case 24: return launch_nj<24>(c, g, n_windows, menu_w, slo, qps, key, s);
-    case 32: return launch_nj<32>(c, g, n_windows, menu_w, slo, qps, key, s);
-    default: return launch_nj<0>(c, g, n_windows, menu_w, slo, qps, key, s);
+    case 4: return launch_nj<4>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
+    case 8: return launch_nj<8>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
+    case 12: return launch_nj<12>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
+    case 16: return launch_nj<16>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
+    case 24: return launch_nj<24>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
+    case 32: return launch_nj<32>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
+    default: return launch_nj<0>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
   }
 }
 

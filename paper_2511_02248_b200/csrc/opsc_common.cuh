@@ -175,9 +175,19 @@ cudaError_t launch_decode(const OpscDag& d, const OpscGrid& g, int n_windows,
 cudaError_t launch_fill_keys(unsigned long long* key, int n, cudaStream_t s);
 int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard, int n_shards,
                   ComposeCfg* cfg);
+// peer key buffers for the fused multi-GPU merge (n = 0: local atomics only)
+struct PeerKeys {
+  unsigned long long* p[OPSC_MAX_PEERS];
+  int32_t n;
+};
+struct PeerFlags {
+  uint32_t* p[OPSC_MAX_PEERS];
+};
 cudaError_t launch_compose(const ComposeCfg& c, const OpscGrid& g, int n_windows,
                            const double* menu_w, const double* slo, const double* qps,
-                           unsigned long long* key, cudaStream_t s);
+                           unsigned long long* key, cudaStream_t s, const PeerKeys* peers = nullptr);
+cudaError_t launch_peer_barrier(const PeerFlags& f, int rank, int n, uint32_t epoch, int timeout_ms,
+                                int32_t* err, cudaStream_t s);
 cudaError_t launch_model_grid(const OpscDag& d, const OpscModelSpec& m, OpscWindows w, int16_t* cfg,
                               uint8_t* feasible, uint32_t* status, cudaStream_t s,
                               void* table_ws = nullptr, size_t table_bytes = 0);

@@ -86,11 +86,11 @@ class DevicePlanner:
         _native.check(rc, what)
         self.launches += 1
 
-    def _init(self):
+    def _init(self, reset_key=True):
         # status = idle bit for qps <= 0, keys = +inf, feasible = 0
         self._ck(self.L.opsc_init_windows(self.win, self.out_t["status"].data_ptr(),
-                                          self.key.data_ptr(), self.out_t["feasible"].data_ptr(),
-                                          self._s()), "init_windows")
+                                          self.key.data_ptr() if reset_key else None,
+                                          self.out_t["feasible"].data_ptr(), self._s()), "init_windows")
 
     def menus(self):
         r = _native.ref
@@ -168,8 +168,12 @@ class DevicePlanner:
         self._model_grid_into(self.model, self.out_t["cfg"], self.out_t["feasible"],
                               self.out_t["status"], self._s())
 
-    def step(self, shard=0, n_shards=1, allreduce=None, compose_events=None):
-        """One pass of the hot path over the resident batch of windows."""
+    def step(self, shard=0, n_shards=1, allreduce=None, compose_events=None, merge=None):
+        """One pass of the hot path over the resident batch of windows.
+        `merge` (dist.PeerMerge): the multi-GPU merge fused into the compose
+        kernel over peer memory instead of `allreduce` after it."""
+        if merge is not None and self.mode == abi.MODE_ORACLE:
+            return merge.step(self, compose_events)
         self._init()
         if self.mode == abi.MODE_ORACLE:
             self.menus()
