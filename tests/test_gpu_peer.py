@@ -82,3 +82,21 @@ def test_peer_merge_two_ranks_sharing_the_gpu():
     p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, (p.stdout[-2000:], p.stderr[-3000:])
     assert p.stdout.count("ok") >= 2
+
+
+def test_host_buffer_round_trip_single_rank():
+    """dist.plan_windows_host_sharded (pinned host windows in, decisions out)
+    equals the device-resident step, with and without the fused merge."""
+    prob, grid, win = _cfg5(24)
+    a = device.DevicePlanner(prob, win, abi.MODE_ORACLE, grid=grid)
+    a.step()
+    want = a.decisions()
+    b = device.DevicePlanner(prob, tables.window_arrays(np.zeros(win.n), win.seq_len, 0, 0.5),
+                             abi.MODE_ORACLE, grid=grid)
+    merge = pdist.PeerMerge(win.n, "cuda")
+    for m in (None, merge):
+        out = tables.DecisionArrays(win.n, prob.n_ops)
+        pdist.plan_windows_host_sharded(b, win, out, merge=m)
+        for f in tables.DecisionArrays.FIELDS:
+            assert getattr(out, f).tobytes() == getattr(want, f).tobytes(), (m, f)
+    merge.close()
