@@ -342,6 +342,7 @@ def ours(args):
     if rank == 0 and not args.no_latency:
         latency = decision_latency(dev)
         latency["trace_pipeline"] = trace_pipeline(dev)
+        latency["capacity_8gpu"] = capacity_8gpu(dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -454,6 +455,32 @@ def decision_latency(dev):
                      "batched_ms_per_window": batch_ms / max(1, len(samples))}
     out["dag"] = "cfg2 Llama-2-70B 10-op chain, 60 x 60 s windows x {prefill, decode}, W = 1"
     return out
+
+
+def capacity_8gpu(dev):
+    """Config 4 (an extension without reference semantics):
+    per window, the largest arrival rate whose exhaustive min-objective
+    decision fits 8 x 80 GB devices -- batched k-ary bisection, each round one
+    planning launch set over windows x 32 rates."""
+    import torch
+
+    from paper_2511_02248_b200 import capacity, model, scenarios
+    dag, prof = scenarios.scenario("cfg1")
+    tw = scenarios.trace_windows("cfg2")
+    idx = np.linspace(0, 59, 8).round().astype(int)
+    pts = [model.WorkloadPoint(float(tw["prefill_qps"][i]), int(tw["prefill_len"][i]), "prefill") for i in idx]
+    params = model.AutoscaleParams(slo=scenarios.SLO["cfg1"]["prefill"])
+    bounds = model.BruteForceBounds(**scenarios.GRIDS["cfg1"])
+    capacity.max_qps_under_budget(dag, prof, pts[:1], params, bounds=bounds, max_rounds=1)  # warm-up
+    torch.cuda.synchronize(dev)
+    t = time.perf_counter()
+    res = capacity.max_qps_under_budget(dag, prof, pts, params, bounds=bounds, budget=8, mem_cap=80e9,
+                                        fan=32, rel_tol=1e-6)
+    dt = time.perf_counter() - t
+    return {"dag": "cfg1 7B 6-op, exhaustive 12^6 grid, 8 windows of the cfg2 trace (prefill)",
+            "budget": "8 x 80 GB, default-stream devices_used", "ms": dt * 1e3, "rounds": res.rounds,
+            "plans_evaluated": res.evaluated, "candidates_composed": res.evaluated * 12 ** 6,
+            "max_qps": [float(x) for x in res.qps], "devices": [int(x) for x in res.devices]}
 
 
 def trace_pipeline(dev):
