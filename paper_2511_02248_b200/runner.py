@@ -207,15 +207,16 @@ def _plan_key(params):
 
 
 def _plan_batch(mode, dag, profiles, points, params_list, bounds, T, max_enumeration):
-    """Plans (or _Raise) for points with qps > 0, one launch per params group."""
+    """(plans or _Raise per point, packed problem or None) for points with
+    qps > 0, one launch per params group."""
     m = _MODE_CODE.get(mode)
     out = [None] * len(points)
     if m is None:
-        return [_Raise(ValueError(f"unknown mode {mode!r}"))] * len(points)
+        return [_Raise(ValueError(f"unknown mode {mode!r}"))] * len(points), None
     try:
         problem = tables.pack_problem(dag, profiles)
     except Exception as exc:  # UnknownProfile etc.: every point raises it
-        return [_Raise(exc)] * len(points)
+        return [_Raise(exc)] * len(points), None
     PT, E = T.plan_types, T.err
     if m == abi.MODE_ORACLE and bounds is None:
         bounds = PT.BruteForceBounds()
@@ -267,10 +268,9 @@ def evaluate_points(mode, dag, profiles, fleet, points, params, placement_mode="
     extras = (fingerprint_extra if isinstance(fingerprint_extra, (list, tuple))
               else [fingerprint_extra] * n)
     energy_params = energy_params or model.EnergyParams()
-    planned = _plan_batch(mode, dag, profiles, points, params_list, bounds, T, max_enumeration)
-    if isinstance(planned, list):  # every point failed before packing
-        return planned
-    plans, problem = planned
+    plans, problem = _plan_batch(mode, dag, profiles, points, params_list, bounds, T, max_enumeration)
+    if problem is None:  # every point failed before packing
+        return plans
     label = f"{mode}/{placement_mode}"
     results = [None] * n
     to_place = []
