@@ -204,7 +204,7 @@ typedef struct OpscDecisions {
   int32_t* devices;   /* [W] devices_used under default-stream placement     */
   int32_t trace_cap;  /* entries per window in `trace` (operator mode)       */
   int32_t* trace_len; /* [W] number of moves (may exceed trace_cap)          */
-  OpscTraceEntry* trace; /* [W][trace_cap]                                   */
+  OpscTraceEntry* trace; /* [W][trace_cap]; entries >= trace_len[w] are unspecified */
 } OpscDecisions;
 
 /* ---- library info ---- */

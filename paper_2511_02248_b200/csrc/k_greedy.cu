@@ -7,9 +7,11 @@
 //     (all distinct (B, P) at R +- 1 for the bottleneck operator, :306-331) in
 //     parallel -- one thread per move: predict_op for the moved operator and
 //     the critical-path DP with that operator's weight replaced;
-//   * thread 0 applies the reference's selection keys in move order and
-//     recomputes the critical path (with its lexicographic tie-break) for the
-//     bottleneck of the next step; the prune pass is sequential as in :562-589.
+//   * the reference's selection keys are lexicographic minima with a unique
+//     (B, P) tie-break, so each is a block-wide reduction (warp shuffles);
+//     thread 0 applies the pick and recomputes the critical path (with its
+//     lexicographic tie-break) for the bottleneck of the next step; the
+//     prune pass is sequential as in :562-589.
 // The uniform reseed uses K3's model-level result for the same window.
 #include "opsc_common.cuh"
 
@@ -204,19 +206,61 @@ __device__ int eval_moves(GShared& S, const GreedyArgs& a, int op, int r_new, in
   return M;
 }
 
-struct Pick {
-  int m;
+// A move's selection key (k0, k1, k2, B, P) for one of the reference's
+// criteria; m < 0 = no candidate. Keys end in the move's unique (B, P), so
+// the lexicographic minimum is a total order: the block reduction below
+// picks exactly the move the reference's in-order scan picks.
+struct PK {
   double k0, k1;
-  int k2;
+  int k2, b, p, m;
 };
 
-__device__ __forceinline__ bool pick_less(double k0, double k1, int k2, int b, int p, const Pick& y, int yb,
-                                          int yp) {
-  if (k0 != y.k0) return k0 < y.k0;
-  if (k1 != y.k1) return k1 < y.k1;
-  if (k2 != y.k2) return k2 < y.k2;
-  if (b != yb) return b < yb;
-  return p < yp;
+__device__ __forceinline__ bool pk_less(const PK& x, const PK& y) {
+  if (x.m < 0) return false;
+  if (y.m < 0) return true;
+  if (x.k0 != y.k0) return x.k0 < y.k0;
+  if (x.k1 != y.k1) return x.k1 < y.k1;
+  if (x.k2 != y.k2) return x.k2 < y.k2;
+  if (x.b != y.b) return x.b < y.b;
+  return x.p < y.p;
+}
+
+__device__ __forceinline__ PK pk_shfl(const PK& x, int off) {
+  PK y;
+  y.k0 = __shfl_xor_sync(0xffffffffu, x.k0, off);
+  y.k1 = __shfl_xor_sync(0xffffffffu, x.k1, off);
+  y.k2 = __shfl_xor_sync(0xffffffffu, x.k2, off);
+  y.b = __shfl_xor_sync(0xffffffffu, x.b, off);
+  y.p = __shfl_xor_sync(0xffffffffu, x.p, off);
+  y.m = __shfl_xor_sync(0xffffffffu, x.m, off);
+  return y;
+}
+
+// Block-wide minimum of NK keys per thread (warp shuffles, then one warp
+// over the per-warp minima). All threads; result in out[] on every thread.
+template <int NK>
+__device__ void block_min(PK (&x)[NK]) {
+  __shared__ PK red[kGreedyThreads / 32][NK];
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+      const PK y = pk_shfl(x[k], off);
+      if (pk_less(y, x[k])) x[k] = y;
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NK; ++k) red[warp][k] = x[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    PK v = red[0][k];
+    for (int w2 = 1; w2 < kGreedyThreads / 32; ++w2)
+      if (pk_less(red[w2][k], v)) v = red[w2][k];
+    x[k] = v;
+  }
+  __syncthreads();
 }
 
 // thread 0: apply move m of `op` (new r), recompute the critical path
@@ -233,6 +277,10 @@ __device__ void apply_move(GShared& S, const OpscDag& d, int op, int m, int r_ne
 
 // One upscale step (greedy loop when headroom == false, _restore_headroom
 // otherwise). All threads; returns (via S.applied) whether a move was made.
+// Selection (autoscaler.py:395-455; headroom :503-557): first the cheapest
+// move reaching slo - eps (objective, latency, B, P), then (loop only) the
+// cheapest reaching slo, else the most efficient improving move
+// (-(dlat / dobj), latency, objective, B, P) -- each a block-wide minimum.
 __device__ void upscale_step(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps,
                              int L, int ph, double slo, double eps, bool headroom) {
   if (threadIdx.x == 0) S.op = bottleneck(S, a.d.n_ops);
@@ -246,35 +294,30 @@ __device__ void upscale_step(GShared& S, const GreedyArgs& a, const OpscDecision
     return;
   }
   const int M = eval_moves(S, a, op, cur_r + 1, 1, qps, L, ph);
-  if (threadIdx.x == 0) {
-    const int np = S.np_d[op];
-    const int base = objective(S, a.d.n_ops);
-    const double target = slo - eps;
-    Pick ach = {-1, 0, 0, 0}, ach2 = {-1, 0, 0, 0}, imp = {-1, 0, 0, 0};
-    int ab = 0, ap = 0, a2b = 0, a2p = 0, ib = 0, ip = 0;
-    for (int m = 0; m < M; ++m) {
-      if (!S.m_ok[m]) continue;
-      const int b = 1 + m / np, p = S.pd[op][m % np];
-      const double lat = S.m_lat[m];
-      const int obj = base - cur_p * cur_r + p * (cur_r + 1);
-      if (lat <= target && (ach.m < 0 || pick_less((double)obj, lat, 0, b, p, ach, ab, ap))) {
-        ach = {m, (double)obj, lat, 0}; ab = b; ap = p;
-      }
-      if (!headroom && lat <= slo && (ach2.m < 0 || pick_less((double)obj, lat, 0, b, p, ach2, a2b, a2p))) {
-        ach2 = {m, (double)obj, lat, 0}; a2b = b; a2p = p;
-      }
-      const bool improving = headroom ? lat < S.lat - 1e-9 * slo : lat < S.lat;
-      if (improving) {
-        const int dobj = obj - base;
-        const double cost = dobj >= 1 ? (double)dobj : 1e-9;
-        const double neg_eff = -((S.lat - lat) / cost);
-        const int k2 = headroom ? 0 : obj;
-        if (imp.m < 0 || pick_less(neg_eff, lat, k2, b, p, imp, ib, ip)) {
-          imp = {m, neg_eff, lat, k2}; ib = b; ip = p;
-        }
-      }
+  const int np = S.np_d[op];
+  const int base = objective(S, a.d.n_ops);
+  const double target = slo - eps, cur_lat = S.lat;
+  PK k[3];  // ach, ach2, imp
+  for (int i = 0; i < 3; ++i) k[i].m = -1;
+  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+    if (!S.m_ok[m]) continue;
+    const int b = 1 + m / np, p = S.pd[op][m % np];
+    const double lat = S.m_lat[m];
+    const int obj = base - cur_p * cur_r + p * (cur_r + 1);
+    const PK reach = {(double)obj, lat, 0, b, p, m};
+    if (lat <= target && pk_less(reach, k[0])) k[0] = reach;
+    if (!headroom && lat <= slo && pk_less(reach, k[1])) k[1] = reach;
+    const bool improving = headroom ? lat < cur_lat - 1e-9 * slo : lat < cur_lat;
+    if (improving) {
+      const int dobj = obj - base;
+      const double cost = dobj >= 1 ? (double)dobj : 1e-9;
+      const PK eff = {-((cur_lat - lat) / cost), lat, headroom ? 0 : obj, b, p, m};
+      if (pk_less(eff, k[2])) k[2] = eff;
     }
-    const int m = ach.m >= 0 ? ach.m : (!headroom && ach2.m >= 0) ? ach2.m : imp.m;
+  }
+  block_min<3>(k);
+  if (threadIdx.x == 0) {
+    const int m = k[0].m >= 0 ? k[0].m : (!headroom && k[1].m >= 0) ? k[1].m : k[2].m;
     S.applied = m >= 0;
     if (m >= 0) {
       apply_move(S, a.d, op, m, cur_r + 1, 1);
@@ -285,6 +328,8 @@ __device__ void upscale_step(GShared& S, const GreedyArgs& a, const OpscDecision
   __syncthreads();
 }
 
+// Downscale (autoscaler.py:456-486): the cheapest (objective, B, P) move at
+// R - 1 that stays within slo - eps and lowers the objective.
 __device__ void downscale_step(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps,
                                int L, int ph, double slo, double eps) {
   if (threadIdx.x == 0) S.op = bottleneck(S, a.d.n_ops);
@@ -298,20 +343,22 @@ __device__ void downscale_step(GShared& S, const GreedyArgs& a, const OpscDecisi
     return;
   }
   const int M = eval_moves(S, a, op, cur_r - 1, cur_b, qps, L, ph);
+  const int np = S.np_d[op];
+  const int base = objective(S, a.d.n_ops);
+  const double bound = slo - eps;
+  PK k[1];
+  k[0].m = -1;
+  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+    if (!S.m_ok[m] || S.m_lat[m] > bound) continue;
+    const int b = cur_b + m / np, p = S.pd[op][m % np];
+    const int obj = base - cur_p * cur_r + p * (cur_r - 1);
+    if (obj >= base) continue;
+    const PK c = {(double)obj, 0.0, 0, b, p, m};
+    if (pk_less(c, k[0])) k[0] = c;
+  }
+  block_min<1>(k);
   if (threadIdx.x == 0) {
-    const int np = S.np_d[op];
-    const int base = objective(S, a.d.n_ops);
-    const double bound = slo - eps;
-    int best = -1, bo = 0, bb = 0, bp = 0;
-    for (int m = 0; m < M; ++m) {
-      if (!S.m_ok[m] || S.m_lat[m] > bound) continue;
-      const int b = cur_b + m / np, p = S.pd[op][m % np];
-      const int obj = base - cur_p * cur_r + p * (cur_r - 1);
-      if (obj >= base) continue;
-      if (best < 0 || obj < bo || (obj == bo && (b < bb || (b == bb && p < bp)))) {
-        best = m; bo = obj; bb = b; bp = p;
-      }
-    }
+    const int best = k[0].m;
     S.applied = best >= 0;
     if (best >= 0) {
       apply_move(S, a.d, op, best, cur_r - 1, cur_b);
