@@ -29,12 +29,17 @@ __device__ __forceinline__ double op_latency(const OpscDag& d, int ph, int v, lo
 }
 
 // queueing.py:54-75: Erlang-B recurrence recomputed with a = R*rho.
+// Once b underflows to +0 every later step is exactly +0 (a*0 = 0, k+0 = k,
+// 0/k = +0), so the loop stops there: the same bits without the remaining
+// steps, whose zero-numerator divisions take the slow path (~3x a normal
+// step on B200; tools/probe/erlang_probe.cu).
 __device__ __forceinline__ double erlang_c(int r, double rho) {
   const double a = (double)r * rho;
   double b = 1.0;
   for (int k = 1; k <= r; ++k) {
     const double ab = a * b;
     b = ab / ((double)k + ab);
+    if (b == 0.0) break;
   }
   return ((double)r * b) / ((double)r - a * (1.0 - b));
 }
