@@ -14,16 +14,24 @@
 //   * positions = topological order; the last two are the k and j levels,
 //     `il-2` middle levels sit above them, the rest are "outer" and fixed per
 //     thread (decoded from the thread's outer index);
-//   * the j menu (innermost op) is staged SORTED by its key (P*R, entry) and
-//     held in registers; per candidate the thread issues exactly
+//   * the j menu (innermost op) is staged in shared memory sorted by WEIGHT
+//     and held in registers. For a fixed prefix (everything but j) the
+//     candidate latency fl(B_j + w_j) is monotone in w_j, so the feasible j
+//     form a prefix of that order and the cheapest feasible j is a table
+//     lookup pm[count] (prefix minimum of the j keys in weight order). Per
+//     candidate the thread issues exactly
 //         DADD  lat = B_j + w_j          (path extension, the DP's last add)
 //         DSETP lat <= slo               (SLO mask)
-//         @P MOV inner = rank            (descending scan: the last hit is the
-//                                         cheapest feasible j of this prefix)
-//     with no loop-carried dependency, so warps issue back to back;
-//   * per k entry the cheapest feasible (k, j) pair is folded into a u64 key
-//     from shared-memory key tables; CTA result = warp-shuffle u64 min ->
-//     smem -> one atomicMin per CTA.
+//         SEL   count = i + 1            (ascending scan: the last hit is the
+//                                         length of the feasible prefix)
+//     with no loop-carried dependency, so warps issue back to back. The
+//     per-k fold works on 32-bit local keys (cost_k + cost_j, local (k, j)
+//     index) from 32-bit shared addresses, converted to the u64 key once per
+//     prefix. (OPSC_COMPOSE_FP32MASK selects an alternative mask on the FMA
+//     pipe; see its definition for why it is off);
+//   * per k entry the cheapest feasible (k, j) pair is folded into the
+//     prefix's minimum; CTA result = warp-shuffle u64 min -> smem -> one
+//     atomicMin per CTA.
 #include <algorithm>
 #include <cstring>
 
@@ -35,7 +43,16 @@ namespace opsc {
 #define OPSC_COMPOSE_THREADS 256
 #endif
 #ifndef OPSC_COMPOSE_MINB
-#define OPSC_COMPOSE_MINB 4  // 64 registers: 32 warps/SM hide the DADD->DSETP->SEL latency (+12% vs 3)
+#define OPSC_COMPOSE_MINB 3  // 80 registers, no spills: 7.38e12 vs 7.28e12 candidates/s at 4 CTAs/SM (64 regs, spills)
+#endif
+#ifndef OPSC_COMPOSE_FP32MASK
+// 1: high-word SLO mask on the FMA pipe (DADD + FFMA.SAT + IADD3/2 per
+//    candidate, superset count trimmed exactly) -- fewer issue slots, but on
+//    B200 it measured 6.1e12 candidates/s against 7.3e12 for the exact
+//    DADD + DSETP + SEL form: ptxas keeps one latency register per thread under
+//    the 64-register cap and the DADD -> FFMA chains stall (ncu: issue active
+//    72%, every pipe < 40%). Kept for A/B runs (tools/variants.sh).
+#define OPSC_COMPOSE_FP32MASK 0
 #endif
 constexpr int kComposeThreads = OPSC_COMPOSE_THREADS;
 constexpr unsigned long long kSentinel = 1ull << 62;  // > any real key (objective < 2^17)
@@ -54,9 +71,192 @@ struct ComposeSmem {
   double* w;                 // [E+1] weights (entry E = virtual, 0.0)
   int32_t* cost;             // [E+1] P*R per entry
   unsigned long long* kk;    // [m_k] (cost_k << 40) + a * kstride
-  double* jw;                // [m_j] j weights sorted by key
-  unsigned long long* jk;    // [m_j + 1] sorted j keys, jk[m_j] = sentinel
+  double* jw;                // [m_j] j weights in ascending order (NaN as +inf)
+  unsigned long long* pmk;   // [m_j + 1] pmk[c] = min key of the c lightest j entries, pmk[0] = sentinel
+  uint32_t* kk32;            // [m_k] local form (register-tile path): cost_k << 20 | a * ks
+  uint32_t* pm32;            // [m_j + 1] local form of pmk: cost_j << 20 | i * js, pm32[0] = 2^31
 };
+
+// Local (k, j) keys of the register-tile path: cost_k + cost_j < 2^11 in
+// bits 20..30 and the (k, j) index in lexicographic order in bits 0..19, so
+// key order is the u64 key order restricted to one prefix, any sum with
+// pm32[0] = 2^31 is >= 2^31 (infeasible), and nothing overflows.
+constexpr uint32_t kLocalInfeasible = 1u << 31;
+
+// High-word SLO mask constants. For a window with 0 < slo and
+// 2^25 <= bits(Hf) >> 23 <= 254, where Hf is the float whose bits are
+// hi32(slo) + 1:
+//     t(lat) = sat(fma(f, -BIG, Hf*BIG)),  f = float with bits hi32(lat),
+//     BIG = 2^(25 - exponent(Hf)),
+// is exactly 1.0f when s32(hi32(lat)) <= s32(hi32(slo)) and +0.0f otherwise
+// (NaN lat -> 0). Distinct floats near Hf differ by >= 2^(e-24), so a
+// passing difference scales to >= 2 before saturation. Every lat <= slo
+// passes: non-negative doubles order like their bit patterns, negative ones
+// have a negative f. Windows outside that slo range (the reference rejects
+// slo <= 0; the others are >= 2^1017 or < 2^-823) take the exact scan.
+struct MaskConsts {
+  float nbig, hb;
+  bool fast;
+};
+
+__device__ __forceinline__ MaskConsts mask_consts(double slo) {
+  MaskConsts m;
+  const int h1 = __double2hiint(slo) + 1;
+  const int ex = h1 >> 23;  // biased float exponent of Hf
+  m.fast = slo > 0.0 && ex >= 25 && ex <= 254;
+  const int eb = m.fast ? 127 + 25 - (ex - 127) : 127;  // BIG = 2^(25 - e)
+  m.nbig = -__int_as_float(eb << 23);
+  m.hb = __int_as_float(h1) * -m.nbig;  // exact: power-of-two scaling into [2^25, 2^26)
+  return m;
+}
+
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(x));
+  return x;
+}
+
+// 32-bit shared-window loads (the k loop keeps four 32-bit addresses live
+// instead of 64-bit generic pointers)
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+
+// High-word mask count of one j row: number of j with t(bj + w_j) = 1.
+template <int NJ>
+__device__ __forceinline__ uint32_t mask_count(double bj, const double (&wj)[NJ], MaskConsts mc) {
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < NJ; i += 2) {
+    const double la = bj + wj[i];
+    const float ta = __saturatef(__fmaf_rn(__int_as_float(__double2hiint(la)), mc.nbig, mc.hb));
+    float tb = 0.0f;
+    if (i + 1 < NJ) {
+      const double lb = bj + wj[i + 1];
+      tb = __saturatef(__fmaf_rn(__int_as_float(__double2hiint(lb)), mc.nbig, mc.hb));
+    }
+    acc += __float_as_uint(ta) + __float_as_uint(tb);
+  }
+  // acc = n * 0x3F800000 (mod 2^32) = 2^23 * 127 n; 383 = 127^-1 mod 512
+  return ((acc >> 23) * 383u) & 511u;
+}
+
+// Two j rows (k entries a and a+1) interleaved: two independent DADD chains
+// per thread over the same register-resident j weights.
+template <int NJ>
+__device__ __forceinline__ void mask_count2(double bj0, double bj1, const double (&wj)[NJ], MaskConsts mc,
+                                            uint32_t& c0, uint32_t& c1) {
+  uint32_t acc0 = 0, acc1 = 0;
+#pragma unroll
+  for (int i = 0; i < NJ; i += 2) {
+    const double la0 = bj0 + wj[i];
+    const double la1 = bj1 + wj[i];
+    const float ta0 = __saturatef(__fmaf_rn(__int_as_float(__double2hiint(la0)), mc.nbig, mc.hb));
+    const float ta1 = __saturatef(__fmaf_rn(__int_as_float(__double2hiint(la1)), mc.nbig, mc.hb));
+    float tb0 = 0.0f, tb1 = 0.0f;
+    if (i + 1 < NJ) {
+      const double lb0 = bj0 + wj[i + 1];
+      const double lb1 = bj1 + wj[i + 1];
+      tb0 = __saturatef(__fmaf_rn(__int_as_float(__double2hiint(lb0)), mc.nbig, mc.hb));
+      tb1 = __saturatef(__fmaf_rn(__int_as_float(__double2hiint(lb1)), mc.nbig, mc.hb));
+    }
+    acc0 += __float_as_uint(ta0) + __float_as_uint(tb0);
+    acc1 += __float_as_uint(ta1) + __float_as_uint(tb1);
+  }
+  c0 = ((acc0 >> 23) * 383u) & 511u;
+  c1 = ((acc1 >> 23) * 383u) & 511u;
+}
+
+// Exact count: the feasible j form a prefix in weight order.
+template <int NJ>
+__device__ __forceinline__ uint32_t exact_count(double bj, const double (&wj)[NJ], double slo) {
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int i = 0; i < NJ; ++i)
+    if (bj + wj[i] <= slo) cnt = (uint32_t)i + 1u;
+  return cnt;
+}
+
+// Superset count -> exact count: drop boundary entries that tie slo's high
+// word but fail the full compare.
+__device__ __forceinline__ uint32_t trim_count(uint32_t cnt, uint32_t mj, double bj, uint32_t a_jw, double slo) {
+  cnt = cnt < mj ? cnt : mj;
+  while (cnt > 0 && !(bj + lds_f64(a_jw + 8u * (cnt - 1u)) <= slo)) --cnt;
+  return cnt;
+}
+
+template <bool CHAIN>
+__device__ __forceinline__ double j_base(double bk, double bj0, double lo0, bool k_to_j, bool k_sink, double slo) {
+  if (CHAIN) return bk;  // j's only predecessor is k, k is not a sink
+  const double bj = k_to_j ? fmax(bj0, bk) : bj0;
+  const double lo = k_sink ? fmax(lo0, bk) : lo0;
+  return lo <= slo ? bj : OPSC_INF;
+}
+
+// The k and j levels for one prefix. Register-tile path (NJ > 0): returns
+// the minimum local key (>= kLocalInfeasible if no candidate is feasible).
+// a_wk / a_kk / a_pm / a_jw: shared addresses of w[koff], kk32, pm32, jw.
+template <int NJ, bool CHAIN, bool FAST>
+__device__ __forceinline__ uint32_t k_level_tile(uint32_t a_wk, uint32_t a_kk, uint32_t a_pm, uint32_t a_jw,
+                                                 int mk, int mj, const double (&wj)[NJ], double in_k, double bj0,
+                                                 double lo0, bool k_to_j, bool k_sink, double slo, MaskConsts mc) {
+  uint32_t mbest = 0xffffffffu;
+  const uint32_t a_end = a_kk + 4u * (uint32_t)mk;
+  if (FAST) {
+#pragma unroll 1
+    for (; a_kk + 4u < a_end; a_kk += 8u, a_wk += 16u) {
+      const double bja = j_base<CHAIN>(in_k + lds_f64(a_wk), bj0, lo0, k_to_j, k_sink, slo);
+      const double bjb = j_base<CHAIN>(in_k + lds_f64(a_wk + 8u), bj0, lo0, k_to_j, k_sink, slo);
+      uint32_t ca, cb;
+      mask_count2<NJ>(bja, bjb, wj, mc, ca, cb);
+      ca = trim_count(ca, (uint32_t)mj, bja, a_jw, slo);
+      cb = trim_count(cb, (uint32_t)mj, bjb, a_jw, slo);
+      const uint32_t ka = lds_u32(a_kk) + lds_u32(a_pm + 4u * ca);
+      const uint32_t kb = lds_u32(a_kk + 4u) + lds_u32(a_pm + 4u * cb);
+      mbest = min(mbest, min(ka, kb));
+    }
+  }
+#pragma unroll 1
+  for (; a_kk < a_end; a_kk += 4u, a_wk += 8u) {
+    const double bj = j_base<CHAIN>(in_k + lds_f64(a_wk), bj0, lo0, k_to_j, k_sink, slo);
+    uint32_t cnt = FAST ? trim_count(mask_count<NJ>(bj, wj, mc), (uint32_t)mj, bj, a_jw, slo)
+                        : min(exact_count<NJ>(bj, wj, slo), (uint32_t)mj);
+    const uint32_t kl = lds_u32(a_kk) + lds_u32(a_pm + 4u * cnt);
+    mbest = kl < mbest ? kl : mbest;
+  }
+  return mbest;
+}
+
+// Shared-memory path for large j menus (NJ == 0): u64 keys, exact compares.
+template <bool CHAIN>
+__device__ __forceinline__ unsigned long long k_level_smem(const ComposeSmem& s, int mk, int mj, int koff,
+                                                           double in_k, double bj0, double lo0, bool k_to_j,
+                                                           bool k_sink, double slo) {
+  unsigned long long mbest = kSentinel;
+  for (int a = 0; a < mk; ++a) {
+    const double bk = in_k + s.w[koff + a];
+    double bj;
+    if (CHAIN) {
+      bj = bk;
+    } else {
+      bj = k_to_j ? fmax(bj0, bk) : bj0;
+      const double lo = k_sink ? fmax(lo0, bk) : lo0;
+      if (!(lo <= slo)) bj = OPSC_INF;
+    }
+    int cnt = 0;
+    for (int i = 0; i < mj; ++i)
+      if (bj + s.jw[i] <= slo) cnt = i + 1;
+    const unsigned long long kl = s.kk[a] + s.pmk[cnt];
+    mbest = kl < mbest ? kl : mbest;
+  }
+  return mbest;
+}
 
 template <int NJ, bool CHAIN>
 __global__ void __launch_bounds__(kComposeThreads, OPSC_COMPOSE_MINB)
@@ -72,9 +272,11 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
   ComposeSmem s;
   s.w = reinterpret_cast<double*>(smem_raw);  // offset 0: 16-byte aligned TMA target
   s.kk = reinterpret_cast<unsigned long long*>(s.w + c.E + 1);
-  s.jk = s.kk + mk;
-  s.jw = reinterpret_cast<double*>(s.jk + mj + 1);
+  s.pmk = s.kk + mk;
+  s.jw = reinterpret_cast<double*>(s.pmk + mj + 1);
   s.cost = reinterpret_cast<int32_t*>(s.jw + mj);
+  s.kk32 = reinterpret_cast<uint32_t*>(s.cost + c.E + 1);
+  s.pm32 = s.kk32 + mk;
 
   const int w = blockIdx.x / c.blocks_per_window;
   const int bw = blockIdx.x - w * c.blocks_per_window;
@@ -125,23 +327,71 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
   }
   __syncthreads();
   const int koff = c.off[kp], joff = c.off[jp];
-  for (int a = threadIdx.x; a < mk; a += kComposeThreads)
+  const uint32_t ks = c.kj_major ? (uint32_t)mj : 1u, js = c.kj_major ? 1u : (uint32_t)mk;
+  for (int a = threadIdx.x; a < mk; a += kComposeThreads) {
     s.kk[a] = ((unsigned long long)s.cost[koff + a] << OPSC_KEY_LEX_BITS) + (unsigned long long)a * c.stride[kp];
+    s.kk32[a] = ((uint32_t)s.cost[koff + a] << 20) + (uint32_t)a * ks;
+  }
   for (int i = threadIdx.x; i < mj; i += kComposeThreads) {
-    // rank of entry i in (cost, entry) order == order of its key
-    const int ci = s.cost[joff + i];
+    // rank of entry i in (weight, entry) order; NaN never passes a compare,
+    // exactly like +inf, so it sorts as +inf
+    double wi = s.w[joff + i];
+    wi = wi != wi ? OPSC_INF : wi;
     int rank = 0;
     for (int q = 0; q < mj; ++q) {
-      const int cq = s.cost[joff + q];
-      rank += (cq < ci) || (cq == ci && q < i);
+      double wq = s.w[joff + q];
+      wq = wq != wq ? OPSC_INF : wq;
+      rank += (wq < wi) || (wq == wi && q < i);
     }
-    s.jw[rank] = s.w[joff + i];
-    s.jk[rank] = ((unsigned long long)ci << OPSC_KEY_LEX_BITS) + (unsigned long long)i * c.stride[jp];
+    s.jw[rank] = wi;
+    s.pmk[rank + 1] = ((unsigned long long)s.cost[joff + i] << OPSC_KEY_LEX_BITS) +
+                      (unsigned long long)i * c.stride[jp];
+    s.pm32[rank + 1] = ((uint32_t)s.cost[joff + i] << 20) + (uint32_t)i * js;
   }
-  if (threadIdx.x == 0) s.jk[mj] = kSentinel;
+  __syncthreads();
+  if (threadIdx.x < 32) {  // pmk[1..mj] = running minimum (warp scan in chunks of 32)
+    unsigned long long carry = kSentinel;
+    uint32_t carry32 = 0xffffffffu;
+    for (int base = 0; base < mj; base += 32) {
+      const int i = base + threadIdx.x;
+      unsigned long long v = i < mj ? s.pmk[i + 1] : kSentinel;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long u = __shfl_up_sync(0xffffffffu, v, o);
+        if ((int)threadIdx.x >= o) v = u < v ? u : v;
+      }
+      v = carry < v ? carry : v;
+      if (i < mj) s.pmk[i + 1] = v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
+      uint32_t v32 = i < mj ? s.pm32[i + 1] : 0xffffffffu;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, v32, o);
+        if ((int)threadIdx.x >= o) v32 = u < v32 ? u : v32;
+      }
+      v32 = carry32 < v32 ? carry32 : v32;
+      if (i < mj) s.pm32[i + 1] = v32;
+      carry32 = __shfl_sync(0xffffffffu, v32, 31);
+    }
+    if (threadIdx.x == 0) {
+      s.pmk[0] = kSentinel;
+      s.pm32[0] = kLocalInfeasible;
+    }
+  }
   __syncthreads();
 
-  const double slo = slo_w[w];
+  // An infinite SLO admits every candidate whose weights are all finite (the
+  // reference skips non-finite menu weights, autoscaler.py:800-801): compare
+  // against DBL_MAX, which keeps the INF-weighted (unstable) entries out.
+  const double slo = fmin(slo_w[w], 1.7976931348623157e308);
+  const MaskConsts mc = mask_consts(slo);
+  // opaque copies: keeps the k loop from rematerialising the addresses
+  // (CgaCtaId + parameter loads) in every iteration under register pressure
+  const uint32_t a_wk = opaque_u32((uint32_t)__cvta_generic_to_shared(s.w + koff));
+  const uint32_t a_kk = opaque_u32((uint32_t)__cvta_generic_to_shared(s.kk32));
+  const uint32_t a_pm = opaque_u32((uint32_t)__cvta_generic_to_shared(s.pm32));
+  const uint32_t a_jw = opaque_u32((uint32_t)__cvta_generic_to_shared(s.jw));
+  const int mk_r = (int)opaque_u32((uint32_t)mk), mj_r = (int)opaque_u32((uint32_t)mj);
   unsigned long long best = kSentinel;
   const uint32_t o = c.lo + (uint32_t)bw * kComposeThreads + threadIdx.x;
   if (qps_w[w] > 0.0 && o < c.hi) {
@@ -192,31 +442,22 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
       if (CHAIN && !(lo0 <= slo)) in_k = OPSC_INF;  // another sink already misses the SLO
 
       unsigned long long mbest = kSentinel;
-      for (int a = 0; a < mk; ++a) {
-        const double bk = in_k + s.w[koff + a];
-        double bj;
-        if (CHAIN) {
-          bj = bk;  // j's only predecessor is k, k is not a sink
-        } else {
-          bj = k_to_j ? fmax(bj0, bk) : bj0;
-          const double lo = k_sink ? fmax(lo0, bk) : lo0;
-          if (!(lo <= slo)) bj = OPSC_INF;
+      if constexpr (NJ > 0) {
+        const uint32_t m32 =
+            (OPSC_COMPOSE_FP32MASK && mc.fast)
+                ? k_level_tile<NJ, CHAIN, true>(a_wk, a_kk, a_pm, a_jw, mk_r, mj_r, wj, in_k, bj0, lo0, k_to_j,
+                                                k_sink, slo, mc)
+                : k_level_tile<NJ, CHAIN, false>(a_wk, a_kk, a_pm, a_jw, mk_r, mj_r, wj, in_k, bj0, lo0, k_to_j,
+                                                 k_sink, slo, mc);
+        if (m32 < kLocalInfeasible) {  // back to the global key
+          const uint32_t loc = m32 & 0xfffffu;
+          const uint32_t a = c.kj_major ? loc / (uint32_t)mj : loc % (uint32_t)mk;
+          const uint32_t i = c.kj_major ? loc % (uint32_t)mj : loc / (uint32_t)mk;
+          mbest = ((unsigned long long)(m32 >> 20) << OPSC_KEY_LEX_BITS) + (unsigned long long)a * c.stride[kp] +
+                  (unsigned long long)i * c.stride[jp];
         }
-        int inner = mj;
-        if (NJ > 0) {
-#pragma unroll
-          for (int i = NJ - 1; i >= 0; --i) {
-            const double lat = bj + wj[i];
-            if (lat <= slo) inner = i;
-          }
-        } else {
-          for (int i = mj - 1; i >= 0; --i) {
-            const double lat = bj + s.jw[i];
-            if (lat <= slo) inner = i;
-          }
-        }
-        const unsigned long long kl = s.kk[a] + s.jk[inner];
-        mbest = kl < mbest ? kl : mbest;
+      } else {
+        mbest = k_level_smem<CHAIN>(s, mk, mj, koff, in_k, bj0, lo0, k_to_j, k_sink, slo);
       }
       if (mbest < kSentinel) {
         const unsigned long long key = ((unsigned long long)cost1 << OPSC_KEY_LEX_BITS) + lex1 + mbest;
@@ -316,8 +557,22 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
   c.hi = (uint32_t)((unsigned long long)c.m_out * (shard + 1) / n_shards);
   c.blocks_per_window = (int)((c.hi - c.lo + kComposeThreads - 1) / kComposeThreads);
   if (c.blocks_per_window < 1) c.blocks_per_window = 1;
-  const int mj = c.m[c.n - 1];
+  const int mj = c.m[c.n - 1], mk = c.m[c.n - 2];
   c.nj = mj <= 4 ? 4 : mj <= 8 ? 8 : mj <= 12 ? 12 : mj <= 16 ? 16 : mj <= 24 ? 24 : mj <= 32 ? 32 : 0;
+  c.kj_major = c.stride[c.n - 2] > c.stride[c.n - 1] ? 1 : 0;
+  // register-tile local keys: (k, j) index < 2^20 and cost_k + cost_j < 2^11
+  auto max_cost = [&](int pos) {
+    int mx = 0;
+    for (int e = 0; e < c.m[pos]; ++e) {
+      if (c.off[pos] >= c.E) break;  // virtual position: cost 0
+      const int v = d.topo[pos - nvirt];
+      int p, r, b;
+      opsc::entry_prb(g, v, e, p, r, b);
+      mx = std::max(mx, p * r);
+    }
+    return mx;
+  };
+  if ((long long)mj * mk >= (1 << 20) || max_cost(c.n - 1) + max_cost(c.n - 2) >= (1 << 11)) c.nj = 0;
   // chain fast path: j's only predecessor is k and k is not a sink
   const int jp = c.n - 1, kp = c.n - 2;
   c.chain = (c.pmask[jp] == (1u << kp)) && !(c.sinkmask >> kp & 1u);
@@ -331,7 +586,7 @@ static cudaError_t launch_t(const ComposeCfg& c, const OpscGrid& g, int n_window
                             const PeerKeys& pk) {
   const int mj = c.m[c.n - 1], mk = c.m[c.n - 2];
   const size_t smem = (size_t)mk * 8 + (size_t)(mj + 1) * 8 + (size_t)(c.E + 1) * 8 + (size_t)mj * 8 +
-                      (size_t)(c.E + 1) * 4;
+                      (size_t)(c.E + 1) * 4 + (size_t)mk * 4 + (size_t)(mj + 1) * 4;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(compose_kernel<NJ, CHAIN>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

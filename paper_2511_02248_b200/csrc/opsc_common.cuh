@@ -104,7 +104,7 @@ __device__ __forceinline__ double weight(const Pred& o, int layers) {
 }
 
 // menu entry -> (P, R, B), lexicographic (P, R, B) order (autoscaler.py:747-749)
-__device__ __forceinline__ void entry_prb(const OpscGrid& g, int v, int e, int& p, int& r, int& b) {
+__host__ __device__ __forceinline__ void entry_prb(const OpscGrid& g, int v, int e, int& p, int& r, int& b) {
   const int bm = g.b_max[v];
   b = e % bm + 1;
   r = (e / bm) % g.r_max + 1;
@@ -162,6 +162,7 @@ struct ComposeCfg {
   int32_t blocks_per_window;
   int32_t nj;                  // register tile of the innermost menu
   int32_t chain;               // j's only predecessor is k and k is not a sink
+  int32_t kj_major;            // k precedes j in lexicographic order: local (k, j) index a*m_j + i, else i*m_k + a
 };
 
 namespace opsc {

@@ -1,0 +1,115 @@
+"""Compose-kernel edge cases on crafted menus, device keys against the CPU
+oracle's literal enumeration on the SAME menu weights:
+
+* sums landing within a few ulps of the SLO (ties at the 2^-40 grain,
+  slo = 1.0 and non-power-of-two slos), which separates an exact mask from
+  any high-word or threshold shortcut and checks the weight-sorted feasible-
+  prefix count;
+* slo = +inf with unstable (INF-weighted) entries: only all-finite candidates
+  qualify, as in the reference's skip of non-finite weights
+  (autoscaler.py:800-801);
+* a menu with negative weights (the kernel's exact-scan path);
+* chain (CHAIN kernel) and merge / fork DAGs (generic kernel), j menus from
+  4 to 32 entries (every NJ specialisation) and > 32 (smem loop).
+"""
+
+import zlib
+
+import numpy as np
+import pytest
+
+from paper_2511_02248_b200 import abi, model, tables
+
+pytestmark = pytest.mark.gpu
+
+ULP40 = 2.0 ** -40
+
+
+@pytest.fixture(scope="module")
+def nat_loaded():
+    from paper_2511_02248_b200 import _native
+    _native.load()
+    assert _native.device_count() >= 1, "no CUDA device"
+    return _native
+
+
+def _dag(n, shape):
+    ids = [f"op{chr(97 + i)}" for i in range(n)]
+    if shape == "chain":
+        edges = [(ids[i], ids[i + 1]) for i in range(n - 1)]
+    elif shape == "merge":
+        edges = [(ids[i], ids[i + 1]) for i in range(n - 3)] + [(ids[n - 3], ids[n - 1]), (ids[n - 2], ids[n - 1])]
+    else:  # fork: two sinks
+        edges = [(ids[i], ids[i + 1]) for i in range(n - 2)] + [(ids[n - 3], ids[n - 1])]
+    nodes = [{"id": i, "kind": "linear", "layer_count": 1, "profile_ref": "p" + i} for i in ids]
+    prof = {"_link_bandwidth": 900e9}
+    for i in ids:
+        prof["p" + i] = {"prefill": {"c0": 1e-5, "c1": 1e-8}, "decode": {"c0": 1e-5, "c1": 1e-8},
+                         "weight_mem": 1e8, "m1": 1e4, "v1": 1e4, "s0": 0.1, "s1": 1e-4}
+    dag = {"nodes": nodes, "edges": [{"src": a, "dst": b, "volume_ref": "p" + a} for a, b in edges]}
+    return tables.pack_problem(model.build_dag(dag), model.profiles_from_dict(prof))
+
+
+def _menus(rng, prob, grid, slos, kind):
+    """Menu weights whose candidate latencies crowd the SLO at the 2^-40 grain.
+    Every path of the DAGs here visits n_path ops; each op's weight is
+    slo/n_path plus a few 2^-40 steps, so sums are exact and tie the SLO."""
+    n = prob.n_ops
+    E = grid.menu_off[n]
+    # per-entry cost P*R in the menu's (P, R, B) order; cheaper entries are
+    # heavier (as on real menus), so the argmin sits in the SLO's tie band
+    cost = np.concatenate([[p * r for p in (1, 2) for r in range(1, grid.r_max + 1) for _ in range(grid.b_max[v])]
+                           for v in range(n)]).astype(np.float64)
+    assert cost.size == E
+    mw = np.empty((len(slos), E))
+    for w, slo in enumerate(slos):
+        base = (1.0 if not np.isfinite(slo) else slo) / (n if kind != "short" else n - 1)
+        base = np.ldexp(np.round(np.ldexp(base, 40)), -40)  # on the 2^-40 grid
+        mw[w] = base + (rng.integers(-3, 4, E) + 2.0 * (cost.mean() - cost)) * ULP40
+        if kind == "inf":
+            mw[w, rng.uniform(size=E) < 0.2] = np.inf
+        if kind == "neg":
+            mw[w, rng.uniform(size=E) < 0.1] *= -1.0
+    return mw
+
+
+@pytest.mark.parametrize("shape,n,r_max,b_max,kind", [
+    ("chain", 6, 3, 2, "tie"), ("chain", 5, 2, 1, "tie"), ("chain", 5, 4, 1, "tie"),
+    ("chain", 5, 3, 4, "tie"), ("chain", 4, 4, 4, "tie"), ("chain", 4, 6, 3, "tie"),
+    ("chain", 6, 3, 2, "inf"), ("chain", 6, 3, 2, "neg"),
+    ("merge", 6, 3, 2, "tie"), ("fork", 6, 3, 2, "tie"), ("fork", 6, 3, 2, "inf"), ("merge", 6, 3, 2, "neg"),
+])
+def test_compose_edges_vs_oracle(nat_loaded, orc, shape, n, r_max, b_max, kind):
+    import torch
+
+    from paper_2511_02248_b200 import _native as nat
+    rng = np.random.default_rng(zlib.crc32(repr((shape, n, r_max, b_max, kind)).encode()))
+    prob = _dag(n, shape)
+    grid = tables.pack_grid(prob, model.AutoscaleParams(slo=1.0),
+                            model.BruteForceBounds(r_max=r_max, b_max=b_max, parallelism=(1, 2)))
+    slos = [1.0, 0.7, 0.3 + 1e-13, 2.5, 1.0, 0.9999999999999999]
+    if kind == "inf":
+        slos = [np.inf, np.inf, 1.0, np.inf]
+    W = len(slos)
+    win = tables.window_arrays(np.full(W, 10.0), np.full(W, 512), 0, 1.0)
+    win.slo[:] = slos
+    mw = _menus(rng, prob, grid, slos, kind if shape == "chain" else ("short" if kind == "tie" else kind))
+
+    want = orc.compose(prob, grid, win, mw)
+    dev = torch.device("cuda:0")
+    t = {k: torch.from_numpy(np.ascontiguousarray(getattr(win, k))).to(dev)
+         for k in ("qps", "seq_len", "phase", "slo", "eps")}
+    dw = abi.OpscWindows()
+    dw.n = W
+    for k in t:
+        setattr(dw, k, t[k].data_ptr())
+    mwd = torch.from_numpy(mw).to(dev)
+    key = torch.full((W,), abi.KEY_INFEASIBLE, dtype=torch.int64, device=dev)
+    s = torch.cuda.current_stream().cuda_stream
+    L = nat.load()
+    nat.check(L.opsc_compose_argmin(nat.ref(prob.table), nat.ref(grid), dw, mwd.data_ptr(), 0, 1,
+                                    key.data_ptr(), s), "compose")
+    got = key.cpu().numpy()
+    assert (got == want).all(), (shape, kind, got, want)
+    if kind == "inf":
+        assert (got != abi.KEY_INFEASIBLE).any()

@@ -45,12 +45,12 @@ def _golden(nat, c, mode):
 
 
 def test_golden_oracle_cases(nat):
-    for c in G.load("oracle.json"):
+    for c in G.load("oracle.json") + G.load("edges_oracle.json"):
         _golden(nat, c, abi.MODE_ORACLE)
 
 
 def test_golden_model_cases(nat):
-    for c in G.load("model.json"):
+    for c in G.load("model.json") + G.load("edges_model.json"):
         _golden(nat, c, abi.MODE_MODEL)
 
 
@@ -225,7 +225,7 @@ def test_golden_greedy_cases(nat):
     """greedy_autoscale (operator mode) on the device == the reference's plans,
     move traces and metrics, bit for bit."""
     errs = []
-    for c in G.load("greedy.json"):
+    for c in G.load("greedy.json") + G.load("edges_greedy.json"):
         prob = G.case_problem(c)
         params = G.case_params(c)
         place = tables.pack_place(G.fleet_for("model_metrics"), model.EnergyParams())

@@ -1,5 +1,8 @@
 """Quick device timing of the cfg5 pipeline (dev tool)."""
+import os
+import sys
 import time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 from paper_2511_02248_b200 import _native, abi, model, scenarios, tables
