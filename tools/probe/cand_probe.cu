@@ -85,6 +85,24 @@ __global__ void __launch_bounds__(256, 4) probe(int iters, double seed, double* 
         if (i & 1) acc1 += t; else acc0 += t;
       }
       inner = (int)(acc0 + acc1);
+    } else if (KIND == 10) {
+      // DSETP only, predicates AND-chained (DSETP.LE.AND P, ..., P)
+      bool ok = true;
+#pragma unroll
+      for (int i = 0; i < 24; ++i) ok = ok & (wj[i] <= bj);
+      inner = ok;
+    } else if (KIND == 11) {
+      // DADD + DSETP, predicates AND-chained (no select)
+      bool ok = true;
+#pragma unroll
+      for (int i = 0; i < 24; ++i) ok = ok & (bj + wj[i] <= slo);
+      inner = ok;
+    } else if (KIND == 12) {
+      // DADD only: hi words OR-ed (DADD + LOP3 per candidate)
+      uint32_t m = 0;
+#pragma unroll
+      for (int i = 0; i < 24; i += 2) m |= (uint32_t)__double2hiint(bj + wj[i]) ^ (uint32_t)__double2hiint(bj + wj[i + 1]);
+      inner = (int)m;
     } else {
       uint32_t m = 0;
 #pragma unroll
@@ -125,10 +143,11 @@ int main() {
   const int blocks = sms * 4 * 8;
   const int iters = 20000;
   const double cands = (double)blocks * 256 * iters * 24;
-  float t[10];
+  float t[13];
   t[1] = run<1>(iters, sink, blocks); t[2] = run<2>(iters, sink, blocks); t[3] = run<3>(iters, sink, blocks);
   t[4] = run<4>(iters, sink, blocks); t[5] = run<5>(iters, sink, blocks); t[6] = run<6>(iters, sink, blocks);
   t[7] = run<7>(iters, sink, blocks); t[8] = run<8>(iters, sink, blocks); t[9] = run<9>(iters, sink, blocks);
-  for (int k = 1; k <= 9; ++k) printf("kind%d %.3e cand/s\n", k, cands / t[k] * 1e3);
+  t[10] = run<10>(iters, sink, blocks); t[11] = run<11>(iters, sink, blocks); t[12] = run<12>(iters, sink, blocks);
+  for (int k = 1; k <= 12; ++k) printf("kind%d %.3e cand/s\n", k, cands / t[k] * 1e3);
   return 0;
 }
