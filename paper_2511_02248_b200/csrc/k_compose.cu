@@ -258,6 +258,81 @@ __device__ __forceinline__ unsigned long long k_level_smem(const ComposeSmem& s,
   return mbest;
 }
 
+// CTA minimum -> one atomicMin per CTA into this GPU's key (or, for the
+// fused multi-GPU merge, into EVERY rank's key buffer over NVLink peer memory).
+__device__ __forceinline__ void cta_min_commit(unsigned long long best, int w, unsigned long long* key_out,
+                                               const PeerKeys& peers, unsigned long long* warp_best) {
+  best = warp_min_u64(best);
+  if ((threadIdx.x & 31) == 0) warp_best[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    unsigned long long b = threadIdx.x < kComposeThreads / 32 ? warp_best[threadIdx.x] : kSentinel;
+    b = warp_min_u64(b);
+    if (threadIdx.x == 0 && b < kSentinel) {
+      if (peers.n == 0) {
+        atomicMin(&key_out[w], b);
+      } else {
+        for (int p = 0; p < peers.n; ++p) atomicMin(peers.p[p] + w, b);
+        __threadfence_system();
+      }
+    }
+  }
+}
+
+// Large-menu path (menus that do not fit the shared-memory tile, or a menu
+// over 65535 entries): one thread per candidate index of the window's
+// lexicographic space, weights read from the global menu slab (L1/L2
+// resident), the same critical-path DP (max over predecessors, then + own
+// weight, topological order) and the same key. Literal and exact, slower per
+// candidate; only reachable with few operators (the reference's 1e7 guard).
+__global__ void __launch_bounds__(kComposeThreads)
+compose_flat_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ OpscGrid g,
+                    const double* __restrict__ menu_w, const double* __restrict__ slo_w,
+                    const double* __restrict__ qps_w, unsigned long long* __restrict__ key_out,
+                    const __grid_constant__ PeerKeys peers) {
+  __shared__ unsigned long long warp_best[kComposeThreads / 32];
+  const int w = blockIdx.x / c.blocks_per_window;
+  const int bw = blockIdx.x - w * c.blocks_per_window;
+  const double slo = fmin(slo_w[w], 1.7976931348623157e308);
+  const double* mw = menu_w + (size_t)w * c.E;
+  unsigned long long best = kSentinel;
+  if (qps_w[w] > 0.0) {
+    const unsigned long long step = (unsigned long long)c.blocks_per_window * kComposeThreads;
+    for (unsigned long long idx = c.flo + (unsigned long long)bw * kComposeThreads + threadIdx.x; idx < c.fhi;
+         idx += step) {
+      int dig[OPSC_CMAX];
+      unsigned long long rem = idx;
+      for (int pos = c.n - 1; pos >= 0; --pos) {
+        const unsigned long long mm = (unsigned long long)c.m[pos];
+        const unsigned long long q = rem / mm;
+        dig[pos] = (int)(rem - q * mm);
+        rem = q;
+      }
+      double val[OPSC_CMAX];
+      long long cost = 0;
+      unsigned long long lex = 0;
+      double lat = 0.0;
+      for (int pos = 0; pos < c.n; ++pos) {
+        double wt = 0.0;
+        if (c.vop[pos] >= 0) {
+          wt = mw[c.off[pos] + dig[pos]];
+          int p, r, b;
+          entry_prb(g, c.vop[pos], dig[pos], p, r, b);
+          cost += p * r;
+          lex += (unsigned long long)dig[pos] * c.stride[pos];
+        }
+        val[pos] = dp_in(c.pmask[pos], val) + wt;
+        if (c.sinkmask >> pos & 1u) lat = fmax(lat, val[pos]);
+      }
+      if (lat <= slo) {
+        const unsigned long long key = ((unsigned long long)cost << OPSC_KEY_LEX_BITS) + lex;
+        best = key < best ? key : best;
+      }
+    }
+  }
+  cta_min_commit(best, w, key_out, peers, warp_best);
+}
+
 template <int NJ, bool CHAIN>
 __global__ void __launch_bounds__(kComposeThreads, OPSC_COMPOSE_MINB)
 compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ OpscGrid g,
@@ -465,23 +540,13 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
       }
     }
   }
-  best = warp_min_u64(best);
-  if ((threadIdx.x & 31) == 0) warp_best[threadIdx.x >> 5] = best;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    unsigned long long b = threadIdx.x < kComposeThreads / 32 ? warp_best[threadIdx.x] : kSentinel;
-    b = warp_min_u64(b);
-    if (threadIdx.x == 0 && b < kSentinel) {
-      if (peers.n == 0) {
-        atomicMin(&key_out[w], b);
-      } else {
-        // fused multi-GPU merge: the CTA's minimum straight into every
-        // rank's key buffer over NVLink (IPC-mapped peer memory)
-        for (int p = 0; p < peers.n; ++p) atomicMin(peers.p[p] + w, b);
-        __threadfence_system();
-      }
-    }
-  }
+  cta_min_commit(best, w, key_out, peers, warp_best);
+}
+
+// Dynamic shared memory of the tile kernel: menu slab + costs, k / j tables.
+static size_t compose_smem_bytes(int E, int mk, int mj) {
+  return (size_t)mk * 8 + (size_t)(mj + 1) * 8 + (size_t)(E + 1) * 8 + (size_t)mj * 8 + (size_t)(E + 1) * 4 +
+         (size_t)mk * 4 + (size_t)(mj + 1) * 4;
 }
 
 // Host: topological positions, lexicographic strides, level split.
@@ -500,7 +565,7 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
   unsigned long long s = 1;
   for (int v = nr - 1; v >= 0; --v) {
     const int m = g.menu_off[v + 1] - g.menu_off[v];
-    if (m < 1 || m > 65535) return OPSC_ERR_ARG;
+    if (m < 1) return OPSC_ERR_ARG;
     lexstride[v] = s;
     s *= (unsigned long long)m;
     space *= (double)m;
@@ -512,9 +577,11 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
     if (pos < nvirt) {
       c.m[pos] = 1;
       c.off[pos] = c.E;
+      c.vop[pos] = -1;
       continue;
     }
     const int v = d.topo[pos - nvirt];
+    c.vop[pos] = v;
     c.m[pos] = g.menu_off[v + 1] - g.menu_off[v];
     c.off[pos] = g.menu_off[v];
     c.stride[pos] = lexstride[v];
@@ -532,6 +599,28 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
     max_obj += (long long)pmax * g.r_max;
   }
   if (max_obj >= (1 << 17)) return OPSC_ERR_ARG;
+  // Large menus: the shared-memory tile needs every window's menu slab plus
+  // the k / j tables on chip; past ~200 KB (or a menu over 65535 entries)
+  // the flat kernel runs instead.
+  {
+    const size_t mj = (size_t)c.m[c.n - 1], mk = (size_t)c.m[c.n - 2];
+    const size_t need = compose_smem_bytes(c.E, (int)mk, (int)mj);
+    int big = 0;
+    for (int pos = 0; pos < c.n; ++pos) big |= c.m[pos] > 65535;
+    if (big || need > 200 * 1024) {
+      c.flat = 1;
+      c.flo = s * (unsigned long long)shard / (unsigned long long)n_shards;
+      c.fhi = s * (unsigned long long)(shard + 1) / (unsigned long long)n_shards;
+      const unsigned long long per_cta = (unsigned long long)kComposeThreads * 64ull;
+      unsigned long long bpw = (c.fhi - c.flo + per_cta - 1) / per_cta;
+      const unsigned long long cap = (unsigned long long)(148 * 8 * 4) / (unsigned long long)(n_windows > 0 ? n_windows : 1) + 1;
+      bpw = bpw < 1 ? 1 : bpw;
+      bpw = bpw > cap ? cap : bpw;
+      c.blocks_per_window = (int)bpw;
+      *cfg = c;
+      return OPSC_OK;
+    }
+  }
   // level split: enough in-thread candidates to amortise the outer decode,
   // while keeping at least half a wave of threads
   auto prod = [&](int lo, int hi) {
@@ -585,8 +674,7 @@ static cudaError_t launch_t(const ComposeCfg& c, const OpscGrid& g, int n_window
                             const double* slo, const double* qps, unsigned long long* key, cudaStream_t s,
                             const PeerKeys& pk) {
   const int mj = c.m[c.n - 1], mk = c.m[c.n - 2];
-  const size_t smem = (size_t)mk * 8 + (size_t)(mj + 1) * 8 + (size_t)(c.E + 1) * 8 + (size_t)mj * 8 +
-                      (size_t)(c.E + 1) * 4 + (size_t)mk * 4 + (size_t)(mj + 1) * 4;
+  const size_t smem = compose_smem_bytes(c.E, mk, mj);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(compose_kernel<NJ, CHAIN>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -609,10 +697,17 @@ static cudaError_t launch_nj(const ComposeCfg& c, const OpscGrid& g, int n_windo
 cudaError_t launch_compose(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,
                            const double* slo, const double* qps, unsigned long long* key, cudaStream_t s,
                            const PeerKeys* peers) {
-  if (n_windows <= 0 || c.hi <= c.lo) return cudaSuccess;
+  if (n_windows <= 0 || (!c.flat && c.hi <= c.lo)) return cudaSuccess;
   PeerKeys pk;
   memset(&pk, 0, sizeof(pk));
   if (peers) pk = *peers;
+  if (c.flat) {
+    if (c.fhi <= c.flo) return cudaSuccess;
+    const long long blocks = (long long)n_windows * c.blocks_per_window;
+    if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    compose_flat_kernel<<<(unsigned)blocks, kComposeThreads, 0, s>>>(c, g, menu_w, slo, qps, key, pk);
+    return cudaGetLastError();
+  }
   switch (c.nj) {
     case 4: return launch_nj<4>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
     case 8: return launch_nj<8>(c, g, n_windows, menu_w, slo, qps, key, s, pk);

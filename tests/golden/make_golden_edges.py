@@ -28,6 +28,20 @@ def oracle_cases():
     cases.append(dict(name="edge/slo_inf/cfg1/decode", scenario="cfg1",
                       point=dict(qps=60.0, seq_len=2048, phase="decode"), params=dict(slo=INF),
                       bounds=dict(r_max=2, b_max=3, parallelism=[1, 2])))
+    # menus too large for the shared-memory tile (the flat compose kernel):
+    # one operator with a 65536-entry menu, two operators with 8192 x 16
+    one = {"nodes": [{"id": "solo", "kind": "linear", "layer_count": 32, "profile_ref": "mlp"}],
+           "edges": []}
+    c7, p7 = M.S.SCENARIOS["cfg1"]
+    cases.append(dict(name="edge/large_menu/single_op_65536", dag=one, profiles=p7,
+                      point=dict(qps=300.0, seq_len=2048, phase="prefill"), params=dict(slo=0.05),
+                      bounds=dict(r_max=512, b_max=32, parallelism=[1, 2, 4, 8])))
+    two = {"nodes": [{"id": "b2", "kind": "linear", "layer_count": 32, "profile_ref": "mlp"},
+                     {"id": "a1", "kind": "attention", "layer_count": 32, "profile_ref": "attn"}],
+           "edges": [{"src": "b2", "dst": "a1", "volume_ref": "mlp"}]}
+    cases.append(dict(name="edge/large_menu/two_op", dag=two, profiles=p7,
+                      point=dict(qps=120.0, seq_len=2048, phase="prefill"), params=dict(slo=0.3),
+                      bounds=dict(r_max=256, b_max=16, parallelism=[1, 2])))
     cases.append(dict(name="edge/slo_inf/nostable_bounds", scenario="cfg1",
                       point=dict(qps=40.0, seq_len=4096, phase="prefill"), params=dict(slo=INF),
                       bounds=dict(r_max=1, b_max=1, parallelism=[1])))

@@ -10,7 +10,8 @@ oracle's literal enumeration on the SAME menu weights:
   (autoscaler.py:800-801);
 * a menu with negative weights (the kernel's exact-scan path);
 * chain (CHAIN kernel) and merge / fork DAGs (generic kernel), j menus from
-  4 to 32 entries (every NJ specialisation) and > 32 (smem loop).
+  4 to 32 entries (every NJ specialisation) and > 32 (smem loop);
+* menus too large for the shared-memory tile (the flat kernel), sharded.
 """
 
 import zlib
@@ -113,3 +114,43 @@ def test_compose_edges_vs_oracle(nat_loaded, orc, shape, n, r_max, b_max, kind):
     assert (got == want).all(), (shape, kind, got, want)
     if kind == "inf":
         assert (got != abi.KEY_INFEASIBLE).any()
+
+
+def _device_compose(nat, prob, grid, win, mw, shard=0, n_shards=1):
+    import torch
+    dev = torch.device("cuda:0")
+    t = {k: torch.from_numpy(np.ascontiguousarray(getattr(win, k))).to(dev)
+         for k in ("qps", "seq_len", "phase", "slo", "eps")}
+    dw = abi.OpscWindows()
+    dw.n = win.n
+    for k in t:
+        setattr(dw, k, t[k].data_ptr())
+    mwd = torch.from_numpy(np.ascontiguousarray(mw)).to(dev)
+    key = torch.full((win.n,), abi.KEY_INFEASIBLE, dtype=torch.int64, device=dev)
+    L = nat.load()
+    nat.check(L.opsc_compose_argmin(nat.ref(prob.table), nat.ref(grid), dw, mwd.data_ptr(), shard, n_shards,
+                                    key.data_ptr(), torch.cuda.current_stream().cuda_stream), "compose")
+    return key.cpu().numpy()
+
+
+@pytest.mark.parametrize("shape,r_max,b_max", [("chain", 512, 20), ("fork", 128, 10)])
+def test_flat_kernel_large_menus(nat_loaded, orc, shape, r_max, b_max):
+    """Two 20480-entry menus (past the shared-memory tile: the flat kernel)
+    and three 2560-entry menus (the tile's shared-memory j loop)."""
+    from paper_2511_02248_b200 import _native as nat
+    n = 2 if shape == "chain" else 3
+    rng = np.random.default_rng(r_max + b_max)
+    prob = _dag(n, shape)
+    grid = tables.pack_grid(prob, model.AutoscaleParams(slo=1.0),
+                            model.BruteForceBounds(r_max=r_max, b_max=b_max, parallelism=(1, 2)))
+    slos = [1.0, 0.7, np.inf, 0.3]
+    W = len(slos)
+    win = tables.window_arrays(np.full(W, 10.0), np.full(W, 512), 0, 1.0)
+    win.slo[:] = slos
+    mw = _menus(rng, prob, grid, slos, "inf" if shape == "chain" else "short")
+    want = orc.compose(prob, grid, win, mw)
+    got = _device_compose(nat, prob, grid, win, mw)
+    assert (got == want).all(), (got, want)
+    merged = np.minimum.reduce([_device_compose(nat, prob, grid, win, mw, sh, 3) for sh in range(3)])
+    assert (merged == want).all()
+    assert (got != abi.KEY_INFEASIBLE).any()

@@ -171,11 +171,12 @@ def test_greedy_decisions(orc, idx):
     _check_greedy(orc, G.load("greedy.json")[idx])
 
 
-# slo = +inf (tests/golden/make_golden_edges.py): unstable (INF-weighted)
-# entries must stay out of the feasible set in every mode
+# tests/golden/make_golden_edges.py: slo = +inf (unstable, INF-weighted
+# entries must stay out of the feasible set in every mode) and brute-force
+# menus too large for the GPU's shared-memory tile
 @pytest.mark.parametrize("fname,mode", [("edges_oracle.json", abi.MODE_ORACLE), ("edges_model.json", abi.MODE_MODEL),
                                         ("edges_greedy.json", abi.MODE_OPERATOR)])
-def test_slo_inf_decisions(orc, fname, mode):
+def test_edge_decisions(orc, fname, mode):
     for c in G.load(fname):
         if mode == abi.MODE_OPERATOR:
             _check_greedy(orc, c)
