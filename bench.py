@@ -362,7 +362,11 @@ def ours(args):
                        "mode": "oracle (exhaustive brute force, every candidate composed)",
                        "parallelism": f"candidate-range shards x{world}" if world > 1 else "single GPU",
                        "merge": merge_kind,
-                       "l2": "flushed between timed steps (256 MiB write outside the events)"},
+                       "l2": "flushed between timed steps (256 MiB write outside the events)",
+                       "workload_choice": "BASELINE config 5 is the throughput config (the 1e8-candidate x "
+                                          "1440-window sweep sharded over 1/2/4/8 GPUs); config 2 (70B, 1 h "
+                                          "trace, per-minute windows) is the decision-latency config: "
+                                          "decision_latency_ms, incl. its batched candidates/s"},
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "kernel": "compose_kernel (opsc_compose_argmin)",
@@ -453,6 +457,11 @@ def decision_latency(dev):
                      "eager_median": statistics.median(eager),
                      "eager_p99": eager[min(len(eager) - 1, int(0.99 * len(eager)))],
                      "batched_ms_per_window": batch_ms / max(1, len(samples))}
+        if mode == abi.MODE_ORACLE:  # cfg2 throughput: whole trace per launch set, 6^10 candidates per window
+            cpw = 1
+            for v in range(problem.n_ops):
+                cpw *= grid.menu_off[v + 1] - grid.menu_off[v]
+            out[name]["batched_candidates_per_s"] = cpw / (out[name]["batched_ms_per_window"] * 1e-3)
     out["dag"] = "cfg2 Llama-2-70B 10-op chain, 60 x 60 s windows x {prefill, decode}, W = 1"
     return out
 

@@ -112,11 +112,19 @@ struct OpscContext {
 
 namespace {
 
+// (Re)allocate a context buffer, zero-filled: fields a kernel leaves
+// undefined (trace entries past trace_len, devices past devices_used) read as
+// 0, never as uninitialised memory (compute-sanitizer initcheck). Growth
+// happens on a context's first calls only.
 template <class T>
 cudaError_t regrow(T*& p, size_t n) {
   if (p) cudaFree(p);
   p = nullptr;
-  return cudaMalloc((void**)&p, n * sizeof(T) > 0 ? n * sizeof(T) : sizeof(T));
+  const size_t bytes = n * sizeof(T) > 0 ? n * sizeof(T) : sizeof(T);
+  cudaError_t e = cudaMalloc((void**)&p, bytes);
+  if (e == cudaSuccess) e = cudaMemset(p, 0, bytes);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+  return e;
 }
 
 int ensure(OpscContext* c, size_t W, size_t E, size_t n, size_t ndev, size_t trace_cap = 0) {

@@ -350,9 +350,14 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
       __shared__ int s_best;
       __shared__ double s_best_score;
       if (threadIdx.x == 0) s_best = -1;
-      // default-stream placement never shares: straight to take_unused
-      for (int c0 = 0; probe && c0 < S.used; c0 += kMaxDevProbe) {
-      const int U = min(S.used - c0, kMaxDevProbe);
+      // default-stream placement never shares: straight to take_unused.
+      // The device count is read once: thread 0 bumps S.used right after the
+      // loop, while other threads may still be evaluating its exit condition
+      // (compute-sanitizer racecheck; a fleet with a multiple of kMaxDevProbe
+      // used devices would otherwise split the CTA across __syncthreads).
+      const int n_used = S.used;
+      for (int c0 = 0; probe && c0 < n_used; c0 += kMaxDevProbe) {
+      const int U = min(n_used - c0, kMaxDevProbe);
       // stage 1: per-device admission + tentative group totals
       for (int dj = threadIdx.x; dj < U; dj += blockDim.x) {
         const int dev = c0 + dj;
