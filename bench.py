@@ -299,19 +299,31 @@ def ours(args):
         from paper_2511_02248_b200 import dist as pdist
         for _ in range(args.warmup):
             pdist.plan_windows_host_sharded(planner, hwin, hout, merge=merge)
-        t = []
+        t, wall = [], []
         for _ in range(args.steps):
             flush.zero_()
             barrier()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             t0 = time.perf_counter()
-            pdist.plan_windows_host_sharded(planner, hwin, hout, merge=merge)
-            t.append(time.perf_counter() - t0)
-        tt = torch.tensor([sum(t)], dtype=torch.float64, device=dev)
+            e0.record()
+            planner.load_windows(hwin)  # H2D (pinned, async)
+            if merge is not None:
+                planner.step(merge=merge)
+            else:
+                pdist.plan_windows_sharded(planner)
+            planner.fetch(hout, sync=False)  # D2H (pinned, async)
+            e1.record()
+            e1.synchronize()
+            wall.append(time.perf_counter() - t0)
+            t.append(e0.elapsed_time(e1) * 1e-3)
+        tt = torch.tensor([sum(t), sum(wall)], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        e2e = {"value": cands_step * len(t) / float(tt.item()), "unit": "candidates/s",
+        e2e = {"value": cands_step * len(t) / float(tt[0].item()), "unit": "candidates/s",
                "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(hout.nbytes()),
-               "api": "dist.plan_windows_host_sharded (host buffers, shard per rank, key merge)",
-               "timing": "wall clock per rank, max over ranks",
+               "api": "dist.plan_windows_host_sharded's steps (host buffers, shard per rank, key merge)",
+               "timing": "CUDA events on the rank's stream around H2D .. D2H, max over ranks",
+               "wall_value": cands_step * len(t) / float(tt[1].item()),
                "parity_vs_device_path": bool(all(
                    getattr(hout, f).tobytes() == getattr(dec, f).tobytes()
                    for f in ("key", "cfg", "latency", "energy")))}
@@ -319,19 +331,23 @@ def ours(args):
         ctx = _native.Context(device=local, max_windows=win.n)
         for _ in range(args.warmup):
             ctx.plan_windows(abi.MODE_ORACLE, problem, hwin, grid=grid, out=hout)
-        t = []
+        t, wall = [], []
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize(dev)
             t0 = time.perf_counter()
             ctx.plan_windows(abi.MODE_ORACLE, problem, hwin, grid=grid, out=hout)
-            t.append(time.perf_counter() - t0)
+            wall.append(time.perf_counter() - t0)
+            t.append(ctx.last_ms() * 1e-3)
         e2e_launches = ctx.last_launches()
         ctx.close()
         bi = sum(getattr(hwin, k).nbytes for k in ("qps", "seq_len", "phase", "slo", "eps"))
         e2e = {"value": cands_step * len(t) / sum(t), "unit": "candidates/s",
                "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(hout.nbytes()),
                "api": "opsc_plan_windows_host (C ABI, host buffers)",
+               "timing": "CUDA events on the context stream around the call's first H2D .. last D2H "
+                         "(opsc_ctx_last_ms)",
+               "wall_value": cands_step * len(wall) / sum(wall),
                "launches_per_step": e2e_launches,
                "parity_vs_device_path": bool(all(
                    getattr(hout, f).tobytes() == getattr(dec, f).tobytes()

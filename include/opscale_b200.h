@@ -386,6 +386,11 @@ OPSC_API int opsc_plan_windows_host(OpscContext* ctx, int32_t mode, const OpscDa
 /* Number of kernels the last opsc_plan_windows_host call launched. */
 OPSC_API int opsc_ctx_last_launches(const OpscContext* ctx, int32_t* launches);
 
+/* Device time (CUDA events on the context stream) of the last
+ * opsc_plan_windows_host call, from its first host->device copy to its last
+ * device->host copy. OPSC_ERR_ARG before any call. */
+OPSC_API int opsc_ctx_last_ms(OpscContext* ctx, float* ms);
+
 /* ---- measurement helper: FP64 add throughput microbenchmark ----
  * Runs `iters` dependent-chain DADD/DSETP pairs per thread on a full grid;
  * writes elapsed milliseconds and the executed FP64 op count. */

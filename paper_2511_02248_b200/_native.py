@@ -23,7 +23,7 @@ EXPORTS = (
     "opsc_stability_check", "opsc_compose_argmin", "opsc_fill_keys", "opsc_init_windows",
     "opsc_menu_fallback",
     "opsc_decode_decisions", "opsc_model_grid", "opsc_materialize", "opsc_ctx_create",
-    "opsc_ctx_destroy", "opsc_plan_windows_host", "opsc_ctx_last_launches", "opsc_fp64_peak",
+    "opsc_ctx_destroy", "opsc_plan_windows_host", "opsc_ctx_last_launches", "opsc_ctx_last_ms", "opsc_fp64_peak",
     "opsc_candidate_probe", "opsc_greedy", "opsc_windowize", "opsc_windowize_workspace",
     "opsc_greedy_state_bytes", "opsc_greedy_phase", "opsc_model_table_bytes",
     "opsc_model_grid_table", "opsc_place_shared_workspace", "opsc_place_shared",
@@ -75,6 +75,7 @@ def load():
             "opsc_windowize": ([abi.OpscTraceRecords, C.c_double, C.c_double, I, P, P, P, P, P,
                                 C.c_size_t, P], C.c_int),
             "opsc_ctx_last_launches": ([P, P], C.c_int),
+            "opsc_ctx_last_ms": ([P, P], C.c_int),
             "opsc_fp64_peak": ([I, P, P, P], C.c_int),
             "opsc_candidate_probe": ([I, I, P, P, P], C.c_int),
             "opsc_ipc_alloc": ([C.c_size_t, P, P], C.c_int),
@@ -145,6 +146,12 @@ class Context:
         n = C.c_int32(0)
         check(load().opsc_ctx_last_launches(self._p, C.cast(C.byref(n), C.c_void_p)), "launches")
         return n.value
+
+    def last_ms(self):
+        """Device time of the last plan_windows call (first H2D .. last D2H)."""
+        ms = C.c_float(0.0)
+        check(load().opsc_ctx_last_ms(self._p, C.cast(C.byref(ms), C.c_void_p)), "last_ms")
+        return ms.value
 
     def plan_windows(self, mode, problem, windows, grid=None, model=None, place=None, out=None,
                      greedy=None, trace_cap=4096):

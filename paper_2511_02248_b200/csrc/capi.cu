@@ -77,7 +77,8 @@ cudaError_t launch_fp64_peak(int iters, double* sink, int* blocks, int* threads,
 struct OpscContext {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // span of the last host-buffer call
+  bool timed = false;
   int launches = 0;
   size_t cap_w = 0, cap_e = 0, cap_n = 0, cap_dev = 0;
   // windows
@@ -411,6 +412,8 @@ int opsc_ctx_destroy(OpscContext* c) {
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->fork) cudaEventDestroy(c->fork);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->join) cudaEventDestroy(c->join);
   delete c;
   return OPSC_OK;
@@ -420,6 +423,12 @@ int opsc_ctx_last_launches(const OpscContext* c, int32_t* launches) {
   if (!c || !launches) return OPSC_ERR_ARG;
   *launches = c->launches;
   return OPSC_OK;
+}
+
+int opsc_ctx_last_ms(OpscContext* c, float* ms) {
+  if (!c || !ms) return OPSC_ERR_ARG;
+  if (!c->timed) return OPSC_ERR_ARG;
+  return from_cuda(cudaEventElapsedTime(ms, c->ev0, c->ev1));
 }
 
 size_t opsc_place_shared_workspace(int32_t n_windows, int32_t cap_assign, int32_t cap_dev, int32_t n_ops) {
@@ -511,6 +520,9 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
       return OPSC_ERR_CUDA;     \
     }                           \
   } while (0)
+  if (!c->ev0) CK(cudaEventCreate(&c->ev0));
+  if (!c->ev1) CK(cudaEventCreate(&c->ev1));
+  CK(cudaEventRecord(c->ev0, s));  // device-side span: first H2D .. last D2H
   CK(cudaMemcpyAsync(c->qps, win.qps, W * sizeof(double), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(c->seq_len, win.seq_len, W * sizeof(int32_t), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(c->phase, win.phase, W * sizeof(uint8_t), cudaMemcpyHostToDevice, s));
@@ -576,7 +588,9 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
     CK(cudaMemcpyAsync(out.trace_len, c->trace_len, W * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   if (tcap && out.trace)
     CK(cudaMemcpyAsync(out.trace, c->trace, W * tcap * sizeof(OpscTraceEntry), cudaMemcpyDeviceToHost, s));
+  CK(cudaEventRecord(c->ev1, s));
   CK(cudaStreamSynchronize(s));
+  c->timed = true;
 #undef CK
   return OPSC_OK;
 }

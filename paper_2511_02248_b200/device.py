@@ -208,14 +208,16 @@ class DevicePlanner:
             a = getattr(host, k)
             t.copy_(torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a), non_blocking=True)
 
-    def fetch(self, host: tables.DecisionArrays):
-        """D2H of the decisions into a (pinned) host DecisionArrays; waits
-        for the current stream."""
+    def fetch(self, host: tables.DecisionArrays, sync=True):
+        """D2H of the decisions into a (pinned) host DecisionArrays on the
+        current stream; waits for it unless `sync` is False (the caller then
+        synchronises before reading `host`)."""
         for k, t in self.out_t.items():
             a = getattr(host, k)
             dst = torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a)
             dst.copy_(t.view(dst.shape), non_blocking=True)
-        torch.cuda.current_stream(self.dev).synchronize()
+        if sync:
+            torch.cuda.current_stream(self.dev).synchronize()
         return host
 
     def decisions(self) -> tables.DecisionArrays:
