@@ -32,8 +32,10 @@ def case_problem(c):
 
 def case_params(c):
     p = c["params"]
+    par = p["parallelism"]
+    par = {k: tuple(v) for k, v in par.items()} if isinstance(par, dict) else tuple(par)
     return model.AutoscaleParams(slo=F(p["slo"]), epsilon=F(p["epsilon"]), b_max=p["b_max"],
-                                 parallelism=tuple(p["parallelism"]), r_cap=p["r_cap"],
+                                 parallelism=par, r_cap=p["r_cap"],
                                  max_iterations=p.get("max_iterations", 10_000),
                                  prune_excess_replicas=p.get("prune_excess_replicas", False))
 
@@ -41,7 +43,7 @@ def case_params(c):
 def case_bounds(c):
     b = c["bounds"]
     return model.BruteForceBounds(r_max=b["r_max"], b_max=b["b_max"],
-                                  parallelism=tuple(b["parallelism"]))
+                                  parallelism=None if b["parallelism"] is None else tuple(b["parallelism"]))
 
 
 def case_point(c):
