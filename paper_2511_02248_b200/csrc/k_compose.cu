@@ -647,7 +647,9 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
   c.blocks_per_window = (int)((c.hi - c.lo + kComposeThreads - 1) / kComposeThreads);
   if (c.blocks_per_window < 1) c.blocks_per_window = 1;
   const int mj = c.m[c.n - 1], mk = c.m[c.n - 2];
-  c.nj = mj <= 4 ? 4 : mj <= 8 ? 8 : mj <= 12 ? 12 : mj <= 16 ? 16 : mj <= 24 ? 24 : mj <= 32 ? 32 : 0;
+  // register tile widths (padded entries are +inf and still cost their
+  // DADD/DSETP/SEL, so common menu sizes get exact tiles: 6 = P{1,2} x R<=3)
+  c.nj = mj <= 4 ? 4 : mj <= 6 ? 6 : mj <= 8 ? 8 : mj <= 12 ? 12 : mj <= 16 ? 16 : mj <= 24 ? 24 : mj <= 32 ? 32 : 0;
   c.kj_major = c.stride[c.n - 2] > c.stride[c.n - 1] ? 1 : 0;
   // register-tile local keys: (k, j) index < 2^20 and cost_k + cost_j < 2^11
   auto max_cost = [&](int pos) {
@@ -710,6 +712,7 @@ cudaError_t launch_compose(const ComposeCfg& c, const OpscGrid& g, int n_windows
   }
   switch (c.nj) {
     case 4: return launch_nj<4>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
+    case 6: return launch_nj<6>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
     case 8: return launch_nj<8>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
     case 12: return launch_nj<12>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
     case 16: return launch_nj<16>(c, g, n_windows, menu_w, slo, qps, key, s, pk);

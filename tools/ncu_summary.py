@@ -41,6 +41,17 @@ def launches(path, out):
     for k, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         lines.append(f"| `{k}` | {c} | {t:.3f} | {t / total:.1%} |")
     lines.append(f"\n{n} launches, {total:.3f} ms total (ncu-serialised, cold cache).")
+    # the bench step's own kernels: everything but the live FP64-peak
+    # microbenchmark (a measurement helper) and torch fill kernels (L2 flush,
+    # buffer resets outside the timed region)
+    step = {k: v for k, v in agg.items() if k.startswith(("opsc::", "void opsc::")) and "peak" not in k}
+    st = sum(v[1] for v in step.values())
+    if st > 0:
+        lines.append("\nShare of the planning step (opsc kernels only):\n")
+        lines.append("| kernel | share of step |")
+        lines.append("|---|---|")
+        for k, (c, t) in sorted(step.items(), key=lambda kv: -kv[1][1]):
+            lines.append(f"| `{k}` | {t / st:.2%} |")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
