@@ -164,7 +164,7 @@ __device__ void eval_full(GShared& S, const OpscDag& d, double qps, int L, int p
   __syncthreads();
   for (int v = threadIdx.x; v < d.n_ops; v += blockDim.x) {
     uint32_t st = 0;
-    const Pred o = predict(d, qps, L, ph, v, S.p[v], S.r[v], S.b[v], &st);
+    const Pred o = predict<true>(d, qps, L, ph, v, S.p[v], S.r[v], S.b[v], &st);
     S.soj[v] = o.wait + o.service;
     S.wt[v] = weight(o, d.layer_count[v]);
     if (!o.stable) atomicOr(&s_unstable, 1);
@@ -193,7 +193,7 @@ __device__ int eval_moves(GShared& S, const GreedyArgs& a, int op, int r_new, in
   for (int m = threadIdx.x; m < M; m += blockDim.x) {
     const int b = b_lo + m / np, p = S.pd[op][m % np];
     uint32_t st = 0;
-    const Pred o = predict(a.d, qps, L, ph, op, p, r_new, b, &st);
+    const Pred o = predict<true>(a.d, qps, L, ph, op, p, r_new, b, &st);
     S.m_ok[m] = o.stable;
     if (o.stable) {
       S.m_wt[m] = weight(o, a.d.layer_count[op]);
@@ -402,7 +402,7 @@ __device__ void prune_pass(GShared& S, const GreedyArgs& a, const OpscDecisions&
     for (int v = threadIdx.x; v < d.n_ops; v += blockDim.x) {
       if (!t_need[v] || S.r[v] <= 1) continue;
       uint32_t st = 0;
-      const Pred o = predict(d, qps, L, ph, v, S.p[v], S.r[v] - 1, S.b[v], &st);
+      const Pred o = predict<true>(d, qps, L, ph, v, S.p[v], S.r[v] - 1, S.b[v], &st);
       if (st) atomicOr(&S.st, st);
       t_ok[v] = o.stable;
       t_wt[v] = weight(o, d.layer_count[v]);
@@ -527,7 +527,8 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
       if (r >= 0) {
         const double util = lam / ((double)r * mu);
         if (util >= 1.0 || util <= 0.0) st |= OPSC_W_UNSTABLE_ROUNDING;
-        S.i_soj[v][b - 1] = expected_wait(lam, mu, r) + t / (double)b;
+        const double service = t / (double)b;  // sojourn key: wait only inside wait + service
+        S.i_soj[v][b - 1] = wait_for_sum(r, lam / ((double)r * mu), (double)r * mu - lam, service) + service;
       }
       if (st) atomicOr(&S.st, st);
     }

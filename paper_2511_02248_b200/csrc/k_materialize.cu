@@ -204,17 +204,23 @@ __global__ void __launch_bounds__(32 * kMatWarps) materialize_kernel(const __gri
     stable = o.stable;
     s_wt[warp][v] = weight(o, d.layer_count[v]);
     s_T[warp][v] = o.t;
-    if (feas) {
-      // request_energy terms under default-stream placement: factors 1,
-      // t_eff = (T * R) / R (placement.py:257), wait re-derived from t_eff
-      const double layers = (double)d.layer_count[v];
-      const double t_eff = (o.t * (double)r) / (double)r;
-      const double mu = 1.0 / (t_eff * layers), lam = qps / (double)b;
-      const double wait = lam < (double)r * mu ? expected_wait(lam, mu, r) : OPSC_INF;
-      const double wl = wait * layers, sl = t_eff * layers;
-      s_e1[warp][v] = ((pl.alpha * (double)p) * (double)r) * (wl + sl);
-      s_e2[warp][v] = pl.beta * sl;
-    }
+  }
+  // request_energy terms under default-stream placement: factors 1,
+  // t_eff = (T * R) / R (placement.py:257), wait re-derived from t_eff -- a
+  // second Erlang-B chain per op, run in lanes n..2n-1 next to the predict
+  // chains of lanes 0..n-1 (in lane v itself when n > 16)
+  const int ev = n <= 16 ? lane - n : lane;
+  if (feas && ev >= 0 && ev < n) {
+    const int v = ev;
+    const int p = c[v * 3], r = c[v * 3 + 1], b = c[v * 3 + 2];
+    const double layers = (double)d.layer_count[v];
+    const double t = op_latency(d, ph, v, b, L, p);
+    const double t_eff = (t * (double)r) / (double)r;
+    const double mu = 1.0 / (t_eff * layers), lam = qps / (double)b;
+    const double wait = lam < (double)r * mu ? expected_wait(lam, mu, r) : OPSC_INF;
+    const double wl = wait * layers, sl = t_eff * layers;
+    s_e1[warp][v] = ((pl.alpha * (double)p) * (double)r) * (wl + sl);
+    s_e2[warp][v] = pl.beta * sl;
   }
   const bool all = __all_sync(0xffffffffu, stable);
   st = __reduce_or_sync(0xffffffffu, st);

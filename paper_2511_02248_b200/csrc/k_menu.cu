@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) menu_build_kernel(const __grid_constant__
   int p, r, b;
   entry_prb(g, v, j - g.menu_off[v], p, r, b);
   uint32_t st = 0;
-  const Pred o = predict(d, qps, win.seq_len[w], win.phase[w], v, p, r, b, &st);
+  const Pred o = predict<true>(d, qps, win.seq_len[w], win.phase[w], v, p, r, b, &st);
   menu_w[idx] = o.stable ? weight(o, d.layer_count[v]) : OPSC_INF;
   if (st) atomicOr(&status[w], st);
 }
@@ -72,13 +72,17 @@ cudaError_t launch_menu_build(const OpscDag& d, const OpscGrid& g, OpscWindows w
   return cudaGetLastError();
 }
 
-// One thread per (window, op): does some (P in params, B <= params.b_max)
-// have a strict-stability replica floor within r_cap?
+// One warp per (window, op): does some (P in params, B <= params.b_max) have
+// a strict-stability replica floor within r_cap? P in ascending order (the
+// reference's init_configs pre-check, autoscaler.py:254-294), all B of one P
+// across the lanes; flags accumulate over every (P, B) visited up to and
+// including the first P with a stable B, as in the sequential scan.
 __global__ void stability_kernel(const __grid_constant__ OpscDag d, const __grid_constant__ OpscGrid g,
                                  const __grid_constant__ OpscWindows win, uint32_t* __restrict__ status) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= win.n * d.n_ops) return;
-  const int w = idx / d.n_ops, v = idx - w * d.n_ops;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= win.n * d.n_ops) return;
+  const int w = gw / d.n_ops, v = gw - w * d.n_ops;
   const double qps = win.qps[w];
   if (!(qps > 0.0)) return;
   const int L = win.seq_len[w], ph = win.phase[w];
@@ -86,7 +90,8 @@ __global__ void stability_kernel(const __grid_constant__ OpscDag d, const __grid
   bool found = false;
   for (int pi = 0; pi < g.params_n_p[v] && !found; ++pi) {
     const int p = g.params_p_vals[v][pi];
-    for (int b = 1; b <= g.params_b_max[v]; ++b) {
+    bool mine = false;
+    for (int b = lane + 1; b <= g.params_b_max[v]; b += 32) {
       const double tl = op_latency(d, ph, v, b, L, p) * (double)d.layer_count[v];
       if (tl == 0.0) st |= OPSC_W_ZERO_DIVISION;
       const double mu = 1.0 / tl, lam = qps / (double)b;
@@ -94,18 +99,20 @@ __global__ void stability_kernel(const __grid_constant__ OpscDag d, const __grid
       if (r < 0) continue;
       const double util = lam / ((double)r * mu);
       if (util >= 1.0 || util <= 0.0) st |= OPSC_W_UNSTABLE_ROUNDING;
-      found = true;
+      mine = true;
     }
+    found = __any_sync(0xffffffffu, mine);
   }
+  st = __reduce_or_sync(0xffffffffu, st);
   if (!found) st |= OPSC_W_NO_STABLE_PARAMS;
-  if (st) atomicOr(&status[w], st);
+  if (lane == 0 && st) atomicOr(&status[w], st);
 }
 
 cudaError_t launch_stability(const OpscDag& d, const OpscGrid& g, OpscWindows w, uint32_t* status,
                              cudaStream_t s) {
-  const int total = w.n * d.n_ops;
-  if (total <= 0) return cudaSuccess;
-  stability_kernel<<<(total + 127) / 128, 128, 0, s>>>(d, g, w, status);
+  const long long threads = (long long)w.n * d.n_ops * 32;
+  if (threads <= 0) return cudaSuccess;
+  stability_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(d, g, w, status);
   return cudaGetLastError();
 }
 

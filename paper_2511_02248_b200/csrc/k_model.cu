@@ -27,7 +27,7 @@ __device__ double eval_uniform(const OpscDag& d, const OpscModelSpec& m, double 
   const int n = d.n_ops;
   bool stable = true;
   if (lane < n) {
-    const Pred o = predict(d, qps, L, ph, lane, m.p_base[lane], r, b, st);
+    const Pred o = predict<true>(d, qps, L, ph, lane, m.p_base[lane], r, b, st);
     stable = o.stable;
     wsh[lane] = weight(o, d.layer_count[lane]);
   }
@@ -228,7 +228,7 @@ __global__ void model_tab_weights(const __grid_constant__ ModelArgs a, const __g
     const double qps = win.qps[w];
     if (!(qps > 0.0)) continue;
     uint32_t st = 0;
-    const Pred o = predict(d, qps, win.seq_len[w], win.phase[w], v, m.p_base[v], r, b, &st);
+    const Pred o = predict<true>(d, qps, win.seq_len[w], win.phase[w], v, m.p_base[v], r, b, &st);
     wt[i] = o.stable ? weight(o, d.layer_count[v]) : OPSC_INF;
     wst[i] = (uint8_t)st;
   }

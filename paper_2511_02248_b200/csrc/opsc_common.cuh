@@ -50,6 +50,29 @@ __device__ __forceinline__ double expected_wait(double lam, double mu, int r) {
   return erlang_c(r, rho) / ((double)r * mu - lam);
 }
 
+// The M/M/R wait for consumers that only use it inside fl(W + service)
+// (sojourn = wait + T/B, and the critical-path weight built from it): the
+// reference's exact recurrence, except that it returns +0.0 as soon as the
+// final W is provably below 2^-56 * service. Then W < half an ulp of service,
+// so fl(W + service) == service == fl(+0 + service): the same bits, without
+// the tail of a long Erlang-B chain. Proof sketch: for k >= a = R*rho every
+// later step multiplies b by a / (k + a b) <= 1 (rounding adds at most a
+// relative 1e-13 over 512 steps), so b_R <= b_k; C_R = R b_R / (R - a(1 - b_R))
+// <= R b_k / (R - a); W = C_R / (R mu - lam). The bound below carries a 4x
+// margin on top. `den` = R*mu - lam as the reference computes it.
+__device__ __forceinline__ double wait_for_sum(int r, double rho, double den, double service) {
+  const double a = (double)r * rho;
+  const double cut = service * 0x1p-56 * den * ((double)r - a) * 0.25;  // on R*b_k
+  double b = 1.0;
+  for (int k = 1; k <= r; ++k) {
+    const double ab = a * b;
+    b = ab / ((double)k + ab);
+    if (b == 0.0) break;
+    if ((double)k >= a && (double)r * b < cut) return 0.0;
+  }
+  return (((double)r * b) / ((double)r - a * (1.0 - b))) / den;
+}
+
 // autoscaler.py:224-228; -1 == None
 __device__ __forceinline__ int strict_min_replicas(double lam, double mu, int r_cap) {
   const double q = ceil(lam / mu);
@@ -77,7 +100,11 @@ struct Pred {
 };
 
 // autoscaler.py:174-194 predict_op; status bits flag the reference's
-// ZeroDivisionError / Unstable raises.
+// ZeroDivisionError / Unstable raises. SUM_ONLY: the caller uses `wait` only
+// through wait + service (sojourn, weight) -- wait_for_sum may then return
+// +0.0 for a wait below half an ulp of the service time (same sojourn bits).
+// Reported PredictedSojourn fields (K4) use the exact form.
+template <bool SUM_ONLY = false>
 __device__ __forceinline__ Pred predict(const OpscDag& d, double qps, int L, int ph, int v, int p,
                                         int r, int b, uint32_t* st) {
   Pred o;
@@ -89,11 +116,12 @@ __device__ __forceinline__ Pred predict(const OpscDag& d, double qps, int L, int
   o.stable = o.lam < (double)r * o.mu;
   o.util = o.lam / ((double)r * o.mu);
   o.wait = OPSC_INF;
+  o.service = o.t / (double)b;
   if (o.stable) {
     if (o.util >= 1.0 || o.util <= 0.0) *st |= OPSC_W_UNSTABLE_ROUNDING;
-    o.wait = erlang_c(r, o.util) / ((double)r * o.mu - o.lam);
+    const double den = (double)r * o.mu - o.lam;
+    o.wait = SUM_ONLY ? wait_for_sum(r, o.util, den, o.service) : erlang_c(r, o.util) / den;
   }
-  o.service = o.t / (double)b;
   o.comm = comm_time(d, v, b, L);
   return o;
 }
