@@ -46,65 +46,9 @@ struct GShared {
   int trace_len;
 };
 
-__device__ double crit_path(const OpscDag& d, const double* wt, int8_t* path_out);
-
 // critical path with the reference's lexicographic path tie-break (opgraph.py:223-244)
-__device__ double crit_path(const OpscDag& d, const double* wt, int8_t* path_out) {
-  const int n = d.n_ops;
-  double val[OPSC_MAX_OPS];
-  int8_t pth[OPSC_MAX_OPS][OPSC_MAX_OPS];
-  int plen[OPSC_MAX_OPS];
-  for (int i = 0; i < n; ++i) {
-    const int v = d.topo[i];
-    const uint32_t pm = d.pred_mask[v];
-    if (!pm) {
-      val[v] = wt[v];
-      pth[v][0] = (int8_t)v;
-      plen[v] = 1;
-      continue;
-    }
-    int cand = -1;
-    double cv = 0.0;
-    for (int p = 0; p < n; ++p) {
-      if (!(pm >> p & 1u)) continue;
-      const double ev = val[p] + wt[v];
-      bool take = cand < 0 || ev > cv;
-      if (!take && ev == cv) {
-        const int la = plen[p], lb = plen[cand], mn = la < lb ? la : lb;
-        int k = 0;
-        while (k < mn && pth[p][k] == pth[cand][k]) ++k;
-        if (k < mn) take = pth[p][k] < pth[cand][k];
-        else if (la < lb) take = (int8_t)v < pth[cand][la];
-        else if (lb < la) take = pth[p][lb] < (int8_t)v;
-      }
-      if (take) {
-        cand = p;
-        cv = ev;
-      }
-    }
-    val[v] = cv;
-    for (int k = 0; k < plen[cand]; ++k) pth[v][k] = pth[cand][k];
-    pth[v][plen[cand]] = (int8_t)v;
-    plen[v] = plen[cand] + 1;
-  }
-  int tv = -1;
-  double top = 0.0;
-  for (int s = 0; s < n; ++s) {
-    if (!(d.sink_mask >> s & 1u)) continue;
-    bool take = tv < 0 || val[s] > top;
-    if (!take && val[s] == top) {
-      const int la = plen[s], lb = plen[tv], mn = la < lb ? la : lb;
-      int k = 0;
-      while (k < mn && pth[s][k] == pth[tv][k]) ++k;
-      take = k < mn ? pth[s][k] < pth[tv][k] : la < lb;
-    }
-    if (take) {
-      tv = s;
-      top = val[s];
-    }
-  }
-  for (int i = 0; i < n; ++i) path_out[i] = i < plen[tv] ? pth[tv][i] : (int8_t)-1;
-  return top;
+__device__ __forceinline__ double crit_path(const OpscDag& d, const double* wt, int8_t* path_out) {
+  return critical_path_lex(d, wt, path_out);
 }
 
 // latency of the current plan with op `v`'s weight replaced (value only)
@@ -414,15 +358,20 @@ __device__ void prune_pass(GShared& S, const GreedyArgs& a, const OpscDecisions&
       changed = 0;
       for (int v = 0; v < d.n_ops; ++v) {
         if (S.r[v] <= 1 || !t_ok[v]) continue;
-        if (!(trial_latency(d, S.wt, v, t_wt[v]) <= target)) continue;
+        const double lat = trial_latency(d, S.wt, v, t_wt[v]);
+        if (!(lat <= target)) continue;
         S.r[v] -= 1;
         S.wt[v] = t_wt[v];
         S.soj[v] = t_soj[v];
-        S.lat = crit_path(d, S.wt, S.path);
+        // the accepted trial's DP value IS the new critical-path latency
+        // (max over predecessors commutes with the monotone + w); the path
+        // itself is only needed after the pass
+        S.lat = lat;
         push_trace(S, out, w, OPSC_ACT_PRUNE, v, S.r[v], S.b[v], S.p[v], S.lat, objective(S, d.n_ops));
         t_need[v] = 1;
         changed = 1;
       }
+      if (!changed) S.lat = crit_path(d, S.wt, S.path);  // path (and the same value) for what follows
     }
     __syncthreads();
     if (!changed) break;

@@ -13,67 +13,6 @@
 
 namespace opsc {
 
-__device__ __forceinline__ bool path_less(const int8_t* a, int la, const int8_t* b, int lb) {
-  const int n = la < lb ? la : lb;
-  for (int i = 0; i < n; ++i)
-    if (a[i] != b[i]) return a[i] < b[i];
-  return la < lb;
-}
-
-__device__ double critical_path(const OpscDag& d, const double* wt, int8_t* path_out) {
-  const int n = d.n_ops;
-  double val[OPSC_MAX_OPS];
-  int8_t pth[OPSC_MAX_OPS][OPSC_MAX_OPS];
-  int plen[OPSC_MAX_OPS];
-  for (int i = 0; i < n; ++i) {
-    const int v = d.topo[i];
-    const uint32_t pm = d.pred_mask[v];
-    if (!pm) {
-      val[v] = wt[v];
-      pth[v][0] = (int8_t)v;
-      plen[v] = 1;
-      continue;
-    }
-    int cand = -1;
-    double cv = 0.0;
-    for (int p = 0; p < n; ++p) {
-      if (!(pm >> p & 1u)) continue;
-      const double ev = val[p] + wt[v];
-      // candidate path = pth[p] + (v,); compare against pth[cand] + (v,)
-      bool take = cand < 0 || ev > cv;
-      if (!take && ev == cv) {
-        // (pp + (v,)) < (cp + (v,)) lexicographically
-        const int la = plen[p], lb = plen[cand];
-        const int mn = la < lb ? la : lb;
-        int i2 = 0;
-        while (i2 < mn && pth[p][i2] == pth[cand][i2]) ++i2;
-        if (i2 < mn) take = pth[p][i2] < pth[cand][i2];
-        else if (la < lb) take = (int8_t)v < pth[cand][la];
-        else if (lb < la) take = pth[p][lb] < (int8_t)v;
-      }
-      if (take) {
-        cand = p;
-        cv = ev;
-      }
-    }
-    val[v] = cv;
-    for (int k = 0; k < plen[cand]; ++k) pth[v][k] = pth[cand][k];
-    pth[v][plen[cand]] = (int8_t)v;
-    plen[v] = plen[cand] + 1;
-  }
-  int tv = -1;
-  double top = 0.0;
-  for (int s = 0; s < n; ++s) {
-    if (!(d.sink_mask >> s & 1u)) continue;
-    if (tv < 0 || val[s] > top || (val[s] == top && path_less(pth[s], plen[s], pth[tv], plen[tv]))) {
-      tv = s;
-      top = val[s];
-    }
-  }
-  for (int i = 0; i < n; ++i) path_out[i] = i < plen[tv] ? pth[tv][i] : (int8_t)-1;
-  return top;
-}
-
 __device__ __forceinline__ double op_memory(const OpscDag& d, int v, int p, int b, int L) {
   return (d.weight_mem[v] / (double)p + d.m0[v]) + (d.m1[v] * (double)b) * (double)L;
 }
@@ -229,7 +168,7 @@ __global__ void __launch_bounds__(32 * kMatWarps) materialize_kernel(const __gri
   int obj = 0;
   for (int v = 0; v < n; ++v) obj += (int)c[v * 3] * (int)c[v * 3 + 1];
   out.objective[w] = obj;
-  if (all) out.latency[w] = critical_path(d, s_wt[warp], out.path + (size_t)w * n);
+  if (all) out.latency[w] = critical_path_lex(d, s_wt[warp], out.path + (size_t)w * n);
   st |= st0;
   if (feas) {
     int dev = 0;

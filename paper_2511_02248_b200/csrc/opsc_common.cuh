@@ -94,6 +94,81 @@ __device__ __forceinline__ double comm_time(const OpscDag& d, int v, long long b
   return best;
 }
 
+// Critical path with the reference's lexicographic path tie-break
+// (opgraph.py:199-244): best[v] = max over predecessors of best[p] + w[v],
+// ties to the lexicographically smallest path tuple (op ids are lex ranks),
+// latency = max over sinks with the same tie-break. Kept as parent pointers:
+// O(n + E) per call; paths are materialised only to break an exact tie.
+__device__ __forceinline__ int cp_path_of(const int8_t* parent, int v, int8_t* buf) {
+  int8_t tmp[OPSC_MAX_OPS];
+  int len = 0;
+  for (int u = v; u >= 0; u = parent[u]) tmp[len++] = (int8_t)u;
+  for (int i = 0; i < len; ++i) buf[i] = tmp[len - 1 - i];
+  return len;
+}
+
+__device__ __forceinline__ bool cp_seq_less(const int8_t* a, int la, const int8_t* b, int lb) {
+  const int n = la < lb ? la : lb;
+  for (int i = 0; i < n; ++i)
+    if (a[i] != b[i]) return a[i] < b[i];
+  return la < lb;
+}
+
+static __device__ __noinline__ double critical_path_lex(const OpscDag& d, const double* wt, int8_t* path_out) {
+  const int n = d.n_ops;
+  double val[OPSC_MAX_OPS];
+  int8_t parent[OPSC_MAX_OPS];
+  for (int i = 0; i < n; ++i) {
+    const int v = d.topo[i];
+    uint32_t pm = d.pred_mask[v];
+    if (!pm) {
+      val[v] = wt[v];
+      parent[v] = -1;
+      continue;
+    }
+    int cand = -1;
+    double cv = 0.0;
+    while (pm) {
+      const int p = __ffs(pm) - 1;
+      pm &= pm - 1;
+      const double ev = val[p] + wt[v];
+      bool take = cand < 0 || ev > cv;
+      if (!take && ev == cv) {  // path(p) + (v,) < path(cand) + (v,) ?
+        int8_t pa[OPSC_MAX_OPS], pb[OPSC_MAX_OPS];
+        const int la = cp_path_of(parent, p, pa), lb = cp_path_of(parent, cand, pb);
+        pa[la] = (int8_t)v;
+        pb[lb] = (int8_t)v;
+        take = cp_seq_less(pa, la + 1, pb, lb + 1);
+      }
+      if (take) {
+        cand = p;
+        cv = ev;
+      }
+    }
+    val[v] = cv;
+    parent[v] = (int8_t)cand;
+  }
+  int tv = -1;
+  double top = 0.0;
+  for (int s = 0; s < n; ++s) {
+    if (!(d.sink_mask >> s & 1u)) continue;
+    bool take = tv < 0 || val[s] > top;
+    if (!take && val[s] == top) {
+      int8_t pa[OPSC_MAX_OPS], pb[OPSC_MAX_OPS];
+      const int la = cp_path_of(parent, s, pa), lb = cp_path_of(parent, tv, pb);
+      take = cp_seq_less(pa, la, pb, lb);
+    }
+    if (take) {
+      tv = s;
+      top = val[s];
+    }
+  }
+  int8_t buf[OPSC_MAX_OPS];
+  const int len = cp_path_of(parent, tv, buf);
+  for (int i = 0; i < n; ++i) path_out[i] = i < len ? buf[i] : (int8_t)-1;
+  return top;
+}
+
 struct Pred {
   double t, lam, mu, util, wait, service, comm;
   bool stable;
