@@ -33,6 +33,7 @@
 //     prefix's minimum; CTA result = warp-shuffle u64 min -> smem -> one
 //     atomicMin per CTA.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "opsc_common.cuh"
@@ -635,6 +636,10 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
     if (!too_many && prod(c.n - il, c.n) >= 2048.0) break;
     if (!too_many && (double)n_windows * prod(0, c.n - il - 1) < min_threads) break;
     ++il;
+  }
+  if (const char* f = getenv("OPSC_COMPOSE_IL")) {  // dev override (tools/w1_latency.py)
+    const int want = atoi(f);
+    if (want >= 2 && want <= 6 && want <= c.n && prod(0, c.n - want) < 4294967295.0) il = want;
   }
   if (prod(0, c.n - il) >= 4294967295.0) return OPSC_ERR_SPACE;
   c.il = il;
