@@ -56,6 +56,7 @@ namespace opsc {
 #define OPSC_COMPOSE_FP32MASK 0
 #endif
 constexpr int kComposeThreads = OPSC_COMPOSE_THREADS;
+constexpr int kOdoLevels = 4;  // middle levels kept in registers on path DAGs (il <= 6)
 constexpr unsigned long long kSentinel = 1ull << 62;  // > any real key (objective < 2^17)
 
 __device__ __forceinline__ double dp_in(uint32_t pm, const double* val) {
@@ -496,26 +497,72 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
     const bool k_to_j = (c.pmask[jp] & kmask) != 0;
     const bool k_sink = (c.sinkmask & kmask) != 0;
 
+    // Path DAGs (every position's only predecessor is the previous one, one
+    // sink): the middle levels run as an odometer with their prefix values in
+    // registers -- val[pos] = val[pos-1] + w, the DP's own adds in the same
+    // order -- instead of re-decoding the digits with divisions and re-running
+    // the DP through local memory for every middle index.
+    const int nmid = kp - nout;
+    const bool odo = CHAIN && c.path_dag && nmid <= kOdoLevels;
+    int od[kOdoLevels];
+#pragma unroll
+    for (int l = 0; l < kOdoLevels; ++l) od[l] = 0;
+    bool odo_dirty = true;
+
     for (uint32_t mid = 0; mid < c.mid_count; ++mid) {
-      uint32_t r2 = mid;
-      for (int pos = kp - 1; pos >= nout; --pos) {
-        const uint32_t mm = (uint32_t)c.m[pos];
-        const uint32_t q = r2 / mm;
-        dig[pos] = (int)(r2 - q * mm);
-        r2 = q;
+      long long cost1;
+      unsigned long long lex1;
+      double in_k;
+      double bj0 = 0.0, lo0 = 0.0;
+      if (odo) {
+        if (!odo_dirty) {  // advance the odometer (innermost middle level fastest)
+          bool carry = true;
+#pragma unroll
+          for (int l = kOdoLevels - 1; l >= 0; --l) {
+            if (l < nmid && carry) {
+              if (++od[l] == c.m[nout + l]) od[l] = 0;
+              else carry = false;
+            }
+          }
+        }
+        odo_dirty = false;
+        // dp_in of a single predecessor: fmax(0.0, val[prev]); no predecessor: 0.0
+        double pv = nout > 0 ? fmax(0.0, val[nout - 1]) : 0.0;
+        long long pc = cost0;
+        unsigned long long pl = lex0;
+#pragma unroll
+        for (int l = 0; l < kOdoLevels; ++l) {
+          if (l < nmid) {
+            const int e = c.off[nout + l] + od[l];
+            pv = fmax(0.0, pv + s.w[e]);  // val[pos], then the next position's dp_in
+            pc += s.cost[e];
+            pl += (unsigned long long)od[l] * c.stride[nout + l];
+          }
+        }
+        in_k = pv;
+        cost1 = pc;
+        lex1 = pl;
+      } else {
+        uint32_t r2 = mid;
+        for (int pos = kp - 1; pos >= nout; --pos) {
+          const uint32_t mm = (uint32_t)c.m[pos];
+          const uint32_t q = r2 / mm;
+          dig[pos] = (int)(r2 - q * mm);
+          r2 = q;
+        }
+        cost1 = cost0;
+        lex1 = lex0;
+        for (int pos = nout; pos < kp; ++pos) {
+          const int e = c.off[pos] + dig[pos];
+          val[pos] = dp_in(c.pmask[pos], val) + s.w[e];
+          cost1 += s.cost[e];
+          lex1 += (unsigned long long)dig[pos] * c.stride[pos];
+        }
+        in_k = dp_in(c.pmask[kp], val);
+        bj0 = dp_in(c.pmask[jp] & ~kmask, val);
+        lo0 = dp_in(c.sinkmask & ~(kmask | jmask), val);
+        if (CHAIN && !(lo0 <= slo)) in_k = OPSC_INF;  // another sink already misses the SLO
       }
-      long long cost1 = cost0;
-      unsigned long long lex1 = lex0;
-      for (int pos = nout; pos < kp; ++pos) {
-        const int e = c.off[pos] + dig[pos];
-        val[pos] = dp_in(c.pmask[pos], val) + s.w[e];
-        cost1 += s.cost[e];
-        lex1 += (unsigned long long)dig[pos] * c.stride[pos];
-      }
-      double in_k = dp_in(c.pmask[kp], val);
-      const double bj0 = dp_in(c.pmask[jp] & ~kmask, val);
-      const double lo0 = dp_in(c.sinkmask & ~(kmask | jmask), val);
-      if (CHAIN && !(lo0 <= slo)) in_k = OPSC_INF;  // another sink already misses the SLO
 
       unsigned long long mbest = kSentinel;
       if constexpr (NJ > 0) {
@@ -672,6 +719,10 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
   // chain fast path: j's only predecessor is k and k is not a sink
   const int jp = c.n - 1, kp = c.n - 2;
   c.chain = (c.pmask[jp] == (1u << kp)) && !(c.sinkmask >> kp & 1u);
+  // path DAG: position 0 a source, every later position fed by the previous
+  // one only, a single sink at the end
+  c.path_dag = c.pmask[0] == 0u && c.sinkmask == (1u << jp);
+  for (int pos = 1; pos < c.n; ++pos) c.path_dag &= c.pmask[pos] == (1u << (pos - 1));
   *cfg = c;
   return OPSC_OK;
 }
