@@ -680,7 +680,7 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
   int il = 2;
   while (il < c.n && il < 6) {
     const bool too_many = prod(0, c.n - il) >= 4294967295.0;
-    if (!too_many && prod(c.n - il, c.n) >= 2048.0) break;
+    if (!too_many && prod(c.n - il, c.n) >= 1024.0) break;  // in-thread candidates amortise the outer decode
     if (!too_many && (double)n_windows * prod(0, c.n - il - 1) < min_threads) break;
     ++il;
   }

@@ -1,4 +1,7 @@
-"""Quick device timing of the cfg5 pipeline (dev tool)."""
+"""Quick device timing of the exhaustive pipeline (dev tool): cfg5 (default) or cfg2.
+
+    python tools/quick_time.py [cfg5|cfg2]
+"""
 import os
 import sys
 import time
@@ -9,11 +12,12 @@ from paper_2511_02248_b200 import _native, abi, model, scenarios, tables
 
 nat = _native
 L = nat.load()
-prob = tables.pack_problem(*scenarios.scenario("cfg5"))
-g = scenarios.GRIDS["cfg5"]
+CFG = sys.argv[1] if len(sys.argv) > 1 else "cfg5"
+prob = tables.pack_problem(*scenarios.scenario(CFG))
+g = scenarios.GRIDS[CFG]
 grid = tables.pack_grid(prob, model.AutoscaleParams(slo=1.0), model.BruteForceBounds(**g))
-tw = scenarios.trace_windows("cfg5")
-win = tables.window_arrays(tw["prefill_qps"], tw["prefill_len"], 0, 0.5)
+tw = scenarios.trace_windows(CFG)
+win = tables.window_arrays(tw["prefill_qps"], tw["prefill_len"], 0, scenarios.SLO[CFG]["prefill"])
 dev = torch.device("cuda:0")
 t = {k: torch.from_numpy(np.ascontiguousarray(getattr(win, k))).to(dev) for k in ("qps", "seq_len", "phase", "slo", "eps")}
 dw = abi.OpscWindows(); dw.n = win.n
@@ -34,8 +38,8 @@ e0.record();
 for _ in range(5): step()
 e1.record(); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 5
-cands = win.n * 24**6
-print(f"cfg5 step {ms:.3f} ms  candidates {cands:.3e}  rate {cands/ms*1e3:.3e}/s")
+cands = win.n * int(np.prod([grid.menu_off[v + 1] - grid.menu_off[v] for v in range(prob.n_ops)]))
+print(f"{CFG} step {ms:.3f} ms  candidates {cands:.3e}  rate {cands/ms*1e3:.3e}/s")
 ms2 = ctypes_ms = None
 import ctypes as C
 f = C.c_float(); ops = C.c_double()
