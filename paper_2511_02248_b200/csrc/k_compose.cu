@@ -46,6 +46,9 @@ namespace opsc {
 #ifndef OPSC_COMPOSE_MINB
 #define OPSC_COMPOSE_MINB 3  // 80 registers, no spills: 7.38e12 vs 7.28e12 candidates/s at 4 CTAs/SM (64 regs, spills)
 #endif
+#ifndef OPSC_COMPOSE_KUNROLL
+#define OPSC_COMPOSE_KUNROLL 3  // k-loop unroll of the exact form: +5% on 6-entry menus, neutral on 24
+#endif
 #ifndef OPSC_COMPOSE_FP32MASK
 // 1: high-word SLO mask on the FMA pipe (DADD + FFMA.SAT + IADD3/2 per
 //    candidate, superset count trimmed exactly) -- fewer issue slots, but on
@@ -56,7 +59,8 @@ namespace opsc {
 #define OPSC_COMPOSE_FP32MASK 0
 #endif
 constexpr int kComposeThreads = OPSC_COMPOSE_THREADS;
-constexpr int kOdoLevels = 4;  // middle levels kept in registers on path DAGs (il <= 6)
+constexpr int kOdoLevels = 4;
+constexpr int kKUnroll = OPSC_COMPOSE_KUNROLL;  // middle levels kept in registers on path DAGs (il <= 6)
 constexpr unsigned long long kSentinel = 1ull << 62;  // > any real key (objective < 2^17)
 
 __device__ __forceinline__ double dp_in(uint32_t pm, const double* val) {
@@ -210,7 +214,7 @@ __device__ __forceinline__ uint32_t k_level_tile(uint32_t a_wk, uint32_t a_kk, u
                                                  double lo0, bool k_to_j, bool k_sink, double slo, MaskConsts mc) {
   uint32_t mbest = 0xffffffffu;
   const uint32_t a_end = a_kk + 4u * (uint32_t)mk;
-  if (FAST) {
+  if constexpr (FAST) {
 #pragma unroll 1
     for (; a_kk + 4u < a_end; a_kk += 8u, a_wk += 16u) {
       const double bja = j_base<CHAIN>(in_k + lds_f64(a_wk), bj0, lo0, k_to_j, k_sink, slo);
@@ -223,16 +227,26 @@ __device__ __forceinline__ uint32_t k_level_tile(uint32_t a_wk, uint32_t a_kk, u
       const uint32_t kb = lds_u32(a_kk + 4u) + lds_u32(a_pm + 4u * cb);
       mbest = min(mbest, min(ka, kb));
     }
-  }
 #pragma unroll 1
+    for (; a_kk < a_end; a_kk += 4u, a_wk += 8u) {
+      const double bj = j_base<CHAIN>(in_k + lds_f64(a_wk), bj0, lo0, k_to_j, k_sink, slo);
+      const uint32_t cnt = trim_count(mask_count<NJ>(bj, wj, mc), (uint32_t)mj, bj, a_jw, slo);
+      const uint32_t kl = lds_u32(a_kk) + lds_u32(a_pm + 4u * cnt);
+      mbest = kl < mbest ? kl : mbest;
+    }
+    return mbest;
+  } else {
+  // exact form; the +inf padding past m_j never passes (slo <= DBL_MAX), so
+  // the count needs no clamp
+#pragma unroll(kKUnroll)
   for (; a_kk < a_end; a_kk += 4u, a_wk += 8u) {
     const double bj = j_base<CHAIN>(in_k + lds_f64(a_wk), bj0, lo0, k_to_j, k_sink, slo);
-    uint32_t cnt = FAST ? trim_count(mask_count<NJ>(bj, wj, mc), (uint32_t)mj, bj, a_jw, slo)
-                        : min(exact_count<NJ>(bj, wj, slo), (uint32_t)mj);
+    const uint32_t cnt = exact_count<NJ>(bj, wj, slo);
     const uint32_t kl = lds_u32(a_kk) + lds_u32(a_pm + 4u * cnt);
     mbest = kl < mbest ? kl : mbest;
   }
   return mbest;
+  }
 }
 
 // Shared-memory path for large j menus (NJ == 0): u64 keys, exact compares.
