@@ -59,7 +59,7 @@ def build(verbose=False, force=False):
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
-    with open(os.path.join(OUT, "ptxas.log"), "a") as fh:
+    with open(os.path.join(OUT, "ptxas.log"), "w") as fh:  # this build's compiles only
         fh.write("".join(log))
     if verbose:
         print("".join(log))

@@ -27,8 +27,8 @@
 //     with no loop-carried dependency, so warps issue back to back. The
 //     per-k fold works on 32-bit local keys (cost_k + cost_j, local (k, j)
 //     index) from 32-bit shared addresses, converted to the u64 key once per
-//     prefix. (OPSC_COMPOSE_FP32MASK selects an alternative mask on the FMA
-//     pipe; see its definition for why it is off);
+//     prefix. (A high-word mask on the FMA pipe was measured and rejected:
+//     DESIGN.md, instruction-mix paragraph; tools/probe/cand_probe.cu);
 //   * per k entry the cheapest feasible (k, j) pair is folded into the
 //     prefix's minimum; CTA result = warp-shuffle u64 min -> smem -> one
 //     atomicMin per CTA.
@@ -48,15 +48,6 @@ namespace opsc {
 #endif
 #ifndef OPSC_COMPOSE_KUNROLL
 #define OPSC_COMPOSE_KUNROLL 3  // k-loop unroll of the exact form: +5% on 6-entry menus, neutral on 24
-#endif
-#ifndef OPSC_COMPOSE_FP32MASK
-// 1: high-word SLO mask on the FMA pipe (DADD + FFMA.SAT + IADD3/2 per
-//    candidate, superset count trimmed exactly) -- fewer issue slots, but on
-//    B200 it measured 6.1e12 candidates/s against 7.3e12 for the exact
-//    DADD + DSETP + SEL form: ptxas keeps one latency register per thread under
-//    the 64-register cap and the DADD -> FFMA chains stall (ncu: issue active
-//    72%, every pipe < 40%). Kept for A/B runs (tools/variants.sh).
-#define OPSC_COMPOSE_FP32MASK 0
 #endif
 constexpr int kComposeThreads = OPSC_COMPOSE_THREADS;
 constexpr int kOdoLevels = 4;
@@ -89,40 +80,13 @@ struct ComposeSmem {
 // pm32[0] = 2^31 is >= 2^31 (infeasible), and nothing overflows.
 constexpr uint32_t kLocalInfeasible = 1u << 31;
 
-// High-word SLO mask constants. For a window with 0 < slo and
-// 2^25 <= bits(Hf) >> 23 <= 254, where Hf is the float whose bits are
-// hi32(slo) + 1:
-//     t(lat) = sat(fma(f, -BIG, Hf*BIG)),  f = float with bits hi32(lat),
-//     BIG = 2^(25 - exponent(Hf)),
-// is exactly 1.0f when s32(hi32(lat)) <= s32(hi32(slo)) and +0.0f otherwise
-// (NaN lat -> 0). Distinct floats near Hf differ by >= 2^(e-24), so a
-// passing difference scales to >= 2 before saturation. Every lat <= slo
-// passes: non-negative doubles order like their bit patterns, negative ones
-// have a negative f. Windows outside that slo range (the reference rejects
-// slo <= 0; the others are >= 2^1017 or < 2^-823) take the exact scan.
-struct MaskConsts {
-  float nbig, hb;
-  bool fast;
-};
-
-__device__ __forceinline__ MaskConsts mask_consts(double slo) {
-  MaskConsts m;
-  const int h1 = __double2hiint(slo) + 1;
-  const int ex = h1 >> 23;  // biased float exponent of Hf
-  m.fast = slo > 0.0 && ex >= 25 && ex <= 254;
-  const int eb = m.fast ? 127 + 25 - (ex - 127) : 127;  // BIG = 2^(25 - e)
-  m.nbig = -__int_as_float(eb << 23);
-  m.hb = __int_as_float(h1) * -m.nbig;  // exact: power-of-two scaling into [2^25, 2^26)
-  return m;
-}
-
 __device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
   asm volatile("mov.b32 %0, %0;" : "+r"(x));
   return x;
 }
 
-// 32-bit shared-window loads (the k loop keeps four 32-bit addresses live
-// instead of 64-bit generic pointers)
+// 32-bit shared-window loads (the k loop keeps 32-bit addresses live instead
+// of 64-bit generic pointers)
 __device__ __forceinline__ double lds_f64(uint32_t a) {
   double v;
   asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
@@ -134,51 +98,6 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
   return v;
 }
 
-// High-word mask count of one j row: number of j with t(bj + w_j) = 1.
-template <int NJ>
-__device__ __forceinline__ uint32_t mask_count(double bj, const double (&wj)[NJ], MaskConsts mc) {
-  uint32_t acc = 0;
-#pragma unroll
-  for (int i = 0; i < NJ; i += 2) {
-    const double la = bj + wj[i];
-    const float ta = __saturatef(__fmaf_rn(__int_as_float(__double2hiint(la)), mc.nbig, mc.hb));
-    float tb = 0.0f;
-    if (i + 1 < NJ) {
-      const double lb = bj + wj[i + 1];
-      tb = __saturatef(__fmaf_rn(__int_as_float(__double2hiint(lb)), mc.nbig, mc.hb));
-    }
-    acc += __float_as_uint(ta) + __float_as_uint(tb);
-  }
-  // acc = n * 0x3F800000 (mod 2^32) = 2^23 * 127 n; 383 = 127^-1 mod 512
-  return ((acc >> 23) * 383u) & 511u;
-}
-
-// Two j rows (k entries a and a+1) interleaved: two independent DADD chains
-// per thread over the same register-resident j weights.
-template <int NJ>
-__device__ __forceinline__ void mask_count2(double bj0, double bj1, const double (&wj)[NJ], MaskConsts mc,
-                                            uint32_t& c0, uint32_t& c1) {
-  uint32_t acc0 = 0, acc1 = 0;
-#pragma unroll
-  for (int i = 0; i < NJ; i += 2) {
-    const double la0 = bj0 + wj[i];
-    const double la1 = bj1 + wj[i];
-    const float ta0 = __saturatef(__fmaf_rn(__int_as_float(__double2hiint(la0)), mc.nbig, mc.hb));
-    const float ta1 = __saturatef(__fmaf_rn(__int_as_float(__double2hiint(la1)), mc.nbig, mc.hb));
-    float tb0 = 0.0f, tb1 = 0.0f;
-    if (i + 1 < NJ) {
-      const double lb0 = bj0 + wj[i + 1];
-      const double lb1 = bj1 + wj[i + 1];
-      tb0 = __saturatef(__fmaf_rn(__int_as_float(__double2hiint(lb0)), mc.nbig, mc.hb));
-      tb1 = __saturatef(__fmaf_rn(__int_as_float(__double2hiint(lb1)), mc.nbig, mc.hb));
-    }
-    acc0 += __float_as_uint(ta0) + __float_as_uint(tb0);
-    acc1 += __float_as_uint(ta1) + __float_as_uint(tb1);
-  }
-  c0 = ((acc0 >> 23) * 383u) & 511u;
-  c1 = ((acc1 >> 23) * 383u) & 511u;
-}
-
 // Exact count: the feasible j form a prefix in weight order.
 template <int NJ>
 __device__ __forceinline__ uint32_t exact_count(double bj, const double (&wj)[NJ], double slo) {
@@ -186,14 +105,6 @@ __device__ __forceinline__ uint32_t exact_count(double bj, const double (&wj)[NJ
 #pragma unroll
   for (int i = 0; i < NJ; ++i)
     if (bj + wj[i] <= slo) cnt = (uint32_t)i + 1u;
-  return cnt;
-}
-
-// Superset count -> exact count: drop boundary entries that tie slo's high
-// word but fail the full compare.
-__device__ __forceinline__ uint32_t trim_count(uint32_t cnt, uint32_t mj, double bj, uint32_t a_jw, double slo) {
-  cnt = cnt < mj ? cnt : mj;
-  while (cnt > 0 && !(bj + lds_f64(a_jw + 8u * (cnt - 1u)) <= slo)) --cnt;
   return cnt;
 }
 
@@ -207,37 +118,14 @@ __device__ __forceinline__ double j_base(double bk, double bj0, double lo0, bool
 
 // The k and j levels for one prefix. Register-tile path (NJ > 0): returns
 // the minimum local key (>= kLocalInfeasible if no candidate is feasible).
-// a_wk / a_kk / a_pm / a_jw: shared addresses of w[koff], kk32, pm32, jw.
-template <int NJ, bool CHAIN, bool FAST>
-__device__ __forceinline__ uint32_t k_level_tile(uint32_t a_wk, uint32_t a_kk, uint32_t a_pm, uint32_t a_jw,
-                                                 int mk, int mj, const double (&wj)[NJ], double in_k, double bj0,
-                                                 double lo0, bool k_to_j, bool k_sink, double slo, MaskConsts mc) {
+// a_wk / a_kk / a_pm: shared addresses of w[koff], kk32, pm32. The +inf
+// padding past m_j never passes (slo <= DBL_MAX), so the count needs no clamp.
+template <int NJ, bool CHAIN>
+__device__ __forceinline__ uint32_t k_level_tile(uint32_t a_wk, uint32_t a_kk, uint32_t a_pm, int mk,
+                                                 const double (&wj)[NJ], double in_k, double bj0, double lo0,
+                                                 bool k_to_j, bool k_sink, double slo) {
   uint32_t mbest = 0xffffffffu;
   const uint32_t a_end = a_kk + 4u * (uint32_t)mk;
-  if constexpr (FAST) {
-#pragma unroll 1
-    for (; a_kk + 4u < a_end; a_kk += 8u, a_wk += 16u) {
-      const double bja = j_base<CHAIN>(in_k + lds_f64(a_wk), bj0, lo0, k_to_j, k_sink, slo);
-      const double bjb = j_base<CHAIN>(in_k + lds_f64(a_wk + 8u), bj0, lo0, k_to_j, k_sink, slo);
-      uint32_t ca, cb;
-      mask_count2<NJ>(bja, bjb, wj, mc, ca, cb);
-      ca = trim_count(ca, (uint32_t)mj, bja, a_jw, slo);
-      cb = trim_count(cb, (uint32_t)mj, bjb, a_jw, slo);
-      const uint32_t ka = lds_u32(a_kk) + lds_u32(a_pm + 4u * ca);
-      const uint32_t kb = lds_u32(a_kk + 4u) + lds_u32(a_pm + 4u * cb);
-      mbest = min(mbest, min(ka, kb));
-    }
-#pragma unroll 1
-    for (; a_kk < a_end; a_kk += 4u, a_wk += 8u) {
-      const double bj = j_base<CHAIN>(in_k + lds_f64(a_wk), bj0, lo0, k_to_j, k_sink, slo);
-      const uint32_t cnt = trim_count(mask_count<NJ>(bj, wj, mc), (uint32_t)mj, bj, a_jw, slo);
-      const uint32_t kl = lds_u32(a_kk) + lds_u32(a_pm + 4u * cnt);
-      mbest = kl < mbest ? kl : mbest;
-    }
-    return mbest;
-  } else {
-  // exact form; the +inf padding past m_j never passes (slo <= DBL_MAX), so
-  // the count needs no clamp
 #pragma unroll(kKUnroll)
   for (; a_kk < a_end; a_kk += 4u, a_wk += 8u) {
     const double bj = j_base<CHAIN>(in_k + lds_f64(a_wk), bj0, lo0, k_to_j, k_sink, slo);
@@ -246,7 +134,6 @@ __device__ __forceinline__ uint32_t k_level_tile(uint32_t a_wk, uint32_t a_kk, u
     mbest = kl < mbest ? kl : mbest;
   }
   return mbest;
-  }
 }
 
 // Shared-memory path for large j menus (NJ == 0): u64 keys, exact compares.
@@ -475,14 +362,12 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
   // reference skips non-finite menu weights, autoscaler.py:800-801): compare
   // against DBL_MAX, which keeps the INF-weighted (unstable) entries out.
   const double slo = fmin(slo_w[w], 1.7976931348623157e308);
-  const MaskConsts mc = mask_consts(slo);
   // opaque copies: keeps the k loop from rematerialising the addresses
   // (CgaCtaId + parameter loads) in every iteration under register pressure
   const uint32_t a_wk = opaque_u32((uint32_t)__cvta_generic_to_shared(s.w + koff));
   const uint32_t a_kk = opaque_u32((uint32_t)__cvta_generic_to_shared(s.kk32));
   const uint32_t a_pm = opaque_u32((uint32_t)__cvta_generic_to_shared(s.pm32));
-  const uint32_t a_jw = opaque_u32((uint32_t)__cvta_generic_to_shared(s.jw));
-  const int mk_r = (int)opaque_u32((uint32_t)mk), mj_r = (int)opaque_u32((uint32_t)mj);
+  const int mk_r = (int)opaque_u32((uint32_t)mk);
   unsigned long long best = kSentinel;
   const uint32_t o = c.lo + (uint32_t)bw * kComposeThreads + threadIdx.x;
   if (qps_w[w] > 0.0 && o < c.hi) {
@@ -580,12 +465,7 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
 
       unsigned long long mbest = kSentinel;
       if constexpr (NJ > 0) {
-        const uint32_t m32 =
-            (OPSC_COMPOSE_FP32MASK && mc.fast)
-                ? k_level_tile<NJ, CHAIN, true>(a_wk, a_kk, a_pm, a_jw, mk_r, mj_r, wj, in_k, bj0, lo0, k_to_j,
-                                                k_sink, slo, mc)
-                : k_level_tile<NJ, CHAIN, false>(a_wk, a_kk, a_pm, a_jw, mk_r, mj_r, wj, in_k, bj0, lo0, k_to_j,
-                                                 k_sink, slo, mc);
+        const uint32_t m32 = k_level_tile<NJ, CHAIN>(a_wk, a_kk, a_pm, mk_r, wj, in_k, bj0, lo0, k_to_j, k_sink, slo);
         if (m32 < kLocalInfeasible) {  // back to the global key
           const uint32_t loc = m32 & 0xfffffu;
           const uint32_t a = c.kj_major ? loc / (uint32_t)mj : loc % (uint32_t)mk;
