@@ -17,57 +17,84 @@ __device__ __forceinline__ double op_memory(const OpscDag& d, int v, int p, int 
   return (d.weight_mem[v] / (double)p + d.m0[v]) + (d.m1[v] * (double)b) * (double)L;
 }
 
-// default_stream_place; returns 0 or an error bit
-__device__ uint32_t place_default_stream(const OpscDag& d, const OpscPlaceSpec& pl, const int16_t* c,
-                                         const double* T, int L, int* devices, double* memory) {
+// Per-warp shared scratch of the serial lane-0 section: a one-shot walk over
+// cold local memory would pay an L2 round trip per access.
+struct MatScratch {
+  double mem[OPSC_MAX_OPS];
+  double val[OPSC_MAX_OPS];
+  double ds_f[OPSC_MAX_OPS], ds_c[OPSC_MAX_OPS];  // per-device PySum state (Neumaier)
+  int order[OPSC_MAX_OPS], xord[OPSC_MAX_OPS], inst_dev[OPSC_MAX_OPS];
+  int k_base;
+  int8_t parent[OPSC_MAX_OPS];
+};
+
+// Warp-parallel part of default_stream_place (lane v = operator v): memory
+// per replica, and the two stable sorts as ranks -- (-(weight_mem/P), id)
+// for base instances and (-op_latency, id) for extra replicas
+// (placement.py:358-396, 465-491).
+__device__ __forceinline__ void place_prepare(const OpscDag& d, const int16_t* c, const double* T, int L,
+                                              MatScratch& S, int lane) {
   const int n = d.n_ops;
-  int k_base = 1 << 30;
-  double mem[OPSC_MAX_OPS], ratio[OPSC_MAX_OPS];
-  int order[OPSC_MAX_OPS], xord[OPSC_MAX_OPS];
-  for (int v = 0; v < n; ++v) {
-    k_base = min(k_base, (int)c[v * 3 + 1]);
-    mem[v] = op_memory(d, v, c[v * 3], c[v * 3 + 2], L);
-    ratio[v] = -(d.weight_mem[v] / (double)c[v * 3]);
-    order[v] = v;
-    xord[v] = v;
+  int kb = 1 << 30;
+  if (lane < n) {
+    const int v = lane;
+    S.mem[v] = op_memory(d, v, c[v * 3], c[v * 3 + 2], L);
+    const double rv = -(d.weight_mem[v] / (double)c[v * 3]);
+    const double tv = -T[v];
+    int r1 = 0, r2 = 0;
+    for (int u = 0; u < n; ++u) {
+      const double ru = -(d.weight_mem[u] / (double)c[u * 3]);
+      const double tu = -T[u];
+      r1 += ru < rv || (ru == rv && u < v);
+      r2 += tu < tv || (tu == tv && u < v);
+    }
+    S.order[r1] = v;
+    S.xord[r2] = v;
+    kb = c[v * 3 + 1];
   }
-  // sort keys (-(weight_mem/P), id) and (-op_latency, id); insertion sort is stable
-  for (int i = 1; i < n; ++i) {
-    const int x = order[i];
-    int j = i - 1;
-    while (j >= 0 && ratio[order[j]] > ratio[x]) { order[j + 1] = order[j]; --j; }
-    order[j + 1] = x;
-    const int y = xord[i];
-    j = i - 1;
-    while (j >= 0 && -T[xord[j]] > -T[y]) { xord[j + 1] = xord[j]; --j; }
-    xord[j + 1] = y;
-  }
+  kb = __reduce_min_sync(0xffffffffu, kb);
+  if (lane == 0) S.k_base = kb;
+  __syncwarp();
+}
+
+// default_stream_place (lane 0, sequential as the reference); returns 0 or an error bit
+__device__ uint32_t place_default_stream(const OpscPlaceSpec& pl, const int16_t* c, int n, MatScratch& S,
+                                         int* devices, double* memory) {
+  const int k_base = S.k_base;
   PySum total;
   total.reset();
   int used = 0;
   auto cap_of = [&](int dev) { return pl.uniform_cap ? pl.mem_cap[0] : pl.mem_cap[dev]; };
+  auto dev_value = [&](int j) { const double f = S.ds_f[j], cc = S.ds_c[j]; return (cc != 0.0 && isfinite(cc)) ? f + cc : f; };
   // base instances (placement.py:358-385)
-  int inst_dev[OPSC_MAX_OPS];
-  PySum dev_sum[OPSC_MAX_OPS];
   const int full_sim = pl.uniform_cap ? 1 : k_base;  // uniform caps: every instance packs alike
   int per_inst = 0;
   for (int inst = 1; inst <= full_sim; ++inst) {
     int nd = 0;
     for (int i = 0; i < n; ++i) {
-      const int v = order[i];
+      const int v = S.order[i];
+      const double m = S.mem[v];
       int t = -1;
       for (int j = 0; j < nd; ++j)
-        if (dev_sum[j].value() + mem[v] <= cap_of(inst_dev[j])) { t = j; break; }
+        if (dev_value(j) + m <= cap_of(S.inst_dev[j])) { t = j; break; }
       if (t < 0) {
         if (used >= pl.n_devices) return OPSC_W_FLEET_EXHAUSTED;
         const int dev = used++;
-        if (mem[v] > cap_of(dev)) return OPSC_W_INFEASIBLE_PLACEMENT;
-        inst_dev[nd] = dev;
-        dev_sum[nd].reset();
+        if (m > cap_of(dev)) return OPSC_W_INFEASIBLE_PLACEMENT;
+        S.inst_dev[nd] = dev;
+        S.ds_f[nd] = 0.0 + m;  // PySum's first add
+        S.ds_c[nd] = 0.0;
         t = nd++;
+      } else {
+        PySum ds;
+        ds.f = S.ds_f[t];
+        ds.c = S.ds_c[t];
+        ds.started = true;
+        ds.add(m);
+        S.ds_f[t] = ds.f;
+        S.ds_c[t] = ds.c;
       }
-      dev_sum[t].add(mem[v]);
-      total.add(mem[v]);
+      total.add(m);
     }
     per_inst = nd;
   }
@@ -76,16 +103,17 @@ __device__ uint32_t place_default_stream(const OpscDag& d, const OpscPlaceSpec& 
       return OPSC_W_FLEET_EXHAUSTED;
     used += (k_base - 1) * per_inst;
     for (int inst = 2; inst <= k_base; ++inst)
-      for (int i = 0; i < n; ++i) total.add(mem[order[i]]);
+      for (int i = 0; i < n; ++i) total.add(S.mem[S.order[i]]);
   }
   // extra replicas on dedicated devices, heaviest op_latency first (placement.py:388-396, 482-490)
   for (int i = 0; i < n; ++i) {
-    const int v = xord[i];
+    const int v = S.xord[i];
+    const double m = S.mem[v];
     for (int k = k_base + 1; k <= c[v * 3 + 1]; ++k) {
       if (used >= pl.n_devices) return OPSC_W_FLEET_EXHAUSTED;
       const int dev = used++;
-      if (mem[v] > cap_of(dev)) return OPSC_W_INFEASIBLE_PLACEMENT;
-      total.add(mem[v]);
+      if (m > cap_of(dev)) return OPSC_W_INFEASIBLE_PLACEMENT;
+      total.add(m);
     }
   }
   *devices = used;
@@ -106,6 +134,7 @@ __global__ void __launch_bounds__(32 * kMatWarps) materialize_kernel(const __gri
                                                                      const __grid_constant__ OpscDecisions out) {
   __shared__ double s_wt[kMatWarps][OPSC_MAX_OPS], s_T[kMatWarps][OPSC_MAX_OPS];
   __shared__ double s_e1[kMatWarps][OPSC_MAX_OPS], s_e2[kMatWarps][OPSC_MAX_OPS];
+  __shared__ MatScratch s_scr[kMatWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int w = blockIdx.x * kMatWarps + warp;
   if (w >= win.n) return;
@@ -156,7 +185,12 @@ __global__ void __launch_bounds__(32 * kMatWarps) materialize_kernel(const __gri
     const double t = op_latency(d, ph, v, b, L, p);
     const double t_eff = (t * (double)r) / (double)r;
     const double mu = 1.0 / (t_eff * layers), lam = qps / (double)b;
-    const double wait = lam < (double)r * mu ? expected_wait(lam, mu, r) : OPSC_INF;
+    // the wait only enters fl(wait * layers + t_eff * layers): wait_for_sum
+    // against t_eff gives the same bits (a W below 2^-56 t_eff scales to
+    // below half an ulp of t_eff * layers)
+    const double wait = lam < (double)r * mu
+                            ? wait_for_sum(r, lam / ((double)r * mu), (double)r * mu - lam, t_eff)
+                            : OPSC_INF;
     const double wl = wait * layers, sl = t_eff * layers;
     s_e1[warp][v] = ((pl.alpha * (double)p) * (double)r) * (wl + sl);
     s_e2[warp][v] = pl.beta * sl;
@@ -164,16 +198,18 @@ __global__ void __launch_bounds__(32 * kMatWarps) materialize_kernel(const __gri
   const bool all = __all_sync(0xffffffffu, stable);
   st = __reduce_or_sync(0xffffffffu, st);
   __syncwarp();
+  MatScratch& S = s_scr[warp];
+  if (feas) place_prepare(d, c, s_T[warp], L, S, lane);
   if (lane != 0) return;
   int obj = 0;
   for (int v = 0; v < n; ++v) obj += (int)c[v * 3] * (int)c[v * 3 + 1];
   out.objective[w] = obj;
-  if (all) out.latency[w] = critical_path_lex(d, s_wt[warp], out.path + (size_t)w * n);
+  if (all) out.latency[w] = critical_path_lex(d, s_wt[warp], out.path + (size_t)w * n, S.val, S.parent);
   st |= st0;
   if (feas) {
     int dev = 0;
     double mem = 0.0;
-    const uint32_t e = place_default_stream(d, pl, c, s_T[warp], L, &dev, &mem);
+    const uint32_t e = place_default_stream(pl, c, n, S, &dev, &mem);
     st |= e;
     if (!e) {
       out.devices[w] = dev;

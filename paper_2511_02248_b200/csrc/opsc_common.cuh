@@ -114,10 +114,11 @@ __device__ __forceinline__ bool cp_seq_less(const int8_t* a, int la, const int8_
   return la < lb;
 }
 
-static __device__ __noinline__ double critical_path_lex(const OpscDag& d, const double* wt, int8_t* path_out) {
+// val / parent: caller scratch (shared memory in K4, where cold local
+// memory would cost an L2 round trip per access of a one-shot serial walk).
+static __device__ __noinline__ double critical_path_lex(const OpscDag& d, const double* wt, int8_t* path_out,
+                                                        double* val, int8_t* parent) {
   const int n = d.n_ops;
-  double val[OPSC_MAX_OPS];
-  int8_t parent[OPSC_MAX_OPS];
   for (int i = 0; i < n; ++i) {
     const int v = d.topo[i];
     uint32_t pm = d.pred_mask[v];
@@ -163,10 +164,18 @@ static __device__ __noinline__ double critical_path_lex(const OpscDag& d, const 
       top = val[s];
     }
   }
-  int8_t buf[OPSC_MAX_OPS];
-  const int len = cp_path_of(parent, tv, buf);
-  for (int i = 0; i < n; ++i) path_out[i] = i < len ? buf[i] : (int8_t)-1;
+  int len = 0;
+  for (int u = tv; u >= 0; u = parent[u]) ++len;
+  int i = len;
+  for (int u = tv; u >= 0; u = parent[u]) path_out[--i] = (int8_t)u;
+  for (int k = len; k < n; ++k) path_out[k] = (int8_t)-1;
   return top;
+}
+
+static __device__ __forceinline__ double critical_path_lex(const OpscDag& d, const double* wt, int8_t* path_out) {
+  double val[OPSC_MAX_OPS];
+  int8_t parent[OPSC_MAX_OPS];
+  return critical_path_lex(d, wt, path_out, val, parent);
 }
 
 struct Pred {
@@ -222,9 +231,13 @@ struct PySum {
   __device__ void reset() { f = 0.0; c = 0.0; started = false; }
   __device__ void add(double x) {
     if (!started) { f = 0.0 + x; c = 0.0; started = true; return; }
+    // both compensation terms, then a select: the same ops as the
+    // reference's branch, but the f -> t chain (one DADD per element) is the
+    // only serial dependency left (long replica sums in K4 / K6)
     const double t = f + x;
-    if (fabs(f) >= fabs(x)) c += (f - t) + x;
-    else c += (x - t) + f;
+    const double d1 = (f - t) + x;
+    const double d2 = (x - t) + f;
+    c += fabs(f) >= fabs(x) ? d1 : d2;
     f = t;
   }
   __device__ double value() const {
