@@ -24,6 +24,8 @@ struct MatScratch {
   double val[OPSC_MAX_OPS];
   double ds_f[OPSC_MAX_OPS], ds_c[OPSC_MAX_OPS];  // per-device PySum state (Neumaier)
   int order[OPSC_MAX_OPS], xord[OPSC_MAX_OPS], inst_dev[OPSC_MAX_OPS];
+  int cp[OPSC_MAX_OPS], cr[OPSC_MAX_OPS], cb[OPSC_MAX_OPS];  // decided (P, R, B), loaded once by the lanes
+  double ratio[OPSC_MAX_OPS];
   int k_base;
   int8_t parent[OPSC_MAX_OPS];
 };
@@ -32,25 +34,26 @@ struct MatScratch {
 // per replica, and the two stable sorts as ranks -- (-(weight_mem/P), id)
 // for base instances and (-op_latency, id) for extra replicas
 // (placement.py:358-396, 465-491).
-__device__ __forceinline__ void place_prepare(const OpscDag& d, const int16_t* c, const double* T, int L,
-                                              MatScratch& S, int lane) {
+__device__ __forceinline__ void place_prepare(const OpscDag& d, const double* T, int L, MatScratch& S, int lane) {
   const int n = d.n_ops;
   int kb = 1 << 30;
+  if (lane < n) S.ratio[lane] = -(d.weight_mem[lane] / (double)S.cp[lane]);
+  __syncwarp();
   if (lane < n) {
     const int v = lane;
-    S.mem[v] = op_memory(d, v, c[v * 3], c[v * 3 + 2], L);
-    const double rv = -(d.weight_mem[v] / (double)c[v * 3]);
+    S.mem[v] = op_memory(d, v, S.cp[v], S.cb[v], L);
+    const double rv = S.ratio[v];
     const double tv = -T[v];
     int r1 = 0, r2 = 0;
     for (int u = 0; u < n; ++u) {
-      const double ru = -(d.weight_mem[u] / (double)c[u * 3]);
+      const double ru = S.ratio[u];
       const double tu = -T[u];
       r1 += ru < rv || (ru == rv && u < v);
       r2 += tu < tv || (tu == tv && u < v);
     }
     S.order[r1] = v;
     S.xord[r2] = v;
-    kb = c[v * 3 + 1];
+    kb = S.cr[v];
   }
   kb = __reduce_min_sync(0xffffffffu, kb);
   if (lane == 0) S.k_base = kb;
@@ -58,8 +61,8 @@ __device__ __forceinline__ void place_prepare(const OpscDag& d, const int16_t* c
 }
 
 // default_stream_place (lane 0, sequential as the reference); returns 0 or an error bit
-__device__ uint32_t place_default_stream(const OpscPlaceSpec& pl, const int16_t* c, int n, MatScratch& S,
-                                         int* devices, double* memory) {
+__device__ uint32_t place_default_stream(const OpscPlaceSpec& pl, int n, MatScratch& S, int* devices,
+                                         double* memory) {
   const int k_base = S.k_base;
   PySum total;
   total.reset();
@@ -109,7 +112,7 @@ __device__ uint32_t place_default_stream(const OpscPlaceSpec& pl, const int16_t*
   for (int i = 0; i < n; ++i) {
     const int v = S.xord[i];
     const double m = S.mem[v];
-    for (int k = k_base + 1; k <= c[v * 3 + 1]; ++k) {
+    for (int k = k_base + 1; k <= S.cr[v]; ++k) {
       if (used >= pl.n_devices) return OPSC_W_FLEET_EXHAUSTED;
       const int dev = used++;
       if (m > cap_of(dev)) return OPSC_W_INFEASIBLE_PLACEMENT;
@@ -161,9 +164,13 @@ __global__ void __launch_bounds__(32 * kMatWarps) materialize_kernel(const __gri
   const bool feas = out.feasible[w] != 0;
   uint32_t st = 0;
   bool stable = true;
+  MatScratch& S = s_scr[warp];
   if (lane < n) {
     const int v = lane;
     const int p = c[v * 3], r = c[v * 3 + 1], b = c[v * 3 + 2];
+    S.cp[v] = p;
+    S.cr[v] = r;
+    S.cb[v] = b;
     const Pred o = predict(d, qps, L, ph, v, p, r, b, &st);
     double* pf = out.pred + ((size_t)w * n + v) * OPSC_PRED_FIELDS;
     pf[0] = o.t; pf[1] = o.lam; pf[2] = o.mu; pf[3] = o.util;
@@ -198,18 +205,17 @@ __global__ void __launch_bounds__(32 * kMatWarps) materialize_kernel(const __gri
   const bool all = __all_sync(0xffffffffu, stable);
   st = __reduce_or_sync(0xffffffffu, st);
   __syncwarp();
-  MatScratch& S = s_scr[warp];
-  if (feas) place_prepare(d, c, s_T[warp], L, S, lane);
+  if (feas) place_prepare(d, s_T[warp], L, S, lane);
   if (lane != 0) return;
   int obj = 0;
-  for (int v = 0; v < n; ++v) obj += (int)c[v * 3] * (int)c[v * 3 + 1];
+  for (int v = 0; v < n; ++v) obj += S.cp[v] * S.cr[v];
   out.objective[w] = obj;
   if (all) out.latency[w] = critical_path_lex(d, s_wt[warp], out.path + (size_t)w * n, S.val, S.parent);
   st |= st0;
   if (feas) {
     int dev = 0;
     double mem = 0.0;
-    const uint32_t e = place_default_stream(pl, c, n, S, &dev, &mem);
+    const uint32_t e = place_default_stream(pl, n, S, &dev, &mem);
     st |= e;
     if (!e) {
       out.devices[w] = dev;
