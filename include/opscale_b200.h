@@ -224,6 +224,14 @@ OPSC_API int opsc_menu_build(const OpscDag* dag, const OpscGrid* grid, OpscWindo
 OPSC_API int opsc_stability_check(const OpscDag* dag, const OpscGrid* grid, OpscWindows win,
                          uint32_t* status, void* stream);
 
+/* Diagnostic (not on the planning path): per window, ADDS to count_out the
+ * number of candidates whose canonical critical-path latency is finite and
+ * within band_ulps ulps of slo -- the only ones whose feasibility could
+ * depend on the reference's frozenset-ordered sum() (autoscaler.py:792-794).
+ * count_out must be zeroed by the caller. */
+OPSC_API int opsc_compose_boundary(const OpscDag* dag, const OpscGrid* grid, OpscWindows win,
+                                   const double* menu_w, double band_ulps, int64_t* count_out, void* stream);
+
 /* Exhaustive compose + SLO mask + lexicographic argmin over the shard
  * [shard/n_shards] of every window's candidate space. key_out must be
  * initialised to OPSC_KEY_INFEASIBLE (opsc_fill_keys); results are min-merged. */

@@ -24,6 +24,7 @@ EXPORTS = (
     "opsc_menu_fallback",
     "opsc_decode_decisions", "opsc_model_grid", "opsc_materialize", "opsc_ctx_create",
     "opsc_ctx_destroy", "opsc_plan_windows_host", "opsc_ctx_last_launches", "opsc_ctx_last_ms", "opsc_fp64_peak",
+    "opsc_compose_boundary",
     "opsc_candidate_probe", "opsc_greedy", "opsc_windowize", "opsc_windowize_workspace",
     "opsc_greedy_state_bytes", "opsc_greedy_phase", "opsc_model_table_bytes",
     "opsc_model_grid_table", "opsc_place_shared_workspace", "opsc_place_shared",
@@ -76,6 +77,7 @@ def load():
                                 C.c_size_t, P], C.c_int),
             "opsc_ctx_last_launches": ([P, P], C.c_int),
             "opsc_ctx_last_ms": ([P, P], C.c_int),
+            "opsc_compose_boundary": ([P, P, abi.OpscWindows, P, C.c_double, P, P], C.c_int),
             "opsc_fp64_peak": ([I, P, P, P], C.c_int),
             "opsc_candidate_probe": ([I, I, P, P, P], C.c_int),
             "opsc_ipc_alloc": ([C.c_size_t, P, P], C.c_int),

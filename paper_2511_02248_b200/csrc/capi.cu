@@ -271,6 +271,16 @@ int opsc_compose_argmin(const OpscDag* dag, const OpscGrid* grid, OpscWindows wi
                                   (unsigned long long*)key_out, (cudaStream_t)stream));
 }
 
+int opsc_compose_boundary(const OpscDag* dag, const OpscGrid* grid, OpscWindows win, const double* menu_w,
+                          double band_ulps, int64_t* count_out, void* stream) {
+  if (!valid_dag(dag) || !grid || !count_out || !(band_ulps >= 0.0)) return OPSC_ERR_ARG;
+  ComposeCfg c;
+  const int rc = compose_setup(*dag, *grid, win.n, 0, 1, &c);
+  if (rc != OPSC_OK) return rc;
+  return from_cuda(launch_compose_boundary(c, *grid, win.n, menu_w, win.slo, win.qps, band_ulps,
+                                           (unsigned long long*)count_out, (cudaStream_t)stream));
+}
+
 int opsc_compose_argmin_peers(const OpscDag* dag, const OpscGrid* grid, OpscWindows win, const double* menu_w,
                               int32_t shard, int32_t n_shards, int64_t* const* peer_keys, int32_t n_peers,
                               void* stream) {

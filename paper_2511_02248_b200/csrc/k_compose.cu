@@ -188,17 +188,28 @@ __device__ __forceinline__ void cta_min_commit(unsigned long long best, int w, u
 // resident), the same critical-path DP (max over predecessors, then + own
 // weight, topological order) and the same key. Literal and exact, slower per
 // candidate; only reachable with few operators (the reference's 1e7 guard).
+//
+// COUNT = true is the boundary diagnostic (opsc_compose_boundary): instead of
+// the argmin it counts the candidates whose canonical latency lies within
+// `band` of slo, i.e. those whose feasibility could depend on the reference's
+// own summation order (a frozenset-ordered, Neumaier-compensated sum(),
+// autoscaler.py:792-794). A zero count certifies the window's decision
+// independent of that order.
+template <bool COUNT>
 __global__ void __launch_bounds__(kComposeThreads)
 compose_flat_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ OpscGrid g,
                     const double* __restrict__ menu_w, const double* __restrict__ slo_w,
                     const double* __restrict__ qps_w, unsigned long long* __restrict__ key_out,
-                    const __grid_constant__ PeerKeys peers) {
+                    const __grid_constant__ PeerKeys peers, double band_ulps = 0.0) {
   __shared__ unsigned long long warp_best[kComposeThreads / 32];
   const int w = blockIdx.x / c.blocks_per_window;
   const int bw = blockIdx.x - w * c.blocks_per_window;
   const double slo = fmin(slo_w[w], 1.7976931348623157e308);
   const double* mw = menu_w + (size_t)w * c.E;
   unsigned long long best = kSentinel;
+  // band = band_ulps ulps of slo (ulp from the exponent of slo)
+  const double band = COUNT ? band_ulps * (nextafter(slo, OPSC_INF) - slo) : 0.0;
+  unsigned long long near = 0;
   if (qps_w[w] > 0.0) {
     const unsigned long long step = (unsigned long long)c.blocks_per_window * kComposeThreads;
     for (unsigned long long idx = c.flo + (unsigned long long)bw * kComposeThreads + threadIdx.x; idx < c.fhi;
@@ -227,11 +238,18 @@ compose_flat_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant_
         val[pos] = dp_in(c.pmask[pos], val) + wt;
         if (c.sinkmask >> pos & 1u) lat = fmax(lat, val[pos]);
       }
-      if (lat <= slo) {
+      if (COUNT) {
+        near += lat < OPSC_INF && fabs(lat - slo) <= band;
+      } else if (lat <= slo) {
         const unsigned long long key = ((unsigned long long)cost << OPSC_KEY_LEX_BITS) + lex;
         best = key < best ? key : best;
       }
     }
+  }
+  if (COUNT) {
+    for (int o = 16; o > 0; o >>= 1) near += __shfl_xor_sync(0xffffffffu, near, o);
+    if ((threadIdx.x & 31) == 0 && near) atomicAdd(&key_out[w], near);
+    return;
   }
   cta_min_commit(best, w, key_out, peers, warp_best);
 }
@@ -657,7 +675,7 @@ cudaError_t launch_compose(const ComposeCfg& c, const OpscGrid& g, int n_windows
     if (c.fhi <= c.flo) return cudaSuccess;
     const long long blocks = (long long)n_windows * c.blocks_per_window;
     if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    compose_flat_kernel<<<(unsigned)blocks, kComposeThreads, 0, s>>>(c, g, menu_w, slo, qps, key, pk);
+    compose_flat_kernel<false><<<(unsigned)blocks, kComposeThreads, 0, s>>>(c, g, menu_w, slo, qps, key, pk);
     return cudaGetLastError();
   }
   switch (c.nj) {
@@ -670,6 +688,30 @@ cudaError_t launch_compose(const ComposeCfg& c, const OpscGrid& g, int n_windows
     case 32: return launch_nj<32>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
     default: return launch_nj<0>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
   }
+}
+
+// Boundary diagnostic over the whole candidate space (flat kernel, literal).
+cudaError_t launch_compose_boundary(const ComposeCfg& c0, const OpscGrid& g, int n_windows, const double* menu_w,
+                                    const double* slo, const double* qps, double band_ulps,
+                                    unsigned long long* count, cudaStream_t s) {
+  if (n_windows <= 0) return cudaSuccess;
+  ComposeCfg c = c0;
+  unsigned long long space = 1;
+  for (int pos = 0; pos < c.n; ++pos) space *= (unsigned long long)c.m[pos];
+  c.flo = 0;
+  c.fhi = space;
+  const unsigned long long per_cta = (unsigned long long)kComposeThreads * 256ull;
+  unsigned long long bpw = (space + per_cta - 1) / per_cta;
+  const unsigned long long cap = 148ull * 16ull * 8ull / (unsigned long long)n_windows + 1ull;
+  bpw = bpw < 1 ? 1 : (bpw > cap ? cap : bpw);
+  c.blocks_per_window = (int)bpw;
+  const long long blocks = (long long)n_windows * c.blocks_per_window;
+  if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  PeerKeys pk;
+  memset(&pk, 0, sizeof(pk));
+  compose_flat_kernel<true><<<(unsigned)blocks, kComposeThreads, 0, s>>>(c, g, menu_w, slo, qps, count, pk,
+                                                                          band_ulps);
+  return cudaGetLastError();
 }
 
 }  // namespace opsc

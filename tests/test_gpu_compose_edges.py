@@ -177,3 +177,49 @@ def test_level_splits_vs_oracle(nat_loaded, orc, il, monkeypatch):
     got = _device_compose(nat, prob, grid, win, mw)
     assert (got == want).all(), (il, got, want)
     assert (got != abi.KEY_INFEASIBLE).any()
+
+
+def test_boundary_count_vs_numpy(nat_loaded, orc):
+    """opsc_compose_boundary counts the candidates within `band` ulps of slo:
+    checked against a numpy enumeration of the same crafted tie menus (chain
+    DP = plain adds in topological order)."""
+    import itertools
+
+    import torch
+
+    from paper_2511_02248_b200 import _native as nat
+    rng = np.random.default_rng(5)
+    prob = _dag(4, "chain")
+    grid = tables.pack_grid(prob, model.AutoscaleParams(slo=1.0),
+                            model.BruteForceBounds(r_max=3, b_max=2, parallelism=(1, 2)))
+    slos = [1.0, 0.7, 0.3 + 1e-13]
+    win = tables.window_arrays(np.full(3, 10.0), np.full(3, 512), 0, 1.0)
+    win.slo[:] = slos
+    mw = _menus(rng, prob, grid, slos, "tie")
+    mw[:, ::7] = np.inf  # unstable entries never count
+    dev = torch.device("cuda:0")
+    t = {k: torch.from_numpy(np.ascontiguousarray(getattr(win, k))).to(dev)
+         for k in ("qps", "seq_len", "phase", "slo", "eps")}
+    dw = abi.OpscWindows()
+    dw.n = 3
+    for k in t:
+        setattr(dw, k, t[k].data_ptr())
+    mwd = torch.from_numpy(mw).to(dev)
+    topo = [int(v) for v in prob.table.topo[:prob.n_ops]]
+    off = [grid.menu_off[v] for v in range(prob.n_ops + 1)]
+    for band in (0.0, 3.0, 40.0):
+        cnt = torch.zeros(3, dtype=torch.int64, device=dev)
+        nat.check(nat.load().opsc_compose_boundary(nat.ref(prob.table), nat.ref(grid), dw, mwd.data_ptr(), band,
+                                                   cnt.data_ptr(), torch.cuda.current_stream().cuda_stream),
+                  "boundary")
+        got = cnt.cpu().numpy()
+        for w, slo in enumerate(slos):
+            ulp = np.nextafter(slo, np.inf) - slo
+            want = 0
+            for combo in itertools.product(*[range(off[v], off[v + 1]) for v in topo]):
+                lat = 0.0
+                for e in combo:
+                    lat = lat + mw[w, e]
+                want += bool(np.isfinite(lat) and abs(lat - slo) <= band * ulp)
+            assert got[w] == want, (band, w, got[w], want)
+    assert got.sum() > 0
