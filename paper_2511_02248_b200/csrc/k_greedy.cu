@@ -17,7 +17,10 @@
 
 namespace opsc {
 
-constexpr int kGreedyThreads = 128;
+#ifndef OPSC_GREEDY_THREADS
+#define OPSC_GREEDY_THREADS 128
+#endif
+constexpr int kGreedyThreads = OPSC_GREEDY_THREADS;
 constexpr int kMaxMoves = 32 * OPSC_MAX_P * 2;  // b_max <= 64 per op in this kernel
 
 struct GreedyArgs {
