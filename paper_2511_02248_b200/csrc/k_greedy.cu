@@ -21,7 +21,8 @@ namespace opsc {
 #define OPSC_GREEDY_THREADS 128
 #endif
 constexpr int kGreedyThreads = OPSC_GREEDY_THREADS;
-constexpr int kMaxMoves = 32 * OPSC_MAX_P * 2;  // b_max <= 64 per op in this kernel
+constexpr int kMaxMoves = 32 * OPSC_MAX_P * 2;  // move-set chunk (larger sets run in chunks)
+constexpr int kInitChunk = 64;                   // init_configs B chunk per operator
 
 struct GreedyArgs {
   OpscDag d;
@@ -37,9 +38,11 @@ struct GShared {
   // move results
   double m_lat[kMaxMoves], m_soj[kMaxMoves], m_wt[kMaxMoves];
   uint8_t m_ok[kMaxMoves];
-  // init scratch
-  double i_soj[OPSC_MAX_OPS][64];
-  int i_r[OPSC_MAX_OPS][64];
+  // init scratch (one B chunk) and the running per-op argmin over chunks
+  double i_soj[OPSC_MAX_OPS][kInitChunk];
+  int i_r[OPSC_MAX_OPS][kInitChunk];
+  double i_bs[OPSC_MAX_OPS];
+  int i_bb[OPSC_MAX_OPS], i_br[OPSC_MAX_OPS];
   int chosen[OPSC_MAX_OPS];
   // control
   int op, applied, flag;
@@ -130,22 +133,26 @@ __device__ void eval_full(GShared& S, const OpscDag& d, double qps, int L, int p
   __syncthreads();
 }
 
-// Evaluate the move set of `op` at replica count r_new over B in [b_lo, b_max]
-// and all distinct P (all threads; ends synchronised).
+// Evaluate moves [m0, m0 + kMaxMoves) of the move set of `op` at replica
+// count r_new (move m = (B = b_lo + m / np, P = pd[m % np]), all distinct P)
+// into the scratch slots m - m0 (all threads; ends synchronised). Returns
+// the size of the whole set; sets larger than kMaxMoves run in chunks.
 __device__ int eval_moves(GShared& S, const GreedyArgs& a, int op, int r_new, int b_lo, double qps, int L,
-                          int ph) {
+                          int ph, int m0) {
   const int np = S.np_d[op];
   const int nb = a.s.b_max[op] - b_lo + 1;
   const int M = nb * np;
-  for (int m = threadIdx.x; m < M; m += blockDim.x) {
+  const int m1 = min(M, m0 + kMaxMoves);
+  for (int m = m0 + threadIdx.x; m < m1; m += blockDim.x) {
     const int b = b_lo + m / np, p = S.pd[op][m % np];
     uint32_t st = 0;
     const Pred o = predict<true>(a.d, qps, L, ph, op, p, r_new, b, &st);
-    S.m_ok[m] = o.stable;
+    const int i = m - m0;
+    S.m_ok[i] = o.stable;
     if (o.stable) {
-      S.m_wt[m] = weight(o, a.d.layer_count[op]);
-      S.m_soj[m] = o.wait + o.service;
-      S.m_lat[m] = trial_latency(a.d, S.wt, op, S.m_wt[m]);
+      S.m_wt[i] = weight(o, a.d.layer_count[op]);
+      S.m_soj[i] = o.wait + o.service;
+      S.m_lat[i] = trial_latency(a.d, S.wt, op, S.m_wt[i]);
     }
     if (st) atomicOr(&S.st, st);
   }
@@ -210,15 +217,25 @@ __device__ void block_min(PK (&x)[NK]) {
   __syncthreads();
 }
 
-// thread 0: apply move m of `op` (new r), recompute the critical path
-__device__ void apply_move(GShared& S, const OpscDag& d, int op, int m, int r_new, int b_lo) {
+// thread 0: apply move m of `op` (new r), recompute the critical path. The
+// move's weight / sojourn come from the scratch when its chunk is the last
+// one evaluated, else they are recomputed (same predict, same bits).
+__device__ void apply_move(GShared& S, const GreedyArgs& a, int op, int m, int r_new, int b_lo, int m0, double qps,
+                           int L, int ph) {
   const int np = S.np_d[op];
   S.p[op] = S.pd[op][m % np];
   S.b[op] = b_lo + m / np;
   S.r[op] = r_new;
-  S.wt[op] = S.m_wt[m];
-  S.soj[op] = S.m_soj[m];
-  S.lat = crit_path(d, S.wt, S.path);
+  if (m >= m0 && m < m0 + kMaxMoves) {
+    S.wt[op] = S.m_wt[m - m0];
+    S.soj[op] = S.m_soj[m - m0];
+  } else {
+    uint32_t st = 0;
+    const Pred o = predict<true>(a.d, qps, L, ph, op, S.p[op], r_new, S.b[op], &st);
+    S.wt[op] = weight(o, a.d.layer_count[op]);
+    S.soj[op] = o.wait + o.service;
+  }
+  S.lat = crit_path(a.d, S.wt, S.path);
   S.stable = 1;
 }
 
@@ -240,16 +257,19 @@ __device__ void upscale_step(GShared& S, const GreedyArgs& a, const OpscDecision
     __syncthreads();
     return;
   }
-  const int M = eval_moves(S, a, op, cur_r + 1, 1, qps, L, ph);
   const int np = S.np_d[op];
   const int base = objective(S, a.d.n_ops);
   const double target = slo - eps, cur_lat = S.lat;
   PK k[3];  // ach, ach2, imp
   for (int i = 0; i < 3; ++i) k[i].m = -1;
-  for (int m = threadIdx.x; m < M; m += blockDim.x) {
-    if (!S.m_ok[m]) continue;
+  int M = 0, m0 = 0;
+  do {
+    if (m0 > 0) __syncthreads();  // previous chunk's scratch fully read
+    M = eval_moves(S, a, op, cur_r + 1, 1, qps, L, ph, m0);
+  for (int m = m0 + threadIdx.x; m < min(M, m0 + kMaxMoves); m += blockDim.x) {
+    if (!S.m_ok[m - m0]) continue;
     const int b = 1 + m / np, p = S.pd[op][m % np];
-    const double lat = S.m_lat[m];
+    const double lat = S.m_lat[m - m0];
     const int obj = base - cur_p * cur_r + p * (cur_r + 1);
     const PK reach = {(double)obj, lat, 0, b, p, m};
     if (lat <= target && pk_less(reach, k[0])) k[0] = reach;
@@ -262,12 +282,15 @@ __device__ void upscale_step(GShared& S, const GreedyArgs& a, const OpscDecision
       if (pk_less(eff, k[2])) k[2] = eff;
     }
   }
+    m0 += kMaxMoves;
+  } while (m0 < M);
+  m0 -= kMaxMoves;  // the chunk still in the scratch
   block_min<3>(k);
   if (threadIdx.x == 0) {
     const int m = k[0].m >= 0 ? k[0].m : (!headroom && k[1].m >= 0) ? k[1].m : k[2].m;
     S.applied = m >= 0;
     if (m >= 0) {
-      apply_move(S, a.d, op, m, cur_r + 1, 1);
+      apply_move(S, a, op, m, cur_r + 1, 1, m0, qps, L, ph);
       push_trace(S, out, w, headroom ? OPSC_ACT_HEADROOM : OPSC_ACT_UPSCALE, op, S.r[op], S.b[op], S.p[op],
                  S.lat, objective(S, a.d.n_ops));
     }
@@ -289,26 +312,32 @@ __device__ void downscale_step(GShared& S, const GreedyArgs& a, const OpscDecisi
     __syncthreads();
     return;
   }
-  const int M = eval_moves(S, a, op, cur_r - 1, cur_b, qps, L, ph);
   const int np = S.np_d[op];
   const int base = objective(S, a.d.n_ops);
   const double bound = slo - eps;
   PK k[1];
   k[0].m = -1;
-  for (int m = threadIdx.x; m < M; m += blockDim.x) {
-    if (!S.m_ok[m] || S.m_lat[m] > bound) continue;
-    const int b = cur_b + m / np, p = S.pd[op][m % np];
-    const int obj = base - cur_p * cur_r + p * (cur_r - 1);
-    if (obj >= base) continue;
-    const PK c = {(double)obj, 0.0, 0, b, p, m};
-    if (pk_less(c, k[0])) k[0] = c;
-  }
+  int M = 0, m0 = 0;
+  do {
+    if (m0 > 0) __syncthreads();  // previous chunk's scratch fully read
+    M = eval_moves(S, a, op, cur_r - 1, cur_b, qps, L, ph, m0);
+    for (int m = m0 + threadIdx.x; m < min(M, m0 + kMaxMoves); m += blockDim.x) {
+      if (!S.m_ok[m - m0] || S.m_lat[m - m0] > bound) continue;
+      const int b = cur_b + m / np, p = S.pd[op][m % np];
+      const int obj = base - cur_p * cur_r + p * (cur_r - 1);
+      if (obj >= base) continue;
+      const PK c = {(double)obj, 0.0, 0, b, p, m};
+      if (pk_less(c, k[0])) k[0] = c;
+    }
+    m0 += kMaxMoves;
+  } while (m0 < M);
+  m0 -= kMaxMoves;
   block_min<1>(k);
   if (threadIdx.x == 0) {
     const int best = k[0].m;
     S.applied = best >= 0;
     if (best >= 0) {
-      apply_move(S, a.d, op, best, cur_r - 1, cur_b);
+      apply_move(S, a, op, best, cur_r - 1, cur_b, m0, qps, L, ph);
       push_trace(S, out, w, OPSC_ACT_DOWNSCALE, op, S.r[op], S.b[op], S.p[op], S.lat,
                  objective(S, a.d.n_ops));
     }
@@ -464,9 +493,14 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
   // ---- init_configs (:254-294): per parallelism rank, (op, B) pairs in parallel
   int max_np = 0;
   for (int v = 0; v < n; ++v) max_np = max(max_np, a.s.n_p[v]);
+  int max_b = 0;
+  for (int v = 0; v < n; ++v) max_b = max(max_b, a.s.b_max[v]);
   for (int pi = 0; pi < max_np; ++pi) {
-    for (int k = threadIdx.x; k < n * 64; k += blockDim.x) {
-      const int v = k / 64, b = k % 64 + 1;
+    for (int v = threadIdx.x; v < n; v += blockDim.x) S.i_bb[v] = -1;
+    for (int b0 = 0; b0 < max_b; b0 += kInitChunk) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < n * kInitChunk; k += blockDim.x) {
+      const int v = k / kInitChunk, b = b0 + k % kInitChunk + 1;
       if (S.chosen[v] || pi >= a.s.n_p[v] || b > a.s.b_max[v]) continue;
       const int p = a.s.p_vals[v][pi];
       const double t = op_latency(d, ph, v, b, L, p);
@@ -475,33 +509,38 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
       if (tl == 0.0) st |= OPSC_W_ZERO_DIVISION;
       const double mu = 1.0 / tl, lam = qps / (double)b;
       const int r = strict_min_replicas(lam, mu, a.s.r_cap);
-      S.i_r[v][b - 1] = r;
+      const int j = b - b0 - 1;
+      S.i_r[v][j] = r;
       if (r >= 0) {
         const double util = lam / ((double)r * mu);
         if (util >= 1.0 || util <= 0.0) st |= OPSC_W_UNSTABLE_ROUNDING;
         const double service = t / (double)b;  // sojourn key: wait only inside wait + service
-        S.i_soj[v][b - 1] = wait_for_sum(r, lam / ((double)r * mu), (double)r * mu - lam, service) + service;
+        S.i_soj[v][j] = wait_for_sum(r, lam / ((double)r * mu), (double)r * mu - lam, service) + service;
       }
       if (st) atomicOr(&S.st, st);
     }
     __syncthreads();
+    // running argmin over the chunks: min sojourn, ties to the lowest B (strict <, ascending B)
     for (int v = threadIdx.x; v < n; v += blockDim.x) {
       if (S.chosen[v] || pi >= a.s.n_p[v]) continue;
-      int bb = -1;
-      double bs = 0.0;
-      for (int b = 1; b <= a.s.b_max[v]; ++b) {
-        if (S.i_r[v][b - 1] < 0) continue;
-        if (bb < 0 || S.i_soj[v][b - 1] < bs) {
-          bb = b;
-          bs = S.i_soj[v][b - 1];
+      for (int b = b0 + 1; b <= min(a.s.b_max[v], b0 + kInitChunk); ++b) {
+        const int j = b - b0 - 1;
+        if (S.i_r[v][j] < 0) continue;
+        if (S.i_bb[v] < 0 || S.i_soj[v][j] < S.i_bs[v]) {
+          S.i_bb[v] = b;
+          S.i_bs[v] = S.i_soj[v][j];
+          S.i_br[v] = S.i_r[v][j];
         }
       }
-      if (bb > 0) {
-        S.p[v] = a.s.p_vals[v][pi];
-        S.b[v] = bb;
-        S.r[v] = S.i_r[v][bb - 1];
-        S.chosen[v] = 1;
-      }
+    }
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < n; v += blockDim.x) {
+      if (S.chosen[v] || pi >= a.s.n_p[v] || S.i_bb[v] < 0) continue;
+      S.p[v] = a.s.p_vals[v][pi];
+      S.b[v] = S.i_bb[v];
+      S.r[v] = S.i_br[v];
+      S.chosen[v] = 1;
     }
     __syncthreads();
   }
@@ -605,7 +644,7 @@ cudaError_t launch_greedy(const OpscDag& d, const OpscGreedySpec& s, OpscWindows
   if (w.n <= 0) return cudaSuccess;
   if (phase < 0 || phase > 2 || (phase != 0 && !save)) return cudaErrorInvalidValue;
   for (int v = 0; v < d.n_ops; ++v)
-    if (s.b_max[v] < 1 || s.b_max[v] > 64 || s.n_p[v] < 1) return cudaErrorInvalidValue;
+    if (s.b_max[v] < 1 || s.n_p[v] < 1) return cudaErrorInvalidValue;
   GreedyArgs a;
   a.d = d;
   a.s = s;

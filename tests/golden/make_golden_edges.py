@@ -88,9 +88,15 @@ def model_cases():
 
 
 def greedy_cases():
+    # large batch bounds: init_configs over B in several 64-wide chunks, and
+    # move sets (B x distinct P) past one 512-move chunk
+    big = [dict(name=f"edge/greedy_big_b/{b}/{ph}", scenario="cfg1",
+                point=dict(qps=q, seq_len=1024, phase=ph), params=dict(slo=slo, b_max=b, epsilon=slo * 0.05))
+           for b, ph, q, slo in ((100, "prefill", 120.0, 0.3), (200, "decode", 3000.0, 0.05),
+                                 (160, "prefill", 400.0, 0.2))]
     return [dict(name=f"edge/slo_inf/{cfg}/{ph}", scenario=cfg,
                  point=dict(qps=q, seq_len=2048, phase=ph), params=dict(slo=INF))
-            for cfg, q in (("cfg1", 30.0), ("cfg2", 12.0)) for ph in ("prefill", "decode")] + dict_cases(False)
+            for cfg, q in (("cfg1", 30.0), ("cfg2", 12.0)) for ph in ("prefill", "decode")] + dict_cases(False) + big
 
 
 def case_inputs(c):
