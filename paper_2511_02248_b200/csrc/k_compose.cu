@@ -254,12 +254,15 @@ compose_flat_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant_
   cta_min_commit(best, w, key_out, peers, warp_best);
 }
 
-template <int NJ, bool CHAIN>
+// MODE: 0 generic DAG, 1 CHAIN (j's only predecessor is k, k no sink),
+// 2 path DAG (every position fed by the previous one only, one sink).
+template <int NJ, int MODE>
 __global__ void __launch_bounds__(kComposeThreads, OPSC_COMPOSE_MINB)
 compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ OpscGrid g,
                const double* __restrict__ menu_w, const double* __restrict__ slo_w,
                const double* __restrict__ qps_w, unsigned long long* __restrict__ key_out,
                const __grid_constant__ PeerKeys peers) {
+  constexpr bool CHAIN = MODE >= 1, PATH = MODE == 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ unsigned long long warp_best[kComposeThreads / 32];
   __shared__ __align__(8) unsigned long long tma_bar;
@@ -414,16 +417,25 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
     const bool k_to_j = (c.pmask[jp] & kmask) != 0;
     const bool k_sink = (c.sinkmask & kmask) != 0;
 
-    // Path DAGs (every position's only predecessor is the previous one, one
-    // sink): the middle levels run as an odometer with their prefix values in
-    // registers -- val[pos] = val[pos-1] + w, the DP's own adds in the same
-    // order -- instead of re-decoding the digits with divisions and re-running
-    // the DP through local memory for every middle index.
+    // Middle levels (<= kOdoLevels of them) run as an odometer with their DP
+    // values in registers instead of re-decoding the digits with divisions
+    // and re-running the DP through local memory for every middle index. A
+    // dp_in is a max over predecessors (exact, order-free), so it splits into
+    // the outer predecessors' part, fixed per thread, and the middle ones'.
     const int nmid = kp - nout;
-    const bool odo = CHAIN && c.path_dag && nmid <= kOdoLevels;
+    const bool odo = nmid <= kOdoLevels;
+    const uint32_t outer = (1u << nout) - 1u;
     int od[kOdoLevels];
+    double o_in[kOdoLevels], mv[kOdoLevels];
 #pragma unroll
-    for (int l = 0; l < kOdoLevels; ++l) od[l] = 0;
+    for (int l = 0; l < kOdoLevels; ++l) {
+      od[l] = 0;
+      mv[l] = 0.0;
+      o_in[l] = (!PATH && odo && l < nmid) ? dp_in(c.pmask[nout + l] & outer, val) : 0.0;
+    }
+    const double o_k = (!PATH && odo) ? dp_in(c.pmask[kp] & outer, val) : 0.0;
+    const double o_j = (!PATH && odo) ? dp_in(c.pmask[jp] & ~kmask & outer, val) : 0.0;
+    const double o_lo = (!PATH && odo) ? dp_in(c.sinkmask & ~(kmask | jmask) & outer, val) : 0.0;
     bool odo_dirty = true;
 
     for (uint32_t mid = 0; mid < c.mid_count; ++mid) {
@@ -443,20 +455,45 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
           }
         }
         odo_dirty = false;
-        // dp_in of a single predecessor: fmax(0.0, val[prev]); no predecessor: 0.0
-        double pv = nout > 0 ? fmax(0.0, val[nout - 1]) : 0.0;
         long long pc = cost0;
         unsigned long long pl = lex0;
+        if constexpr (PATH) {
+          // dp_in of the single predecessor: fmax(0.0, val[prev]); none: 0.0
+          double pv = nout > 0 ? fmax(0.0, val[nout - 1]) : 0.0;
+#pragma unroll
+          for (int l = 0; l < kOdoLevels; ++l) {
+            if (l < nmid) {
+              const int e = c.off[nout + l] + od[l];
+              pv = fmax(0.0, pv + s.w[e]);  // val[pos], then the next position's dp_in
+              pc += s.cost[e];
+              pl += (unsigned long long)od[l] * c.stride[nout + l];
+            }
+          }
+          in_k = pv;
+        } else {
+        in_k = o_k;
+        bj0 = o_j;
+        lo0 = o_lo;
 #pragma unroll
         for (int l = 0; l < kOdoLevels; ++l) {
           if (l < nmid) {
-            const int e = c.off[nout + l] + od[l];
-            pv = fmax(0.0, pv + s.w[e]);  // val[pos], then the next position's dp_in
+            const int pos = nout + l;
+            double in = o_in[l];
+#pragma unroll
+            for (int l2 = 0; l2 < l; ++l2)
+              if (c.pmask[pos] >> (nout + l2) & 1u) in = fmax(in, mv[l2]);
+            const int e = c.off[pos] + od[l];
+            mv[l] = in + s.w[e];
             pc += s.cost[e];
-            pl += (unsigned long long)od[l] * c.stride[nout + l];
+            pl += (unsigned long long)od[l] * c.stride[pos];
+            const uint32_t bit = 1u << pos;
+            if (c.pmask[kp] & bit) in_k = fmax(in_k, mv[l]);
+            if (c.pmask[jp] & ~kmask & bit) bj0 = fmax(bj0, mv[l]);
+            if (c.sinkmask & bit) lo0 = fmax(lo0, mv[l]);
           }
         }
-        in_k = pv;
+        if (CHAIN && !(lo0 <= slo)) in_k = OPSC_INF;  // another sink already misses the SLO
+        }
         cost1 = pc;
         lex1 = pl;
       } else {
@@ -639,20 +676,20 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
   return OPSC_OK;
 }
 
-template <int NJ, bool CHAIN>
+template <int NJ, int MODE>
 static cudaError_t launch_t(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,
                             const double* slo, const double* qps, unsigned long long* key, cudaStream_t s,
                             const PeerKeys& pk) {
   const int mj = c.m[c.n - 1], mk = c.m[c.n - 2];
   const size_t smem = compose_smem_bytes(c.E, mk, mj);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(compose_kernel<NJ, CHAIN>,
+    cudaError_t e = cudaFuncSetAttribute(compose_kernel<NJ, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   const long long blocks = (long long)n_windows * c.blocks_per_window;
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  compose_kernel<NJ, CHAIN><<<(unsigned)blocks, kComposeThreads, smem, s>>>(c, g, menu_w, slo, qps, key, pk);
+  compose_kernel<NJ, MODE><<<(unsigned)blocks, kComposeThreads, smem, s>>>(c, g, menu_w, slo, qps, key, pk);
   return cudaGetLastError();
 }
 
@@ -660,8 +697,9 @@ template <int NJ>
 static cudaError_t launch_nj(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,
                              const double* slo, const double* qps, unsigned long long* key, cudaStream_t s,
                              const PeerKeys& pk) {
-  return c.chain ? launch_t<NJ, true>(c, g, n_windows, menu_w, slo, qps, key, s, pk)
-                 : launch_t<NJ, false>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
+  if (c.path_dag) return launch_t<NJ, 2>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
+  return c.chain ? launch_t<NJ, 1>(c, g, n_windows, menu_w, slo, qps, key, s, pk)
+                 : launch_t<NJ, 0>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
 }
 
 cudaError_t launch_compose(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,
