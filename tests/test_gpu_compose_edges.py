@@ -156,23 +156,30 @@ def test_flat_kernel_large_menus(nat_loaded, orc, shape, r_max, b_max):
     assert (got != abi.KEY_INFEASIBLE).any()
 
 
+_SPLIT_ORACLE = {}
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3"])
 @pytest.mark.parametrize("il", [2, 3, 4, 5, 6])
-def test_level_splits_vs_oracle(nat_loaded, orc, il, monkeypatch):
-    """Every in-thread level count on the 10-op 70B path DAG: il - 2 middle
-    levels run as the register odometer (0..4 of them), the rest are decoded
-    per thread (OPSC_COMPOSE_IL is the compose_setup dev override)."""
+def test_level_splits_vs_oracle(nat_loaded, orc, cfg, il, monkeypatch):
+    """Every in-thread level count on the 10-op 70B path DAG (cfg2, MODE 2)
+    and the 12-op two-source multimodal DAG (cfg3, generic MODE): il - 2
+    middle levels run as the register odometer (0..4 of them), the rest are
+    decoded per thread (OPSC_COMPOSE_IL is the compose_setup dev override)."""
     from paper_2511_02248_b200 import _native as nat
     from paper_2511_02248_b200 import scenarios
-    prob = tables.pack_problem(*scenarios.scenario("cfg2"))
-    g = scenarios.GRIDS["cfg2"]
+    prob = tables.pack_problem(*scenarios.scenario(cfg))
+    g = scenarios.GRIDS[cfg]
     grid = tables.pack_grid(prob, model.AutoscaleParams(slo=1.0), model.BruteForceBounds(**g))
-    tw = scenarios.trace_windows("cfg2")
-    idx = np.arange(0, 60, 6)
+    tw = scenarios.trace_windows(cfg)
+    idx = np.arange(0, 60, 6) if cfg == "cfg2" else np.array([3, 17, 30, 45])
     win = tables.window_arrays(tw["prefill_qps"][idx], tw["prefill_len"][idx], 0, 1.0)
     # SLOs 1x..6x the scenario's, so feasible and infeasible windows mix
-    win.slo[:] = np.linspace(1.0, 6.0, len(idx)) * scenarios.SLO["cfg2"]["prefill"]
-    mw, _ = orc.menus(prob, grid, win)
-    want = orc.compose(prob, grid, win, mw)
+    win.slo[:] = np.linspace(1.0, 6.0, len(idx)) * scenarios.SLO[cfg]["prefill"]
+    if cfg not in _SPLIT_ORACLE:  # the oracle's answer does not depend on the split
+        mw, _ = orc.menus(prob, grid, win)
+        _SPLIT_ORACLE[cfg] = (mw, orc.compose(prob, grid, win, mw))
+    mw, want = _SPLIT_ORACLE[cfg]
     monkeypatch.setenv("OPSC_COMPOSE_IL", str(il))
     got = _device_compose(nat, prob, grid, win, mw)
     assert (got == want).all(), (il, got, want)
