@@ -72,6 +72,7 @@ struct ComposeSmem {
   unsigned long long* pmk;   // [m_j + 1] pmk[c] = min key of the c lightest j entries, pmk[0] = sentinel
   uint32_t* kk32;            // [m_k] local form (register-tile path): cost_k << 20 | a * ks
   uint32_t* pm32;            // [m_j + 1] local form of pmk: cost_j << 20 | i * js, pm32[0] = 2^31
+  uint32_t* lk32;            // [E + 1] local key contribution of every entry of an in-thread position (tkey)
 };
 
 // Local (k, j) keys of the register-tile path: cost_k + cost_j < 2^11 in
@@ -276,6 +277,7 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
   s.cost = reinterpret_cast<int32_t*>(s.jw + mj);
   s.kk32 = reinterpret_cast<uint32_t*>(s.cost + c.E + 1);
   s.pm32 = s.kk32 + mk;
+  s.lk32 = s.pm32 + mj + 1;
 
   const int w = blockIdx.x / c.blocks_per_window;
   const int bw = blockIdx.x - w * c.blocks_per_window;
@@ -309,10 +311,16 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
     int p, r, b;
     entry_prb(g, v, i - g.menu_off[v], p, r, b);
     s.cost[i] = p * r;  // objective contribution (autoscaler.py:220-221, 756)
+    if (c.tkey) {
+      int pos = 0;
+      while (c.vop[pos] != v) ++pos;
+      s.lk32[i] = ((uint32_t)(p * r) << 20) + (uint32_t)(i - g.menu_off[v]) * c.cs[pos];
+    }
   }
   if (threadIdx.x == 0) {
     s.w[c.E] = 0.0;
     s.cost[c.E] = 0;
+    s.lk32[c.E] = 0;
   }
   if (use_tma) {
     uint32_t done = 0;
@@ -326,7 +334,7 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
   }
   __syncthreads();
   const int koff = c.off[kp], joff = c.off[jp];
-  const uint32_t ks = c.kj_major ? (uint32_t)mj : 1u, js = c.kj_major ? 1u : (uint32_t)mk;
+  const uint32_t ks = c.cs[kp], js = c.cs[jp];
   for (int a = threadIdx.x; a < mk; a += kComposeThreads) {
     s.kk[a] = ((unsigned long long)s.cost[koff + a] << OPSC_KEY_LEX_BITS) + (unsigned long long)a * c.stride[kp];
     s.kk32[a] = ((uint32_t)s.cost[koff + a] << 20) + (uint32_t)a * ks;
@@ -437,6 +445,10 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
     const double o_j = (!PATH && odo) ? dp_in(c.pmask[jp] & ~kmask & outer, val) : 0.0;
     const double o_lo = (!PATH && odo) ? dp_in(c.sinkmask & ~(kmask | jmask) & outer, val) : 0.0;
     bool odo_dirty = true;
+    // tkey: the thread's running minimum as one 32-bit local key over the
+    // middle, k and j levels (pb = the middle levels' part), decoded once
+    const bool tkey = NJ > 0 && c.tkey;
+    uint32_t pb = 0, best32 = 0xffffffffu;
 
     for (uint32_t mid = 0; mid < c.mid_count; ++mid) {
       long long cost1;
@@ -457,6 +469,7 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
         odo_dirty = false;
         long long pc = cost0;
         unsigned long long pl = lex0;
+        pb = 0;
         if constexpr (PATH) {
           // dp_in of the single predecessor: fmax(0.0, val[prev]); none: 0.0
           double pv = nout > 0 ? fmax(0.0, val[nout - 1]) : 0.0;
@@ -465,8 +478,12 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
             if (l < nmid) {
               const int e = c.off[nout + l] + od[l];
               pv = fmax(0.0, pv + s.w[e]);  // val[pos], then the next position's dp_in
-              pc += s.cost[e];
-              pl += (unsigned long long)od[l] * c.stride[nout + l];
+              if (tkey) {
+                pb += s.lk32[e];
+              } else {
+                pc += s.cost[e];
+                pl += (unsigned long long)od[l] * c.stride[nout + l];
+              }
             }
           }
           in_k = pv;
@@ -484,8 +501,12 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
               if (c.pmask[pos] >> (nout + l2) & 1u) in = fmax(in, mv[l2]);
             const int e = c.off[pos] + od[l];
             mv[l] = in + s.w[e];
-            pc += s.cost[e];
-            pl += (unsigned long long)od[l] * c.stride[pos];
+            if (tkey) {
+              pb += s.lk32[e];
+            } else {
+              pc += s.cost[e];
+              pl += (unsigned long long)od[l] * c.stride[pos];
+            }
             const uint32_t bit = 1u << pos;
             if (c.pmask[kp] & bit) in_k = fmax(in_k, mv[l]);
             if (c.pmask[jp] & ~kmask & bit) bj0 = fmax(bj0, mv[l]);
@@ -521,10 +542,15 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
       unsigned long long mbest = kSentinel;
       if constexpr (NJ > 0) {
         const uint32_t m32 = k_level_tile<NJ, CHAIN>(a_wk, a_kk, a_pm, mk_r, wj, in_k, bj0, lo0, k_to_j, k_sink, slo);
+        if (tkey) {
+          const uint32_t t = m32 + pb;  // no overflow: feasible m32 + pb < 2^31
+          if (m32 < kLocalInfeasible) best32 = t < best32 ? t : best32;
+          continue;
+        }
         if (m32 < kLocalInfeasible) {  // back to the global key
           const uint32_t loc = m32 & 0xfffffu;
-          const uint32_t a = c.kj_major ? loc / (uint32_t)mj : loc % (uint32_t)mk;
-          const uint32_t i = c.kj_major ? loc % (uint32_t)mj : loc / (uint32_t)mk;
+          const uint32_t a = (loc / c.cs[kp]) % (uint32_t)mk;
+          const uint32_t i = (loc / c.cs[jp]) % (uint32_t)mj;
           mbest = ((unsigned long long)(m32 >> 20) << OPSC_KEY_LEX_BITS) + (unsigned long long)a * c.stride[kp] +
                   (unsigned long long)i * c.stride[jp];
         }
@@ -536,6 +562,13 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
         best = key < best ? key : best;
       }
     }
+    if (tkey && best32 < kLocalInfeasible) {  // decode the in-thread minimum once
+      const uint32_t loc = best32 & 0xfffffu;
+      unsigned long long lex = lex0;
+      for (int pos = nout; pos < c.n; ++pos)
+        lex += (unsigned long long)((loc / c.cs[pos]) % (uint32_t)c.m[pos]) * c.stride[pos];
+      best = ((unsigned long long)(cost0 + (best32 >> 20)) << OPSC_KEY_LEX_BITS) + lex;
+    }
   }
   cta_min_commit(best, w, key_out, peers, warp_best);
 }
@@ -543,7 +576,7 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
 // Dynamic shared memory of the tile kernel: menu slab + costs, k / j tables.
 static size_t compose_smem_bytes(int E, int mk, int mj) {
   return (size_t)mk * 8 + (size_t)(mj + 1) * 8 + (size_t)(E + 1) * 8 + (size_t)mj * 8 + (size_t)(E + 1) * 4 +
-         (size_t)mk * 4 + (size_t)(mj + 1) * 4;
+         (size_t)mk * 4 + (size_t)(mj + 1) * 4 + (size_t)(E + 1) * 4;
 }
 
 // Host: topological positions, lexicographic strides, level split.
@@ -651,8 +684,10 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
   // register tile widths (padded entries are +inf and still cost their
   // DADD/DSETP/SEL, so common menu sizes get exact tiles: 6 = P{1,2} x R<=3)
   c.nj = mj <= 4 ? 4 : mj <= 6 ? 6 : mj <= 8 ? 8 : mj <= 12 ? 12 : mj <= 16 ? 16 : mj <= 24 ? 24 : mj <= 32 ? 32 : 0;
-  c.kj_major = c.stride[c.n - 2] > c.stride[c.n - 1] ? 1 : 0;
-  // register-tile local keys: (k, j) index < 2^20 and cost_k + cost_j < 2^11
+  // register-tile local keys: cost << 20 | compact index, index < 2^20 and
+  // cost < 2^11. The compact index of a set of positions orders them by
+  // lexicographic significance (global stride), so within one thread's
+  // prefix it orders candidates exactly as the global key does.
   auto max_cost = [&](int pos) {
     int mx = 0;
     for (int e = 0; e < c.m[pos]; ++e) {
@@ -664,7 +699,24 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
     }
     return mx;
   };
-  if ((long long)mj * mk >= (1 << 20) || max_cost(c.n - 1) + max_cost(c.n - 2) >= (1 << 11)) c.nj = 0;
+  auto compact = [&](int lo) {  // cs over positions lo..n-1; false if the local key does not fit
+    double space = 1.0;
+    long long cmax = 0;
+    for (int p = lo; p < c.n; ++p) {
+      space *= c.m[p];
+      cmax += max_cost(p);
+      unsigned long long cs = 1;
+      for (int q = lo; q < c.n; ++q)
+        if (c.stride[q] < c.stride[p]) cs *= (unsigned long long)c.m[q];
+      c.cs[p] = (uint32_t)std::min(cs, 0xffffffffull);
+    }
+    return space < (double)(1 << 20) && cmax < (1 << 11);
+  };
+  // middle levels in the local key: one 32-bit running minimum per thread,
+  // decoded to the global key once (odometer path only)
+  c.tkey = (c.n - 2 - (c.n - il) <= kOdoLevels) && compact(c.n - il) ? 1 : 0;
+  if (!c.tkey && !compact(c.n - 2)) c.nj = 0;
+  if (c.nj == 0) c.tkey = 0;
   // chain fast path: j's only predecessor is k and k is not a sink
   const int jp = c.n - 1, kp = c.n - 2;
   c.chain = (c.pmask[jp] == (1u << kp)) && !(c.sinkmask >> kp & 1u);

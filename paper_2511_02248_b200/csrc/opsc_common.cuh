@@ -278,7 +278,8 @@ struct ComposeCfg {
   int32_t blocks_per_window;
   int32_t nj;                  // register tile of the innermost menu
   int32_t chain;               // j's only predecessor is k and k is not a sink
-  int32_t kj_major;            // k precedes j in lexicographic order: local (k, j) index a*m_j + i, else i*m_k + a
+  int32_t tkey;                // 32-bit in-thread keys span the middle levels too (cs over all in-thread positions)
+  uint32_t cs[OPSC_CMAX];      // compact in-thread lexicographic strides (local key index = sum dig * cs)
   int32_t path_dag;            // every position fed only by the previous one, one sink (middle-level odometer)
   int32_t flat;                // menus too large for the shared-memory tile: flat kernel over the candidate index
   int32_t vop[OPSC_CMAX];      // real operator per position (-1 virtual)
