@@ -256,7 +256,8 @@ compose_flat_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant_
 }
 
 // MODE: 0 generic DAG, 1 CHAIN (j's only predecessor is k, k no sink),
-// 2 path DAG (every position fed by the previous one only, one sink).
+// 2 path suffix (every in-thread position fed by the previous one only, j the
+// only in-thread sink; outer sinks checked once per thread).
 template <int NJ, int MODE>
 __global__ void __launch_bounds__(kComposeThreads, OPSC_COMPOSE_MINB)
 compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ OpscGrid g,
@@ -445,6 +446,13 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
     const double o_j = (!PATH && odo) ? dp_in(c.pmask[jp] & ~kmask & outer, val) : 0.0;
     const double o_lo = (!PATH && odo) ? dp_in(c.sinkmask & ~(kmask | jmask) & outer, val) : 0.0;
     bool odo_dirty = true;
+    // path suffix: the first in-thread position's dp_in (outer predecessors
+    // only), +inf if an outer sink already misses the SLO
+    double pv0 = 0.0;
+    if constexpr (PATH) {
+      pv0 = dp_in(c.pmask[nout], val);
+      if (!(dp_in(c.sinkmask & outer, val) <= slo)) pv0 = OPSC_INF;
+    }
     // tkey: the thread's running minimum as one 32-bit local key over the
     // middle, k and j levels (pb = the middle levels' part), decoded once
     const bool tkey = NJ > 0 && c.tkey;
@@ -471,8 +479,7 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
         unsigned long long pl = lex0;
         pb = 0;
         if constexpr (PATH) {
-          // dp_in of the single predecessor: fmax(0.0, val[prev]); none: 0.0
-          double pv = nout > 0 ? fmax(0.0, val[nout - 1]) : 0.0;
+          double pv = pv0;  // then dp_in of the single predecessor: fmax(0.0, val[prev])
 #pragma unroll
           for (int l = 0; l < kOdoLevels; ++l) {
             if (l < nmid) {
@@ -720,10 +727,17 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
   // chain fast path: j's only predecessor is k and k is not a sink
   const int jp = c.n - 1, kp = c.n - 2;
   c.chain = (c.pmask[jp] == (1u << kp)) && !(c.sinkmask >> kp & 1u);
-  // path DAG: position 0 a source, every later position fed by the previous
-  // one only, a single sink at the end
-  c.path_dag = c.pmask[0] == 0u && c.sinkmask == (1u << jp);
-  for (int pos = 1; pos < c.n; ++pos) c.path_dag &= c.pmask[pos] == (1u << (pos - 1));
+  // path suffix: the in-thread positions form a path (each fed by the
+  // previous one only; the first by outer positions only) ending in the only
+  // in-thread sink j. Sinks among the outer positions are checked once per
+  // thread. True for the chain DAGs (7B, 70B) and for DAGs whose branches
+  // merge above the in-thread levels (the multimodal DAG).
+  {
+    const int nout = c.n - il;
+    const uint32_t inner = ~((1u << nout) - 1u);
+    c.path_dag = (c.sinkmask & inner) == (1u << jp);
+    for (int pos = nout + 1; pos < c.n; ++pos) c.path_dag &= c.pmask[pos] == (1u << (pos - 1));
+  }
   *cfg = c;
   return OPSC_OK;
 }

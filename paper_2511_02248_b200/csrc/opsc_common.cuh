@@ -280,7 +280,7 @@ struct ComposeCfg {
   int32_t chain;               // j's only predecessor is k and k is not a sink
   int32_t tkey;                // 32-bit in-thread keys span the middle levels too (cs over all in-thread positions)
   uint32_t cs[OPSC_CMAX];      // compact in-thread lexicographic strides (local key index = sum dig * cs)
-  int32_t path_dag;            // every position fed only by the previous one, one sink (middle-level odometer)
+  int32_t path_dag;            // in-thread positions form a path ending in the only in-thread sink (middle-level odometer)
   int32_t flat;                // menus too large for the shared-memory tile: flat kernel over the candidate index
   int32_t vop[OPSC_CMAX];      // real operator per position (-1 virtual)
   unsigned long long flo, fhi; // flat kernel: this shard's candidate index range

@@ -16,6 +16,11 @@ def _random_dag(rng, n, shape):
         edges = [(ids[i], ids[i + 1]) for i in range(n - 3)] + [(ids[n - 3], ids[n - 1]), (ids[n - 2], ids[n - 1])]
     elif shape == "fork":     # two sinks
         edges = [(ids[i], ids[i + 1]) for i in range(n - 2)] + [(ids[n - 3], ids[n - 1])]
+    elif shape == "early_sink":  # a->b->c (sink c above the in-thread levels), b->d->...->last
+        edges = [(ids[0], ids[1]), (ids[1], ids[2]), (ids[1], ids[3])] + [(ids[i], ids[i + 1]) for i in range(3, n - 1)]
+    elif shape == "two_source":  # a->b->c and d->c, then a chain (merge above the in-thread levels)
+        edges = [(ids[0], ids[1]), (ids[1], ids[2]), (ids[3], ids[2])] + [(ids[2], ids[4])] + \
+                [(ids[i], ids[i + 1]) for i in range(4, n - 1)]
     else:                     # random DAG
         edges = [(ids[i], ids[j]) for j in range(1, n) for i in range(j) if rng.uniform() < 0.35]
     nodes = [{"id": i, "kind": "linear", "layer_count": int(rng.choice([1, 8, 32])), "profile_ref": "p" + i}
@@ -30,7 +35,8 @@ def _random_dag(rng, n, shape):
     return model.build_dag(dag), model.profiles_from_dict(prof)
 
 
-@pytest.mark.parametrize("shape,n", [("merge", 7), ("fork", 7), ("random", 7), ("random", 8)])
+@pytest.mark.parametrize("shape,n", [("merge", 7), ("fork", 7), ("random", 7), ("random", 8),
+                                     ("early_sink", 7), ("early_sink", 8), ("two_source", 7), ("two_source", 8)])
 def test_generic_dag_exhaustive_vs_oracle(nat_loaded, orc, shape, n):
     from paper_2511_02248_b200 import _native
     rng = np.random.default_rng(n * 7 + len(shape))
