@@ -137,6 +137,23 @@ __device__ __forceinline__ uint32_t k_level_tile(uint32_t a_wk, uint32_t a_kk, u
   return mbest;
 }
 
+// Small menus (m_k <= NJ <= 8): the k menu in registers too, fully unrolled
+// (padding: w = +inf never passes, local key 0 + pm32[0] = infeasible).
+template <int NJ, bool CHAIN>
+__device__ __forceinline__ uint32_t k_level_reg(uint32_t a_pm, const double (&wk)[NJ], const uint32_t (&kk)[NJ],
+                                                const double (&wj)[NJ], double in_k, double bj0, double lo0,
+                                                bool k_to_j, bool k_sink, double slo) {
+  uint32_t mbest = 0xffffffffu;
+#pragma unroll
+  for (int a = 0; a < NJ; ++a) {
+    const double bj = j_base<CHAIN>(in_k + wk[a], bj0, lo0, k_to_j, k_sink, slo);
+    const uint32_t cnt = exact_count<NJ>(bj, wj, slo);
+    const uint32_t kl = kk[a] + lds_u32(a_pm + 4u * cnt);
+    mbest = kl < mbest ? kl : mbest;
+  }
+  return mbest;
+}
+
 // Shared-memory path for large j menus (NJ == 0): u64 keys, exact compares.
 template <bool CHAIN>
 __device__ __forceinline__ unsigned long long k_level_smem(const ComposeSmem& s, int mk, int mj, int koff,
@@ -258,7 +275,7 @@ compose_flat_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant_
 // MODE: 0 generic DAG, 1 CHAIN (j's only predecessor is k, k no sink),
 // 2 path suffix (every in-thread position fed by the previous one only, j the
 // only in-thread sink; outer sinks checked once per thread).
-template <int NJ, int MODE>
+template <int NJ, int MODE, bool KREG>
 __global__ void __launch_bounds__(kComposeThreads, OPSC_COMPOSE_MINB)
 compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ OpscGrid g,
                const double* __restrict__ menu_w, const double* __restrict__ slo_w,
@@ -405,6 +422,14 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
     double wj[NJ > 0 ? NJ : 1];
 #pragma unroll
     for (int i = 0; i < NJ; ++i) wj[i] = i < mj ? s.jw[i] : OPSC_INF;
+    constexpr int NK = KREG ? NJ : 1;
+    double wk[NK];
+    uint32_t kkr[NK];
+#pragma unroll
+    for (int i = 0; i < NK; ++i) {
+      wk[i] = KREG && i < mk ? s.w[koff + i] : OPSC_INF;
+      kkr[i] = KREG && i < mk ? s.kk32[i] : 0u;
+    }
     double val[OPSC_CMAX];
     int dig[OPSC_CMAX];
     uint32_t rem = o;
@@ -548,7 +573,12 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
 
       unsigned long long mbest = kSentinel;
       if constexpr (NJ > 0) {
-        const uint32_t m32 = k_level_tile<NJ, CHAIN>(a_wk, a_kk, a_pm, mk_r, wj, in_k, bj0, lo0, k_to_j, k_sink, slo);
+        uint32_t m32;
+        if constexpr (KREG) {
+          m32 = k_level_reg<NJ, CHAIN>(a_pm, wk, kkr, wj, in_k, bj0, lo0, k_to_j, k_sink, slo);
+        } else {
+          m32 = k_level_tile<NJ, CHAIN>(a_wk, a_kk, a_pm, mk_r, wj, in_k, bj0, lo0, k_to_j, k_sink, slo);
+        }
         if (tkey) {
           const uint32_t t = m32 + pb;  // no overflow: feasible m32 + pb < 2^31
           if (m32 < kLocalInfeasible) best32 = t < best32 ? t : best32;
@@ -742,30 +772,41 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
   return OPSC_OK;
 }
 
-template <int NJ, int MODE>
+template <int NJ, int MODE, bool KREG>
 static cudaError_t launch_t(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,
                             const double* slo, const double* qps, unsigned long long* key, cudaStream_t s,
                             const PeerKeys& pk) {
   const int mj = c.m[c.n - 1], mk = c.m[c.n - 2];
   const size_t smem = compose_smem_bytes(c.E, mk, mj);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(compose_kernel<NJ, MODE>,
+    cudaError_t e = cudaFuncSetAttribute(compose_kernel<NJ, MODE, KREG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   const long long blocks = (long long)n_windows * c.blocks_per_window;
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  compose_kernel<NJ, MODE><<<(unsigned)blocks, kComposeThreads, smem, s>>>(c, g, menu_w, slo, qps, key, pk);
+  compose_kernel<NJ, MODE, KREG><<<(unsigned)blocks, kComposeThreads, smem, s>>>(c, g, menu_w, slo, qps, key, pk);
   return cudaGetLastError();
+}
+
+template <int NJ, bool KREG>
+static cudaError_t launch_mode(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,
+                               const double* slo, const double* qps, unsigned long long* key, cudaStream_t s,
+                               const PeerKeys& pk) {
+  if (c.path_dag) return launch_t<NJ, 2, KREG>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
+  return c.chain ? launch_t<NJ, 1, KREG>(c, g, n_windows, menu_w, slo, qps, key, s, pk)
+                 : launch_t<NJ, 0, KREG>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
 }
 
 template <int NJ>
 static cudaError_t launch_nj(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,
                              const double* slo, const double* qps, unsigned long long* key, cudaStream_t s,
                              const PeerKeys& pk) {
-  if (c.path_dag) return launch_t<NJ, 2>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
-  return c.chain ? launch_t<NJ, 1>(c, g, n_windows, menu_w, slo, qps, key, s, pk)
-                 : launch_t<NJ, 0>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
+  if constexpr (NJ > 0 && NJ <= 8) {
+    if (c.m[c.n - 2] <= NJ && !getenv("OPSC_COMPOSE_NO_KREG"))
+      return launch_mode<NJ, true>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
+  }
+  return launch_mode<NJ, false>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
 }
 
 cudaError_t launch_compose(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,

@@ -76,3 +76,33 @@ def nat_loaded():
     _native.load()
     assert _native.device_count() >= 1
     return _native
+
+
+@pytest.mark.parametrize("p_of", [
+    {"down": (1,), "lm_head": (1, 2)},             # k menu 3 < j tile 6 (padded register k tile)
+    {"down": (1, 2), "lm_head": (1,)},             # j menu 3 -> tile 4, k menu 6 > 4 (shared k loop)
+    {"act": (1,), "down": (1, 2, 4), "lm_head": (2, 4)},  # k 9 / j 6
+])
+def test_ragged_menus_70b_vs_oracle(nat_loaded, orc, p_of):
+    """Per-operator parallelism dicts give the k / j levels different menu
+    sizes: the register k tile with +inf padding, and the shared-memory k loop
+    next to a small j tile, against the oracle on the 10-op 70B chain."""
+    from paper_2511_02248_b200 import _native
+    dag, prof = scenarios.scenario("cfg2")
+    prob = tables.pack_problem(dag, prof)
+    par = {op: p_of.get(op, (1, 2)) for op in prob.ids}
+    params = model.AutoscaleParams(slo=1.0, parallelism=par, b_max=1)
+    grid = tables.pack_grid(prob, params, model.BruteForceBounds(r_max=3))
+    tw = scenarios.trace_windows("cfg2")
+    idx = np.array([0, 7, 19, 33, 58])
+    n_feasible = 0
+    for phase in ("prefill", "decode"):
+        for scale in (1.0, 4.0):  # the scenario SLO and a loose one (feasible decisions to compare)
+            win = tables.window_arrays(tw[phase + "_qps"][idx], tw[phase + "_len"][idx],
+                                       tables.PHASE_INDEX[phase], scale * scenarios.SLO["cfg2"][phase])
+            gpu = _native.plan_windows_host(abi.MODE_ORACLE, prob, win, grid=grid)
+            cpu = orc.plan_windows(abi.MODE_ORACLE, prob, win, grid=grid)
+            for f in tables.DecisionArrays.FIELDS:
+                assert getattr(gpu, f).tobytes() == getattr(cpu, f).tobytes(), (phase, scale, f)
+            n_feasible += int(cpu.feasible.sum())
+    assert n_feasible > 0
