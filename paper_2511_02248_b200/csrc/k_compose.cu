@@ -451,126 +451,14 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
     const bool k_to_j = (c.pmask[jp] & kmask) != 0;
     const bool k_sink = (c.sinkmask & kmask) != 0;
 
-    // Middle levels (<= kOdoLevels of them) run as an odometer with their DP
-    // values in registers instead of re-decoding the digits with divisions
-    // and re-running the DP through local memory for every middle index. A
-    // dp_in is a max over predecessors (exact, order-free), so it splits into
-    // the outer predecessors' part, fixed per thread, and the middle ones'.
-    const int nmid = kp - nout;
-    const bool odo = nmid <= kOdoLevels;
-    const uint32_t outer = (1u << nout) - 1u;
-    int od[kOdoLevels];
-    double o_in[kOdoLevels], mv[kOdoLevels];
-#pragma unroll
-    for (int l = 0; l < kOdoLevels; ++l) {
-      od[l] = 0;
-      mv[l] = 0.0;
-      o_in[l] = (!PATH && odo && l < nmid) ? dp_in(c.pmask[nout + l] & outer, val) : 0.0;
-    }
-    const double o_k = (!PATH && odo) ? dp_in(c.pmask[kp] & outer, val) : 0.0;
-    const double o_j = (!PATH && odo) ? dp_in(c.pmask[jp] & ~kmask & outer, val) : 0.0;
-    const double o_lo = (!PATH && odo) ? dp_in(c.sinkmask & ~(kmask | jmask) & outer, val) : 0.0;
-    bool odo_dirty = true;
-    // path suffix: the first in-thread position's dp_in (outer predecessors
-    // only), +inf if an outer sink already misses the SLO
-    double pv0 = 0.0;
-    if constexpr (PATH) {
-      pv0 = dp_in(c.pmask[nout], val);
-      if (!(dp_in(c.sinkmask & outer, val) <= slo)) pv0 = OPSC_INF;
-    }
     // tkey: the thread's running minimum as one 32-bit local key over the
     // middle, k and j levels (pb = the middle levels' part), decoded once
     const bool tkey = NJ > 0 && c.tkey;
-    uint32_t pb = 0, best32 = 0xffffffffu;
-
-    for (uint32_t mid = 0; mid < c.mid_count; ++mid) {
-      long long cost1;
-      unsigned long long lex1;
-      double in_k;
-      double bj0 = 0.0, lo0 = 0.0;
-      if (odo) {
-        if (!odo_dirty) {  // advance the odometer (innermost middle level fastest)
-          bool carry = true;
-#pragma unroll
-          for (int l = kOdoLevels - 1; l >= 0; --l) {
-            if (l < nmid && carry) {
-              if (++od[l] == c.m[nout + l]) od[l] = 0;
-              else carry = false;
-            }
-          }
-        }
-        odo_dirty = false;
-        long long pc = cost0;
-        unsigned long long pl = lex0;
-        pb = 0;
-        if constexpr (PATH) {
-          double pv = pv0;  // then dp_in of the single predecessor: fmax(0.0, val[prev])
-#pragma unroll
-          for (int l = 0; l < kOdoLevels; ++l) {
-            if (l < nmid) {
-              const int e = c.off[nout + l] + od[l];
-              pv = fmax(0.0, pv + s.w[e]);  // val[pos], then the next position's dp_in
-              if (tkey) {
-                pb += s.lk32[e];
-              } else {
-                pc += s.cost[e];
-                pl += (unsigned long long)od[l] * c.stride[nout + l];
-              }
-            }
-          }
-          in_k = pv;
-        } else {
-        in_k = o_k;
-        bj0 = o_j;
-        lo0 = o_lo;
-#pragma unroll
-        for (int l = 0; l < kOdoLevels; ++l) {
-          if (l < nmid) {
-            const int pos = nout + l;
-            double in = o_in[l];
-#pragma unroll
-            for (int l2 = 0; l2 < l; ++l2)
-              if (c.pmask[pos] >> (nout + l2) & 1u) in = fmax(in, mv[l2]);
-            const int e = c.off[pos] + od[l];
-            mv[l] = in + s.w[e];
-            if (tkey) {
-              pb += s.lk32[e];
-            } else {
-              pc += s.cost[e];
-              pl += (unsigned long long)od[l] * c.stride[pos];
-            }
-            const uint32_t bit = 1u << pos;
-            if (c.pmask[kp] & bit) in_k = fmax(in_k, mv[l]);
-            if (c.pmask[jp] & ~kmask & bit) bj0 = fmax(bj0, mv[l]);
-            if (c.sinkmask & bit) lo0 = fmax(lo0, mv[l]);
-          }
-        }
-        if (CHAIN && !(lo0 <= slo)) in_k = OPSC_INF;  // another sink already misses the SLO
-        }
-        cost1 = pc;
-        lex1 = pl;
-      } else {
-        uint32_t r2 = mid;
-        for (int pos = kp - 1; pos >= nout; --pos) {
-          const uint32_t mm = (uint32_t)c.m[pos];
-          const uint32_t q = r2 / mm;
-          dig[pos] = (int)(r2 - q * mm);
-          r2 = q;
-        }
-        cost1 = cost0;
-        lex1 = lex0;
-        for (int pos = nout; pos < kp; ++pos) {
-          const int e = c.off[pos] + dig[pos];
-          val[pos] = dp_in(c.pmask[pos], val) + s.w[e];
-          cost1 += s.cost[e];
-          lex1 += (unsigned long long)dig[pos] * c.stride[pos];
-        }
-        in_k = dp_in(c.pmask[kp], val);
-        bj0 = dp_in(c.pmask[jp] & ~kmask, val);
-        lo0 = dp_in(c.sinkmask & ~(kmask | jmask), val);
-        if (CHAIN && !(lo0 <= slo)) in_k = OPSC_INF;  // another sink already misses the SLO
-      }
-
+    uint32_t best32 = 0xffffffffu;
+    // The k and j levels for one prefix (middle digits fixed): pb / cost1 /
+    // lex1 are the prefix's key parts (local key, or objective and index).
+    auto kj_levels = [&](double in_k, double bj0, double lo0, uint32_t pb, long long cost1,
+                         unsigned long long lex1) {
       unsigned long long mbest = kSentinel;
       if constexpr (NJ > 0) {
         uint32_t m32;
@@ -582,7 +470,7 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
         if (tkey) {
           const uint32_t t = m32 + pb;  // no overflow: feasible m32 + pb < 2^31
           if (m32 < kLocalInfeasible) best32 = t < best32 ? t : best32;
-          continue;
+          return;
         }
         if (m32 < kLocalInfeasible) {  // back to the global key
           const uint32_t loc = m32 & 0xfffffu;
@@ -597,6 +485,108 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
       if (mbest < kSentinel) {
         const unsigned long long key = ((unsigned long long)cost1 << OPSC_KEY_LEX_BITS) + lex1 + mbest;
         best = key < best ? key : best;
+      }
+    };
+
+    // Middle levels (<= kOdoLevels of them): the last one is a plain loop
+    // over its menu, the ones above it an odometer, all DP values in
+    // registers (no per-index digit divisions, no DP through local memory).
+    // A dp_in is a max over predecessors (exact, order-free), so it splits
+    // into the outer predecessors' part, fixed per thread, and the middle ones'.
+    const int nmid = kp - nout;  // <= kOdoLevels (compose_setup: il <= kOdoLevels + 2)
+    {
+      const uint32_t outer = (1u << nout) - 1u;
+      const int nm1 = nmid > 0 ? nmid - 1 : 0;  // odometer levels above the last middle level
+      const int lpos = nout + nmid - 1;         // the last middle level (nmid > 0)
+      const uint32_t m_last = nmid > 0 ? (uint32_t)c.m[lpos] : 1u;
+      const uint32_t n_pre = c.mid_count / m_last;
+      int od[kOdoLevels];
+      double o_in[kOdoLevels], mv[kOdoLevels];
+#pragma unroll
+      for (int l = 0; l < kOdoLevels; ++l) {
+        od[l] = 0;
+        mv[l] = 0.0;
+        o_in[l] = (!PATH && l < nmid) ? dp_in(c.pmask[nout + l] & outer, val) : 0.0;
+      }
+      const double o_k = !PATH ? dp_in(c.pmask[kp] & outer, val) : 0.0;
+      const double o_j = !PATH ? dp_in(c.pmask[jp] & ~kmask & outer, val) : 0.0;
+      const double o_lo = !PATH ? dp_in(c.sinkmask & ~(kmask | jmask) & outer, val) : 0.0;
+      // path suffix: the first in-thread position's dp_in (outer predecessors
+      // only), +inf if an outer sink already misses the SLO
+      double pv0 = 0.0;
+      if constexpr (PATH) {
+        pv0 = dp_in(c.pmask[nout], val);
+        if (!(dp_in(c.sinkmask & outer, val) <= slo)) pv0 = OPSC_INF;
+      }
+      const uint32_t bit_last = nmid > 0 ? 1u << lpos : 0u;
+      const bool last_to_k = (c.pmask[kp] & bit_last) != 0;
+      const bool last_to_j = (c.pmask[jp] & ~kmask & bit_last) != 0;
+      const bool last_sink = (c.sinkmask & bit_last) != 0;
+      const int off_last = nmid > 0 ? c.off[lpos] : c.E;  // entry E: weight +0.0, cost 0, local key 0
+      const unsigned long long stride_last = nmid > 0 ? c.stride[lpos] : 0ull;
+
+      for (uint32_t pre = 0; pre < n_pre; ++pre) {
+        if (pre > 0) {  // advance the odometer (innermost level fastest)
+          bool carry = true;
+#pragma unroll
+          for (int l = kOdoLevels - 1; l >= 0; --l) {
+            if (l < nm1 && carry) {
+              if (++od[l] == c.m[nout + l]) od[l] = 0;
+              else carry = false;
+            }
+          }
+        }
+        // prefix state over the odometer levels
+        long long pc = cost0;
+        unsigned long long pl = lex0;
+        uint32_t pbp = 0;
+        double pv = pv0;                                 // PATH: dp_in of the next position
+        double in_k = o_k, bj0 = o_j, lo0 = o_lo, in_last = 0.0;  // generic
+        if (!PATH && nmid > 0) in_last = o_in[nmid - 1];
+#pragma unroll
+        for (int l = 0; l < kOdoLevels; ++l) {
+          if (l < nm1) {
+            const int pos = nout + l;
+            const int e = c.off[pos] + od[l];
+            if constexpr (PATH) {
+              pv = fmax(0.0, pv + s.w[e]);  // val[pos], then the next position's dp_in
+            } else {
+              double in = o_in[l];
+#pragma unroll
+              for (int l2 = 0; l2 < l; ++l2)
+                if (c.pmask[pos] >> (nout + l2) & 1u) in = fmax(in, mv[l2]);
+              mv[l] = in + s.w[e];
+              const uint32_t bit = 1u << pos;
+              if (c.pmask[kp] & bit) in_k = fmax(in_k, mv[l]);
+              if (c.pmask[jp] & ~kmask & bit) bj0 = fmax(bj0, mv[l]);
+              if (c.sinkmask & bit) lo0 = fmax(lo0, mv[l]);
+              if (c.pmask[lpos] & bit) in_last = fmax(in_last, mv[l]);
+            }
+            if (tkey) {
+              pbp += s.lk32[e];
+            } else {
+              pc += s.cost[e];
+              pl += (unsigned long long)od[l] * c.stride[pos];
+            }
+          }
+        }
+        for (uint32_t i = 0; i < m_last; ++i) {  // the last middle level (none: the virtual entry E)
+          const int e = off_last + (int)i;
+          const double wl = s.w[e];
+          const uint32_t pb = tkey ? pbp + s.lk32[e] : 0u;
+          const long long cost1 = tkey ? 0 : pc + s.cost[e];
+          const unsigned long long lex1 = tkey ? 0ull : pl + (unsigned long long)i * stride_last;
+          if constexpr (PATH) {
+            kj_levels(fmax(0.0, pv + wl), 0.0, 0.0, pb, cost1, lex1);
+          } else {
+            const double v = in_last + wl;
+            double ik = last_to_k ? fmax(in_k, v) : in_k;
+            const double b0 = last_to_j ? fmax(bj0, v) : bj0;
+            const double l0 = last_sink ? fmax(lo0, v) : lo0;
+            if (CHAIN && !(l0 <= slo)) ik = OPSC_INF;  // another sink already misses the SLO
+            kj_levels(ik, b0, l0, pb, cost1, lex1);
+          }
+        }
       }
     }
     if (tkey && best32 < kLocalInfeasible) {  // decode the in-thread minimum once
@@ -697,7 +687,7 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
   };
   const double min_threads = 148.0 * 512.0;
   int il = 2;
-  while (il < c.n && il < 6) {
+  while (il < c.n && il < kOdoLevels + 2) {
     const bool too_many = prod(0, c.n - il) >= 4294967295.0;
     if (!too_many && prod(c.n - il, c.n) >= 1024.0) break;  // in-thread candidates amortise the outer decode
     if (!too_many && (double)n_windows * prod(0, c.n - il - 1) < min_threads) break;
@@ -705,7 +695,7 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
   }
   if (const char* f = getenv("OPSC_COMPOSE_IL")) {  // dev override (tools/w1_latency.py)
     const int want = atoi(f);
-    if (want >= 2 && want <= 6 && want <= c.n && prod(0, c.n - want) < 4294967295.0) il = want;
+    if (want >= 2 && want <= kOdoLevels + 2 && want <= c.n && prod(0, c.n - want) < 4294967295.0) il = want;
   }
   if (prod(0, c.n - il) >= 4294967295.0) return OPSC_ERR_SPACE;
   c.il = il;
@@ -794,8 +784,8 @@ static cudaError_t launch_mode(const ComposeCfg& c, const OpscGrid& g, int n_win
                                const double* slo, const double* qps, unsigned long long* key, cudaStream_t s,
                                const PeerKeys& pk) {
   if (c.path_dag) return launch_t<NJ, 2, KREG>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
-  return c.chain ? launch_t<NJ, 1, KREG>(c, g, n_windows, menu_w, slo, qps, key, s, pk)
-                 : launch_t<NJ, 0, KREG>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
+  if (c.chain) return launch_t<NJ, 1, KREG>(c, g, n_windows, menu_w, slo, qps, key, s, pk);
+  return launch_t<NJ, 0, false>(c, g, n_windows, menu_w, slo, qps, key, s, pk);  // k registers spill there
 }
 
 template <int NJ>
