@@ -359,6 +359,7 @@ def ours(args):
         latency = decision_latency(dev)
         latency["trace_pipeline"] = trace_pipeline(dev)
         latency["capacity_8gpu"] = capacity_8gpu(dev)
+        latency["multimodal_cfg3"] = multimodal_batched(dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -479,6 +480,49 @@ def decision_latency(dev):
                 cpw *= grid.menu_off[v + 1] - grid.menu_off[v]
             out[name]["batched_candidates_per_s"] = cpw / (out[name]["batched_ms_per_window"] * 1e-3)
     out["dag"] = "cfg2 Llama-2-70B 10-op chain, 60 x 60 s windows x {prefill, decode}, W = 1"
+    return out
+
+
+def multimodal_batched(dev):
+    """Config 3: the 12-op multimodal DAG (vision branch + text embed merging
+    into the LLM stack, heavy-tailed lengths) over its whole trace, both
+    phases, one launch set per phase: exhaustive (P in {1,2}, R<=3, B=1)^12 =
+    2.2e9 candidates per window, model level and greedy."""
+    import torch
+
+    from paper_2511_02248_b200 import abi, device, model, scenarios, tables
+    problem = tables.pack_problem(*scenarios.scenario("cfg3"))
+    g = scenarios.GRIDS["cfg3"]
+    tw = scenarios.trace_windows("cfg3")
+    out = {"dag": "cfg3 multimodal 12-op DAG (two sources), whole trace x {prefill, decode}, one launch set per phase"}
+    for mode, name in ((abi.MODE_ORACLE, "oracle"), (abi.MODE_MODEL, "model_level"),
+                       (abi.MODE_OPERATOR, "operator_greedy")):
+        ms, n_win, cands = 0.0, 0, 0
+        for phase in ("prefill", "decode"):
+            slo = scenarios.SLO["cfg3"][phase]
+            params = model.AutoscaleParams(slo=slo)
+            grid = tables.pack_grid(problem, params, model.BruteForceBounds(**g))
+            qs, ls = tw[phase + "_qps"], tw[phase + "_len"]
+            allw = tables.window_arrays(qs, ls, tables.PHASE_INDEX[phase], slo)
+            pb = device.DevicePlanner(problem, allw, mode, grid=grid, model=tables.pack_model(problem, params),
+                                      greedy=tables.pack_greedy(problem, params), device=dev)
+            pb.step()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            pb.step()
+            e1.record()
+            e1.synchronize()
+            ms += e0.elapsed_time(e1)
+            active = int((qs > 0).sum())
+            n_win += active
+            cpw = 1
+            for v in range(problem.n_ops):
+                cpw *= grid.menu_off[v + 1] - grid.menu_off[v]
+            cands += cpw * active
+        out[name] = {"ms": ms, "windows": n_win, "ms_per_window": ms / max(1, n_win)}
+        if mode == abi.MODE_ORACLE:
+            out[name]["candidates"] = cands
+            out[name]["candidates_per_s"] = cands / (ms * 1e-3)
     return out
 
 
