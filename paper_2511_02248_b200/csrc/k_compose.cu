@@ -451,15 +451,15 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
     const bool k_to_j = (c.pmask[jp] & kmask) != 0;
     const bool k_sink = (c.sinkmask & kmask) != 0;
 
-    // tkey: the thread's running minimum as one 32-bit local key over the
-    // middle, k and j levels (pb = the middle levels' part), decoded once
-    const bool tkey = NJ > 0 && c.tkey;
+    // register tiles (NJ > 0, compose_setup guarantees c.tkey): the thread's
+    // running minimum as one 32-bit local key over the middle, k and j levels
+    // (pb = the middle levels' part), decoded once
+    constexpr bool tkey = NJ > 0;
     uint32_t best32 = 0xffffffffu;
     // The k and j levels for one prefix (middle digits fixed): pb / cost1 /
     // lex1 are the prefix's key parts (local key, or objective and index).
     auto kj_levels = [&](double in_k, double bj0, double lo0, uint32_t pb, long long cost1,
                          unsigned long long lex1) {
-      unsigned long long mbest = kSentinel;
       if constexpr (NJ > 0) {
         uint32_t m32;
         if constexpr (KREG) {
@@ -467,24 +467,14 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
         } else {
           m32 = k_level_tile<NJ, CHAIN>(a_wk, a_kk, a_pm, mk_r, wj, in_k, bj0, lo0, k_to_j, k_sink, slo);
         }
-        if (tkey) {
-          const uint32_t t = m32 + pb;  // no overflow: feasible m32 + pb < 2^31
-          if (m32 < kLocalInfeasible) best32 = t < best32 ? t : best32;
-          return;
-        }
-        if (m32 < kLocalInfeasible) {  // back to the global key
-          const uint32_t loc = m32 & 0xfffffu;
-          const uint32_t a = (loc / c.cs[kp]) % (uint32_t)mk;
-          const uint32_t i = (loc / c.cs[jp]) % (uint32_t)mj;
-          mbest = ((unsigned long long)(m32 >> 20) << OPSC_KEY_LEX_BITS) + (unsigned long long)a * c.stride[kp] +
-                  (unsigned long long)i * c.stride[jp];
-        }
+        const uint32_t t = m32 + pb;  // no overflow: feasible m32 + pb < 2^31
+        if (m32 < kLocalInfeasible) best32 = t < best32 ? t : best32;
       } else {
-        mbest = k_level_smem<CHAIN>(s, mk, mj, koff, in_k, bj0, lo0, k_to_j, k_sink, slo);
-      }
-      if (mbest < kSentinel) {
-        const unsigned long long key = ((unsigned long long)cost1 << OPSC_KEY_LEX_BITS) + lex1 + mbest;
-        best = key < best ? key : best;
+        const unsigned long long mbest = k_level_smem<CHAIN>(s, mk, mj, koff, in_k, bj0, lo0, k_to_j, k_sink, slo);
+        if (mbest < kSentinel) {
+          const unsigned long long key = ((unsigned long long)cost1 << OPSC_KEY_LEX_BITS) + lex1 + mbest;
+          best = key < best ? key : best;
+        }
       }
     };
 
@@ -562,7 +552,7 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
               if (c.sinkmask & bit) lo0 = fmax(lo0, mv[l]);
               if (c.pmask[lpos] & bit) in_last = fmax(in_last, mv[l]);
             }
-            if (tkey) {
+            if constexpr (tkey) {
               pbp += s.lk32[e];
             } else {
               pc += s.cost[e];
@@ -589,7 +579,7 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
         }
       }
     }
-    if (tkey && best32 < kLocalInfeasible) {  // decode the in-thread minimum once
+    if (NJ > 0 && best32 < kLocalInfeasible) {  // decode the in-thread minimum once
       const uint32_t loc = best32 & 0xfffffu;
       unsigned long long lex = lex0;
       for (int pos = nout; pos < c.n; ++pos)
@@ -739,11 +729,11 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
     }
     return space < (double)(1 << 20) && cmax < (1 << 11);
   };
-  // middle levels in the local key: one 32-bit running minimum per thread,
-  // decoded to the global key once (odometer path only)
-  c.tkey = (c.n - 2 - (c.n - il) <= kOdoLevels) && compact(c.n - il) ? 1 : 0;
-  if (!c.tkey && !compact(c.n - 2)) c.nj = 0;
-  if (c.nj == 0) c.tkey = 0;
+  // register tiles keep one 32-bit running minimum per thread over all its
+  // in-thread levels, decoded to the global key once; when the in-thread
+  // space or cost does not fit the local key, the u64 shared-memory path runs
+  c.tkey = c.nj > 0 && compact(c.n - il) ? 1 : 0;
+  if (!c.tkey) c.nj = 0;
   // chain fast path: j's only predecessor is k and k is not a sink
   const int jp = c.n - 1, kp = c.n - 2;
   c.chain = (c.pmask[jp] == (1u << kp)) && !(c.sinkmask >> kp & 1u);
