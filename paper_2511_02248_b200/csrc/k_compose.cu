@@ -49,7 +49,11 @@ namespace opsc {
 #ifndef OPSC_COMPOSE_KUNROLL
 #define OPSC_COMPOSE_KUNROLL 3  // k-loop unroll of the exact form: +5% on 6-entry menus, neutral on 24
 #endif
+#ifndef OPSC_COMPOSE_LUNROLL
+#define OPSC_COMPOSE_LUNROLL 2  // +1.5% on 6-entry menus (cfg2 / cfg3), neutral on cfg5 (tools/variants_lunroll.sh)
+#endif
 constexpr int kComposeThreads = OPSC_COMPOSE_THREADS;
+constexpr int kLUnroll = OPSC_COMPOSE_LUNROLL;  // unroll of the last middle level's loop
 constexpr int kOdoLevels = 4;
 constexpr int kKUnroll = OPSC_COMPOSE_KUNROLL;  // middle levels kept in registers on path DAGs (il <= 6)
 constexpr unsigned long long kSentinel = 1ull << 62;  // > any real key (objective < 2^17)
@@ -560,6 +564,7 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
             }
           }
         }
+#pragma unroll(kLUnroll)
         for (uint32_t i = 0; i < m_last; ++i) {  // the last middle level (none: the virtual entry E)
           const int e = off_last + (int)i;
           const double wl = s.w[e];
