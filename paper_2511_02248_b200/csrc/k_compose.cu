@@ -33,6 +33,7 @@
 //     prefix's minimum; CTA result = warp-shuffle u64 min -> smem -> one
 //     atomicMin per CTA.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 
@@ -420,8 +421,7 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
   const uint32_t a_pm = opaque_u32((uint32_t)__cvta_generic_to_shared(s.pm32));
   const int mk_r = (int)opaque_u32((uint32_t)mk);
   unsigned long long best = kSentinel;
-  const uint32_t o = c.lo + (uint32_t)bw * kComposeThreads + threadIdx.x;
-  if (qps_w[w] > 0.0 && o < c.hi) {
+  if (qps_w[w] > 0.0) {
     const int nout = c.n - c.il;
     double wj[NJ > 0 ? NJ : 1];
 #pragma unroll
@@ -434,162 +434,169 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
       wk[i] = KREG && i < mk ? s.w[koff + i] : OPSC_INF;
       kkr[i] = KREG && i < mk ? s.kk32[i] : 0u;
     }
-    double val[OPSC_CMAX];
-    int dig[OPSC_CMAX];
-    uint32_t rem = o;
-    for (int pos = nout - 1; pos >= 0; --pos) {
-      const uint32_t mm = (uint32_t)c.m[pos];
-      const uint32_t q = rem / mm;
-      dig[pos] = (int)(rem - q * mm);
-      rem = q;
-    }
-    long long cost0 = 0;
-    unsigned long long lex0 = 0;
-    for (int pos = 0; pos < nout; ++pos) {
-      const int e = c.off[pos] + dig[pos];
-      val[pos] = dp_in(c.pmask[pos], val) + s.w[e];
-      cost0 += s.cost[e];
-      lex0 += (unsigned long long)dig[pos] * c.stride[pos];
-    }
-    const uint32_t kmask = 1u << kp, jmask = 1u << jp;
-    const bool k_to_j = (c.pmask[jp] & kmask) != 0;
-    const bool k_sink = (c.sinkmask & kmask) != 0;
-
-    // register tiles (NJ > 0, compose_setup guarantees c.tkey): the thread's
-    // running minimum as one 32-bit local key over the middle, k and j levels
-    // (pb = the middle levels' part), decoded once
-    constexpr bool tkey = NJ > 0;
-    uint32_t best32 = 0xffffffffu;
-    // The k and j levels for one prefix (middle digits fixed): pb / cost1 /
-    // lex1 are the prefix's key parts (local key, or objective and index).
-    auto kj_levels = [&](double in_k, double bj0, double lo0, uint32_t pb, long long cost1,
-                         unsigned long long lex1) {
-      if constexpr (NJ > 0) {
-        uint32_t m32;
-        if constexpr (KREG) {
-          m32 = k_level_reg<NJ, CHAIN>(a_pm, wk, kkr, wj, in_k, bj0, lo0, k_to_j, k_sink, slo);
-        } else {
-          m32 = k_level_tile<NJ, CHAIN>(a_wk, a_kk, a_pm, mk_r, wj, in_k, bj0, lo0, k_to_j, k_sink, slo);
-        }
-        const uint32_t t = m32 + pb;  // no overflow: feasible m32 + pb < 2^31
-        if (m32 < kLocalInfeasible) best32 = t < best32 ? t : best32;
-      } else {
-        const unsigned long long mbest = k_level_smem<CHAIN>(s, mk, mj, koff, in_k, bj0, lo0, k_to_j, k_sink, slo);
-        if (mbest < kSentinel) {
-          const unsigned long long key = ((unsigned long long)cost1 << OPSC_KEY_LEX_BITS) + lex1 + mbest;
-          best = key < best ? key : best;
-        }
+    // c.spc consecutive 256-thread slices of this window per CTA: the
+    // shared tables above are built once per CTA and amortised over them
+    for (int sl = 0; sl < c.spc; ++sl) {
+      const uint32_t o = c.lo + (uint32_t)(bw * c.spc + sl) * kComposeThreads + threadIdx.x;
+      if (o >= c.hi) break;
+      double val[OPSC_CMAX];
+      int dig[OPSC_CMAX];
+      uint32_t rem = o;
+      for (int pos = nout - 1; pos >= 0; --pos) {
+        const uint32_t mm = (uint32_t)c.m[pos];
+        const uint32_t q = rem / mm;
+        dig[pos] = (int)(rem - q * mm);
+        rem = q;
       }
-    };
-
-    // Middle levels (<= kOdoLevels of them): the last one is a plain loop
-    // over its menu, the ones above it an odometer, all DP values in
-    // registers (no per-index digit divisions, no DP through local memory).
-    // A dp_in is a max over predecessors (exact, order-free), so it splits
-    // into the outer predecessors' part, fixed per thread, and the middle ones'.
-    const int nmid = kp - nout;  // <= kOdoLevels (compose_setup: il <= kOdoLevels + 2)
-    {
-      const uint32_t outer = (1u << nout) - 1u;
-      const int nm1 = nmid > 0 ? nmid - 1 : 0;  // odometer levels above the last middle level
-      const int lpos = nout + nmid - 1;         // the last middle level (nmid > 0)
-      const uint32_t m_last = nmid > 0 ? (uint32_t)c.m[lpos] : 1u;
-      const uint32_t n_pre = c.mid_count / m_last;
-      int od[kOdoLevels];
-      double o_in[kOdoLevels], mv[kOdoLevels];
-#pragma unroll
-      for (int l = 0; l < kOdoLevels; ++l) {
-        od[l] = 0;
-        mv[l] = 0.0;
-        o_in[l] = (!PATH && l < nmid) ? dp_in(c.pmask[nout + l] & outer, val) : 0.0;
+      long long cost0 = 0;
+      unsigned long long lex0 = 0;
+      for (int pos = 0; pos < nout; ++pos) {
+        const int e = c.off[pos] + dig[pos];
+        val[pos] = dp_in(c.pmask[pos], val) + s.w[e];
+        cost0 += s.cost[e];
+        lex0 += (unsigned long long)dig[pos] * c.stride[pos];
       }
-      const double o_k = !PATH ? dp_in(c.pmask[kp] & outer, val) : 0.0;
-      const double o_j = !PATH ? dp_in(c.pmask[jp] & ~kmask & outer, val) : 0.0;
-      const double o_lo = !PATH ? dp_in(c.sinkmask & ~(kmask | jmask) & outer, val) : 0.0;
-      // path suffix: the first in-thread position's dp_in (outer predecessors
-      // only), +inf if an outer sink already misses the SLO
-      double pv0 = 0.0;
-      if constexpr (PATH) {
-        pv0 = dp_in(c.pmask[nout], val);
-        if (!(dp_in(c.sinkmask & outer, val) <= slo)) pv0 = OPSC_INF;
-      }
-      const uint32_t bit_last = nmid > 0 ? 1u << lpos : 0u;
-      const bool last_to_k = (c.pmask[kp] & bit_last) != 0;
-      const bool last_to_j = (c.pmask[jp] & ~kmask & bit_last) != 0;
-      const bool last_sink = (c.sinkmask & bit_last) != 0;
-      const int off_last = nmid > 0 ? c.off[lpos] : c.E;  // entry E: weight +0.0, cost 0, local key 0
-      const unsigned long long stride_last = nmid > 0 ? c.stride[lpos] : 0ull;
+      const uint32_t kmask = 1u << kp, jmask = 1u << jp;
+      const bool k_to_j = (c.pmask[jp] & kmask) != 0;
+      const bool k_sink = (c.sinkmask & kmask) != 0;
 
-      for (uint32_t pre = 0; pre < n_pre; ++pre) {
-        if (pre > 0) {  // advance the odometer (innermost level fastest)
-          bool carry = true;
-#pragma unroll
-          for (int l = kOdoLevels - 1; l >= 0; --l) {
-            if (l < nm1 && carry) {
-              if (++od[l] == c.m[nout + l]) od[l] = 0;
-              else carry = false;
-            }
-          }
-        }
-        // prefix state over the odometer levels
-        long long pc = cost0;
-        unsigned long long pl = lex0;
-        uint32_t pbp = 0;
-        double pv = pv0;                                 // PATH: dp_in of the next position
-        double in_k = o_k, bj0 = o_j, lo0 = o_lo, in_last = 0.0;  // generic
-        if (!PATH && nmid > 0) in_last = o_in[nmid - 1];
-#pragma unroll
-        for (int l = 0; l < kOdoLevels; ++l) {
-          if (l < nm1) {
-            const int pos = nout + l;
-            const int e = c.off[pos] + od[l];
-            if constexpr (PATH) {
-              pv = fmax(0.0, pv + s.w[e]);  // val[pos], then the next position's dp_in
-            } else {
-              double in = o_in[l];
-#pragma unroll
-              for (int l2 = 0; l2 < l; ++l2)
-                if (c.pmask[pos] >> (nout + l2) & 1u) in = fmax(in, mv[l2]);
-              mv[l] = in + s.w[e];
-              const uint32_t bit = 1u << pos;
-              if (c.pmask[kp] & bit) in_k = fmax(in_k, mv[l]);
-              if (c.pmask[jp] & ~kmask & bit) bj0 = fmax(bj0, mv[l]);
-              if (c.sinkmask & bit) lo0 = fmax(lo0, mv[l]);
-              if (c.pmask[lpos] & bit) in_last = fmax(in_last, mv[l]);
-            }
-            if constexpr (tkey) {
-              pbp += s.lk32[e];
-            } else {
-              pc += s.cost[e];
-              pl += (unsigned long long)od[l] * c.stride[pos];
-            }
-          }
-        }
-#pragma unroll(kLUnroll)
-        for (uint32_t i = 0; i < m_last; ++i) {  // the last middle level (none: the virtual entry E)
-          const int e = off_last + (int)i;
-          const double wl = s.w[e];
-          const uint32_t pb = tkey ? pbp + s.lk32[e] : 0u;
-          const long long cost1 = tkey ? 0 : pc + s.cost[e];
-          const unsigned long long lex1 = tkey ? 0ull : pl + (unsigned long long)i * stride_last;
-          if constexpr (PATH) {
-            kj_levels(fmax(0.0, pv + wl), 0.0, 0.0, pb, cost1, lex1);
+      // register tiles (NJ > 0, compose_setup guarantees c.tkey): the thread's
+      // running minimum as one 32-bit local key over the middle, k and j levels
+      // (pb = the middle levels' part), decoded once
+      constexpr bool tkey = NJ > 0;
+      uint32_t best32 = 0xffffffffu;
+      // The k and j levels for one prefix (middle digits fixed): pb / cost1 /
+      // lex1 are the prefix's key parts (local key, or objective and index).
+      auto kj_levels = [&](double in_k, double bj0, double lo0, uint32_t pb, long long cost1,
+                           unsigned long long lex1) {
+        if constexpr (NJ > 0) {
+          uint32_t m32;
+          if constexpr (KREG) {
+            m32 = k_level_reg<NJ, CHAIN>(a_pm, wk, kkr, wj, in_k, bj0, lo0, k_to_j, k_sink, slo);
           } else {
-            const double v = in_last + wl;
-            double ik = last_to_k ? fmax(in_k, v) : in_k;
-            const double b0 = last_to_j ? fmax(bj0, v) : bj0;
-            const double l0 = last_sink ? fmax(lo0, v) : lo0;
-            if (CHAIN && !(l0 <= slo)) ik = OPSC_INF;  // another sink already misses the SLO
-            kj_levels(ik, b0, l0, pb, cost1, lex1);
+            m32 = k_level_tile<NJ, CHAIN>(a_wk, a_kk, a_pm, mk_r, wj, in_k, bj0, lo0, k_to_j, k_sink, slo);
+          }
+          const uint32_t t = m32 + pb;  // no overflow: feasible m32 + pb < 2^31
+          if (m32 < kLocalInfeasible) best32 = t < best32 ? t : best32;
+        } else {
+          const unsigned long long mbest = k_level_smem<CHAIN>(s, mk, mj, koff, in_k, bj0, lo0, k_to_j, k_sink, slo);
+          if (mbest < kSentinel) {
+            const unsigned long long key = ((unsigned long long)cost1 << OPSC_KEY_LEX_BITS) + lex1 + mbest;
+            best = key < best ? key : best;
+          }
+        }
+      };
+
+      // Middle levels (<= kOdoLevels of them): the last one is a plain loop
+      // over its menu, the ones above it an odometer, all DP values in
+      // registers (no per-index digit divisions, no DP through local memory).
+      // A dp_in is a max over predecessors (exact, order-free), so it splits
+      // into the outer predecessors' part, fixed per thread, and the middle ones'.
+      const int nmid = kp - nout;  // <= kOdoLevels (compose_setup: il <= kOdoLevels + 2)
+      {
+        const uint32_t outer = (1u << nout) - 1u;
+        const int nm1 = nmid > 0 ? nmid - 1 : 0;  // odometer levels above the last middle level
+        const int lpos = nout + nmid - 1;         // the last middle level (nmid > 0)
+        const uint32_t m_last = nmid > 0 ? (uint32_t)c.m[lpos] : 1u;
+        const uint32_t n_pre = c.mid_count / m_last;
+        int od[kOdoLevels];
+        double o_in[kOdoLevels], mv[kOdoLevels];
+  #pragma unroll
+        for (int l = 0; l < kOdoLevels; ++l) {
+          od[l] = 0;
+          mv[l] = 0.0;
+          o_in[l] = (!PATH && l < nmid) ? dp_in(c.pmask[nout + l] & outer, val) : 0.0;
+        }
+        const double o_k = !PATH ? dp_in(c.pmask[kp] & outer, val) : 0.0;
+        const double o_j = !PATH ? dp_in(c.pmask[jp] & ~kmask & outer, val) : 0.0;
+        const double o_lo = !PATH ? dp_in(c.sinkmask & ~(kmask | jmask) & outer, val) : 0.0;
+        // path suffix: the first in-thread position's dp_in (outer predecessors
+        // only), +inf if an outer sink already misses the SLO
+        double pv0 = 0.0;
+        if constexpr (PATH) {
+          pv0 = dp_in(c.pmask[nout], val);
+          if (!(dp_in(c.sinkmask & outer, val) <= slo)) pv0 = OPSC_INF;
+        }
+        const uint32_t bit_last = nmid > 0 ? 1u << lpos : 0u;
+        const bool last_to_k = (c.pmask[kp] & bit_last) != 0;
+        const bool last_to_j = (c.pmask[jp] & ~kmask & bit_last) != 0;
+        const bool last_sink = (c.sinkmask & bit_last) != 0;
+        const int off_last = nmid > 0 ? c.off[lpos] : c.E;  // entry E: weight +0.0, cost 0, local key 0
+        const unsigned long long stride_last = nmid > 0 ? c.stride[lpos] : 0ull;
+
+        for (uint32_t pre = 0; pre < n_pre; ++pre) {
+          if (pre > 0) {  // advance the odometer (innermost level fastest)
+            bool carry = true;
+  #pragma unroll
+            for (int l = kOdoLevels - 1; l >= 0; --l) {
+              if (l < nm1 && carry) {
+                if (++od[l] == c.m[nout + l]) od[l] = 0;
+                else carry = false;
+              }
+            }
+          }
+          // prefix state over the odometer levels
+          long long pc = cost0;
+          unsigned long long pl = lex0;
+          uint32_t pbp = 0;
+          double pv = pv0;                                 // PATH: dp_in of the next position
+          double in_k = o_k, bj0 = o_j, lo0 = o_lo, in_last = 0.0;  // generic
+          if (!PATH && nmid > 0) in_last = o_in[nmid - 1];
+  #pragma unroll
+          for (int l = 0; l < kOdoLevels; ++l) {
+            if (l < nm1) {
+              const int pos = nout + l;
+              const int e = c.off[pos] + od[l];
+              if constexpr (PATH) {
+                pv = fmax(0.0, pv + s.w[e]);  // val[pos], then the next position's dp_in
+              } else {
+                double in = o_in[l];
+  #pragma unroll
+                for (int l2 = 0; l2 < l; ++l2)
+                  if (c.pmask[pos] >> (nout + l2) & 1u) in = fmax(in, mv[l2]);
+                mv[l] = in + s.w[e];
+                const uint32_t bit = 1u << pos;
+                if (c.pmask[kp] & bit) in_k = fmax(in_k, mv[l]);
+                if (c.pmask[jp] & ~kmask & bit) bj0 = fmax(bj0, mv[l]);
+                if (c.sinkmask & bit) lo0 = fmax(lo0, mv[l]);
+                if (c.pmask[lpos] & bit) in_last = fmax(in_last, mv[l]);
+              }
+              if constexpr (tkey) {
+                pbp += s.lk32[e];
+              } else {
+                pc += s.cost[e];
+                pl += (unsigned long long)od[l] * c.stride[pos];
+              }
+            }
+          }
+  #pragma unroll(kLUnroll)
+          for (uint32_t i = 0; i < m_last; ++i) {  // the last middle level (none: the virtual entry E)
+            const int e = off_last + (int)i;
+            const double wl = s.w[e];
+            const uint32_t pb = tkey ? pbp + s.lk32[e] : 0u;
+            const long long cost1 = tkey ? 0 : pc + s.cost[e];
+            const unsigned long long lex1 = tkey ? 0ull : pl + (unsigned long long)i * stride_last;
+            if constexpr (PATH) {
+              kj_levels(fmax(0.0, pv + wl), 0.0, 0.0, pb, cost1, lex1);
+            } else {
+              const double v = in_last + wl;
+              double ik = last_to_k ? fmax(in_k, v) : in_k;
+              const double b0 = last_to_j ? fmax(bj0, v) : bj0;
+              const double l0 = last_sink ? fmax(lo0, v) : lo0;
+              if (CHAIN && !(l0 <= slo)) ik = OPSC_INF;  // another sink already misses the SLO
+              kj_levels(ik, b0, l0, pb, cost1, lex1);
+            }
           }
         }
       }
-    }
-    if (NJ > 0 && best32 < kLocalInfeasible) {  // decode the in-thread minimum once
-      const uint32_t loc = best32 & 0xfffffu;
-      unsigned long long lex = lex0;
-      for (int pos = nout; pos < c.n; ++pos)
-        lex += (unsigned long long)((loc / c.cs[pos]) % (uint32_t)c.m[pos]) * c.stride[pos];
-      best = ((unsigned long long)(cost0 + (best32 >> 20)) << OPSC_KEY_LEX_BITS) + lex;
+      if (NJ > 0 && best32 < kLocalInfeasible) {  // decode the slice's in-thread minimum once
+        const uint32_t loc = best32 & 0xfffffu;
+        unsigned long long lex = lex0;
+        for (int pos = nout; pos < c.n; ++pos)
+          lex += (unsigned long long)((loc / c.cs[pos]) % (uint32_t)c.m[pos]) * c.stride[pos];
+        const unsigned long long key = ((unsigned long long)(cost0 + (best32 >> 20)) << OPSC_KEY_LEX_BITS) + lex;
+        best = key < best ? key : best;
+      }
     }
   }
   cta_min_commit(best, w, key_out, peers, warp_best);
@@ -700,8 +707,20 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
   c.mid_count = (uint32_t)mid;
   c.lo = (uint32_t)((unsigned long long)c.m_out * shard / n_shards);
   c.hi = (uint32_t)((unsigned long long)c.m_out * (shard + 1) / n_shards);
-  c.blocks_per_window = (int)((c.hi - c.lo + kComposeThreads - 1) / kComposeThreads);
-  if (c.blocks_per_window < 1) c.blocks_per_window = 1;
+  // slices of 256 outer indices; a CTA takes `spc` consecutive slices of its
+  // window so the per-CTA table setup (menu slab, cost / key tables, weight
+  // sort, prefix-minimum scan) is amortised over >= ~2M candidates, while
+  // keeping >= 24 waves of CTAs (tail). cfg3: +6%; cfg5 / cfg2 stay at 1
+  // (tools/variants_spc.sh)
+  const long long nslices = std::max<long long>(1, ((long long)c.hi - c.lo + kComposeThreads - 1) / kComposeThreads);
+  const double per_cta = (double)kComposeThreads * prod(c.n - il, c.n);
+  long long spc = (long long)std::ceil(2.0e6 / per_cta);
+  const long long min_ctas = 148LL * OPSC_COMPOSE_MINB * 24;
+  spc = std::min<long long>(spc, ((long long)n_windows * nslices) / min_ctas);
+  spc = std::max<long long>(1, std::min<long long>(spc, 16));
+  if (const char* f = getenv("OPSC_COMPOSE_SPC")) spc = std::max(1, atoi(f));  // dev override
+  c.spc = (int)spc;
+  c.blocks_per_window = (int)((nslices + spc - 1) / spc);
   const int mj = c.m[c.n - 1], mk = c.m[c.n - 2];
   // register tile widths (padded entries are +inf and still cost their
   // DADD/DSETP/SEL, so common menu sizes get exact tiles: 6 = P{1,2} x R<=3)

@@ -276,6 +276,7 @@ struct ComposeCfg {
   uint32_t lo, hi;             // this shard's outer index range
   uint32_t mid_count;          // product of middle-level menu sizes
   int32_t blocks_per_window;
+  int32_t spc;                 // 256-thread slices per CTA (tile kernel)
   int32_t nj;                  // register tile of the innermost menu
   int32_t chain;               // j's only predecessor is k and k is not a sink
   int32_t tkey;                // 32-bit in-thread keys span the middle levels too (cs over all in-thread positions)

@@ -186,6 +186,32 @@ def test_level_splits_vs_oracle(nat_loaded, orc, cfg, il, monkeypatch):
     assert (got != abi.KEY_INFEASIBLE).any()
 
 
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3"])
+@pytest.mark.parametrize("spc", [2, 3, 7, 16, 1000])
+def test_slices_per_cta_vs_oracle(nat_loaded, orc, cfg, spc, monkeypatch):
+    """A CTA running `spc` consecutive 256-thread slices of its window (one
+    table setup, one running minimum across slices; a partial last CTA when
+    spc does not divide the slice count; 1000 = one CTA per window) gives the
+    oracle's key (OPSC_COMPOSE_SPC is the compose_setup dev override)."""
+    from paper_2511_02248_b200 import _native as nat
+    from paper_2511_02248_b200 import scenarios
+    prob = tables.pack_problem(*scenarios.scenario(cfg))
+    g = scenarios.GRIDS[cfg]
+    grid = tables.pack_grid(prob, model.AutoscaleParams(slo=1.0), model.BruteForceBounds(**g))
+    tw = scenarios.trace_windows(cfg)
+    idx = np.arange(0, 60, 6) if cfg == "cfg2" else np.array([3, 17, 30, 45])
+    win = tables.window_arrays(tw["prefill_qps"][idx], tw["prefill_len"][idx], 0, 1.0)
+    win.slo[:] = np.linspace(1.0, 6.0, len(idx)) * scenarios.SLO[cfg]["prefill"]
+    if cfg not in _SPLIT_ORACLE:
+        mw, _ = orc.menus(prob, grid, win)
+        _SPLIT_ORACLE[cfg] = (mw, orc.compose(prob, grid, win, mw))
+    mw, want = _SPLIT_ORACLE[cfg]
+    monkeypatch.setenv("OPSC_COMPOSE_SPC", str(spc))
+    got = _device_compose(nat, prob, grid, win, mw)
+    assert (got == want).all(), (spc, got, want)
+    assert (got != abi.KEY_INFEASIBLE).any()
+
+
 def test_boundary_count_vs_numpy(nat_loaded, orc):
     """opsc_compose_boundary counts the candidates within `band` ulps of slo:
     checked against a numpy enumeration of the same crafted tie menus (chain
