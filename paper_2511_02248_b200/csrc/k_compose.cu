@@ -224,6 +224,7 @@ compose_flat_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant_
                     const double* __restrict__ menu_w, const double* __restrict__ slo_w,
                     const double* __restrict__ qps_w, unsigned long long* __restrict__ key_out,
                     const __grid_constant__ PeerKeys peers, double band_ulps = 0.0) {
+  pdl_wait();
   __shared__ unsigned long long warp_best[kComposeThreads / 32];
   const int w = blockIdx.x / c.blocks_per_window;
   const int bw = blockIdx.x - w * c.blocks_per_window;
@@ -286,6 +287,7 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
                const double* __restrict__ menu_w, const double* __restrict__ slo_w,
                const double* __restrict__ qps_w, unsigned long long* __restrict__ key_out,
                const __grid_constant__ PeerKeys peers) {
+  pdl_wait();
   constexpr bool CHAIN = MODE >= 1, PATH = MODE == 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ unsigned long long warp_best[kComposeThreads / 32];
@@ -789,8 +791,8 @@ static cudaError_t launch_t(const ComposeCfg& c, const OpscGrid& g, int n_window
   }
   const long long blocks = (long long)n_windows * c.blocks_per_window;
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  compose_kernel<NJ, MODE, KREG><<<(unsigned)blocks, kComposeThreads, smem, s>>>(c, g, menu_w, slo, qps, key, pk);
-  return cudaGetLastError();
+  return launch_pdl(compose_kernel<NJ, MODE, KREG>, dim3((unsigned)blocks), dim3(kComposeThreads), smem, s, c, g, menu_w,
+                    slo, qps, key, pk);
 }
 
 template <int NJ, bool KREG>
@@ -824,8 +826,8 @@ cudaError_t launch_compose(const ComposeCfg& c, const OpscGrid& g, int n_windows
     if (c.fhi <= c.flo) return cudaSuccess;
     const long long blocks = (long long)n_windows * c.blocks_per_window;
     if (blocks > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    compose_flat_kernel<false><<<(unsigned)blocks, kComposeThreads, 0, s>>>(c, g, menu_w, slo, qps, key, pk);
-    return cudaGetLastError();
+    return launch_pdl(compose_flat_kernel<false>, dim3((unsigned)blocks), dim3(kComposeThreads), 0, s, c, g, menu_w, slo,
+                      qps, key, pk, 0.0);
   }
   switch (c.nj) {
     case 4: return launch_nj<4>(c, g, n_windows, menu_w, slo, qps, key, s, pk);

@@ -135,6 +135,8 @@ __global__ void __launch_bounds__(32 * kMatWarps) materialize_kernel(const __gri
                                                                      int config_order,
                                                                      const __grid_constant__ OpscPlaceSpec pl,
                                                                      const __grid_constant__ OpscDecisions out) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double s_wt[kMatWarps][OPSC_MAX_OPS], s_T[kMatWarps][OPSC_MAX_OPS];
   __shared__ double s_e1[kMatWarps][OPSC_MAX_OPS], s_e2[kMatWarps][OPSC_MAX_OPS];
   __shared__ MatScratch s_scr[kMatWarps];
@@ -235,8 +237,8 @@ __global__ void __launch_bounds__(32 * kMatWarps) materialize_kernel(const __gri
 cudaError_t launch_materialize(const OpscDag& d, OpscWindows w, int config_order, const OpscPlaceSpec& p,
                                OpscDecisions out, cudaStream_t s) {
   if (w.n <= 0) return cudaSuccess;
-  materialize_kernel<<<(w.n + kMatWarps - 1) / kMatWarps, 32 * kMatWarps, 0, s>>>(d, w, config_order, p, out);
-  return cudaGetLastError();
+  return launch_pdl(materialize_kernel, dim3((w.n + kMatWarps - 1) / kMatWarps), dim3(32 * kMatWarps), 0, s, d, w,
+                    config_order, p, out);
 }
 
 }  // namespace opsc

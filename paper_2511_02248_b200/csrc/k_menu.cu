@@ -14,6 +14,8 @@ namespace opsc {
 
 __global__ void init_kernel(int n, const double* __restrict__ qps, uint32_t* __restrict__ status,
                             unsigned long long* __restrict__ key, uint8_t* __restrict__ feasible) {
+  pdl_trigger();
+  pdl_wait();
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= n) return;
   status[w] = qps[w] > 0.0 ? 0u : OPSC_W_IDLE;
@@ -24,8 +26,7 @@ __global__ void init_kernel(int n, const double* __restrict__ qps, uint32_t* __r
 cudaError_t launch_init(int n, const double* qps, uint32_t* status, unsigned long long* key,
                         uint8_t* feasible, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  init_kernel<<<(n + 255) / 256, 256, 0, s>>>(n, qps, status, key, feasible);
-  return cudaGetLastError();
+  return launch_pdl(init_kernel, dim3((n + 255) / 256), dim3(256), 0, s, n, qps, status, key, feasible);
 }
 
 __global__ void fill_keys_kernel(unsigned long long* key, int n) {
@@ -44,6 +45,8 @@ __global__ void __launch_bounds__(256) menu_build_kernel(const __grid_constant__
                                                          const __grid_constant__ OpscWindows win,
                                                          double* __restrict__ menu_w,
                                                          uint32_t* __restrict__ status) {
+  pdl_trigger();
+  pdl_wait();
   const int E = g.menu_off[d.n_ops];
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)win.n * E) return;
@@ -68,8 +71,7 @@ cudaError_t launch_menu_build(const OpscDag& d, const OpscGrid& g, OpscWindows w
                               uint32_t* status, cudaStream_t s) {
   const long long total = (long long)w.n * g.menu_off[d.n_ops];
   if (total <= 0) return cudaSuccess;
-  menu_build_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(d, g, w, menu_w, status);
-  return cudaGetLastError();
+  return launch_pdl(menu_build_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, s, d, g, w, menu_w, status);
 }
 
 // One warp per (window, op): does some (P in params, B <= params.b_max) have
@@ -79,6 +81,8 @@ cudaError_t launch_menu_build(const OpscDag& d, const OpscGrid& g, OpscWindows w
 // including the first P with a stable B, as in the sequential scan.
 __global__ void stability_kernel(const __grid_constant__ OpscDag d, const __grid_constant__ OpscGrid g,
                                  const __grid_constant__ OpscWindows win, uint32_t* __restrict__ status) {
+  pdl_trigger();
+  pdl_wait();
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= win.n * d.n_ops) return;
@@ -112,13 +116,14 @@ cudaError_t launch_stability(const OpscDag& d, const OpscGrid& g, OpscWindows w,
                              cudaStream_t s) {
   const long long threads = (long long)w.n * d.n_ops * 32;
   if (threads <= 0) return cudaSuccess;
-  stability_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(d, g, w, status);
-  return cudaGetLastError();
+  return launch_pdl(stability_kernel, dim3((unsigned)((threads + 127) / 128)), dim3(128), 0, s, d, g, w, status);
 }
 
 // One warp per (window, op): min over finite entries of (weight, entry).
 __global__ void fallback_kernel(int n_ops, int n_windows, const __grid_constant__ OpscGrid g,
                                 const double* __restrict__ menu_w, int32_t* __restrict__ fb) {
+  pdl_trigger();
+  pdl_wait();
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= n_windows * n_ops) return;
@@ -145,14 +150,16 @@ cudaError_t launch_fallback(const OpscDag& d, const OpscGrid& g, int n_windows, 
                             int32_t* fb, cudaStream_t s) {
   const long long threads = (long long)n_windows * d.n_ops * 32;
   if (threads <= 0) return cudaSuccess;
-  fallback_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(d.n_ops, n_windows, g, menu_w, fb);
-  return cudaGetLastError();
+  return launch_pdl(fallback_kernel, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s, d.n_ops, n_windows, g,
+                    menu_w, fb);
 }
 
 __global__ void decode_kernel(int n_ops, int n_windows, const __grid_constant__ OpscGrid g,
                               const unsigned long long* __restrict__ key, const int32_t* __restrict__ fb,
                               int16_t* __restrict__ cfg, uint8_t* __restrict__ feasible,
                               uint32_t* __restrict__ status) {
+  pdl_trigger();
+  pdl_wait();
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= n_windows) return;
   feasible[w] = 0;
@@ -193,9 +200,8 @@ cudaError_t launch_decode(const OpscDag& d, const OpscGrid& g, int n_windows,
                           const unsigned long long* key, const int32_t* fb, int16_t* cfg,
                           uint8_t* feasible, uint32_t* status, cudaStream_t s) {
   if (n_windows <= 0) return cudaSuccess;
-  decode_kernel<<<(n_windows + 127) / 128, 128, 0, s>>>(d.n_ops, n_windows, g, key, fb, cfg, feasible,
-                                                        status);
-  return cudaGetLastError();
+  return launch_pdl(decode_kernel, dim3((n_windows + 127) / 128), dim3(128), 0, s, d.n_ops, n_windows, g, key, fb,
+                    cfg, feasible, status);
 }
 
 }  // namespace opsc

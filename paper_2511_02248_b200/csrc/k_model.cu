@@ -113,6 +113,8 @@ __global__ void __launch_bounds__(1024) model_grid_kernel(const __grid_constant_
                                                           uint32_t* __restrict__ status,
                                                           const double* __restrict__ lt_all,
                                                           const uint8_t* __restrict__ ls_all) {
+  pdl_trigger();
+  pdl_wait();
   const OpscDag& d = a.d;
   const OpscModelSpec& m = a.m;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -213,6 +215,8 @@ __global__ void __launch_bounds__(1024) model_grid_kernel(const __grid_constant_
 // thread per (window, B, R, op): weight of op under uniform (B, R) at P_base
 __global__ void model_tab_weights(const __grid_constant__ ModelArgs a, const __grid_constant__ OpscWindows win,
                                   double* __restrict__ wt, uint8_t* __restrict__ wst) {
+  pdl_trigger();
+  pdl_wait();
   const OpscDag& d = a.d;
   const OpscModelSpec& m = a.m;
   const int n = d.n_ops;
@@ -238,6 +242,8 @@ __global__ void model_tab_weights(const __grid_constant__ ModelArgs a, const __g
 __global__ void model_tab_latency(const __grid_constant__ ModelArgs a, int n_windows,
                                   const double* __restrict__ wt, const uint8_t* __restrict__ wst,
                                   double* __restrict__ lt, uint8_t* __restrict__ ls) {
+  pdl_trigger();
+  pdl_wait();
   const OpscDag& d = a.d;
   const int n = d.n_ops;
   const long long total = (long long)n_windows * a.m.b_cap * a.m.r_cap;
@@ -294,8 +300,8 @@ cudaError_t launch_model_grid(const OpscDag& d, const OpscModelSpec& m, OpscWind
     if (e != cudaSuccess) return e;
   }
   if (!table) {
-    model_grid_kernel<false><<<w.n, nwarps * 32, smem, s>>>(a, w, cfg, feasible, status, nullptr, nullptr);
-    return cudaGetLastError();
+    return launch_pdl(model_grid_kernel<false>, dim3(w.n), dim3(nwarps * 32), smem, s, a, w, cfg, feasible, status,
+                      (const double*)nullptr, (const uint8_t*)nullptr);
   }
   const size_t pts = (size_t)w.n * m.b_cap * m.r_cap;
   double* wt = (double*)table_ws;
@@ -307,12 +313,14 @@ cudaError_t launch_model_grid(const OpscDag& d, const OpscModelSpec& m, OpscWind
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long t1 = (long long)pts * d.n_ops;
   const int g1 = (int)((t1 + 127) / 128 < (long long)sms * 32 ? (t1 + 127) / 128 : (long long)sms * 32);
-  model_tab_weights<<<g1, 128, 0, s>>>(a, w, wt, wst);
+  cudaError_t e = launch_pdl(model_tab_weights, dim3(g1), dim3(128), 0, s, a, w, wt, wst);
+  if (e != cudaSuccess) return e;
   const int g2 = (int)(((long long)pts + 127) / 128 < (long long)sms * 32 ? ((long long)pts + 127) / 128
                                                                           : (long long)sms * 32);
-  model_tab_latency<<<g2, 128, 0, s>>>(a, w.n, wt, wst, lt, ls);
-  model_grid_kernel<true><<<w.n, nwarps * 32, smem, s>>>(a, w, cfg, feasible, status, lt, ls);
-  return cudaGetLastError();
+  e = launch_pdl(model_tab_latency, dim3(g2), dim3(128), 0, s, a, w.n, (const double*)wt, (const uint8_t*)wst, lt, ls);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(model_grid_kernel<true>, dim3(w.n), dim3(nwarps * 32), smem, s, a, w, cfg, feasible, status,
+                    (const double*)lt, (const uint8_t*)ls);
 }
 
 }  // namespace opsc

@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <math_constants.h>
 #include <stdint.h>
 
@@ -16,6 +17,16 @@
 #define OPSC_LEXMASK ((1ull << OPSC_KEY_LEX_BITS) - 1ull)
 
 namespace opsc {
+
+// Programmatic dependent launch (sm_90+): the planning pipeline's kernels are
+// launched with programmatic stream serialization, so a kernel's launch and
+// CTA rasterisation overlap its predecessor's tail. Every such kernel calls
+// pdl_wait() before touching memory a predecessor wrote (griddepcontrol.wait
+// returns once the preceding grid has completed and its writes are visible);
+// small kernels call pdl_trigger() first to release their dependents early.
+// Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // perfmodel.py:62-64 and :133-157. At the planners' sm_share = 1.0 the
 // SM-share factor is exactly 1: demand = min(1, s0+s1*B*L) <= 1 gives
@@ -288,6 +299,31 @@ struct ComposeCfg {
 };
 
 namespace opsc {
+// Host launch with the programmatic-stream-serialization attribute (see
+// pdl_wait); OPSC_NO_PDL=1 launches plainly (A/B switch).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* f = getenv("OPSC_NO_PDL");
+    return !(f && f[0] == '1');
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // launchers (defined in the k_*.cu files), all asynchronous on `s`
 cudaError_t launch_init(int n_windows, const double* qps, uint32_t* status, unsigned long long* key,
                         uint8_t* feasible, cudaStream_t s);
