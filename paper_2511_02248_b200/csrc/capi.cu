@@ -109,6 +109,8 @@ struct OpscContext {
   size_t cap_mtab = 0;
   cudaStream_t side = nullptr;      // K3 runs here concurrently with greedy phase 1
   cudaEvent_t fork = nullptr, join = nullptr;
+  unsigned char* h_stage = nullptr;  // pinned staging for pageable caller buffers
+  size_t cap_stage = 0;
 };
 
 namespace {
@@ -195,6 +197,69 @@ OpscDecisions dev_decisions(const OpscContext* c) {
 }
 
 bool valid_dag(const OpscDag* d) { return d && d->n_ops >= 1 && d->n_ops <= OPSC_MAX_OPS; }
+
+bool pageable(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+// Host side of the host-buffer call. Pinned caller buffers are copied
+// directly; pageable ones (numpy arrays from the Python API) go through the
+// context's pinned staging buffer, so every copy is a true async DMA instead
+// of a driver-staged synchronous one (~10 us each for the ~20 small arrays).
+struct HostIO {
+  OpscContext* c;
+  cudaStream_t s;
+  bool stage;
+  size_t off = 0;
+  struct Out {
+    void* dst;
+    size_t at, bytes;
+  };
+  Out outs[24];
+  int n_out = 0;
+  unsigned char* slot(size_t bytes) {
+    unsigned char* p = c->h_stage + off;
+    off += (bytes + 15) & ~(size_t)15;
+    return p;
+  }
+  cudaError_t h2d(void* dev, const void* host, size_t bytes) {
+    if (!bytes) return cudaSuccess;
+    if (!stage) return cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, s);
+    unsigned char* p = slot(bytes);
+    memcpy(p, host, bytes);
+    return cudaMemcpyAsync(dev, p, bytes, cudaMemcpyHostToDevice, s);
+  }
+  cudaError_t d2h(void* host, const void* dev, size_t bytes) {
+    if (!host || !bytes) return cudaSuccess;
+    if (!stage) return cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, s);
+    const size_t at = off;
+    unsigned char* p = slot(bytes);
+    outs[n_out++] = Out{host, at, bytes};
+    return cudaMemcpyAsync(p, dev, bytes, cudaMemcpyDeviceToHost, s);
+  }
+  void finish() {  // after the stream synchronised
+    for (int i = 0; i < n_out; ++i) memcpy(outs[i].dst, c->h_stage + outs[i].at, outs[i].bytes);
+  }
+};
+
+int ensure_stage(OpscContext* c, size_t bytes) {
+  if (bytes <= c->cap_stage) return OPSC_OK;
+  if (c->h_stage) cudaFreeHost(c->h_stage);
+  c->h_stage = nullptr;
+  c->cap_stage = 0;
+  if (cudaHostAlloc((void**)&c->h_stage, bytes, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    return OPSC_ERR_CUDA;
+  }
+  c->cap_stage = bytes;
+  return OPSC_OK;
+}
 
 // small batches tabulate every (B, R) point (4M weights max, ~40 MB)
 constexpr long long kModelTablePoints = 1ll << 22;
@@ -425,6 +490,7 @@ int opsc_ctx_destroy(OpscContext* c) {
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->join) cudaEventDestroy(c->join);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
   delete c;
   return OPSC_OK;
 }
@@ -532,13 +598,22 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
   } while (0)
   if (!c->ev0) CK(cudaEventCreate(&c->ev0));
   if (!c->ev1) CK(cudaEventCreate(&c->ev1));
+  const size_t wn = (size_t)W * n;
+  HostIO io{c, s, pageable(win.qps) || pageable(out.cfg) || pageable(out.latency)};
+  if (io.stage) {
+    const size_t in_b = W * (3 * sizeof(double) + sizeof(int32_t) + 1) + ndev * sizeof(double);
+    const size_t out_b = W * (4 * sizeof(double) + 5 * sizeof(int32_t) + 1) + wn * (3 * sizeof(int16_t) + 2) +
+                         wn * OPSC_PRED_FIELDS * sizeof(double) + W * tcap * sizeof(OpscTraceEntry);
+    rc = ensure_stage(c, in_b + out_b + 24 * 16);
+    if (rc) return rc;
+  }
   CK(cudaEventRecord(c->ev0, s));  // device-side span: first H2D .. last D2H
-  CK(cudaMemcpyAsync(c->qps, win.qps, W * sizeof(double), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(c->seq_len, win.seq_len, W * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(c->phase, win.phase, W * sizeof(uint8_t), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(c->slo, win.slo, W * sizeof(double), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(c->eps, win.eps, W * sizeof(double), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(c->mem_cap, place->mem_cap, ndev * sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(io.h2d(c->qps, win.qps, W * sizeof(double)));
+  CK(io.h2d(c->seq_len, win.seq_len, W * sizeof(int32_t)));
+  CK(io.h2d(c->phase, win.phase, W * sizeof(uint8_t)));
+  CK(io.h2d(c->slo, win.slo, W * sizeof(double)));
+  CK(io.h2d(c->eps, win.eps, W * sizeof(double)));
+  CK(io.h2d(c->mem_cap, place->mem_cap, ndev * sizeof(double)));
   OpscPlaceSpec dplace = *place;
   dplace.mem_cap = c->mem_cap;
   const OpscWindows dw = dev_windows(c, W);
@@ -581,25 +656,23 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
     CK(launch_materialize(*dag, dw, 1, dplace, dd, s));
   }
   c->launches++;
-  const size_t wn = (size_t)W * n;
-  if (out.key) CK(cudaMemcpyAsync(out.key, c->key, W * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  if (out.cfg) CK(cudaMemcpyAsync(out.cfg, c->cfg, wn * 3 * sizeof(int16_t), cudaMemcpyDeviceToHost, s));
-  if (out.feasible) CK(cudaMemcpyAsync(out.feasible, c->feasible, W, cudaMemcpyDeviceToHost, s));
-  if (out.status) CK(cudaMemcpyAsync(out.status, c->status, W * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-  if (out.latency) CK(cudaMemcpyAsync(out.latency, c->latency, W * sizeof(double), cudaMemcpyDeviceToHost, s));
-  if (out.objective) CK(cudaMemcpyAsync(out.objective, c->objective, W * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  if (out.path) CK(cudaMemcpyAsync(out.path, c->path, wn, cudaMemcpyDeviceToHost, s));
-  if (out.pred) CK(cudaMemcpyAsync(out.pred, c->pred, wn * OPSC_PRED_FIELDS * sizeof(double), cudaMemcpyDeviceToHost, s));
-  if (out.stable) CK(cudaMemcpyAsync(out.stable, c->stable, wn, cudaMemcpyDeviceToHost, s));
-  if (out.energy) CK(cudaMemcpyAsync(out.energy, c->energy, W * sizeof(double), cudaMemcpyDeviceToHost, s));
-  if (out.memory) CK(cudaMemcpyAsync(out.memory, c->memory, W * sizeof(double), cudaMemcpyDeviceToHost, s));
-  if (out.devices) CK(cudaMemcpyAsync(out.devices, c->devices, W * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  if (tcap && out.trace_len)
-    CK(cudaMemcpyAsync(out.trace_len, c->trace_len, W * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  if (tcap && out.trace)
-    CK(cudaMemcpyAsync(out.trace, c->trace, W * tcap * sizeof(OpscTraceEntry), cudaMemcpyDeviceToHost, s));
+  CK(io.d2h(out.key, c->key, W * sizeof(int64_t)));
+  CK(io.d2h(out.cfg, c->cfg, wn * 3 * sizeof(int16_t)));
+  CK(io.d2h(out.feasible, c->feasible, W));
+  CK(io.d2h(out.status, c->status, W * sizeof(uint32_t)));
+  CK(io.d2h(out.latency, c->latency, W * sizeof(double)));
+  CK(io.d2h(out.objective, c->objective, W * sizeof(int32_t)));
+  CK(io.d2h(out.path, c->path, wn));
+  CK(io.d2h(out.pred, c->pred, wn * OPSC_PRED_FIELDS * sizeof(double)));
+  CK(io.d2h(out.stable, c->stable, wn));
+  CK(io.d2h(out.energy, c->energy, W * sizeof(double)));
+  CK(io.d2h(out.memory, c->memory, W * sizeof(double)));
+  CK(io.d2h(out.devices, c->devices, W * sizeof(int32_t)));
+  if (tcap) CK(io.d2h(out.trace_len, c->trace_len, W * sizeof(int32_t)));
+  if (tcap) CK(io.d2h(out.trace, c->trace, W * tcap * sizeof(OpscTraceEntry)));
   CK(cudaEventRecord(c->ev1, s));
   CK(cudaStreamSynchronize(s));
+  io.finish();
   c->timed = true;
 #undef CK
   return OPSC_OK;
