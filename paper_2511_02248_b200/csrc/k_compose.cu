@@ -44,6 +44,13 @@ namespace opsc {
 #ifndef OPSC_COMPOSE_THREADS
 #define OPSC_COMPOSE_THREADS 256
 #endif
+#ifndef OPSC_COMPOSE_MINB_SMALL
+// path-suffix kernels with register tiles of <= 8 entries fit 40 registers
+// without spills: 6 CTAs (48 warps) per SM instead of 3 -- cfg2 5.2e12 ->
+// 6.2e12, cfg3 5.6e12 -> 6.5e12 candidates/s (tools/variants_minb_small.sh;
+// the generic-DAG modes spill there and keep OPSC_COMPOSE_MINB)
+#define OPSC_COMPOSE_MINB_SMALL 6
+#endif
 #ifndef OPSC_COMPOSE_MINB
 #define OPSC_COMPOSE_MINB 3  // 80 registers, no spills: 7.38e12 vs 7.28e12 candidates/s at 4 CTAs/SM (64 regs, spills)
 #endif
@@ -282,7 +289,8 @@ compose_flat_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant_
 // 2 path suffix (every in-thread position fed by the previous one only, j the
 // only in-thread sink; outer sinks checked once per thread).
 template <int NJ, int MODE, bool KREG>
-__global__ void __launch_bounds__(kComposeThreads, OPSC_COMPOSE_MINB)
+__global__ void __launch_bounds__(kComposeThreads,
+                                  NJ > 0 && NJ <= 8 && MODE == 2 ? OPSC_COMPOSE_MINB_SMALL : OPSC_COMPOSE_MINB)
 compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ OpscGrid g,
                const double* __restrict__ menu_w, const double* __restrict__ slo_w,
                const double* __restrict__ qps_w, unsigned long long* __restrict__ key_out,
