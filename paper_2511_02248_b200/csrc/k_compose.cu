@@ -51,6 +51,9 @@ namespace opsc {
 // the generic-DAG modes spill there and keep OPSC_COMPOSE_MINB)
 #define OPSC_COMPOSE_MINB_SMALL 6
 #endif
+#ifndef OPSC_COMPOSE_MINB_PATH
+#define OPSC_COMPOSE_MINB_PATH 4  // path-suffix kernels with 12..32-entry tiles: 64 registers, no spills (cfg5 8.16e12 -> 8.20e12; 5 / 6: 8.15 / 8.16, tools/variants_minb_path.sh)
+#endif
 #ifndef OPSC_COMPOSE_MINB
 #define OPSC_COMPOSE_MINB 3  // 80 registers, no spills: 7.38e12 vs 7.28e12 candidates/s at 4 CTAs/SM (64 regs, spills)
 #endif
@@ -290,7 +293,9 @@ compose_flat_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant_
 // only in-thread sink; outer sinks checked once per thread).
 template <int NJ, int MODE, bool KREG>
 __global__ void __launch_bounds__(kComposeThreads,
-                                  NJ > 0 && NJ <= 8 && MODE == 2 ? OPSC_COMPOSE_MINB_SMALL : OPSC_COMPOSE_MINB)
+                                  NJ > 0 && NJ <= 8 && MODE == 2   ? OPSC_COMPOSE_MINB_SMALL
+                                  : NJ > 8 && MODE == 2            ? OPSC_COMPOSE_MINB_PATH
+                                                                   : OPSC_COMPOSE_MINB)
 compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ OpscGrid g,
                const double* __restrict__ menu_w, const double* __restrict__ slo_w,
                const double* __restrict__ qps_w, unsigned long long* __restrict__ key_out,
