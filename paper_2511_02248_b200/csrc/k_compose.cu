@@ -24,14 +24,20 @@
 //         DSETP lat <= slo               (SLO mask)
 //         SEL   count = i + 1            (ascending scan: the last hit is the
 //                                         length of the feasible prefix)
-//     with no loop-carried dependency, so warps issue back to back. The
-//     per-k fold works on 32-bit local keys (cost_k + cost_j, local (k, j)
-//     index) from 32-bit shared addresses, converted to the u64 key once per
-//     prefix. (A high-word mask on the FMA pipe was measured and rejected:
-//     DESIGN.md, instruction-mix paragraph; tools/probe/cand_probe.cu);
-//   * per k entry the cheapest feasible (k, j) pair is folded into the
-//     prefix's minimum; CTA result = warp-shuffle u64 min -> smem -> one
-//     atomicMin per CTA.
+//     with no loop-carried dependency, so warps issue back to back. (A
+//     high-word mask on the FMA pipe and integer-pipe compares were measured
+//     and rejected: DESIGN.md, instruction-mix paragraph;
+//     tools/probe/cand_probe.cu);
+//   * keys: each thread keeps one 32-bit running minimum over all its
+//     in-thread candidates (cost << 20 | compact lexicographic index of the
+//     middle, k and j digits), one fused add+min per k entry, decoded to the
+//     u64 key once per 256-thread slice; CTA result = warp-shuffle u64 min ->
+//     smem -> one atomicMin per CTA;
+//   * the middle levels run as a register odometer over a plain inner loop
+//     (the last middle level); template MODE 2 ("path suffix") covers every
+//     DAG whose in-thread positions form a path (the chains and the
+//     multimodal DAG); a CTA takes `spc` consecutive slices of its window;
+//   * launched with programmatic stream serialization (pdl_wait at entry).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
