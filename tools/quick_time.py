@@ -19,7 +19,7 @@ grid = tables.pack_grid(prob, model.AutoscaleParams(slo=1.0), model.BruteForceBo
 tw = scenarios.trace_windows(CFG)
 win = tables.window_arrays(tw["prefill_qps"], tw["prefill_len"], 0, scenarios.SLO[CFG]["prefill"])
 dev = torch.device("cuda:0")
-t = {k: torch.from_numpy(np.ascontiguousarray(getattr(win, k))).to(dev) for k in ("qps", "seq_len", "phase", "slo", "eps")}
+t = {k: torch.from_numpy(np.array(getattr(win, k))).to(dev) for k in ("qps", "seq_len", "phase", "slo", "eps")}
 dw = abi.OpscWindows(); dw.n = win.n
 for k in t: setattr(dw, k, t[k].data_ptr())
 E = grid.menu_off[prob.n_ops]
