@@ -276,3 +276,36 @@ def test_public_greedy_api(nat):
     for p, plan in zip(pts, batch):
         assert planners.greedy_autoscale(dag, prof, p, params).to_dict() == plan.to_dict()
         assert plan.trace  # the move trace travels with the plan
+
+
+@pytest.mark.parametrize("mode", [abi.MODE_ORACLE, abi.MODE_MODEL, abi.MODE_OPERATOR])
+def test_host_buffers_pinned_vs_pageable(nat, mode):
+    """opsc_plan_windows_host stages pageable caller buffers (numpy) through
+    the context's pinned buffer and copies pinned ones directly: both give
+    the same bytes in every output field, and over repeated calls with a
+    changing window count (staging reuse and growth)."""
+    import torch
+
+    def pin(a):  # a pinned (page-locked) copy of a host array, any dtype
+        buf = torch.empty(max(a.nbytes, 1), dtype=torch.uint8, pin_memory=True).numpy()
+        out = buf[:a.nbytes].view(a.dtype).reshape(a.shape)
+        out[...] = a
+        return out
+
+    prob = tables.pack_problem(*scenarios.scenario("cfg2"))
+    params = model.AutoscaleParams(slo=scenarios.SLO["cfg2"]["prefill"])
+    grid = _grid("cfg2", prob)
+    spec = tables.pack_model(prob, params)
+    gspec = tables.pack_greedy(prob, params)
+    ctx = nat.context()
+    cap = 256 if mode == abi.MODE_OPERATOR else 0
+    for idx in (np.arange(0, 60, 7), np.arange(3, 5), np.arange(0, 60)):
+        win = _scenario_windows("cfg2", "prefill", idx)
+        a = ctx.plan_windows(mode, prob, win, grid=grid, model=spec, greedy=gspec, trace_cap=cap)
+        pw = tables.WindowArrays(*(pin(getattr(win, k)) for k in ("qps", "seq_len", "phase", "slo", "eps")))
+        po = tables.DecisionArrays(win.n, prob.n_ops, cap)
+        for f in tables.DecisionArrays.FIELDS + (("trace_len", "trace") if cap else ()):
+            setattr(po, f, pin(getattr(po, f)))
+        b = ctx.plan_windows(mode, prob, pw, grid=grid, model=spec, greedy=gspec, out=po, trace_cap=cap)
+        for f in tables.DecisionArrays.FIELDS + (("trace_len",) if cap else ()):
+            assert getattr(a, f).tobytes() == getattr(b, f).tobytes(), (mode, len(idx), f)
