@@ -13,6 +13,8 @@ from paper_2511_02248_b200 import abi, device, model, scenarios, tables  # noqa:
 
 mode = {"model": abi.MODE_MODEL, "operator": abi.MODE_OPERATOR, "oracle": abi.MODE_ORACLE}[sys.argv[1]]
 nw = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+if os.environ.get("OPSC_MODEL_TABLE_POINTS"):  # dev override of the small-batch table threshold
+    device.DevicePlanner.MODEL_TABLE_POINTS = int(os.environ["OPSC_MODEL_TABLE_POINTS"])
 prob = tables.pack_problem(*scenarios.scenario("cfg2"))
 tw = scenarios.trace_windows("cfg2")
 out = []
