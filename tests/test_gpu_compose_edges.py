@@ -210,6 +210,9 @@ def test_slices_per_cta_vs_oracle(nat_loaded, orc, cfg, spc, monkeypatch):
     got = _device_compose(nat, prob, grid, win, mw)
     assert (got == want).all(), (spc, got, want)
     assert (got != abi.KEY_INFEASIBLE).any()
+    # with the outer index space sharded over 3 ranks (uneven slice counts)
+    parts = [_device_compose(nat, prob, grid, win, mw, shard=r, n_shards=3) for r in range(3)]
+    assert (np.minimum.reduce(parts) == want).all(), spc
 
 
 def test_boundary_count_vs_numpy(nat_loaded, orc):
