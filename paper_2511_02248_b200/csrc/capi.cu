@@ -604,8 +604,10 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
     const size_t in_b = W * (3 * sizeof(double) + sizeof(int32_t) + 1) + ndev * sizeof(double);
     const size_t out_b = W * (4 * sizeof(double) + 5 * sizeof(int32_t) + 1) + wn * (3 * sizeof(int16_t) + 2) +
                          wn * OPSC_PRED_FIELDS * sizeof(double) + W * tcap * sizeof(OpscTraceEntry);
-    rc = ensure_stage(c, in_b + out_b + 24 * 16);
-    if (rc) return rc;
+    // large batches (long move traces) copy directly: the staging buffer is
+    // for the many-small-copies case and stays bounded
+    if (in_b + out_b > ((size_t)64 << 20)) io.stage = false;
+    else if ((rc = ensure_stage(c, in_b + out_b + 24 * 16))) return rc;
   }
   CK(cudaEventRecord(c->ev0, s));  // device-side span: first H2D .. last D2H
   CK(io.h2d(c->qps, win.qps, W * sizeof(double)));
