@@ -712,7 +712,13 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
   int il = 2;
   while (il < c.n && il < kOdoLevels + 2) {
     const bool too_many = prod(0, c.n - il) >= 4294967295.0;
-    if (!too_many && prod(c.n - il, c.n) >= 1024.0) break;  // in-thread candidates amortise the outer decode
+    // in-thread candidates amortise the outer decode: >= 1024, or >= 4096
+    // while the next split still leaves >= 1.8M threads (~8 waves; cfg3's
+    // 12-op DAG: il 4 -> 5 is +7%, tools/quick_time.py with OPSC_COMPOSE_IL)
+    const double in_thread = prod(c.n - il, c.n);
+    if (!too_many && in_thread >= 1024.0 &&
+        (in_thread >= 4096.0 || (double)n_windows * prod(0, c.n - il - 1) < 1.8e6))
+      break;
     if (!too_many && (double)n_windows * prod(0, c.n - il - 1) < min_threads) break;
     ++il;
   }
