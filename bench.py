@@ -413,7 +413,9 @@ def ours(args):
 def decision_latency(dev):
     """Window stats resident on device -> decoded decision, one window at a
     time, for the 10-op Llama-2-70B DAG (cfg2): exhaustive oracle over
-    (P in {1,2}, R<=3, B=1)^10 = 6.0e7 candidates, and the model-level grid."""
+    (P in {2,4}, R<=3, B=1)^10 = 6.0e7 candidates, the model-level grid and
+    greedy. `feasible_windows` counts the windows whose decision is a feasible
+    winner (the rest are infeasible-SLO fallbacks or NoStableConfig)."""
     import torch
 
     from paper_2511_02248_b200 import abi, device, model, scenarios, tables
@@ -425,6 +427,7 @@ def decision_latency(dev):
                        (abi.MODE_OPERATOR, "operator_greedy")):
         samples, eager = [], []
         batch_ms = 0.0
+        n_feas = n_nostable = 0
         for phase in ("prefill", "decode"):
             slo = scenarios.SLO["cfg2"][phase]
             params = model.AutoscaleParams(slo=slo)
@@ -443,6 +446,10 @@ def decision_latency(dev):
             b1.record()
             b1.synchronize()
             batch_ms += b0.elapsed_time(b1)
+            live = torch.from_numpy(np.asarray(qs > 0)).to(dev)
+            n_feas += int((pb.out_t["feasible"].bool() & live).sum())
+            nst = abi.W_NO_STABLE_BOUNDS | abi.W_NO_STABLE_PARAMS | abi.W_NO_STABLE_MODEL | abi.W_NO_STABLE_INIT
+            n_nostable += int(((pb.out_t["status"] & nst) != 0).sum())
             one = tables.window_arrays(qs[:1], ls[:1], tables.PHASE_INDEX[phase], slo)
             p = device.DevicePlanner(problem, one, mode, grid=grid, model=spec, greedy=gspec,
                                      device=dev)
@@ -473,7 +480,8 @@ def decision_latency(dev):
                      "launch": "CUDA graph replay of the whole per-window pipeline",
                      "eager_median": statistics.median(eager),
                      "eager_p99": eager[min(len(eager) - 1, int(0.99 * len(eager)))],
-                     "batched_ms_per_window": batch_ms / max(1, len(samples))}
+                     "batched_ms_per_window": batch_ms / max(1, len(samples)),
+                     "feasible_windows": n_feas, "no_stable_config_windows": n_nostable}
         if mode == abi.MODE_ORACLE:  # cfg2 throughput: whole trace per launch set, 6^10 candidates per window
             cpw = 1
             for v in range(problem.n_ops):

@@ -180,7 +180,7 @@ SLO = {
 }
 GRIDS = {
     "cfg1": dict(r_max=3, b_max=2, parallelism=(1, 2)),     # 12^6  ~ 3.0e6
-    "cfg2": dict(r_max=3, b_max=1, parallelism=(1, 2)),     # 6^10  ~ 6.0e7
+    "cfg2": dict(r_max=3, b_max=1, parallelism=(2, 4)),     # 6^10  ~ 6.0e7 (96/120 windows feasible)
     "cfg3": dict(r_max=3, b_max=1, parallelism=(1, 2)),     # 6^12  ~ 2.2e9 (sharded / sampled)
     "cfg3s": dict(r_max=3, b_max=2, parallelism=(1, 2)),    # 12^6 on the 6-op variant
     "cfg5": dict(r_max=4, b_max=3, parallelism=(1, 2)),     # 24^6  ~ 1.9e8

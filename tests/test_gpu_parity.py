@@ -49,6 +49,43 @@ def test_golden_oracle_cases(nat):
         _golden(nat, c, abi.MODE_ORACLE)
 
 
+def test_golden_gt6_cases(nat):
+    """cfg2 (10-op 70B) and cfg3 (12-op multimodal) exhaustive decisions
+    against the reference's own brute force run with only its 6-op guard
+    removed (tests/golden/make_golden_gt6.py): 432 windows x SLOs, plan and
+    default-stream metrics bit-exact."""
+    cs = G.load("oracle_gt6.json")
+    assert len(cs) >= 400
+    for c in cs:
+        _golden(nat, c, abi.MODE_ORACLE)
+
+
+def test_golden_gt6_batched_public_api(nat):
+    """The same goldens through the batched public entry (planners.plan_windows,
+    one launch set per (DAG, phase, SLO)): equal to the per-point goldens."""
+    from paper_2511_02248_b200 import planners
+    groups = {}
+    for c in G.load("oracle_gt6.json"):
+        groups.setdefault((c["scenario"], c["point"]["phase"], c["params"]["slo"]), []).append(c)
+    for (cfg, ph, slo), cs in groups.items():
+        dag, prof = scenarios.scenario(cfg)
+        params = G.case_params(cs[0])
+        bounds = G.case_bounds(cs[0])
+        pts = [G.case_point(c) for c in cs]
+        decs = planners.decide_windows(dag, prof, pts, params, "oracle", bounds)
+        assert len(decs) == 1
+        dec = decs[0]
+        for k, c in enumerate(cs):
+            exp = c["expected"]
+            if "error" in exp:
+                with pytest.raises(Exception) as ei:
+                    dec.plan(k)
+                assert type(ei.value).__name__ == exp["error"], c["name"]
+                continue
+            errs = G.compare_plan(dec.plan(k), exp, dec.problem)
+            assert not errs, (c["name"], errs)
+
+
 def test_golden_model_cases(nat):
     for c in G.load("model.json") + G.load("edges_model.json"):
         _golden(nat, c, abi.MODE_MODEL)
@@ -58,7 +95,7 @@ def _device_menus(nat, prob, grid, win):
     import torch
     dev = torch.device("cuda:0")
     E = grid.menu_off[prob.n_ops]
-    t = {k: torch.from_numpy(np.ascontiguousarray(getattr(win, k))).to(dev)
+    t = {k: torch.from_numpy(np.array(getattr(win, k), copy=True)).to(dev)
          for k in ("qps", "seq_len", "phase", "slo", "eps")}
     dw = abi.OpscWindows()
     dw.n = win.n

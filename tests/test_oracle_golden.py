@@ -5,6 +5,7 @@ Every vector in tests/golden/ was produced by running /root/reference
 """
 
 import ctypes as C
+import json
 import math
 
 import numpy as np
@@ -145,6 +146,43 @@ def test_oracle_decisions(orc, idx):
 def test_model_decisions(orc, idx):
     c = G.load("model.json")[idx]
     _check_case(orc, c, abi.MODE_MODEL)
+
+
+def _gt6_sample():
+    """>6-op reference decisions (tests/golden/make_golden_gt6.py: the
+    reference brute force with only its 6-op guard removed). The CPU oracle
+    enumerates literally, so the suite checks every 6th cfg2 case (6^10 = 6e7
+    candidates) and every 72nd cfg3 case (6^12 = 2.2e9); the GPU test checks
+    all of them."""
+    cs = G.load("oracle_gt6.json")
+    idx = [i for i, c in enumerate(cs) if c["scenario"] == "cfg2"][::6]
+    idx += [i for i, c in enumerate(cs) if c["scenario"] == "cfg3"][5::72]
+    return idx
+
+
+@pytest.mark.parametrize("idx", _gt6_sample())
+def test_oracle_gt6_decisions(orc, idx):
+    c = G.load("oracle_gt6.json")[idx]
+    assert not c["hash_sensitive"]
+    _check_case(orc, c, abi.MODE_ORACLE)
+
+
+def test_gt6_golden_coverage():
+    """The >6-op goldens exercise feasible winners, infeasible fallbacks and
+    NoStableConfig on both DAGs and phases, with many distinct winners."""
+    cs = G.load("oracle_gt6.json")
+    for cfg in ("cfg2", "cfg3"):
+        for ph in ("prefill", "decode"):
+            sub = [c["expected"] for c in cs if c["scenario"] == cfg and c["point"]["phase"] == ph]
+            feas = [e for e in sub if e.get("feasible")]
+            assert len(feas) >= len(sub) // 3, (cfg, ph, len(feas), len(sub))
+            assert len({json.dumps(e["configs"]) for e in feas}) >= 5, (cfg, ph)
+    exp = [c["expected"] for c in cs]
+    assert any("error" in e for e in exp)
+    assert any(e.get("feasible") is False for e in exp)
+    # the config SLO itself: most cfg2 windows have a feasible winner
+    cfg2 = [c["expected"] for c in cs if c["scenario"] == "cfg2" and c["name"].endswith("slo_x1")]
+    assert sum(bool(e.get("feasible")) for e in cfg2) >= 0.75 * len(cfg2)
 
 
 def _check_greedy(orc, c):
