@@ -86,6 +86,16 @@ extern "C" {
 
 #define OPSC_W_NO_STABLE_INIT 0x100u    /* NoStableConfig from init_configs (autoscaler.py:289) in greedy mode */
 #define OPSC_W_TRACE_TRUNCATED 0x200u   /* more trace entries than trace_cap */
+/* Which operator the reference's NoStableConfig message names (so the host can
+ * raise it with the reference's exact text):
+ *   bits 16..21: 1 + position in dag.node_ids order of the first operator
+ *                init_configs finds unstable at every (B, P) (autoscaler.py:289-292;
+ *                set with OPSC_W_NO_STABLE_PARAMS / OPSC_W_NO_STABLE_INIT);
+ *   bits 22..27: 1 + lexicographic rank of the first operator without a finite
+ *                menu entry (autoscaler.py:833-837; set with OPSC_W_NO_STABLE_BOUNDS). */
+#define OPSC_W_INIT_OP_SHIFT 16
+#define OPSC_W_BOUNDS_OP_SHIFT 22
+#define OPSC_W_OP_FIELD 0x3fu
 
 /* greedy trace actions (autoscaler.py:363, 446-454, 478-486, 549-557, 579-587) */
 #define OPSC_ACT_UPSCALE 1

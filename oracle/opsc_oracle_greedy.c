@@ -35,6 +35,7 @@ typedef struct {
   double qps, slo, eps;
   int L, ph;
   uint32_t st;
+  int init_fail; /* 1 + node-order position of the op init_configs could not seed */
   OpscTraceEntry* trace;
   int32_t cap, len;
   int np_distinct[OPSC_MAX_OPS];
@@ -253,7 +254,10 @@ static int init_configs(G* g, GCfg* c) {
         chosen = 1;
       }
     }
-    if (!chosen) return 0;
+    if (!chosen) {
+      g->init_fail = i + 1;
+      return 0;
+    }
   }
   return 1;
 }
@@ -284,7 +288,7 @@ int orc_greedy(const OpscDag* d, const OpscGreedySpec* s, OpscWindows win, const
     }
     GCfg c[OPSC_MAX_OPS];
     if (!init_configs(&g, c)) {
-      out.status[w] |= g.st | OPSC_W_NO_STABLE_INIT;
+      out.status[w] |= g.st | OPSC_W_NO_STABLE_INIT | ((uint32_t)g.init_fail << OPSC_W_INIT_OP_SHIFT);
       continue;
     }
     GEval e;

@@ -25,6 +25,9 @@ W_INFEASIBLE_PLACEMENT = 0x40
 W_IDLE = 0x80
 W_NO_STABLE_INIT = 0x100
 W_TRACE_TRUNCATED = 0x200
+W_INIT_OP_SHIFT = 16     # 1 + dag.node_ids position of the op init_configs names
+W_BOUNDS_OP_SHIFT = 22   # 1 + lex rank of the op without a finite menu entry
+W_OP_FIELD = 0x3F
 
 ACT_UPSCALE, ACT_DOWNSCALE, ACT_HEADROOM, ACT_PRUNE, ACT_RESEED = 1, 2, 3, 4, 5
 ACTION_NAMES = {1: "upscale", 2: "downscale", 3: "headroom", 4: "prune", 5: "reseed_uniform"}

@@ -545,12 +545,17 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    S.flag = 1;
-    for (int v = 0; v < n; ++v) S.flag &= S.chosen[v];
+    // 0, or 1 + dag.node_ids position of the first operator without a stable
+    // (B, P): the one the reference's NoStableConfig names (autoscaler.py:289-292)
+    int fail = 0;
+    for (int pos = n - 1; pos >= 0; --pos)
+      if (!S.chosen[d.node_order[pos]]) fail = pos + 1;
+    S.flag = fail;
   }
   __syncthreads();
-  if (!S.flag) {
-    if (threadIdx.x == 0) out.status[w] |= S.st | OPSC_W_NO_STABLE_INIT;
+  if (S.flag) {
+    if (threadIdx.x == 0)
+      out.status[w] |= S.st | OPSC_W_NO_STABLE_INIT | ((uint32_t)S.flag << OPSC_W_INIT_OP_SHIFT);
     return;
   }
   eval_full(S, d, qps, L, ph);

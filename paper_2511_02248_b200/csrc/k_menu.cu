@@ -108,8 +108,26 @@ __global__ void stability_kernel(const __grid_constant__ OpscDag d, const __grid
     found = __any_sync(0xffffffffu, mine);
   }
   st = __reduce_or_sync(0xffffffffu, st);
-  if (!found) st |= OPSC_W_NO_STABLE_PARAMS;
-  if (lane == 0 && st) atomicOr(&status[w], st);
+  if (lane != 0) return;
+  if (found) {
+    if (st) atomicOr(&status[w], st);
+    return;
+  }
+  // NoStableConfig names the first unstable operator in dag.node_ids order
+  // (autoscaler.py:268, 289-292): keep the minimum position over the warps
+  int pos = 0;
+  while (d.node_order[pos] != v) ++pos;
+  const uint32_t mine = (uint32_t)(pos + 1);
+  st |= OPSC_W_NO_STABLE_PARAMS;
+  uint32_t old = status[w], assumed;
+  do {
+    assumed = old;
+    const uint32_t cur = (assumed >> OPSC_W_INIT_OP_SHIFT) & OPSC_W_OP_FIELD;
+    uint32_t nv = assumed | st;
+    if (cur == 0 || mine < cur)
+      nv = (nv & ~(OPSC_W_OP_FIELD << OPSC_W_INIT_OP_SHIFT)) | (mine << OPSC_W_INIT_OP_SHIFT);
+    old = atomicCAS(&status[w], assumed, nv);
+  } while (old != assumed);
 }
 
 cudaError_t launch_stability(const OpscDag& d, const OpscGrid& g, OpscWindows w, uint32_t* status,
@@ -176,13 +194,13 @@ __global__ void decode_kernel(int n_ops, int n_windows, const __grid_constant__ 
     }
     feasible[w] = 1;
   } else {
-    bool ok = true;
+    int bad = 0;  // 1 + rank of the first operator without a finite entry (autoscaler.py:833-837)
     for (int v = 0; v < n_ops; ++v) {
       ent[v] = fb[w * n_ops + v];
-      ok &= ent[v] >= 0;
+      if (ent[v] < 0 && !bad) bad = v + 1;
     }
-    if (!ok) {
-      status[w] |= OPSC_W_NO_STABLE_BOUNDS;
+    if (bad) {
+      status[w] |= OPSC_W_NO_STABLE_BOUNDS | ((uint32_t)bad << OPSC_W_BOUNDS_OP_SHIFT);
       return;
     }
   }

@@ -62,6 +62,9 @@ def install(pkg=None):
     `uninstall` callable restoring the originals."""
     if pkg is None:
         import opscaler as pkg  # noqa: F811
+    import importlib
+    for sub in ("autoscaler", "placement", "runner", "cli", "metrics", "queueing"):
+        importlib.import_module(f"{pkg.__name__}.{sub}")  # submodules the wrappers rebind
     A = pkg.autoscaler
     T, E = _namespaces(pkg)
     names = ("brute_force_autoscale", "model_level_autoscale", "greedy_autoscale")

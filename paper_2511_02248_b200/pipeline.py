@@ -76,7 +76,8 @@ class TracePlanner:
             arrays = pr.decisions()
             pts = [model.WorkloadPoint(max(float(q), 0.0), int(l), ph)
                    for q, l in zip(arrays_qps(pr), pr.win_t["seq_len"].cpu().numpy())]
-            decs[ph] = WindowDecisions(self.problem, pts, arrays, self.mode)
+            decs[ph] = WindowDecisions(self.problem, pts, arrays, self.mode,
+                                       r_cap=self.params[ph].r_cap)
         W = len(decs["prefill"])
         return [(decs["prefill"].plan(i), decs["decode"].plan(i)) for i in range(W)]
 

@@ -93,7 +93,7 @@ def _run(mode, problem, points, params, bounds, fleet, energy, types, err, trace
     place = tables.pack_place(fleet, energy)
     arrays = _native.plan_windows_host(mode, problem, win, grid=grid, model=spec, place=place,
                                        greedy=greedy, trace_cap=trace_cap)
-    return WindowDecisions(problem, points, arrays, mode, types, err)
+    return WindowDecisions(problem, points, arrays, mode, types, err, r_cap=params.r_cap)
 
 
 _MODES = {"oracle": abi.MODE_ORACLE, "model": abi.MODE_MODEL, "operator": abi.MODE_OPERATOR}

@@ -19,26 +19,42 @@ from . import abi, errors, model
 ORDER_LEX, ORDER_NODE = 0, 1
 
 
-def raise_for_status(status: int, mode: int, err=errors):
+def _op_named(status, shift, problem, node_order):
+    """The operator id the device recorded in a status word's op field."""
+    k = (status >> shift) & abi.W_OP_FIELD
+    if not k or problem is None:
+        return "?"
+    rank = problem.table.node_order[k - 1] if node_order else k - 1
+    return problem.ids[rank]
+
+
+def raise_for_status(status: int, mode: int, err=errors, *, problem=None, qps=None, r_cap=None):
+    """Raise the reference's exception (class and text) for a window status.
+
+    The texts are the reference's: init_configs (autoscaler.py:289-292, also
+    reached by brute force through its greedy warm start, :771), the
+    brute-force bounds fallback (:835-837), model level (:678-681) and
+    erlang_c on a utilization that rounds to 1 (queueing.py:68-69)."""
     if status & abi.W_ZERO_DIVISION:
         raise ZeroDivisionError("float division by zero")
     if status & abi.W_UNSTABLE_ROUNDING:
-        raise err.Unstable("utilization rounds to 1: queue has no steady state")
+        raise err.Unstable("utilization 1.0 >= 1: queue has no steady state")
+    init_msg = lambda: (f"operator {_op_named(status, abi.W_INIT_OP_SHIFT, problem, True)}: "
+                        f"arrival rate {qps} exceeds capacity at every (B, P) within r_cap={r_cap}")
     if mode == abi.MODE_ORACLE:
         if status & abi.W_NO_STABLE_PARAMS:
-            raise err.NoStableConfig(
-                "arrival rate exceeds capacity at every (B, P) within r_cap")
+            raise err.NoStableConfig(init_msg())
         if status & abi.W_NO_STABLE_BOUNDS:
-            raise err.NoStableConfig("operator has no stable configuration within bounds")
+            op = _op_named(status, abi.W_BOUNDS_OP_SHIFT, problem, False)
+            raise err.NoStableConfig(f"operator {op}: no stable configuration within bounds")
     elif mode == abi.MODE_OPERATOR:
         if status & abi.W_NO_STABLE_INIT:
-            raise err.NoStableConfig(
-                "arrival rate exceeds capacity at every (B, P) within r_cap")
+            raise err.NoStableConfig(init_msg())
         if status & abi.W_TRACE_TRUNCATED:
             raise RuntimeError("greedy move trace exceeded trace_cap; raise trace_cap")
     elif status & abi.W_NO_STABLE_MODEL:
         raise err.NoStableConfig(
-            "model-level: arrival rate exceeds capacity at every batch size within r_cap")
+            f"model-level: arrival rate {qps} exceeds capacity at every batch size within r_cap={r_cap}")
 
 
 @dataclass
@@ -54,9 +70,10 @@ class PlanMetrics:
 class WindowDecisions:
     """Decisions for a batch of windows, with lazy plan materialisation."""
 
-    def __init__(self, problem, points, arrays, mode, types=model, err=errors):
+    def __init__(self, problem, points, arrays, mode, types=model, err=errors, r_cap=None):
         self.problem, self.points, self.arrays, self.mode = problem, points, arrays, mode
         self.types, self.err = types, err
+        self.r_cap = r_cap  # AutoscaleParams.r_cap, for the NoStableConfig texts
 
     def __len__(self):
         return self.arrays.n_windows
@@ -69,7 +86,8 @@ class WindowDecisions:
         st = int(a.status[i])
         if st & abi.W_IDLE:
             return None
-        raise_for_status(st, self.mode, self.err)
+        raise_for_status(st, self.mode, self.err, problem=self.problem, qps=self.points[i].qps,
+                         r_cap=self.r_cap)
         if self.mode == abi.MODE_ORACLE:
             order = range(n)
         else:

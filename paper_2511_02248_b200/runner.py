@@ -240,7 +240,7 @@ def _plan_batch(mode, dag, profiles, points, params_list, bounds, T, max_enumera
             greedy = tables.pack_greedy(problem, prm) if m == abi.MODE_OPERATOR else None
             arrays = _native.plan_windows_host(m, problem, win, grid=grid, model=spec,
                                                place=tables.pack_place(), greedy=greedy)
-            dec = WindowDecisions(problem, pts, arrays, m, PT, E)
+            dec = WindowDecisions(problem, pts, arrays, m, PT, E, r_cap=prm.r_cap)
         except Exception as exc:
             for i in idx:
                 out[i] = _Raise(exc)

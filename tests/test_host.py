@@ -217,3 +217,45 @@ def test_oracle_windowize_matches_reference_fixture(orc, cfg):
     perm = np.random.default_rng(0).permutation(len(arr))
     pq2, pl2, dq2 = orc.windowize(arr[perm], li[perm], lo[perm], spec["window_len"], spec["quantile"])
     assert np.array_equal(pq, pq2) and np.array_equal(pl, pl2) and np.array_equal(dq, dq2)
+
+
+def test_error_texts_match_reference(orc):
+    from paper_2511_02248_b200 import errors, plans
+    """NoStableConfig raised from device status words carries the reference's
+    own text (operator named via the status op fields): init_configs
+    (autoscaler.py:289-292) in oracle and greedy mode, the bounds fallback
+    (:835-837), model level (:678-681). Decisions come from the CPU oracle
+    here (same status words as the kernels, checked bitwise on the GPU)."""
+    import refpkg
+    op = refpkg.import_reference()
+    dag_spec, prof = scenarios.SCENARIOS["cfg1"]
+    rdag, rprof = op.build_dag(dag_spec), op.perfmodel.profiles_from_dict(prof)
+    dag, profm = model.build_dag(dag_spec), model.profiles_from_dict(prof)
+    prob = tables.pack_problem(dag, profm)
+    cases = [("oracle", dict(qps=1e9, seq_len=2048), dict(slo=0.5), dict(r_max=3, b_max=2, parallelism=(1, 2))),
+             ("oracle", dict(qps=40.0, seq_len=4096), dict(slo=0.5), dict(r_max=1, b_max=1, parallelism=(1,))),
+             ("operator", dict(qps=1e9, seq_len=2048), dict(slo=0.5), None),
+             ("operator", dict(qps=3e4, seq_len=2048), dict(slo=0.5, r_cap=64), None),   # attn
+             ("oracle", dict(qps=1e5, seq_len=2048), dict(slo=0.5, r_cap=16),            # qkv
+              dict(r_max=3, b_max=2, parallelism=(1, 2))),
+             ("model", dict(qps=5e4, seq_len=2048), dict(slo=0.5, r_cap=4), None)]
+    seen = 0
+    for mode, pt, prm, bnd in cases:
+        rpt = op.WorkloadPoint(pt["qps"], pt["seq_len"], "prefill")
+        rparams = op.AutoscaleParams(**prm)
+        with pytest.raises(op.autoscaler.NoStableConfig) as want:
+            op.runner.plan_for_mode(mode, rdag, rprof, rpt, rparams,
+                                    op.BruteForceBounds(**bnd) if bnd else None)
+        mpt = model.WorkloadPoint(pt["qps"], pt["seq_len"], "prefill")
+        params = model.AutoscaleParams(**prm)
+        m = {"oracle": abi.MODE_ORACLE, "model": abi.MODE_MODEL, "operator": abi.MODE_OPERATOR}[mode]
+        win = tables.pack_windows([mpt], params.slo, params.epsilon)
+        out = orc.plan_windows(m, prob, win,
+                               grid=tables.pack_grid(prob, params, model.BruteForceBounds(**bnd)) if bnd else None,
+                               model=tables.pack_model(prob, params), greedy=tables.pack_greedy(prob, params))
+        dec = plans.WindowDecisions(prob, [mpt], out, m, r_cap=params.r_cap)
+        with pytest.raises(errors.NoStableConfig) as got:
+            dec.plan(0)
+        assert str(got.value) == str(want.value), mode
+        seen += 1
+    assert seen == len(cases)
