@@ -58,7 +58,8 @@ def dist_env():
 
 
 def workload():
-    from paper_2511_02248_b200 import model, scenarios, tables
+    from paper_2511_02248_b200 import model, tables
+    from workloads import scenarios
     problem = tables.pack_problem(*scenarios.scenario("cfg5"))
     g = scenarios.GRIDS["cfg5"]
     grid = tables.pack_grid(problem, model.AutoscaleParams(slo=scenarios.SLO["cfg5"]["prefill"]),
@@ -195,11 +196,21 @@ def ours(args):
     rank, world, local = dist_env()
     # one rank per GPU; OPSC_DIST_BACKEND=gloo (test only) lets several ranks
     # share a GPU to exercise the N>1 path on a 1-GPU box
+    backend = os.environ.get("OPSC_DIST_BACKEND", "nccl")
+    if world > 1 and backend == "nccl" and torch.cuda.device_count() < world:
+        print(f"bench.py: {world} ranks need {world} CUDA devices, {torch.cuda.device_count()} visible",
+              file=sys.stderr, flush=True)
+        sys.exit(2)
     local = local % max(1, torch.cuda.device_count())
+    nccl = None
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group(os.environ.get("OPSC_DIST_BACKEND", "nccl"))
+        if backend == "nccl":  # communicator setup (ranks, NVLS / P2P transport) logged to stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            nccl = ".".join(str(x) for x in torch.cuda.nccl.version())
+        dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     problem, grid, win, space, active = workload()
@@ -362,7 +373,7 @@ def ours(args):
         latency["multimodal_cfg3"] = multimodal_batched(dev)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:  # after every timed region; other ranks wait
         k, dt, threads = cpu_run(problem, grid, win, target_s=12.0)
         cpu = {"value": k * space / dt, "unit": "candidates/s", "cores": threads, "kind": "port",
                "sample": f"{k} of {win.n} cfg5 prefill windows (evenly spaced), full pipeline "
@@ -378,7 +389,8 @@ def ours(args):
                        "candidates_per_window": space, "candidates_per_step": cands_step,
                        "mode": "oracle (exhaustive brute force, every candidate composed)",
                        "parallelism": f"candidate-range shards x{world}" if world > 1 else "single GPU",
-                       "merge": merge_kind,
+                       "merge": merge_kind, "dist_backend": backend if world > 1 else None,
+                       "nccl_version": nccl,
                        "l2": "flushed between timed steps (256 MiB write outside the events)",
                        "workload_choice": "BASELINE config 5 is the throughput config (the 1e8-candidate x "
                                           "1440-window sweep sharded over 1/2/4/8 GPUs); config 2 (70B, 1 h "
@@ -418,7 +430,8 @@ def decision_latency(dev):
     winner (the rest are infeasible-SLO fallbacks or NoStableConfig)."""
     import torch
 
-    from paper_2511_02248_b200 import abi, device, model, scenarios, tables
+    from paper_2511_02248_b200 import abi, device, model, tables
+    from workloads import scenarios
     problem = tables.pack_problem(*scenarios.scenario("cfg2"))
     g = scenarios.GRIDS["cfg2"]
     tw = scenarios.trace_windows("cfg2")
@@ -498,7 +511,8 @@ def multimodal_batched(dev):
     2.2e9 candidates per window, model level and greedy."""
     import torch
 
-    from paper_2511_02248_b200 import abi, device, model, scenarios, tables
+    from paper_2511_02248_b200 import abi, device, model, tables
+    from workloads import scenarios
     problem = tables.pack_problem(*scenarios.scenario("cfg3"))
     g = scenarios.GRIDS["cfg3"]
     tw = scenarios.trace_windows("cfg3")
@@ -541,7 +555,8 @@ def capacity_8gpu(dev):
     planning launch set over windows x 32 rates."""
     import torch
 
-    from paper_2511_02248_b200 import capacity, model, scenarios
+    from paper_2511_02248_b200 import capacity, model
+    from workloads import scenarios
     dag, prof = scenarios.scenario("cfg1")
     tw = scenarios.trace_windows("cfg2")
     idx = np.linspace(0, 59, 8).round().astype(int)
@@ -566,7 +581,8 @@ def trace_pipeline(dev):
     around the call (includes the host's launch gaps)."""
     import torch
 
-    from paper_2511_02248_b200 import model, pipeline, scenarios, workload
+    from paper_2511_02248_b200 import model, pipeline, workload
+    from workloads import scenarios
     spec = scenarios.TRACES["cfg2"]
     recs = workload.synth_workload(workload.SynthSpec(**spec["spec"]), spec["seed"])
     arr = torch.tensor([r.arrival_time for r in recs], dtype=torch.float64, device=dev)
@@ -593,8 +609,37 @@ def trace_pipeline(dev):
     return out
 
 
+def spawn(args):
+    """`--gpus N` (N > 1) outside torchrun: re-exec this command under
+    torch.distributed.run with one rank per GPU (127.0.0.1 rendezvous). The
+    GPU arm refuses to start when fewer than N devices are visible instead of
+    silently time-sharing one."""
+    if args.impl == "ours" and os.environ.get("OPSC_DIST_BACKEND", "nccl") == "nccl":
+        import torch
+        n = torch.cuda.device_count()
+        if n < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} CUDA devices, {n} visible",
+                  file=sys.stderr, flush=True)
+            sys.exit(2)
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ:
+        if args.gpus > 1 and args.impl == "ours":
+            spawn(args)
+    elif int(os.environ["WORLD_SIZE"]) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}",
+              file=sys.stderr, flush=True)
+        sys.exit(2)
     if args.impl == "reference":
         reference_arm(args)
     else:

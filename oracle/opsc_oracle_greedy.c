@@ -329,7 +329,7 @@ int orc_greedy(const OpscDag* d, const OpscGreedySpec* s, OpscWindows win, const
       out.cfg[(w * n + v) * 3 + 2] = (int16_t)c[v].b;
     }
     out.trace_len[w] = g.len;
-    if (g.len > g.cap) g.st |= OPSC_W_TRACE_TRUNCATED;
+    if (g.cap > 0 && g.len > g.cap) g.st |= OPSC_W_TRACE_TRUNCATED;
     out.status[w] |= g.st;
   }
   return OPSC_OK;

@@ -182,5 +182,22 @@ def context():
 
 def plan_windows_host(mode, problem, windows, grid=None, model=None, place=None, greedy=None,
                       trace_cap=4096):
-    return context().plan_windows(mode, problem, windows, grid=grid, model=model, place=place,
-                                  greedy=greedy, trace_cap=trace_cap)
+    """One host-buffer planning call on this thread's context. Greedy move
+    traces have no length limit in the reference (max_iterations per loop plus
+    headroom / prune entries, autoscaler.py:391, 446-587): windows whose
+    trace outgrew `trace_cap` (the kernel keeps counting past the cap) are
+    re-planned with room for their whole trace -- the planner is
+    deterministic, so only the trace rows change."""
+    ctx = context()
+    out = ctx.plan_windows(mode, problem, windows, grid=grid, model=model, place=place,
+                           greedy=greedy, trace_cap=trace_cap)
+    if mode == abi.MODE_OPERATOR and out.trace_cap:
+        import numpy as np
+        cut = np.nonzero(out.status & abi.W_TRACE_TRUNCATED)[0]
+        if len(cut):
+            cap = int(out.trace_len[cut].max())
+            again = ctx.plan_windows(mode, problem, windows.take(cut), grid=grid, model=model,
+                                     place=place, greedy=greedy, trace_cap=cap)
+            out = out.with_trace_cap(cap)
+            out.splice(cut, again)
+    return out

@@ -709,6 +709,8 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
     return x;
   };
   const double min_threads = 148.0 * 512.0;
+  // thread counts are per rank: a shard enumerates 1/n_shards of the outer space
+  const double per_rank = (double)n_windows / (double)(n_shards > 0 ? n_shards : 1);
   int il = 2;
   while (il < c.n && il < kOdoLevels + 2) {
     const bool too_many = prod(0, c.n - il) >= 4294967295.0;
@@ -717,9 +719,9 @@ int compose_setup(const OpscDag& d, const OpscGrid& g, int n_windows, int shard,
     // 12-op DAG: il 4 -> 5 is +7%, tools/quick_time.py with OPSC_COMPOSE_IL)
     const double in_thread = prod(c.n - il, c.n);
     if (!too_many && in_thread >= 1024.0 &&
-        (in_thread >= 4096.0 || (double)n_windows * prod(0, c.n - il - 1) < 1.8e6))
+        (in_thread >= 4096.0 || per_rank * prod(0, c.n - il - 1) < 1.8e6))
       break;
-    if (!too_many && (double)n_windows * prod(0, c.n - il - 1) < min_threads) break;
+    if (!too_many && per_rank * prod(0, c.n - il - 1) < min_threads) break;
     ++il;
   }
   if (const char* f = getenv("OPSC_COMPOSE_IL")) {  // dev override (tools/w1_latency.py)

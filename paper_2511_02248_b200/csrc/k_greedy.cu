@@ -638,7 +638,8 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
     }
     out.trace_len[w] = S.trace_len;
     uint32_t st = S.st;
-    if (S.trace_len > out.trace_cap) st |= OPSC_W_TRACE_TRUNCATED;
+    // trace_cap == 0: the caller asked for no trace (e.g. capacity search)
+    if (out.trace_cap > 0 && S.trace_len > out.trace_cap) st |= OPSC_W_TRACE_TRUNCATED;
     out.status[w] |= st;
   }
 }

@@ -63,7 +63,11 @@ __global__ void __launch_bounds__(256) menu_build_kernel(const __grid_constant__
   entry_prb(g, v, j - g.menu_off[v], p, r, b);
   uint32_t st = 0;
   const Pred o = predict<true>(d, qps, win.seq_len[w], win.phase[w], v, p, r, b, &st);
-  menu_w[idx] = o.stable ? weight(o, d.layer_count[v]) : OPSC_INF;
+  // the reference skips every non-finite weight (autoscaler.py:800-801, 833):
+  // NaN (possible only with NaN profile data) is stored as +inf so that every
+  // compose level excludes it, not just the innermost one
+  const double wt = weight(o, d.layer_count[v]);
+  menu_w[idx] = (o.stable && !isnan(wt)) ? wt : OPSC_INF;
   if (st) atomicOr(&status[w], st);
 }
 

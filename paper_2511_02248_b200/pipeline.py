@@ -9,9 +9,10 @@ leaving HBM, and only the decisions come back.
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 
-from . import abi, device, model, tables, workload
+from . import _native, abi, device, model, tables, workload
 from .plans import WindowDecisions
 
 _MODES = {"oracle": abi.MODE_ORACLE, "model": abi.MODE_MODEL, "operator": abi.MODE_OPERATOR}
@@ -74,6 +75,15 @@ class TracePlanner:
         decs = {}
         for ph, pr in res.items():
             arrays = pr.decisions()
+            cut = np.nonzero(arrays.status & abi.W_TRACE_TRUNCATED)[0]
+            if len(cut):  # move traces past trace_cap: re-plan those windows with room
+                host = tables.WindowArrays(*(pr.win_t[k].cpu().numpy()[cut] for k in
+                                             ("qps", "seq_len", "phase", "slo", "eps")))
+                grid, spec, greedy = self._specs(ph)
+                again = _native.plan_windows_host(self.mode, self.problem, host, grid=grid, model=spec,
+                                                  greedy=greedy, trace_cap=int(arrays.trace_len[cut].max()))
+                arrays = arrays.with_trace_cap(again.trace_cap)
+                arrays.splice(cut, again)
             pts = [model.WorkloadPoint(max(float(q), 0.0), int(l), ph)
                    for q, l in zip(arrays_qps(pr), pr.win_t["seq_len"].cpu().numpy())]
             decs[ph] = WindowDecisions(self.problem, pts, arrays, self.mode,

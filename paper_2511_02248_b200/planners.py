@@ -45,7 +45,7 @@ def _guard(problem, params, bounds, max_enumeration, err):
 
 def _points_ok(points):
     for p in points:
-        if not p.qps > 0:
+        if p.qps <= 0:  # autoscaler.py:148-149 (NaN passes; see plans.nonfinite_qps)
             raise ValueError("workload point must have qps > 0")
 
 
@@ -114,7 +114,7 @@ def decide_windows(dag, profiles, points, params, mode="oracle", bounds=None, *,
     by_phase = params if isinstance(params, dict) else None
     groups = {}
     for i, p in enumerate(points):
-        if not p.qps > 0:
+        if p.qps <= 0:  # idle window (cli.py:138)
             continue
         groups.setdefault(p.phase, []).append(i)
     out = []

@@ -57,6 +57,17 @@ def raise_for_status(status: int, mode: int, err=errors, *, problem=None, qps=No
             f"model-level: arrival rate {qps} exceeds capacity at every batch size within r_cap={r_cap}")
 
 
+def nonfinite_qps(qps):
+    """A NaN / +inf arrival rate passes the reference's `qps <= 0` check
+    (autoscaler.py:148) and fails in _strict_min_replicas' math.ceil
+    (autoscaler.py:225), reached by every planner; the device treats such a
+    window as idle, so the host raises the reference's error here."""
+    if math.isnan(qps):
+        raise ValueError("cannot convert float NaN to integer")
+    if math.isinf(qps) and qps > 0:
+        raise OverflowError("cannot convert float infinity to integer")
+
+
 @dataclass
 class PlanMetrics:
     """Default-stream placement figures of a feasible plan (runner.py:94-96)."""
@@ -84,6 +95,7 @@ class WindowDecisions:
     def plan(self, i):
         a, n, ids, T = self.arrays, self.problem.n_ops, self.problem.ids, self.types
         st = int(a.status[i])
+        nonfinite_qps(self.points[i].qps)
         if st & abi.W_IDLE:
             return None
         raise_for_status(st, self.mode, self.err, problem=self.problem, qps=self.points[i].qps,

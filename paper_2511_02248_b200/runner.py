@@ -351,7 +351,8 @@ def compare_points(dag, profiles, fleet, points, params, placement_mode="shared"
     extras = (fingerprint_extra if isinstance(fingerprint_extra, (list, tuple))
               else [fingerprint_extra] * n)
     values = values if values is not None else [0.0] * n
-    live = [i for i in range(n) if not isinstance(points[i], _Raise) and points[i].qps > 0.0]
+    # the reference's predicate: vacuous iff qps <= 0.0 (runner.py:157); NaN is live
+    live = [i for i in range(n) if not isinstance(points[i], _Raise) and not points[i].qps <= 0.0]
     sub = lambda seq: [seq[i] for i in live]
     base = evaluate_points("model", dag, profiles, fleet, sub(points), sub(params_list), "shared",
                            energy_params, None, sub(extras), types=T) if live else []
@@ -445,7 +446,7 @@ def autoscale_windows(dag, profiles, fleet, windows, mode, placement_mode, param
         except Exception as exc:
             prm[ph] = _Raise(exc)
     live = [(i, pt) for i, pair in enumerate(windows) for pt in pair
-            if pt.qps > 0.0 and not isinstance(prm[pt.phase], _Raise)]
+            if not pt.qps <= 0.0 and not isinstance(prm[pt.phase], _Raise)]  # cli.py:138
     res = {}
     if live:
         outcomes = evaluate_points(mode, dag, profiles, fleet, [pt for _, pt in live],

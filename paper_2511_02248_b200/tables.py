@@ -299,6 +299,24 @@ class DecisionArrays:
         n = sum(getattr(self, f).nbytes for f in self.FIELDS)
         return n + (self.trace_len.nbytes + self.trace.nbytes if self.trace_cap else 0)
 
+    def with_trace_cap(self, cap):
+        """A copy whose move-trace rows hold `cap` entries (existing entries kept)."""
+        out = DecisionArrays(self.n_windows, self.n_ops, cap)
+        for f in self.FIELDS + ("trace_len",):
+            getattr(out, f)[...] = getattr(self, f)
+        k = min(self.trace_cap, cap)
+        out.trace[:, :k] = self.trace[:, :k]
+        return out
+
+    def splice(self, idx, other):
+        """Rows `idx` replaced by `other`'s rows 0..len(idx)-1 (trace_cap of
+        self must hold other's entries)."""
+        for f in self.FIELDS + ("trace_len",):
+            getattr(self, f)[idx] = getattr(other, f)
+        if self.trace_cap:
+            k = min(self.trace_cap, other.trace_cap)
+            self.trace[idx, :k] = other.trace[:, :k]
+
 
 def c_ptr(x):
     return C.byref(x)

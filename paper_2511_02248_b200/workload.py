@@ -4,7 +4,7 @@ Same generators and windowing as the reference (workload.py:107-232):
 Poisson thinning against the peak rate with numpy's default_rng, lognormal
 input/output lengths, and per-window (prefill, decode) demand points with the
 "higher" empirical quantile of input lengths. tests/test_host.py checks the
-output bit-for-bit against the reference-generated fixture in data/traces.npz.
+output bit-for-bit against the reference-generated fixture in workloads/traces.npz.
 """
 
 from __future__ import annotations

@@ -45,7 +45,7 @@ from opscaler import perfmodel as PM  # noqa: E402
 from opscaler import queueing as Q  # noqa: E402
 from opscaler import opgraph as G  # noqa: E402
 
-from paper_2511_02248_b200 import scenarios as S  # noqa: E402
+from workloads import scenarios as S  # noqa: E402
 
 A.MAX_ENUMERATION = 10**12  # sampled windows exceed the 1e7 guard on purpose
 

@@ -27,7 +27,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 from opscaler import cli as ref_cli  # noqa: E402
 from opscaler import workload as ref_workload  # noqa: E402
 
-from paper_2511_02248_b200 import scenarios  # noqa: E402
+from workloads import scenarios  # noqa: E402
 
 IN = os.path.join(HERE, "cli")
 

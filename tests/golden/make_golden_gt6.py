@@ -45,7 +45,7 @@ import make_golden as MG  # noqa: E402  (plan_json / metrics_json / case_inputs 
 from opscaler import autoscaler as A  # noqa: E402
 import opscaler as ref  # noqa: E402
 
-from paper_2511_02248_b200 import scenarios as S  # noqa: E402
+from workloads import scenarios as S  # noqa: E402
 
 LADDER = (0.5, 2.0, 4.0, 6.0)
 N_WORKERS = int(os.environ.get("GOLDEN_WORKERS", os.cpu_count() or 4))

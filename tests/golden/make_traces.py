@@ -1,7 +1,7 @@
 """Generate per-window trace statistics with the REFERENCE implementation.
 
 Runs only in the build container (it imports the read-only reference from
-/root/reference). Writes paper_2511_02248_b200/data/traces.npz: for every
+/root/reference). Writes workloads/traces.npz: for every
 config in scenarios.TRACES, the reference's synth_workload(spec, seed)
 (workload.py:195-232) cut by windowize (workload.py:114-158) into
 prefill/decode demand points.
@@ -41,7 +41,7 @@ def main():
                        dtype=np.float64)
         out[f"{name}/head_records"] = arr
         print(name, len(recs), "records", len(wins), "windows")
-    path = os.path.join(REPO, "paper_2511_02248_b200", "data", "traces.npz")
+    path = os.path.join(REPO, "workloads", "traces.npz")
     np.savez_compressed(path, **out)
     print("wrote", path)
 

@@ -7,7 +7,8 @@ import os
 
 import numpy as np
 
-from paper_2511_02248_b200 import model, scenarios, tables
+from paper_2511_02248_b200 import model, tables
+from workloads import scenarios
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 

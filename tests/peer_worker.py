@@ -10,7 +10,8 @@ import torch
 import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2511_02248_b200 import abi, device, dist as pdist, model, scenarios, tables  # noqa: E402
+from paper_2511_02248_b200 import abi, device, dist as pdist, model, tables  # noqa: E402
+from workloads import scenarios  # noqa: E402
 
 
 def main():
@@ -41,7 +42,8 @@ def main():
                 print(f"rank {rank} step {step}: {f} differs", flush=True)
                 ok = False
     merge.close()
-    flag = torch.tensor([0 if ok else 1], dtype=torch.int32)
+    flag = torch.tensor([0 if ok else 1], dtype=torch.int32,
+                        device=dev if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(flag)
     dist.destroy_process_group()
     print(f"rank {rank}/{world}: {'ok' if int(flag) == 0 else 'FAILED'}", flush=True)

@@ -26,6 +26,12 @@ def path():
 
 
 def import_reference():
+    if "opscaler" in sys.modules:  # already imported (by another test) from a candidate path
+        mod = sys.modules["opscaler"]
+        assert os.path.dirname(os.path.dirname(mod.__file__)) in CANDIDATES, mod.__file__
+        for sub in ("runner", "cli"):
+            importlib.import_module("opscaler." + sub)
+        return mod
     p = path()
     if p is None:
         pytest.skip("reference package not installed (baseline/_ref) and /root/reference absent")

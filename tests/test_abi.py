@@ -81,7 +81,8 @@ def test_no_cpu_fallback_on_cpu_host():
     """Without a GPU the planner raises instead of computing on the CPU."""
     if _native.device_count() > 0:
         pytest.skip("GPU present")
-    from paper_2511_02248_b200 import DeviceUnavailable, model, planners, scenarios
+    from paper_2511_02248_b200 import DeviceUnavailable, model, planners
+    from workloads import scenarios
     dag, prof = scenarios.scenario("cfg1")
     with pytest.raises(DeviceUnavailable):
         planners.brute_force_autoscale(dag, prof, model.WorkloadPoint(10.0, 512, "prefill"),

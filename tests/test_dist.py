@@ -2,6 +2,7 @@
 MIN all-reduce of packed keys reproduce the single-process decision."""
 
 import os
+import sys
 
 import numpy as np
 import pytest
@@ -9,7 +10,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2511_02248_b200 import abi, model, scenarios, tables
+from paper_2511_02248_b200 import abi, model, tables
+from workloads import scenarios
 
 
 def _inputs(cfg, phase, idx):
@@ -74,3 +76,22 @@ def test_shard_ranges_cover_space(orc):
         for s in range(n):
             merged = np.minimum(merged, orc.compose(prob, grid, win, mw, shard=s, n_shards=n))
         assert (merged == base).all()
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    """`bench.py --gpus N` outside torchrun spawns N ranks itself, and fails
+    loudly (exit 2) rather than printing an n_gpus: 1 line when fewer than N
+    devices are visible (here: none)."""
+    import subprocess
+    import torch
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("multi-GPU host")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2"],
+                       capture_output=True, text=True, timeout=300)
+    assert p.returncode == 2 and p.stdout == "", (p.returncode, p.stdout, p.stderr)
+    assert "needs 2 CUDA devices" in p.stderr
+    env = dict(os.environ, WORLD_SIZE="3", RANK="0", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert p.returncode == 2 and "WORLD_SIZE=3" in p.stderr

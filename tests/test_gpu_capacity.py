@@ -5,7 +5,8 @@ reference is unpinned: the reference has no such operation)."""
 import numpy as np
 import pytest
 
-from paper_2511_02248_b200 import abi, capacity, model, scenarios, tables
+from paper_2511_02248_b200 import abi, capacity, model, tables
+from workloads import scenarios
 
 pytestmark = pytest.mark.gpu
 

@@ -167,7 +167,7 @@ def test_level_splits_vs_oracle(nat_loaded, orc, cfg, il, monkeypatch):
     middle levels run as the register odometer (0..4 of them), the rest are
     decoded per thread (OPSC_COMPOSE_IL is the compose_setup dev override)."""
     from paper_2511_02248_b200 import _native as nat
-    from paper_2511_02248_b200 import scenarios
+    from workloads import scenarios
     prob = tables.pack_problem(*scenarios.scenario(cfg))
     g = scenarios.GRIDS[cfg]
     grid = tables.pack_grid(prob, model.AutoscaleParams(slo=1.0), model.BruteForceBounds(**g))
@@ -194,7 +194,7 @@ def test_slices_per_cta_vs_oracle(nat_loaded, orc, cfg, spc, monkeypatch):
     spc does not divide the slice count; 1000 = one CTA per window) gives the
     oracle's key (OPSC_COMPOSE_SPC is the compose_setup dev override)."""
     from paper_2511_02248_b200 import _native as nat
-    from paper_2511_02248_b200 import scenarios
+    from workloads import scenarios
     prob = tables.pack_problem(*scenarios.scenario(cfg))
     g = scenarios.GRIDS[cfg]
     grid = tables.pack_grid(prob, model.AutoscaleParams(slo=1.0), model.BruteForceBounds(**g))

@@ -5,7 +5,8 @@ GPU decisions and every plan field against the CPU oracle."""
 import numpy as np
 import pytest
 
-from paper_2511_02248_b200 import abi, model, scenarios, tables
+from paper_2511_02248_b200 import abi, model, tables
+from workloads import scenarios
 
 pytestmark = pytest.mark.gpu
 

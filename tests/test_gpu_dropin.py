@@ -20,7 +20,7 @@ import pytest
 
 import golden_cases as G
 import refpkg
-from paper_2511_02248_b200 import scenarios
+from workloads import scenarios
 
 pytestmark = pytest.mark.gpu
 

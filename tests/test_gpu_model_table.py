@@ -4,7 +4,8 @@ probe/bisect over the table) is bit-identical to the per-window probe path."""
 import numpy as np
 import pytest
 
-from paper_2511_02248_b200 import abi, device, model, scenarios, tables
+from paper_2511_02248_b200 import abi, device, model, tables
+from workloads import scenarios
 
 pytestmark = pytest.mark.gpu
 

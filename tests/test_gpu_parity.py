@@ -5,7 +5,8 @@ import numpy as np
 import pytest
 
 import golden_cases as G
-from paper_2511_02248_b200 import abi, model, plans, scenarios, tables
+from paper_2511_02248_b200 import abi, model, plans, tables
+from workloads import scenarios
 
 pytestmark = pytest.mark.gpu
 
@@ -279,6 +280,45 @@ def test_golden_greedy_cases(nat):
         if e:
             errs.append((c["name"], e))
     assert not errs, errs[:3]
+
+
+def test_greedy_trace_grows_past_trace_cap(nat):
+    """The reference's move trace is unbounded: with trace_cap = 1 or 3 the
+    drop-in re-plans the windows whose trace outgrew the cap and returns the
+    reference's full trace (never the RuntimeError it used to raise)."""
+    from paper_2511_02248_b200 import planners
+    cs = [c for c in G.load("greedy.json") if len(c["expected"].get("trace", [])) > 3]
+    assert len(cs) >= 10
+    for cap in (1, 3):
+        for c in cs:
+            prob = G.case_problem(c)
+            params = G.case_params(c)
+            out = nat.plan_windows_host(abi.MODE_OPERATOR, prob, G.case_windows(c),
+                                        greedy=tables.pack_greedy(prob, params), trace_cap=cap)
+            assert out.trace_cap >= len(c["expected"]["trace"])
+            plan = plans.WindowDecisions(prob, [G.case_point(c)], out, abi.MODE_OPERATOR).plan(0)
+            assert not G.compare_plan(plan, c["expected"], prob), c["name"]
+    # batched: several windows truncated at once, the others untouched
+    import json
+    groups = {}
+    for c in G.load("greedy.json"):
+        if "scenario" in c and "error" not in c["expected"]:
+            groups.setdefault((c["scenario"], json.dumps(c["params"]), c["point"]["phase"]), []).append(c)
+    same = max(groups.values(), key=lambda g: sum(len(c["expected"]["trace"]) > 2 for c in g))
+    c0 = same[0]
+    prob = G.case_problem(c0)
+    params = G.case_params(c0)
+    pts = [G.case_point(c) for c in same]
+    win = tables.pack_windows(pts, params.slo, params.epsilon)
+    out = nat.plan_windows_host(abi.MODE_OPERATOR, prob, win, greedy=tables.pack_greedy(prob, params),
+                                trace_cap=2)
+    dec = plans.WindowDecisions(prob, pts, out, abi.MODE_OPERATOR)
+    for k, c in enumerate(same):
+        assert not G.compare_plan(dec.plan(k), c["expected"], prob), c["name"]
+    plan = planners.greedy_autoscale(G.case_problem(c0).dag, G.case_problem(c0).profiles,
+                                     G.case_point(c0), params, trace_cap=1)
+    assert len(plan.trace) == len(c0["expected"]["trace"])
+    assert sum(len(c["expected"]["trace"]) > 2 for c in same) >= 3
 
 
 def test_full_trace_greedy_vs_oracle(nat, orc):

@@ -9,7 +9,8 @@ import numpy as np
 import pytest
 import torch
 
-from paper_2511_02248_b200 import _native, abi, device, dist as pdist, model, scenarios, tables
+from paper_2511_02248_b200 import _native, abi, device, dist as pdist, model, tables
+from workloads import scenarios
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -100,3 +101,36 @@ def test_host_buffer_round_trip_single_rank():
         for f in tables.DecisionArrays.FIELDS:
             assert getattr(out, f).tobytes() == getattr(want, f).tobytes(), (m, f)
     merge.close()
+
+
+def _need_gpus(n):
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs, {torch.cuda.device_count()} visible")
+
+
+def test_peer_merge_across_two_devices():
+    """Two ranks on two DIFFERENT GPUs (NCCL group, CUDA-IPC handles opened on
+    the peer device, NVLink atomics and the device barrier across the link):
+    every rank's decisions equal a single-rank plan on every step."""
+    _need_gpus(2)
+    env = dict(os.environ, OPSC_DIST_BACKEND="nccl", PYTHONPATH=os.path.dirname(HERE))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29537", os.path.join(HERE, "peer_worker.py")]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, (p.stdout[-2000:], p.stderr[-3000:])
+    assert p.stdout.count("ok") >= 2
+
+
+def test_bench_two_gpus_self_spawned():
+    """`bench.py --gpus 2` (no torchrun) spawns one rank per GPU and prints an
+    n_gpus: 2 line whose decisions match the CPU oracle."""
+    _need_gpus(2)
+    import json
+    repo = os.path.dirname(HERE)
+    p = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2", "--steps", "2",
+                        "--warmup", "3", "--no-latency", "--no-cpu-baseline"],
+                       capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["parity_vs_oracle"] is True
+    assert line["e2e"]["parity_vs_device_path"] is True

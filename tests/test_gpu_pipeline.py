@@ -4,7 +4,8 @@ host-side flow: reference-equivalent windowize, then the per-window planners."""
 import numpy as np
 import pytest
 
-from paper_2511_02248_b200 import model, pipeline, planners, scenarios, workload
+from paper_2511_02248_b200 import model, pipeline, planners, workload
+from workloads import scenarios
 
 pytestmark = pytest.mark.gpu
 

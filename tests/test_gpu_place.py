@@ -6,7 +6,8 @@ import pytest
 
 import golden_cases as G
 import test_oracle_place as TP
-from paper_2511_02248_b200 import abi, model, placement, scenarios, tables
+from paper_2511_02248_b200 import abi, model, placement, tables
+from workloads import scenarios
 
 pytestmark = pytest.mark.gpu
 

@@ -1,10 +1,11 @@
 """GPU windowize (csrc/k_windowize.cu) against the reference-generated window
-statistics (data/traces.npz) and the CPU oracle on unsorted / edge traces."""
+statistics (workloads/traces.npz) and the CPU oracle on unsorted / edge traces."""
 
 import numpy as np
 import pytest
 
-from paper_2511_02248_b200 import scenarios, workload
+from paper_2511_02248_b200 import workload
+from workloads import scenarios
 
 pytestmark = pytest.mark.gpu
 

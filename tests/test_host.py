@@ -14,8 +14,9 @@ import pytest
 import golden_cases as G
 from paper_2511_02248_b200 import (
     NoStableConfig, SearchSpaceTooLarge, UnknownPhase, UnknownProfile, abi, model, planners,
-    scenarios, tables, workload,
+    tables, workload,
 )
+from workloads import scenarios
 
 
 def test_pack_problem_topology():
@@ -259,3 +260,29 @@ def test_error_texts_match_reference(orc):
         assert str(got.value) == str(want.value), mode
         seen += 1
     assert seen == len(cases)
+
+
+@pytest.mark.parametrize("qps", [float("nan"), float("inf")])
+def test_nonfinite_qps_raises_like_reference(orc, qps):
+    """NaN / +inf qps pass the reference's `qps <= 0` check and fail in
+    _strict_min_replicas (autoscaler.py:225) in every planner: same class and
+    text from the drop-in (the device treats the window as idle)."""
+    from paper_2511_02248_b200 import plans
+    import refpkg
+    op = refpkg.import_reference()
+    dag_spec, prof = scenarios.SCENARIOS["cfg1"]
+    rdag, rprof = op.build_dag(dag_spec), op.perfmodel.profiles_from_dict(prof)
+    prob = tables.pack_problem(model.build_dag(dag_spec), model.profiles_from_dict(prof))
+    for mode, m in (("oracle", abi.MODE_ORACLE), ("model", abi.MODE_MODEL), ("operator", abi.MODE_OPERATOR)):
+        bnd = dict(r_max=2, b_max=1, parallelism=(1,))
+        with pytest.raises(Exception) as want:
+            op.runner.plan_for_mode(mode, rdag, rprof, op.WorkloadPoint(qps, 512, "prefill"),
+                                    op.AutoscaleParams(slo=0.5), op.BruteForceBounds(**bnd))
+        pt = model.WorkloadPoint(qps, 512, "prefill")
+        params = model.AutoscaleParams(slo=0.5)
+        out = orc.plan_windows(m, prob, tables.pack_windows([pt], 0.5, 0.0),
+                               grid=tables.pack_grid(prob, params, model.BruteForceBounds(**bnd)),
+                               model=tables.pack_model(prob, params), greedy=tables.pack_greedy(prob, params))
+        with pytest.raises(Exception) as got:
+            plans.WindowDecisions(prob, [pt], out, m, r_cap=512).plan(0)
+        assert type(got.value) is type(want.value) and str(got.value) == str(want.value), mode

@@ -6,7 +6,8 @@ import numpy as np
 import pytest
 
 import golden_cases as G
-from paper_2511_02248_b200 import abi, model, placement, scenarios, tables
+from paper_2511_02248_b200 import abi, model, placement, tables
+from workloads import scenarios
 
 
 def _setting_fleet(setting, slo, default_stream=False):

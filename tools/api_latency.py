@@ -10,7 +10,8 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2511_02248_b200 import model, planners, scenarios  # noqa: E402
+from paper_2511_02248_b200 import model, planners  # noqa: E402
+from workloads import scenarios  # noqa: E402
 from paper_2511_02248_b200.errors import NoStableConfig  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 30

@@ -17,7 +17,8 @@ import torch
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, REPO)
-from paper_2511_02248_b200 import _native, abi, model, scenarios, tables  # noqa: E402
+from paper_2511_02248_b200 import _native, abi, model, tables  # noqa: E402
+from workloads import scenarios  # noqa: E402
 
 BAND = float(sys.argv[1]) if len(sys.argv) > 1 else 64.0
 L = _native.load()

@@ -11,7 +11,8 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2511_02248_b200 import model, pipeline, placement, scenarios, workload  # noqa: E402
+from paper_2511_02248_b200 import model, pipeline, placement, workload  # noqa: E402
+from workloads import scenarios  # noqa: E402
 
 
 def main():

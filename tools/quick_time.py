@@ -8,7 +8,8 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
-from paper_2511_02248_b200 import _native, abi, model, scenarios, tables
+from paper_2511_02248_b200 import _native, abi, model, tables
+from workloads import scenarios
 
 nat = _native
 L = nat.load()

@@ -24,7 +24,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 import opscaler as ref  # noqa: E402
 from opscaler import autoscaler as A  # noqa: E402
 
-from paper_2511_02248_b200 import scenarios  # noqa: E402
+from workloads import scenarios  # noqa: E402
 
 A.MAX_ENUMERATION = 10**12
 

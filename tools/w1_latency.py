@@ -9,7 +9,8 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2511_02248_b200 import abi, device, model, scenarios, tables  # noqa: E402
+from paper_2511_02248_b200 import abi, device, model, tables  # noqa: E402
+from workloads import scenarios  # noqa: E402
 
 mode = {"model": abi.MODE_MODEL, "operator": abi.MODE_OPERATOR, "oracle": abi.MODE_ORACLE}[sys.argv[1]]
 nw = int(sys.argv[2]) if len(sys.argv) > 2 else 30

@@ -8,7 +8,8 @@ import sys
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2511_02248_b200 import abi, device, model, scenarios, tables  # noqa: E402
+from paper_2511_02248_b200 import abi, device, model, tables  # noqa: E402
+from workloads import scenarios  # noqa: E402
 
 prob = tables.pack_problem(*scenarios.scenario("cfg2"))
 tw = scenarios.trace_windows("cfg2")

@@ -17,8 +17,11 @@ tests/golden/ pin decisions on identical inputs.
 
 Window statistics of every trace (qps, seq_len per window and phase) were
 produced by the reference's synth_workload + windowize and are stored in
-data/traces.npz by tests/golden/make_traces.py; `workload.py` regenerates
-them bit-identically.
+workloads/traces.npz by tests/golden/make_traces.py; the package's
+`workload.py` regenerates them bit-identically.
+
+Bench and test data only: nothing in the product package
+(paper_2511_02248_b200/) imports this module.
 """
 
 from __future__ import annotations
@@ -27,9 +30,9 @@ import os
 
 import numpy as np
 
-from .model import build_dag, profiles_from_dict
+from paper_2511_02248_b200.model import build_dag, profiles_from_dict
 
-_DATA = os.path.join(os.path.dirname(__file__), "data")
+_DATA = os.path.dirname(os.path.abspath(__file__))
 
 
 def _chain(spec):
