@@ -77,22 +77,43 @@ def workload():
 # ---------------------------------------------------------------- CPU arm
 
 
-def cpu_run(problem, grid, win, target_s=12.0, threads=None):
-    """The CPU port (oracle/, literal enumeration, OpenMP over all host
-    threads) on an evenly spaced bounded sample of the workload windows."""
+CPU_SAMPLE_STEP = 2   # the CPU legs plan every 2nd window (720 of 1440); the GPU arm plans all
+
+
+def cpu_sample(win):
+    idx = np.arange(0, win.n, CPU_SAMPLE_STEP)
+    return idx[win.qps[idx] > 0]
+
+
+def common_config(win, active, space):
+    """The `config` both arms print (identical dicts: same workload, same sample)."""
+    return {"workload": WORKLOAD, "windows": win.n, "active_windows": active,
+            "candidates_per_window": space, "candidates_per_step": active * space,
+            "mode": "oracle (exhaustive brute force: every candidate of every window decided)",
+            "cpu_sample": f"every {CPU_SAMPLE_STEP}nd window ({len(cpu_sample(win))} of {win.n}): "
+                          "the CPU legs (--impl reference, cpu_baseline) plan these per step, the "
+                          "GPU arm plans all windows",
+            "l2": "flushed between timed GPU steps (256 MiB write outside the events)",
+            "workload_choice": "BASELINE config 5 is the throughput config (the 1e8-candidate x "
+                               "1440-window sweep sharded over 1/2/4/8 GPUs); config 2 (70B, 1 h "
+                               "trace, per-minute windows) is the decision-latency config: "
+                               "decision_latency_ms, incl. its batched candidates/s"}
+
+
+def reference_jobs(win, idx, mode="oracle"):
+    return [(mode, float(win.qps[i]), int(win.seq_len[i]), "prefill", float(win.slo[i])) for i in idx]
+
+
+def cpu_run(problem, grid, win, idx, threads=None):
+    """The CPU port (oracle/: the reference's arithmetic restated in C, literal
+    enumeration, OpenMP over all host threads) on windows `idx`."""
     from oracle import oracle as orc
     from paper_2511_02248_b200 import abi
     threads = threads or os.cpu_count() or 1
-    t = time.perf_counter()
-    orc.plan_windows(abi.MODE_ORACLE, problem, win.take(np.array([0])), grid=grid, n_threads=threads)
-    t1 = time.perf_counter() - t
-    k = int(max(1, min(win.n, round(target_s / max(t1, 1e-6)))))
-    idx = np.linspace(0, win.n - 1, k).round().astype(np.int64)
     sub = win.take(idx)
     t = time.perf_counter()
-    orc.plan_windows(abi.MODE_ORACLE, problem, sub, grid=grid, n_threads=threads)
-    dt = time.perf_counter() - t
-    return k, dt, threads
+    out = orc.plan_windows(abi.MODE_ORACLE, problem, sub, grid=grid, n_threads=threads)
+    return time.perf_counter() - t, threads, out
 
 
 def cpu_model():
@@ -105,34 +126,116 @@ def cpu_model():
     return "unknown"
 
 
+def reference_grid():
+    from workloads import scenarios
+    return dict(scenarios.GRIDS["cfg5"])
+
+
 def reference_arm(args):
+    """The reference's own CPU implementation of the path on this host's
+    cores: its Python brute_force_autoscale (branch-and-bound + greedy warm
+    start, baseline/reference_cpu.py) over one worker process per core, on
+    the stated window sample. If the reference package is not installed
+    (baseline/_ref), the C port of oracle/ stands in (kind "port")."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    sys.path.insert(0, os.path.join(REPO, "baseline"))
     problem, grid, win, space, active = workload()
+    idx = cpu_sample(win)
     times = []
-    sample = None
-    for i in range(args.warmup + args.steps):
-        k, dt, threads = cpu_run(problem, grid, win, target_s=8.0)
-        if i >= args.warmup:
-            times.append((k, dt))
-        sample = k
-    cands = sum(k * space for k, _ in times)
-    secs = sum(dt for _, dt in times)
-    value = cands / secs
+    from baseline import reference_cpu as RC
+    if RC.available():
+        pool = RC.Pool("cfg5", reference_grid())
+        jobs = reference_jobs(win, idx)
+        for i in range(args.warmup + args.steps):
+            wall, _ = pool.run(jobs)
+            if i >= args.warmup:
+                times.append(wall)
+        pool.close()
+        kind, cores = "reference", pool.workers
+        how = (f"the reference's own brute_force_autoscale (opscaler 0.1.0 from baseline/_ref, "
+               f"MAX_ENUMERATION raised), one worker process per core")
+        n_win = len(jobs)
+    else:
+        sub = idx[:: max(1, len(idx) // 72)]
+        for i in range(args.warmup + args.steps):
+            dt, cores, _ = cpu_run(problem, grid, win, sub)
+            if i >= args.warmup:
+                times.append(dt)
+        kind = "port"
+        how = "oracle/ C port (literal enumeration, OpenMP); reference package not installed"
+        n_win = len(sub)
+    secs = sum(times)
+    value = n_win * space * len(times) / secs
     line = {
         "impl": "reference", "metric": "candidate configs evaluated/sec", "value": value,
         "unit": "candidates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": secs / len(times) * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "windows": win.n, "candidates_per_window": space},
-        "cpu_baseline": {"value": value, "unit": "candidates/s", "cores": threads, "kind": "port",
-                         "sample": f"{sample} of {win.n} cfg5 prefill windows per step "
-                                   f"(evenly spaced), full pipeline, {cpu_model()}"},
+        "config": common_config(win, active, space),
+        "cpu_baseline": {"value": value, "unit": "candidates/s", "cores": cores, "kind": kind,
+                         "sample": f"{n_win} cfg5 prefill windows per step ({how}); semantic "
+                                   f"candidates = {space} per window; {cpu_model()}"},
         "e2e": {"value": value, "unit": "candidates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(problem, grid, win, space, dec):
+    """cpu_baseline of the GPU arm (rank 0, after every timed region):
+    (1) the reference's own Python brute force over all host cores on the
+        stated window sample -- `value`, and its decisions compared with this
+        run's GPU decisions (configs, objective, feasibility, latency bits);
+    (2) single-process per-window latency of the reference's three planners
+        (BASELINE.md CPU plan items 1-2: brute force on cfg5, model level and
+        greedy on the 70B cfg2 trace);
+    (3) the oracle/ C port (literal enumeration, OpenMP) on the same sample."""
+    from baseline import reference_cpu as RC
+    from workloads import scenarios
+    idx = cpu_sample(win)
+    out = {"unit": "candidates/s", "cpu": cpu_model()}
+    dt, threads, port = cpu_run(problem, grid, win, idx)
+    port_rate = len(idx) * space / dt
+    out["port"] = {"value": port_rate, "cores": threads, "seconds": dt,
+                   "what": "oracle/ C restatement, literal enumeration of every candidate, OpenMP"}
+    if not RC.available():
+        out.update(value=port_rate, cores=threads, kind="port",
+                   sample=f"{len(idx)} cfg5 prefill windows (every {CPU_SAMPLE_STEP}nd), oracle/ C port")
+        return out
+    pool = RC.Pool("cfg5", reference_grid())
+    jobs = reference_jobs(win, idx)
+    pool.run(jobs[: pool.workers])  # worker start-up
+    wall, res = pool.run(jobs)
+    pool.close()
+    ids = problem.ids
+    agree = True
+    for k, i in enumerate(idx):
+        r = res[k][1]
+        if isinstance(r, str):
+            agree &= int(dec.status[i]) != 0 and not dec.feasible[i]
+            continue
+        cfgs = tuple(sorted((ids[v], *(int(x) for x in dec.cfg[i, v])) for v in range(len(ids))))
+        agree &= (cfgs == r[0] and int(dec.objective[i]) == r[1] and bool(dec.feasible[i]) == r[2]
+                  and float(dec.latency[i]).hex() == r[3])
+    out.update(value=len(jobs) * space / wall, cores=pool.workers, kind="reference",
+               sample=f"{len(jobs)} cfg5 prefill windows (every {CPU_SAMPLE_STEP}nd): the reference's own "
+                      f"brute_force_autoscale (branch-and-bound + greedy warm start; semantic "
+                      f"candidates = {space} per window), one worker process per core",
+               parity_vs_gpu=bool(agree))
+    single = {}
+    g5 = reference_grid()
+    sub = idx[:: max(1, len(idx) // 24)]
+    single["brute_force_cfg5"] = RC.per_window_stats(RC.single("cfg5", g5, reference_jobs(win, sub)), space)
+    tw = scenarios.trace_windows("cfg2")
+    live = np.nonzero(tw["prefill_qps"] > 0)[0][::3]
+    jobs2 = lambda mode: [(mode, float(tw["prefill_qps"][i]), int(tw["prefill_len"][i]), "prefill",
+                           scenarios.SLO["cfg2"]["prefill"]) for i in live]
+    single["model_level_cfg2_70b"] = RC.per_window_stats(RC.single("cfg2", None, jobs2("model")))
+    single["greedy_cfg2_70b"] = RC.per_window_stats(RC.single("cfg2", None, jobs2("operator")))
+    out["reference_python_single_process"] = single
+    return out
 
 
 # ---------------------------------------------------------------- clocks
@@ -374,10 +477,7 @@ def ours(args):
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:  # after every timed region; other ranks wait
-        k, dt, threads = cpu_run(problem, grid, win, target_s=12.0)
-        cpu = {"value": k * space / dt, "unit": "candidates/s", "cores": threads, "kind": "port",
-               "sample": f"{k} of {win.n} cfg5 prefill windows (evenly spaced), full pipeline "
-                         f"(menus, literal enumeration, decode, materialise), OpenMP, {cpu_model()}"}
+        cpu = cpu_baseline(problem, grid, win, space, dec)
 
     if rank == 0:
         line = {
@@ -385,17 +485,10 @@ def ours(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "windows": win.n, "active_windows": active,
-                       "candidates_per_window": space, "candidates_per_step": cands_step,
-                       "mode": "oracle (exhaustive brute force, every candidate composed)",
-                       "parallelism": f"candidate-range shards x{world}" if world > 1 else "single GPU",
-                       "merge": merge_kind, "dist_backend": backend if world > 1 else None,
-                       "nccl_version": nccl,
-                       "l2": "flushed between timed steps (256 MiB write outside the events)",
-                       "workload_choice": "BASELINE config 5 is the throughput config (the 1e8-candidate x "
-                                          "1440-window sweep sharded over 1/2/4/8 GPUs); config 2 (70B, 1 h "
-                                          "trace, per-minute windows) is the decision-latency config: "
-                                          "decision_latency_ms, incl. its batched candidates/s"},
+            "config": common_config(win, active, space),
+            "run": {"parallelism": f"candidate-range shards x{world}" if world > 1 else "single GPU",
+                    "merge": merge_kind, "dist_backend": backend if world > 1 else None,
+                    "nccl_version": nccl},
             "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                          "kernel": "compose_kernel (opsc_compose_argmin)",

@@ -161,14 +161,17 @@ class Context:
         if out is None:
             out = tables.DecisionArrays(windows.n, problem.n_ops,
                                         trace_cap if mode == abi.MODE_OPERATOR else 0)
-        g = grid if grid is not None else abi.OpscGrid()
-        m = model if model is not None else abi.OpscModelSpec()
-        gs = greedy if greedy is not None else abi.OpscGreedySpec()
-        rc = load().opsc_plan_windows_host(self._p, mode, ref(problem.table), ref(g), ref(m),
-                                           ref(gs), ref(place.spec), windows.struct(),
-                                           out.struct())
+        g = grid if grid is not None else _EMPTY[0]
+        m = model if model is not None else _EMPTY[1]
+        gs = greedy if greedy is not None else _EMPTY[2]
+        A = C.addressof
+        rc = load().opsc_plan_windows_host(self._p, mode, A(problem.table), A(g), A(m), A(gs),
+                                           A(place.spec), windows.struct(), out.struct())
         check(rc, "opsc_plan_windows_host")
         return out
+
+
+_EMPTY = (abi.OpscGrid(), abi.OpscModelSpec(), abi.OpscGreedySpec())  # read-only placeholders
 
 
 def context():
@@ -181,7 +184,7 @@ def context():
 
 
 def plan_windows_host(mode, problem, windows, grid=None, model=None, place=None, greedy=None,
-                      trace_cap=4096):
+                      trace_cap=4096, out=None):
     """One host-buffer planning call on this thread's context. Greedy move
     traces have no length limit in the reference (max_iterations per loop plus
     headroom / prune entries, autoscaler.py:391, 446-587): windows whose
@@ -190,7 +193,7 @@ def plan_windows_host(mode, problem, windows, grid=None, model=None, place=None,
     deterministic, so only the trace rows change."""
     ctx = context()
     out = ctx.plan_windows(mode, problem, windows, grid=grid, model=model, place=place,
-                           greedy=greedy, trace_cap=trace_cap)
+                           greedy=greedy, trace_cap=trace_cap, out=out)
     if mode == abi.MODE_OPERATOR and out.trace_cap:
         import numpy as np
         cut = np.nonzero(out.status & abi.W_TRACE_TRUNCATED)[0]

@@ -22,12 +22,67 @@ planners keep them unless called with guards=False.
 from __future__ import annotations
 
 import math
+import threading
+
+import numpy as np
+from collections import OrderedDict
 
 from . import _native, abi, errors, model, tables
 from .plans import WindowDecisions
 
 MAX_ENUMERATION = 10_000_000
 MAX_BRUTE_FORCE_OPS = 6
+
+
+class _Packed:
+    """LRU of packed tables for the per-point API.
+
+    The reference's planners are called once per WorkloadPoint with the same
+    DAG / ProfileSet / AutoscaleParams objects (runner.run_point,
+    cli.cmd_autoscale's window loop), and repacking them dominated the
+    per-point cost. Entries are keyed by object identity and hold strong
+    references, so an id cannot be reused while cached; a ProfileSet (a
+    mutable container in the reference, perfmodel.py:111-130) is revalidated
+    by a cheap signature of its contents' identities, link bandwidth and
+    interference model. OperatorDag and AutoscaleParams / BruteForceBounds are
+    immutable by the reference's contract (opgraph.py:71-76, frozen
+    dataclasses at autoscaler.py:102, 688)."""
+
+    def __init__(self, size=32):
+        self.size, self.lock, self.d = size, threading.Lock(), OrderedDict()
+
+    def get(self, key, refs, sig, make):
+        with self.lock:
+            hit = self.d.get(key)
+            if hit is not None and hit[1] == sig and all(a is b for a, b in zip(hit[0], refs)):
+                self.d.move_to_end(key)
+                return hit[2]
+        val = make()
+        with self.lock:
+            self.d[key] = (refs, sig, val)
+            while len(self.d) > self.size:
+                self.d.popitem(last=False)
+        return val
+
+
+_PROBLEMS, _SPECS = _Packed(), _Packed(128)
+
+
+def _profile_sig(dag, profiles):
+    profs = getattr(profiles, "profiles", None)
+    return (len(dag.nodes), len(dag.edges), getattr(profiles, "link_bandwidth", None),
+            id(getattr(profiles, "interference", None)), id(profs),
+            tuple(map(id, profs.values())) if isinstance(profs, dict) else None)
+
+
+def packed_problem(dag, profiles):
+    """tables.pack_problem, cached per (DAG, ProfileSet) object."""
+    return _PROBLEMS.get((id(dag), id(profiles)), (dag, profiles), _profile_sig(dag, profiles),
+                         lambda: tables.pack_problem(dag, profiles))
+
+
+def _spec(kind, problem, params, bounds, make):
+    return _SPECS.get((kind, id(problem), id(params), id(bounds)), (problem, params, bounds), None, make)
 
 
 def _guard(problem, params, bounds, max_enumeration, err):
@@ -56,19 +111,21 @@ def brute_force_autoscale(dag, profiles, point, params, bounds=None, *, guards=T
     (ties: lexicographically smallest config vector in node-id order)."""
     bounds = bounds if bounds is not None else types.BruteForceBounds()
     _points_ok([point])
-    problem = tables.pack_problem(dag, profiles)
+    problem = packed_problem(dag, profiles)
     if guards:
         _guard(problem, params, bounds,
                MAX_ENUMERATION if max_enumeration is None else max_enumeration, err)
-    return _run(abi.MODE_ORACLE, problem, [point], params, bounds, fleet, energy, types, err).plan(0)
+    return _run(abi.MODE_ORACLE, problem, [point], params, bounds, fleet, energy, types, err,
+                single=True).plan(0)
 
 
 def model_level_autoscale(dag, profiles, point, params, *, fleet=None, energy=None,
                           types=model, err=errors):
     """Monolithic baseline: one (B, R) shared by every operator."""
     _points_ok([point])
-    problem = tables.pack_problem(dag, profiles)
-    return _run(abi.MODE_MODEL, problem, [point], params, None, fleet, energy, types, err).plan(0)
+    problem = packed_problem(dag, profiles)
+    return _run(abi.MODE_MODEL, problem, [point], params, None, fleet, energy, types, err,
+                single=True).plan(0)
 
 
 def greedy_autoscale(dag, profiles, point, params, *, fleet=None, energy=None, types=model,
@@ -77,22 +134,56 @@ def greedy_autoscale(dag, profiles, point, params, *, fleet=None, energy=None, t
     codes it, autoscaler.py:334-589), one CTA per window on the device; the
     returned plan carries the reference's move trace."""
     _points_ok([point])
-    problem = tables.pack_problem(dag, profiles)
+    problem = packed_problem(dag, profiles)
     return _run(abi.MODE_OPERATOR, problem, [point], params, None, fleet, energy, types, err,
-                trace_cap).plan(0)
+                trace_cap, single=True).plan(0)
 
 
-def _run(mode, problem, points, params, bounds, fleet, energy, types, err, trace_cap=4096):
+_TLS = threading.local()
+
+
+def _single_io(point, params, n_ops, tcap):
+    """Per-thread W=1 window / decision buffers of the per-point planners
+    (their plan is materialised before the call returns, so the next call may
+    overwrite them)."""
+    io = getattr(_TLS, "io", None)
+    if io is None:
+        io = _TLS.io = {}
+    win = io.get("win")
+    if win is None:
+        win = io["win"] = tables.WindowArrays(np.zeros(1), np.zeros(1, np.int32), np.zeros(1, np.uint8),
+                                              np.zeros(1), np.zeros(1))
+    win.qps[0], win.seq_len[0] = point.qps, point.seq_len
+    win.phase[0] = tables.PHASE_INDEX[point.phase]
+    win.slo[0], win.eps[0] = params.slo, params.epsilon
+    out = io.get((n_ops, tcap))
+    if out is None:
+        out = io[(n_ops, tcap)] = tables.DecisionArrays(1, n_ops, tcap)
+    return win, out
+
+
+def _run(mode, problem, points, params, bounds, fleet, energy, types, err, trace_cap=4096, single=False):
     phases = {p.phase for p in points}
     for ph in sorted(phases):
         problem.require_phase(ph)
-    win = tables.pack_windows(points, params.slo, params.epsilon)
-    grid = tables.pack_grid(problem, params, bounds) if mode == abi.MODE_ORACLE else None
-    spec = tables.pack_model(problem, params) if mode == abi.MODE_MODEL else None
-    greedy = tables.pack_greedy(problem, params) if mode == abi.MODE_OPERATOR else None
-    place = tables.pack_place(fleet, energy)
+    out = None
+    if single:
+        win, out = _single_io(points[0], params, problem.n_ops,
+                              trace_cap if mode == abi.MODE_OPERATOR else 0)
+    else:
+        win = tables.pack_windows(points, params.slo, params.epsilon)
+    grid = spec = greedy = None
+    if mode == abi.MODE_ORACLE:
+        grid = _spec("grid", problem, params, bounds, lambda: tables.pack_grid(problem, params, bounds))
+    elif mode == abi.MODE_MODEL:
+        spec = _spec("model", problem, params, None, lambda: tables.pack_model(problem, params))
+    else:
+        greedy = _spec("greedy", problem, params, None, lambda: tables.pack_greedy(problem, params))
+    place = _SPECS.get(("place", id(fleet), id(energy)), (fleet, energy),
+                       None if fleet is None else tuple(map(id, fleet)),
+                       lambda: tables.pack_place(fleet, energy))
     arrays = _native.plan_windows_host(mode, problem, win, grid=grid, model=spec, place=place,
-                                       greedy=greedy, trace_cap=trace_cap)
+                                       greedy=greedy, trace_cap=trace_cap, out=out)
     return WindowDecisions(problem, points, arrays, mode, types, err, r_cap=params.r_cap)
 
 
@@ -110,7 +201,7 @@ def decide_windows(dag, profiles, points, params, mode="oracle", bounds=None, *,
     """
     m = _MODES[mode] if isinstance(mode, str) else mode
     bounds = bounds if (bounds is not None or m != abi.MODE_ORACLE) else types.BruteForceBounds()
-    problem = tables.pack_problem(dag, profiles)
+    problem = packed_problem(dag, profiles)
     by_phase = params if isinstance(params, dict) else None
     groups = {}
     for i, p in enumerate(points):

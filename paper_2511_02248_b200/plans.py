@@ -68,6 +68,40 @@ def nonfinite_qps(qps):
         raise OverflowError("cannot convert float infinity to integer")
 
 
+def _builder(cls, names):
+    """Fast constructor for the plan's frozen value types (OperatorConfig,
+    PredictedSojourn -- this package's or the reference's, autoscaler.py:44-73):
+    fills the instance dict directly, skipping dataclass __init__ /
+    __post_init__, whose checks (P, R, B >= 1) the device results satisfy by
+    construction. Equality, hash and repr are the dataclass's own. Classes
+    without an instance dict fall back to the normal constructor."""
+    probe = object.__new__(cls)
+    if not hasattr(probe, "__dict__"):
+        return cls
+    new = object.__new__
+
+    def make(*vals):
+        o = new(cls)
+        o.__dict__.update(zip(names, vals))
+        return o
+    return make
+
+
+_BUILDERS = {}
+
+
+def builders(T):
+    b = _BUILDERS.get(id(T))
+    if b is None or b[0] is not T:
+        import dataclasses
+        oc = T.OperatorConfig
+        ps = T.PredictedSojourn
+        b = (T, _builder(oc, [f.name for f in dataclasses.fields(oc)]),
+             _builder(ps, [f.name for f in dataclasses.fields(ps)]))
+        _BUILDERS[id(T)] = b
+    return b[1], b[2]
+
+
 @dataclass
 class PlanMetrics:
     """Default-stream placement figures of a feasible plan (runner.py:94-96)."""
@@ -103,17 +137,18 @@ class WindowDecisions:
         if self.mode == abi.MODE_ORACLE:
             order = range(n)
         else:
-            order = [self.problem.table.node_order[k] for k in range(n)]
+            order = self.problem.node_order
+        cfg, pred, stable = a.cfg[i].tolist(), a.pred[i].tolist(), a.stable[i].tolist()
+        OC, PS = builders(T)
         configs, predicted = {}, {}
         for v in order:
-            p, r, b = (int(x) for x in a.cfg[i, v])
-            configs[ids[v]] = T.OperatorConfig(p=p, r=r, b=b)
-            f = [float(x) for x in a.pred[i, v]]
-            predicted[ids[v]] = T.PredictedSojourn(
-                op_latency=f[0], lam=f[1], mu=f[2], utilization=f[3], wait=f[4],
-                service=f[5], comm=f[6], stable=bool(a.stable[i, v]))
+            p, r, b = cfg[v]
+            op = ids[v]
+            configs[op] = OC(p, r, b, 100)  # sm_share: planners run at 100 (autoscaler.py:50)
+            f = pred[v]
+            predicted[op] = PS(f[0], f[1], f[2], f[3], f[4], f[5], f[6], bool(stable[v]))
         lat = float(a.latency[i])
-        path = [ids[x] for x in a.path[i] if x >= 0] if math.isfinite(lat) else []
+        path = [ids[x] for x in a.path[i].tolist() if x >= 0] if math.isfinite(lat) else []
         return T.ScalingPlan(
             configs=configs, predicted=predicted, iteration_latency=lat,
             critical_path=path, objective=int(a.objective[i]),
@@ -126,14 +161,14 @@ class WindowDecisions:
         if self.mode != abi.MODE_OPERATOR or not a.trace_cap:
             return []
         out = []
-        for t in a.trace[i, :min(int(a.trace_len[i]), a.trace_cap)]:
-            name = abi.ACTION_NAMES[int(t["action"])]
+        ids = self.problem.ids
+        for lat, obj, r, b, p, op, act, _ in a.trace[i, :min(int(a.trace_len[i]), a.trace_cap)].tolist():
+            name = abi.ACTION_NAMES[act]
             if name == "reseed_uniform":
-                out.append({"action": name, "objective": int(t["objective"])})
+                out.append({"action": name, "objective": obj})
             else:
-                out.append({"action": name, "op": self.problem.ids[int(t["op"])],
-                            "to": {"R": int(t["to_r"]), "B": int(t["to_b"]), "P": int(t["to_p"])},
-                            "latency": float(t["latency"]), "objective": int(t["objective"])})
+                out.append({"action": name, "op": ids[op], "to": {"R": r, "B": b, "P": p},
+                            "latency": lat, "objective": obj})
         return out
 
     def plans(self):

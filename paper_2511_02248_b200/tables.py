@@ -41,6 +41,11 @@ class Problem:
     def n_ops(self):
         return len(self.ids)
 
+    @property
+    def node_order(self):
+        """Lex ranks in dag.node_ids order (the model level's / greedy's config order)."""
+        return [self.table.node_order[k] for k in range(len(self.ids))]
+
     def require_phase(self, phase):
         """UnknownPhase exactly when some operator's profile lacks `phase`
         (perfmodel.py:100-105), which the reference hits on the first
@@ -219,10 +224,17 @@ class WindowArrays:
         return int(self.qps.shape[0])
 
     def struct(self) -> abi.OpscWindows:
+        """The C-ABI view (cached while the same arrays are attached: building
+        it costs ~10 us of numpy attribute lookups per call)."""
+        arrs = (self.qps, self.seq_len, self.phase, self.slo, self.eps)
+        hit = self.__dict__.get("_struct")
+        if hit is not None and all(a is b for a, b in zip(hit[0], arrs)):
+            return hit[1]
         w = abi.OpscWindows()
         w.n = self.n
         w.qps, w.seq_len, w.phase = self.qps.ctypes.data, self.seq_len.ctypes.data, self.phase.ctypes.data
         w.slo, w.eps = self.slo.ctypes.data, self.eps.ctypes.data
+        self.__dict__["_struct"] = (arrs, w)
         return w
 
     def take(self, idx):
@@ -287,12 +299,18 @@ class DecisionArrays:
               "pred", "stable", "energy", "memory", "devices")
 
     def struct(self) -> abi.OpscDecisions:
+        """The C-ABI view (cached while the same arrays are attached)."""
+        arrs = tuple(getattr(self, f) for f in self.FIELDS) + (self.trace_len, self.trace)
+        hit = self.__dict__.get("_struct")
+        if hit is not None and hit[2] == self.trace_cap and all(a is b for a, b in zip(hit[0], arrs)):
+            return hit[1]
         d = abi.OpscDecisions()
         for f in self.FIELDS:
             setattr(d, f, getattr(self, f).ctypes.data)
         d.trace_cap = self.trace_cap
         d.trace_len = self.trace_len.ctypes.data
         d.trace = self.trace.ctypes.data
+        self.__dict__["_struct"] = (arrs, d, self.trace_cap)
         return d
 
     def nbytes(self):
