@@ -384,6 +384,21 @@ def ours(args):
         ref = orc.plan_windows(abi.MODE_ORACLE, problem, win.take(idx), grid=grid)
         parity = all(getattr(dec, f)[idx].tobytes() == getattr(ref, f).tobytes()
                      for f in ("key", "cfg", "latency", "energy", "memory", "devices"))
+    # summation-order certificate over every window of this run (outside the
+    # timed region): argmin at slo -/+ 64 ulps must agree, else the decision
+    # could depend on the reference's frozenset-ordered leaf sum
+    certificate = None
+    if rank == 0:
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        planner.certify()
+        c1.record()
+        c1.synchronize()
+        st = planner.out_t["status"].cpu().numpy().view(np.uint32)
+        certificate = {"windows": int(win.n), "band_ulps": abi.CERTIFY_BAND_ULPS,
+                       "order_sensitive_windows": int(((st & abi.W_ORDER_SENSITIVE) != 0).sum()),
+                       "ms": c0.elapsed_time(c1),
+                       "what": "OPSC_W_ORDER_SENSITIVE: argmin(lat <= slo - band) != argmin(lat <= slo + band)"}
 
     # roofline of the dominant kernel (compose_argmin)
     peak = device.fp64_peak()
@@ -505,6 +520,7 @@ def ours(args):
             "clocks": clk.summary(),
             "decision_latency_ms": latency,
             "parity_vs_oracle": parity,
+            "order_certificate": certificate,
         }
         print(json.dumps(line), flush=True)
     if merge is not None:

@@ -86,6 +86,16 @@ extern "C" {
 
 #define OPSC_W_NO_STABLE_INIT 0x100u    /* NoStableConfig from init_configs (autoscaler.py:289) in greedy mode */
 #define OPSC_W_TRACE_TRUNCATED 0x200u   /* more trace entries than trace_cap */
+#define OPSC_W_ORDER_SENSITIVE 0x400u   /* brute force, opt-in certificate (OPSC_PLAN_CERTIFY /
+                                           opsc_certify_order): the decision could depend on the
+                                           reference's frozenset-ordered leaf sum (autoscaler.py:792-796),
+                                           i.e. argmin over lat <= slo - band != argmin over
+                                           lat <= slo + band (band = OPSC_CERTIFY_BAND_ULPS ulps of slo) */
+/* OR'ed into the mode of opsc_plan_windows_host: brute force also runs the
+ * order certificate and sets OPSC_W_ORDER_SENSITIVE (ignored by the other modes,
+ * whose latencies are the canonical critical_path_latency, opgraph.py:223-244) */
+#define OPSC_PLAN_CERTIFY 0x100
+#define OPSC_CERTIFY_BAND_ULPS 64.0
 /* Which operator the reference's NoStableConfig message names (so the host can
  * raise it with the reference's exact text):
  *   bits 16..21: 1 + position in dag.node_ids order of the first operator
@@ -241,6 +251,18 @@ OPSC_API int opsc_stability_check(const OpscDag* dag, const OpscGrid* grid, Opsc
  * count_out must be zeroed by the caller. */
 OPSC_API int opsc_compose_boundary(const OpscDag* dag, const OpscGrid* grid, OpscWindows win,
                                    const double* menu_w, double band_ulps, int64_t* count_out, void* stream);
+
+/* Opt-in summation-order certificate of brute-force decisions
+ * (autoscaler.py:765, 792-796: the reference's leaf sums path weights over a
+ * frozenset, so its order depends on PYTHONHASHSEED). Runs the compose argmin
+ * twice more with slo -/+ band_ulps ulps and ORs OPSC_W_ORDER_SENSITIVE into
+ * status where the two keys differ. Windows left unflagged decide identically
+ * under every summation order whose error stays inside the band.
+ * workspace: opsc_certify_workspace(win.n) bytes of device memory. */
+OPSC_API size_t opsc_certify_workspace(int32_t n_windows);
+OPSC_API int opsc_certify_order(const OpscDag* dag, const OpscGrid* grid, OpscWindows win,
+                                const double* menu_w, double band_ulps, void* workspace,
+                                size_t workspace_bytes, uint32_t* status, void* stream);
 
 /* Exhaustive compose + SLO mask + lexicographic argmin over the shard
  * [shard/n_shards] of every window's candidate space. key_out must be

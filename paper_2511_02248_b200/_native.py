@@ -30,6 +30,7 @@ EXPORTS = (
     "opsc_model_grid_table", "opsc_place_shared_workspace", "opsc_place_shared",
     "opsc_ipc_alloc", "opsc_ipc_open", "opsc_ipc_close", "opsc_ipc_free",
     "opsc_compose_argmin_peers", "opsc_peer_barrier", "opsc_copy_keys",
+    "opsc_certify_workspace", "opsc_certify_order",
 )
 
 _lib = None
@@ -87,6 +88,8 @@ def load():
             "opsc_compose_argmin_peers": ([P, P, W, P, I, I, P, I, P], C.c_int),
             "opsc_peer_barrier": ([P, I, I, C.c_uint32, I, P, P], C.c_int),
             "opsc_copy_keys": ([P, P, I, P], C.c_int),
+            "opsc_certify_workspace": ([I], C.c_size_t),
+            "opsc_certify_order": ([P, P, W, P, C.c_double, P, C.c_size_t, P, P], C.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -156,7 +159,7 @@ class Context:
         return ms.value
 
     def plan_windows(self, mode, problem, windows, grid=None, model=None, place=None, out=None,
-                     greedy=None, trace_cap=4096):
+                     greedy=None, trace_cap=4096, certify=False):
         place = place or tables.pack_place()
         if out is None:
             out = tables.DecisionArrays(windows.n, problem.n_ops,
@@ -165,7 +168,8 @@ class Context:
         m = model if model is not None else _EMPTY[1]
         gs = greedy if greedy is not None else _EMPTY[2]
         A = C.addressof
-        rc = load().opsc_plan_windows_host(self._p, mode, A(problem.table), A(g), A(m), A(gs),
+        flags = abi.PLAN_CERTIFY if certify and mode == abi.MODE_ORACLE else 0
+        rc = load().opsc_plan_windows_host(self._p, mode | flags, A(problem.table), A(g), A(m), A(gs),
                                            A(place.spec), windows.struct(), out.struct())
         check(rc, "opsc_plan_windows_host")
         return out
@@ -184,7 +188,7 @@ def context():
 
 
 def plan_windows_host(mode, problem, windows, grid=None, model=None, place=None, greedy=None,
-                      trace_cap=4096, out=None):
+                      trace_cap=4096, out=None, certify=False):
     """One host-buffer planning call on this thread's context. Greedy move
     traces have no length limit in the reference (max_iterations per loop plus
     headroom / prune entries, autoscaler.py:391, 446-587): windows whose
@@ -193,7 +197,7 @@ def plan_windows_host(mode, problem, windows, grid=None, model=None, place=None,
     deterministic, so only the trace rows change."""
     ctx = context()
     out = ctx.plan_windows(mode, problem, windows, grid=grid, model=model, place=place,
-                           greedy=greedy, trace_cap=trace_cap, out=out)
+                           greedy=greedy, trace_cap=trace_cap, out=out, certify=certify)
     if mode == abi.MODE_OPERATOR and out.trace_cap:
         import numpy as np
         cut = np.nonzero(out.status & abi.W_TRACE_TRUNCATED)[0]

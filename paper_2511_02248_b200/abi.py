@@ -25,6 +25,7 @@ W_INFEASIBLE_PLACEMENT = 0x40
 W_IDLE = 0x80
 W_NO_STABLE_INIT = 0x100
 W_TRACE_TRUNCATED = 0x200
+W_ORDER_SENSITIVE = 0x400  # opt-in brute-force certificate: decision may depend on the leaf-sum order
 W_INIT_OP_SHIFT = 16     # 1 + dag.node_ids position of the op init_configs names
 W_BOUNDS_OP_SHIFT = 22   # 1 + lex rank of the op without a finite menu entry
 W_OP_FIELD = 0x3F
@@ -35,6 +36,8 @@ ACTION_NAMES = {1: "upscale", 2: "downscale", 3: "headroom", 4: "prune", 5: "res
 MODE_ORACLE = 0
 MODE_MODEL = 1
 MODE_OPERATOR = 2
+PLAN_CERTIFY = 0x100       # OR'ed into the host-buffer mode: run the order certificate (brute force)
+CERTIFY_BAND_ULPS = 64.0
 
 KEY_INFEASIBLE = 0x7FFFFFFFFFFFFFFF
 KEY_LEX_BITS = 40

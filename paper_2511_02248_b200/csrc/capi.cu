@@ -91,6 +91,8 @@ struct OpscContext {
   double* menu = nullptr;
   int32_t* fb = nullptr;
   double* mem_cap = nullptr;
+  unsigned char* cert = nullptr;     // order-certificate workspace (OPSC_PLAN_CERTIFY)
+  size_t cap_cert = 0;
   // decisions
   unsigned long long* key = nullptr;
   int16_t* cfg = nullptr;
@@ -392,6 +394,20 @@ int opsc_compose_boundary(const OpscDag* dag, const OpscGrid* grid, OpscWindows 
                                            (unsigned long long*)count_out, (cudaStream_t)stream));
 }
 
+size_t opsc_certify_workspace(int32_t n_windows) { return certify_workspace(n_windows); }
+
+int opsc_certify_order(const OpscDag* dag, const OpscGrid* grid, OpscWindows win, const double* menu_w,
+                       double band_ulps, void* workspace, size_t workspace_bytes, uint32_t* status, void* stream) {
+  if (!valid_dag(dag) || !grid || !status || !workspace || !(band_ulps >= 0.0) || win.n < 0 ||
+      workspace_bytes < certify_workspace(win.n))
+    return OPSC_ERR_ARG;
+  ComposeCfg c;
+  const int rc = compose_setup(*dag, *grid, win.n, 0, 1, &c);
+  if (rc != OPSC_OK) return rc;
+  return from_cuda(launch_certify(c, *grid, win.n, menu_w, win.slo, win.qps, band_ulps, workspace, status,
+                                  (cudaStream_t)stream));
+}
+
 int opsc_compose_argmin_peers(const OpscDag* dag, const OpscGrid* grid, OpscWindows win, const double* menu_w,
                               int32_t shard, int32_t n_shards, int64_t* const* peer_keys, int32_t n_peers,
                               void* stream) {
@@ -524,7 +540,7 @@ int opsc_ctx_destroy(OpscContext* c) {
   if (!c) return OPSC_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  void* ptrs[] = {c->io, c->menu, c->fb, c->u_cfg, c->u_feas, c->u_status, c->gstate, c->mtab};
+  void* ptrs[] = {c->io, c->menu, c->fb, c->u_cfg, c->u_feas, c->u_status, c->gstate, c->mtab, c->cert};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& g : c->graphs)
@@ -639,6 +655,10 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
                            const OpscModelSpec* model, const OpscGreedySpec* greedy,
                            const OpscPlaceSpec* place, OpscWindows win, OpscDecisions out) {
   if (!c || !valid_dag(dag) || !place || win.n < 0) return OPSC_ERR_ARG;
+  if (mode & ~(int32_t)(0xff | OPSC_PLAN_CERTIFY)) return OPSC_ERR_ARG;
+  const int32_t flags = mode;
+  mode &= 0xff;
+  const bool certify = mode == OPSC_MODE_ORACLE && (flags & OPSC_PLAN_CERTIFY);
   if (mode == OPSC_MODE_ORACLE && !grid) return OPSC_ERR_ARG;
   if (mode == OPSC_MODE_MODEL && !model) return OPSC_ERR_ARG;
   if (mode == OPSC_MODE_OPERATOR && !greedy) return OPSC_ERR_ARG;
@@ -662,6 +682,15 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
   void* tw = mode == OPSC_MODE_MODEL ? model_table_ws(c, W, *model, n, &tb) : nullptr;  // before any capture
   ComposeCfg cc;
   if (mode == OPSC_MODE_ORACLE && (rc = compose_setup(*dag, *grid, W, 0, 1, &cc))) return rc;
+  if (certify && certify_workspace(W) > c->cap_cert) {  // before any capture
+    if (regrow(c->cert, certify_workspace(W)) != cudaSuccess) {
+      cudaGetLastError();
+      c->cap_cert = 0;
+      return OPSC_ERR_CUDA;
+    }
+    c->cap_cert = certify_workspace(W);
+    c->gen++;
+  }
   cudaStream_t s = c->stream;
   cudaError_t e;
 #define CK(x)                   \
@@ -715,6 +744,10 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
       EQ(launch_menu_build(*dag, *grid, dw, c->menu, c->status, s));
       EQ(launch_stability(*dag, *grid, dw, c->status, s));
       EQ(launch_compose(cc, *grid, W, c->menu, c->slo, c->qps, c->key, s));
+      if (certify) {
+        EQ(launch_certify(cc, *grid, W, c->menu, c->slo, c->qps, OPSC_CERTIFY_BAND_ULPS, c->cert, c->status, s));
+        c->launches += 4;
+      }
       EQ(launch_fallback(*dag, *grid, W, c->menu, c->fb, s));
       EQ(launch_decode(*dag, *grid, W, c->key, c->fb, c->cfg, c->feasible, c->status, s));
       c->launches += 5;
@@ -761,7 +794,7 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
   int graph_launches = 0;
   if (stage && !getenv("OPSC_NO_GRAPH")) {
     std::vector<unsigned char> sig;
-    plan_signature(sig, c, mode, W, tcap, ndev, dag, grid, model, greedy, place);
+    plan_signature(sig, c, certify ? flags : mode, W, tcap, ndev, dag, grid, model, greedy, place);
     c->tick++;
     OpscContext::Graph* hit = nullptr;
     for (auto& g : c->graphs)

@@ -120,6 +120,18 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
   return v;
 }
 
+// max(0, x) for the path-suffix DP: dp_in of a position fed by one
+// predecessor (in = 0.0, then max with its value). Three instructions
+// (DSETP + two selects) instead of fmax's NaN/-0 sequence; differs from fmax
+// only in the sign of a zero, which no later add or SLO compare can see.
+__device__ __forceinline__ double clamp0(double x) {
+  double r;  // inline PTX: the front end would turn the select back into fmax
+  asm("{ .reg .pred p; setp.gt.f64 p, %1, 0d0000000000000000; selp.f64 %0, %1, 0d0000000000000000, p; }"
+      : "=d"(r)
+      : "d"(x));
+  return r;
+}
+
 // Exact count: the feasible j form a prefix in weight order.
 template <int NJ>
 __device__ __forceinline__ uint32_t exact_count(double bj, const double (&wj)[NJ], double slo) {
@@ -146,7 +158,7 @@ template <int NJ, bool CHAIN>
 __device__ __forceinline__ uint32_t k_level_tile(uint32_t a_wk, uint32_t a_kk, uint32_t a_pm, int mk,
                                                  const double (&wj)[NJ], double in_k, double bj0, double lo0,
                                                  bool k_to_j, bool k_sink, double slo) {
-  uint32_t mbest = 0xffffffffu;
+  uint32_t mbest = kLocalInfeasible;  // min with any infeasible kl (>= 2^31) stays 2^31
   const uint32_t a_end = a_kk + 4u * (uint32_t)mk;
 #pragma unroll(kKUnroll)
   for (; a_kk < a_end; a_kk += 4u, a_wk += 8u) {
@@ -161,15 +173,14 @@ __device__ __forceinline__ uint32_t k_level_tile(uint32_t a_wk, uint32_t a_kk, u
 // Small menus (m_k <= NJ <= 8): the k menu in registers too, fully unrolled
 // (padding: w = +inf never passes, local key 0 + pm32[0] = infeasible).
 template <int NJ, bool CHAIN>
-__device__ __forceinline__ uint32_t k_level_reg(uint32_t a_pm, const double (&wk)[NJ], const uint32_t (&kk)[NJ],
-                                                const double (&wj)[NJ], double in_k, double bj0, double lo0,
-                                                bool k_to_j, bool k_sink, double slo) {
-  uint32_t mbest = 0xffffffffu;
+__device__ __forceinline__ uint32_t k_level_reg(uint32_t a_pm, const double (&wk)[NJ],
+                                                const uint32_t (&kk)[NJ], const double (&wj)[NJ], double in_k,
+                                                double bj0, double lo0, bool k_to_j, bool k_sink, double slo) {
+  uint32_t mbest = kLocalInfeasible;
 #pragma unroll
   for (int a = 0; a < NJ; ++a) {
     const double bj = j_base<CHAIN>(in_k + wk[a], bj0, lo0, k_to_j, k_sink, slo);
-    const uint32_t cnt = exact_count<NJ>(bj, wj, slo);
-    const uint32_t kl = kk[a] + lds_u32(a_pm + 4u * cnt);
+    const uint32_t kl = kk[a] + lds_u32(a_pm + 4u * exact_count<NJ>(bj, wj, slo));
     mbest = kl < mbest ? kl : mbest;
   }
   return mbest;
@@ -497,8 +508,10 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
           } else {
             m32 = k_level_tile<NJ, CHAIN>(a_wk, a_kk, a_pm, mk_r, wj, in_k, bj0, lo0, k_to_j, k_sink, slo);
           }
-          const uint32_t t = m32 + pb;  // no overflow: feasible m32 + pb < 2^31
-          if (m32 < kLocalInfeasible) best32 = t < best32 ? t : best32;
+          // m32 < 2^31 + (kk part) and kk part + pb < 2^31 (the host's local-key
+          // budget), so m32 + pb never wraps and stays >= 2^31 when infeasible
+          const uint32_t t = m32 + pb;
+          best32 = t < best32 ? t : best32;
         } else {
           const unsigned long long mbest = k_level_smem<CHAIN>(s, mk, mj, koff, in_k, bj0, lo0, k_to_j, k_sink, slo);
           if (mbest < kSentinel) {
@@ -569,7 +582,7 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
               const int pos = nout + l;
               const int e = c.off[pos] + od[l];
               if constexpr (PATH) {
-                pv = fmax(0.0, pv + s.w[e]);  // val[pos], then the next position's dp_in
+                pv = clamp0(pv + s.w[e]);  // val[pos], then the next position's dp_in
               } else {
                 double in = o_in[l];
   #pragma unroll
@@ -598,7 +611,7 @@ compose_kernel(const __grid_constant__ ComposeCfg c, const __grid_constant__ Ops
             const long long cost1 = tkey ? 0 : pc + s.cost[e];
             const unsigned long long lex1 = tkey ? 0ull : pl + (unsigned long long)i * stride_last;
             if constexpr (PATH) {
-              kj_levels(fmax(0.0, pv + wl), 0.0, 0.0, pb, cost1, lex1);
+              kj_levels(clamp0(pv + wl), 0.0, 0.0, pb, cost1, lex1);
             } else {
               const double v = in_last + wl;
               double ik = last_to_k ? fmax(in_k, v) : in_k;
@@ -890,6 +903,61 @@ cudaError_t launch_compose_boundary(const ComposeCfg& c0, const OpscGrid& g, int
   compose_flat_kernel<true><<<(unsigned)blocks, kComposeThreads, 0, s>>>(c, g, menu_w, slo, qps, count, pk,
                                                                           band_ulps);
   return cudaGetLastError();
+}
+
+
+// Summation-order certificate (opt-in, OPSC_PLAN_CERTIFY / opsc_certify_order).
+// The reference accepts a leaf when its frozenset-ordered plain and Neumaier
+// path sums are <= slo (autoscaler.py:792-796); any such sum of the same
+// weights lies within a few ulps of the canonical DP latency. With
+// band = band_ulps * ulp(slo), every candidate the reference could accept is
+// in F_hi = {lat <= slo + band} and every candidate it must accept is in
+// F_lo = {lat <= slo - band}. The reference's argmin is squeezed between
+// argmin(F_hi) and argmin(F_lo) (the same key order), so equal keys certify
+// the window's decision for every PYTHONHASHSEED (both empty: the per-op
+// fallback, which does not depend on the SLO). Unequal keys set
+// OPSC_W_ORDER_SENSITIVE. Cost: two more compose launches over the window.
+__global__ void certify_prep_kernel(int n, const double* __restrict__ slo, double band_ulps, double* __restrict__ lo,
+                                    double* __restrict__ hi, unsigned long long* __restrict__ klo,
+                                    unsigned long long* __restrict__ khi) {
+  pdl_trigger();
+  pdl_wait();
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= n) return;
+  const double s = slo[w];
+  double band = 0.0;
+  if (s < OPSC_INF) band = band_ulps * (nextafter(s, OPSC_INF) - s);
+  lo[w] = s - band;
+  hi[w] = s + band;
+  klo[w] = (unsigned long long)OPSC_KEY_INFEASIBLE;
+  khi[w] = (unsigned long long)OPSC_KEY_INFEASIBLE;
+}
+
+__global__ void certify_mark_kernel(int n, const unsigned long long* __restrict__ klo,
+                                    const unsigned long long* __restrict__ khi, uint32_t* __restrict__ status) {
+  pdl_trigger();
+  pdl_wait();
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w < n && klo[w] != khi[w]) status[w] |= OPSC_W_ORDER_SENSITIVE;
+}
+
+size_t certify_workspace(int n_windows) { return n_windows > 0 ? (size_t)n_windows * 32u : 0u; }
+
+cudaError_t launch_certify(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,
+                           const double* slo, const double* qps, double band_ulps, void* ws, uint32_t* status,
+                           cudaStream_t s) {
+  if (n_windows <= 0) return cudaSuccess;
+  double* lo = (double*)ws;
+  double* hi = lo + n_windows;
+  unsigned long long* klo = (unsigned long long*)(hi + n_windows);
+  unsigned long long* khi = klo + n_windows;
+  const unsigned nb = (unsigned)((n_windows + 255) / 256);
+  cudaError_t e = launch_pdl(certify_prep_kernel, dim3(nb), dim3(256), 0, s, n_windows, slo, band_ulps, lo, hi, klo, khi);
+  if (e == cudaSuccess) e = launch_compose(c, g, n_windows, menu_w, lo, qps, klo, s);
+  if (e == cudaSuccess) e = launch_compose(c, g, n_windows, menu_w, hi, qps, khi, s);
+  if (e == cudaSuccess) e = launch_pdl(certify_mark_kernel, dim3(nb), dim3(256), 0, s, n_windows,
+                                       (const unsigned long long*)klo, (const unsigned long long*)khi, status);
+  return e;
 }
 
 }  // namespace opsc

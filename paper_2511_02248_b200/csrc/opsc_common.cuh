@@ -353,6 +353,10 @@ cudaError_t launch_compose(const ComposeCfg& c, const OpscGrid& g, int n_windows
 cudaError_t launch_compose_boundary(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,
                                     const double* slo, const double* qps, double band_ulps,
                                     unsigned long long* count, cudaStream_t s);
+size_t certify_workspace(int n_windows);
+cudaError_t launch_certify(const ComposeCfg& c, const OpscGrid& g, int n_windows, const double* menu_w,
+                           const double* slo, const double* qps, double band_ulps, void* ws, uint32_t* status,
+                           cudaStream_t s);
 cudaError_t launch_peer_barrier(const PeerFlags& f, int rank, int n, uint32_t epoch, int timeout_ms,
                                 int32_t* err, cudaStream_t s);
 cudaError_t launch_model_grid(const OpscDag& d, const OpscModelSpec& m, OpscWindows w, int16_t* cfg,

@@ -107,6 +107,21 @@ class DevicePlanner:
                                             self.menu.data_ptr(), shard, n_shards,
                                             self.key.data_ptr(), self._s()), "compose_argmin")
 
+    def certify(self, band_ulps=abi.CERTIFY_BAND_ULPS):
+        """Opt-in summation-order certificate (brute force, after compose):
+        ORs W_ORDER_SENSITIVE into status where argmin over lat <= slo - band
+        and argmin over lat <= slo + band differ (opsc_certify_order)."""
+        if self.mode != abi.MODE_ORACLE:
+            return
+        if getattr(self, "_cert_ws", None) is None:
+            nb = int(self.L.opsc_certify_workspace(self.W))
+            self._cert_ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=self.dev)
+        r = _native.ref
+        self._ck(self.L.opsc_certify_order(r(self.problem.table), r(self.grid), self.win,
+                                           self.menu.data_ptr(), float(band_ulps),
+                                           self._cert_ws.data_ptr(), self._cert_ws.numel(),
+                                           self.out_t["status"].data_ptr(), self._s()), "certify_order")
+
     def finish(self):
         r, s = _native.ref, self._s()
         if self.mode == abi.MODE_ORACLE:
@@ -170,10 +185,11 @@ class DevicePlanner:
         self._model_grid_into(self.model, self.out_t["cfg"], self.out_t["feasible"],
                               self.out_t["status"], self._s())
 
-    def step(self, shard=0, n_shards=1, allreduce=None, compose_events=None, merge=None):
+    def step(self, shard=0, n_shards=1, allreduce=None, compose_events=None, merge=None, certify=False):
         """One pass of the hot path over the resident batch of windows.
         `merge` (dist.PeerMerge): the multi-GPU merge fused into the compose
-        kernel over peer memory instead of `allreduce` after it."""
+        kernel over peer memory instead of `allreduce` after it. `certify`:
+        also run the summation-order certificate (single GPU)."""
         if merge is not None and self.mode == abi.MODE_ORACLE:
             return merge.step(self, compose_events)
         self._init()
@@ -186,6 +202,8 @@ class DevicePlanner:
                 compose_events[1].record()
             if allreduce is not None:
                 allreduce(self.key)
+            if certify:
+                self.certify()
         elif self.mode == abi.MODE_OPERATOR:
             self.operator()
         else:

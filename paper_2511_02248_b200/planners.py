@@ -162,7 +162,8 @@ def _single_io(point, params, n_ops, tcap):
     return win, out
 
 
-def _run(mode, problem, points, params, bounds, fleet, energy, types, err, trace_cap=4096, single=False):
+def _run(mode, problem, points, params, bounds, fleet, energy, types, err, trace_cap=4096, single=False,
+         certify=False):
     phases = {p.phase for p in points}
     for ph in sorted(phases):
         problem.require_phase(ph)
@@ -183,7 +184,7 @@ def _run(mode, problem, points, params, bounds, fleet, energy, types, err, trace
                        None if fleet is None else tuple(map(id, fleet)),
                        lambda: tables.pack_place(fleet, energy))
     arrays = _native.plan_windows_host(mode, problem, win, grid=grid, model=spec, place=place,
-                                       greedy=greedy, trace_cap=trace_cap, out=out)
+                                       greedy=greedy, trace_cap=trace_cap, out=out, certify=certify)
     return WindowDecisions(problem, points, arrays, mode, types, err, r_cap=params.r_cap)
 
 
@@ -191,13 +192,19 @@ _MODES = {"oracle": abi.MODE_ORACLE, "model": abi.MODE_MODEL, "operator": abi.MO
 
 
 def decide_windows(dag, profiles, points, params, mode="oracle", bounds=None, *,
-                   fleet=None, energy=None, guards=False, types=model, err=errors):
+                   fleet=None, energy=None, guards=False, types=model, err=errors, certify=False):
     """Batched planning over many WorkloadPoints.
 
     `params` is an AutoscaleParams or a {phase: AutoscaleParams} map (prefill
     SLO = TTFT, decode SLO = TBT; cli.py:114-120). Points with qps <= 0 are
     idle windows: they get no plan (cli.py:138-144). Returns a list of
     WindowDecisions groups aligned with `points` via .index.
+
+    certify=True (brute force only) also runs the summation-order
+    certificate: WindowDecisions.order_sensitive(k) is True for windows whose
+    decision could differ under the reference's frozenset-ordered leaf sum
+    (autoscaler.py:792-796), i.e. where some candidate that could win lies
+    within 64 ulps of the SLO. The decisions themselves are unchanged.
     """
     m = _MODES[mode] if isinstance(mode, str) else mode
     bounds = bounds if (bounds is not None or m != abi.MODE_ORACLE) else types.BruteForceBounds()
@@ -213,7 +220,8 @@ def decide_windows(dag, profiles, points, params, mode="oracle", bounds=None, *,
         prm = by_phase[ph] if by_phase is not None else params
         if guards and m == abi.MODE_ORACLE:
             _guard(problem, prm, bounds, MAX_ENUMERATION, err)
-        dec = _run(m, problem, [points[i] for i in idx], prm, bounds, fleet, energy, types, err)
+        dec = _run(m, problem, [points[i] for i in idx], prm, bounds, fleet, energy, types, err,
+                   certify=certify)
         dec.index = idx
         out.append(dec)
     return out

@@ -126,6 +126,12 @@ class WindowDecisions:
     def status(self, i):
         return int(self.arrays.status[i])
 
+    def order_sensitive(self, i):
+        """True if the opt-in certificate (decide_windows(certify=True)) found
+        that window i's brute-force decision could depend on the reference's
+        leaf summation order (OPSC_W_ORDER_SENSITIVE)."""
+        return bool(self.arrays.status[i] & abi.W_ORDER_SENSITIVE)
+
     def plan(self, i):
         a, n, ids, T = self.arrays, self.problem.n_ops, self.problem.ids, self.types
         st = int(a.status[i])
