@@ -4,6 +4,7 @@
 // The host-buffer path owns a per-context stream and device workspace, so
 // concurrent callers (runner.sweep's threads, runner.py:237-240) each use
 // their own context and never share mutable state.
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -126,6 +127,7 @@ struct OpscContext {
   };
   Graph graphs[8];
   std::vector<unsigned char> seen[8];  // signatures met once (captured on the second call)
+  std::vector<unsigned char> sig;      // this call's signature (scratch)
   unsigned long long tick = 0;
 };
 
@@ -793,7 +795,7 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
   cudaGraphExec_t exec = nullptr;
   int graph_launches = 0;
   if (stage && !getenv("OPSC_NO_GRAPH")) {
-    std::vector<unsigned char> sig;
+    std::vector<unsigned char>& sig = c->sig;  // reused: no allocation per call
     plan_signature(sig, c, certify ? flags : mode, W, tcap, ndev, dag, grid, model, greedy, place);
     c->tick++;
     OpscContext::Graph* hit = nullptr;
@@ -846,7 +848,24 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
     CK(enqueue());
   }
   CK(cudaEventRecord(c->ev1, s));
-  CK(cudaStreamSynchronize(s));
+  // the caller waits for this call anyway: poll the completion event for up
+  // to ~0.5 ms (per-point calls finish inside that; a blocking synchronize
+  // adds its yield / wake-up latency to every call), then block
+  {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      e = cudaEventQuery(c->ev1);
+      if (e == cudaSuccess) break;
+      if (e != cudaErrorNotReady) {
+        cudaGetLastError();
+        return OPSC_ERR_CUDA;
+      }
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(500)) {
+        CK(cudaEventSynchronize(c->ev1));
+        break;
+      }
+    }
+  }
   if (stage)
     for (const Arr& a : outs)
       if (a.host && a.bytes) memcpy(a.host, c->h_stage + a.at, a.bytes);

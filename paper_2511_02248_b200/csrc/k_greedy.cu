@@ -13,6 +13,9 @@
 //     lexicographic tie-break) for the bottleneck of the next step; the
 //     prune pass is sequential as in :562-589.
 // The uniform reseed uses K3's model-level result for the same window.
+// The step functions are __noinline__: inlined at every call site the kernel
+// was 32k instructions (512 KB of SASS) and a single-window run spent ~22% of
+// its warp samples waiting on instruction fetch (ncu stall "no_inst").
 #include "opsc_common.cuh"
 
 namespace opsc {
@@ -50,30 +53,62 @@ struct GShared {
   int pd[OPSC_MAX_OPS][OPSC_MAX_P];
   uint32_t st;
   int trace_len;
+  int bneck;                     // bottleneck of the current path (set with the path)
+  double cpv[OPSC_MAX_OPS];      // critical-path DP values of the current weights (thread 0's walk)
+  int8_t cppar[OPSC_MAX_OPS];
+  int8_t tpos[OPSC_MAX_OPS];     // topological position of every op
+  int cpv_ok;                    // cpv matches wt and every weight is >= 0 (trial_latency prefix)
+  int chain;                     // the DAG is one path (each op feeds the next in topological order)
 };
 
-// critical path with the reference's lexicographic path tie-break (opgraph.py:223-244)
-__device__ __forceinline__ double crit_path(const OpscDag& d, const double* wt, int8_t* path_out) {
-  return critical_path_lex(d, wt, path_out);
-}
 
-// latency of the current plan with op `v`'s weight replaced (value only)
-__device__ double trial_latency(const OpscDag& d, const double* wt, int v, double wv) {
+// latency of the current plan with op `v`'s weight replaced (value only).
+// prefix: S.cpv holds the DP values of the current weights and every weight
+// is >= 0 (S.cpv_ok) -- then the values of v's topological predecessors in
+// the order are unchanged and the DP restarts at v (for weights >= 0 the
+// critical-path DP and this one, which clamps dp_in at 0, agree bit for bit).
+__device__ double trial_latency(const GShared& S, const OpscDag& d, const double* wt, int v, double wv,
+                                bool prefix) {
+  if (prefix && S.chain) {  // a chain: one running value from v's predecessor on
+    const int n = d.n_ops, i0 = S.tpos[v];
+    double t = i0 > 0 ? S.cpv[d.topo[i0 - 1]] : 0.0;  // >= 0 (all weights >= 0)
+    t = t + wv;
+    for (int i = i0 + 1; i < n; ++i) t = t + wt[d.topo[i]];
+    return fmax(0.0, t);
+  }
   double val[OPSC_MAX_OPS];
   double top = 0.0;
-  for (int i = 0; i < d.n_ops; ++i) {
+  int i0 = 0;
+  if (prefix) {
+    i0 = S.tpos[v];
+    for (int i = 0; i < i0; ++i) {
+      const int u = d.topo[i];
+      if (d.sink_mask >> u & 1u) top = fmax(top, S.cpv[u]);
+    }
+  }
+  for (int i = i0; i < d.n_ops; ++i) {
     const int u = d.topo[i];
     double in = 0.0;
     uint32_t pm = d.pred_mask[u];
     while (pm) {
       const int p = __ffs(pm) - 1;
       pm &= pm - 1;
-      in = fmax(in, val[p]);
+      in = fmax(in, S.tpos[p] < i0 ? S.cpv[p] : val[p]);
     }
     val[u] = in + (u == v ? wv : wt[u]);
     if (d.sink_mask >> u & 1u) top = fmax(top, val[u]);
   }
   return top;
+}
+
+// the DAG is a single path: topo[0] a source, every later op fed by exactly
+// the previous one, the last op the only sink
+__device__ bool is_chain(const OpscDag& d) {
+  const int n = d.n_ops;
+  if (d.pred_mask[d.topo[0]] != 0u || d.sink_mask != (1u << d.topo[n - 1])) return false;
+  for (int i = 1; i < n; ++i)
+    if (d.pred_mask[d.topo[i]] != (1u << d.topo[i - 1])) return false;
+  return true;
 }
 
 __device__ int objective(const GShared& S, int n) {
@@ -89,6 +124,30 @@ __device__ int bottleneck(const GShared& S, int n) {
     if (best < 0 || S.soj[v] > S.soj[best] || (S.soj[v] == S.soj[best] && v < best)) best = v;
   }
   return best;
+}
+
+// thread 0: critical path of the current weights with the reference's
+// lexicographic path tie-break (opgraph.py:223-244), DP scratch in shared
+// memory, and the bottleneck the next step starts from (:306-331) -- so the
+// steps need no serial section of their own before evaluating moves
+__device__ __forceinline__ void set_path(GShared& S, const OpscDag& d) {
+  if (S.chain) {  // one source-sink path: val[v] = val[prev] + w[v] in order, the path is every op
+    const int n = d.n_ops;
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const int u = d.topo[i];
+      acc = i == 0 ? S.wt[u] : acc + S.wt[u];
+      S.cpv[u] = acc;
+      S.path[i] = (int8_t)u;
+    }
+    S.lat = acc;
+  } else {
+    S.lat = critical_path_lex_body(d, S.wt, S.path, S.cpv, S.cppar);
+  }
+  S.bneck = bottleneck(S, d.n_ops);
+  bool nonneg = true;
+  for (int v = 0; v < d.n_ops; ++v) nonneg &= S.wt[v] >= 0.0;
+  S.cpv_ok = nonneg;
 }
 
 __device__ void push_trace(GShared& S, const OpscDecisions& out, int w, int action, int op, int r,
@@ -108,7 +167,7 @@ __device__ void push_trace(GShared& S, const OpscDecisions& out, int w, int acti
 }
 
 // full evaluation of the current configs (all threads; ends synchronised)
-__device__ void eval_full(GShared& S, const OpscDag& d, double qps, int L, int ph) {
+__device__ __noinline__ void eval_full(GShared& S, const OpscDag& d, double qps, int L, int ph) {
   __shared__ int s_unstable;
   if (threadIdx.x == 0) s_unstable = 0;
   __syncthreads();
@@ -124,10 +183,12 @@ __device__ void eval_full(GShared& S, const OpscDag& d, double qps, int L, int p
   if (threadIdx.x == 0) {
     S.stable = !s_unstable;
     if (S.stable) {
-      S.lat = crit_path(d, S.wt, S.path);
+      set_path(S, d);
     } else {
       S.lat = OPSC_INF;
       for (int i = 0; i < d.n_ops; ++i) S.path[i] = -1;
+      S.bneck = -1;
+      S.cpv_ok = 0;
     }
   }
   __syncthreads();
@@ -137,7 +198,7 @@ __device__ void eval_full(GShared& S, const OpscDag& d, double qps, int L, int p
 // count r_new (move m = (B = b_lo + m / np, P = pd[m % np]), all distinct P)
 // into the scratch slots m - m0 (all threads; ends synchronised). Returns
 // the size of the whole set; sets larger than kMaxMoves run in chunks.
-__device__ int eval_moves(GShared& S, const GreedyArgs& a, int op, int r_new, int b_lo, double qps, int L,
+__device__ __noinline__ int eval_moves(GShared& S, const GreedyArgs& a, int op, int r_new, int b_lo, double qps, int L,
                           int ph, int m0) {
   const int np = S.np_d[op];
   const int nb = a.s.b_max[op] - b_lo + 1;
@@ -152,7 +213,7 @@ __device__ int eval_moves(GShared& S, const GreedyArgs& a, int op, int r_new, in
     if (o.stable) {
       S.m_wt[i] = weight(o, a.d.layer_count[op]);
       S.m_soj[i] = o.wait + o.service;
-      S.m_lat[i] = trial_latency(a.d, S.wt, op, S.m_wt[i]);
+      S.m_lat[i] = trial_latency(S, a.d, S.wt, op, S.m_wt[i], S.cpv_ok);
     }
     if (st) atomicOr(&S.st, st);
   }
@@ -161,33 +222,46 @@ __device__ int eval_moves(GShared& S, const GreedyArgs& a, int op, int r_new, in
 }
 
 // A move's selection key (k0, k1, k2, B, P) for one of the reference's
-// criteria; m < 0 = no candidate. Keys end in the move's unique (B, P), so
-// the lexicographic minimum is a total order: the block reduction below
-// picks exactly the move the reference's in-order scan picks.
+// criteria. Keys end in the move's unique (B, P), so the lexicographic
+// minimum is a total order: the block reduction below picks exactly the move
+// the reference's in-order scan picks. (k2, B, P) travel packed in one u64
+// (k2 >= 0, B and P < 2^16); "no candidate" is (+inf, +inf, ~0) -- k0 and
+// k1 of a real move are never +inf (objectives, -(dlat/dobj) and stable
+// latencies). The move index is recovered from (B, P) (move_index).
 struct PK {
   double k0, k1;
-  int k2, b, p, m;
+  unsigned long long tie;
 };
 
+__device__ __forceinline__ PK pk_none() { return PK{OPSC_INF, OPSC_INF, ~0ull}; }
+__device__ __forceinline__ PK pk_make(double k0, double k1, int k2, int b, int p) {
+  return PK{k0, k1, ((unsigned long long)(uint32_t)k2 << 32) | ((unsigned long long)b << 16) | (unsigned long long)p};
+}
+__device__ __forceinline__ bool pk_valid(const PK& x) { return x.tie != ~0ull; }
+__device__ __forceinline__ int pk_b(const PK& x) { return (int)((x.tie >> 16) & 0xffffu); }
+__device__ __forceinline__ int pk_p(const PK& x) { return (int)(x.tie & 0xffffu); }
+
+// branch-free lexicographic (k0, k1, tie) compare (NaN compares false
+// everywhere, as in the branchy form)
 __device__ __forceinline__ bool pk_less(const PK& x, const PK& y) {
-  if (x.m < 0) return false;
-  if (y.m < 0) return true;
-  if (x.k0 != y.k0) return x.k0 < y.k0;
-  if (x.k1 != y.k1) return x.k1 < y.k1;
-  if (x.k2 != y.k2) return x.k2 < y.k2;
-  if (x.b != y.b) return x.b < y.b;
-  return x.p < y.p;
+  const bool e0 = x.k0 == y.k0, e1 = x.k1 == y.k1;
+  return (x.k0 < y.k0) | (e0 & ((x.k1 < y.k1) | (e1 & (x.tie < y.tie))));
 }
 
 __device__ __forceinline__ PK pk_shfl(const PK& x, int off) {
   PK y;
   y.k0 = __shfl_xor_sync(0xffffffffu, x.k0, off);
   y.k1 = __shfl_xor_sync(0xffffffffu, x.k1, off);
-  y.k2 = __shfl_xor_sync(0xffffffffu, x.k2, off);
-  y.b = __shfl_xor_sync(0xffffffffu, x.b, off);
-  y.p = __shfl_xor_sync(0xffffffffu, x.p, off);
-  y.m = __shfl_xor_sync(0xffffffffu, x.m, off);
+  y.tie = __shfl_xor_sync(0xffffffffu, x.tie, off);
   return y;
+}
+
+// index m of move (B, P) in the move set of `op` starting at b_lo
+__device__ __forceinline__ int move_index(const GShared& S, int op, int b_lo, int b, int p) {
+  const int np = S.np_d[op];
+  int pi = 0;
+  while (pi < np - 1 && S.pd[op][pi] != p) ++pi;
+  return (b - b_lo) * np + pi;
 }
 
 // Block-wide minimum of NK keys per thread (warp shuffles, then one warp
@@ -220,7 +294,7 @@ __device__ void block_min(PK (&x)[NK]) {
 // thread 0: apply move m of `op` (new r), recompute the critical path. The
 // move's weight / sojourn come from the scratch when its chunk is the last
 // one evaluated, else they are recomputed (same predict, same bits).
-__device__ void apply_move(GShared& S, const GreedyArgs& a, int op, int m, int r_new, int b_lo, int m0, double qps,
+__device__ __noinline__ void apply_move(GShared& S, const GreedyArgs& a, int op, int m, int r_new, int b_lo, int m0, double qps,
                            int L, int ph) {
   const int np = S.np_d[op];
   S.p[op] = S.pd[op][m % np];
@@ -235,7 +309,7 @@ __device__ void apply_move(GShared& S, const GreedyArgs& a, int op, int m, int r
     S.wt[op] = weight(o, a.d.layer_count[op]);
     S.soj[op] = o.wait + o.service;
   }
-  S.lat = crit_path(a.d, S.wt, S.path);
+  set_path(S, a.d);
   S.stable = 1;
 }
 
@@ -245,11 +319,9 @@ __device__ void apply_move(GShared& S, const GreedyArgs& a, int op, int m, int r
 // move reaching slo - eps (objective, latency, B, P), then (loop only) the
 // cheapest reaching slo, else the most efficient improving move
 // (-(dlat / dobj), latency, objective, B, P) -- each a block-wide minimum.
-__device__ void upscale_step(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps,
+__device__ __noinline__ void upscale_step(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps,
                              int L, int ph, double slo, double eps, bool headroom) {
-  if (threadIdx.x == 0) S.op = bottleneck(S, a.d.n_ops);
-  __syncthreads();
-  const int op = S.op;
+  const int op = S.bneck;  // set with the current path (every writer ends synchronised)
   const int cur_p = S.p[op], cur_r = S.r[op];
   if (cur_r + 1 > a.s.r_cap) {
     __syncthreads();
@@ -261,7 +333,7 @@ __device__ void upscale_step(GShared& S, const GreedyArgs& a, const OpscDecision
   const int base = objective(S, a.d.n_ops);
   const double target = slo - eps, cur_lat = S.lat;
   PK k[3];  // ach, ach2, imp
-  for (int i = 0; i < 3; ++i) k[i].m = -1;
+  for (int i = 0; i < 3; ++i) k[i] = pk_none();
   int M = 0, m0 = 0;
   do {
     if (m0 > 0) __syncthreads();  // previous chunk's scratch fully read
@@ -271,14 +343,14 @@ __device__ void upscale_step(GShared& S, const GreedyArgs& a, const OpscDecision
     const int b = 1 + m / np, p = S.pd[op][m % np];
     const double lat = S.m_lat[m - m0];
     const int obj = base - cur_p * cur_r + p * (cur_r + 1);
-    const PK reach = {(double)obj, lat, 0, b, p, m};
+    const PK reach = pk_make((double)obj, lat, 0, b, p);
     if (lat <= target && pk_less(reach, k[0])) k[0] = reach;
     if (!headroom && lat <= slo && pk_less(reach, k[1])) k[1] = reach;
     const bool improving = headroom ? lat < cur_lat - 1e-9 * slo : lat < cur_lat;
     if (improving) {
       const int dobj = obj - base;
       const double cost = dobj >= 1 ? (double)dobj : 1e-9;
-      const PK eff = {-((cur_lat - lat) / cost), lat, headroom ? 0 : obj, b, p, m};
+      const PK eff = pk_make(-((cur_lat - lat) / cost), lat, headroom ? 0 : obj, b, p);
       if (pk_less(eff, k[2])) k[2] = eff;
     }
   }
@@ -287,7 +359,8 @@ __device__ void upscale_step(GShared& S, const GreedyArgs& a, const OpscDecision
   m0 -= kMaxMoves;  // the chunk still in the scratch
   block_min<3>(k);
   if (threadIdx.x == 0) {
-    const int m = k[0].m >= 0 ? k[0].m : (!headroom && k[1].m >= 0) ? k[1].m : k[2].m;
+    const PK& pick = pk_valid(k[0]) ? k[0] : (!headroom && pk_valid(k[1])) ? k[1] : k[2];
+    const int m = pk_valid(pick) ? move_index(S, op, 1, pk_b(pick), pk_p(pick)) : -1;
     S.applied = m >= 0;
     if (m >= 0) {
       apply_move(S, a, op, m, cur_r + 1, 1, m0, qps, L, ph);
@@ -300,11 +373,9 @@ __device__ void upscale_step(GShared& S, const GreedyArgs& a, const OpscDecision
 
 // Downscale (autoscaler.py:456-486): the cheapest (objective, B, P) move at
 // R - 1 that stays within slo - eps and lowers the objective.
-__device__ void downscale_step(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps,
+__device__ __noinline__ void downscale_step(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps,
                                int L, int ph, double slo, double eps) {
-  if (threadIdx.x == 0) S.op = bottleneck(S, a.d.n_ops);
-  __syncthreads();
-  const int op = S.op;
+  const int op = S.bneck;  // set with the current path (every writer ends synchronised)
   const int cur_p = S.p[op], cur_r = S.r[op], cur_b = S.b[op];
   if (cur_r - 1 < 1) {
     __syncthreads();
@@ -316,7 +387,7 @@ __device__ void downscale_step(GShared& S, const GreedyArgs& a, const OpscDecisi
   const int base = objective(S, a.d.n_ops);
   const double bound = slo - eps;
   PK k[1];
-  k[0].m = -1;
+  k[0] = pk_none();
   int M = 0, m0 = 0;
   do {
     if (m0 > 0) __syncthreads();  // previous chunk's scratch fully read
@@ -326,7 +397,7 @@ __device__ void downscale_step(GShared& S, const GreedyArgs& a, const OpscDecisi
       const int b = cur_b + m / np, p = S.pd[op][m % np];
       const int obj = base - cur_p * cur_r + p * (cur_r - 1);
       if (obj >= base) continue;
-      const PK c = {(double)obj, 0.0, 0, b, p, m};
+      const PK c = pk_make((double)obj, 0.0, 0, b, p);
       if (pk_less(c, k[0])) k[0] = c;
     }
     m0 += kMaxMoves;
@@ -334,7 +405,7 @@ __device__ void downscale_step(GShared& S, const GreedyArgs& a, const OpscDecisi
   m0 -= kMaxMoves;
   block_min<1>(k);
   if (threadIdx.x == 0) {
-    const int best = k[0].m;
+    const int best = pk_valid(k[0]) ? move_index(S, op, cur_b, pk_b(k[0]), pk_p(k[0])) : -1;
     S.applied = best >= 0;
     if (best >= 0) {
       apply_move(S, a, op, best, cur_r - 1, cur_b, m0, qps, L, ph);
@@ -345,7 +416,7 @@ __device__ void downscale_step(GShared& S, const GreedyArgs& a, const OpscDecisi
   __syncthreads();
 }
 
-__device__ void greedy_loop(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps,
+__device__ __noinline__ void greedy_loop(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps,
                             int L, int ph, double slo, double eps) {
   for (int it = 0; it < a.s.max_iterations; ++it) {
     const double lat = S.lat;
@@ -366,7 +437,7 @@ __device__ void greedy_loop(GShared& S, const GreedyArgs& a, const OpscDecisions
 // all pending trials run in parallel threads; thread 0 then sweeps in id
 // order with the cheap DP, and only accepted operators are re-predicted
 // before the next pass (the same set of evaluations the reference makes).
-__device__ void prune_pass(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps, int L,
+__device__ __noinline__ void prune_pass(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps, int L,
                            int ph, double target) {
   __shared__ double t_wt[OPSC_MAX_OPS], t_soj[OPSC_MAX_OPS];
   __shared__ uint8_t t_ok[OPSC_MAX_OPS], t_need[OPSC_MAX_OPS];
@@ -390,7 +461,7 @@ __device__ void prune_pass(GShared& S, const GreedyArgs& a, const OpscDecisions&
       changed = 0;
       for (int v = 0; v < d.n_ops; ++v) {
         if (S.r[v] <= 1 || !t_ok[v]) continue;
-        const double lat = trial_latency(d, S.wt, v, t_wt[v]);
+        const double lat = trial_latency(S, d, S.wt, v, t_wt[v], false);  // S.wt moves inside the pass
         if (!(lat <= target)) continue;
         S.r[v] -= 1;
         S.wt[v] = t_wt[v];
@@ -399,11 +470,12 @@ __device__ void prune_pass(GShared& S, const GreedyArgs& a, const OpscDecisions&
         // (max over predecessors commutes with the monotone + w); the path
         // itself is only needed after the pass
         S.lat = lat;
+        S.cpv_ok = 0;
         push_trace(S, out, w, OPSC_ACT_PRUNE, v, S.r[v], S.b[v], S.p[v], S.lat, objective(S, d.n_ops));
         t_need[v] = 1;
         changed = 1;
       }
-      if (!changed) S.lat = crit_path(d, S.wt, S.path);  // path (and the same value) for what follows
+      if (!changed) set_path(S, d);  // path (and the same value) for what follows
     }
     __syncthreads();
     if (!changed) break;
@@ -463,6 +535,10 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
       S.trace_len = g.trace_len;
       S.st = g.st;
       S.flag = g.ok;
+      S.bneck = bottleneck(S, n);
+      S.cpv_ok = 0;
+      for (int i = 0; i < n; ++i) S.tpos[d.topo[i]] = (int8_t)i;
+      S.chain = is_chain(d);
     }
     __syncthreads();
     if (!S.flag) return;
@@ -474,19 +550,22 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
   }
   for (int i = threadIdx.x; i < n * 3; i += blockDim.x) out.cfg[(size_t)w * n * 3 + i] = 0;
   if (!(qps > 0.0)) return;
+  for (int v = threadIdx.x; v < n; v += blockDim.x) {  // distinct P per operator, one thread each
+    int k = 0;
+    for (int i = 0; i < a.s.n_p[v]; ++i) {
+      bool dup = false;
+      for (int j = 0; j < k; ++j) dup |= S.pd[v][j] == a.s.p_vals[v][i];
+      if (!dup) S.pd[v][k++] = a.s.p_vals[v][i];
+    }
+    S.np_d[v] = k;
+    S.chosen[v] = 0;
+    S.tpos[d.topo[v]] = (int8_t)v;
+  }
   if (threadIdx.x == 0) {
     S.st = 0;
     S.trace_len = 0;
-    for (int v = 0; v < n; ++v) {
-      int k = 0;
-      for (int i = 0; i < a.s.n_p[v]; ++i) {
-        bool dup = false;
-        for (int j = 0; j < k; ++j) dup |= S.pd[v][j] == a.s.p_vals[v][i];
-        if (!dup) S.pd[v][k++] = a.s.p_vals[v][i];
-      }
-      S.np_d[v] = k;
-      S.chosen[v] = 0;
-    }
+    S.cpv_ok = 0;
+    S.chain = is_chain(d);
   }
   __syncthreads();
 
@@ -614,6 +693,8 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
         }
         S.lat = keep_lat;
         S.stable = 1;
+        S.bneck = bottleneck(S, n);
+        S.cpv_ok = 0;  // cpv belongs to the discarded reseeded plan
       }
       __syncthreads();
     }

@@ -22,13 +22,21 @@ namespace opsc {
 
 constexpr int kPlaceThreads = 128;
 constexpr int kMaxDevProbe = 128;  // device probes per chunk held in smem
+constexpr size_t kPlaceSmemMax = 200 * 1024;  // static PShared + per-window workspace
 
 struct PlaceArgs {
   OpscDag d;
   OpscPlaceShared f;
 };
 
-struct PWork {  // per-window global workspace
+struct PWork {  // per-window workspace (shared memory when it fits, else global)
+  int32_t* a_op;    // operator of assignment i
+  int32_t* a_dev;   // device of assignment i
+  double* a_gmax;   // max demand over the members of i's group on i's device
+  double* dev_lf;   // standing load of each device: the PySum state (f, c, started) of its
+  double* dev_lc;   //   group maxima in first-occurrence order, kept current at every push
+  int32_t* dev_ls;
+  uint32_t* dev_mask;  // operators with a member on each device
   int32_t* a_group;
   int32_t* a_next;
   double* a_dem;
@@ -45,7 +53,8 @@ struct PWork {  // per-window global workspace
 __host__ __device__ inline size_t pw_bytes(int A, int D, int n) {
   (void)n;
   // rounded to 16 B so every window's double arrays stay 8-byte aligned
-  const size_t b = (size_t)A * (4 + 4 + 8 + 8 + 8) + (size_t)D * (4 + 4 + 4 + 8 + 8) + (size_t)A * 4 + 64;
+  const size_t b = (size_t)A * (4 + 4 + 4 + 4 + 8 + 8 + 8 + 8) + (size_t)D * (4 + 4 + 4 + 8 + 8 + 8 + 8 + 4 + 4) +
+                   (size_t)A * 4 + 64;
   return (b + 15) & ~(size_t)15;
 }
 
@@ -57,7 +66,14 @@ __device__ PWork carve(unsigned char* base, int A, int D) {
   p.a_fac = dp; dp += A;
   p.dev_mem_f = dp; dp += D;
   p.dev_mem_c = dp; dp += D;
+  p.a_gmax = dp; dp += A;
+  p.dev_lf = dp; dp += D;
+  p.dev_lc = dp; dp += D;
   int32_t* ip = (int32_t*)dp;
+  p.dev_ls = ip; ip += D;
+  p.dev_mask = (uint32_t*)ip; ip += D;
+  p.a_op = ip; ip += A;
+  p.a_dev = ip; ip += A;
   p.a_group = ip; ip += A;
   p.a_next = ip; ip += A;
   p.dev_head = ip; ip += D;
@@ -85,14 +101,19 @@ __device__ __forceinline__ double psum_value(double f, double c, bool started) {
   return (c != 0.0 && isfinite(c)) ? f + c : f;
 }
 
-// standing load of device `dev` (+ optional extra member of group xg, demand xd):
-// Neumaier sum of group maxima in insertion order; returns total, and the
-// group max of `query_group` in *qmax
-__device__ double dev_load(const PWork& P, int dev, int xg, double xd, int query_group, double* qmax) {
-  // groups of one device are few; scan members for first occurrences
+// interference factor of member i of `dev` with an optional extra (group xg, demand xd)
+__device__ double member_factor(const PWork& P, const OpscPlaceShared& f, int dev, int i, int xg, double xd,
+                                double total) {
+  (void)dev;
+  double gm = P.a_gmax[i];  // = the scan over dev's members of i's group, kept by push
+  if (xg == P.a_group[i]) gm = gm >= xd ? gm : xd;
+  return interference(f, total - gm, P.a_dem[i]);
+}
+
+// standing load of `dev` as the PySum state dev_load builds (no extra member)
+__device__ PySum dev_load_sum(const PWork& P, int dev) {
   PySum t;
   t.reset();
-  double qm = 0.0;
   for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) {
     const int g = P.a_group[i];
     bool first = true;
@@ -101,31 +122,17 @@ __device__ double dev_load(const PWork& P, int dev, int xg, double xd, int query
     double m = 0.0;
     for (int j = i; j >= 0; j = P.a_next[j])
       if (P.a_group[j] == g) m = m >= P.a_dem[j] ? m : P.a_dem[j];
-    if (g == xg) m = m >= xd ? m : xd;
     t.add(m);
-    if (g == query_group) qm = m;
   }
-  if (xg >= 0) {  // the extra's group is new (extras own their group)
-    bool seen = false;
-    for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) seen |= P.a_group[i] == xg;
-    if (!seen) {
-      const double m = 0.0 >= xd ? 0.0 : xd;
-      t.add(m);
-      if (xg == query_group) qm = m;
-    }
-  }
-  if (qmax) *qmax = qm;
-  return t.value();
+  return t;
 }
 
-// interference factor of member i of `dev` with an optional extra (group xg, demand xd)
-__device__ double member_factor(const PWork& P, const OpscPlaceShared& f, int dev, int i, int xg, double xd,
-                                double total) {
-  double gm = 0.0;
-  for (int j = P.dev_head[dev]; j >= 0; j = P.a_next[j])
-    if (P.a_group[j] == P.a_group[i]) gm = gm >= P.a_dem[j] ? gm : P.a_dem[j];
-  if (xg == P.a_group[i]) gm = gm >= xd ? gm : xd;
-  return interference(f, total - gm, P.a_dem[i]);
+__device__ __forceinline__ PySum cached_load(const PWork& P, int dev) {
+  PySum t;
+  t.f = P.dev_lf[dev];
+  t.c = P.dev_lc[dev];
+  t.started = P.dev_ls[dev] != 0;
+  return t;
 }
 
 struct OpAdj {
@@ -194,6 +201,7 @@ struct PShared {
   int used, na, err, best;
 };
 
+template <bool SMEM>
 __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_constant__ PlaceArgs a,
                                                               const __grid_constant__ OpscWindows win,
                                                               const int16_t* __restrict__ cfg,
@@ -202,6 +210,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
                                                               const __grid_constant__ OpscPlacement out,
                                                               unsigned char* __restrict__ ws) {
   __shared__ PShared S;
+  extern __shared__ __align__(16) unsigned char pw_smem[];
   const OpscDag& d = a.d;
   const OpscPlaceShared& f = a.f;
   const int n = d.n_ops;
@@ -216,8 +225,11 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
   const int L = win.seq_len[w], ph = win.phase[w];
   const double slo = (f.flags & OPSC_PLACE_WINDOW_SLO) ? win.slo[w] : f.slo;
   const bool probe = !(f.flags & OPSC_PLACE_DEFAULT_STREAM);
-  PWork P = carve(ws + (size_t)w * pw_bytes(A, D, n), A, D);
-  const int32_t* adev = out.a_device + (size_t)w * A;
+  // the window's assignment lists / device tables are walked by every probe:
+  // in shared memory when they fit (smem_ws), else in its global slice
+  // (SMEM: a compile-time choice, so the walks compile to shared-memory loads)
+  PWork P = carve(SMEM ? pw_smem : ws + (size_t)w * pw_bytes(A, D, n), A, D);
+  const int32_t* adev = P.a_dev;
   if (threadIdx.x == 0) {
     S.rep_off[0] = 0;
     for (int v = 0; v < n; ++v) {
@@ -248,6 +260,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
   for (int i = threadIdx.x; i < D; i += blockDim.x) {
     P.dev_head[i] = -1; P.dev_tail[i] = -1; P.dev_cnt[i] = 0;
     P.dev_mem_f[i] = 0.0; P.dev_mem_c[i] = 0.0;
+    P.dev_lf[i] = 0.0; P.dev_lc[i] = 0.0; P.dev_ls[i] = 0; P.dev_mask[i] = 0u;
   }
   __syncthreads();
 
@@ -275,7 +288,21 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
     }
     P.dev_cnt[dev]++;
     P.rep[S.rep_off[v] + k - 1] = i;
+    P.dev_mask[dev] |= 1u << v;
+    // group maxima of the new member's group on this device (the scan
+    // member_factor made per call) and the device's standing-load sum
+    double gm = 0.0;
+    for (int j = P.dev_head[dev]; j >= 0; j = P.a_next[j])
+      if (P.a_group[j] == group) gm = gm >= P.a_dem[j] ? gm : P.a_dem[j];
+    for (int j = P.dev_head[dev]; j >= 0; j = P.a_next[j])
+      if (P.a_group[j] == group) P.a_gmax[j] = gm;
+    const PySum ls = dev_load_sum(P, dev);
+    P.dev_lf[dev] = ls.f;
+    P.dev_lc[dev] = ls.c;
+    P.dev_ls[dev] = ls.started ? 1 : 0;
     const size_t o = (size_t)w * A + i;
+    P.a_op[i] = v;
+    P.a_dev[i] = dev;
     out.a_op[o] = (int8_t)v;
     out.a_replica[o] = (int16_t)k;
     out.a_device[o] = dev;
@@ -283,7 +310,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
   };
   auto dev_mem = [&](int dev) { return psum_value(P.dev_mem_f[dev], P.dev_mem_c[dev], P.dev_cnt[dev] > 0); };
   auto refresh_factors = [&](int dev) {
-    const double total = dev_load(P, dev, -1, 0.0, -1, nullptr);
+    const double total = cached_load(P, dev).value();
     for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) P.a_fac[i] = member_factor(P, f, dev, i, -1, 0.0, total);
   };
 
@@ -363,13 +390,17 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
         const int dev = c0 + dj;
         const double mu = dev_mem(dev);
         bool ok = !(mu + mem > f.mem_cap[dev]);
-        const double load = dev_load(P, dev, -1, 0.0, -1, nullptr);
+        // standing load, and with the tentative replica appended: extras own a
+        // fresh group (groups count up per extra replica), so dev_load with the
+        // extra is the device's cached sum plus one more term max(0, demand)
+        const PySum ls = cached_load(P, dev);
+        const double load = ls.value();
         ok = ok && !(load + demand > f.max_sm_load);
-        double xg_max = 0.0;
-        const double total = dev_load(P, dev, group, demand, group, &xg_max);
-        uint32_t mask = 0;
-        for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) mask |= 1u << out.a_op[(size_t)w * A + i];
-        S.on_dev[dj] = mask | (1u << v);
+        const double xg_max = 0.0 >= demand ? 0.0 : demand;
+        PySum lt = ls;
+        lt.add(xg_max);
+        const double total = lt.value();
+        S.on_dev[dj] = P.dev_mask[dev] | (1u << v);
         S.dev_total[dj] = total;
         S.dev_load0[dj] = load;
         S.dev_xf[dj] = interference(f, total - xg_max, demand);
@@ -435,8 +466,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
       // refresh the cached figures of ops with a replica on the chosen device
       {
         const int dev = S.best;
-        uint32_t mask = 0;
-        for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) mask |= 1u << out.a_op[(size_t)w * A + i];
+        const uint32_t mask = P.dev_mask[dev];
         for (int u = threadIdx.x; u < n; u += blockDim.x) {
           if (!(mask >> u & 1u)) continue;
           const OpAdj o = adjust_op(d, f, P, S.rep_off, adev, u, S.p[u], S.r[u], S.b[u], S.T[u], S.comm[u], qps, -1,
@@ -462,18 +492,18 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
     double* de = out.d_energy + (size_t)w * D;
     for (int dev = 0; dev < S.used; ++dev) {
       out.d_mem[(size_t)w * D + dev] = dev_mem(dev);
-      out.d_sm[(size_t)w * D + dev] = dev_load(P, dev, -1, 0.0, -1, nullptr);
+      out.d_sm[(size_t)w * D + dev] = cached_load(P, dev).value();
       de[dev] = 0.0;
     }
     for (int i = 0; i < S.na; ++i) {
       const size_t o = (size_t)w * A + i;
-      const int u = out.a_op[o];
+      const int u = P.a_op[i];
       out.a_latency[o] = S.T[u] * P.a_fac[i];
       memsum.add(P.a_mem[i]);
       const double layers = (double)d.layer_count[u];
       double sh = ((f.alpha * (double)S.p[u]) * (S.cur_wait[u] + S.cur_teff[u])) * layers;
       sh += ((f.beta * S.cur_teff[u]) * layers) / (double)S.r[u];
-      de[out.a_device[o]] += sh;
+      de[P.a_dev[i]] += sh;
     }
     out.memory[w] = memsum.value();
     double total = 0.0;
@@ -501,7 +531,24 @@ cudaError_t launch_place_shared(const OpscDag& d, const OpscPlaceShared& f, Opsc
   PlaceArgs a;
   a.d = d;
   a.f = f;
-  place_kernel<<<w.n, kPlaceThreads, 0, s>>>(a, w, cfg, feas, config_order, out, (unsigned char*)ws);
+  const size_t pw = pw_bytes(out.cap_assign, out.cap_dev, d.n_ops);
+  const bool smem_ws = pw + sizeof(PShared) + 1024 <= kPlaceSmemMax;
+  const size_t dyn = smem_ws ? pw : 0;
+  // static PShared + dynamic workspace may pass the 48 KB default: raise the
+  // kernel's dynamic limit (once per size increase, per device)
+  static int set_dyn[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dyn > 0 && dev < 64 && (int)dyn > set_dyn[dev]) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(place_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return e;
+    set_dyn[dev] = (int)dyn;
+  }
+  if (smem_ws)
+    place_kernel<true><<<w.n, kPlaceThreads, dyn, s>>>(a, w, cfg, feas, config_order, out, (unsigned char*)ws);
+  else
+    place_kernel<false><<<w.n, kPlaceThreads, 0, s>>>(a, w, cfg, feas, config_order, out, (unsigned char*)ws);
   return cudaGetLastError();
 }
 

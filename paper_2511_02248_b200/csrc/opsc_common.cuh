@@ -127,8 +127,8 @@ __device__ __forceinline__ bool cp_seq_less(const int8_t* a, int la, const int8_
 
 // val / parent: caller scratch (shared memory in K4, where cold local
 // memory would cost an L2 round trip per access of a one-shot serial walk).
-static __device__ __noinline__ double critical_path_lex(const OpscDag& d, const double* wt, int8_t* path_out,
-                                                        double* val, int8_t* parent) {
+static __device__ __forceinline__ double critical_path_lex_body(const OpscDag& d, const double* wt, int8_t* path_out,
+                                                                double* val, int8_t* parent) {
   const int n = d.n_ops;
   for (int i = 0; i < n; ++i) {
     const int v = d.topo[i];
@@ -181,6 +181,11 @@ static __device__ __noinline__ double critical_path_lex(const OpscDag& d, const 
   for (int u = tv; u >= 0; u = parent[u]) path_out[--i] = (int8_t)u;
   for (int k = len; k < n; ++k) path_out[k] = (int8_t)-1;
   return top;
+}
+
+static __device__ __noinline__ double critical_path_lex(const OpscDag& d, const double* wt, int8_t* path_out,
+                                                        double* val, int8_t* parent) {
+  return critical_path_lex_body(d, wt, path_out, val, parent);
 }
 
 static __device__ __forceinline__ double critical_path_lex(const OpscDag& d, const double* wt, int8_t* path_out) {

@@ -91,15 +91,33 @@ _BUILDERS = {}
 
 
 def builders(T):
+    """(OperatorConfig factory, PredictedSojourn factory, ScalingPlan factory)
+    of a type namespace. OperatorConfig is a frozen value type with a small
+    domain, so its factory hands out one shared instance per (P, R, B)
+    (as immutable as the ones the reference creates per plan)."""
     b = _BUILDERS.get(id(T))
     if b is None or b[0] is not T:
         import dataclasses
         oc = T.OperatorConfig
         ps = T.PredictedSojourn
-        b = (T, _builder(oc, [f.name for f in dataclasses.fields(oc)]),
-             _builder(ps, [f.name for f in dataclasses.fields(ps)]))
+        sp = T.ScalingPlan
+        mk_oc = _builder(oc, [f.name for f in dataclasses.fields(oc)])
+        frozen = getattr(getattr(oc, "__dataclass_params__", None), "frozen", False)
+        if frozen:
+            cache = {}
+
+            def make_oc(p, r, b_, share, _c=cache, _mk=mk_oc):
+                k = (p << 42) | (r << 21) | b_
+                o = _c.get(k)
+                if o is None:
+                    o = _c[k] = _mk(p, r, b_, share)
+                return o
+        else:
+            make_oc = mk_oc
+        b = (T, make_oc, _builder(ps, [f.name for f in dataclasses.fields(ps)]),
+             _builder(sp, [f.name for f in dataclasses.fields(sp)]))
         _BUILDERS[id(T)] = b
-    return b[1], b[2]
+    return b[1], b[2], b[3]
 
 
 @dataclass
@@ -133,32 +151,27 @@ class WindowDecisions:
         return bool(self.arrays.status[i] & abi.W_ORDER_SENSITIVE)
 
     def plan(self, i):
-        a, n, ids, T = self.arrays, self.problem.n_ops, self.problem.ids, self.types
+        a, ids = self.arrays, self.problem.ids
         st = int(a.status[i])
-        nonfinite_qps(self.points[i].qps)
+        qps = self.points[i].qps
+        nonfinite_qps(qps)
         if st & abi.W_IDLE:
             return None
-        raise_for_status(st, self.mode, self.err, problem=self.problem, qps=self.points[i].qps,
-                         r_cap=self.r_cap)
-        if self.mode == abi.MODE_ORACLE:
-            order = range(n)
-        else:
-            order = self.problem.node_order
+        if st:
+            raise_for_status(st, self.mode, self.err, problem=self.problem, qps=qps, r_cap=self.r_cap)
+        order = range(self.problem.n_ops) if self.mode == abi.MODE_ORACLE else self.problem.node_order
         cfg, pred, stable = a.cfg[i].tolist(), a.pred[i].tolist(), a.stable[i].tolist()
-        OC, PS = builders(T)
+        OC, PS, SP = builders(self.types)
         configs, predicted = {}, {}
         for v in order:
             p, r, b = cfg[v]
             op = ids[v]
             configs[op] = OC(p, r, b, 100)  # sm_share: planners run at 100 (autoscaler.py:50)
-            f = pred[v]
-            predicted[op] = PS(f[0], f[1], f[2], f[3], f[4], f[5], f[6], bool(stable[v]))
+            predicted[op] = PS(*pred[v], stable[v] != 0)
         lat = float(a.latency[i])
         path = [ids[x] for x in a.path[i].tolist() if x >= 0] if math.isfinite(lat) else []
-        return T.ScalingPlan(
-            configs=configs, predicted=predicted, iteration_latency=lat,
-            critical_path=path, objective=int(a.objective[i]),
-            feasible=bool(a.feasible[i]), phase=self.points[i].phase, trace=self.trace(i))
+        return SP(configs, predicted, lat, path, int(a.objective[i]), bool(a.feasible[i]),
+                  self.points[i].phase, self.trace(i))
 
     def trace(self, i):
         """ScalingPlan.trace of the greedy planner (autoscaler.py:363, 446-454,
