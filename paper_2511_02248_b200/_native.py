@@ -15,7 +15,8 @@ from . import abi, tables
 from .errors import DeviceUnavailable, SearchSpaceTooLarge
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libopscale_b200.so")
+# OPSC_LIB_PATH: dev-only override for same-box A/B timing of two builds
+LIB_PATH = os.environ.get("OPSC_LIB_PATH") or os.path.join(HERE, "_lib", "libopscale_b200.so")
 
 # every symbol include/opscale_b200.h declares
 EXPORTS = (
