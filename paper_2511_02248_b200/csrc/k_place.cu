@@ -198,6 +198,9 @@ struct PShared {
   double dev_xf[kMaxDevProbe];      // tentative replica's factor on d
   uint8_t dev_ok[kMaxDevProbe];
   double probe_wt[kMaxDevProbe][OPSC_MAX_OPS];
+  double dev_score[kMaxDevProbe];   // weighted slack of each admissible device
+  double red_score[kPlaceThreads / 32];
+  int red_dj[kPlaceThreads / 32];
   int used, na, err, best;
 };
 
@@ -288,18 +291,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
     }
     P.dev_cnt[dev]++;
     P.rep[S.rep_off[v] + k - 1] = i;
-    P.dev_mask[dev] |= 1u << v;
-    // group maxima of the new member's group on this device (the scan
-    // member_factor made per call) and the device's standing-load sum
-    double gm = 0.0;
-    for (int j = P.dev_head[dev]; j >= 0; j = P.a_next[j])
-      if (P.a_group[j] == group) gm = gm >= P.a_dem[j] ? gm : P.a_dem[j];
-    for (int j = P.dev_head[dev]; j >= 0; j = P.a_next[j])
-      if (P.a_group[j] == group) P.a_gmax[j] = gm;
-    const PySum ls = dev_load_sum(P, dev);
-    P.dev_lf[dev] = ls.f;
-    P.dev_lc[dev] = ls.c;
-    P.dev_ls[dev] = ls.started ? 1 : 0;
+    P.dev_mask[dev] |= 1u << v;  // group maxima, load sum and factors: refresh_device
     const size_t o = (size_t)w * A + i;
     P.a_op[i] = v;
     P.a_dev[i] = dev;
@@ -309,8 +301,21 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
     out.a_share[o] = (int16_t)share;
   };
   auto dev_mem = [&](int dev) { return psum_value(P.dev_mem_f[dev], P.dev_mem_c[dev], P.dev_cnt[dev] > 0); };
-  auto refresh_factors = [&](int dev) {
-    const double total = cached_load(P, dev).value();
+  // after members were pushed to `dev`: the group maxima (the scan
+  // member_factor made per call), the standing-load sum and every member's
+  // interference factor
+  auto refresh_device = [&](int dev) {
+    for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) {
+      double gm = 0.0;
+      for (int j = P.dev_head[dev]; j >= 0; j = P.a_next[j])
+        if (P.a_group[j] == P.a_group[i]) gm = gm >= P.a_dem[j] ? gm : P.a_dem[j];
+      P.a_gmax[i] = gm;
+    }
+    const PySum ls = dev_load_sum(P, dev);
+    P.dev_lf[dev] = ls.f;
+    P.dev_lc[dev] = ls.c;
+    P.dev_ls[dev] = ls.started ? 1 : 0;
+    const double total = ls.value();
     for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) P.a_fac[i] = member_factor(P, f, dev, i, -1, 0.0, total);
   };
 
@@ -343,8 +348,9 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
         push(v, inst, target, inst - 1, 100);
       }
     }
-    for (int dev = 0; dev < S.used; ++dev) refresh_factors(dev);
   }
+  __syncthreads();
+  for (int dev = threadIdx.x; dev < S.used; dev += blockDim.x) refresh_device(dev);  // devices in parallel
   __syncthreads();
   if (S.err) {
     if (threadIdx.x == 0) out.status[w] = S.err;
@@ -420,29 +426,66 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
         S.probe_wt[dj][u] = o.stable ? o.wt : OPSC_INF;
       }
       __syncthreads();
-      // stage 3: recomputed latency must meet the SLO (placement.py:434-438)
+      // stage 3: recomputed latency must meet the SLO (placement.py:434-438),
+      // and the weighted slack score of every admissible device (:338-351)
+      bool nan_score = false;
+      int my_dj = -1;
+      double my_score = 0.0;
       for (int dj = threadIdx.x; dj < U; dj += blockDim.x) {
         if (!S.dev_ok[dj]) continue;
         bool fin = true;
         for (int u = 0; u < n; ++u) fin &= S.probe_wt[dj][u] != OPSC_INF;
         const double lat = fin ? dp_latency(d, S.probe_wt[dj]) : OPSC_INF;
-        if (lat > slo) S.dev_ok[dj] = 0;
-      }
-      __syncthreads();
-      // weighted slack (placement.py:338-351); best score, ties to the lowest id
-      if (threadIdx.x == 0) {
-        for (int dj = 0; dj < U; ++dj) {
-          if (!S.dev_ok[dj]) continue;
-          const int dev = c0 + dj;
-          const double mu = dev_mem(dev), load = S.dev_load0[dj];
-          const double ms = f.mem_cap[dev] - (mu + mem), cs = f.compute_cap[dev] - (load + demand);
-          const double mf = (0.0 >= ms ? 0.0 : ms) / f.mem_cap[dev];
-          const double cf = (0.0 >= cs ? 0.0 : cs) / f.compute_cap[dev];
-          const double score = f.slack_weight_mem * mf + f.slack_weight_compute * cf;
-          if (s_best < 0 || score > s_best_score) { s_best = dev; s_best_score = score; }
+        if (lat > slo) {
+          S.dev_ok[dj] = 0;
+          continue;
         }
+        const int dev = c0 + dj;
+        const double mu = dev_mem(dev), load = S.dev_load0[dj];
+        const double ms = f.mem_cap[dev] - (mu + mem), cs = f.compute_cap[dev] - (load + demand);
+        const double mf = (0.0 >= ms ? 0.0 : ms) / f.mem_cap[dev];
+        const double cf = (0.0 >= cs ? 0.0 : cs) / f.compute_cap[dev];
+        const double score = f.slack_weight_mem * mf + f.slack_weight_compute * cf;
+        S.dev_score[dj] = score;
+        nan_score |= score != score;
+        if (my_dj < 0 || score > my_score) { my_dj = dj; my_score = score; }  // ascending dj per thread
       }
-      __syncthreads();
+      // best score, ties to the lowest device id: a block-wide (score, -dj)
+      // maximum -- the reference's in-order scan with a strict '>' -- unless a
+      // score is NaN, where only the literal scan reproduces it (thread 0)
+      {
+        const bool any_nan = __syncthreads_or(nan_score);
+        for (int o = 16; o > 0; o >>= 1) {
+          const double os = __shfl_xor_sync(0xffffffffu, my_score, o);
+          const int od = __shfl_xor_sync(0xffffffffu, my_dj, o);
+          if (od >= 0 && (my_dj < 0 || os > my_score || (os == my_score && od < my_dj))) {
+            my_score = os;
+            my_dj = od;
+          }
+        }
+        if ((threadIdx.x & 31) == 0) {
+          S.red_score[threadIdx.x >> 5] = my_score;
+          S.red_dj[threadIdx.x >> 5] = my_dj;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          int bd = -1;
+          double bs = 0.0;
+          if (any_nan) {
+            for (int dj = 0; dj < U; ++dj)
+              if (S.dev_ok[dj] && (bd < 0 || S.dev_score[dj] > bs)) { bd = dj; bs = S.dev_score[dj]; }
+          } else {
+            for (int wi = 0; wi < kPlaceThreads / 32; ++wi) {
+              const int od = S.red_dj[wi];
+              const double os = S.red_score[wi];
+              if (od >= 0 && (bd < 0 || os > bs || (os == bs && od < bd))) { bd = od; bs = os; }
+            }
+          }
+          // across device chunks: a later chunk wins only with a strictly greater score
+          if (bd >= 0 && (s_best < 0 || bs > s_best_score)) { s_best = c0 + bd; s_best_score = bs; }
+        }
+        __syncthreads();
+      }
       }
       if (threadIdx.x == 0) {
         int best = s_best;
@@ -455,7 +498,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
           if (mem > f.mem_cap[best]) S.err = OPSC_W_INFEASIBLE_PLACEMENT;
           else push(v, k, best, group, 100);
         }
-        if (!S.err) refresh_factors(best);
+        if (!S.err) refresh_device(best);
         S.best = best;
       }
       __syncthreads();
