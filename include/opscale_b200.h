@@ -297,6 +297,18 @@ OPSC_API int opsc_model_grid(const OpscDag* dag, const OpscModelSpec* spec, Opsc
 OPSC_API int opsc_materialize(const OpscDag* dag, OpscWindows win, int32_t config_order,
                      const OpscPlaceSpec* place, OpscDecisions out, void* stream);
 
+/* Fused forms of the per-window brute-force chain (fewer launches on the
+ * W=1 decision path; same bits as the separate entry points):
+ *   opsc_menu_stability    = opsc_menu_build + opsc_stability_check
+ *                            (autoscaler.py:743-757 and its init_configs pre-check :254-294, 771);
+ *   opsc_decode_materialize = opsc_menu_fallback + opsc_decode_decisions + opsc_materialize
+ *                            with config_order 0 (autoscaler.py:828-847, 196-247, metrics.py:84-132). */
+OPSC_API int opsc_menu_stability(const OpscDag* dag, const OpscGrid* grid, OpscWindows win, double* menu_w,
+                                 uint32_t* status, void* stream);
+OPSC_API int opsc_decode_materialize(const OpscDag* dag, const OpscGrid* grid, OpscWindows win,
+                                     const int64_t* key, const double* menu_w, const OpscPlaceSpec* place,
+                                     OpscDecisions out, void* stream);
+
 /* greedy_autoscale per window (autoscaler.py:334-589): init_configs, the
  * bottleneck up/downscale loop, uniform reseed + prune, headroom restore and
  * the optional prune pass. uniform_cfg / uniform_feasible / uniform_status are

@@ -507,6 +507,19 @@ int opsc_materialize(const OpscDag* dag, OpscWindows win, int32_t config_order, 
   return from_cuda(launch_materialize(*dag, win, config_order, *place, out, (cudaStream_t)stream));
 }
 
+int opsc_menu_stability(const OpscDag* dag, const OpscGrid* grid, OpscWindows win, double* menu_w,
+                        uint32_t* status, void* stream) {
+  if (!valid_dag(dag) || !grid || !status) return OPSC_ERR_ARG;
+  return from_cuda(launch_menu_stability(*dag, *grid, win, menu_w, status, (cudaStream_t)stream));
+}
+
+int opsc_decode_materialize(const OpscDag* dag, const OpscGrid* grid, OpscWindows win, const int64_t* key,
+                            const double* menu_w, const OpscPlaceSpec* place, OpscDecisions out, void* stream) {
+  if (!valid_dag(dag) || !grid || !place || !key) return OPSC_ERR_ARG;
+  return from_cuda(launch_decode_materialize(*dag, *grid, win, (const unsigned long long*)key, menu_w, *place, out,
+                                             (cudaStream_t)stream));
+}
+
 int opsc_ctx_create(int32_t device, int32_t max_windows, OpscContext** out) {
   if (!out) return OPSC_ERR_ARG;
   *out = nullptr;
@@ -682,8 +695,16 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
   point_io(c, L);
   size_t tb = 0;
   void* tw = mode == OPSC_MODE_MODEL ? model_table_ws(c, W, *model, n, &tb) : nullptr;  // before any capture
+  // the compose launch shape (host work: level split, strides) is needed
+  // only when this call is captured or launched eagerly, not on a replay
   ComposeCfg cc;
-  if (mode == OPSC_MODE_ORACLE && (rc = compose_setup(*dag, *grid, W, 0, 1, &cc))) return rc;
+  bool cc_done = mode != OPSC_MODE_ORACLE;
+  auto ensure_cc = [&]() -> int {
+    if (cc_done) return OPSC_OK;
+    const int r = compose_setup(*dag, *grid, W, 0, 1, &cc);
+    cc_done = r == OPSC_OK;
+    return r;
+  };
   if (certify && certify_workspace(W) > c->cap_cert) {  // before any capture
     if (regrow(c->cert, certify_workspace(W)) != cudaSuccess) {
       cudaGetLastError();
@@ -723,6 +744,22 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
   if (stage)
     for (const Arr& a : ins)
       if (a.host && a.bytes) memcpy(c->h_stage + a.at, a.host, a.bytes);
+  // the per-window prologue (init_kernel: status = idle bit for qps <= 0, key
+  // = infeasible, feasible = 0, cfg zeroed) rides along with the H2D of the
+  // inputs for the staged brute-force and model-level calls: one launch less
+  const bool fold_init = stage && mode != OPSC_MODE_OPERATOR;
+  if (fold_init) {
+    unsigned char* h = c->h_stage;
+    const double* q = (const double*)(h + L.qps);
+    unsigned long long* hk = (unsigned long long*)(h + L.key);
+    uint32_t* hs = (uint32_t*)(h + L.status);
+    for (int i = 0; i < W; ++i) {
+      hk[i] = (unsigned long long)OPSC_KEY_INFEASIBLE;
+      hs[i] = q[i] > 0.0 ? 0u : OPSC_W_IDLE;
+    }
+    memset(h + L.cfg, 0, L.status - L.cfg);  // cfg and feasible
+  }
+  const size_t h2d_end = fold_init ? L.latency : L.in_end;
   OpscPlaceSpec dplace = *place;
   dplace.mem_cap = c->mem_cap;
   const OpscWindows dw = dev_windows(c, W);
@@ -735,25 +772,25 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
   } while (0)
     c->launches = 0;
     if (stage) {
-      EQ(cudaMemcpyAsync(c->io, c->h_stage, L.in_end, cudaMemcpyHostToDevice, s));
+      EQ(cudaMemcpyAsync(c->io, c->h_stage, h2d_end, cudaMemcpyHostToDevice, s));
     } else {
       for (const Arr& a : ins)
         if (a.host && a.bytes) EQ(cudaMemcpyAsync(c->io + a.at, a.host, a.bytes, cudaMemcpyHostToDevice, s));
     }
-    EQ(launch_init(W, c->qps, c->status, c->key, c->feasible, s));
-    c->launches++;
+    if (!fold_init) {
+      EQ(launch_init(W, c->qps, c->status, c->key, c->feasible, s));
+      c->launches++;
+    }
     if (mode == OPSC_MODE_ORACLE) {
-      EQ(launch_menu_build(*dag, *grid, dw, c->menu, c->status, s));
-      EQ(launch_stability(*dag, *grid, dw, c->status, s));
+      // K1 + K1b fused, K2, then fallback + decode fused into K4
+      EQ(launch_menu_stability(*dag, *grid, dw, c->menu, c->status, s));
       EQ(launch_compose(cc, *grid, W, c->menu, c->slo, c->qps, c->key, s));
       if (certify) {
         EQ(launch_certify(cc, *grid, W, c->menu, c->slo, c->qps, OPSC_CERTIFY_BAND_ULPS, c->cert, c->status, s));
         c->launches += 4;
       }
-      EQ(launch_fallback(*dag, *grid, W, c->menu, c->fb, s));
-      EQ(launch_decode(*dag, *grid, W, c->key, c->fb, c->cfg, c->feasible, c->status, s));
-      c->launches += 5;
-      EQ(launch_materialize(*dag, dw, 0, dplace, dev_decisions(c), s));
+      c->launches += 2;
+      EQ(launch_decode_materialize(*dag, *grid, dw, c->key, c->menu, dplace, dev_decisions(c), s));
     } else if (mode == OPSC_MODE_MODEL) {
       EQ(launch_model_grid(*dag, *model, dw, c->cfg, c->feasible, c->status, s, tw, tb));
       c->launches += 1;
@@ -802,6 +839,7 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
     for (auto& g : c->graphs)
       if (g.exec && g.sig == sig) hit = &g;
     if (!hit) {
+      if ((rc = ensure_cc())) return rc;
       bool again = false;
       for (auto& v : c->seen) again |= v == sig;
       if (again) {  // capture now
@@ -840,6 +878,7 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
       graph_launches = hit->launches;
     }
   }
+  if (!exec && (rc = ensure_cc())) return rc;
   CK(cudaEventRecord(c->ev0, s));  // device-side span: first H2D .. last D2H
   if (exec) {
     CK(cudaGraphLaunch(exec, s));

@@ -9,6 +9,8 @@
 //   * request_energy (metrics.py:84-102) with every interference factor equal
 //     to 1 (single-group devices under default-stream placement), i.e.
 //     t_eff = (T * R) / R as _adjusted_ops computes it (placement.py:257).
+#include <cstring>
+
 #include "opsc_common.cuh"
 
 namespace opsc {
@@ -130,11 +132,88 @@ __device__ uint32_t place_default_stream(const OpscPlaceSpec& pl, int n, MatScra
 // plan's config order), exactly as the sequential reference.
 constexpr int kMatWarps = 4;
 
+// Brute-force decode in the window's warp (DECODE): the per-op fallback
+// argmin when no candidate met the SLO (autoscaler.py:828-841: min over
+// finite weights of (weight, entry), one warp reduction per op) or the
+// winner's lexicographic index split into menu entries (:843-845), then the
+// (P, R, B) configs -- the work of fallback_kernel + decode_kernel, fused so
+// the per-window chain is one launch shorter by two.
+struct DecodeIn {
+  OpscGrid g;
+  const unsigned long long* key;
+  const double* menu_w;
+};
+
+__device__ __forceinline__ void decode_window(const OpscDag& d, const DecodeIn& dc, const OpscDecisions& out, int w,
+                                              int lane) {
+  const int n = d.n_ops;
+  int16_t* cw = out.cfg + (size_t)w * n * 3;
+  for (int i = lane; i < n * 3; i += 32) cw[i] = 0;  // defined output for idle / error windows
+  if (lane == 0) out.feasible[w] = 0;
+  __syncwarp();
+  if (out.status[w] & OPSC_W_IDLE) return;
+  const unsigned long long key = dc.key[w];
+  const OpscGrid& g = dc.g;
+  if (key != (unsigned long long)OPSC_KEY_INFEASIBLE) {
+    if (lane == 0) {
+      unsigned long long lex = key & OPSC_LEXMASK;
+      for (int v = n - 1; v >= 0; --v) {
+        const unsigned long long m = (unsigned long long)(g.menu_off[v + 1] - g.menu_off[v]);
+        const int e = (int)(lex % m);
+        lex /= m;
+        int p, r, b;
+        entry_prb(g, v, e, p, r, b);
+        cw[v * 3] = (int16_t)p;
+        cw[v * 3 + 1] = (int16_t)r;
+        cw[v * 3 + 2] = (int16_t)b;
+      }
+      out.feasible[w] = 1;
+    }
+    __syncwarp();
+    return;
+  }
+  const int E = g.menu_off[n];
+  int bad = 0;  // 1 + rank of the first operator without a finite entry (autoscaler.py:833-837)
+  for (int v = 0; v < n; ++v) {
+    const double* mw = dc.menu_w + (size_t)w * E + g.menu_off[v];
+    const int m = g.menu_off[v + 1] - g.menu_off[v];
+    double bw = OPSC_INF;
+    int be = 0x7fffffff;
+    for (int e = lane; e < m; e += 32) {
+      const double x = mw[e];
+      if (isfinite(x) && (x < bw || (x == bw && e < be))) { bw = x; be = e; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double x = __shfl_xor_sync(0xffffffffu, bw, o);
+      const int e = __shfl_xor_sync(0xffffffffu, be, o);
+      if (x < bw || (x == bw && e < be)) { bw = x; be = e; }
+    }
+    if (be == 0x7fffffff) {
+      if (!bad) bad = v + 1;
+    } else if (lane == 0 && !bad) {
+      int p, r, b;
+      entry_prb(g, v, be, p, r, b);
+      cw[v * 3] = (int16_t)p;
+      cw[v * 3 + 1] = (int16_t)r;
+      cw[v * 3 + 2] = (int16_t)b;
+    }
+  }
+  if (bad) {  // configs stay zero, as decode_kernel leaves them
+    for (int i = lane; i < n * 3; i += 32) cw[i] = 0;
+    __syncwarp();
+    if (lane == 0) out.status[w] |= OPSC_W_NO_STABLE_BOUNDS | ((uint32_t)bad << OPSC_W_BOUNDS_OP_SHIFT);
+  }
+  __syncwarp();
+}
+
+template <bool DECODE>
 __global__ void __launch_bounds__(32 * kMatWarps) materialize_kernel(const __grid_constant__ OpscDag d,
                                                                      const __grid_constant__ OpscWindows win,
                                                                      int config_order,
                                                                      const __grid_constant__ OpscPlaceSpec pl,
-                                                                     const __grid_constant__ OpscDecisions out) {
+                                                                     const __grid_constant__ OpscDecisions out,
+                                                                     const __grid_constant__ DecodeIn dc) {
   pdl_trigger();
   pdl_wait();
   __shared__ double s_wt[kMatWarps][OPSC_MAX_OPS], s_T[kMatWarps][OPSC_MAX_OPS];
@@ -144,6 +223,7 @@ __global__ void __launch_bounds__(32 * kMatWarps) materialize_kernel(const __gri
   const int w = blockIdx.x * kMatWarps + warp;
   if (w >= win.n) return;
   const int n = d.n_ops;
+  if (DECODE) decode_window(d, dc, out, w, lane);
   const uint32_t st0 = out.status[w];
   if (lane < n) {
     out.path[(size_t)w * n + lane] = -1;
@@ -237,8 +317,22 @@ __global__ void __launch_bounds__(32 * kMatWarps) materialize_kernel(const __gri
 cudaError_t launch_materialize(const OpscDag& d, OpscWindows w, int config_order, const OpscPlaceSpec& p,
                                OpscDecisions out, cudaStream_t s) {
   if (w.n <= 0) return cudaSuccess;
-  return launch_pdl(materialize_kernel, dim3((w.n + kMatWarps - 1) / kMatWarps), dim3(32 * kMatWarps), 0, s, d, w,
-                    config_order, p, out);
+  DecodeIn dc;
+  memset(&dc, 0, sizeof(dc));
+  return launch_pdl(materialize_kernel<false>, dim3((w.n + kMatWarps - 1) / kMatWarps), dim3(32 * kMatWarps), 0, s,
+                    d, w, config_order, p, out, dc);
+}
+
+cudaError_t launch_decode_materialize(const OpscDag& d, const OpscGrid& g, OpscWindows w,
+                                      const unsigned long long* key, const double* menu_w, const OpscPlaceSpec& p,
+                                      OpscDecisions out, cudaStream_t s) {
+  if (w.n <= 0) return cudaSuccess;
+  DecodeIn dc;
+  dc.g = g;
+  dc.key = key;
+  dc.menu_w = menu_w;
+  return launch_pdl(materialize_kernel<true>, dim3((w.n + kMatWarps - 1) / kMatWarps), dim3(32 * kMatWarps), 0, s,
+                    d, w, 0, p, out, dc);
 }
 
 }  // namespace opsc

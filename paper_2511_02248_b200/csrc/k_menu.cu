@@ -40,15 +40,11 @@ cudaError_t launch_fill_keys(unsigned long long* key, int n, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-__global__ void __launch_bounds__(256) menu_build_kernel(const __grid_constant__ OpscDag d,
-                                                         const __grid_constant__ OpscGrid g,
-                                                         const __grid_constant__ OpscWindows win,
-                                                         double* __restrict__ menu_w,
-                                                         uint32_t* __restrict__ status) {
-  pdl_trigger();
-  pdl_wait();
+__device__ __forceinline__ void menu_build_body(const OpscDag& d, const OpscGrid& g, const OpscWindows& win,
+                                                double* __restrict__ menu_w, uint32_t* __restrict__ status,
+                                                int block) {
   const int E = g.menu_off[d.n_ops];
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long idx = (long long)block * blockDim.x + threadIdx.x;
   if (idx >= (long long)win.n * E) return;
   const int w = (int)(idx / E);
   const int j = (int)(idx - (long long)w * E);
@@ -71,6 +67,16 @@ __global__ void __launch_bounds__(256) menu_build_kernel(const __grid_constant__
   if (st) atomicOr(&status[w], st);
 }
 
+__global__ void __launch_bounds__(256) menu_build_kernel(const __grid_constant__ OpscDag d,
+                                                         const __grid_constant__ OpscGrid g,
+                                                         const __grid_constant__ OpscWindows win,
+                                                         double* __restrict__ menu_w,
+                                                         uint32_t* __restrict__ status) {
+  pdl_trigger();
+  pdl_wait();
+  menu_build_body(d, g, win, menu_w, status, blockIdx.x);
+}
+
 cudaError_t launch_menu_build(const OpscDag& d, const OpscGrid& g, OpscWindows w, double* menu_w,
                               uint32_t* status, cudaStream_t s) {
   const long long total = (long long)w.n * g.menu_off[d.n_ops];
@@ -83,11 +89,9 @@ cudaError_t launch_menu_build(const OpscDag& d, const OpscGrid& g, OpscWindows w
 // reference's init_configs pre-check, autoscaler.py:254-294), all B of one P
 // across the lanes; flags accumulate over every (P, B) visited up to and
 // including the first P with a stable B, as in the sequential scan.
-__global__ void stability_kernel(const __grid_constant__ OpscDag d, const __grid_constant__ OpscGrid g,
-                                 const __grid_constant__ OpscWindows win, uint32_t* __restrict__ status) {
-  pdl_trigger();
-  pdl_wait();
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+__device__ __forceinline__ void stability_body(const OpscDag& d, const OpscGrid& g, const OpscWindows& win,
+                                               uint32_t* __restrict__ status, int block) {
+  const int gw = (block * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= win.n * d.n_ops) return;
   const int w = gw / d.n_ops, v = gw - w * d.n_ops;
@@ -132,6 +136,38 @@ __global__ void stability_kernel(const __grid_constant__ OpscDag d, const __grid
       nv = (nv & ~(OPSC_W_OP_FIELD << OPSC_W_INIT_OP_SHIFT)) | (mine << OPSC_W_INIT_OP_SHIFT);
     old = atomicCAS(&status[w], assumed, nv);
   } while (old != assumed);
+}
+
+__global__ void stability_kernel(const __grid_constant__ OpscDag d, const __grid_constant__ OpscGrid g,
+                                 const __grid_constant__ OpscWindows win, uint32_t* __restrict__ status) {
+  pdl_trigger();
+  pdl_wait();
+  stability_body(d, g, win, status, blockIdx.x);
+}
+
+// K1 + K1b in one launch (the per-window chains of the host-buffer path and
+// DevicePlanner): the first nb_menu blocks build menus, the rest run the
+// init_configs stability pre-check; both only OR into status.
+__global__ void __launch_bounds__(256) menu_stability_kernel(const __grid_constant__ OpscDag d,
+                                                             const __grid_constant__ OpscGrid g,
+                                                             const __grid_constant__ OpscWindows win,
+                                                             double* __restrict__ menu_w,
+                                                             uint32_t* __restrict__ status, int nb_menu) {
+  pdl_trigger();
+  pdl_wait();
+  if ((int)blockIdx.x < nb_menu) menu_build_body(d, g, win, menu_w, status, blockIdx.x);
+  else stability_body(d, g, win, status, blockIdx.x - nb_menu);
+}
+
+cudaError_t launch_menu_stability(const OpscDag& d, const OpscGrid& g, OpscWindows w, double* menu_w,
+                                  uint32_t* status, cudaStream_t s) {
+  if (w.n <= 0) return cudaSuccess;
+  const long long menu_threads = (long long)w.n * g.menu_off[d.n_ops];
+  const long long stab_threads = (long long)w.n * d.n_ops * 32;
+  const long long nb_menu = (menu_threads + 255) / 256, nb_stab = (stab_threads + 255) / 256;
+  if (nb_menu + nb_stab > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  return launch_pdl(menu_stability_kernel, dim3((unsigned)(nb_menu + nb_stab)), dim3(256), 0, s, d, g, w, menu_w,
+                    status, (int)nb_menu);
 }
 
 cudaError_t launch_stability(const OpscDag& d, const OpscGrid& g, OpscWindows w, uint32_t* status,

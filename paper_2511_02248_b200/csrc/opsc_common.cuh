@@ -370,6 +370,11 @@ cudaError_t launch_model_grid(const OpscDag& d, const OpscModelSpec& m, OpscWind
 size_t model_table_bytes(int n_windows, const OpscModelSpec& m, int n_ops);
 cudaError_t launch_materialize(const OpscDag& d, OpscWindows w, int config_order,
                                const OpscPlaceSpec& p, OpscDecisions out, cudaStream_t s);
+cudaError_t launch_menu_stability(const OpscDag& d, const OpscGrid& g, OpscWindows w, double* menu_w,
+                                  uint32_t* status, cudaStream_t s);
+cudaError_t launch_decode_materialize(const OpscDag& d, const OpscGrid& g, OpscWindows w,
+                                      const unsigned long long* key, const double* menu_w, const OpscPlaceSpec& p,
+                                      OpscDecisions out, cudaStream_t s);
 cudaError_t launch_fp64_peak(int iters, double* sink, int* blocks, int* threads, cudaStream_t s);
 cudaError_t launch_greedy(const OpscDag& d, const OpscGreedySpec& s, OpscWindows w, const int16_t* ucfg,
                           const uint8_t* ufeas, const uint32_t* ustatus, OpscDecisions out, cudaStream_t st,

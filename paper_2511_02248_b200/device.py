@@ -93,13 +93,11 @@ class DevicePlanner:
                                           self.out_t["feasible"].data_ptr(), self._s()), "init_windows")
 
     def menus(self):
+        """K1 menus + K1b stability pre-check, one fused launch."""
         r = _native.ref
-        self._ck(self.L.opsc_menu_build(r(self.problem.table), r(self.grid), self.win,
-                                        self.menu.data_ptr(), self.out_t["status"].data_ptr(),
-                                        self._s()), "menu_build")
-        self._ck(self.L.opsc_stability_check(r(self.problem.table), r(self.grid), self.win,
-                                             self.out_t["status"].data_ptr(), self._s()),
-                 "stability_check")
+        self._ck(self.L.opsc_menu_stability(r(self.problem.table), r(self.grid), self.win,
+                                            self.menu.data_ptr(), self.out_t["status"].data_ptr(),
+                                            self._s()), "menu_stability")
 
     def compose(self, shard=0, n_shards=1):
         r = _native.ref
@@ -125,16 +123,12 @@ class DevicePlanner:
     def finish(self):
         r, s = _native.ref, self._s()
         if self.mode == abi.MODE_ORACLE:
-            self._ck(self.L.opsc_menu_fallback(r(self.problem.table), r(self.grid), self.W,
-                                               self.menu.data_ptr(), self.fb.data_ptr(), s),
-                     "menu_fallback")
-            self._ck(self.L.opsc_decode_decisions(
-                r(self.problem.table), r(self.grid), self.W, self.key.data_ptr(),
-                self.fb.data_ptr(), self.out_t["cfg"].data_ptr(), self.out_t["feasible"].data_ptr(),
-                self.out_t["status"].data_ptr(), s), "decode")
-            order = 0
-        else:
-            order = 1
+            # fallback + decode fused into the materialisation launch
+            self._ck(self.L.opsc_decode_materialize(r(self.problem.table), r(self.grid), self.win,
+                                                    self.key.data_ptr(), self.menu.data_ptr(),
+                                                    r(self.dplace), self.out, s), "decode_materialize")
+            return
+        order = 1
         self._ck(self.L.opsc_materialize(r(self.problem.table), self.win, order, r(self.dplace),
                                          self.out, s), "materialize")
 

@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import math
 import threading
+from operator import is_
 
 import numpy as np
 from collections import OrderedDict
@@ -54,7 +55,7 @@ class _Packed:
     def get(self, key, refs, sig, make):
         with self.lock:
             hit = self.d.get(key)
-            if hit is not None and hit[1] == sig and all(a is b for a, b in zip(hit[0], refs)):
+            if hit is not None and hit[1] == sig and all(map(is_, hit[0], refs)):
                 self.d.move_to_end(key)
                 return hit[2]
         val = make()

@@ -69,22 +69,23 @@ def nonfinite_qps(qps):
 
 
 def _builder(cls, names):
-    """Fast constructor for the plan's frozen value types (OperatorConfig,
-    PredictedSojourn -- this package's or the reference's, autoscaler.py:44-73):
-    fills the instance dict directly, skipping dataclass __init__ /
-    __post_init__, whose checks (P, R, B >= 1) the device results satisfy by
-    construction. Equality, hash and repr are the dataclass's own. Classes
+    """Fast constructor for the plan's value types (OperatorConfig,
+    PredictedSojourn, ScalingPlan -- this package's or the reference's,
+    autoscaler.py:44-99): fills the instance dict directly, skipping
+    dataclass __init__ / __post_init__, whose checks (P, R, B >= 1) the device
+    results satisfy by construction. Equality, hash and repr are the
+    dataclass's own. The body is generated for the class's field names (one
+    dict store per field: ~3x faster than dict.update(zip(...))). Classes
     without an instance dict fall back to the normal constructor."""
     probe = object.__new__(cls)
-    if not hasattr(probe, "__dict__"):
+    if not hasattr(probe, "__dict__") or not all(n.isidentifier() for n in names):
         return cls
-    new = object.__new__
-
-    def make(*vals):
-        o = new(cls)
-        o.__dict__.update(zip(names, vals))
-        return o
-    return make
+    args = ", ".join(f"v{i}" for i in range(len(names)))
+    body = "".join(f"    d[{n!r}] = v{i}\n" for i, n in enumerate(names))
+    src = f"def make({args}):\n    o = new(cls)\n    d = o.__dict__\n{body}    return o\n"
+    ns = {"new": object.__new__, "cls": cls}
+    exec(src, ns)  # noqa: S102 -- field names are the dataclass's own identifiers
+    return ns["make"]
 
 
 _BUILDERS = {}

@@ -19,6 +19,8 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass
 
+from operator import is_
+
 import numpy as np
 
 from . import abi
@@ -228,7 +230,7 @@ class WindowArrays:
         it costs ~10 us of numpy attribute lookups per call)."""
         arrs = (self.qps, self.seq_len, self.phase, self.slo, self.eps)
         hit = self.__dict__.get("_struct")
-        if hit is not None and all(a is b for a, b in zip(hit[0], arrs)):
+        if hit is not None and all(map(is_, hit[0], arrs)):
             return hit[1]
         w = abi.OpscWindows()
         w.n = self.n
@@ -302,7 +304,7 @@ class DecisionArrays:
         """The C-ABI view (cached while the same arrays are attached)."""
         arrs = tuple(getattr(self, f) for f in self.FIELDS) + (self.trace_len, self.trace)
         hit = self.__dict__.get("_struct")
-        if hit is not None and hit[2] == self.trace_cap and all(a is b for a, b in zip(hit[0], arrs)):
+        if hit is not None and hit[2] == self.trace_cap and all(map(is_, hit[0], arrs)):
             return hit[1]
         d = abi.OpscDecisions()
         for f in self.FIELDS:
