@@ -694,7 +694,13 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
   if ((rc = ensure_io(c, L.out_end, stage))) return rc;
   point_io(c, L);
   size_t tb = 0;
-  void* tw = mode == OPSC_MODE_MODEL ? model_table_ws(c, W, *model, n, &tb) : nullptr;  // before any capture
+  // model-level (B, R) table workspace (before any capture): the model mode's
+  // planner and greedy's uniform reseed on the side stream (for a prefill
+  // 70B window the one-kernel form took 129 us there vs 32 us tabulated, and
+  // it is on the critical path when the greedy loop is short)
+  void* tw = mode == OPSC_MODE_MODEL      ? model_table_ws(c, W, *model, n, &tb)
+             : mode == OPSC_MODE_OPERATOR ? model_table_ws(c, W, greedy->model, n, &tb)
+                                          : nullptr;
   // the compose launch shape (host work: level split, strides) is needed
   // only when this call is captured or launched eagerly, not on a replay
   ComposeCfg cc;
@@ -802,9 +808,7 @@ int opsc_plan_windows_host(OpscContext* c, int32_t mode, const OpscDag* dag, con
       EQ(cudaEventRecord(c->fork, s));
       EQ(cudaStreamWaitEvent(c->side, c->fork, 0));
       EQ(launch_init(W, c->qps, c->u_status, nullptr, c->u_feas, c->side));
-      // hidden behind phase 1: the one-kernel form (no (B, R) table) is the
-      // cheaper side-stream load (70B W=1 median 0.177 -> 0.169 ms)
-      EQ(launch_model_grid(*dag, greedy->model, dw, c->u_cfg, c->u_feas, c->u_status, c->side, nullptr, 0));
+      EQ(launch_model_grid(*dag, greedy->model, dw, c->u_cfg, c->u_feas, c->u_status, c->side, tw, tb));
       EQ(cudaEventRecord(c->join, c->side));
       OpscDecisions dd = dev_decisions(c);
       dd.trace_cap = (int32_t)tcap;

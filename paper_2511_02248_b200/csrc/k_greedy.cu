@@ -130,7 +130,7 @@ __device__ int bottleneck(const GShared& S, int n) {
 // lexicographic path tie-break (opgraph.py:223-244), DP scratch in shared
 // memory, and the bottleneck the next step starts from (:306-331) -- so the
 // steps need no serial section of their own before evaluating moves
-__device__ __forceinline__ void set_path(GShared& S, const OpscDag& d) {
+__device__ __noinline__ void set_path(GShared& S, const OpscDag& d) {
   if (S.chain) {  // one source-sink path: val[v] = val[prev] + w[v] in order, the path is every op
     const int n = d.n_ops;
     double acc = 0.0;
@@ -166,6 +166,15 @@ __device__ void push_trace(GShared& S, const OpscDecisions& out, int w, int acti
   S.trace_len++;
 }
 
+// one out-of-line copy of predict_op for the whole kernel (instruction-cache
+// footprint; called per thread, the call overhead is a few instructions)
+__device__ __noinline__ Pred gpredict(const OpscDag& d, double qps, int L, int ph, int v, int p, int r, int b,
+                                      uint32_t* st) {
+  return predict<true>(d, qps, L, ph, v, p, r, b, st);
+}
+
+__device__ __noinline__ void set_path_warp(GShared& S, const OpscDag& d);
+
 // full evaluation of the current configs (all threads; ends synchronised)
 __device__ __noinline__ void eval_full(GShared& S, const OpscDag& d, double qps, int L, int ph) {
   __shared__ int s_unstable;
@@ -173,23 +182,24 @@ __device__ __noinline__ void eval_full(GShared& S, const OpscDag& d, double qps,
   __syncthreads();
   for (int v = threadIdx.x; v < d.n_ops; v += blockDim.x) {
     uint32_t st = 0;
-    const Pred o = predict<true>(d, qps, L, ph, v, S.p[v], S.r[v], S.b[v], &st);
+    const Pred o = gpredict(d, qps, L, ph, v, S.p[v], S.r[v], S.b[v], &st);
     S.soj[v] = o.wait + o.service;
     S.wt[v] = weight(o, d.layer_count[v]);
     if (!o.stable) atomicOr(&s_unstable, 1);
     if (st) atomicOr(&S.st, st);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    S.stable = !s_unstable;
-    if (S.stable) {
-      set_path(S, d);
-    } else {
+  if (threadIdx.x < 32) {  // warp 0
+    const bool stable = !s_unstable;
+    if (stable) {
+      set_path_warp(S, d);
+    } else if (threadIdx.x == 0) {
       S.lat = OPSC_INF;
       for (int i = 0; i < d.n_ops; ++i) S.path[i] = -1;
       S.bneck = -1;
       S.cpv_ok = 0;
     }
+    if (threadIdx.x == 0) S.stable = stable;
   }
   __syncthreads();
 }
@@ -207,7 +217,7 @@ __device__ __noinline__ int eval_moves(GShared& S, const GreedyArgs& a, int op, 
   for (int m = m0 + threadIdx.x; m < m1; m += blockDim.x) {
     const int b = b_lo + m / np, p = S.pd[op][m % np];
     uint32_t st = 0;
-    const Pred o = predict<true>(a.d, qps, L, ph, op, p, r_new, b, &st);
+    const Pred o = gpredict(a.d, qps, L, ph, op, p, r_new, b, &st);
     const int i = m - m0;
     S.m_ok[i] = o.stable;
     if (o.stable) {
@@ -291,26 +301,80 @@ __device__ void block_min(PK (&x)[NK]) {
   __syncthreads();
 }
 
-// thread 0: apply move m of `op` (new r), recompute the critical path. The
-// move's weight / sojourn come from the scratch when its chunk is the last
-// one evaluated, else they are recomputed (same predict, same bits).
-__device__ __noinline__ void apply_move(GShared& S, const GreedyArgs& a, int op, int m, int r_new, int b_lo, int m0, double qps,
-                           int L, int ph) {
-  const int np = S.np_d[op];
-  S.p[op] = S.pd[op][m % np];
-  S.b[op] = b_lo + m / np;
-  S.r[op] = r_new;
-  if (m >= m0 && m < m0 + kMaxMoves) {
-    S.wt[op] = S.m_wt[m - m0];
-    S.soj[op] = S.m_soj[m - m0];
-  } else {
-    uint32_t st = 0;
-    const Pred o = predict<true>(a.d, qps, L, ph, op, S.p[op], r_new, S.b[op], &st);
-    S.wt[op] = weight(o, a.d.layer_count[op]);
-    S.soj[op] = o.wait + o.service;
+// warp 0 (all lanes): set_path's results with the serial parts spread over
+// the lanes -- a chain's weights gathered by shuffles and summed left to
+// right in every lane (lane i keeps the DP value of position i), the
+// bottleneck as a warp (sojourn, -id) max (literal scan if a sojourn is
+// NaN), the non-negativity check as a vote. Same values as set_path.
+__device__ __noinline__ void set_path_warp(GShared& S, const OpscDag& d) {
+  const int lane = threadIdx.x & 31, n = d.n_ops;
+  if (S.chain) {
+    const int u = lane < n ? d.topo[lane] : 0;
+    const double wl = lane < n ? S.wt[u] : 0.0;
+    double acc = 0.0, mine = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double wi = __shfl_sync(0xffffffffu, wl, i);
+      acc = i == 0 ? wi : acc + wi;
+      if (lane == i) mine = acc;
+    }
+    if (lane < n) {
+      S.cpv[u] = mine;
+      S.path[lane] = (int8_t)u;
+    }
+    if (lane == 0) S.lat = acc;
+  } else if (lane == 0) {
+    S.lat = critical_path_lex_body(d, S.wt, S.path, S.cpv, S.cppar);
   }
-  set_path(S, a.d);
-  S.stable = 1;
+  __syncwarp();
+  const int v = lane < n ? S.path[lane] : -1;
+  const double sj = v >= 0 ? S.soj[v] : 0.0;
+  const bool nan = __any_sync(0xffffffffu, v >= 0 && sj != sj);
+  int bv = v;
+  double bs = sj;
+  for (int o = 16; o > 0; o >>= 1) {
+    const int ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const double os = __shfl_xor_sync(0xffffffffu, bs, o);
+    if (ov >= 0 && (bv < 0 || os > bs || (os == bs && ov < bv))) {
+      bv = ov;
+      bs = os;
+    }
+  }
+  const bool nonneg = __all_sync(0xffffffffu, lane >= n || S.wt[lane] >= 0.0);
+  if (lane == 0) {
+    S.bneck = nan ? bottleneck(S, n) : bv;
+    S.cpv_ok = nonneg;
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ int objective_warp(const GShared& S, int n) {
+  const int lane = threadIdx.x & 31;
+  return __reduce_add_sync(0xffffffffu, lane < n ? S.p[lane] * S.r[lane] : 0);
+}
+
+// warp 0: apply move m of `op` (new r; lane 0 updates the config and the
+// move's weight / sojourn -- from the scratch when its chunk is the last one
+// evaluated, else recomputed, same bits) and the path (set_path_warp)
+__device__ __noinline__ void apply_move_warp(GShared& S, const GreedyArgs& a, int op, int m, int r_new, int b_lo,
+                                             int m0, double qps, int L, int ph) {
+  if ((threadIdx.x & 31) == 0) {
+    const int np = S.np_d[op];
+    S.p[op] = S.pd[op][m % np];
+    S.b[op] = b_lo + m / np;
+    S.r[op] = r_new;
+    if (m >= m0 && m < m0 + kMaxMoves) {
+      S.wt[op] = S.m_wt[m - m0];
+      S.soj[op] = S.m_soj[m - m0];
+    } else {
+      uint32_t st = 0;
+      const Pred o = gpredict(a.d, qps, L, ph, op, S.p[op], r_new, S.b[op], &st);
+      S.wt[op] = weight(o, a.d.layer_count[op]);
+      S.soj[op] = o.wait + o.service;
+    }
+    S.stable = 1;
+  }
+  __syncwarp();
+  set_path_warp(S, a.d);
 }
 
 // One upscale step (greedy loop when headroom == false, _restore_headroom
@@ -330,7 +394,7 @@ __device__ __noinline__ void upscale_step(GShared& S, const GreedyArgs& a, const
     return;
   }
   const int np = S.np_d[op];
-  const int base = objective(S, a.d.n_ops);
+  const int base = objective_warp(S, a.d.n_ops);  // every warp: one add-reduction
   const double target = slo - eps, cur_lat = S.lat;
   PK k[3];  // ach, ach2, imp
   for (int i = 0; i < 3; ++i) k[i] = pk_none();
@@ -358,14 +422,16 @@ __device__ __noinline__ void upscale_step(GShared& S, const GreedyArgs& a, const
   } while (m0 < M);
   m0 -= kMaxMoves;  // the chunk still in the scratch
   block_min<3>(k);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // warp 0 applies the pick (every thread holds the same minima)
     const PK& pick = pk_valid(k[0]) ? k[0] : (!headroom && pk_valid(k[1])) ? k[1] : k[2];
     const int m = pk_valid(pick) ? move_index(S, op, 1, pk_b(pick), pk_p(pick)) : -1;
-    S.applied = m >= 0;
+    if (threadIdx.x == 0) S.applied = m >= 0;
     if (m >= 0) {
-      apply_move(S, a, op, m, cur_r + 1, 1, m0, qps, L, ph);
-      push_trace(S, out, w, headroom ? OPSC_ACT_HEADROOM : OPSC_ACT_UPSCALE, op, S.r[op], S.b[op], S.p[op],
-                 S.lat, objective(S, a.d.n_ops));
+      apply_move_warp(S, a, op, m, cur_r + 1, 1, m0, qps, L, ph);
+      const int obj = objective_warp(S, a.d.n_ops);
+      if (threadIdx.x == 0)
+        push_trace(S, out, w, headroom ? OPSC_ACT_HEADROOM : OPSC_ACT_UPSCALE, op, S.r[op], S.b[op], S.p[op],
+                   S.lat, obj);
     }
   }
   __syncthreads();
@@ -384,7 +450,7 @@ __device__ __noinline__ void downscale_step(GShared& S, const GreedyArgs& a, con
     return;
   }
   const int np = S.np_d[op];
-  const int base = objective(S, a.d.n_ops);
+  const int base = objective_warp(S, a.d.n_ops);  // every warp: one add-reduction
   const double bound = slo - eps;
   PK k[1];
   k[0] = pk_none();
@@ -404,13 +470,14 @@ __device__ __noinline__ void downscale_step(GShared& S, const GreedyArgs& a, con
   } while (m0 < M);
   m0 -= kMaxMoves;
   block_min<1>(k);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     const int best = pk_valid(k[0]) ? move_index(S, op, cur_b, pk_b(k[0]), pk_p(k[0])) : -1;
-    S.applied = best >= 0;
+    if (threadIdx.x == 0) S.applied = best >= 0;
     if (best >= 0) {
-      apply_move(S, a, op, best, cur_r - 1, cur_b, m0, qps, L, ph);
-      push_trace(S, out, w, OPSC_ACT_DOWNSCALE, op, S.r[op], S.b[op], S.p[op], S.lat,
-                 objective(S, a.d.n_ops));
+      apply_move_warp(S, a, op, best, cur_r - 1, cur_b, m0, qps, L, ph);
+      const int obj = objective_warp(S, a.d.n_ops);
+      if (threadIdx.x == 0)
+        push_trace(S, out, w, OPSC_ACT_DOWNSCALE, op, S.r[op], S.b[op], S.p[op], S.lat, obj);
     }
   }
   __syncthreads();
@@ -449,7 +516,7 @@ __device__ __noinline__ void prune_pass(GShared& S, const GreedyArgs& a, const O
     for (int v = threadIdx.x; v < d.n_ops; v += blockDim.x) {
       if (!t_need[v] || S.r[v] <= 1) continue;
       uint32_t st = 0;
-      const Pred o = predict<true>(d, qps, L, ph, v, S.p[v], S.r[v] - 1, S.b[v], &st);
+      const Pred o = gpredict(d, qps, L, ph, v, S.p[v], S.r[v] - 1, S.b[v], &st);
       if (st) atomicOr(&S.st, st);
       t_ok[v] = o.stable;
       t_wt[v] = weight(o, d.layer_count[v]);

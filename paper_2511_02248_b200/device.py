@@ -146,9 +146,9 @@ class DevicePlanner:
         side = self._side.cuda_stream
         self._ck(self.L.opsc_init_windows(self.win, self.u_status.data_ptr(), None,
                                           self.u_feas.data_ptr(), side), "init_windows")
-        # the reseed is hidden behind phase 1: the one-kernel form (no table) is
-        # the cheaper side-stream load (W=1 70B median 0.177 -> 0.169 ms)
-        self._model_grid_into(self.greedy.model, self.u_cfg, self.u_feas, self.u_status, side, table=False)
+        # the reseed runs beside phase 1; tabulated (B, R) points: a 70B prefill
+        # window's K3 took 129 us in the one-kernel form, more than phase 1
+        self._model_grid_into(self.greedy.model, self.u_cfg, self.u_feas, self.u_status, side)
         args = (r(self.problem.table), r(self.greedy), self.win)
         uni = (self.u_cfg.data_ptr(), self.u_feas.data_ptr(), self.u_status.data_ptr())
         self._ck(self.L.opsc_greedy_phase(*args, 1, self._gstate.data_ptr(), *uni, self.out,

@@ -37,5 +37,8 @@ for ph in ("prefill", "decode"):
         e1.record()
         e1.synchronize()
         out.append(e0.elapsed_time(e1))
+        if os.environ.get("W1_DETAIL"):
+            tl = int(p.trace_len[0].item()) if p.trace_cap else -1
+            print(f"  {ph} w{i}: {out[-1]:.4f} ms trace_len {tl} status {int(p.out_t['status'][0].item()):#x}")
 print(f"{sys.argv[1]} IL={os.environ.get('OPSC_COMPOSE_IL', 'auto')}: median {statistics.median(out):.4f} ms, "
       f"max {max(out):.4f} ms over {len(out)} windows")
