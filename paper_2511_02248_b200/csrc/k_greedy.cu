@@ -101,16 +101,6 @@ __device__ double trial_latency(const GShared& S, const OpscDag& d, const double
   return top;
 }
 
-// the DAG is a single path: topo[0] a source, every later op fed by exactly
-// the previous one, the last op the only sink
-__device__ bool is_chain(const OpscDag& d) {
-  const int n = d.n_ops;
-  if (d.pred_mask[d.topo[0]] != 0u || d.sink_mask != (1u << d.topo[n - 1])) return false;
-  for (int i = 1; i < n; ++i)
-    if (d.pred_mask[d.topo[i]] != (1u << d.topo[i - 1])) return false;
-  return true;
-}
-
 __device__ int objective(const GShared& S, int n) {
   int o = 0;
   for (int v = 0; v < n; ++v) o += S.p[v] * S.r[v];

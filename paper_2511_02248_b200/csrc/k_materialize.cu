@@ -126,11 +126,15 @@ __device__ uint32_t place_default_stream(const OpscPlaceSpec& pl, int n, MatScra
   return 0;
 }
 
-// One warp per window: lane v predicts operator v (its Erlang-B recurrences
-// run in parallel lanes) and its Eq. 9 energy terms; lane 0 then runs the
-// order-dependent parts (critical path, placement, the energy sum in the
-// plan's config order), exactly as the sequential reference.
-constexpr int kMatWarps = 4;
+// Two warps per window. Warp A: lane v predicts operator v (its Erlang-B
+// recurrences run in parallel lanes) and its Eq. 9 energy terms, then the
+// critical path (a chain's weights summed left to right by shuffles; any
+// other DAG by lane 0 with the reference's lexicographic path tie-break) and
+// the energy sum in the plan's config order. Warp B, at the same time: the
+// default-stream placement, which needs only the configs, op latencies and
+// memory (lane-parallel sorts, then lane 0's sequential packing, as the
+// reference). A named barrier per window joins them.
+constexpr int kMatWin = 2;  // windows per CTA (2 warps each)
 
 // Brute-force decode in the window's warp (DECODE): the per-op fallback
 // argmin when no candidate met the SLO (autoscaler.py:828-841: min over
@@ -207,35 +211,55 @@ __device__ __forceinline__ void decode_window(const OpscDag& d, const DecodeIn& 
   __syncwarp();
 }
 
+// the two warps of window `pair` (barrier ids 1, 2 as immediates: ptxas
+// reserves only what it sees)
+__device__ __forceinline__ void pair_barrier(int pair) {
+  static_assert(kMatWin == 2, "one named barrier per window of the CTA");
+  if (pair == 0) asm volatile("bar.sync 1, 64;" ::: "memory");
+  else asm volatile("bar.sync 2, 64;" ::: "memory");
+}
+
+struct MatPlace {
+  uint32_t err;
+  int devices;
+  double memory;
+};
+
 template <bool DECODE>
-__global__ void __launch_bounds__(32 * kMatWarps) materialize_kernel(const __grid_constant__ OpscDag d,
-                                                                     const __grid_constant__ OpscWindows win,
-                                                                     int config_order,
-                                                                     const __grid_constant__ OpscPlaceSpec pl,
-                                                                     const __grid_constant__ OpscDecisions out,
-                                                                     const __grid_constant__ DecodeIn dc) {
+__global__ void __launch_bounds__(64 * kMatWin) materialize_kernel(const __grid_constant__ OpscDag d,
+                                                                   const __grid_constant__ OpscWindows win,
+                                                                   int config_order,
+                                                                   const __grid_constant__ OpscPlaceSpec pl,
+                                                                   const __grid_constant__ OpscDecisions out,
+                                                                   const __grid_constant__ DecodeIn dc) {
   pdl_trigger();
   pdl_wait();
-  __shared__ double s_wt[kMatWarps][OPSC_MAX_OPS], s_T[kMatWarps][OPSC_MAX_OPS];
-  __shared__ double s_e1[kMatWarps][OPSC_MAX_OPS], s_e2[kMatWarps][OPSC_MAX_OPS];
-  __shared__ MatScratch s_scr[kMatWarps];
+  __shared__ double s_wt[kMatWin][OPSC_MAX_OPS], s_T[kMatWin][OPSC_MAX_OPS];
+  __shared__ double s_e1[kMatWin][OPSC_MAX_OPS], s_e2[kMatWin][OPSC_MAX_OPS];
+  __shared__ MatScratch s_scr[kMatWin];
+  __shared__ MatPlace s_pl[kMatWin];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int w = blockIdx.x * kMatWarps + warp;
-  if (w >= win.n) return;
+  const int pair = warp >> 1;
+  const bool A = (warp & 1) == 0;
+  const int w = blockIdx.x * kMatWin + pair;
+  if (w >= win.n) return;  // both warps of a window leave together
   const int n = d.n_ops;
-  if (DECODE) decode_window(d, dc, out, w, lane);
+  if (DECODE && A) decode_window(d, dc, out, w, lane);
+  if (DECODE) pair_barrier(pair);
   const uint32_t st0 = out.status[w];
-  if (lane < n) {
-    out.path[(size_t)w * n + lane] = -1;
-    out.stable[(size_t)w * n + lane] = 0;
-    for (int f = 0; f < OPSC_PRED_FIELDS; ++f) out.pred[((size_t)w * n + lane) * OPSC_PRED_FIELDS + f] = 0.0;
-  }
-  if (lane == 0) {
-    out.latency[w] = OPSC_INF;
-    out.objective[w] = 0;
-    out.energy[w] = 0.0;
-    out.memory[w] = 0.0;
-    out.devices[w] = 0;
+  if (A) {
+    if (lane < n) {
+      out.path[(size_t)w * n + lane] = -1;
+      out.stable[(size_t)w * n + lane] = 0;
+      for (int f = 0; f < OPSC_PRED_FIELDS; ++f) out.pred[((size_t)w * n + lane) * OPSC_PRED_FIELDS + f] = 0.0;
+    }
+    if (lane == 0) {
+      out.latency[w] = OPSC_INF;
+      out.objective[w] = 0;
+      out.energy[w] = 0.0;
+      out.memory[w] = 0.0;
+      out.devices[w] = 0;
+    }
   }
   if (st0 & (OPSC_W_IDLE | OPSC_W_NO_STABLE_BOUNDS | OPSC_W_NO_STABLE_PARAMS | OPSC_W_NO_STABLE_MODEL |
              OPSC_W_NO_STABLE_INIT))
@@ -244,23 +268,45 @@ __global__ void __launch_bounds__(32 * kMatWarps) materialize_kernel(const __gri
   const double qps = win.qps[w];
   const int L = win.seq_len[w], ph = win.phase[w];
   const bool feas = out.feasible[w] != 0;
+  MatScratch& S = s_scr[pair];
+  if (!A) {  // ---- warp B: default-stream placement (placement.py:358-396, 465-491)
+    if (feas) {
+      if (lane < n) {
+        const int v = lane;
+        const int p = c[v * 3], r = c[v * 3 + 1], b = c[v * 3 + 2];
+        S.cp[v] = p;
+        S.cr[v] = r;
+        S.cb[v] = b;
+        s_T[pair][v] = op_latency(d, ph, v, b, L, p);
+      }
+      __syncwarp();
+      place_prepare(d, s_T[pair], L, S, lane);
+      if (lane == 0) {
+        MatPlace& P = s_pl[pair];
+        P.devices = 0;
+        P.memory = 0.0;
+        P.err = place_default_stream(pl, n, S, &P.devices, &P.memory);
+      }
+    }
+    pair_barrier(pair);
+    return;
+  }
+  // ---- warp A: evaluate (autoscaler.py:196-206) and request_energy terms
   uint32_t st = 0;
   bool stable = true;
-  MatScratch& S = s_scr[warp];
+  int cpv = 0, crv = 0;
   if (lane < n) {
     const int v = lane;
     const int p = c[v * 3], r = c[v * 3 + 1], b = c[v * 3 + 2];
-    S.cp[v] = p;
-    S.cr[v] = r;
-    S.cb[v] = b;
+    cpv = p;
+    crv = r;
     const Pred o = predict(d, qps, L, ph, v, p, r, b, &st);
     double* pf = out.pred + ((size_t)w * n + v) * OPSC_PRED_FIELDS;
     pf[0] = o.t; pf[1] = o.lam; pf[2] = o.mu; pf[3] = o.util;
     pf[4] = o.wait; pf[5] = o.service; pf[6] = o.comm;
     out.stable[(size_t)w * n + v] = o.stable;
     stable = o.stable;
-    s_wt[warp][v] = weight(o, d.layer_count[v]);
-    s_T[warp][v] = o.t;
+    s_wt[pair][v] = weight(o, d.layer_count[v]);
   }
   // request_energy terms under default-stream placement: factors 1,
   // t_eff = (T * R) / R (placement.py:257), wait re-derived from t_eff -- a
@@ -281,33 +327,46 @@ __global__ void __launch_bounds__(32 * kMatWarps) materialize_kernel(const __gri
                             ? wait_for_sum(r, lam / ((double)r * mu), (double)r * mu - lam, t_eff)
                             : OPSC_INF;
     const double wl = wait * layers, sl = t_eff * layers;
-    s_e1[warp][v] = ((pl.alpha * (double)p) * (double)r) * (wl + sl);
-    s_e2[warp][v] = pl.beta * sl;
+    s_e1[pair][v] = ((pl.alpha * (double)p) * (double)r) * (wl + sl);
+    s_e2[pair][v] = pl.beta * sl;
   }
   const bool all = __all_sync(0xffffffffu, stable);
   st = __reduce_or_sync(0xffffffffu, st);
+  const int obj = __reduce_add_sync(0xffffffffu, cpv * crv);
   __syncwarp();
-  if (feas) place_prepare(d, s_T[warp], L, S, lane);
+  if (all) {
+    if (is_chain(d)) {  // one source-sink path: val = val(prev) + w in order, the path is every op
+      const int u = lane < n ? d.topo[lane] : 0;
+      const double wl = lane < n ? s_wt[pair][u] : 0.0;
+      double acc = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const double wi = __shfl_sync(0xffffffffu, wl, i);
+        acc = i == 0 ? wi : acc + wi;
+      }
+      if (lane < n) out.path[(size_t)w * n + lane] = (int8_t)u;
+      if (lane == 0) out.latency[w] = acc;
+    } else if (lane == 0) {
+      out.latency[w] = critical_path_lex(d, s_wt[pair], out.path + (size_t)w * n, S.val, S.parent);
+    }
+  }
+  double total = 0.0;
+  if (feas && lane == 0) {  // the energy sum in the plan's config order
+    for (int i = 0; i < n; ++i) {
+      const int v = config_order == 0 ? i : d.node_order[i];
+      total = total + s_e1[pair][v];
+      total = total + s_e2[pair][v];
+    }
+  }
+  pair_barrier(pair);  // warp B's placement is in s_pl
   if (lane != 0) return;
-  int obj = 0;
-  for (int v = 0; v < n; ++v) obj += S.cp[v] * S.cr[v];
   out.objective[w] = obj;
-  if (all) out.latency[w] = critical_path_lex(d, s_wt[warp], out.path + (size_t)w * n, S.val, S.parent);
   st |= st0;
   if (feas) {
-    int dev = 0;
-    double mem = 0.0;
-    const uint32_t e = place_default_stream(pl, n, S, &dev, &mem);
-    st |= e;
-    if (!e) {
-      out.devices[w] = dev;
-      out.memory[w] = mem;
-      double total = 0.0;
-      for (int i = 0; i < n; ++i) {
-        const int v = config_order == 0 ? i : d.node_order[i];
-        total = total + s_e1[warp][v];
-        total = total + s_e2[warp][v];
-      }
+    const MatPlace& P = s_pl[pair];
+    st |= P.err;
+    if (!P.err) {
+      out.devices[w] = P.devices;
+      out.memory[w] = P.memory;
       out.energy[w] = total;
     }
   }
@@ -319,8 +378,8 @@ cudaError_t launch_materialize(const OpscDag& d, OpscWindows w, int config_order
   if (w.n <= 0) return cudaSuccess;
   DecodeIn dc;
   memset(&dc, 0, sizeof(dc));
-  return launch_pdl(materialize_kernel<false>, dim3((w.n + kMatWarps - 1) / kMatWarps), dim3(32 * kMatWarps), 0, s,
-                    d, w, config_order, p, out, dc);
+  return launch_pdl(materialize_kernel<false>, dim3((w.n + kMatWin - 1) / kMatWin), dim3(64 * kMatWin), 0, s, d, w,
+                    config_order, p, out, dc);
 }
 
 cudaError_t launch_decode_materialize(const OpscDag& d, const OpscGrid& g, OpscWindows w,
@@ -331,8 +390,8 @@ cudaError_t launch_decode_materialize(const OpscDag& d, const OpscGrid& g, OpscW
   dc.g = g;
   dc.key = key;
   dc.menu_w = menu_w;
-  return launch_pdl(materialize_kernel<true>, dim3((w.n + kMatWarps - 1) / kMatWarps), dim3(32 * kMatWarps), 0, s,
-                    d, w, 0, p, out, dc);
+  return launch_pdl(materialize_kernel<true>, dim3((w.n + kMatWin - 1) / kMatWin), dim3(64 * kMatWin), 0, s, d, w,
+                    0, p, out, dc);
 }
 
 }  // namespace opsc

@@ -194,6 +194,17 @@ static __device__ __forceinline__ double critical_path_lex(const OpscDag& d, con
   return critical_path_lex(d, wt, path_out, val, parent);
 }
 
+// the DAG is a single path: topo[0] a source, every later op fed by exactly
+// the previous one, the last op the only sink (critical path = the whole
+// chain, its latency the left-to-right sum of the weights)
+__device__ __forceinline__ bool is_chain(const OpscDag& d) {
+  const int n = d.n_ops;
+  if (d.pred_mask[d.topo[0]] != 0u || d.sink_mask != (1u << d.topo[n - 1])) return false;
+  for (int i = 1; i < n; ++i)
+    if (d.pred_mask[d.topo[i]] != (1u << d.topo[i - 1])) return false;
+  return true;
+}
+
 struct Pred {
   double t, lam, mu, util, wait, service, comm;
   bool stable;
