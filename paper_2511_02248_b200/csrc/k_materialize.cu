@@ -215,8 +215,11 @@ __device__ __forceinline__ void decode_window(const OpscDag& d, const DecodeIn& 
 // reserves only what it sees)
 __device__ __forceinline__ void pair_barrier(int pair) {
   static_assert(kMatWin == 2, "one named barrier per window of the CTA");
-  if (pair == 0) asm volatile("bar.sync 1, 64;" ::: "memory");
-  else asm volatile("bar.sync 2, 64;" ::: "memory");
+  // non-.aligned form: a warp may arrive with its lanes not yet reconverged
+  // (compute-sanitizer synccheck flags bar.sync = barrier.sync.aligned there)
+  __syncwarp();
+  if (pair == 0) asm volatile("barrier.sync 1, 64;" ::: "memory");
+  else asm volatile("barrier.sync 2, 64;" ::: "memory");
 }
 
 struct MatPlace {
