@@ -69,6 +69,14 @@ struct GShared {
 // critical-path DP and this one, which clamps dp_in at 0, agree bit for bit).
 __device__ double trial_latency(const GShared& S, const OpscDag& d, const double* wt, int v, double wv,
                                 bool prefix) {
+  if (!prefix && S.chain) {  // a chain, literally the DP below: t = max(0, t) + w in topological order
+    double t = 0.0;
+    for (int i = 0; i < d.n_ops; ++i) {
+      const int u = d.topo[i];
+      t = fmax(0.0, t) + (u == v ? wv : wt[u]);
+    }
+    return fmax(0.0, t);
+  }
   if (prefix && S.chain) {  // a chain: one running value from v's predecessor on
     const int n = d.n_ops, i0 = S.tpos[v];
     double t = i0 > 0 ? S.cpv[d.topo[i0 - 1]] : 0.0;  // >= 0 (all weights >= 0)
@@ -514,25 +522,43 @@ __device__ __noinline__ void prune_pass(GShared& S, const GreedyArgs& a, const O
       t_need[v] = 0;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      changed = 0;
-      for (int v = 0; v < d.n_ops; ++v) {
-        if (S.r[v] <= 1 || !t_ok[v]) continue;
-        const double lat = trial_latency(S, d, S.wt, v, t_wt[v], false);  // S.wt moves inside the pass
-        if (!(lat <= target)) continue;
-        S.r[v] -= 1;
-        S.wt[v] = t_wt[v];
-        S.soj[v] = t_soj[v];
-        // the accepted trial's DP value IS the new critical-path latency
-        // (max over predecessors commutes with the monotone + w); the path
-        // itself is only needed after the pass
-        S.lat = lat;
-        S.cpv_ok = 0;
-        push_trace(S, out, w, OPSC_ACT_PRUNE, v, S.r[v], S.b[v], S.p[v], S.lat, objective(S, d.n_ops));
-        t_need[v] = 1;
-        changed = 1;
+    // The sweep in id order (each accepted prune changes the state the next
+    // trial sees), by warp 0 with one lane per operator: every remaining
+    // operator's trial runs at once against the current state, the lowest id
+    // that passes is accepted -- exactly the one the sequential sweep accepts
+    // next, since the ids before it failed against the same state -- and the
+    // sweep resumes after it.
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x, n = d.n_ops;
+      bool any = false;
+      for (int start = 0; start < n;) {
+        const bool cand = lane >= start && lane < n && S.r[lane] > 1 && t_ok[lane];
+        double lat = OPSC_INF;
+        if (cand) lat = trial_latency(S, d, S.wt, lane, t_wt[lane], false);  // S.wt moves inside the pass
+        const unsigned pass = __ballot_sync(0xffffffffu, cand && lat <= target);
+        if (!pass) break;
+        const int v = __ffs(pass) - 1;
+        const double lv = __shfl_sync(0xffffffffu, lat, v);
+        if (lane == 0) {
+          S.r[v] -= 1;
+          S.wt[v] = t_wt[v];
+          S.soj[v] = t_soj[v];
+          // the accepted trial's DP value IS the new critical-path latency
+          // (max over predecessors commutes with the monotone + w); the path
+          // itself is only needed after the pass
+          S.lat = lv;
+          S.cpv_ok = 0;
+          t_need[v] = 1;
+        }
+        __syncwarp();
+        const int obj = objective_warp(S, n);
+        if (lane == 0) push_trace(S, out, w, OPSC_ACT_PRUNE, v, S.r[v], S.b[v], S.p[v], S.lat, obj);
+        __syncwarp();
+        any = true;
+        start = v + 1;
       }
-      if (!changed) set_path(S, d);  // path (and the same value) for what follows
+      if (lane == 0) changed = any;
+      if (!any) set_path_warp(S, d);  // path (and the same value) for what follows
     }
     __syncthreads();
     if (!changed) break;
