@@ -16,6 +16,9 @@
 // The step functions are __noinline__: inlined at every call site the kernel
 // was 32k instructions (512 KB of SASS) and a single-window run spent ~22% of
 // its warp samples waiting on instruction fetch (ncu stall "no_inst").
+#include <cstdio>
+#include <cstring>
+
 #include "opsc_common.cuh"
 
 namespace opsc {
@@ -171,19 +174,33 @@ __device__ __noinline__ Pred gpredict(const OpscDag& d, double qps, int L, int p
   return predict<true>(d, qps, L, ph, v, p, r, b, st);
 }
 
+// predict_op of (v, P, R, B) for window w as the steps use it
+struct GPt {
+  double wt, soj;
+  bool ok;
+};
+
+__device__ __forceinline__ GPt gpoint(const GreedyArgs& a, int w, double qps, int L, int ph, int v, int p, int r,
+                                      int b, uint32_t* st) {
+  (void)w;
+  const Pred o = gpredict(a.d, qps, L, ph, v, p, r, b, st);
+  return GPt{weight(o, a.d.layer_count[v]), o.wait + o.service, o.stable};
+}
+
 __device__ __noinline__ void set_path_warp(GShared& S, const OpscDag& d);
 
 // full evaluation of the current configs (all threads; ends synchronised)
-__device__ __noinline__ void eval_full(GShared& S, const OpscDag& d, double qps, int L, int ph) {
+__device__ __noinline__ void eval_full(GShared& S, const GreedyArgs& a, int w, double qps, int L, int ph) {
+  const OpscDag& d = a.d;
   __shared__ int s_unstable;
   if (threadIdx.x == 0) s_unstable = 0;
   __syncthreads();
   for (int v = threadIdx.x; v < d.n_ops; v += blockDim.x) {
     uint32_t st = 0;
-    const Pred o = gpredict(d, qps, L, ph, v, S.p[v], S.r[v], S.b[v], &st);
-    S.soj[v] = o.wait + o.service;
-    S.wt[v] = weight(o, d.layer_count[v]);
-    if (!o.stable) atomicOr(&s_unstable, 1);
+    const GPt o = gpoint(a, w, qps, L, ph, v, S.p[v], S.r[v], S.b[v], &st);
+    S.soj[v] = o.soj;
+    S.wt[v] = o.wt;
+    if (!o.ok) atomicOr(&s_unstable, 1);
     if (st) atomicOr(&S.st, st);
   }
   __syncthreads();
@@ -206,8 +223,8 @@ __device__ __noinline__ void eval_full(GShared& S, const OpscDag& d, double qps,
 // count r_new (move m = (B = b_lo + m / np, P = pd[m % np]), all distinct P)
 // into the scratch slots m - m0 (all threads; ends synchronised). Returns
 // the size of the whole set; sets larger than kMaxMoves run in chunks.
-__device__ __noinline__ int eval_moves(GShared& S, const GreedyArgs& a, int op, int r_new, int b_lo, double qps, int L,
-                          int ph, int m0) {
+__device__ __noinline__ int eval_moves(GShared& S, const GreedyArgs& a, int w, int op, int r_new, int b_lo, double qps,
+                                       int L, int ph, int m0) {
   const int np = S.np_d[op];
   const int nb = a.s.b_max[op] - b_lo + 1;
   const int M = nb * np;
@@ -215,12 +232,12 @@ __device__ __noinline__ int eval_moves(GShared& S, const GreedyArgs& a, int op, 
   for (int m = m0 + threadIdx.x; m < m1; m += blockDim.x) {
     const int b = b_lo + m / np, p = S.pd[op][m % np];
     uint32_t st = 0;
-    const Pred o = gpredict(a.d, qps, L, ph, op, p, r_new, b, &st);
+    const GPt o = gpoint(a, w, qps, L, ph, op, p, r_new, b, &st);
     const int i = m - m0;
-    S.m_ok[i] = o.stable;
-    if (o.stable) {
-      S.m_wt[i] = weight(o, a.d.layer_count[op]);
-      S.m_soj[i] = o.wait + o.service;
+    S.m_ok[i] = o.ok;
+    if (o.ok) {
+      S.m_wt[i] = o.wt;
+      S.m_soj[i] = o.soj;
       S.m_lat[i] = trial_latency(S, a.d, S.wt, op, S.m_wt[i], S.cpv_ok);
     }
     if (st) atomicOr(&S.st, st);
@@ -353,7 +370,7 @@ __device__ __forceinline__ int objective_warp(const GShared& S, int n) {
 // warp 0: apply move m of `op` (new r; lane 0 updates the config and the
 // move's weight / sojourn -- from the scratch when its chunk is the last one
 // evaluated, else recomputed, same bits) and the path (set_path_warp)
-__device__ __noinline__ void apply_move_warp(GShared& S, const GreedyArgs& a, int op, int m, int r_new, int b_lo,
+__device__ __noinline__ void apply_move_warp(GShared& S, const GreedyArgs& a, int w, int op, int m, int r_new, int b_lo,
                                              int m0, double qps, int L, int ph) {
   if ((threadIdx.x & 31) == 0) {
     const int np = S.np_d[op];
@@ -365,9 +382,9 @@ __device__ __noinline__ void apply_move_warp(GShared& S, const GreedyArgs& a, in
       S.soj[op] = S.m_soj[m - m0];
     } else {
       uint32_t st = 0;
-      const Pred o = gpredict(a.d, qps, L, ph, op, S.p[op], r_new, S.b[op], &st);
-      S.wt[op] = weight(o, a.d.layer_count[op]);
-      S.soj[op] = o.wait + o.service;
+      const GPt o = gpoint(a, w, qps, L, ph, op, S.p[op], r_new, S.b[op], &st);
+      S.wt[op] = o.wt;
+      S.soj[op] = o.soj;
     }
     S.stable = 1;
   }
@@ -397,9 +414,16 @@ __device__ __noinline__ void upscale_step(GShared& S, const GreedyArgs& a, const
   PK k[3];  // ach, ach2, imp
   for (int i = 0; i < 3; ++i) k[i] = pk_none();
   int M = 0, m0 = 0;
+#ifdef OPSC_GREEDY_PROF
+  const long long u0 = clock64();
+  long long u1 = 0;
+#endif
   do {
     if (m0 > 0) __syncthreads();  // previous chunk's scratch fully read
-    M = eval_moves(S, a, op, cur_r + 1, 1, qps, L, ph, m0);
+    M = eval_moves(S, a, w, op, cur_r + 1, 1, qps, L, ph, m0);
+#ifdef OPSC_GREEDY_PROF
+    u1 = clock64();
+#endif
   for (int m = m0 + threadIdx.x; m < min(M, m0 + kMaxMoves); m += blockDim.x) {
     if (!S.m_ok[m - m0]) continue;
     const int b = 1 + m / np, p = S.pd[op][m % np];
@@ -419,13 +443,19 @@ __device__ __noinline__ void upscale_step(GShared& S, const GreedyArgs& a, const
     m0 += kMaxMoves;
   } while (m0 < M);
   m0 -= kMaxMoves;  // the chunk still in the scratch
+#ifdef OPSC_GREEDY_PROF
+  const long long u2 = clock64();
+#endif
   block_min<3>(k);
+#ifdef OPSC_GREEDY_PROF
+  const long long u3 = clock64();
+#endif
   if (threadIdx.x < 32) {  // warp 0 applies the pick (every thread holds the same minima)
     const PK& pick = pk_valid(k[0]) ? k[0] : (!headroom && pk_valid(k[1])) ? k[1] : k[2];
     const int m = pk_valid(pick) ? move_index(S, op, 1, pk_b(pick), pk_p(pick)) : -1;
     if (threadIdx.x == 0) S.applied = m >= 0;
     if (m >= 0) {
-      apply_move_warp(S, a, op, m, cur_r + 1, 1, m0, qps, L, ph);
+      apply_move_warp(S, a, w, op, m, cur_r + 1, 1, m0, qps, L, ph);
       const int obj = objective_warp(S, a.d.n_ops);
       if (threadIdx.x == 0)
         push_trace(S, out, w, headroom ? OPSC_ACT_HEADROOM : OPSC_ACT_UPSCALE, op, S.r[op], S.b[op], S.p[op],
@@ -433,6 +463,11 @@ __device__ __noinline__ void upscale_step(GShared& S, const GreedyArgs& a, const
     }
   }
   __syncthreads();
+#ifdef OPSC_GREEDY_PROF
+  if (threadIdx.x == 0)
+    printf("  up step op %d r %d M %d: eval %lld keys %lld reduce %lld apply %lld cycles\n", op, cur_r + 1, M,
+           u1 - u0, u2 - u1, u3 - u2, clock64() - u3);
+#endif
 }
 
 // Downscale (autoscaler.py:456-486): the cheapest (objective, B, P) move at
@@ -455,7 +490,7 @@ __device__ __noinline__ void downscale_step(GShared& S, const GreedyArgs& a, con
   int M = 0, m0 = 0;
   do {
     if (m0 > 0) __syncthreads();  // previous chunk's scratch fully read
-    M = eval_moves(S, a, op, cur_r - 1, cur_b, qps, L, ph, m0);
+    M = eval_moves(S, a, w, op, cur_r - 1, cur_b, qps, L, ph, m0);
     for (int m = m0 + threadIdx.x; m < min(M, m0 + kMaxMoves); m += blockDim.x) {
       if (!S.m_ok[m - m0] || S.m_lat[m - m0] > bound) continue;
       const int b = cur_b + m / np, p = S.pd[op][m % np];
@@ -472,7 +507,7 @@ __device__ __noinline__ void downscale_step(GShared& S, const GreedyArgs& a, con
     const int best = pk_valid(k[0]) ? move_index(S, op, cur_b, pk_b(k[0]), pk_p(k[0])) : -1;
     if (threadIdx.x == 0) S.applied = best >= 0;
     if (best >= 0) {
-      apply_move_warp(S, a, op, best, cur_r - 1, cur_b, m0, qps, L, ph);
+      apply_move_warp(S, a, w, op, best, cur_r - 1, cur_b, m0, qps, L, ph);
       const int obj = objective_warp(S, a.d.n_ops);
       if (threadIdx.x == 0)
         push_trace(S, out, w, OPSC_ACT_DOWNSCALE, op, S.r[op], S.b[op], S.p[op], S.lat, obj);
@@ -514,11 +549,11 @@ __device__ __noinline__ void prune_pass(GShared& S, const GreedyArgs& a, const O
     for (int v = threadIdx.x; v < d.n_ops; v += blockDim.x) {
       if (!t_need[v] || S.r[v] <= 1) continue;
       uint32_t st = 0;
-      const Pred o = gpredict(d, qps, L, ph, v, S.p[v], S.r[v] - 1, S.b[v], &st);
+      const GPt o = gpoint(a, w, qps, L, ph, v, S.p[v], S.r[v] - 1, S.b[v], &st);
       if (st) atomicOr(&S.st, st);
-      t_ok[v] = o.stable;
-      t_wt[v] = weight(o, d.layer_count[v]);
-      t_soj[v] = o.wait + o.service;
+      t_ok[v] = o.ok;
+      t_wt[v] = o.wt;
+      t_soj[v] = o.soj;
       t_need[v] = 0;
     }
     __syncthreads();
@@ -652,6 +687,9 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
   }
   __syncthreads();
 
+#ifdef OPSC_GREEDY_PROF
+  const long long t_init0 = clock64();
+#endif
   // ---- init_configs (:254-294): per parallelism rank, (op, B) pairs in parallel
   int max_np = 0;
   for (int v = 0; v < n; ++v) max_np = max(max_np, a.s.n_p[v]);
@@ -662,7 +700,10 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
     for (int b0 = 0; b0 < max_b; b0 += kInitChunk) {
     __syncthreads();
     for (int k = threadIdx.x; k < n * kInitChunk; k += blockDim.x) {
-      const int v = k / kInitChunk, b = b0 + k % kInitChunk + 1;
+      // B-major: a round of threads covers a few B values of every operator,
+      // so the long Erlang chains of small B (R ~ qps T_B / B) share rounds
+      // instead of setting every round's length
+      const int v = k % n, b = b0 + k / n + 1;
       if (S.chosen[v] || pi >= a.s.n_p[v] || b > a.s.b_max[v]) continue;
       const int p = a.s.p_vals[v][pi];
       const double t = op_latency(d, ph, v, b, L, p);
@@ -682,18 +723,49 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
       if (st) atomicOr(&S.st, st);
     }
     __syncthreads();
-    // running argmin over the chunks: min sojourn, ties to the lowest B (strict <, ascending B)
-    for (int v = threadIdx.x; v < n; v += blockDim.x) {
+    // running argmin over the chunks: min sojourn, ties to the lowest B
+    // (the reference's strict '<' over ascending B), one warp per operator:
+    // lanes reduce the chunk's (sojourn, B) minimum over the non-NaN entries;
+    // a chunk whose first valid entry is NaN (which the strict scan would keep
+    // when nothing precedes it) goes through the literal scan
+    for (int v = threadIdx.x >> 5; v < n; v += blockDim.x >> 5) {
       if (S.chosen[v] || pi >= a.s.n_p[v]) continue;
-      for (int b = b0 + 1; b <= min(a.s.b_max[v], b0 + kInitChunk); ++b) {
+      const int lane = threadIdx.x & 31;
+      const int bend = min(a.s.b_max[v], b0 + kInitChunk);
+      int fv = 0x7fffffff, bb = 0x7fffffff;
+      double bs = 0.0;
+      for (int b = b0 + 1 + lane; b <= bend; b += 32) {
         const int j = b - b0 - 1;
         if (S.i_r[v][j] < 0) continue;
-        if (S.i_bb[v] < 0 || S.i_soj[v][j] < S.i_bs[v]) {
-          S.i_bb[v] = b;
-          S.i_bs[v] = S.i_soj[v][j];
-          S.i_br[v] = S.i_r[v][j];
-        }
+        fv = min(fv, b);
+        const double x = S.i_soj[v][j];
+        if (x == x && (bb == 0x7fffffff || x < bs || (x == bs && b < bb))) { bs = x; bb = b; }
       }
+      fv = __reduce_min_sync(0xffffffffu, fv);
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ox = __shfl_xor_sync(0xffffffffu, bs, o);
+        const int ob = __shfl_xor_sync(0xffffffffu, bb, o);
+        if (ob != 0x7fffffff && (bb == 0x7fffffff || ox < bs || (ox == bs && ob < bb))) { bs = ox; bb = ob; }
+      }
+      if (lane == 0 && fv != 0x7fffffff) {  // (no valid entry in this chunk: nothing to do)
+      const double first = S.i_soj[v][fv - b0 - 1];
+      if (first != first || S.i_bs[v] != S.i_bs[v]) {  // NaN in play: the literal scan
+        for (int b = b0 + 1; b <= bend; ++b) {
+          const int j = b - b0 - 1;
+          if (S.i_r[v][j] < 0) continue;
+          if (S.i_bb[v] < 0 || S.i_soj[v][j] < S.i_bs[v]) {
+            S.i_bb[v] = b;
+            S.i_bs[v] = S.i_soj[v][j];
+            S.i_br[v] = S.i_r[v][j];
+          }
+        }
+      } else if (bb != 0x7fffffff && (S.i_bb[v] < 0 || bs < S.i_bs[v])) {
+        S.i_bb[v] = bb;
+        S.i_bs[v] = bs;
+        S.i_br[v] = S.i_r[v][bb - b0 - 1];
+      }
+      }
+      __syncwarp();
     }
     }
     __syncthreads();
@@ -720,8 +792,19 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
       out.status[w] |= S.st | OPSC_W_NO_STABLE_INIT | ((uint32_t)S.flag << OPSC_W_INIT_OP_SHIFT);
     return;
   }
-  eval_full(S, d, qps, L, ph);
+#ifdef OPSC_GREEDY_PROF
+  const long long t_init1 = clock64();
+#endif
+  eval_full(S, a, w, qps, L, ph);
+#ifdef OPSC_GREEDY_PROF
+  const long long t_eval1 = clock64();
+#endif
   greedy_loop(S, a, out, w, qps, L, ph, slo, eps);
+#ifdef OPSC_GREEDY_PROF
+  if (threadIdx.x == 0)  // dev build only (tools): cycles of init / first evaluation / loop
+    printf("greedy w%d phase %d: init %lld eval %lld loop %lld cycles, trace %d\n", w, phase, t_init1 - t_init0,
+           t_eval1 - t_init1, clock64() - t_eval1, S.trace_len);
+#endif
   if (phase == 1) {
     if (threadIdx.x == 0) {
       GSave& g = save[w];
@@ -766,7 +849,7 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
     }
     __syncthreads();
     if (reseed) {
-      eval_full(S, d, qps, L, ph);
+      eval_full(S, a, w, qps, L, ph);
       prune_pass(S, a, out, w, qps, L, ph, slo - eps);
       greedy_loop(S, a, out, w, qps, L, ph, slo, eps);
       if (threadIdx.x == 0 && !(objective(S, n) < base_obj)) {
