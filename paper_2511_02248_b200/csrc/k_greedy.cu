@@ -628,11 +628,29 @@ __device__ void distinct_p(GShared& S, const GreedyArgs& a, int n) {
 
 // phase 0: whole planner; phase 1: init_configs + first greedy loop, state
 // saved; phase 2: state loaded, uniform reseed, headroom, prune, outputs.
+// The DAG and spec tables are read per operator by lane-varying indices
+// (init pairs, the path update, the prune sweep): from the kernel's parameter
+// (constant) bank every such load serialises over the distinct addresses of a
+// warp, so the CTA first copies them to shared memory (16-byte words).
+constexpr size_t kGreedyArgsWords = (sizeof(GreedyArgs) + 15) / 16;
+
 __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
-    const __grid_constant__ GreedyArgs a, const __grid_constant__ OpscWindows win,
+    const __grid_constant__ GreedyArgs ga, const __grid_constant__ OpscWindows win,
     const int16_t* __restrict__ ucfg, const uint8_t* __restrict__ ufeas, const uint32_t* __restrict__ ustatus,
     const __grid_constant__ OpscDecisions out, int phase, GSave* __restrict__ save) {
   __shared__ GShared S;
+  extern __shared__ __align__(16) unsigned char g_args[];
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(&ga);
+    uint4* dst = reinterpret_cast<uint4*>(g_args);
+    for (int i = threadIdx.x; i < (int)(sizeof(GreedyArgs) / 16); i += blockDim.x) dst[i] = src[i];
+    if (threadIdx.x == 0 && sizeof(GreedyArgs) % 16) {
+      const unsigned char* sb = reinterpret_cast<const unsigned char*>(&ga);
+      for (size_t k = sizeof(GreedyArgs) / 16 * 16; k < sizeof(GreedyArgs); ++k) g_args[k] = sb[k];
+    }
+    __syncthreads();
+  }
+  const GreedyArgs& a = *reinterpret_cast<const GreedyArgs*>(g_args);
   const OpscDag& d = a.d;
   const int n = d.n_ops;
   const int w = blockIdx.x;
@@ -901,7 +919,16 @@ cudaError_t launch_greedy(const OpscDag& d, const OpscGreedySpec& s, OpscWindows
   GreedyArgs a;
   a.d = d;
   a.s = s;
-  greedy_kernel<<<w.n, kGreedyThreads, 0, st>>>(a, w, ucfg, ufeas, ustatus, out, phase, (GSave*)save);
+  const size_t dyn = kGreedyArgsWords * 16;
+  static int set_dyn[64];  // raise the dynamic limit once per device (static GShared + args pass 48 KB)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !set_dyn[dev]) {
+    const cudaError_t e = cudaFuncSetAttribute(greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return e;
+    set_dyn[dev] = 1;
+  }
+  greedy_kernel<<<w.n, kGreedyThreads, dyn, st>>>(a, w, ucfg, ufeas, ustatus, out, phase, (GSave*)save);
   return cudaGetLastError();
 }
 
