@@ -187,7 +187,7 @@ __device__ __forceinline__ GPt gpoint(const GreedyArgs& a, int w, double qps, in
   return GPt{weight(o, a.d.layer_count[v]), o.wait + o.service, o.stable};
 }
 
-__device__ __noinline__ void set_path_warp(GShared& S, const OpscDag& d);
+__device__ __forceinline__ void set_path_warp(GShared& S, const OpscDag& d);
 
 // full evaluation of the current configs (all threads; ends synchronised)
 __device__ __noinline__ void eval_full(GShared& S, const GreedyArgs& a, int w, double qps, int L, int ph) {
@@ -321,7 +321,7 @@ __device__ void block_min(PK (&x)[NK]) {
 // right in every lane (lane i keeps the DP value of position i), the
 // bottleneck as a warp (sojourn, -id) max (literal scan if a sojourn is
 // NaN), the non-negativity check as a vote. Same values as set_path.
-__device__ __noinline__ void set_path_warp(GShared& S, const OpscDag& d) {
+__device__ __forceinline__ void set_path_warp(GShared& S, const OpscDag& d) {
   const int lane = threadIdx.x & 31, n = d.n_ops;
   if (S.chain) {
     const int u = lane < n ? d.topo[lane] : 0;
@@ -370,7 +370,7 @@ __device__ __forceinline__ int objective_warp(const GShared& S, int n) {
 // warp 0: apply move m of `op` (new r; lane 0 updates the config and the
 // move's weight / sojourn -- from the scratch when its chunk is the last one
 // evaluated, else recomputed, same bits) and the path (set_path_warp)
-__device__ __noinline__ void apply_move_warp(GShared& S, const GreedyArgs& a, int w, int op, int m, int r_new, int b_lo,
+__device__ __forceinline__ void apply_move_warp(GShared& S, const GreedyArgs& a, int w, int op, int m, int r_new, int b_lo,
                                              int m0, double qps, int L, int ph) {
   if ((threadIdx.x & 31) == 0) {
     const int np = S.np_d[op];
