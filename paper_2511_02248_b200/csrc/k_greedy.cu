@@ -24,11 +24,13 @@
 namespace opsc {
 
 #ifndef OPSC_GREEDY_THREADS
-#define OPSC_GREEDY_THREADS 128
+#define OPSC_GREEDY_THREADS 256  // 128 evaluate and commit a move, the other 128 speculate the next move set
 #endif
 constexpr int kGreedyThreads = OPSC_GREEDY_THREADS;
 constexpr int kMaxMoves = 32 * OPSC_MAX_P * 2;  // move-set chunk (larger sets run in chunks)
 constexpr int kInitChunk = 64;                   // init_configs B chunk per operator
+constexpr int kSpecBase = 128;                   // threads from here on evaluate the next move set
+constexpr int kSpecMoves = 128;                  // largest speculated move set
 
 struct GreedyArgs {
   OpscDag d;
@@ -62,6 +64,12 @@ struct GShared {
   int8_t tpos[OPSC_MAX_OPS];     // topological position of every op
   int cpv_ok;                    // cpv matches wt and every weight is >= 0 (trial_latency prefix)
   int chain;                     // the DAG is one path (each op feeds the next in topological order)
+  // speculated next move set (predict_op of (n_op, P, n_r, B >= n_blo), a pure
+  // function of its key, so it is valid whenever the key matches)
+  double n_wt[kSpecMoves], n_soj[kSpecMoves];
+  uint8_t n_ok[kSpecMoves];
+  int n_op, n_r, n_blo, n_M, n_valid;
+  uint32_t n_st;                 // status bits of the speculated points, ORed in when consumed
 };
 
 
@@ -229,10 +237,12 @@ __device__ __noinline__ int eval_moves(GShared& S, const GreedyArgs& a, int w, i
   const int nb = a.s.b_max[op] - b_lo + 1;
   const int M = nb * np;
   const int m1 = min(M, m0 + kMaxMoves);
+  // the previous step speculated this very move set: its predict_op values
+  const bool spec = m0 == 0 && S.n_valid && S.n_op == op && S.n_r == r_new && S.n_blo == b_lo && S.n_M == M;
   for (int m = m0 + threadIdx.x; m < m1; m += blockDim.x) {
     const int b = b_lo + m / np, p = S.pd[op][m % np];
     uint32_t st = 0;
-    const GPt o = gpoint(a, w, qps, L, ph, op, p, r_new, b, &st);
+    const GPt o = spec ? GPt{S.n_wt[m], S.n_soj[m], S.n_ok[m] != 0} : gpoint(a, w, qps, L, ph, op, p, r_new, b, &st);
     const int i = m - m0;
     S.m_ok[i] = o.ok;
     if (o.ok) {
@@ -243,7 +253,70 @@ __device__ __noinline__ int eval_moves(GShared& S, const GreedyArgs& a, int w, i
     if (st) atomicOr(&S.st, st);
   }
   __syncthreads();
+  if (threadIdx.x == 0 && m0 == 0) {  // consumed or superseded (the next speculation starts after block_min)
+    if (spec) S.st |= S.n_st;
+    S.n_valid = 0;
+    S.n_st = 0;
+  }
   return M;
+}
+
+// After a step's pick is known (all threads agree on it) and before warp 0
+// commits it: on a chain whose weights are >= 0 the next step is determined
+// already -- the new latency is the pick's trial latency (the critical path of
+// a chain is the whole chain, and the clamped trial DP equals it for weights
+// >= 0) and the next bottleneck is the argmax of the sojourns with the moved
+// operator's replaced -- so threads >= kSpecBase evaluate that move set while
+// warp 0 commits. A wrong guess only costs the work: the next step uses the
+// values only if its (op, R, B_lo) key matches.
+__device__ void speculate_next(GShared& S, const GreedyArgs& a, int w, double qps, int L, int ph, int op, int r_new,
+                               int b_new, double soj_new, double wt_new, double lat_new, double slo, double eps,
+                               bool headroom, bool cpv_ok0) {
+  // cpv_ok0: S.cpv_ok read at the start of the step (warp 0 rewrites it while this runs)
+  if ((int)threadIdx.x < kSpecBase || !S.chain || !cpv_ok0 || !(wt_new >= 0.0)) return;
+  const int n = a.d.n_ops;
+  const bool up = headroom ? lat_new > slo - eps : lat_new > slo;
+  const bool down = !headroom && !up && lat_new <= slo - eps;
+  if (!up && !down) return;
+  int v = -1;  // bottleneck(): the path of a chain is every op in topological order
+  double sv = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const int u = a.d.topo[i];
+    const double su = u == op ? soj_new : S.soj[u];
+    if (v < 0 || su > sv || (su == sv && u < v)) {
+      v = u;
+      sv = su;
+    }
+  }
+  const int rv = v == op ? r_new : S.r[v], bv = v == op ? b_new : S.b[v];
+  int nr, nblo;
+  if (up) {
+    if (rv + 1 > a.s.r_cap) return;
+    nr = rv + 1;
+    nblo = 1;
+  } else {
+    if (rv - 1 < 1) return;
+    nr = rv - 1;
+    nblo = bv;
+  }
+  const int np = S.np_d[v];
+  const int M = (a.s.b_max[v] - nblo + 1) * np;
+  if (M > kSpecMoves || M < 1) return;
+  uint32_t st = 0;
+  for (int m = (int)threadIdx.x - kSpecBase; m < M; m += (int)blockDim.x - kSpecBase) {
+    const GPt o = gpoint(a, w, qps, L, ph, v, S.pd[v][m % np], nr, nblo + m / np, &st);
+    S.n_wt[m] = o.wt;
+    S.n_soj[m] = o.soj;
+    S.n_ok[m] = o.ok;
+  }
+  if (st) atomicOr(&S.n_st, st);
+  if ((int)threadIdx.x == kSpecBase) {
+    S.n_op = v;
+    S.n_r = nr;
+    S.n_blo = nblo;
+    S.n_M = M;
+    S.n_valid = 1;
+  }
 }
 
 // A move's selection key (k0, k1, k2, B, P) for one of the reference's
@@ -411,6 +484,7 @@ __device__ __noinline__ void upscale_step(GShared& S, const GreedyArgs& a, const
   const int np = S.np_d[op];
   const int base = objective_warp(S, a.d.n_ops);  // every warp: one add-reduction
   const double target = slo - eps, cur_lat = S.lat;
+  const bool cpv_ok0 = S.cpv_ok;
   PK k[3];  // ach, ach2, imp
   for (int i = 0; i < 3; ++i) k[i] = pk_none();
   int M = 0, m0 = 0;
@@ -450,6 +524,15 @@ __device__ __noinline__ void upscale_step(GShared& S, const GreedyArgs& a, const
 #ifdef OPSC_GREEDY_PROF
   const long long u3 = clock64();
 #endif
+  if ((int)threadIdx.x >= kSpecBase) {  // the next move set, while warp 0 commits this one
+    const PK& pick = pk_valid(k[0]) ? k[0] : (!headroom && pk_valid(k[1])) ? k[1] : k[2];
+    if (pk_valid(pick) && m0 == 0) {
+      const int i = move_index(S, op, 1, pk_b(pick), pk_p(pick));
+      if (i < kMaxMoves)
+        speculate_next(S, a, w, qps, L, ph, op, cur_r + 1, pk_b(pick), S.m_soj[i], S.m_wt[i], S.m_lat[i], slo, eps,
+                       headroom, cpv_ok0);
+    }
+  }
   if (threadIdx.x < 32) {  // warp 0 applies the pick (every thread holds the same minima)
     const PK& pick = pk_valid(k[0]) ? k[0] : (!headroom && pk_valid(k[1])) ? k[1] : k[2];
     const int m = pk_valid(pick) ? move_index(S, op, 1, pk_b(pick), pk_p(pick)) : -1;
@@ -485,6 +568,7 @@ __device__ __noinline__ void downscale_step(GShared& S, const GreedyArgs& a, con
   const int np = S.np_d[op];
   const int base = objective_warp(S, a.d.n_ops);  // every warp: one add-reduction
   const double bound = slo - eps;
+  const bool cpv_ok0 = S.cpv_ok;
   PK k[1];
   k[0] = pk_none();
   int M = 0, m0 = 0;
@@ -503,6 +587,12 @@ __device__ __noinline__ void downscale_step(GShared& S, const GreedyArgs& a, con
   } while (m0 < M);
   m0 -= kMaxMoves;
   block_min<1>(k);
+  if ((int)threadIdx.x >= kSpecBase && pk_valid(k[0]) && m0 == 0) {
+    const int i = move_index(S, op, cur_b, pk_b(k[0]), pk_p(k[0]));
+    if (i < kMaxMoves)
+      speculate_next(S, a, w, qps, L, ph, op, cur_r - 1, pk_b(k[0]), S.m_soj[i], S.m_wt[i], S.m_lat[i], slo, eps,
+                     false, cpv_ok0);
+  }
   if (threadIdx.x < 32) {
     const int best = pk_valid(k[0]) ? move_index(S, op, cur_b, pk_b(k[0]), pk_p(k[0])) : -1;
     if (threadIdx.x == 0) S.applied = best >= 0;
@@ -675,6 +765,8 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
       S.cpv_ok = 0;
       for (int i = 0; i < n; ++i) S.tpos[d.topo[i]] = (int8_t)i;
       S.chain = is_chain(d);
+      S.n_valid = 0;
+      S.n_st = 0;
     }
     __syncthreads();
     if (!S.flag) return;
@@ -702,6 +794,8 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
     S.trace_len = 0;
     S.cpv_ok = 0;
     S.chain = is_chain(d);
+    S.n_valid = 0;
+    S.n_st = 0;
   }
   __syncthreads();
 
