@@ -88,16 +88,43 @@ __global__ void wz_nwin(WzWork w, double len, int max_w, int32_t* n_windows) {
   *n_windows = (int32_t)n;
 }
 
+// exact sum (mod 2^64, as the u64 atomics) of x over the lanes of `grp`:
+// four 16-bit slices, each slice sum < 2^21
+__device__ __forceinline__ unsigned long long group_sum_u64(unsigned grp, unsigned long long x) {
+  unsigned long long s = 0;
+#pragma unroll
+  for (int sh = 0; sh < 64; sh += 16)
+    s += (unsigned long long)__reduce_add_sync(grp, (unsigned)((x >> sh) & 0xffffull)) << sh;
+  return s;
+}
+
+// Records of a trace arrive (nearly) in time order, so the lanes of a warp
+// mostly share a window: lanes are grouped by window (__match_any_sync) and
+// one leader per group adds the group's count and output-token sum -- integer
+// sums, so the totals are the same in any grouping (no same-address atomic
+// storm on a handful of window counters).
 __global__ void wz_count(OpscTraceRecords rec, double len, WzWork w, const int32_t* __restrict__ n_windows) {
   if (*w.err) return;
   const long long n = *n_windows;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < rec.n;
-       i += (long long)gridDim.x * blockDim.x) {
-    long long k = (long long)(rec.arrival[i] / len);  // int() truncates (t >= 0)
-    if (k > n - 1) k = n - 1;
-    w.widx[i] = (uint32_t)k;
-    atomicAdd(&w.counts[k], 1u);
-    atomicAdd(&w.sums[k], (unsigned long long)rec.output_len[i]);
+  const int lane = threadIdx.x & 31;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < rec.n; base += stride) {
+    const long long i = base + threadIdx.x;  // whole warps iterate together
+    uint32_t k = 0xffffffffu;
+    unsigned long long out = 0;
+    if (i < rec.n) {
+      long long kk = (long long)(rec.arrival[i] / len);  // int() truncates (t >= 0)
+      if (kk > n - 1) kk = n - 1;
+      k = (uint32_t)kk;
+      w.widx[i] = k;
+      out = (unsigned long long)rec.output_len[i];
+    }
+    const unsigned grp = __match_any_sync(0xffffffffu, k);
+    const unsigned long long sum = group_sum_u64(grp, out);
+    if (k != 0xffffffffu && lane == __ffs(grp) - 1) {
+      atomicAdd(&w.counts[k], (uint32_t)__popc(grp));
+      atomicAdd(&w.sums[k], sum);
+    }
   }
 }
 
@@ -128,13 +155,24 @@ __global__ void __launch_bounds__(1024) wz_scan(WzWork w, const int32_t* __restr
   if (threadIdx.x == 0) w.offsets[n] = carry;
 }
 
+// the same grouping: one cursor reservation per (warp, window), lanes take
+// consecutive slots (the order inside a window does not matter to the select)
 __global__ void wz_scatter(OpscTraceRecords rec, WzWork w) {
   if (*w.err) return;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < rec.n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const uint32_t k = w.widx[i];
-    const unsigned long long pos = w.offsets[k] + atomicAdd(&w.cursors[k], 1u);
-    w.grouped[pos] = (uint32_t)rec.input_len[i];
+  const int lane = threadIdx.x & 31;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long base = (long long)blockIdx.x * blockDim.x; base < rec.n; base += stride) {
+    const long long i = base + threadIdx.x;
+    const uint32_t k = i < rec.n ? w.widx[i] : 0xffffffffu;
+    const unsigned grp = __match_any_sync(0xffffffffu, k);
+    const int leader = __ffs(grp) - 1;
+    uint32_t at = 0;
+    if (k != 0xffffffffu && lane == leader) at = atomicAdd(&w.cursors[k], (uint32_t)__popc(grp));
+    at = __shfl_sync(grp, at, leader);
+    if (k != 0xffffffffu) {
+      const uint32_t rank = (uint32_t)__popc(grp & ((1u << lane) - 1u));
+      w.grouped[w.offsets[k] + at + rank] = (uint32_t)rec.input_len[i];
+    }
   }
 }
 
@@ -144,6 +182,7 @@ __global__ void __launch_bounds__(256) wz_select(WzWork w, double len, double q,
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t s_prefix, s_mask;
   __shared__ long long s_k;
+  __shared__ unsigned long long s_wsum[8];
   if (*w.err) return;
   const int win = blockIdx.x;
   if (win >= *n_windows) return;
@@ -175,19 +214,41 @@ __global__ void __launch_bounds__(256) wz_select(WzWork w, double len, double q,
       if ((v & mask) == prefix) atomicAdd(&hist[(v >> shifts[pass]) & (uint32_t)(nb - 1)], 1u);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      long long k = s_k, cum = 0;
-      int sel = nb - 1;
-      for (int b = 0; b < nb; ++b) {
-        if (cum + hist[b] > k) {
-          sel = b;
-          break;
-        }
-        cum += hist[b];
+    // the bin holding the k-th value: each thread sums a run of nb / 256 bins,
+    // a block scan of the run sums finds the run, its thread walks the run
+    {
+      const int per = nb / (int)blockDim.x;  // 8 or 4 bins
+      const int b0 = threadIdx.x * per;
+      unsigned long long run = 0;
+      for (int b = 0; b < per; ++b) run += hist[b0 + b];
+      unsigned long long incl = run;  // inclusive scan over the block (warp shuffles + warp totals)
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
       }
-      s_k = k - cum;
-      s_prefix = prefix | ((uint32_t)sel << shifts[pass]);
-      s_mask = mask | ((uint32_t)(nb - 1) << shifts[pass]);
+      if (lane == 31) s_wsum[wid] = incl;
+      __syncthreads();
+      unsigned long long before = 0;
+      for (int j = 0; j < wid; ++j) before += s_wsum[j];
+      incl += before;
+      const unsigned long long excl = incl - run;
+      const long long k = s_k;
+      __syncthreads();  // everyone has read s_k
+      if ((long long)excl <= k && k < (long long)incl) {  // exactly one run holds the k-th value
+        unsigned long long cum = excl;
+        int sel = b0 + per - 1;
+        for (int b = 0; b < per; ++b) {
+          if ((long long)(cum + hist[b0 + b]) > k) {
+            sel = b0 + b;
+            break;
+          }
+          cum += hist[b0 + b];
+        }
+        s_k = k - (long long)cum;
+        s_prefix = prefix | ((uint32_t)sel << shifts[pass]);
+        s_mask = mask | ((uint32_t)(nb - 1) << shifts[pass]);
+      }
     }
     __syncthreads();
   }
