@@ -16,12 +16,15 @@
 // (:338-351, best score, ties to the lowest device id) and commits.
 // Sums the reference takes with Python's sum() use CPython 3.12's Neumaier
 // summation (PySum), in the reference's iteration order.
+#include <cstdio>
+
 #include "opsc_common.cuh"
 
 namespace opsc {
 
 constexpr int kPlaceThreads = 128;
 constexpr int kMaxDevProbe = 128;  // device probes per chunk held in smem
+constexpr int kMaxMembers = 256;   // members of one device refreshed by a warp (more: lane 0 alone)
 constexpr size_t kPlaceSmemMax = 200 * 1024;  // static PShared + per-window workspace
 
 struct PlaceArgs {
@@ -49,6 +52,13 @@ struct PWork {  // per-window workspace (shared memory when it fits, else global
   double* dev_mem_c;
   int32_t* rep;  // [sum R] assignment index per (op, replica), -1 unplaced
 };
+
+// per-window global store of the stage-2 probe results (t_eff, wait,
+// weight, stable) of every (device, operator) pair: after a commit the chosen
+// device's entries ARE the operators' new figures (same factors, same sums)
+__host__ __device__ inline size_t probe_bytes(int D, int n) {
+  return (((size_t)D * n * (8 + 8 + 8 + 1)) + 15) & ~(size_t)15;
+}
 
 __host__ __device__ inline size_t pw_bytes(int A, int D, int n) {
   (void)n;
@@ -199,6 +209,13 @@ struct PShared {
   uint8_t dev_ok[kMaxDevProbe];
   double probe_wt[kMaxDevProbe][OPSC_MAX_OPS];
   double dev_score[kMaxDevProbe];   // weighted slack of each admissible device
+  int ord[kMaxMembers];             // refresh_device_warp: the device's members in list order
+  uint8_t ofirst[kMaxMembers];      // ... first occurrence of its group
+  int nord;
+  double ototal;
+#ifdef OPSC_PLACE_PROF
+  long long prof[6];
+#endif
   double red_score[kPlaceThreads / 32];
   int red_dj[kPlaceThreads / 32];
   int used, na, err, best;
@@ -231,7 +248,12 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
   // the window's assignment lists / device tables are walked by every probe:
   // in shared memory when they fit (smem_ws), else in its global slice
   // (SMEM: a compile-time choice, so the walks compile to shared-memory loads)
-  PWork P = carve(SMEM ? pw_smem : ws + (size_t)w * pw_bytes(A, D, n), A, D);
+  unsigned char* wbase = ws + (size_t)w * (pw_bytes(A, D, n) + probe_bytes(D, n));
+  PWork P = carve(SMEM ? pw_smem : wbase, A, D);
+  double* p_teff = reinterpret_cast<double*>(wbase + pw_bytes(A, D, n));
+  double* p_wait = p_teff + (size_t)D * n;
+  double* p_wt = p_wait + (size_t)D * n;
+  uint8_t* p_ok = reinterpret_cast<uint8_t*>(p_wt + (size_t)D * n);
   const int32_t* adev = P.a_dev;
   if (threadIdx.x == 0) {
     S.rep_off[0] = 0;
@@ -242,6 +264,9 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
       S.rep_off[v + 1] = S.rep_off[v] + S.r[v];
     }
     S.err = S.rep_off[n] > A ? OPSC_W_TRACE_TRUNCATED : 0;
+#ifdef OPSC_PLACE_PROF
+    for (int q = 0; q < 6; ++q) S.prof[q] = 0;
+#endif
     S.used = 0;
     S.na = 0;
   }
@@ -319,6 +344,54 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
     for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) P.a_fac[i] = member_factor(P, f, dev, i, -1, 0.0, total);
   };
 
+  // the same refresh by warp 0 after a commit: the device's member list as an
+  // array, each lane one member's group maximum and first-occurrence flag,
+  // lane 0 the load sum in list order (the serial PySum), lanes the factors
+  auto refresh_device_warp = [&](int dev) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) {
+      int m = 0, i = P.dev_head[dev];
+      for (; i >= 0 && m < kMaxMembers; i = P.a_next[i]) S.ord[m++] = i;
+      S.nord = i >= 0 ? -1 : m;
+      if (i >= 0) refresh_device(dev);  // more members than the array holds
+    }
+    __syncwarp();
+    const int m = S.nord;
+    if (m < 0) return;
+    for (int x = lane; x < m; x += 32) {
+      const int i = S.ord[x], g = P.a_group[i];
+      double gm = 0.0;
+      bool first = true;
+      for (int y = 0; y < m; ++y) {
+        const int j = S.ord[y];
+        if (P.a_group[j] == g) {
+          gm = gm >= P.a_dem[j] ? gm : P.a_dem[j];
+          first &= y >= x;
+        }
+      }
+      P.a_gmax[i] = gm;
+      S.ofirst[x] = first;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      PySum t;
+      t.reset();
+      for (int x = 0; x < m; ++x)
+        if (S.ofirst[x]) t.add(P.a_gmax[S.ord[x]]);
+      P.dev_lf[dev] = t.f;
+      P.dev_lc[dev] = t.c;
+      P.dev_ls[dev] = t.started ? 1 : 0;
+      S.ototal = t.value();
+    }
+    __syncwarp();
+    const double total = S.ototal;
+    for (int x = lane; x < m; x += 32) {
+      const int i = S.ord[x];
+      P.a_fac[i] = member_factor(P, f, dev, i, -1, 0.0, total);
+    }
+    __syncwarp();
+  };
+
   // ---- base instances (placement.py:358-385), thread 0
   int k_base = 1 << 30;
   for (int v = 0; v < n; ++v) k_base = min(k_base, S.r[v]);
@@ -389,6 +462,9 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
       // (compute-sanitizer racecheck; a fleet with a multiple of kMaxDevProbe
       // used devices would otherwise split the CTA across __syncthreads).
       const int n_used = S.used;
+#ifdef OPSC_PLACE_PROF
+      long long q0 = clock64(), q1 = q0, q2 = q0, q3 = q0;
+#endif
       for (int c0 = 0; probe && c0 < n_used; c0 += kMaxDevProbe) {
       const int U = min(n_used - c0, kMaxDevProbe);
       // stage 1: per-device admission + tentative group totals
@@ -413,6 +489,9 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
         S.dev_ok[dj] = ok;
       }
       __syncthreads();
+#ifdef OPSC_PLACE_PROF
+      q1 = clock64();
+#endif
       // stage 2: (device, affected op) re-evaluations in parallel
       for (int t = threadIdx.x; t < U * n; t += blockDim.x) {
         const int dj = t / n, u = t - dj * n;
@@ -424,8 +503,16 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
         const OpAdj o = adjust_op(d, f, P, S.rep_off, adev, u, S.p[u], S.r[u], S.b[u], S.T[u], S.comm[u], qps,
                                   c0 + dj, group, demand, v, k, S.dev_xf[dj], S.dev_total[dj]);
         S.probe_wt[dj][u] = o.stable ? o.wt : OPSC_INF;
+        const size_t pi = (size_t)(c0 + dj) * n + u;
+        p_teff[pi] = o.t_eff;
+        p_wait[pi] = o.wait;
+        p_wt[pi] = o.wt;
+        p_ok[pi] = o.stable;
       }
       __syncthreads();
+#ifdef OPSC_PLACE_PROF
+      q2 = clock64();
+#endif
       // stage 3: recomputed latency must meet the SLO (placement.py:434-438),
       // and the weighted slack score of every admissible device (:338-351)
       bool nan_score = false;
@@ -487,39 +574,71 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
         __syncthreads();
       }
       }
-      if (threadIdx.x == 0) {
-        int best = s_best;
-        if (best >= 0) {
-          push(v, k, best, group, share);
-        } else if (S.used >= f.n_devices || S.used >= D) {
-          S.err = OPSC_W_FLEET_EXHAUSTED;
-        } else {
-          best = S.used++;
-          if (mem > f.mem_cap[best]) S.err = OPSC_W_INFEASIBLE_PLACEMENT;
-          else push(v, k, best, group, 100);
+#ifdef OPSC_PLACE_PROF
+      q3 = clock64();
+#endif
+      __shared__ int s_probed, s_fresh_same;
+      if (threadIdx.x < 32) {  // warp 0: lane 0 commits, the warp refreshes the device
+        if (threadIdx.x == 0) {
+          int best = s_best;
+          s_probed = best >= 0;
+          if (best >= 0) {
+            push(v, k, best, group, share);
+          } else if (S.used >= f.n_devices || S.used >= D) {
+            S.err = OPSC_W_FLEET_EXHAUSTED;
+          } else {
+            best = S.used++;
+            if (mem > f.mem_cap[best]) S.err = OPSC_W_INFEASIBLE_PLACEMENT;
+            else push(v, k, best, group, 100);
+          }
+          S.best = best;
         }
-        if (!S.err) refresh_device(best);
-        S.best = best;
+        __syncwarp();
+        if (!S.err) refresh_device_warp(S.best);
+        // a replica placed alone on a fresh device gets factor 1.0 -- exactly
+        // the factor its operator's figures already counted it with while it
+        // was unplaced (adjust_op), so those figures are unchanged
+        if (threadIdx.x == 0) s_fresh_same = !S.err && !s_probed && P.dev_cnt[S.best] == 1 && P.a_fac[S.na - 1] == 1.0;
       }
       __syncthreads();
       if (S.err) {
         if (threadIdx.x == 0) out.status[w] = S.err;
         return;
       }
+#ifdef OPSC_PLACE_PROF
+      const long long q4 = clock64();
+#endif
       // refresh the cached figures of ops with a replica on the chosen device
       {
         const int dev = S.best;
         const uint32_t mask = P.dev_mask[dev];
-        for (int u = threadIdx.x; u < n; u += blockDim.x) {
+        for (int u = threadIdx.x; u < n && !s_fresh_same; u += blockDim.x) {
           if (!(mask >> u & 1u)) continue;
+          if (s_probed) {  // the probe of this device computed exactly these figures
+            const size_t pi = (size_t)dev * n + u;
+            S.cur_wt[u] = p_wt[pi]; S.cur_teff[u] = p_teff[pi]; S.cur_wait[u] = p_wait[pi];
+            S.cur_stable[u] = p_ok[pi] != 0;
+            continue;
+          }
           const OpAdj o = adjust_op(d, f, P, S.rep_off, adev, u, S.p[u], S.r[u], S.b[u], S.T[u], S.comm[u], qps, -1,
                                     -1, 0.0, -1, 0, 1.0, 0.0);
           S.cur_wt[u] = o.wt; S.cur_teff[u] = o.t_eff; S.cur_wait[u] = o.wait; S.cur_stable[u] = o.stable;
         }
       }
       __syncthreads();
+#ifdef OPSC_PLACE_PROF
+      if (threadIdx.x == 0) {
+        S.prof[0] += q1 - q0; S.prof[1] += q2 - q1; S.prof[2] += q3 - q2; S.prof[3] += q4 - q3;
+        S.prof[4] += clock64() - q4; S.prof[5] += 1;
+      }
+#endif
     }
   }
+#ifdef OPSC_PLACE_PROF
+  if (threadIdx.x == 0 && w < 4)
+    printf("place w%d: %lld extras, stage1 %lld stage2 %lld stage3+score %lld commit %lld refresh %lld cycles\n", w,
+           S.prof[5], S.prof[0], S.prof[1], S.prof[2], S.prof[3], S.prof[4]);
+#endif
 
   // ---- _finalize + metrics (thread 0)
   if (threadIdx.x == 0) {
@@ -562,7 +681,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
 }
 
 size_t place_shared_workspace(int n_windows, int A, int D, int n) {
-  return (size_t)(n_windows > 0 ? n_windows : 1) * pw_bytes(A, D, n);
+  return (size_t)(n_windows > 0 ? n_windows : 1) * (pw_bytes(A, D, n) + probe_bytes(D, n));
 }
 
 cudaError_t launch_place_shared(const OpscDag& d, const OpscPlaceShared& f, OpscWindows w, const int16_t* cfg,
