@@ -24,13 +24,14 @@
 namespace opsc {
 
 #ifndef OPSC_GREEDY_THREADS
-#define OPSC_GREEDY_THREADS 256  // 128 evaluate and commit a move, the other 128 speculate the next move set
+#define OPSC_GREEDY_THREADS 384  // 128 evaluate and commit a move, 256 speculate the next move sets
 #endif
 constexpr int kGreedyThreads = OPSC_GREEDY_THREADS;
-constexpr int kMaxMoves = 32 * OPSC_MAX_P * 2;  // move-set chunk (larger sets run in chunks)
+constexpr int kMaxMoves = 256;                   // move-set chunk (larger sets run in chunks)
 constexpr int kInitChunk = 64;                   // init_configs B chunk per operator
-constexpr int kSpecBase = 128;                   // threads from here on evaluate the next move set
-constexpr int kSpecMoves = 128;                  // largest speculated move set
+constexpr int kCore = 128;                       // threads that evaluate, reduce and commit a step
+constexpr int kSpecMoves = 128;                  // largest speculated move set (one per spec thread)
+static_assert(kGreedyThreads == kCore || kGreedyThreads == kCore + 2 * kSpecMoves, "core + two speculated sets");
 
 struct GreedyArgs {
   OpscDag d;
@@ -64,13 +65,21 @@ struct GShared {
   int8_t tpos[OPSC_MAX_OPS];     // topological position of every op
   int cpv_ok;                    // cpv matches wt and every weight is >= 0 (trial_latency prefix)
   int chain;                     // the DAG is one path (each op feeds the next in topological order)
-  // speculated next move set (predict_op of (n_op, P, n_r, B >= n_blo), a pure
-  // function of its key, so it is valid whenever the key matches)
-  double n_wt[kSpecMoves], n_soj[kSpecMoves];
-  uint8_t n_ok[kSpecMoves];
-  int n_op, n_r, n_blo, n_M, n_valid;
-  uint32_t n_st;                 // status bits of the speculated points, ORed in when consumed
+  // speculated move sets, [parity][set]: predict_op of (op, P, R, B >= B_lo)
+  // for a key (op, R, B_lo) -- a pure function of the key, so valid whenever
+  // it matches; step c consumes parity c & 1 and fills parity (c + 1) & 1
+  double n_wt[2][2][kSpecMoves], n_soj[2][2][kSpecMoves];
+  uint8_t n_ok[2][2][kSpecMoves];
+  int n_op[2][2], n_r[2][2], n_blo[2][2], n_M[2][2], n_valid[2][2];
+  uint32_t n_st[2][2];           // status bits of the speculated points, ORed in when consumed
 };
+
+// barrier of the kCore threads that run a step's evaluation, reduction and
+// commit (the speculating threads only meet them at the step's end)
+__device__ __forceinline__ void core_sync() {
+  if (kGreedyThreads == kCore) __syncthreads();
+  else asm volatile("barrier.sync 1, %0;" ::"n"(kCore) : "memory");
+}
 
 
 // latency of the current plan with op `v`'s weight replaced (value only).
@@ -229,20 +238,27 @@ __device__ __noinline__ void eval_full(GShared& S, const GreedyArgs& a, int w, d
 
 // Evaluate moves [m0, m0 + kMaxMoves) of the move set of `op` at replica
 // count r_new (move m = (B = b_lo + m / np, P = pd[m % np]), all distinct P)
-// into the scratch slots m - m0 (all threads; ends synchronised). Returns
-// the size of the whole set; sets larger than kMaxMoves run in chunks.
+// into the scratch slots m - m0 (the kCore threads; ends core-synchronised).
+// Returns the size of the whole set; sets larger than kMaxMoves run in
+// chunks. A speculated set of parity `par` with this key supplies the
+// predict_op values.
 __device__ __noinline__ int eval_moves(GShared& S, const GreedyArgs& a, int w, int op, int r_new, int b_lo, double qps,
-                                       int L, int ph, int m0) {
+                                       int L, int ph, int m0, int par) {
   const int np = S.np_d[op];
   const int nb = a.s.b_max[op] - b_lo + 1;
   const int M = nb * np;
   const int m1 = min(M, m0 + kMaxMoves);
-  // the previous step speculated this very move set: its predict_op values
-  const bool spec = m0 == 0 && S.n_valid && S.n_op == op && S.n_r == r_new && S.n_blo == b_lo && S.n_M == M;
-  for (int m = m0 + threadIdx.x; m < m1; m += blockDim.x) {
+  int spec = -1;
+  if (m0 == 0)
+    for (int q = 0; q < 2; ++q)
+      if (S.n_valid[par][q] && S.n_op[par][q] == op && S.n_r[par][q] == r_new && S.n_blo[par][q] == b_lo &&
+          S.n_M[par][q] == M)
+        spec = q;
+  for (int m = m0 + threadIdx.x; m < m1; m += kCore) {
     const int b = b_lo + m / np, p = S.pd[op][m % np];
     uint32_t st = 0;
-    const GPt o = spec ? GPt{S.n_wt[m], S.n_soj[m], S.n_ok[m] != 0} : gpoint(a, w, qps, L, ph, op, p, r_new, b, &st);
+    const GPt o = spec >= 0 ? GPt{S.n_wt[par][spec][m], S.n_soj[par][spec][m], S.n_ok[par][spec][m] != 0}
+                            : gpoint(a, w, qps, L, ph, op, p, r_new, b, &st);
     const int i = m - m0;
     S.m_ok[i] = o.ok;
     if (o.ok) {
@@ -252,70 +268,59 @@ __device__ __noinline__ int eval_moves(GShared& S, const GreedyArgs& a, int w, i
     }
     if (st) atomicOr(&S.st, st);
   }
-  __syncthreads();
-  if (threadIdx.x == 0 && m0 == 0) {  // consumed or superseded (the next speculation starts after block_min)
-    if (spec) S.st |= S.n_st;
-    S.n_valid = 0;
-    S.n_st = 0;
+  core_sync();
+  if (threadIdx.x == 0 && m0 == 0) {  // consumed or superseded
+    if (spec >= 0) S.st |= S.n_st[par][spec];
+    S.n_valid[par][0] = S.n_valid[par][1] = 0;
   }
   return M;
 }
 
-// After a step's pick is known (all threads agree on it) and before warp 0
-// commits it: on a chain whose weights are >= 0 the next step is determined
-// already -- the new latency is the pick's trial latency (the critical path of
-// a chain is the whole chain, and the clamped trial DP equals it for weights
-// >= 0) and the next bottleneck is the argmax of the sojourns with the moved
-// operator's replaced -- so threads >= kSpecBase evaluate that move set while
-// warp 0 commits. A wrong guess only costs the work: the next step uses the
-// values only if its (op, R, B_lo) key matches.
-__device__ void speculate_next(GShared& S, const GreedyArgs& a, int w, double qps, int L, int ph, int op, int r_new,
-                               int b_new, double soj_new, double wt_new, double lat_new, double slo, double eps,
-                               bool headroom, bool cpv_ok0) {
-  // cpv_ok0: S.cpv_ok read at the start of the step (warp 0 rewrites it while this runs)
-  if ((int)threadIdx.x < kSpecBase || !S.chain || !cpv_ok0 || !(wt_new >= 0.0)) return;
+// Speculation (threads kCore.. of an upscale step, concurrently with the
+// step's evaluation / reduction / commit): on a chain the next bottleneck is
+// either the moved operator itself or, whatever the pick, the argmax of the
+// other operators' sojourns -- so the two upscale move sets the next step can
+// need, (op, R + 2, 1) and (op2, R_op2 + 1, 1), are evaluated now into the
+// buffers of parity `par`. Wrong guesses (a downscale next, or an early
+// stop) only cost idle threads' work: a set is used on an exact key match.
+__device__ void speculate_up(GShared& S, const GreedyArgs& a, int w, double qps, int L, int ph, int op, int cur_r,
+                             int par) {
+  const int t = (int)threadIdx.x - kCore;  // 0 .. 2 * kSpecMoves - 1
+  const int q = t / kSpecMoves, m = t - q * kSpecMoves;
   const int n = a.d.n_ops;
-  const bool up = headroom ? lat_new > slo - eps : lat_new > slo;
-  const bool down = !headroom && !up && lat_new <= slo - eps;
-  if (!up && !down) return;
-  int v = -1;  // bottleneck(): the path of a chain is every op in topological order
-  double sv = 0.0;
-  for (int i = 0; i < n; ++i) {
-    const int u = a.d.topo[i];
-    const double su = u == op ? soj_new : S.soj[u];
-    if (v < 0 || su > sv || (su == sv && u < v)) {
-      v = u;
-      sv = su;
+  int v = op, r = cur_r + 2;
+  if (q == 1) {  // bottleneck() over every op but `op` (the chain's path is every op, topological order)
+    v = -1;
+    double sv = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const int u = a.d.topo[i];
+      if (u == op) continue;
+      const double su = S.soj[u];
+      if (v < 0 || su > sv || (su == sv && u < v)) {
+        v = u;
+        sv = su;
+      }
     }
-  }
-  const int rv = v == op ? r_new : S.r[v], bv = v == op ? b_new : S.b[v];
-  int nr, nblo;
-  if (up) {
-    if (rv + 1 > a.s.r_cap) return;
-    nr = rv + 1;
-    nblo = 1;
-  } else {
-    if (rv - 1 < 1) return;
-    nr = rv - 1;
-    nblo = bv;
+    if (v < 0) return;
+    r = S.r[v] + 1;
   }
   const int np = S.np_d[v];
-  const int M = (a.s.b_max[v] - nblo + 1) * np;
-  if (M > kSpecMoves || M < 1) return;
+  const int M = a.s.b_max[v] * np;
+  if (r > a.s.r_cap || M > kSpecMoves) return;
   uint32_t st = 0;
-  for (int m = (int)threadIdx.x - kSpecBase; m < M; m += (int)blockDim.x - kSpecBase) {
-    const GPt o = gpoint(a, w, qps, L, ph, v, S.pd[v][m % np], nr, nblo + m / np, &st);
-    S.n_wt[m] = o.wt;
-    S.n_soj[m] = o.soj;
-    S.n_ok[m] = o.ok;
+  if (m < M) {
+    const GPt o = gpoint(a, w, qps, L, ph, v, S.pd[v][m % np], r, 1 + m / np, &st);
+    S.n_wt[par][q][m] = o.wt;
+    S.n_soj[par][q][m] = o.soj;
+    S.n_ok[par][q][m] = o.ok;
   }
-  if (st) atomicOr(&S.n_st, st);
-  if ((int)threadIdx.x == kSpecBase) {
-    S.n_op = v;
-    S.n_r = nr;
-    S.n_blo = nblo;
-    S.n_M = M;
-    S.n_valid = 1;
+  if (st) atomicOr(&S.n_st[par][q], st);
+  if (m == 0) {
+    S.n_op[par][q] = v;
+    S.n_r[par][q] = r;
+    S.n_blo[par][q] = 1;
+    S.n_M[par][q] = M;
+    S.n_valid[par][q] = 1;
   }
 }
 
@@ -365,8 +370,8 @@ __device__ __forceinline__ int move_index(const GShared& S, int op, int b_lo, in
 // Block-wide minimum of NK keys per thread (warp shuffles, then one warp
 // over the per-warp minima). All threads; result in out[] on every thread.
 template <int NK>
-__device__ void block_min(PK (&x)[NK]) {
-  __shared__ PK red[kGreedyThreads / 32][NK];
+__device__ void block_min(PK (&x)[NK]) {  // the kCore threads
+  __shared__ PK red[kCore / 32][NK];
   for (int off = 16; off > 0; off >>= 1) {
 #pragma unroll
     for (int k = 0; k < NK; ++k) {
@@ -378,15 +383,15 @@ __device__ void block_min(PK (&x)[NK]) {
   if (lane == 0)
 #pragma unroll
     for (int k = 0; k < NK; ++k) red[warp][k] = x[k];
-  __syncthreads();
+  core_sync();
 #pragma unroll
   for (int k = 0; k < NK; ++k) {
     PK v = red[0][k];
-    for (int w2 = 1; w2 < kGreedyThreads / 32; ++w2)
+    for (int w2 = 1; w2 < kCore / 32; ++w2)
       if (pk_less(red[w2][k], v)) v = red[w2][k];
     x[k] = v;
   }
-  __syncthreads();
+  core_sync();
 }
 
 // warp 0 (all lanes): set_path's results with the serial parts spread over
@@ -472,7 +477,7 @@ __device__ __forceinline__ void apply_move_warp(GShared& S, const GreedyArgs& a,
 // cheapest reaching slo, else the most efficient improving move
 // (-(dlat / dobj), latency, objective, B, P) -- each a block-wide minimum.
 __device__ __noinline__ void upscale_step(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps,
-                             int L, int ph, double slo, double eps, bool headroom) {
+                                          int L, int ph, double slo, double eps, bool headroom, int c) {
   const int op = S.bneck;  // set with the current path (every writer ends synchronised)
   const int cur_p = S.p[op], cur_r = S.r[op];
   if (cur_r + 1 > a.s.r_cap) {
@@ -481,10 +486,14 @@ __device__ __noinline__ void upscale_step(GShared& S, const GreedyArgs& a, const
     __syncthreads();
     return;
   }
+  if ((int)threadIdx.x >= kCore) {  // speculate the next step's two candidate move sets, then wait
+    if (S.chain) speculate_up(S, a, w, qps, L, ph, op, cur_r, (c + 1) & 1);
+    __syncthreads();
+    return;
+  }
   const int np = S.np_d[op];
   const int base = objective_warp(S, a.d.n_ops);  // every warp: one add-reduction
   const double target = slo - eps, cur_lat = S.lat;
-  const bool cpv_ok0 = S.cpv_ok;
   PK k[3];  // ach, ach2, imp
   for (int i = 0; i < 3; ++i) k[i] = pk_none();
   int M = 0, m0 = 0;
@@ -493,27 +502,27 @@ __device__ __noinline__ void upscale_step(GShared& S, const GreedyArgs& a, const
   long long u1 = 0;
 #endif
   do {
-    if (m0 > 0) __syncthreads();  // previous chunk's scratch fully read
-    M = eval_moves(S, a, w, op, cur_r + 1, 1, qps, L, ph, m0);
+    if (m0 > 0) core_sync();  // previous chunk's scratch fully read
+    M = eval_moves(S, a, w, op, cur_r + 1, 1, qps, L, ph, m0, c & 1);
 #ifdef OPSC_GREEDY_PROF
     u1 = clock64();
 #endif
-  for (int m = m0 + threadIdx.x; m < min(M, m0 + kMaxMoves); m += blockDim.x) {
-    if (!S.m_ok[m - m0]) continue;
-    const int b = 1 + m / np, p = S.pd[op][m % np];
-    const double lat = S.m_lat[m - m0];
-    const int obj = base - cur_p * cur_r + p * (cur_r + 1);
-    const PK reach = pk_make((double)obj, lat, 0, b, p);
-    if (lat <= target && pk_less(reach, k[0])) k[0] = reach;
-    if (!headroom && lat <= slo && pk_less(reach, k[1])) k[1] = reach;
-    const bool improving = headroom ? lat < cur_lat - 1e-9 * slo : lat < cur_lat;
-    if (improving) {
-      const int dobj = obj - base;
-      const double cost = dobj >= 1 ? (double)dobj : 1e-9;
-      const PK eff = pk_make(-((cur_lat - lat) / cost), lat, headroom ? 0 : obj, b, p);
-      if (pk_less(eff, k[2])) k[2] = eff;
+    for (int m = m0 + threadIdx.x; m < min(M, m0 + kMaxMoves); m += kCore) {
+      if (!S.m_ok[m - m0]) continue;
+      const int b = 1 + m / np, p = S.pd[op][m % np];
+      const double lat = S.m_lat[m - m0];
+      const int obj = base - cur_p * cur_r + p * (cur_r + 1);
+      const PK reach = pk_make((double)obj, lat, 0, b, p);
+      if (lat <= target && pk_less(reach, k[0])) k[0] = reach;
+      if (!headroom && lat <= slo && pk_less(reach, k[1])) k[1] = reach;
+      const bool improving = headroom ? lat < cur_lat - 1e-9 * slo : lat < cur_lat;
+      if (improving) {
+        const int dobj = obj - base;
+        const double cost = dobj >= 1 ? (double)dobj : 1e-9;
+        const PK eff = pk_make(-((cur_lat - lat) / cost), lat, headroom ? 0 : obj, b, p);
+        if (pk_less(eff, k[2])) k[2] = eff;
+      }
     }
-  }
     m0 += kMaxMoves;
   } while (m0 < M);
   m0 -= kMaxMoves;  // the chunk still in the scratch
@@ -524,15 +533,6 @@ __device__ __noinline__ void upscale_step(GShared& S, const GreedyArgs& a, const
 #ifdef OPSC_GREEDY_PROF
   const long long u3 = clock64();
 #endif
-  if ((int)threadIdx.x >= kSpecBase) {  // the next move set, while warp 0 commits this one
-    const PK& pick = pk_valid(k[0]) ? k[0] : (!headroom && pk_valid(k[1])) ? k[1] : k[2];
-    if (pk_valid(pick) && m0 == 0) {
-      const int i = move_index(S, op, 1, pk_b(pick), pk_p(pick));
-      if (i < kMaxMoves)
-        speculate_next(S, a, w, qps, L, ph, op, cur_r + 1, pk_b(pick), S.m_soj[i], S.m_wt[i], S.m_lat[i], slo, eps,
-                       headroom, cpv_ok0);
-    }
-  }
   if (threadIdx.x < 32) {  // warp 0 applies the pick (every thread holds the same minima)
     const PK& pick = pk_valid(k[0]) ? k[0] : (!headroom && pk_valid(k[1])) ? k[1] : k[2];
     const int m = pk_valid(pick) ? move_index(S, op, 1, pk_b(pick), pk_p(pick)) : -1;
@@ -555,8 +555,8 @@ __device__ __noinline__ void upscale_step(GShared& S, const GreedyArgs& a, const
 
 // Downscale (autoscaler.py:456-486): the cheapest (objective, B, P) move at
 // R - 1 that stays within slo - eps and lowers the objective.
-__device__ __noinline__ void downscale_step(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps,
-                               int L, int ph, double slo, double eps) {
+__device__ __noinline__ void downscale_step(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w,
+                                            double qps, int L, int ph, double slo, double eps, int c) {
   const int op = S.bneck;  // set with the current path (every writer ends synchronised)
   const int cur_p = S.p[op], cur_r = S.r[op], cur_b = S.b[op];
   if (cur_r - 1 < 1) {
@@ -565,34 +565,31 @@ __device__ __noinline__ void downscale_step(GShared& S, const GreedyArgs& a, con
     __syncthreads();
     return;
   }
+  if ((int)threadIdx.x >= kCore) {  // nothing speculated after a downscale step
+    __syncthreads();
+    return;
+  }
   const int np = S.np_d[op];
   const int base = objective_warp(S, a.d.n_ops);  // every warp: one add-reduction
   const double bound = slo - eps;
-  const bool cpv_ok0 = S.cpv_ok;
   PK k[1];
   k[0] = pk_none();
   int M = 0, m0 = 0;
   do {
-    if (m0 > 0) __syncthreads();  // previous chunk's scratch fully read
-    M = eval_moves(S, a, w, op, cur_r - 1, cur_b, qps, L, ph, m0);
-    for (int m = m0 + threadIdx.x; m < min(M, m0 + kMaxMoves); m += blockDim.x) {
+    if (m0 > 0) core_sync();  // previous chunk's scratch fully read
+    M = eval_moves(S, a, w, op, cur_r - 1, cur_b, qps, L, ph, m0, c & 1);
+    for (int m = m0 + threadIdx.x; m < min(M, m0 + kMaxMoves); m += kCore) {
       if (!S.m_ok[m - m0] || S.m_lat[m - m0] > bound) continue;
       const int b = cur_b + m / np, p = S.pd[op][m % np];
       const int obj = base - cur_p * cur_r + p * (cur_r - 1);
       if (obj >= base) continue;
-      const PK c = pk_make((double)obj, 0.0, 0, b, p);
-      if (pk_less(c, k[0])) k[0] = c;
+      const PK cand = pk_make((double)obj, 0.0, 0, b, p);
+      if (pk_less(cand, k[0])) k[0] = cand;
     }
     m0 += kMaxMoves;
   } while (m0 < M);
   m0 -= kMaxMoves;
   block_min<1>(k);
-  if ((int)threadIdx.x >= kSpecBase && pk_valid(k[0]) && m0 == 0) {
-    const int i = move_index(S, op, cur_b, pk_b(k[0]), pk_p(k[0]));
-    if (i < kMaxMoves)
-      speculate_next(S, a, w, qps, L, ph, op, cur_r - 1, pk_b(k[0]), S.m_soj[i], S.m_wt[i], S.m_lat[i], slo, eps,
-                     false, cpv_ok0);
-  }
   if (threadIdx.x < 32) {
     const int best = pk_valid(k[0]) ? move_index(S, op, cur_b, pk_b(k[0]), pk_p(k[0])) : -1;
     if (threadIdx.x == 0) S.applied = best >= 0;
@@ -611,9 +608,9 @@ __device__ __noinline__ void greedy_loop(GShared& S, const GreedyArgs& a, const 
   for (int it = 0; it < a.s.max_iterations; ++it) {
     const double lat = S.lat;
     if (lat > slo) {
-      upscale_step(S, a, out, w, qps, L, ph, slo, eps, false);
+      upscale_step(S, a, out, w, qps, L, ph, slo, eps, false, it);
     } else if (lat <= slo - eps) {
-      downscale_step(S, a, out, w, qps, L, ph, slo, eps);
+      downscale_step(S, a, out, w, qps, L, ph, slo, eps, it);
     } else {
       break;
     }
@@ -765,8 +762,10 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
       S.cpv_ok = 0;
       for (int i = 0; i < n; ++i) S.tpos[d.topo[i]] = (int8_t)i;
       S.chain = is_chain(d);
-      S.n_valid = 0;
-      S.n_st = 0;
+      for (int q = 0; q < 4; ++q) {
+        S.n_valid[q >> 1][q & 1] = 0;
+        S.n_st[q >> 1][q & 1] = 0;
+      }
     }
     __syncthreads();
     if (!S.flag) return;
@@ -794,8 +793,10 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
     S.trace_len = 0;
     S.cpv_ok = 0;
     S.chain = is_chain(d);
-    S.n_valid = 0;
-    S.n_st = 0;
+    for (int q = 0; q < 4; ++q) {
+      S.n_valid[q >> 1][q & 1] = 0;
+      S.n_st[q >> 1][q & 1] = 0;
+    }
   }
   __syncthreads();
 
@@ -979,8 +980,8 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
   }
   // ---- headroom restore (:369-374, 503-559)
   if (eps > 0 && S.lat <= slo) {
-    while (S.lat > slo - eps) {
-      upscale_step(S, a, out, w, qps, L, ph, slo, eps, true);
+    for (int c = 0; S.lat > slo - eps; ++c) {
+      upscale_step(S, a, out, w, qps, L, ph, slo, eps, true, c);
       if (!S.applied) break;
     }
   }
