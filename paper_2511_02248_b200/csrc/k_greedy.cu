@@ -476,6 +476,13 @@ __device__ __forceinline__ void apply_move_warp(GShared& S, const GreedyArgs& a,
 // move reaching slo - eps (objective, latency, B, P), then (loop only) the
 // cheapest reaching slo, else the most efficient improving move
 // (-(dlat / dobj), latency, objective, B, P) -- each a block-wide minimum.
+__device__ __forceinline__ void upscale_core(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w,
+                                             double qps, int L, int ph, double slo, double eps, bool headroom, int c,
+                                             int op, int cur_p, int cur_r);
+__device__ __forceinline__ void downscale_core(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w,
+                                               double qps, int L, int ph, double slo, double eps, int c, int op,
+                                               int cur_p, int cur_r, int cur_b);
+
 __device__ __noinline__ void upscale_step(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps,
                                           int L, int ph, double slo, double eps, bool headroom, int c) {
   const int op = S.bneck;  // set with the current path (every writer ends synchronised)
@@ -486,11 +493,18 @@ __device__ __noinline__ void upscale_step(GShared& S, const GreedyArgs& a, const
     __syncthreads();
     return;
   }
-  if ((int)threadIdx.x >= kCore) {  // speculate the next step's two candidate move sets, then wait
+  if ((int)threadIdx.x >= kCore) {  // speculate the next step's two candidate move sets
     if (S.chain) speculate_up(S, a, w, qps, L, ph, op, cur_r, (c + 1) & 1);
-    __syncthreads();
-    return;
+  } else {
+    upscale_core(S, a, out, w, qps, L, ph, slo, eps, headroom, c, op, cur_p, cur_r);
   }
+  __syncthreads();  // one barrier instruction for the whole CTA
+}
+
+// the kCore threads' part of an upscale step
+__device__ __forceinline__ void upscale_core(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w,
+                                             double qps, int L, int ph, double slo, double eps, bool headroom, int c,
+                                             int op, int cur_p, int cur_r) {
   const int np = S.np_d[op];
   const int base = objective_warp(S, a.d.n_ops);  // every warp: one add-reduction
   const double target = slo - eps, cur_lat = S.lat;
@@ -545,7 +559,6 @@ __device__ __noinline__ void upscale_step(GShared& S, const GreedyArgs& a, const
                    S.lat, obj);
     }
   }
-  __syncthreads();
 #ifdef OPSC_GREEDY_PROF
   if (threadIdx.x == 0)
     printf("  up step op %d r %d M %d: eval %lld keys %lld reduce %lld apply %lld cycles\n", op, cur_r + 1, M,
@@ -565,10 +578,13 @@ __device__ __noinline__ void downscale_step(GShared& S, const GreedyArgs& a, con
     __syncthreads();
     return;
   }
-  if ((int)threadIdx.x >= kCore) {  // nothing speculated after a downscale step
-    __syncthreads();
-    return;
-  }
+  if ((int)threadIdx.x < kCore) downscale_core(S, a, out, w, qps, L, ph, slo, eps, c, op, cur_p, cur_r, cur_b);
+  __syncthreads();  // one barrier instruction for the whole CTA (nothing speculated after a downscale)
+}
+
+__device__ __forceinline__ void downscale_core(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w,
+                                               double qps, int L, int ph, double slo, double eps, int c, int op,
+                                               int cur_p, int cur_r, int cur_b) {
   const int np = S.np_d[op];
   const int base = objective_warp(S, a.d.n_ops);  // every warp: one add-reduction
   const double bound = slo - eps;
@@ -600,7 +616,6 @@ __device__ __noinline__ void downscale_step(GShared& S, const GreedyArgs& a, con
         push_trace(S, out, w, OPSC_ACT_DOWNSCALE, op, S.r[op], S.b[op], S.p[op], S.lat, obj);
     }
   }
-  __syncthreads();
 }
 
 __device__ __noinline__ void greedy_loop(GShared& S, const GreedyArgs& a, const OpscDecisions& out, int w, double qps,
