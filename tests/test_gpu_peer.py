@@ -134,3 +134,25 @@ def test_bench_two_gpus_self_spawned():
     line = json.loads(p.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["parity_vs_oracle"] is True
     assert line["e2e"]["parity_vs_device_path"] is True
+
+
+def test_bench_two_ranks_time_sharing_one_gpu():
+    """The bench's N > 1 path end to end on the one GPU of this pool: two ranks
+    under torchrun with the gloo process group (OPSC_DIST_BACKEND=gloo), the
+    fused peer-memory merge between the two processes (CUDA IPC), sharded
+    compose, e2e through dist.plan_windows_host_sharded: one n_gpus: 2 line
+    whose decisions match the CPU oracle and the device path. Correctness of
+    the N > 1 plumbing, not a scaling measurement."""
+    import json
+    repo = os.path.dirname(HERE)
+    env = dict(os.environ, OPSC_DIST_BACKEND="gloo", PYTHONPATH=repo)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29541", os.path.join(repo, "bench.py"),
+           "--gpus", "2", "--steps", "1", "--warmup", "3", "--no-latency", "--no-cpu-baseline"]
+    p = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, (p.stdout[-2000:], p.stderr[-3000:])
+    line = json.loads([x for x in p.stdout.strip().splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["parity_vs_oracle"] is True
+    assert line["e2e"]["parity_vs_device_path"] is True
+    assert line["run"]["merge"].startswith("fused")
+    assert line["order_certificate"]["order_sensitive_windows"] == 0
