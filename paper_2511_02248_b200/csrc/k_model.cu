@@ -62,10 +62,9 @@ template <bool TABLE>
 __device__ __forceinline__ double probe(const OpscDag& d, const OpscModelSpec& m, double qps, int L, int ph,
                                         int b, int r, double* wsh, uint32_t* st, const double* lt,
                                         const uint8_t* ls) {
-  if (TABLE) {
-    const size_t i = (size_t)(b - 1) * m.r_cap + (r - 1);
-    *st |= ls[i];
-    return lt[i];
+  if (TABLE) {  // lt / ls: this B's row (R = 1 .. r_cap)
+    *st |= ls[r - 1];
+    return lt[r - 1];
   }
   return eval_uniform(d, m, qps, L, ph, b, r, wsh, st);
 }
@@ -112,7 +111,7 @@ __global__ void __launch_bounds__(1024) model_grid_kernel(const __grid_constant_
                                                           uint8_t* __restrict__ feasible,
                                                           uint32_t* __restrict__ status,
                                                           const double* __restrict__ lt_all,
-                                                          const uint8_t* __restrict__ ls_all) {
+                                                          const uint8_t* __restrict__ ls_all, int rows_smem) {
   pdl_trigger();
   pdl_wait();
   const OpscDag& d = a.d;
@@ -136,10 +135,31 @@ __global__ void __launch_bounds__(1024) model_grid_kernel(const __grid_constant_
   double* wsh = wsh_all + warp * 32;
   uint32_t st = 0;
   const size_t tab = (size_t)m.b_cap * m.r_cap;
-  const double* lt = TABLE ? lt_all + (size_t)w * tab : nullptr;
-  const uint8_t* ls = TABLE ? ls_all + (size_t)w * tab : nullptr;
+  const double* lt_w = TABLE ? lt_all + (size_t)w * tab : nullptr;
+  const uint8_t* ls_w = TABLE ? ls_all + (size_t)w * tab : nullptr;
+  // table path: each warp stages its B's row of latencies / status bits in
+  // shared memory first (coalesced), so the probe + bisection's dependent
+  // lookups cost a shared-memory load instead of an L2 round trip each
+  double* row_lt = reinterpret_cast<double*>(res_r + m.b_cap + (m.b_cap & 1)) + (size_t)warp * m.r_cap;
+  uint8_t* row_ls = reinterpret_cast<uint8_t*>(reinterpret_cast<double*>(res_r + m.b_cap + (m.b_cap & 1)) +
+                                               (size_t)nwarps * m.r_cap) + (size_t)warp * m.r_cap;
 
   for (int b = warp + 1; b <= m.b_cap; b += nwarps) {
+    const double* lt = nullptr;
+    const uint8_t* ls = nullptr;
+    if (TABLE) {
+      lt = lt_w + (size_t)(b - 1) * m.r_cap;
+      ls = ls_w + (size_t)(b - 1) * m.r_cap;
+      if (rows_smem) {
+        for (int r = lane; r < m.r_cap; r += 32) {
+          row_lt[r] = lt[r];
+          row_ls[r] = ls[r];
+        }
+        __syncwarp();
+        lt = row_lt;
+        ls = row_ls;
+      }
+    }
     int rm = 1;
     bool bad = false;
     if (lane < d.n_ops) {
@@ -161,6 +181,7 @@ __global__ void __launch_bounds__(1024) model_grid_kernel(const __grid_constant_
       res_r[b - 1] = r;
       res_lat[b - 1] = lat;
     }
+    __syncwarp();  // the row buffer is reused by this warp's next B
   }
   if (st) atomicOr(&st_sh, st);
   __syncthreads();
@@ -292,8 +313,12 @@ cudaError_t launch_model_grid(const OpscDag& d, const OpscModelSpec& m, OpscWind
   a.d = d;
   a.m = m;
   const int nwarps = m.b_cap < 32 ? m.b_cap : 32;
-  const size_t smem = (size_t)nwarps * 32 * sizeof(double) + (size_t)m.b_cap * (sizeof(double) + sizeof(int32_t));
+  const size_t smem0 = (size_t)nwarps * 32 * sizeof(double) + (size_t)m.b_cap * sizeof(double) +
+                       (size_t)(m.b_cap + (m.b_cap & 1)) * sizeof(int32_t);
   const bool table = table_ws && table_bytes >= model_table_bytes(w.n, m, d.n_ops);
+  const size_t rows = (size_t)nwarps * m.r_cap * (sizeof(double) + 1);
+  const int rows_smem = table && smem0 + rows <= (size_t)200 * 1024;
+  const size_t smem = smem0 + (rows_smem ? rows : 0);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(table ? model_grid_kernel<true> : model_grid_kernel<false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -301,7 +326,7 @@ cudaError_t launch_model_grid(const OpscDag& d, const OpscModelSpec& m, OpscWind
   }
   if (!table) {
     return launch_pdl(model_grid_kernel<false>, dim3(w.n), dim3(nwarps * 32), smem, s, a, w, cfg, feasible, status,
-                      (const double*)nullptr, (const uint8_t*)nullptr);
+                      (const double*)nullptr, (const uint8_t*)nullptr, 0);
   }
   const size_t pts = (size_t)w.n * m.b_cap * m.r_cap;
   double* wt = (double*)table_ws;
@@ -320,7 +345,7 @@ cudaError_t launch_model_grid(const OpscDag& d, const OpscModelSpec& m, OpscWind
   e = launch_pdl(model_tab_latency, dim3(g2), dim3(128), 0, s, a, w.n, (const double*)wt, (const uint8_t*)wst, lt, ls);
   if (e != cudaSuccess) return e;
   return launch_pdl(model_grid_kernel<true>, dim3(w.n), dim3(nwarps * 32), smem, s, a, w, cfg, feasible, status,
-                    (const double*)lt, (const uint8_t*)ls);
+                    (const double*)lt, (const uint8_t*)ls, rows_smem);
 }
 
 }  // namespace opsc
