@@ -38,6 +38,8 @@ struct GreedyArgs {
   OpscGreedySpec s;
 };
 
+constexpr size_t kGreedyArgsWords = (sizeof(GreedyArgs) + 15) / 16;  // dynamic smem: copied args first
+
 struct GShared {
   int p[OPSC_MAX_OPS], r[OPSC_MAX_OPS], b[OPSC_MAX_OPS];
   double soj[OPSC_MAX_OPS], wt[OPSC_MAX_OPS];
@@ -644,18 +646,54 @@ __device__ __noinline__ void prune_pass(GShared& S, const GreedyArgs& a, const O
   __shared__ double t_wt[OPSC_MAX_OPS], t_soj[OPSC_MAX_OPS];
   __shared__ uint8_t t_ok[OPSC_MAX_OPS], t_need[OPSC_MAX_OPS];
   __shared__ int changed;
+  __shared__ int r_base[OPSC_MAX_OPS];
   const OpscDag& d = a.d;
-  for (int v = threadIdx.x; v < d.n_ops; v += blockDim.x) t_need[v] = 1;
+  const int n = d.n_ops;
+  // Every pass prunes an operator by at most one replica and its P and B stay,
+  // so the trials a pass can need are predict_op(v, P_v, R_v - depth, B_v):
+  // all threads tabulate depth 1 .. kGreedyThreads / n of every operator at
+  // once (one Erlang chain each); a pass then looks its trials up (status bits
+  // ORed when used), computing only past the table's depth.
+  extern __shared__ __align__(16) unsigned char g_dyn[];
+  double* pt_wt = reinterpret_cast<double*>(g_dyn + kGreedyArgsWords * 16);
+  double* pt_soj = pt_wt + kGreedyThreads;
+  uint32_t* pt_st = reinterpret_cast<uint32_t*>(pt_soj + kGreedyThreads);
+  uint8_t* pt_ok = reinterpret_cast<uint8_t*>(pt_st + kGreedyThreads);
+  const int depth = kGreedyThreads / n;
+  for (int v = threadIdx.x; v < n; v += blockDim.x) {
+    t_need[v] = 1;
+    r_base[v] = S.r[v];
+  }
+  {
+    const int e = threadIdx.x, v = e % n, dd = e / n + 1;
+    if (dd <= depth && S.r[v] - dd >= 1) {
+      uint32_t st = 0;
+      const GPt o = gpoint(a, w, qps, L, ph, v, S.p[v], S.r[v] - dd, S.b[v], &st);
+      pt_wt[e] = o.wt;
+      pt_soj[e] = o.soj;
+      pt_ok[e] = o.ok;
+      pt_st[e] = st;
+    }
+  }
   __syncthreads();
   while (true) {
-    for (int v = threadIdx.x; v < d.n_ops; v += blockDim.x) {
+    for (int v = threadIdx.x; v < n; v += blockDim.x) {
       if (!t_need[v] || S.r[v] <= 1) continue;
       uint32_t st = 0;
-      const GPt o = gpoint(a, w, qps, L, ph, v, S.p[v], S.r[v] - 1, S.b[v], &st);
+      const int dd = r_base[v] - (S.r[v] - 1);
+      if (dd >= 1 && dd <= depth) {
+        const int e = (dd - 1) * n + v;
+        st = pt_st[e];
+        t_ok[v] = pt_ok[e];
+        t_wt[v] = pt_wt[e];
+        t_soj[v] = pt_soj[e];
+      } else {
+        const GPt o = gpoint(a, w, qps, L, ph, v, S.p[v], S.r[v] - 1, S.b[v], &st);
+        t_ok[v] = o.ok;
+        t_wt[v] = o.wt;
+        t_soj[v] = o.soj;
+      }
       if (st) atomicOr(&S.st, st);
-      t_ok[v] = o.ok;
-      t_wt[v] = o.wt;
-      t_soj[v] = o.soj;
       t_need[v] = 0;
     }
     __syncthreads();
@@ -734,7 +772,6 @@ __device__ void distinct_p(GShared& S, const GreedyArgs& a, int n) {
 // (init pairs, the path update, the prune sweep): from the kernel's parameter
 // (constant) bank every such load serialises over the distinct addresses of a
 // warp, so the CTA first copies them to shared memory (16-byte words).
-constexpr size_t kGreedyArgsWords = (sizeof(GreedyArgs) + 15) / 16;
 
 __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
     const __grid_constant__ GreedyArgs ga, const __grid_constant__ OpscWindows win,
@@ -977,9 +1014,25 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
     }
     __syncthreads();
     if (reseed) {
+#ifdef OPSC_GREEDY_PROF
+      const long long z0 = clock64();
+      const int tr0 = S.trace_len;
+#endif
       eval_full(S, a, w, qps, L, ph);
+#ifdef OPSC_GREEDY_PROF
+      const long long z1 = clock64();
+#endif
       prune_pass(S, a, out, w, qps, L, ph, slo - eps);
+#ifdef OPSC_GREEDY_PROF
+      const long long z2 = clock64();
+      const int tr1 = S.trace_len;
+#endif
       greedy_loop(S, a, out, w, qps, L, ph, slo, eps);
+#ifdef OPSC_GREEDY_PROF
+      if (threadIdx.x == 0)
+        printf("greedy w%d phase 2 reseed: eval %lld prune %lld (%d moves) loop %lld (%d moves) cycles\n", w, z1 - z0,
+               z2 - z1, tr1 - tr0, clock64() - z2, S.trace_len - tr1);
+#endif
       if (threadIdx.x == 0 && !(objective(S, n) < base_obj)) {
         for (int v = 0; v < n; ++v) {
           S.p[v] = keep_p[v]; S.r[v] = keep_r[v]; S.b[v] = keep_b[v];
@@ -1029,7 +1082,8 @@ cudaError_t launch_greedy(const OpscDag& d, const OpscGreedySpec& s, OpscWindows
   GreedyArgs a;
   a.d = d;
   a.s = s;
-  const size_t dyn = kGreedyArgsWords * 16;
+  // dynamic smem: the copied args, then the prune pass's trial table
+  const size_t dyn = kGreedyArgsWords * 16 + (size_t)kGreedyThreads * (8 + 8 + 4 + 1);
   static int set_dyn[64];  // raise the dynamic limit once per device (static GShared + args pass 48 KB)
   int dev = 0;
   cudaGetDevice(&dev);
