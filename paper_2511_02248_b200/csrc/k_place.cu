@@ -6,14 +6,18 @@
 // (request_energy, fill_device_energy, provisioned_memory; metrics.py:84-132).
 //
 // One CTA per window. Base instances are packed first-fit-decreasing
-// (placement.py:358-385, sequential, thread 0). Each extra replica, heaviest
-// op_latency first (:388-396), probes every used device; a probe needs the
-// interference factors of the device's members with the tentative replica
-// added (:209-231), the adjusted service time and Erlang-C wait of every
-// operator with a replica there (:245-273) and the critical path. Those
-// (device, operator) re-evaluations -- the Erlang-B recurrences -- run in
-// parallel threads; thread 0 scores the feasible devices by weighted slack
-// (:338-351, best score, ties to the lowest device id) and commits.
+// (placement.py:358-385, sequential, thread 0; each base device then holds
+// one instance's group, refreshed one device per thread). Each extra replica,
+// heaviest op_latency first (:388-396), probes every used device; a probe
+// needs the interference factors of the device's members with the tentative
+// replica added (:209-231), the adjusted service time and Erlang-C wait of
+// every operator with a replica there (:245-273) and the critical path.
+// Stage 1 (a thread per device) admits the devices and lists the (device,
+// operator) pairs to re-evaluate; stage 2 runs those Erlang-B recurrences, one
+// listed pair per thread; stage 3 (a thread per device) checks the critical
+// path against the SLO and scores by weighted slack (:338-351), reduced to the
+// best score, ties to the lowest device id; thread 0 commits, and the new
+// load and factors of the chosen device are updated incrementally.
 // Sums the reference takes with Python's sum() use CPython 3.12's Neumaier
 // summation (PySum), in the reference's iteration order.
 #include <cstdio>
@@ -24,7 +28,6 @@ namespace opsc {
 
 constexpr int kPlaceThreads = 128;
 constexpr int kMaxDevProbe = 128;  // device probes per chunk held in smem
-constexpr int kMaxMembers = 256;   // members of one device refreshed by a warp (more: lane 0 alone)
 constexpr size_t kPlaceSmemMax = 200 * 1024;  // static PShared + per-window workspace
 
 struct PlaceArgs {
@@ -120,23 +123,6 @@ __device__ double member_factor(const PWork& P, const OpscPlaceShared& f, int de
   return interference(f, total - gm, P.a_dem[i]);
 }
 
-// standing load of `dev` as the PySum state dev_load builds (no extra member)
-__device__ PySum dev_load_sum(const PWork& P, int dev) {
-  PySum t;
-  t.reset();
-  for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) {
-    const int g = P.a_group[i];
-    bool first = true;
-    for (int j = P.dev_head[dev]; j != i; j = P.a_next[j]) first &= P.a_group[j] != g;
-    if (!first) continue;
-    double m = 0.0;
-    for (int j = i; j >= 0; j = P.a_next[j])
-      if (P.a_group[j] == g) m = m >= P.a_dem[j] ? m : P.a_dem[j];
-    t.add(m);
-  }
-  return t;
-}
-
 __device__ __forceinline__ PySum cached_load(const PWork& P, int dev) {
   PySum t;
   t.f = P.dev_lf[dev];
@@ -202,19 +188,18 @@ struct PShared {
   int rep_off[OPSC_MAX_OPS + 1];
   double cur_wt[OPSC_MAX_OPS], cur_teff[OPSC_MAX_OPS], cur_wait[OPSC_MAX_OPS];
   bool cur_stable[OPSC_MAX_OPS];
-  uint32_t on_dev[kMaxDevProbe];    // ops with a replica on device d (bitmask)
-  double dev_total[kMaxDevProbe];   // standing load with the tentative replica
-  double dev_load0[kMaxDevProbe];   // standing load without it
+  double dev_load0[kMaxDevProbe];   // standing load of device d (without the tentative replica)
+  double dev_total[kMaxDevProbe];   // ... with it
   double dev_xf[kMaxDevProbe];      // tentative replica's factor on d
+  uint16_t items[kMaxDevProbe * OPSC_MAX_OPS];  // stage 2 work list: (d << 5 | op)
+  int n_items;
   uint8_t dev_ok[kMaxDevProbe];
   double probe_wt[kMaxDevProbe][OPSC_MAX_OPS];
   double dev_score[kMaxDevProbe];   // weighted slack of each admissible device
-  int ord[kMaxMembers];             // refresh_device_warp: the device's members in list order
-  uint8_t ofirst[kMaxMembers];      // ... first occurrence of its group
-  int nord;
-  double ototal;
+  double ototal;                    // a commit's device: standing load with the extra
 #ifdef OPSC_PLACE_PROF
-  long long prof[6];
+  long long prof[7];  // stage1+2, stage3+select, commit, refresh, -, extras, device probes
+  long long ph[6];    // phase timestamps: start, setup, base, initial figures, extras, end
 #endif
   double red_score[kPlaceThreads / 32];
   int red_dj[kPlaceThreads / 32];
@@ -265,10 +250,12 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
     }
     S.err = S.rep_off[n] > A ? OPSC_W_TRACE_TRUNCATED : 0;
 #ifdef OPSC_PLACE_PROF
-    for (int q = 0; q < 6; ++q) S.prof[q] = 0;
+    for (int q = 0; q < 7; ++q) S.prof[q] = 0;
+    S.ph[0] = clock64();
 #endif
     S.used = 0;
     S.na = 0;
+    S.n_items = 0;
   }
   __syncthreads();
   if (S.err) {
@@ -291,6 +278,9 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
     P.dev_lf[i] = 0.0; P.dev_lc[i] = 0.0; P.dev_ls[i] = 0; P.dev_mask[i] = 0u;
   }
   __syncthreads();
+#ifdef OPSC_PLACE_PROF
+  if (threadIdx.x == 0) S.ph[1] = clock64();
+#endif
 
   // thread 0 helpers -------------------------------------------------------
   auto push = [&](int v, int k, int dev, int group, int share) {
@@ -316,7 +306,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
     }
     P.dev_cnt[dev]++;
     P.rep[S.rep_off[v] + k - 1] = i;
-    P.dev_mask[dev] |= 1u << v;  // group maxima, load sum and factors: refresh_device
+    P.dev_mask[dev] |= 1u << v;  // group maxima, load sum and factors: by the caller
     const size_t o = (size_t)w * A + i;
     P.a_op[i] = v;
     P.a_dev[i] = dev;
@@ -326,70 +316,26 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
     out.a_share[o] = (int16_t)share;
   };
   auto dev_mem = [&](int dev) { return psum_value(P.dev_mem_f[dev], P.dev_mem_c[dev], P.dev_cnt[dev] > 0); };
-  // after members were pushed to `dev`: the group maxima (the scan
-  // member_factor made per call), the standing-load sum and every member's
-  // interference factor
-  auto refresh_device = [&](int dev) {
-    for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) {
-      double gm = 0.0;
-      for (int j = P.dev_head[dev]; j >= 0; j = P.a_next[j])
-        if (P.a_group[j] == P.a_group[i]) gm = gm >= P.a_dem[j] ? gm : P.a_dem[j];
-      P.a_gmax[i] = gm;
-    }
-    const PySum ls = dev_load_sum(P, dev);
+  // a base device after the first-fit pass: every device is opened within one
+  // instance and only that instance's pushes go to it (first fit over the
+  // devices opened for the instance), so its members form ONE group: each
+  // member's group maximum is the maximum over the device's list (the scan
+  // member_factor made per call, in list order), the standing load is that one
+  // term, and every member's interference factor follows from it
+  auto refresh_base_device = [&](int dev) {
+    double gm = 0.0;
+    for (int j = P.dev_head[dev]; j >= 0; j = P.a_next[j]) gm = gm >= P.a_dem[j] ? gm : P.a_dem[j];
+    PySum ls;
+    ls.reset();
+    ls.add(gm);
     P.dev_lf[dev] = ls.f;
     P.dev_lc[dev] = ls.c;
-    P.dev_ls[dev] = ls.started ? 1 : 0;
+    P.dev_ls[dev] = 1;
     const double total = ls.value();
-    for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) P.a_fac[i] = member_factor(P, f, dev, i, -1, 0.0, total);
-  };
-
-  // the same refresh by warp 0 after a commit: the device's member list as an
-  // array, each lane one member's group maximum and first-occurrence flag,
-  // lane 0 the load sum in list order (the serial PySum), lanes the factors
-  auto refresh_device_warp = [&](int dev) {
-    const int lane = threadIdx.x & 31;
-    if (lane == 0) {
-      int m = 0, i = P.dev_head[dev];
-      for (; i >= 0 && m < kMaxMembers; i = P.a_next[i]) S.ord[m++] = i;
-      S.nord = i >= 0 ? -1 : m;
-      if (i >= 0) refresh_device(dev);  // more members than the array holds
-    }
-    __syncwarp();
-    const int m = S.nord;
-    if (m < 0) return;
-    for (int x = lane; x < m; x += 32) {
-      const int i = S.ord[x], g = P.a_group[i];
-      double gm = 0.0;
-      bool first = true;
-      for (int y = 0; y < m; ++y) {
-        const int j = S.ord[y];
-        if (P.a_group[j] == g) {
-          gm = gm >= P.a_dem[j] ? gm : P.a_dem[j];
-          first &= y >= x;
-        }
-      }
+    for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) {
       P.a_gmax[i] = gm;
-      S.ofirst[x] = first;
+      P.a_fac[i] = interference(f, total - gm, P.a_dem[i]);
     }
-    __syncwarp();
-    if (lane == 0) {
-      PySum t;
-      t.reset();
-      for (int x = 0; x < m; ++x)
-        if (S.ofirst[x]) t.add(P.a_gmax[S.ord[x]]);
-      P.dev_lf[dev] = t.f;
-      P.dev_lc[dev] = t.c;
-      P.dev_ls[dev] = t.started ? 1 : 0;
-      S.ototal = t.value();
-    }
-    __syncwarp();
-    const double total = S.ototal;
-    for (int x = lane; x < m; x += 32) {
-      const int i = S.ord[x];
-      P.a_fac[i] = member_factor(P, f, dev, i, -1, 0.0, total);
-    }
-    __syncwarp();
   };
 
   // ---- base instances (placement.py:358-385), thread 0
@@ -423,8 +369,11 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
     }
   }
   __syncthreads();
-  for (int dev = threadIdx.x; dev < S.used; dev += blockDim.x) refresh_device(dev);  // devices in parallel
+  for (int dev = threadIdx.x; dev < S.used; dev += blockDim.x) refresh_base_device(dev);  // in parallel
   __syncthreads();
+#ifdef OPSC_PLACE_PROF
+  if (threadIdx.x == 0) S.ph[2] = clock64();
+#endif
   if (S.err) {
     if (threadIdx.x == 0) out.status[w] = S.err;
     return;
@@ -436,6 +385,9 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
     S.cur_wt[v] = o.wt; S.cur_teff[v] = o.t_eff; S.cur_wait[v] = o.wait; S.cur_stable[v] = o.stable;
   }
   __syncthreads();
+#ifdef OPSC_PLACE_PROF
+  if (threadIdx.x == 0) S.ph[3] = clock64();
+#endif
 
   // ---- extra replicas, heaviest op_latency first (-T, id, k)
   int xord[OPSC_MAX_OPS];
@@ -453,57 +405,56 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
       const double mem = S.mem[v], demand = S.dem[v];
       const double shf = nearbyint(demand * 100.0);
       const int share = shf < 1.0 ? 1 : (shf > 100.0 ? 100 : (int)shf);
-      __shared__ int s_best;
-      __shared__ double s_best_score;
-      if (threadIdx.x == 0) s_best = -1;
       // default-stream placement never shares: straight to take_unused.
-      // The device count is read once: thread 0 bumps S.used right after the
-      // loop, while other threads may still be evaluating its exit condition
-      // (compute-sanitizer racecheck; a fleet with a multiple of kMaxDevProbe
-      // used devices would otherwise split the CTA across __syncthreads).
+      // The device count is read once: thread 0 bumps S.used in the commit,
+      // while other threads may still be evaluating the chunk loop's exit
+      // condition (compute-sanitizer racecheck; a fleet with a multiple of
+      // kMaxDevProbe used devices would otherwise split the CTA across
+      // __syncthreads).
       const int n_used = S.used;
+      const double xg_max = 0.0 >= demand ? 0.0 : demand;  // the extra's (fresh) group maximum
+      int best_dev = -1;  // thread 0: best admissible device over the chunks
+      double best_score = 0.0;
 #ifdef OPSC_PLACE_PROF
-      long long q0 = clock64(), q1 = q0, q2 = q0, q3 = q0;
+      long long q0 = clock64(), q1 = q0, q2 = q0;
 #endif
       for (int c0 = 0; probe && c0 < n_used; c0 += kMaxDevProbe) {
       const int U = min(n_used - c0, kMaxDevProbe);
-      // stage 1: per-device admission + tentative group totals
+      // stage 1, one thread per device: admission (memory, standing SM load)
+      // and the standing load with the tentative replica -- extras own a fresh
+      // group (groups count up per extra replica), so dev_load with the extra
+      // is the device's cached sum plus one more term max(0, demand); the
+      // (device, operator) pairs to re-evaluate (operators with a replica
+      // there) are appended to a compact work list, so that stage 2 spreads
+      // the Erlang chains over the CTA instead of over a (device x op) grid
+      // where most items are empty and the warps run in lockstep
       for (int dj = threadIdx.x; dj < U; dj += blockDim.x) {
         const int dev = c0 + dj;
         const double mu = dev_mem(dev);
-        bool ok = !(mu + mem > f.mem_cap[dev]);
-        // standing load, and with the tentative replica appended: extras own a
-        // fresh group (groups count up per extra replica), so dev_load with the
-        // extra is the device's cached sum plus one more term max(0, demand)
         const PySum ls = cached_load(P, dev);
         const double load = ls.value();
-        ok = ok && !(load + demand > f.max_sm_load);
-        const double xg_max = 0.0 >= demand ? 0.0 : demand;
+        const bool ok = !(mu + mem > f.mem_cap[dev]) && !(load + demand > f.max_sm_load);
+        S.dev_ok[dj] = ok;
+        S.dev_load0[dj] = load;
+        if (!ok) continue;
         PySum lt = ls;
         lt.add(xg_max);
         const double total = lt.value();
-        S.on_dev[dj] = P.dev_mask[dev] | (1u << v);
         S.dev_total[dj] = total;
-        S.dev_load0[dj] = load;
         S.dev_xf[dj] = interference(f, total - xg_max, demand);
-        S.dev_ok[dj] = ok;
+        uint32_t m = P.dev_mask[dev] | (1u << v);
+        int at = atomicAdd(&S.n_items, __popc(m));
+        for (; m; m &= m - 1) S.items[at++] = (uint16_t)(dj << 5 | (__ffs(m) - 1));
       }
       __syncthreads();
-#ifdef OPSC_PLACE_PROF
-      q1 = clock64();
-#endif
-      // stage 2: (device, affected op) re-evaluations in parallel
-      for (int t = threadIdx.x; t < U * n; t += blockDim.x) {
-        const int dj = t / n, u = t - dj * n;
-        if (!S.dev_ok[dj]) continue;
-        if (!(S.on_dev[dj] >> u & 1u)) {
-          S.probe_wt[dj][u] = S.cur_stable[u] ? S.cur_wt[u] : OPSC_INF;
-          continue;
-        }
+      // stage 2: the listed (device, operator) re-evaluations in parallel
+      for (int it = threadIdx.x; it < S.n_items; it += blockDim.x) {
+        const int dj = S.items[it] >> 5, u = S.items[it] & 31;
+        const int dev = c0 + dj;
         const OpAdj o = adjust_op(d, f, P, S.rep_off, adev, u, S.p[u], S.r[u], S.b[u], S.T[u], S.comm[u], qps,
-                                  c0 + dj, group, demand, v, k, S.dev_xf[dj], S.dev_total[dj]);
+                                  dev, group, demand, v, k, S.dev_xf[dj], S.dev_total[dj]);
         S.probe_wt[dj][u] = o.stable ? o.wt : OPSC_INF;
-        const size_t pi = (size_t)(c0 + dj) * n + u;
+        const size_t pi = (size_t)dev * n + u;
         p_teff[pi] = o.t_eff;
         p_wait[pi] = o.wait;
         p_wt[pi] = o.wt;
@@ -511,7 +462,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
       }
       __syncthreads();
 #ifdef OPSC_PLACE_PROF
-      q2 = clock64();
+      q1 = clock64();
 #endif
       // stage 3: recomputed latency must meet the SLO (placement.py:434-438),
       // and the weighted slack score of every admissible device (:338-351)
@@ -520,8 +471,12 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
       double my_score = 0.0;
       for (int dj = threadIdx.x; dj < U; dj += blockDim.x) {
         if (!S.dev_ok[dj]) continue;
+        const uint32_t m = P.dev_mask[c0 + dj] | (1u << v);  // operators stage 2 re-evaluated
         bool fin = true;
-        for (int u = 0; u < n; ++u) fin &= S.probe_wt[dj][u] != OPSC_INF;
+        for (int u = 0; u < n; ++u) {
+          if (!(m >> u & 1u)) S.probe_wt[dj][u] = S.cur_stable[u] ? S.cur_wt[u] : OPSC_INF;
+          fin &= S.probe_wt[dj][u] != OPSC_INF;
+        }
         const double lat = fin ? dp_latency(d, S.probe_wt[dj]) : OPSC_INF;
         if (lat > slo) {
           S.dev_ok[dj] = 0;
@@ -540,65 +495,76 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
       // best score, ties to the lowest device id: a block-wide (score, -dj)
       // maximum -- the reference's in-order scan with a strict '>' -- unless a
       // score is NaN, where only the literal scan reproduces it (thread 0)
-      {
-        const bool any_nan = __syncthreads_or(nan_score);
-        for (int o = 16; o > 0; o >>= 1) {
-          const double os = __shfl_xor_sync(0xffffffffu, my_score, o);
-          const int od = __shfl_xor_sync(0xffffffffu, my_dj, o);
-          if (od >= 0 && (my_dj < 0 || os > my_score || (os == my_score && od < my_dj))) {
-            my_score = os;
-            my_dj = od;
-          }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double os = __shfl_xor_sync(0xffffffffu, my_score, o);
+        const int od = __shfl_xor_sync(0xffffffffu, my_dj, o);
+        if (od >= 0 && (my_dj < 0 || os > my_score || (os == my_score && od < my_dj))) {
+          my_score = os;
+          my_dj = od;
         }
-        if ((threadIdx.x & 31) == 0) {
-          S.red_score[threadIdx.x >> 5] = my_score;
-          S.red_dj[threadIdx.x >> 5] = my_dj;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          int bd = -1;
-          double bs = 0.0;
-          if (any_nan) {
-            for (int dj = 0; dj < U; ++dj)
-              if (S.dev_ok[dj] && (bd < 0 || S.dev_score[dj] > bs)) { bd = dj; bs = S.dev_score[dj]; }
-          } else {
-            for (int wi = 0; wi < kPlaceThreads / 32; ++wi) {
-              const int od = S.red_dj[wi];
-              const double os = S.red_score[wi];
-              if (od >= 0 && (bd < 0 || os > bs || (os == bs && od < bd))) { bd = od; bs = os; }
-            }
-          }
-          // across device chunks: a later chunk wins only with a strictly greater score
-          if (bd >= 0 && (s_best < 0 || bs > s_best_score)) { s_best = c0 + bd; s_best_score = bs; }
-        }
-        __syncthreads();
       }
+      nan_score = __any_sync(0xffffffffu, nan_score);
+      if ((threadIdx.x & 31) == 0) {
+        S.red_score[threadIdx.x >> 5] = my_score;
+        S.red_dj[threadIdx.x >> 5] = nan_score ? -2 : my_dj;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        bool any_nan = false;
+        for (int wi = 0; wi < kPlaceThreads / 32; ++wi) any_nan |= S.red_dj[wi] == -2;
+        int bd = -1;
+        double bs = 0.0;
+        if (any_nan) {
+          for (int dj = 0; dj < U; ++dj)
+            if (S.dev_ok[dj] && (bd < 0 || S.dev_score[dj] > bs)) { bd = dj; bs = S.dev_score[dj]; }
+        } else {
+          for (int wi = 0; wi < kPlaceThreads / 32; ++wi) {
+            const int od = S.red_dj[wi];
+            const double os = S.red_score[wi];
+            if (od >= 0 && (bd < 0 || os > bs || (os == bs && od < bd))) { bd = od; bs = os; }
+          }
+        }
+        // across device chunks: a later chunk wins only with a strictly greater score
+        if (bd >= 0 && (best_dev < 0 || bs > best_score)) { best_dev = c0 + bd; best_score = bs; }
+        S.n_items = 0;  // stage 1's list, empty for the next chunk / extra (a barrier comes first)
+      }
+      if (c0 + kMaxDevProbe < n_used) __syncthreads();  // the next chunk reuses the stage arrays
       }
 #ifdef OPSC_PLACE_PROF
-      q3 = clock64();
+      q2 = clock64();
 #endif
       __shared__ int s_probed, s_fresh_same;
-      if (threadIdx.x < 32) {  // warp 0: lane 0 commits, the warp refreshes the device
-        if (threadIdx.x == 0) {
-          int best = s_best;
-          s_probed = best >= 0;
-          if (best >= 0) {
-            push(v, k, best, group, share);
-          } else if (S.used >= f.n_devices || S.used >= D) {
-            S.err = OPSC_W_FLEET_EXHAUSTED;
-          } else {
-            best = S.used++;
-            if (mem > f.mem_cap[best]) S.err = OPSC_W_INFEASIBLE_PLACEMENT;
-            else push(v, k, best, group, 100);
-          }
-          S.best = best;
+      if (threadIdx.x == 0) {  // commit (the thread that selected)
+        int best = best_dev;
+        s_probed = best >= 0;
+        if (best >= 0) {
+          push(v, k, best, group, share);
+        } else if (S.used >= f.n_devices || S.used >= D) {
+          S.err = OPSC_W_FLEET_EXHAUSTED;
+        } else {
+          best = S.used++;
+          if (mem > f.mem_cap[best]) S.err = OPSC_W_INFEASIBLE_PLACEMENT;
+          else push(v, k, best, group, 100);
         }
-        __syncwarp();
-        if (!S.err) refresh_device_warp(S.best);
-        // a replica placed alone on a fresh device gets factor 1.0 -- exactly
-        // the factor its operator's figures already counted it with while it
-        // was unplaced (adjust_op), so those figures are unchanged
-        if (threadIdx.x == 0) s_fresh_same = !S.err && !s_probed && P.dev_cnt[S.best] == 1 && P.a_fac[S.na - 1] == 1.0;
+        S.best = best;
+        if (!S.err) {
+          // the extra owns a fresh group, appended last in first-occurrence
+          // order: the device's standing load is its cached PySum plus one
+          // more term (what a from-scratch dev_load would build, and what
+          // stage 1 probed), the other members' group maxima are unchanged
+          PySum lt = cached_load(P, best);
+          lt.add(xg_max);
+          P.dev_lf[best] = lt.f;
+          P.dev_lc[best] = lt.c;
+          P.dev_ls[best] = lt.started ? 1 : 0;
+          P.a_gmax[S.na - 1] = xg_max;
+          S.ototal = lt.value();
+          // a replica placed alone on a fresh device gets factor 1.0 (the
+          // factor the loop below gives it) -- exactly the factor its
+          // operator's figures already counted it with while it was unplaced
+          // (adjust_op), so those figures are unchanged
+          s_fresh_same = !s_probed && P.dev_cnt[best] == 1 && interference(f, S.ototal - xg_max, demand) == 1.0;
+        }
       }
       __syncthreads();
       if (S.err) {
@@ -606,42 +572,72 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
         return;
       }
 #ifdef OPSC_PLACE_PROF
-      const long long q4 = clock64();
+      const long long q3 = clock64();
 #endif
-      // refresh the cached figures of ops with a replica on the chosen device
-      {
-        const int dev = S.best;
-        const uint32_t mask = P.dev_mask[dev];
-        for (int u = threadIdx.x; u < n && !s_fresh_same; u += blockDim.x) {
-          if (!(mask >> u & 1u)) continue;
-          if (s_probed) {  // the probe of this device computed exactly these figures
-            const size_t pi = (size_t)dev * n + u;
-            S.cur_wt[u] = p_wt[pi]; S.cur_teff[u] = p_teff[pi]; S.cur_wait[u] = p_wait[pi];
-            S.cur_stable[u] = p_ok[pi] != 0;
-            continue;
-          }
+      // every member's interference factor under the new load, in parallel
+      // over the assignments (member_factor with no extra); the cached figures
+      // of the ops with a replica on the chosen device: the probe of this
+      // device computed exactly these figures (same factors, same sums)
+      const int bdev = S.best;
+      for (int i = threadIdx.x; i < S.na; i += blockDim.x)
+        if (adev[i] == bdev) P.a_fac[i] = interference(f, S.ototal - P.a_gmax[i], P.a_dem[i]);
+      const uint32_t bmask = P.dev_mask[bdev];
+      if (s_probed) {
+        for (int u = threadIdx.x; u < n; u += blockDim.x) {
+          if (!(bmask >> u & 1u)) continue;
+          const size_t pi = (size_t)bdev * n + u;
+          S.cur_wt[u] = p_wt[pi]; S.cur_teff[u] = p_teff[pi]; S.cur_wait[u] = p_wait[pi];
+          S.cur_stable[u] = p_ok[pi] != 0;
+        }
+      }
+      __syncthreads();
+      if (!s_probed && !s_fresh_same) {  // a fresh device whose factor is not 1.0 (NaN demand)
+        for (int u = threadIdx.x; u < n; u += blockDim.x) {
+          if (!(bmask >> u & 1u)) continue;
           const OpAdj o = adjust_op(d, f, P, S.rep_off, adev, u, S.p[u], S.r[u], S.b[u], S.T[u], S.comm[u], qps, -1,
                                     -1, 0.0, -1, 0, 1.0, 0.0);
           S.cur_wt[u] = o.wt; S.cur_teff[u] = o.t_eff; S.cur_wait[u] = o.wait; S.cur_stable[u] = o.stable;
         }
+        __syncthreads();
       }
-      __syncthreads();
 #ifdef OPSC_PLACE_PROF
       if (threadIdx.x == 0) {
-        S.prof[0] += q1 - q0; S.prof[1] += q2 - q1; S.prof[2] += q3 - q2; S.prof[3] += q4 - q3;
-        S.prof[4] += clock64() - q4; S.prof[5] += 1;
+        S.prof[0] += q1 - q0; S.prof[1] += q2 - q1; S.prof[2] += q3 - q2; S.prof[3] += clock64() - q3;
+        S.prof[5] += 1; S.prof[6] += n_used;
       }
 #endif
     }
   }
 #ifdef OPSC_PLACE_PROF
-  if (threadIdx.x == 0 && w < 4)
-    printf("place w%d: %lld extras, stage1 %lld stage2 %lld stage3+score %lld commit %lld refresh %lld cycles\n", w,
-           S.prof[5], S.prof[0], S.prof[1], S.prof[2], S.prof[3], S.prof[4]);
+  if (threadIdx.x == 0) S.ph[4] = clock64();
 #endif
 
-  // ---- _finalize + metrics (thread 0)
-  if (threadIdx.x == 0) {
+  // ---- _finalize + metrics
+  // per assignment, in parallel: its op latency and its share of the request
+  // energy (metrics.py); the shares are kept in a_gmax, dead after the extras
+  double* a_sh = P.a_gmax;
+  for (int i = threadIdx.x; i < S.na; i += blockDim.x) {
+    const size_t o = (size_t)w * A + i;
+    const int u = P.a_op[i];
+    out.a_latency[o] = S.T[u] * P.a_fac[i];
+    const double layers = (double)d.layer_count[u];
+    double sh = ((f.alpha * (double)S.p[u]) * (S.cur_wait[u] + S.cur_teff[u])) * layers;
+    sh += ((f.beta * S.cur_teff[u]) * layers) / (double)S.r[u];
+    a_sh[i] = sh;
+  }
+  __syncthreads();
+  // per device, in parallel: the shares of its members added in assignment
+  // order (the device's list is in assignment order), as the reference's loop
+  // over the assignments adds each to its device's entry
+  for (int dev = threadIdx.x; dev < S.used; dev += blockDim.x) {
+    double e = 0.0;
+    for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) e += a_sh[i];
+    out.d_energy[(size_t)w * D + dev] = e;
+    out.d_mem[(size_t)w * D + dev] = dev_mem(dev);
+    out.d_sm[(size_t)w * D + dev] = cached_load(P, dev).value();
+  }
+  // the scalar sums, by one thread of the last warp (alongside the devices)
+  if (threadIdx.x == kPlaceThreads - 32) {
     bool all = true;
     for (int u = 0; u < n; ++u) all &= S.cur_stable[u];
     const double lat = all ? dp_latency(d, S.cur_wt) : OPSC_INF;
@@ -651,22 +647,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
     out.n_assign[w] = S.na;
     PySum memsum;
     memsum.reset();
-    double* de = out.d_energy + (size_t)w * D;
-    for (int dev = 0; dev < S.used; ++dev) {
-      out.d_mem[(size_t)w * D + dev] = dev_mem(dev);
-      out.d_sm[(size_t)w * D + dev] = cached_load(P, dev).value();
-      de[dev] = 0.0;
-    }
-    for (int i = 0; i < S.na; ++i) {
-      const size_t o = (size_t)w * A + i;
-      const int u = P.a_op[i];
-      out.a_latency[o] = S.T[u] * P.a_fac[i];
-      memsum.add(P.a_mem[i]);
-      const double layers = (double)d.layer_count[u];
-      double sh = ((f.alpha * (double)S.p[u]) * (S.cur_wait[u] + S.cur_teff[u])) * layers;
-      sh += ((f.beta * S.cur_teff[u]) * layers) / (double)S.r[u];
-      de[P.a_dev[i]] += sh;
-    }
+    for (int i = 0; i < S.na; ++i) memsum.add(P.a_mem[i]);
     out.memory[w] = memsum.value();
     double total = 0.0;
     for (int i = 0; i < n; ++i) {
@@ -678,6 +659,14 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
     }
     out.energy[w] = total;
   }
+#ifdef OPSC_PLACE_PROF
+  __syncthreads();
+  if (threadIdx.x == 0)
+    printf("phases w%d: setup %lld base %lld initial %lld extras %lld finalize %lld | %lld extras, %lld device probes, "
+           "stage1+2 %lld stage3+select %lld commit %lld refresh %lld\n", w, S.ph[1] - S.ph[0], S.ph[2] - S.ph[1],
+           S.ph[3] - S.ph[2], S.ph[4] - S.ph[3], clock64() - S.ph[4], S.prof[5], S.prof[6], S.prof[0], S.prof[1],
+           S.prof[2], S.prof[3]);
+#endif
 }
 
 size_t place_shared_workspace(int n_windows, int A, int D, int n) {
