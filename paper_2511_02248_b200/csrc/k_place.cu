@@ -27,12 +27,14 @@
 namespace opsc {
 
 constexpr int kPlaceThreads = 128;
+static_assert(kPlaceThreads == 128, "the extra-replica commit is split over exactly four warps");
 constexpr int kMaxDevProbe = 128;  // device probes per chunk held in smem
 constexpr size_t kPlaceSmemMax = 200 * 1024;  // static PShared + per-window workspace
 
 struct PlaceArgs {
   OpscDag d;
   OpscPlaceShared f;
+  int probe_smem;  // the probe store of the first kMaxDevProbe devices fits in shared memory
 };
 
 struct PWork {  // per-window workspace (shared memory when it fits, else global)
@@ -61,6 +63,23 @@ struct PWork {  // per-window workspace (shared memory when it fits, else global
 // device's entries ARE the operators' new figures (same factors, same sums)
 __host__ __device__ inline size_t probe_bytes(int D, int n) {
   return (((size_t)D * n * (8 + 8 + 8 + 1)) + 15) & ~(size_t)15;
+}
+
+struct ProbeStore {
+  double* teff;
+  double* wait;
+  double* wt;
+  uint8_t* ok;
+};
+
+// the store's arrays for `devs` devices, indexed [device * n + op]
+__device__ __forceinline__ ProbeStore probe_store(unsigned char* base, int devs, int n) {
+  ProbeStore p;
+  p.teff = reinterpret_cast<double*>(base);
+  p.wait = p.teff + (size_t)devs * n;
+  p.wt = p.wait + (size_t)devs * n;
+  p.ok = reinterpret_cast<uint8_t*>(p.wt + (size_t)devs * n);
+  return p;
 }
 
 __host__ __device__ inline size_t pw_bytes(int A, int D, int n) {
@@ -230,15 +249,16 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
   const int L = win.seq_len[w], ph = win.phase[w];
   const double slo = (f.flags & OPSC_PLACE_WINDOW_SLO) ? win.slo[w] : f.slo;
   const bool probe = !(f.flags & OPSC_PLACE_DEFAULT_STREAM);
+  const bool chain = is_chain(d);  // stage 3's critical path without the DAG walk
   // the window's assignment lists / device tables are walked by every probe:
   // in shared memory when they fit (smem_ws), else in its global slice
   // (SMEM: a compile-time choice, so the walks compile to shared-memory loads)
   unsigned char* wbase = ws + (size_t)w * (pw_bytes(A, D, n) + probe_bytes(D, n));
   PWork P = carve(SMEM ? pw_smem : wbase, A, D);
-  double* p_teff = reinterpret_cast<double*>(wbase + pw_bytes(A, D, n));
-  double* p_wait = p_teff + (size_t)D * n;
-  double* p_wt = p_wait + (size_t)D * n;
-  uint8_t* p_ok = reinterpret_cast<uint8_t*>(p_wt + (size_t)D * n);
+  const ProbeStore pg = probe_store(wbase + pw_bytes(A, D, n), D, n);
+  // while no more than kMaxDevProbe devices are in use, the probe store in
+  // shared memory (behind the workspace) when the launch reserved it
+  const ProbeStore pss = probe_store(pw_smem + pw_bytes(A, D, n), kMaxDevProbe, n);
   const int32_t* adev = P.a_dev;
   if (threadIdx.x == 0) {
     S.rep_off[0] = 0;
@@ -411,9 +431,13 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
       // condition (compute-sanitizer racecheck; a fleet with a multiple of
       // kMaxDevProbe used devices would otherwise split the CTA across
       // __syncthreads).
-      const int n_used = S.used;
+      const int n_used = S.used, na0 = S.na;  // both change only in the commit below
+      // without probes (default stream) no stage barrier separates these reads
+      // and the previous extra's flags from this extra's commit
+      if (!probe) __syncthreads();
+      const ProbeStore ps = SMEM && a.probe_smem && n_used <= kMaxDevProbe ? pss : pg;
       const double xg_max = 0.0 >= demand ? 0.0 : demand;  // the extra's (fresh) group maximum
-      int best_dev = -1;  // thread 0: best admissible device over the chunks
+      int best_dev = -1;  // lane 0 of every warp: best admissible device over the chunks
       double best_score = 0.0;
 #ifdef OPSC_PLACE_PROF
       long long q0 = clock64(), q1 = q0, q2 = q0;
@@ -455,10 +479,10 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
                                   dev, group, demand, v, k, S.dev_xf[dj], S.dev_total[dj]);
         S.probe_wt[dj][u] = o.stable ? o.wt : OPSC_INF;
         const size_t pi = (size_t)dev * n + u;
-        p_teff[pi] = o.t_eff;
-        p_wait[pi] = o.wait;
-        p_wt[pi] = o.wt;
-        p_ok[pi] = o.stable;
+        ps.teff[pi] = o.t_eff;
+        ps.wait[pi] = o.wait;
+        ps.wt[pi] = o.wt;
+        ps.ok[pi] = o.stable;
       }
       __syncthreads();
 #ifdef OPSC_PLACE_PROF
@@ -473,11 +497,23 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
         if (!S.dev_ok[dj]) continue;
         const uint32_t m = P.dev_mask[c0 + dj] | (1u << v);  // operators stage 2 re-evaluated
         bool fin = true;
-        for (int u = 0; u < n; ++u) {
-          if (!(m >> u & 1u)) S.probe_wt[dj][u] = S.cur_stable[u] ? S.cur_wt[u] : OPSC_INF;
-          fin &= S.probe_wt[dj][u] != OPSC_INF;
+        double lat;
+        if (chain) {  // dp_latency's operations on a chain, in registers
+          double x = 0.0;
+          for (int i = 0; i < n; ++i) {
+            const int u = d.topo[i];
+            const double wt = (m >> u & 1u) ? S.probe_wt[dj][u] : (S.cur_stable[u] ? S.cur_wt[u] : OPSC_INF);
+            fin &= wt != OPSC_INF;
+            x = fmax(0.0, x) + wt;
+          }
+          lat = fin ? fmax(0.0, x) : OPSC_INF;
+        } else {
+          for (int u = 0; u < n; ++u) {
+            if (!(m >> u & 1u)) S.probe_wt[dj][u] = S.cur_stable[u] ? S.cur_wt[u] : OPSC_INF;
+            fin &= S.probe_wt[dj][u] != OPSC_INF;
+          }
+          lat = fin ? dp_latency(d, S.probe_wt[dj]) : OPSC_INF;
         }
-        const double lat = fin ? dp_latency(d, S.probe_wt[dj]) : OPSC_INF;
         if (lat > slo) {
           S.dev_ok[dj] = 0;
           continue;
@@ -509,7 +545,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
         S.red_dj[threadIdx.x >> 5] = nan_score ? -2 : my_dj;
       }
       __syncthreads();
-      if (threadIdx.x == 0) {
+      if ((threadIdx.x & 31) == 0) {  // every warp's lane 0 selects (the same device): all commit below
         bool any_nan = false;
         for (int wi = 0; wi < kPlaceThreads / 32; ++wi) any_nan |= S.red_dj[wi] == -2;
         int bd = -1;
@@ -526,28 +562,57 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
         }
         // across device chunks: a later chunk wins only with a strictly greater score
         if (bd >= 0 && (best_dev < 0 || bs > best_score)) { best_dev = c0 + bd; best_score = bs; }
-        S.n_items = 0;  // stage 1's list, empty for the next chunk / extra (a barrier comes first)
       }
+      if (threadIdx.x == 0) S.n_items = 0;  // stage 1's list, empty for the next chunk / extra (a barrier comes first)
       if (c0 + kMaxDevProbe < n_used) __syncthreads();  // the next chunk reuses the stage arrays
       }
 #ifdef OPSC_PLACE_PROF
       q2 = clock64();
 #endif
       __shared__ int s_probed, s_fresh_same;
-      if (threadIdx.x == 0) {  // commit (the thread that selected)
-        int best = best_dev;
-        s_probed = best >= 0;
-        if (best >= 0) {
-          push(v, k, best, group, share);
-        } else if (S.used >= f.n_devices || S.used >= D) {
-          S.err = OPSC_W_FLEET_EXHAUSTED;
-        } else {
-          best = S.used++;
-          if (mem > f.mem_cap[best]) S.err = OPSC_W_INFEASIBLE_PLACEMENT;
-          else push(v, k, best, group, 100);
+      // commit: the lane 0 of each warp takes the same decision (best device,
+      // or the next unused one: take_unused) from the same state and writes
+      // its part of the push, so the four parts run side by side
+      if ((threadIdx.x & 31) == 0) {
+        const bool probed = best_dev >= 0;
+        int best = best_dev, err = 0;
+        if (!probed) {
+          if (n_used >= f.n_devices || n_used >= D) err = OPSC_W_FLEET_EXHAUSTED;
+          else if (mem > f.mem_cap[best = n_used]) err = OPSC_W_INFEASIBLE_PLACEMENT;
         }
-        S.best = best;
-        if (!S.err) {
+        const int i = na0, part = threadIdx.x >> 5;
+        if (part == 0) {  // status, the assignment's list entry and index tables
+          S.err = err;
+          S.best = best;
+          s_probed = probed;
+          if (!probed) S.used = n_used + 1;
+          if (!err) {
+            S.na = i + 1;
+            P.a_group[i] = group;
+            P.a_next[i] = -1;
+            const int tail = P.dev_tail[best];
+            if (tail >= 0) P.a_next[tail] = i;
+            else P.dev_head[best] = i;
+            P.dev_tail[best] = i;
+            P.dev_cnt[best] += 1;
+            P.rep[S.rep_off[v] + k - 1] = i;
+            P.a_op[i] = v;
+            P.a_dev[i] = best;
+          }
+        } else if (part == 1 && !err) {  // device memory: Python sum over members in order
+          P.a_dem[i] = demand;
+          P.a_mem[i] = mem;
+          P.a_fac[i] = 1.0;  // (overwritten with the device's other members after the barrier)
+          if (!probed) {  // a fresh device: its first member
+            P.dev_mem_f[best] = 0.0 + mem;
+            P.dev_mem_c[best] = 0.0;
+          } else {
+            const double fs = P.dev_mem_f[best], t = fs + mem;
+            if (fabs(fs) >= fabs(mem)) P.dev_mem_c[best] += (fs - t) + mem;
+            else P.dev_mem_c[best] += (mem - t) + fs;
+            P.dev_mem_f[best] = t;
+          }
+        } else if (part == 2 && !err) {
           // the extra owns a fresh group, appended last in first-occurrence
           // order: the device's standing load is its cached PySum plus one
           // more term (what a from-scratch dev_load would build, and what
@@ -557,13 +622,20 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
           P.dev_lf[best] = lt.f;
           P.dev_lc[best] = lt.c;
           P.dev_ls[best] = lt.started ? 1 : 0;
-          P.a_gmax[S.na - 1] = xg_max;
+          P.a_gmax[i] = xg_max;
           S.ototal = lt.value();
           // a replica placed alone on a fresh device gets factor 1.0 (the
           // factor the loop below gives it) -- exactly the factor its
           // operator's figures already counted it with while it was unplaced
           // (adjust_op), so those figures are unchanged
-          s_fresh_same = !s_probed && P.dev_cnt[best] == 1 && interference(f, S.ototal - xg_max, demand) == 1.0;
+          s_fresh_same = !probed && interference(f, S.ototal - xg_max, demand) == 1.0;
+        } else if (part == 3 && !err) {  // the output row and the device's operator mask
+          P.dev_mask[best] |= 1u << v;
+          const size_t o = (size_t)w * A + i;
+          out.a_op[o] = (int8_t)v;
+          out.a_replica[o] = (int16_t)k;
+          out.a_device[o] = best;
+          out.a_share[o] = (int16_t)(probed ? share : 100);
         }
       }
       __syncthreads();
@@ -586,8 +658,8 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
         for (int u = threadIdx.x; u < n; u += blockDim.x) {
           if (!(bmask >> u & 1u)) continue;
           const size_t pi = (size_t)bdev * n + u;
-          S.cur_wt[u] = p_wt[pi]; S.cur_teff[u] = p_teff[pi]; S.cur_wait[u] = p_wait[pi];
-          S.cur_stable[u] = p_ok[pi] != 0;
+          S.cur_wt[u] = ps.wt[pi]; S.cur_teff[u] = ps.teff[pi]; S.cur_wait[u] = ps.wait[pi];
+          S.cur_stable[u] = ps.ok[pi] != 0;
         }
       }
       __syncthreads();
@@ -683,8 +755,10 @@ cudaError_t launch_place_shared(const OpscDag& d, const OpscPlaceShared& f, Opsc
   a.d = d;
   a.f = f;
   const size_t pw = pw_bytes(out.cap_assign, out.cap_dev, d.n_ops);
+  const size_t pss = probe_bytes(kMaxDevProbe, d.n_ops);
   const bool smem_ws = pw + sizeof(PShared) + 1024 <= kPlaceSmemMax;
-  const size_t dyn = smem_ws ? pw : 0;
+  a.probe_smem = smem_ws && pw + pss + sizeof(PShared) + 1024 <= kPlaceSmemMax;
+  const size_t dyn = smem_ws ? pw + (a.probe_smem ? pss : 0) : 0;
   // static PShared + dynamic workspace may pass the 48 KB default: raise the
   // kernel's dynamic limit (once per size increase, per device)
   static int set_dyn[64];

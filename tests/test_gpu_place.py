@@ -118,3 +118,28 @@ def test_gpu_place_odd_workspace_strides(orc):
                 g[bad] = 0  # a failed window's slots are unspecified (only status counts)
                 c[bad] = 0
                 assert g.tobytes() == c.tobytes(), (n_dev, ds, f)
+
+
+@pytest.mark.parametrize("n_dev", [600, 4096])
+def test_gpu_place_more_devices_than_a_probe_chunk(orc, n_dev):
+    """Windows whose plans use more devices than one probe chunk holds
+    (kMaxDevProbe = 128: the extras probe the fleet in chunks, the best score
+    carried across them), with the per-window workspace in shared memory
+    (600 devices) and in global memory (4096 devices), against the oracle."""
+    from paper_2511_02248_b200 import _native
+    prob = tables.pack_problem(*scenarios.scenario("cfg2"))
+    tw = scenarios.trace_windows("cfg2")
+    idx = np.argsort(tw["prefill_qps"])[-4:]
+    win = tables.window_arrays(tw["prefill_qps"][idx] * 4.0, tw["prefill_len"][idx], 0, 2.0)
+    prm = model.AutoscaleParams(slo=2.0)
+    dec = _native.plan_windows_host(abi.MODE_OPERATOR, prob, win, model=tables.pack_model(prob, prm),
+                                    greedy=tables.pack_greedy(prob, prm))
+    devs = [model.DeviceSpec(id=f"g{i:04d}", mem_cap=80e9) for i in range(n_dev)]
+    for ds in (False, True):
+        fleet = placement.SharedFleet(devs, 2.0, model.InterferenceParams(0.5, 1.0), model.EnergyParams(),
+                                      default_stream=ds)
+        gpu = placement.place_windows(prob, win, dec.cfg, dec.feasible, fleet, 1)
+        cpu = orc.place_shared(prob, win, dec.cfg, dec.feasible, fleet, 1)
+        assert (cpu.status == 0).all() and cpu.devices_used.min() > 128
+        for f in placement.PlacementArrays.FIELDS:
+            assert getattr(gpu, f).tobytes() == getattr(cpu, f).tobytes(), (n_dev, ds, f)
