@@ -206,7 +206,7 @@ __device__ __forceinline__ GPt gpoint(const GreedyArgs& a, int w, double qps, in
   return GPt{weight(o, a.d.layer_count[v]), o.wait + o.service, o.stable};
 }
 
-__device__ __forceinline__ void set_path_warp(GShared& S, const OpscDag& d);
+__device__ __noinline__ void set_path_warp(GShared& S, const OpscDag& d);
 
 // full evaluation of the current configs (all threads; ends synchronised)
 __device__ __noinline__ void eval_full(GShared& S, const GreedyArgs& a, int w, double qps, int L, int ph) {
@@ -370,8 +370,10 @@ __device__ __forceinline__ int move_index(const GShared& S, int op, int b_lo, in
 }
 
 // Block-wide minimum of NK keys per thread (warp shuffles, then one warp
-// over the per-warp minima). All threads; result in out[] on every thread.
-template <int NK>
+// over the per-warp minima). The kCore threads; the result in x[] on every
+// thread (W0: on warp 0 only -- the steps' commit runs there -- and no
+// closing barrier: the buffer is next written after the step's end)
+template <int NK, bool W0 = false>
 __device__ void block_min(PK (&x)[NK]) {  // the kCore threads
   __shared__ PK red[kCore / 32][NK];
   for (int off = 16; off > 0; off >>= 1) {
@@ -386,6 +388,7 @@ __device__ void block_min(PK (&x)[NK]) {  // the kCore threads
 #pragma unroll
     for (int k = 0; k < NK; ++k) red[warp][k] = x[k];
   core_sync();
+  if (W0 && warp != 0) return;
 #pragma unroll
   for (int k = 0; k < NK; ++k) {
     PK v = red[0][k];
@@ -393,7 +396,7 @@ __device__ void block_min(PK (&x)[NK]) {  // the kCore threads
       if (pk_less(red[w2][k], v)) v = red[w2][k];
     x[k] = v;
   }
-  core_sync();
+  if (!W0) core_sync();
 }
 
 // warp 0 (all lanes): set_path's results with the serial parts spread over
@@ -401,7 +404,10 @@ __device__ void block_min(PK (&x)[NK]) {  // the kCore threads
 // right in every lane (lane i keeps the DP value of position i), the
 // bottleneck as a warp (sojourn, -id) max (literal scan if a sojourn is
 // NaN), the non-negativity check as a vote. Same values as set_path.
-__device__ __forceinline__ void set_path_warp(GShared& S, const OpscDag& d) {
+// Out of line: one copy serves the step commits, the prune pass and
+// eval_full (the kernel's code is larger than the instruction cache, and a
+// step's serial tail runs cold code otherwise).
+__device__ __noinline__ void set_path_warp(GShared& S, const OpscDag& d) {
   const int lane = threadIdx.x & 31, n = d.n_ops;
   if (S.chain) {
     const int u = lane < n ? d.topo[lane] : 0;
@@ -545,7 +551,7 @@ __device__ __forceinline__ void upscale_core(GShared& S, const GreedyArgs& a, co
 #ifdef OPSC_GREEDY_PROF
   const long long u2 = clock64();
 #endif
-  block_min<3>(k);
+  block_min<3, true>(k);
 #ifdef OPSC_GREEDY_PROF
   const long long u3 = clock64();
 #endif
@@ -554,14 +560,23 @@ __device__ __forceinline__ void upscale_core(GShared& S, const GreedyArgs& a, co
     const int m = pk_valid(pick) ? move_index(S, op, 1, pk_b(pick), pk_p(pick)) : -1;
     if (threadIdx.x == 0) S.applied = m >= 0;
     if (m >= 0) {
+#if defined(OPSC_GREEDY_PROF) && defined(OPSC_GREEDY_PROF_STEPS)
+      const long long a0 = clock64();
+#endif
       apply_move_warp(S, a, w, op, m, cur_r + 1, 1, m0, qps, L, ph);
+#if defined(OPSC_GREEDY_PROF) && defined(OPSC_GREEDY_PROF_STEPS)
+      const long long a1 = clock64();
+#endif
       const int obj = objective_warp(S, a.d.n_ops);
       if (threadIdx.x == 0)
         push_trace(S, out, w, headroom ? OPSC_ACT_HEADROOM : OPSC_ACT_UPSCALE, op, S.r[op], S.b[op], S.p[op],
                    S.lat, obj);
+#if defined(OPSC_GREEDY_PROF) && defined(OPSC_GREEDY_PROF_STEPS)
+      if (threadIdx.x == 0) printf("    apply: pick %lld move+path %lld trace %lld\n", a0 - u3, a1 - a0, clock64() - a1);
+#endif
     }
   }
-#ifdef OPSC_GREEDY_PROF
+#if defined(OPSC_GREEDY_PROF) && defined(OPSC_GREEDY_PROF_STEPS)  // per-step split (slows the loop)
   if (threadIdx.x == 0)
     printf("  up step op %d r %d M %d: eval %lld keys %lld reduce %lld apply %lld cycles\n", op, cur_r + 1, M,
            u1 - u0, u2 - u1, u3 - u2, clock64() - u3);
@@ -607,7 +622,7 @@ __device__ __forceinline__ void downscale_core(GShared& S, const GreedyArgs& a, 
     m0 += kMaxMoves;
   } while (m0 < M);
   m0 -= kMaxMoves;
-  block_min<1>(k);
+  block_min<1, true>(k);
   if (threadIdx.x < 32) {
     const int best = pk_valid(k[0]) ? move_index(S, op, cur_b, pk_b(k[0]), pk_p(k[0])) : -1;
     if (threadIdx.x == 0) S.applied = best >= 0;
