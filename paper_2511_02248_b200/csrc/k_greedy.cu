@@ -721,6 +721,7 @@ __device__ __noinline__ void prune_pass(GShared& S, const GreedyArgs& a, const O
     if (threadIdx.x < 32) {
       const int lane = threadIdx.x, n = d.n_ops;
       bool any = false;
+      int obj = objective_warp(S, n);  // kept current per accepted prune (-P_v, exact)
       for (int start = 0; start < n;) {
         const bool cand = lane >= start && lane < n && S.r[lane] > 1 && t_ok[lane];
         double lat = OPSC_INF;
@@ -739,10 +740,9 @@ __device__ __noinline__ void prune_pass(GShared& S, const GreedyArgs& a, const O
           S.lat = lv;
           S.cpv_ok = 0;
           t_need[v] = 1;
+          push_trace(S, out, w, OPSC_ACT_PRUNE, v, S.r[v], S.b[v], S.p[v], S.lat, obj - S.p[v]);
         }
-        __syncwarp();
-        const int obj = objective_warp(S, n);
-        if (lane == 0) push_trace(S, out, w, OPSC_ACT_PRUNE, v, S.r[v], S.b[v], S.p[v], S.lat, obj);
+        obj -= S.p[v];  // R_v dropped by one, P_v unchanged
         __syncwarp();
         any = true;
         start = v + 1;
