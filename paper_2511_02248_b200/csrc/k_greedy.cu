@@ -402,8 +402,8 @@ __device__ void block_min(PK (&x)[NK]) {  // the kCore threads
 // warp 0 (all lanes): set_path's results with the serial parts spread over
 // the lanes -- a chain's weights gathered by shuffles and summed left to
 // right in every lane (lane i keeps the DP value of position i), the
-// bottleneck as a warp (sojourn, -id) max (literal scan if a sojourn is
-// NaN), the non-negativity check as a vote. Same values as set_path.
+// bottleneck as a warp (sojourn, -id) max by integer reductions (literal
+// scan if a sojourn is NaN), the non-negativity check as a vote. Same values as set_path.
 // Out of line: one copy serves the step commits, the prune pass and
 // eval_full (the kernel's code is larger than the instruction cache, and a
 // step's serial tail runs cold code otherwise).
@@ -430,16 +430,16 @@ __device__ __noinline__ void set_path_warp(GShared& S, const OpscDag& d) {
   const int v = lane < n ? S.path[lane] : -1;
   const double sj = v >= 0 ? S.soj[v] : 0.0;
   const bool nan = __any_sync(0xffffffffu, v >= 0 && sj != sj);
-  int bv = v;
-  double bs = sj;
-  for (int o = 16; o > 0; o >>= 1) {
-    const int ov = __shfl_xor_sync(0xffffffffu, bv, o);
-    const double os = __shfl_xor_sync(0xffffffffu, bs, o);
-    if (ov >= 0 && (bv < 0 || os > bs || (os == bs && ov < bv))) {
-      bv = ov;
-      bs = os;
-    }
-  }
+  // (sojourn, -id) maximum as three warp reductions over an order-preserving
+  // integer image of the sojourn: the highest word, then the low word among
+  // those, then the lowest id among the equal ones (-0.0 is folded into +0.0,
+  // they compare equal as doubles; a NaN takes the literal scan below)
+  const long long sb = __double_as_longlong(sj + 0.0);
+  const unsigned long long key = sb < 0 ? ~(unsigned long long)sb : (unsigned long long)sb | 0x8000000000000000ull;
+  const unsigned hi = v >= 0 ? (unsigned)(key >> 32) : 0u, lo = v >= 0 ? (unsigned)key : 0u;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  const int bv = (int)__reduce_min_sync(0xffffffffu, v >= 0 && hi == mh && lo == ml ? (unsigned)v : 0xffffffffu);
   const bool nonneg = __all_sync(0xffffffffu, lane >= n || S.wt[lane] >= 0.0);
   if (lane == 0) {
     S.bneck = nan ? bottleneck(S, n) : bv;
