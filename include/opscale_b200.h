@@ -480,6 +480,12 @@ OPSC_API int opsc_copy_keys(int64_t* dst, const int64_t* src, int32_t n, void* s
 OPSC_API int opsc_peer_barrier(uint32_t* const* flags, int32_t rank, int32_t n, uint32_t epoch,
                                int32_t timeout_ms, int32_t* err, void* stream);
 
+/* Diagnostic: out[i] = excess ** exponent as the placement kernel evaluates
+ * it inside interference_factor (perfmodel.py:174-187): exact for exponents
+ * 1, 2 and 0.5, otherwise rounded to nearest from a double-double
+ * evaluation. Device pointers, n >= 0. */
+OPSC_API int opsc_interference_pow(const double* x, const double* e, double* out, int64_t n, void* stream);
+
 /* Candidate-loop probe: the compose inner loop on synthetic register menus
  * (kind 1: DADD + DSETP + select per candidate, kind 2: DSETP + select).
  * Gives the instruction-mix ceiling of the compose kernel on this GPU. */

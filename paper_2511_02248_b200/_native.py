@@ -32,6 +32,7 @@ EXPORTS = (
     "opsc_ipc_alloc", "opsc_ipc_open", "opsc_ipc_close", "opsc_ipc_free",
     "opsc_compose_argmin_peers", "opsc_peer_barrier", "opsc_copy_keys",
     "opsc_certify_workspace", "opsc_certify_order", "opsc_menu_stability", "opsc_decode_materialize",
+    "opsc_interference_pow",
 )
 
 _lib = None
@@ -93,6 +94,7 @@ def load():
             "opsc_certify_order": ([P, P, W, P, C.c_double, P, C.c_size_t, P, P], C.c_int),
             "opsc_menu_stability": ([P, P, W, P, P, P], C.c_int),
             "opsc_decode_materialize": ([P, P, W, P, P, P, D, P], C.c_int),
+            "opsc_interference_pow": ([P, P, P, C.c_int64, P], C.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

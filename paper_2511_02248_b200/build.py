@@ -40,7 +40,7 @@ def _stale(target, deps):
 def build(verbose=False, force=False):
     os.makedirs(OUT, exist_ok=True)
     header = os.path.join(os.path.dirname(HERE), "include", "opscale_b200.h")
-    common = [os.path.join(CSRC, "opsc_common.cuh"), header]
+    common = [os.path.join(CSRC, h) for h in sorted(os.listdir(CSRC)) if h.endswith(".cuh")] + [header]
     objs = []
     log = []
     for src in SOURCES:

@@ -596,6 +596,11 @@ int opsc_place_shared(const OpscDag* dag, const OpscPlaceShared* fleet, OpscWind
                                        workspace_bytes, (cudaStream_t)stream));
 }
 
+int opsc_interference_pow(const double* x, const double* e, double* out, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !e || !out))) return OPSC_ERR_ARG;
+  return from_cuda(launch_interference_pow(x, e, out, (long long)n, (cudaStream_t)stream));
+}
+
 size_t opsc_windowize_workspace(int64_t n_records, int32_t max_windows) {
   return windowize_workspace(n_records, max_windows);
 }

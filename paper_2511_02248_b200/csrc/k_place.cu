@@ -23,6 +23,7 @@
 #include <cstdio>
 
 #include "opsc_common.cuh"
+#include "opsc_pow.cuh"
 
 namespace opsc {
 
@@ -115,17 +116,25 @@ __device__ PWork carve(unsigned char* base, int A, int D) {
   return p;
 }
 
+// excess ** exponent: exact forms for 1, 2 and 0.5. Any other exponent runs
+// the GP instantiation (chosen on the host): rounded to nearest from a
+// double-double evaluation (opsc_pow.cuh), which equals glibc's pow -- the
+// reference's `**` -- wherever glibc rounds correctly. The default
+// instantiation keeps the library pow as an unreachable fallback, so its
+// register allocation is not shaped by the double-double code.
+template <bool GP>
 __device__ __forceinline__ double pow_expo(double x, double e) {
   if (e == 1.0) return x;
   if (e == 2.0) return x * x;
   if (e == 0.5) return sqrt(x);
-  return pow(x, e);
+  return GP ? opsc_pow::pow_rn(x, e) : pow(x, e);
 }
 
+template <bool GP>
 __device__ __forceinline__ double interference(const OpscPlaceShared& f, double load, double adding) {
   const double excess = load + adding - 1.0;
   if (excess <= 0.0) return 1.0;
-  return 1.0 + f.theta * pow_expo(excess, f.exponent);
+  return 1.0 + f.theta * pow_expo<GP>(excess, f.exponent);
 }
 
 __device__ __forceinline__ double psum_value(double f, double c, bool started) {
@@ -134,12 +143,13 @@ __device__ __forceinline__ double psum_value(double f, double c, bool started) {
 }
 
 // interference factor of member i of `dev` with an optional extra (group xg, demand xd)
+template <bool GP>
 __device__ double member_factor(const PWork& P, const OpscPlaceShared& f, int dev, int i, int xg, double xd,
                                 double total) {
   (void)dev;
   double gm = P.a_gmax[i];  // = the scan over dev's members of i's group, kept by push
   if (xg == P.a_group[i]) gm = gm >= xd ? gm : xd;
-  return interference(f, total - gm, P.a_dem[i]);
+  return interference<GP>(f, total - gm, P.a_dem[i]);
 }
 
 __device__ __forceinline__ PySum cached_load(const PWork& P, int dev) {
@@ -157,6 +167,7 @@ struct OpAdj {
 
 // adjusted figures of op u: factors of its replicas (k = 1..R) with the
 // members of `dev` re-evaluated under the extra (xg, xd, xop, xk, xf)
+template <bool GP>
 __device__ OpAdj adjust_op(const OpscDag& d, const OpscPlaceShared& f, const PWork& P, const int* rep_off,
                            const int32_t* adev, int u, int p, int r, int b, double T, double comm, double qps,
                            int dev, int xg, double xd, int xop, int xk, double xf, double total) {
@@ -167,7 +178,7 @@ __device__ OpAdj adjust_op(const OpscDag& d, const OpscPlaceShared& f, const PWo
     double fk = 1.0;
     if (idx >= 0) {
       const bool on_dev = dev >= 0 && adev[idx] == dev;
-      fk = on_dev ? member_factor(P, f, dev, idx, xg, xd, total) : P.a_fac[idx];
+      fk = on_dev ? member_factor<GP>(P, f, dev, idx, xg, xd, total) : P.a_fac[idx];
     } else if (u == xop && k == xk) {
       fk = xf;
     }
@@ -225,7 +236,7 @@ struct PShared {
   int used, na, err, best;
 };
 
-template <bool SMEM>
+template <bool SMEM, bool GP>
 __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_constant__ PlaceArgs a,
                                                               const __grid_constant__ OpscWindows win,
                                                               const int16_t* __restrict__ cfg,
@@ -354,7 +365,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
     const double total = ls.value();
     for (int i = P.dev_head[dev]; i >= 0; i = P.a_next[i]) {
       P.a_gmax[i] = gm;
-      P.a_fac[i] = interference(f, total - gm, P.a_dem[i]);
+      P.a_fac[i] = interference<GP>(f, total - gm, P.a_dem[i]);
     }
   };
 
@@ -400,7 +411,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
   }
   // current adjusted figures of every op (parallel over ops)
   for (int v = threadIdx.x; v < n; v += blockDim.x) {
-    const OpAdj o = adjust_op(d, f, P, S.rep_off, adev, v, S.p[v], S.r[v], S.b[v], S.T[v], S.comm[v], qps, -1, -1,
+    const OpAdj o = adjust_op<GP>(d, f, P, S.rep_off, adev, v, S.p[v], S.r[v], S.b[v], S.T[v], S.comm[v], qps, -1, -1,
                               0.0, -1, 0, 1.0, 0.0);
     S.cur_wt[v] = o.wt; S.cur_teff[v] = o.t_eff; S.cur_wait[v] = o.wait; S.cur_stable[v] = o.stable;
   }
@@ -465,7 +476,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
         lt.add(xg_max);
         const double total = lt.value();
         S.dev_total[dj] = total;
-        S.dev_xf[dj] = interference(f, total - xg_max, demand);
+        S.dev_xf[dj] = interference<GP>(f, total - xg_max, demand);
         uint32_t m = P.dev_mask[dev] | (1u << v);
         int at = atomicAdd(&S.n_items, __popc(m));
         for (; m; m &= m - 1) S.items[at++] = (uint16_t)(dj << 5 | (__ffs(m) - 1));
@@ -475,7 +486,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
       for (int it = threadIdx.x; it < S.n_items; it += blockDim.x) {
         const int dj = S.items[it] >> 5, u = S.items[it] & 31;
         const int dev = c0 + dj;
-        const OpAdj o = adjust_op(d, f, P, S.rep_off, adev, u, S.p[u], S.r[u], S.b[u], S.T[u], S.comm[u], qps,
+        const OpAdj o = adjust_op<GP>(d, f, P, S.rep_off, adev, u, S.p[u], S.r[u], S.b[u], S.T[u], S.comm[u], qps,
                                   dev, group, demand, v, k, S.dev_xf[dj], S.dev_total[dj]);
         S.probe_wt[dj][u] = o.stable ? o.wt : OPSC_INF;
         const size_t pi = (size_t)dev * n + u;
@@ -628,7 +639,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
           // factor the loop below gives it) -- exactly the factor its
           // operator's figures already counted it with while it was unplaced
           // (adjust_op), so those figures are unchanged
-          s_fresh_same = !probed && interference(f, S.ototal - xg_max, demand) == 1.0;
+          s_fresh_same = !probed && interference<GP>(f, S.ototal - xg_max, demand) == 1.0;
         } else if (part == 3 && !err) {  // the output row and the device's operator mask
           P.dev_mask[best] |= 1u << v;
           const size_t o = (size_t)w * A + i;
@@ -652,7 +663,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
       // device computed exactly these figures (same factors, same sums)
       const int bdev = S.best;
       for (int i = threadIdx.x; i < S.na; i += blockDim.x)
-        if (adev[i] == bdev) P.a_fac[i] = interference(f, S.ototal - P.a_gmax[i], P.a_dem[i]);
+        if (adev[i] == bdev) P.a_fac[i] = interference<GP>(f, S.ototal - P.a_gmax[i], P.a_dem[i]);
       const uint32_t bmask = P.dev_mask[bdev];
       if (s_probed) {
         for (int u = threadIdx.x; u < n; u += blockDim.x) {
@@ -666,7 +677,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(const __grid_const
       if (!s_probed && !s_fresh_same) {  // a fresh device whose factor is not 1.0 (NaN demand)
         for (int u = threadIdx.x; u < n; u += blockDim.x) {
           if (!(bmask >> u & 1u)) continue;
-          const OpAdj o = adjust_op(d, f, P, S.rep_off, adev, u, S.p[u], S.r[u], S.b[u], S.T[u], S.comm[u], qps, -1,
+          const OpAdj o = adjust_op<GP>(d, f, P, S.rep_off, adev, u, S.p[u], S.r[u], S.b[u], S.T[u], S.comm[u], qps, -1,
                                     -1, 0.0, -1, 0, 1.0, 0.0);
           S.cur_wt[u] = o.wt; S.cur_teff[u] = o.t_eff; S.cur_wait[u] = o.wait; S.cur_stable[u] = o.stable;
         }
@@ -764,16 +775,38 @@ cudaError_t launch_place_shared(const OpscDag& d, const OpscPlaceShared& f, Opsc
   static int set_dyn[64];
   int dev = 0;
   cudaGetDevice(&dev);
+  const bool gp = !(f.exponent == 1.0 || f.exponent == 2.0 || f.exponent == 0.5);
   if (dyn > 0 && dev < 64 && (int)dyn > set_dyn[dev]) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(place_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    cudaError_t e = cudaFuncSetAttribute(place_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(place_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return e;
     set_dyn[dev] = (int)dyn;
   }
-  if (smem_ws)
-    place_kernel<true><<<w.n, kPlaceThreads, dyn, s>>>(a, w, cfg, feas, config_order, out, (unsigned char*)ws);
+  unsigned char* wsb = (unsigned char*)ws;
+  if (smem_ws && gp)
+    place_kernel<true, true><<<w.n, kPlaceThreads, dyn, s>>>(a, w, cfg, feas, config_order, out, wsb);
+  else if (smem_ws)
+    place_kernel<true, false><<<w.n, kPlaceThreads, dyn, s>>>(a, w, cfg, feas, config_order, out, wsb);
+  else if (gp)
+    place_kernel<false, true><<<w.n, kPlaceThreads, 0, s>>>(a, w, cfg, feas, config_order, out, wsb);
   else
-    place_kernel<false><<<w.n, kPlaceThreads, 0, s>>>(a, w, cfg, feas, config_order, out, (unsigned char*)ws);
+    place_kernel<false, false><<<w.n, kPlaceThreads, 0, s>>>(a, w, cfg, feas, config_order, out, wsb);
+  return cudaGetLastError();
+}
+
+// Diagnostic: the placement's excess ** exponent on arbitrary inputs
+// (opsc_interference_pow; tests/test_gpu_pow.py).
+__global__ void interference_pow_kernel(const double* __restrict__ x, const double* __restrict__ e,
+                                        double* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = pow_expo<true>(x[i], e[i]);
+}
+
+cudaError_t launch_interference_pow(const double* x, const double* e, double* out, long long n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const long long blocks = (n + 255) / 256;
+  interference_pow_kernel<<<(int)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, s>>>(x, e, out, n);
   return cudaGetLastError();
 }
 

@@ -393,6 +393,7 @@ cudaError_t launch_greedy(const OpscDag& d, const OpscGreedySpec& s, OpscWindows
 size_t greedy_state_bytes(int n_windows);
 size_t windowize_workspace(long long n, int max_w);
 size_t place_shared_workspace(int n_windows, int A, int D, int n);
+cudaError_t launch_interference_pow(const double* x, const double* e, double* out, long long n, cudaStream_t s);
 cudaError_t launch_place_shared(const OpscDag& d, const OpscPlaceShared& f, OpscWindows w, const int16_t* cfg,
                                 const uint8_t* feas, int config_order, OpscPlacement out, void* ws,
                                 size_t ws_bytes, cudaStream_t s);
