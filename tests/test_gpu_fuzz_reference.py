@@ -262,3 +262,78 @@ def _close_placement(g, w, tag):
     assert (ge.label, ge.fingerprint, ge.devices_used, ge.memory_bytes, ge.feasible) == \
         (we.label, we.fingerprint, we.devices_used, we.memory_bytes, we.feasible), tag
     assert _close(ge.energy_joules, we.energy_joules), tag
+
+
+def test_random_traces_windowize_match_live_reference(ref):
+    """GPU windowize (workload.windowize_points, csrc/k_windowize.cu) against
+    the reference's own windowize (workload.py:114-159) on traces from its own
+    synth_workload (workload.py:162-230) with random specs, plus shuffled
+    records and arrivals on exact window boundaries; every point's (qps,
+    seq_len, phase, window) identical."""
+    from paper_2511_02248_b200 import workload as gw
+    W = ref.workload
+    rng = np.random.default_rng(77)
+    n_windows = 0
+    for trial in range(40):
+        kind = ("constant", "diurnal", "burst")[trial % 3]
+        spec = W.SynthSpec(kind=kind, rate=float(rng.uniform(0.2, 40.0)), duration=float(rng.uniform(5.0, 3600.0)),
+                           input_len_median=float(rng.uniform(8, 4096)), input_len_sigma=float(rng.uniform(0, 2)),
+                           output_len_median=float(rng.uniform(1, 1024)), output_len_sigma=float(rng.uniform(0, 2)),
+                           amplitude=float(rng.uniform(0, 0.9)), period=float(rng.uniform(10, 3600)),
+                           burst_factor=float(rng.uniform(1, 6)), burst_duty=float(rng.uniform(0.05, 0.9)))
+        recs = W.synth_workload(spec, int(rng.integers(0, 1 << 30)))
+        if not recs:
+            continue
+        wl = float(rng.choice([0.5, 1.0, 7.5, 60.0, 300.0, float(rng.uniform(0.1, 500.0))]))
+        if trial % 4 == 1:  # unsorted input
+            recs = [recs[i] for i in rng.permutation(len(recs))]
+        if trial % 4 == 2:  # arrivals on exact window boundaries
+            recs = [W.RequestRecord(float(np.floor(r.arrival_time / wl) * wl), r.input_len, r.output_len)
+                    for r in recs]
+        q = float(rng.choice([0.5, 0.9, 0.95, 0.99, 1.0, float(rng.uniform(1e-6, 1.0))]))
+        want = W.windowize(recs, wl, q)
+        got = gw.windowize_points(recs, wl, q)
+        assert len(got) == len(want), (trial, wl, q)
+        for (gp, gd), (wp, wd) in zip(got, want):
+            for a, b in ((gp, wp), (gd, wd)):
+                assert (a.qps, a.seq_len, a.phase, a.window) == (b.qps, b.seq_len, b.phase, b.window), (trial, a, b)
+        n_windows += len(want)
+    assert n_windows > 1000
+
+
+@pytest.mark.parametrize("axis", ["qps", "seqlen", "model_scale"])
+def test_random_sweeps_match_live_reference(ref, axis):
+    """runner.sweep (runner.py:190-240), rerouted to the batched GPU runner
+    (one launch set per params group), on random cases along each axis: the
+    ComparisonRow list (baseline vs candidate plans, placements, energy,
+    savings) identical to the reference's, or the same exception."""
+    A, R = ref.autoscaler, ref.runner
+    rng = np.random.default_rng(5 + len(axis))
+    n_rows = 0
+    for seed in range(12):
+        dag, prof, point, kw, bounds, crng = _case(ref, 500 + seed)
+        if point.qps >= 1e9:
+            continue
+        base = _outcome(lambda: A.model_level_autoscale(dag, prof, point, A.AutoscaleParams(slo=math.inf, **kw)))
+        lat0 = base[1].iteration_latency if base[0] == "ok" and math.isfinite(base[1].iteration_latency) else 1.0
+        params = A.AutoscaleParams(slo=float(lat0 * crng.uniform(0.6, 2.0)) if lat0 > 0 else 1.0,
+                                   epsilon=0.0, **{k: v for k, v in kw.items() if k != "prune_excess_replicas"})
+        fleet = ref.make_fleet(int(rng.choice([8, 64])))
+        if axis == "qps":
+            values = sorted(float(v) for v in point.qps * rng.uniform(0.1, 3.0, 5))
+        elif axis == "seqlen":
+            values = [float(v) for v in sorted(rng.integers(16, 4096, 4))]
+        else:
+            values = [0.5, 1.0, 2.0]
+        pm = ("shared", "default_stream")[seed % 2]
+        want = _outcome(lambda: R.sweep(axis, values, dag, prof, fleet, point, params, pm, None, 1))
+        with installed(ref):
+            got = _outcome(lambda: R.sweep(axis, values, dag, prof, fleet, point, params, pm, None, 1))
+        assert want[0] == got[0], (seed, want[1], got[1])
+        if want[0] == "raise":
+            assert type(want[1]) is type(got[1]) and str(want[1]) == str(got[1]), (seed, want[1], got[1])
+            continue
+        if prof.interference.exponent in EXACT_EXPONENTS:
+            assert repr(got[1]) == repr(want[1]), seed
+        n_rows += len(want[1])
+    assert n_rows >= 20
