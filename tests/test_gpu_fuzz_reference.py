@@ -130,6 +130,10 @@ def _case(op, seed):
     else:
         kw["parallelism"] = par
     kw["prune_excess_replicas"] = bool(rng.random() < 0.4)
+    if rng.random() < 0.15:  # the greedy loops' iteration cap (autoscaler.py:111, 391)
+        kw["max_iterations"] = int(rng.choice([1, 2, 5, 20]))
+    if rng.random() < 0.15:  # replica cap of the stability search (queueing: strict_min_replicas)
+        kw["r_cap"] = int(rng.choice([2, 8, 64]))
     # brute-force bounds: menus of |P| * r_max * b_max entries, from 2-entry
     # menus up to a few hundred entries on 2-op DAGs (every K2 tile width and
     # the shared-memory j level), space small enough for the reference's CPU search
