@@ -341,3 +341,80 @@ def test_random_sweeps_match_live_reference(ref, axis):
             assert repr(got[1]) == repr(want[1]), seed
         n_rows += len(want[1])
     assert n_rows >= 20
+
+
+def _cli_run(main, cwd, argv):
+    import contextlib as _cl
+    import hashlib
+    import io
+    import tempfile
+    with tempfile.TemporaryDirectory() as tmp:
+        out = os.path.join(tmp, "out")
+        err = io.StringIO()
+        old = os.getcwd()
+        os.chdir(cwd)
+        try:
+            with _cl.redirect_stderr(err):
+                rc = main(argv + ["--out", out])
+        finally:
+            os.chdir(old)
+        files = {}
+        if os.path.isdir(out):
+            for name in sorted(os.listdir(out)):
+                with open(os.path.join(out, name), "rb") as fh:
+                    files[name] = hashlib.sha256(fh.read()).hexdigest()
+        return rc, err.getvalue(), files
+
+
+def test_random_cli_runs_match_live_reference(ref, tmp_path):
+    """The reference's own CLI (cli.main: autoscale and sweep, cli.py:123-313)
+    on random scenario files (DAG / profile / fleet JSON written here) and
+    random --synth workloads, windows, quantiles, SLOs, modes and placements:
+    exit code, stderr and every artefact byte-identical with and without the
+    drop-in (cli.cmd_autoscale and runner.sweep rerouted to the batched GPU
+    runner)."""
+    import json
+    A = ref.autoscaler
+    n_files = ok_runs = 0
+    for trial in range(16):
+        r2 = np.random.default_rng(3000 + trial)
+        n = int(r2.integers(2, 7)) if trial % 4 else int(r2.integers(7, 11))
+        spec, names = _dag_spec(r2, n)
+        prof = _profiles(r2, names)
+        prof["_interference"]["exponent"] = float(r2.choice(EXACT_EXPONENTS))
+        d = tmp_path / f"t{trial}"
+        d.mkdir()
+        (d / "dag.json").write_text(json.dumps(spec))
+        (d / "prof.json").write_text(json.dumps(prof))
+        (d / "fleet.json").write_text(json.dumps([{"id": f"g{i:02d}", "mem_cap": float(r2.choice([40e9, 80e9, 180e9]))}
+                                                  for i in range(int(r2.choice([4, 16, 64])))]))
+        dag, pset = ref.build_dag(spec), ref.perfmodel.profiles_from_dict(prof)
+        rate = float(r2.uniform(1.0, 40.0))
+        slos = []
+        for ph, L in (("prefill", 1024), ("decode", 1)):
+            pt = ref.WorkloadPoint(rate if ph == "prefill" else rate * 200.0, L, ph)
+            b = _outcome(lambda: A.model_level_autoscale(dag, pset, pt, A.AutoscaleParams(slo=math.inf)))
+            lat = b[1].iteration_latency if b[0] == "ok" and math.isfinite(b[1].iteration_latency) else 1.0
+            slos.append(float(lat * r2.uniform(0.5, 2.0)) if lat > 0 else 1.0)
+        kind = ("constant", "diurnal", "burst")[trial % 3]
+        synth = (f"{kind}:rate={rate:.3f},duration={float(r2.uniform(60, 900)):.1f},"
+                 f"input_median={float(r2.uniform(64, 4096)):.1f},input_sigma={float(r2.uniform(0, 1.5)):.2f}")
+        common = ["--dag", "dag.json", "--profiles", "prof.json", "--fleet", "fleet.json",
+                  "--slo-prefill", repr(slos[0]), "--slo-decode", repr(slos[1]), "--synth", synth,
+                  "--seed", str(int(r2.integers(0, 1000))), "--window-len", str(float(r2.choice([30.0, 60.0, 120.0]))),
+                  "--quantile", str(float(r2.choice([0.5, 0.95, 0.99]))),
+                  "--placement", ("shared", "default_stream")[trial % 2]]
+        if trial % 5 == 4:
+            argv = ["sweep"] + common + ["--sweep", "qps", "--range", f"{rate * 0.5:.2f},{rate * 2:.2f}"]
+        else:
+            mode = ("operator", "model", "oracle", "operator")[trial % 4]
+            argv = ["autoscale"] + common + ["--mode", mode]
+            if r2.random() < 0.3:
+                argv += ["--epsilon", repr(slos[0] * 0.05)]
+        want = _cli_run(ref.cli.main, str(d), argv)
+        with installed(ref):
+            got = _cli_run(ref.cli.main, str(d), argv)
+        assert got == want, (trial, argv)
+        n_files += len(want[2])
+        ok_runs += want[0] == 0
+    assert n_files >= 10 and ok_runs >= 6, (n_files, ok_runs)
