@@ -792,6 +792,10 @@ __global__ void __launch_bounds__(kGreedyThreads) greedy_kernel(
     const __grid_constant__ GreedyArgs ga, const __grid_constant__ OpscWindows win,
     const int16_t* __restrict__ ucfg, const uint8_t* __restrict__ ufeas, const uint32_t* __restrict__ ustatus,
     const __grid_constant__ OpscDecisions out, int phase, GSave* __restrict__ save) {
+  // programmatic dependent launch: release the next kernel (phase 2, K4) so
+  // its CTAs are resident when this grid ends, then wait for the previous one
+  pdl_trigger();
+  pdl_wait();
   __shared__ GShared S;
   extern __shared__ __align__(16) unsigned char g_args[];
   {
@@ -1107,8 +1111,8 @@ cudaError_t launch_greedy(const OpscDag& d, const OpscGreedySpec& s, OpscWindows
     if (e != cudaSuccess) return e;
     set_dyn[dev] = 1;
   }
-  greedy_kernel<<<w.n, kGreedyThreads, dyn, st>>>(a, w, ucfg, ufeas, ustatus, out, phase, (GSave*)save);
-  return cudaGetLastError();
+  return launch_pdl(greedy_kernel, dim3(w.n), dim3(kGreedyThreads), dyn, st, a, w, ucfg, ufeas, ustatus, out, phase,
+                    (GSave*)save);
 }
 
 }  // namespace opsc
