@@ -50,6 +50,8 @@ static WzWork carve(void* ws, long long n, int max_w) {
 }
 
 __global__ void wz_zero(WzWork w, int max_w) {
+  pdl_trigger();  // dependents launch early; each waits for its predecessor first
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0) {
     *w.horizon_bits = 0ull;
@@ -64,6 +66,8 @@ __global__ void wz_zero(WzWork w, int max_w) {
 
 // non-negative doubles order like their unsigned bit patterns
 __global__ void wz_horizon(const double* __restrict__ t, long long n, WzWork w) {
+  pdl_trigger();  // dependents launch early; each waits for its predecessor first
+  pdl_wait();
   unsigned long long m = 0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const unsigned long long b = (unsigned long long)__double_as_longlong(t[i]);
@@ -78,6 +82,8 @@ __global__ void wz_horizon(const double* __restrict__ t, long long n, WzWork w) 
 }
 
 __global__ void wz_nwin(WzWork w, double len, int max_w, int32_t* n_windows) {
+  pdl_trigger();  // dependents launch early; each waits for its predecessor first
+  pdl_wait();
   const double horizon = __longlong_as_double((long long)*w.horizon_bits);
   const double nw = ceil(horizon / len + 1e-12);
   long long n = nw < 1.0 ? 1 : (long long)nw;
@@ -104,6 +110,8 @@ __device__ __forceinline__ unsigned long long group_sum_u64(unsigned grp, unsign
 // sums, so the totals are the same in any grouping (no same-address atomic
 // storm on a handful of window counters).
 __global__ void wz_count(OpscTraceRecords rec, double len, WzWork w, const int32_t* __restrict__ n_windows) {
+  pdl_trigger();  // dependents launch early; each waits for its predecessor first
+  pdl_wait();
   if (*w.err) return;
   const long long n = *n_windows;
   const int lane = threadIdx.x & 31;
@@ -130,6 +138,8 @@ __global__ void wz_count(OpscTraceRecords rec, double len, WzWork w, const int32
 
 // single-CTA exclusive scan of counts (chunks of 1024)
 __global__ void __launch_bounds__(1024) wz_scan(WzWork w, const int32_t* __restrict__ n_windows) {
+  pdl_trigger();  // dependents launch early; each waits for its predecessor first
+  pdl_wait();
   __shared__ unsigned long long part[1024];
   __shared__ unsigned long long carry;
   if (*w.err) return;
@@ -158,6 +168,8 @@ __global__ void __launch_bounds__(1024) wz_scan(WzWork w, const int32_t* __restr
 // the same grouping: one cursor reservation per (warp, window), lanes take
 // consecutive slots (the order inside a window does not matter to the select)
 __global__ void wz_scatter(OpscTraceRecords rec, WzWork w) {
+  pdl_trigger();  // dependents launch early; each waits for its predecessor first
+  pdl_wait();
   if (*w.err) return;
   const int lane = threadIdx.x & 31;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -179,6 +191,8 @@ __global__ void wz_scatter(OpscTraceRecords rec, WzWork w) {
 __global__ void __launch_bounds__(256) wz_select(WzWork w, double len, double q, const int32_t* __restrict__ n_windows,
                                                  double* __restrict__ pq, int32_t* __restrict__ pl,
                                                  double* __restrict__ dq) {
+  pdl_trigger();  // dependents launch early; each waits for its predecessor first
+  pdl_wait();
   __shared__ uint32_t hist[2048];
   __shared__ uint32_t s_prefix, s_mask;
   __shared__ long long s_k;
@@ -270,14 +284,17 @@ cudaError_t launch_windowize(OpscTraceRecords rec, double len, double q, int max
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long rb = (rec.n + 255) / 256;
   const int grid = (int)(rb < (long long)sms * 8 ? rb : (long long)sms * 8);
-  wz_zero<<<(max_w + 255) / 256, 256, 0, s>>>(w, max_w);
-  wz_horizon<<<grid, 256, 0, s>>>(rec.arrival, rec.n, w);
-  wz_nwin<<<1, 1, 0, s>>>(w, len, max_w, n_windows);
-  wz_count<<<grid, 256, 0, s>>>(rec, len, w, n_windows);
-  wz_scan<<<1, 1024, 0, s>>>(w, n_windows);
-  wz_scatter<<<grid, 256, 0, s>>>(rec, w);
-  wz_select<<<max_w, 256, 0, s>>>(w, len, q, n_windows, pq, pl, dq);
-  return cudaGetLastError();
+  // the chain runs under programmatic dependent launch (launch_pdl): every
+  // kernel releases its successor at entry and waits for its predecessor
+  cudaError_t e = launch_pdl(wz_zero, dim3((max_w + 255) / 256), dim3(256), 0, s, w, max_w);
+  if (e == cudaSuccess) e = launch_pdl(wz_horizon, dim3(grid), dim3(256), 0, s, (const double*)rec.arrival, rec.n, w);
+  if (e == cudaSuccess) e = launch_pdl(wz_nwin, dim3(1), dim3(1), 0, s, w, len, max_w, n_windows);
+  if (e == cudaSuccess) e = launch_pdl(wz_count, dim3(grid), dim3(256), 0, s, rec, len, w, (const int32_t*)n_windows);
+  if (e == cudaSuccess) e = launch_pdl(wz_scan, dim3(1), dim3(1024), 0, s, w, (const int32_t*)n_windows);
+  if (e == cudaSuccess) e = launch_pdl(wz_scatter, dim3(grid), dim3(256), 0, s, rec, w);
+  if (e == cudaSuccess)
+    e = launch_pdl(wz_select, dim3(max_w), dim3(256), 0, s, w, len, q, (const int32_t*)n_windows, pq, pl, dq);
+  return e;
 }
 
 }  // namespace opsc
